@@ -1,0 +1,169 @@
+/*
+ * include/fasq.h -- C ABI of the B200-native FASQ library (libfasq.so).
+ *
+ * FASQ (arXiv 2605.04084, /root/reference/PAPER.md cited as P:<line>) stores
+ * each FP16 linear-layer weight W [F_out][F_in] (y = W.x, the nn.Linear
+ * convention) as product-quantized codebooks + uint8 index tables and computes
+ * products directly on them (Eq. 3):
+ *
+ *     y[b][j] = sum_{ss=0}^{N_ss-1} dot( x[b][ss*d : ss*d+d],
+ *                                        T_cluster[ss/group][T_index[ss][j]] )
+ *
+ * Symbols: d = SZ_ss (sub-vector size), C = K_s (codebook cardinality),
+ * N_ss = F_in/d subspaces over the INPUT axis (Eq. 3 / Alg. 2, P:267-268;
+ * DESIGN.md reading R1), and `group` consecutive subspaces share one codebook
+ * (N_cb = N_ss/group; group = 1 is the paper's Alg. 1).
+ *
+ * Logical arrays (the only layouts that cross this ABI):
+ *   W         fp16 [F_out][F_in]            row major
+ *   codebooks fp16 [N_cb][C][d]             T_cluster
+ *   indices   uint8 [N_ss][F_out]           T_index  ("1 B index" P:274)
+ *   x / X     fp16 [B or M][F_in]           row major
+ *   y / Y     fp16 or fp32 [B or M][F_out]  row major
+ * A layer stores these in a private physical layout tuned for the kernels
+ * (DESIGN.md "Data layout in HBM"); fasq_export returns the logical form.
+ *
+ * Conventions for every call:
+ *   - Pointers named *_dev are CUDA device pointers; *_host are host pointers.
+ *     The caller owns all buffers it passes; the library owns each layer's
+ *     storage (allocated on the current device at creation, released by
+ *     fasq_free).
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls that
+ *     take a stream are stream-ordered and asynchronous unless documented.
+ *   - Layers are immutable after creation and may be shared across streams
+ *     and host threads.
+ *   - No exception crosses the ABI.  Argument errors are returned
+ *     synchronously before anything is enqueued.  CUDA launch/allocation
+ *     failures return FASQ_E_CUDA / FASQ_E_OOM; asynchronous device faults
+ *     surface as FASQ_E_CUDA on a later call.  fasq_last_error_message()
+ *     describes the last failure on the calling thread.
+ *   - There is no CPU fallback: every compute step runs in this library's
+ *     sm_100a kernels; without a usable CUDA device every compute call fails
+ *     with FASQ_E_CUDA.
+ */
+#ifndef FASQ_H_
+#define FASQ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FASQ_ABI_VERSION 1
+
+typedef enum {
+    FASQ_OK = 0,
+    FASQ_E_ARG = -1,              /* null pointer / non-positive size / bad enum        */
+    FASQ_E_NONDIVISIBLE = -2,     /* F_in % d != 0 or N_ss % group != 0 (Eq. 2) */
+    FASQ_E_CLUSTER_OVERFLOW = -3, /* C > group*F_out points per codebook    */
+    FASQ_E_NONFINITE = -4,        /* W holds inf/NaN (SPEC S:73 DegenerateInput)         */
+    FASQ_E_SHAPE = -5,            /* operand shape mismatch          */
+    FASQ_E_UNSUPPORTED = -6,      /* d not in {1,2,4,8}, C > 256, B > 8, n_pts > 2^23    */
+    FASQ_E_CUDA = -7,             /* CUDA runtime / launch error, or no device           */
+    FASQ_E_OOM = -8               /* device allocation failed                            */
+} fasq_status;
+
+typedef enum { FASQ_F16 = 0, FASQ_F32 = 1 } fasq_dtype;
+
+typedef enum {
+    FASQ_GEMM_AUTO = 0,      /* library picks (EXPAND_TC when shapes allow) */
+    FASQ_GEMM_LUT = 1,       /* Alg. 3-style LUT build + gather               */
+    FASQ_GEMM_EXPAND_TC = 2  /* centroid expansion into SMEM tiles + tcgen05 MMA  */
+} fasq_gemm_algo;
+
+/* Flags for the *_ex calls. */
+#define FASQ_FLAG_PDL 1u     /* launch with programmatic dependent launch: the kernel's
+                                 codebook/index prefetch may start before the previous
+                                 kernel on the stream finishes (x is read only after
+                                 griddepcontrol.wait).  Only valid when the layer was
+                                 NOT written by the immediately preceding kernel. */
+
+/* Pack parameters (Alg. 1). */
+typedef struct {
+    int32_t d;        /* SZ_ss: 1, 2, 4 or 8                                     */
+    int32_t C;        /* K_s: 1..256 (uint8 indices)                              */
+    int32_t group;    /* consecutive subspaces per codebook (1 = paper)           */
+    int32_t iters;    /* T >= 0: maximum assign+update rounds (25 = default)      */
+    uint64_t seed;    /* seeded distinct-sample init (splitmix64)                 */
+} fasq_pack_params;
+
+typedef struct fasq_layer fasq_layer; /* opaque */
+
+typedef struct {
+    int64_t F_out, F_in;
+    int32_t d, C, group, N_ss, N_cb;
+    int32_t row_offset;          /* first output row held (fasq_shard_rows), else 0 */
+    int64_t index_bytes;         /* logical: N_ss * F_out                         */
+    int64_t codebook_bytes;      /* logical: N_cb * C * d * 2                     */
+    int64_t device_bytes;        /* physical HBM bytes this layer owns            */
+    double bits_per_weight;      /* 8*(index+codebook bytes)/(F_out*F_in)         */
+    double eff_bits_W;           /* paper #W = ceil(log2 C)/d             */
+} fasq_layer_info;
+
+/* ---- creation --------------------------------------------------------- */
+
+/* Packs W (fp16 [F_out][F_in], device) into a new layer with the GPU k-means
+ * packer.  Output is bit-identical to the CPU oracle's fasq_ref_pack for the
+ * same params.  W is read during the call's stream work only; it may be freed
+ * after the stream reaches this point.  Synchronises `stream` once (to size
+ * the unique-key sets).  *out is NULL on failure. */
+fasq_status fasq_pack(const void* W_dev, int64_t F_out, int64_t F_in,
+                      const fasq_pack_params* params, void* stream, fasq_layer** out);
+
+/* Creates a layer from logical codebooks (fp16 [N_cb][C][d]) and indices
+ * (uint8 [N_ss][F_out]), both device pointers, e.g. an oracle-packed layer.
+ * Indices >= C are a caller error (undefined results).  Asynchronous. */
+fasq_status fasq_import(const void* codebooks_dev, const void* indices_dev,
+                        int64_t F_out, int64_t F_in, int32_t d, int32_t C, int32_t group,
+                        void* stream, fasq_layer** out);
+
+/* Writes the layer's logical codebooks / indices to device buffers of
+ * N_cb*C*d fp16 and N_ss*F_out bytes (either pointer may be NULL). */
+fasq_status fasq_export(const fasq_layer* layer, void* codebooks_dev, void* indices_dev,
+                        void* stream);
+
+/* Row shard for multi-GPU: a new layer holding output rows
+ * [rank*F_out/world, (rank+1)*F_out/world) and ALL codebooks, created on the
+ * current device.  Requires F_out % world == 0. */
+fasq_status fasq_shard_rows(const fasq_layer* layer, int32_t rank, int32_t world,
+                            void* stream, fasq_layer** out);
+
+fasq_status fasq_layer_info_get(const fasq_layer* layer, fasq_layer_info* info);
+void fasq_free(fasq_layer* layer);       /* synchronises the device; NULL is a no-op */
+
+/* ---- products ------------------------------------------------------------ */
+
+/* Decode GEMV (Alg. 2's math): y[b] = W_hat . x[b] for B in 1..8.
+ * x_dev fp16 [B][F_in], y_dev [B][F_out] of y_dtype.  fp32 accumulation of
+ * exact fp16 products; the split-K merge is deterministic (fixed order). */
+fasq_status fasq_gemv(const fasq_layer* layer, const void* x_dev, int32_t B, void* y_dev,
+                      fasq_dtype y_dtype, void* stream);
+fasq_status fasq_gemv_ex(const fasq_layer* layer, const void* x_dev, int32_t B, void* y_dev,
+                         fasq_dtype y_dtype, uint32_t flags, void* stream);
+
+/* Same product with HOST buffers (end-to-end path): copies x_host (fp16
+ * [B][F_in], ideally pinned) to the device, runs fasq_gemv and copies y back
+ * to y_host.  Synchronous: returns after y_host is written. */
+fasq_status fasq_gemv_host(const fasq_layer* layer, const void* x_host, int32_t B,
+                           void* y_host, fasq_dtype y_dtype, void* stream);
+
+/* Prefill GEMM (Alg. 3's math): Y = X . W_hat^T for M >= 1 rows.
+ * X_dev fp16 [M][F_in], Y_dev [M][F_out] of y_dtype. */
+fasq_status fasq_gemm(const fasq_layer* layer, const void* X_dev, int64_t M, void* Y_dev,
+                      fasq_dtype y_dtype, fasq_gemm_algo algo, void* stream);
+
+/* ---- diagnostics ---------------------------------------------------------- */
+
+/* Number of kernel launches the last successful compute call on this host
+ * thread enqueued (bench.py's gpu_launches accounting). */
+int32_t fasq_last_launch_count(void);
+const char* fasq_status_string(fasq_status status);
+const char* fasq_last_error_message(void);
+int32_t fasq_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASQ_H_ */

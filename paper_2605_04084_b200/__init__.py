@@ -1,0 +1,216 @@
+"""B200-native FASQ (arXiv 2605.04084): product-quantized linear layers.
+
+Thin Python binding over the C-ABI library ``lib/libfasq.so`` (declared in
+``include/fasq.h``): argument marshalling only.  Every compute step runs in the
+library's sm_100a CUDA kernels; PyTorch supplies device memory, streams and
+process groups.  There is no CPU fallback: if the library is missing this
+module raises on import, and every compute call raises on a non-CUDA tensor.
+
+Names follow the paper: d = SZ_ss (sub-vector size), C = K_s (codebook
+cardinality), N_ss = F_in/d subspaces, T_cluster = codebooks, T_index = indices.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libfasq.so")
+
+FASQ_F16, FASQ_F32 = 0, 1
+GEMM_AUTO, GEMM_LUT, GEMM_EXPAND_TC = 0, 1, 2
+FLAG_PDL = 1
+
+_STATUS = {0: "FASQ_OK", -1: "FASQ_E_ARG", -2: "FASQ_E_NONDIVISIBLE", -3: "FASQ_E_CLUSTER_OVERFLOW",
+           -4: "FASQ_E_NONFINITE", -5: "FASQ_E_SHAPE", -6: "FASQ_E_UNSUPPORTED", -7: "FASQ_E_CUDA",
+           -8: "FASQ_E_OOM"}
+
+# Every symbol include/fasq.h declares (checked by tests/test_abi.py).
+EXPORTED = ["fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
+            "fasq_free", "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_host", "fasq_gemm",
+            "fasq_last_launch_count", "fasq_status_string", "fasq_last_error_message",
+            "fasq_abi_version"]
+
+
+class FasqError(RuntimeError):
+    def __init__(self, code: int, msg: str = ""):
+        super().__init__("%s (%d)%s" % (_STATUS.get(code, "?"), code, (": " + msg) if msg else ""))
+        self.code = code
+
+
+class _PackParams(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_int32), ("C", ctypes.c_int32), ("group", ctypes.c_int32),
+                ("iters", ctypes.c_int32), ("seed", ctypes.c_uint64)]
+
+
+class LayerInfo(ctypes.Structure):
+    _fields_ = [("F_out", ctypes.c_int64), ("F_in", ctypes.c_int64), ("d", ctypes.c_int32),
+                ("C", ctypes.c_int32), ("group", ctypes.c_int32), ("N_ss", ctypes.c_int32),
+                ("N_cb", ctypes.c_int32), ("row_offset", ctypes.c_int32),
+                ("index_bytes", ctypes.c_int64), ("codebook_bytes", ctypes.c_int64),
+                ("device_bytes", ctypes.c_int64), ("bits_per_weight", ctypes.c_double),
+                ("eff_bits_W", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError("libfasq.so not built (%s); run `python -m paper_2605_04084_b200.build` "
+                          "or __graft_entry__.build() -- there is no CPU fallback" % LIB_PATH)
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, u32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32
+    pp = ctypes.POINTER(ctypes.c_void_p)
+    L.fasq_pack.argtypes = [vp, i64, i64, ctypes.POINTER(_PackParams), vp, pp]
+    L.fasq_import.argtypes = [vp, vp, i64, i64, i32, i32, i32, vp, pp]
+    L.fasq_export.argtypes = [vp, vp, vp, vp]
+    L.fasq_shard_rows.argtypes = [vp, i32, i32, vp, pp]
+    L.fasq_layer_info_get.argtypes = [vp, ctypes.POINTER(LayerInfo)]
+    L.fasq_free.argtypes = [vp]
+    L.fasq_free.restype = None
+    L.fasq_gemv.argtypes = [vp, vp, i32, vp, i32, vp]
+    L.fasq_gemv_ex.argtypes = [vp, vp, i32, vp, i32, u32, vp]
+    L.fasq_gemv_host.argtypes = [vp, vp, i32, vp, i32, vp]
+    L.fasq_gemm.argtypes = [vp, vp, i64, vp, i32, i32, vp]
+    L.fasq_status_string.restype = ctypes.c_char_p
+    L.fasq_last_error_message.restype = ctypes.c_char_p
+    for name in ("fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
+                 "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_host", "fasq_gemm", "fasq_last_launch_count",
+                 "fasq_abi_version"):
+        getattr(L, name).restype = ctypes.c_int32
+    return L
+
+
+lib = _load()
+
+
+def _check(code: int):
+    if code != 0:
+        raise FasqError(code, (lib.fasq_last_error_message() or b"").decode())
+
+
+def _stream(stream=None) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _cuda(t: torch.Tensor, dtype, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("%s must be a CUDA tensor (FASQ has no CPU path)" % name)
+    if t.dtype != dtype:
+        raise TypeError("%s must be %s, got %s" % (name, dtype, t.dtype))
+    return t.contiguous()
+
+
+def last_launch_count() -> int:
+    """Kernel launches enqueued by the last compute call on this thread."""
+    return int(lib.fasq_last_launch_count())
+
+
+class Layer:
+    """A product-quantized linear layer (y = W_hat . x) resident on one GPU."""
+
+    def __init__(self, handle: int):
+        self._h = ctypes.c_void_p(handle)
+        inf = LayerInfo()
+        _check(lib.fasq_layer_info_get(self._h, ctypes.byref(inf)))
+        self.info = inf.as_dict()
+        self.F_out, self.F_in = inf.F_out, inf.F_in
+        self.d, self.C, self.group = inf.d, inf.C, inf.group
+        self.N_ss, self.N_cb = inf.N_ss, inf.N_cb
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free(self):
+        if self._h:
+            lib.fasq_free(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib.fasq_free(self._h)
+        except Exception:
+            pass
+
+    def export(self, stream=None):
+        """Logical arrays: (codebooks fp16 [N_cb][C][d], indices uint8 [N_ss][F_out])."""
+        cb = torch.empty((self.N_cb, self.C, self.d), dtype=torch.float16, device="cuda")
+        idx = torch.empty((self.N_ss, self.F_out), dtype=torch.uint8, device="cuda")
+        _check(lib.fasq_export(self._h, cb.data_ptr(), idx.data_ptr(), _stream(stream)))
+        return cb, idx
+
+    def shard_rows(self, rank: int, world: int, stream=None) -> "Layer":
+        out = ctypes.c_void_p()
+        _check(lib.fasq_shard_rows(self._h, rank, world, _stream(stream), ctypes.byref(out)))
+        return Layer(out.value)
+
+
+def pack(W: torch.Tensor, d: int, C: int, group: int = 1, seed: int = 0, iters: int = 25,
+         stream=None) -> Layer:
+    """Alg. 1 on the GPU: k-means per codebook -> Layer."""
+    W = _cuda(W, torch.float16, "W")
+    prm = _PackParams(d, C, group, iters, seed & (2**64 - 1))
+    out = ctypes.c_void_p()
+    _check(lib.fasq_pack(W.data_ptr(), W.shape[0], W.shape[1], ctypes.byref(prm), _stream(stream),
+                         ctypes.byref(out)))
+    return Layer(out.value)
+
+
+def import_layer(codebooks: torch.Tensor, indices: torch.Tensor, F_in: int, group: int = 1,
+                 stream=None) -> Layer:
+    """Layer from logical codebooks fp16 [N_cb][C][d] + indices uint8 [N_ss][F_out]."""
+    cb = _cuda(codebooks, torch.float16, "codebooks")
+    idx = _cuda(indices, torch.uint8, "indices")
+    N_cb, C, d = cb.shape
+    N_ss, F_out = idx.shape
+    out = ctypes.c_void_p()
+    _check(lib.fasq_import(cb.data_ptr(), idx.data_ptr(), F_out, F_in, d, C, group, _stream(stream),
+                           ctypes.byref(out)))
+    return Layer(out.value)
+
+
+def gemv(layer: Layer, x: torch.Tensor, out: torch.Tensor | None = None,
+         out_dtype: torch.dtype = torch.float32, flags: int = 0, stream=None) -> torch.Tensor:
+    """Decode GEMV (Eq. 3 / Alg. 2): x fp16 [B][F_in] (B <= 8) -> y [B][F_out]."""
+    x = _cuda(x, torch.float16, "x")
+    if x.dim() == 1:
+        x = x.unsqueeze(0)
+    B = x.shape[0]
+    if x.shape[1] != layer.F_in:
+        raise FasqError(-5, "x has %d columns, layer F_in=%d" % (x.shape[1], layer.F_in))
+    if out is None:
+        out = torch.empty((B, layer.F_out), dtype=out_dtype, device=x.device)
+    yt = FASQ_F32 if out.dtype == torch.float32 else FASQ_F16
+    _check(lib.fasq_gemv_ex(layer.handle, x.data_ptr(), B, out.data_ptr(), yt, flags, _stream(stream)))
+    return out
+
+
+def gemv_host(layer: Layer, x_host: torch.Tensor, y_host: torch.Tensor, stream=None) -> torch.Tensor:
+    """End-to-end GEMV with HOST buffers (H2D of x, kernels, D2H of y inside)."""
+    if x_host.is_cuda or y_host.is_cuda:
+        raise TypeError("gemv_host takes host tensors")
+    yt = FASQ_F32 if y_host.dtype == torch.float32 else FASQ_F16
+    _check(lib.fasq_gemv_host(layer.handle, x_host.data_ptr(), x_host.shape[0], y_host.data_ptr(), yt,
+                              _stream(stream)))
+    return y_host
+
+
+def gemm(layer: Layer, X: torch.Tensor, out: torch.Tensor | None = None,
+         out_dtype: torch.dtype = torch.float32, algo: int = GEMM_AUTO, stream=None) -> torch.Tensor:
+    """Prefill GEMM (Alg. 3's math): X fp16 [M][F_in] -> Y [M][F_out]."""
+    X = _cuda(X, torch.float16, "X")
+    M = X.shape[0]
+    if X.shape[1] != layer.F_in:
+        raise FasqError(-5, "X has %d columns, layer F_in=%d" % (X.shape[1], layer.F_in))
+    if out is None:
+        out = torch.empty((M, layer.F_out), dtype=out_dtype, device=X.device)
+    yt = FASQ_F32 if out.dtype == torch.float32 else FASQ_F16
+    _check(lib.fasq_gemm(layer.handle, X.data_ptr(), M, out.data_ptr(), yt, algo, _stream(stream)))
+    return out

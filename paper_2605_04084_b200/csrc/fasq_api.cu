@@ -1,0 +1,250 @@
+// fasq_api.cu -- the extern "C" boundary of libfasq.so (include/fasq.h).
+// Argument marshalling, validation, layer lifetime; all compute is in the
+// kernels of layout.cu / gemv.cu / gemm_*.cu / pack.cu.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "fasq_internal.cuh"
+
+namespace fasq {
+
+static thread_local std::string t_err;
+static thread_local int t_launches = 0;
+
+void set_error(const std::string& msg) { t_err = msg; }
+fasq_status cuda_fail(cudaError_t e, const char* what) {
+    t_err = std::string(what) + ": " + cudaGetErrorString(e);
+    cudaGetLastError();
+    return e == cudaErrorMemoryAllocation ? FASQ_E_OOM : FASQ_E_CUDA;
+}
+void set_launch_count(int n) { t_launches = n; }
+void add_launch_count(int n) { t_launches += n; }
+
+static fasq_status check_device() {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        set_error("no CUDA device available (FASQ has no CPU fallback)");
+        return FASQ_E_CUDA;
+    }
+    return FASQ_OK;
+}
+
+static void destroy(fasq_layer* L) {
+    if (!L) return;
+    if (L->idx) cudaFree(L->idx);
+    if (L->cbimg) cudaFree(L->cbimg);
+    if (L->cb) cudaFree(L->cb);
+    delete L;
+}
+
+}  // namespace fasq
+
+using namespace fasq;
+
+extern "C" {
+
+int32_t fasq_abi_version(void) { return FASQ_ABI_VERSION; }
+
+const char* fasq_status_string(fasq_status s) {
+    switch (s) {
+        case FASQ_OK: return "FASQ_OK";
+        case FASQ_E_ARG: return "FASQ_E_ARG: invalid argument";
+        case FASQ_E_NONDIVISIBLE: return "FASQ_E_NONDIVISIBLE: F_in % d or N_ss % group != 0";
+        case FASQ_E_CLUSTER_OVERFLOW: return "FASQ_E_CLUSTER_OVERFLOW: C > points per codebook";
+        case FASQ_E_NONFINITE: return "FASQ_E_NONFINITE: W holds inf/NaN";
+        case FASQ_E_SHAPE: return "FASQ_E_SHAPE: operand shape mismatch";
+        case FASQ_E_UNSUPPORTED: return "FASQ_E_UNSUPPORTED: parameter outside the supported range";
+        case FASQ_E_CUDA: return "FASQ_E_CUDA: CUDA error";
+        case FASQ_E_OOM: return "FASQ_E_OOM: device allocation failed";
+    }
+    return "FASQ: unknown status";
+}
+
+const char* fasq_last_error_message(void) { return t_err.c_str(); }
+int32_t fasq_last_launch_count(void) { return t_launches; }
+
+fasq_status fasq_import(const void* codebooks_dev, const void* indices_dev, int64_t F_out, int64_t F_in,
+                        int32_t d, int32_t C, int32_t group, void* stream, fasq_layer** out) {
+    if (!out) return FASQ_E_ARG;
+    *out = nullptr;
+    if (!codebooks_dev || !indices_dev) return FASQ_E_ARG;
+    fasq_layer* L = new fasq_layer();
+    fasq_status s = init_layer_shape(L, F_out, F_in, d, C, group);
+    if (s == FASQ_OK) s = check_device();
+    if (s == FASQ_OK) s = alloc_layer_storage(L);
+    if (s == FASQ_OK)
+        s = build_physical_from_logical(L, static_cast<const __half*>(codebooks_dev),
+                                        static_cast<const uint8_t*>(indices_dev), (cudaStream_t)stream);
+    if (s != FASQ_OK) { destroy(L); return s; }
+    set_launch_count(2);
+    *out = L;
+    return FASQ_OK;
+}
+
+fasq_status fasq_pack(const void* W_dev, int64_t F_out, int64_t F_in, const fasq_pack_params* prm,
+                      void* stream, fasq_layer** out) {
+    if (!out) return FASQ_E_ARG;
+    *out = nullptr;
+    if (!W_dev || !prm) return FASQ_E_ARG;
+    if (prm->iters < 0) return FASQ_E_ARG;
+    fasq_layer* L = new fasq_layer();
+    fasq_status s = init_layer_shape(L, F_out, F_in, prm->d, prm->C, prm->group);
+    if (s == FASQ_OK && (int64_t)prm->C > (int64_t)prm->group * F_out) s = FASQ_E_CLUSTER_OVERFLOW;
+    if (s == FASQ_OK && (int64_t)prm->group * F_out > (1ll << 23)) s = FASQ_E_UNSUPPORTED;
+    if (s == FASQ_OK) s = check_device();
+    if (s == FASQ_OK) s = alloc_layer_storage(L);
+    uint8_t* idx_log = nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (s == FASQ_OK) {
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&idx_log), (size_t)L->N_ss * L->F_out, st);
+        if (e != cudaSuccess) { cudaGetLastError(); s = FASQ_E_OOM; }
+    }
+    if (s == FASQ_OK) s = pack_run(static_cast<const __half*>(W_dev), L, prm, st, L->cb, idx_log);
+    if (s == FASQ_OK) s = build_physical_from_logical(L, L->cb, idx_log, st);
+    if (idx_log) cudaFreeAsync(idx_log, st);
+    if (s != FASQ_OK) { cudaStreamSynchronize(st); destroy(L); return s; }
+    *out = L;
+    return FASQ_OK;
+}
+
+fasq_status fasq_export(const fasq_layer* L, void* codebooks_dev, void* indices_dev, void* stream) {
+    if (!L) return FASQ_E_ARG;
+    fasq_status s = export_logical(L, static_cast<__half*>(codebooks_dev), static_cast<uint8_t*>(indices_dev),
+                                   (cudaStream_t)stream);
+    if (s == FASQ_OK) set_launch_count(indices_dev ? 1 : 0);
+    return s;
+}
+
+fasq_status fasq_shard_rows(const fasq_layer* L, int32_t rank, int32_t world, void* stream, fasq_layer** out) {
+    if (!out) return FASQ_E_ARG;
+    *out = nullptr;
+    if (!L || world < 1 || rank < 0 || rank >= world) return FASQ_E_ARG;
+    if (L->F_out % world) return FASQ_E_SHAPE;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t rows = L->F_out / world, row0 = rows * rank;
+    // via the logical form: export -> slice rows -> import (any row0; the
+    // physical rotation depends on r mod 32)
+    uint8_t* full = nullptr;
+    uint8_t* part = nullptr;
+    fasq_status s = FASQ_OK;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&full), (size_t)L->N_ss * L->F_out, st) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&part), (size_t)L->N_ss * rows, st) != cudaSuccess) {
+        cudaGetLastError();
+        s = FASQ_E_OOM;
+    }
+    if (s == FASQ_OK) s = export_logical(L, nullptr, full, st);
+    if (s == FASQ_OK) {
+        cudaError_t e = cudaMemcpy2DAsync(part, (size_t)rows, full + row0, (size_t)L->F_out, (size_t)rows,
+                                          (size_t)L->N_ss, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) s = cuda_fail(e, "shard copy");
+    }
+    fasq_layer* S = nullptr;
+    if (s == FASQ_OK) {
+        S = new fasq_layer();
+        s = init_layer_shape(S, rows, L->F_in, L->d, L->C, L->group);
+        if (s == FASQ_OK) s = alloc_layer_storage(S);
+        if (s == FASQ_OK) s = build_physical_from_logical(S, L->cb, part, st);
+        if (s == FASQ_OK) S->row_offset = L->row_offset + (int32_t)row0;
+    }
+    if (full) cudaFreeAsync(full, st);
+    if (part) cudaFreeAsync(part, st);
+    if (s != FASQ_OK) { cudaStreamSynchronize(st); destroy(S); return s; }
+    *out = S;
+    return FASQ_OK;
+}
+
+fasq_status fasq_layer_info_get(const fasq_layer* L, fasq_layer_info* info) {
+    if (!L || !info) return FASQ_E_ARG;
+    std::memset(info, 0, sizeof(*info));
+    info->F_out = L->F_out;
+    info->F_in = L->F_in;
+    info->d = L->d;
+    info->C = L->C;
+    info->group = L->group;
+    info->N_ss = L->N_ss;
+    info->N_cb = L->N_cb;
+    info->row_offset = L->row_offset;
+    info->index_bytes = (int64_t)L->N_ss * L->F_out;
+    info->codebook_bytes = L->cb_bytes;
+    info->device_bytes = L->idx_bytes + L->cbimg_bytes + L->cb_bytes;
+    info->bits_per_weight = 8.0 * (double)(info->index_bytes + info->codebook_bytes) / ((double)L->F_out * L->F_in);
+    int lg = 0;
+    while ((1 << lg) < L->C) ++lg;
+    info->eff_bits_W = (double)lg / L->d;
+    return FASQ_OK;
+}
+
+void fasq_free(fasq_layer* L) {
+    if (!L) return;
+    cudaDeviceSynchronize();
+    destroy(L);
+}
+
+fasq_status fasq_gemv_ex(const fasq_layer* L, const void* x_dev, int32_t B, void* y_dev, fasq_dtype yt,
+                         uint32_t flags, void* stream) {
+    if (!L || !x_dev || !y_dev) return FASQ_E_ARG;
+    if (B < 1 || B > 8) return FASQ_E_UNSUPPORTED;
+    if (yt != FASQ_F16 && yt != FASQ_F32) return FASQ_E_ARG;
+    return gemv_launch(L, static_cast<const __half*>(x_dev), B, y_dev, yt, flags, (cudaStream_t)stream);
+}
+
+fasq_status fasq_gemv(const fasq_layer* L, const void* x_dev, int32_t B, void* y_dev, fasq_dtype yt,
+                      void* stream) {
+    return fasq_gemv_ex(L, x_dev, B, y_dev, yt, 0u, stream);
+}
+
+fasq_status fasq_gemv_host(const fasq_layer* L, const void* x_host, int32_t B, void* y_host, fasq_dtype yt,
+                           void* stream) {
+    if (!L || !x_host || !y_host) return FASQ_E_ARG;
+    if (B < 1 || B > 8) return FASQ_E_UNSUPPORTED;
+    if (yt != FASQ_F16 && yt != FASQ_F32) return FASQ_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t xb = (size_t)B * L->F_in * 2, yb = (size_t)B * L->F_out * (yt == FASQ_F32 ? 4 : 2);
+    void *xd = nullptr, *yd = nullptr;
+    if (cudaMallocAsync(&xd, xb, st) != cudaSuccess || cudaMallocAsync(&yd, yb, st) != cudaSuccess) {
+        cudaGetLastError();
+        return FASQ_E_OOM;
+    }
+    fasq_status s = FASQ_OK;
+    cudaError_t e = cudaMemcpyAsync(xd, x_host, xb, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) s = cuda_fail(e, "H2D x");
+    int launches = 0;
+    if (s == FASQ_OK) {
+        s = gemv_launch(L, static_cast<const __half*>(xd), B, yd, yt, 0u, st);
+        launches = t_launches;
+    }
+    if (s == FASQ_OK) {
+        e = cudaMemcpyAsync(y_host, yd, yb, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) s = cuda_fail(e, "D2H y");
+    }
+    cudaFreeAsync(xd, st);
+    cudaFreeAsync(yd, st);
+    e = cudaStreamSynchronize(st);
+    if (s == FASQ_OK && e != cudaSuccess) s = cuda_fail(e, "gemv_host sync");
+    if (s == FASQ_OK) set_launch_count(launches);
+    return s;
+}
+
+fasq_status fasq_gemm(const fasq_layer* L, const void* X_dev, int64_t M, void* Y_dev, fasq_dtype yt,
+                      fasq_gemm_algo algo, void* stream) {
+    if (!L || !X_dev || !Y_dev) return FASQ_E_ARG;
+    if (M < 1) return FASQ_E_ARG;
+    if (yt != FASQ_F16 && yt != FASQ_F32) return FASQ_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const __half* X = static_cast<const __half*>(X_dev);
+    switch (algo) {
+        case FASQ_GEMM_LUT: return gemm_lut_launch(L, X, M, Y_dev, yt, st);
+        case FASQ_GEMM_EXPAND_TC:
+            if (!gemm_tc_supported(L, M)) return FASQ_E_UNSUPPORTED;
+            return gemm_tc_launch(L, X, M, Y_dev, yt, st);
+        case FASQ_GEMM_AUTO:
+            if (gemm_tc_supported(L, M)) return gemm_tc_launch(L, X, M, Y_dev, yt, st);
+            return gemm_lut_launch(L, X, M, Y_dev, yt, st);
+    }
+    return FASQ_E_ARG;
+}
+
+}  // extern "C"

@@ -1,0 +1,191 @@
+// fasq_internal.cuh -- shared definitions of the product library (CUDA, sm_100a).
+// Nothing here is shared with oracle/ (which is independent test infrastructure).
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/fasq.h"
+
+namespace fasq {
+
+constexpr int kGroupSubs = 32;   // subspaces per "group" = one per lane of a warp
+
+// ---------------------------------------------------------------------------
+// The layer object (opaque behind the ABI).  Physical layout (DESIGN.md
+// "Data layout in HBM"):
+//
+//  idx    [n_groups][F_out_pad][32] uint8.  Byte p of (group g, row r) holds
+//         T_index[g*32 + ((p + r) & 31)][r]  (row-rotated so that lane l of a
+//         warp working on rows r = l (mod 32) reads subspace (s + l) & 31 at
+//         step s -> conflict-free codebook gathers).
+//         Padded subspaces (>= N_ss) and rows (>= F_out) hold 0.
+//  cbimg  [n_groups][C][32][E] bytes, E = entry bytes (4 for d<=2 -- d=1 is
+//         padded to (c,0) --, 8 for d=4, 16 for d=8): the codebook of each
+//         lane's subspace, k-major so that one k-row is 32*E contiguous bytes.
+//         Padded subspaces hold 0.
+//  cb     [N_cb][C][d] fp16, the logical codebooks (export / GEMM staging).
+// ---------------------------------------------------------------------------
+}  // namespace fasq
+
+struct fasq_layer {
+    int64_t F_out = 0, F_in = 0;
+    int32_t d = 0, C = 0, group = 0, N_ss = 0, N_cb = 0;
+    int32_t row_offset = 0;
+    int32_t F_out_pad = 0;     // multiple of 32
+    int32_t n_groups = 0;      // ceil(N_ss / 32)
+    int32_t E = 0;             // cbimg entry bytes
+    int device = 0;
+    uint8_t* idx = nullptr;    // physical indices
+    uint8_t* cbimg = nullptr;  // GEMV codebook image
+    __half* cb = nullptr;      // logical codebooks
+    int64_t idx_bytes = 0, cbimg_bytes = 0, cb_bytes = 0;
+};
+
+namespace fasq {
+
+// ---- error plumbing --------------------------------------------------------
+void set_error(const std::string& msg);
+fasq_status cuda_fail(cudaError_t e, const char* what);
+void set_launch_count(int n);
+void add_launch_count(int n);
+
+#define FASQ_CUDA_TRY(expr)                                       \
+    do {                                                          \
+        cudaError_t _e = (expr);                                  \
+        if (_e != cudaSuccess) return ::fasq::cuda_fail(_e, #expr); \
+    } while (0)
+
+inline int entry_bytes(int d) { return d <= 2 ? 4 : d * 2; }
+
+// ---- layout kernels (layout.cu) ---------------------------------------------
+fasq_status alloc_layer_storage(fasq_layer* L);
+fasq_status build_physical_from_logical(fasq_layer* L, const __half* cb_logical,
+                                        const uint8_t* idx_logical, cudaStream_t st);
+fasq_status build_cbimg(fasq_layer* L, cudaStream_t st);
+fasq_status export_logical(const fasq_layer* L, __half* cb_out, uint8_t* idx_out, cudaStream_t st);
+fasq_status copy_rows(const fasq_layer* src, fasq_layer* dst, int32_t row0, cudaStream_t st);
+fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
+                             int32_t group);
+
+// ---- compute entry points ---------------------------------------------------
+fasq_status gemv_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt,
+                        uint32_t flags, cudaStream_t st);
+fasq_status gemm_lut_launch(const fasq_layer* L, const __half* X, int64_t M, void* Y,
+                            fasq_dtype yt, cudaStream_t st);
+fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void* Y,
+                           fasq_dtype yt, cudaStream_t st);
+bool gemm_tc_supported(const fasq_layer* L, int64_t M);
+fasq_status pack_run(const __half* W, fasq_layer* L, const fasq_pack_params* p, cudaStream_t st,
+                     __half* cb_logical_out, uint8_t* idx_logical_out);
+
+// ---- device helpers -----------------------------------------------------------
+namespace dev {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+// acc += c.lo*x.lo + c.hi*x.hi with exact fp16 products, fp32 accumulation
+// (fma.rn.f32.f16 -> SASS FHFMA).
+__device__ __forceinline__ float fhfma2(uint32_t c, uint32_t x, float acc) {
+    asm("{.reg .f16 a, b, e, f;\n\t"
+        "mov.b32 {a, b}, %1;\n\t"
+        "mov.b32 {e, f}, %2;\n\t"
+        "fma.rn.f32.f16 %0, a, e, %0;\n\t"
+        "fma.rn.f32.f16 %0, b, f, %0;}"
+        : "+f"(acc) : "r"(c), "r"(x));
+    return acc;
+}
+__device__ __forceinline__ float fhfma1(uint32_t c, uint32_t x, float acc) {
+    asm("{.reg .f16 a, b, e, f;\n\t"
+        "mov.b32 {a, b}, %1;\n\t"
+        "mov.b32 {e, f}, %2;\n\t"
+        "fma.rn.f32.f16 %0, a, e, %0;}"
+        : "+f"(acc) : "r"(c), "r"(x));
+    return acc;
+}
+
+// ---- mbarrier / bulk copy (TMA engine) -------------------------------------
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count));
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;}"
+        : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+// 1-D bulk async copy global -> shared (this CTA), completion on mbarrier.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                              uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        :: "r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(policy) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// Programmatic dependent launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+}  // namespace dev
+}  // namespace fasq

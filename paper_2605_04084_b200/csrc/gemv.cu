@@ -1,0 +1,426 @@
+// gemv.cu -- FASQ decode GEMV for sm_100a (batch 1..8).
+//
+// Computes Eq. 3, y[b][j] = sum_ss dot(x[b]_ss, T_cluster[ss][T_index[ss][j]]),
+// directly on the codebooks + indices, never materialising W.  The
+// paper's RTX 3090 design (Alg. 2: one thread per output row, the
+// subspace codebook through L1, atomicAdd split-K) is prior art only; on
+// B200 its 32 lanes all gather from ONE 1 KiB codebook at random rows, i.e.
+// ~3 SMEM/L1 wavefronts per warp-gather.  This kernel instead:
+//
+//  * lane l of a warp owns output rows r = l (mod 32) and walks the 32
+//    subspaces of a group in a lane-ROTATED order (subspace (s + rot_l) & 31
+//    at step s); the codebook image of the 32 subspaces sits in SMEM k-major,
+//    [C][32 lanes][E bytes], so at every step the 32 lanes hit 32 distinct
+//    banks whatever the indices are -> one wavefront per warp-gather, and each
+//    lane accumulates whole rows in registers (no cross-lane reduction);
+//  * the index table is stored pre-rotated ([group][row][32] bytes, see
+//    layout.cu) so the byte for step s sits at a fixed register position and
+//    ONE `prmt` turns it into the SMEM address (k*256 | 4*sub) -- together
+//    with one LDS and two FHFMA (fma.rn.f32.f16: exact fp16 product, fp32
+//    accumulation) that is 4 instructions per index at d = 2;
+//  * a producer warp streams each (row tile, group) index chunk and the
+//    group's codebook image into a 2-stage SMEM ring with the TMA bulk-copy
+//    engine (cp.async.bulk + mbarrier complete_tx); consumers never issue
+//    global loads in the hot loop;
+//  * split-K over subspace groups (grid.y) is merged deterministically:
+//    partial sums [ks][B][F_out] then a fixed-order reduce kernel (the
+//    paper's atomicAdd merge, is order-nondeterministic).
+#include <algorithm>
+#include <mutex>
+
+#include "fasq_internal.cuh"
+
+namespace fasq {
+
+struct GemvParams {
+    const uint8_t* idx;     // [n_groups][F_out_pad][32]
+    const uint8_t* cbimg;   // [n_groups][C][32][E]
+    const __half* x;        // [B][F_in]
+    void* y;                // [B][F_out]
+    float* partial;         // [ksplit][B][F_out_pad] (ksplit > 1)
+    int F_in, F_out, F_out_pad, N_ss, n_groups, C, B;
+    int ksplit, y_f32;
+    int gmax;               // max groups per CTA (x staging capacity)
+};
+
+template <int E>
+struct CbGeom {  // SMEM codebook ring geometry (2 slots)
+    // E == 4: row k = [slot0: 32 x 4 B][slot1: 32 x 4 B] (256 B), so the
+    // prmt-built address k*256 + 4*sub needs only an immediate slot offset.
+    static __device__ __forceinline__ uint32_t row_bytes() { return E == 4 ? 256u : 32u * E; }
+    static __device__ __forceinline__ uint32_t slot_off(int slot, int C) {
+        return E == 4 ? 128u * slot : (uint32_t)slot * (uint32_t)C * 32u * E;
+    }
+};
+
+// x staging: per group, 64 entries (subspaces 0..31 twice, so the rotated
+// index (s + rot) needs no wrap) x NB batches x E bytes.
+template <int D, int NB, int RPL, int NW>
+__global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
+    constexpr int E = D <= 2 ? 4 : 2 * D;
+    constexpr int R = 32 * NW * RPL;          // rows per CTA tile
+    constexpr int XG = 64 * NB * E;           // x bytes per staged group
+    extern __shared__ __align__(1024) uint8_t smem[];
+
+    const int C = p.C;
+    const int rt = blockIdx.x, ks = blockIdx.y;
+    const int g_begin = (int)((int64_t)ks * p.n_groups / p.ksplit);
+    const int g_end = (int)((int64_t)(ks + 1) * p.n_groups / p.ksplit);
+    const int ng = g_end - g_begin;
+    const int r0 = rt * R;
+    const int rows_valid = min(R, p.F_out_pad - r0);   // multiple of 32
+
+    uint8_t* s_cb = smem;                                     // 2*C*32*E
+    uint8_t* s_x = s_cb + 2 * C * 32 * E;                     // gmax*XG
+    uint8_t* s_idx = s_x + p.gmax * XG;                       // 2*R*32
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_idx + 2 * R * 32);  // full[2], empty[2]
+    const uint32_t cb_u = dev::smem_u32(s_cb);
+    const uint32_t x_u = dev::smem_u32(s_x);
+    const uint32_t idx_u = dev::smem_u32(s_idx);
+    const uint32_t full0 = dev::smem_u32(&bars[0]);
+    const uint32_t empty0 = dev::smem_u32(&bars[2]);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        dev::mbar_init(full0, 1);
+        dev::mbar_init(full0 + 8, 1);
+        dev::mbar_init(empty0, NW);
+        dev::mbar_init(empty0 + 8, NW);
+        dev::fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == NW) {
+        // ------------------------- producer warp -------------------------
+        const uint32_t idx_chunk = (uint32_t)rows_valid * 32u;
+        const uint32_t cb_bytes = (uint32_t)C * 32u * E;
+        for (int i = 0; i < ng; ++i) {
+            const int slot = i & 1;
+            const uint32_t full = full0 + 8 * slot, empty = empty0 + 8 * slot;
+            if (i >= 2) dev::mbar_wait(empty, ((i >> 1) + 1) & 1);
+            const int g = g_begin + i;
+            if (lane == 0) dev::mbar_arrive_expect_tx(full, idx_chunk + cb_bytes);
+            __syncwarp();
+            const uint8_t* cbsrc = p.cbimg + (size_t)g * cb_bytes;
+            if (E == 4) {
+                for (int k = lane; k < C; k += 32)
+                    dev::bulk_g2s(cb_u + (uint32_t)k * 256u + 128u * slot, cbsrc + (size_t)k * 128, 128u, full);
+            } else if (lane == 0) {
+                dev::bulk_g2s(cb_u + CbGeom<E>::slot_off(slot, C), cbsrc, cb_bytes, full);
+            }
+            if (lane == 0)
+                dev::bulk_g2s(idx_u + (uint32_t)slot * R * 32u,
+                              p.idx + ((size_t)g * p.F_out_pad + r0) * 32, idx_chunk, full);
+        }
+        dev::pdl_launch_dependents();
+        return;
+    }
+
+    // --------------------------- consumer warps ----------------------------
+    // x staging (after the previous kernel's writes are visible).
+    dev::pdl_wait();
+    {
+        const int tid = threadIdx.x;
+        const int n_ent = ng * 64 * NB;   // entries of E bytes
+        for (int t = tid; t < n_ent; t += NW * 32) {
+            const int b = t % NB;
+            const int e64 = (t / NB) % 64;
+            const int gl = t / (NB * 64);
+            const int ss = (g_begin + gl) * 32 + (e64 & 31);
+            uint32_t w[4] = {0u, 0u, 0u, 0u};
+            if (b < p.B && ss < p.N_ss) {
+                const uint16_t* src = reinterpret_cast<const uint16_t*>(p.x) + (size_t)b * p.F_in + (size_t)ss * D;
+#pragma unroll
+                for (int e = 0; e < D; ++e) w[e >> 1] |= (uint32_t)src[e] << (16 * (e & 1));
+            }
+            uint32_t* dst = reinterpret_cast<uint32_t*>(s_x + (size_t)t * E);
+#pragma unroll
+            for (int q = 0; q < E / 4; ++q) dst[q] = w[q];
+        }
+        asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
+    }
+
+    const int hA = (lane >> 2) & 1;                 // conflict-free LDS.128 of 32-B rows
+    const int rot = (lane + 16 * hA) & 31;          // lane's subspace rotation
+    // lowbyte constants: byte j of L[w] = E' * sub(4w + j) (E' = 4 or 8)
+    constexpr int LB = (E == 4) ? 4 : 8;            // lowbyte multiplier
+    constexpr int PER = (E == 4) ? 4 : 2;           // lowbytes per register
+    constexpr int NL = 32 / PER;
+    uint32_t Lr[NL];
+#pragma unroll
+    for (int w = 0; w < NL; ++w) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) v |= (uint32_t)(((4 * 0 + w * PER + j + rot) & 31) * LB) << (8 * j);
+        Lr[w] = v;
+    }
+
+    float acc[RPL][NB];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
+
+    const int warp_row0 = warp * 32 * RPL;
+    for (int i = 0; i < ng; ++i) {
+        const int slot = i & 1;
+        dev::mbar_wait(full0 + 8 * slot, (i >> 1) & 1);
+        // this lane's index words: [q][8]
+        uint32_t iw[RPL][8];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+            const int rl = warp_row0 + q * 32 + lane;
+            const uint32_t a = idx_u + (uint32_t)slot * R * 32u + (uint32_t)rl * 32u;
+            if (warp_row0 + q * 32 < rows_valid) {
+                uint4 v0 = dev::lds128(a + 16u * hA);
+                uint4 v1 = dev::lds128(a + 16u * (1 - hA));
+                iw[q][0] = v0.x; iw[q][1] = v0.y; iw[q][2] = v0.z; iw[q][3] = v0.w;
+                iw[q][4] = v1.x; iw[q][5] = v1.y; iw[q][6] = v1.z; iw[q][7] = v1.w;
+            } else {
+#pragma unroll
+                for (int w = 0; w < 8; ++w) iw[q][w] = 0u;
+            }
+        }
+        const uint32_t cbs = cb_u + CbGeom<E>::slot_off(slot, C);
+        const uint32_t xb = x_u + (uint32_t)i * XG + (uint32_t)rot * (NB * E);
+#pragma unroll
+        for (int s = 0; s < 32; ++s) {
+            // x entries for this lane's subspace at step s, all batches
+            uint32_t xv[NB][E / 4];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                const uint32_t xa = xb + (uint32_t)(s * NB * E + b * E);
+                if (E == 4) {
+                    xv[b][0] = dev::lds32(xa);
+                } else if (E == 8) {
+                    uint2 t2 = dev::lds64(xa);
+                    xv[b][0] = t2.x; xv[b][1 % (E / 4)] = t2.y;
+                } else {
+                    uint4 t4 = dev::lds128(xa);
+                    xv[b][0] = t4.x; xv[b][1 % (E / 4)] = t4.y;
+                    xv[b][2 % (E / 4)] = t4.z; xv[b][3 % (E / 4)] = t4.w;
+                }
+            }
+            const int wi = s >> 2, j = s & 3;
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+                uint32_t addr;
+                if (E == 4) {
+                    // byte0 = 4*sub (L byte j), byte1 = k (idx byte j), bytes2,3 = sign of L byte (0)
+                    const uint32_t sel = (uint32_t)(4 + j) | ((uint32_t)j << 4) | ((uint32_t)(12 + j) << 8) |
+                                         ((uint32_t)(12 + j) << 12);
+                    addr = dev::prmt(iw[q][wi], Lr[wi], sel);
+                } else {
+                    // L[w] bytes: [8*sub(2w), 8*sub(2w+1), 0, 0]
+                    const int lw = s >> 1, lj = s & 1;
+                    const uint32_t sel = (uint32_t)(4 + lj) | ((uint32_t)j << 4) | (6u << 8) | (6u << 12);
+                    addr = dev::prmt(iw[q][wi], Lr[lw], sel);
+                    if (E == 16) addr <<= 1;    // k*512 + 16*sub
+                }
+                if (warp_row0 + q * 32 < rows_valid) {
+                    if (E == 4) {
+                        const uint32_t c = dev::lds32(cbs + addr);
+#pragma unroll
+                        for (int b = 0; b < NB; ++b)
+                            acc[q][b] = (D == 1) ? dev::fhfma1(c, xv[b][0], acc[q][b])
+                                                 : dev::fhfma2(c, xv[b][0], acc[q][b]);
+                    } else if (E == 8) {
+                        const uint2 c = dev::lds64(cbs + addr);
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) {
+                            acc[q][b] = dev::fhfma2(c.x, xv[b][0], acc[q][b]);
+                            acc[q][b] = dev::fhfma2(c.y, xv[b][1 % (E / 4)], acc[q][b]);
+                        }
+                    } else {
+                        const uint4 c = dev::lds128(cbs + addr);
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) {
+                            acc[q][b] = dev::fhfma2(c.x, xv[b][0], acc[q][b]);
+                            acc[q][b] = dev::fhfma2(c.y, xv[b][1 % (E / 4)], acc[q][b]);
+                            acc[q][b] = dev::fhfma2(c.z, xv[b][2 % (E / 4)], acc[q][b]);
+                            acc[q][b] = dev::fhfma2(c.w, xv[b][3 % (E / 4)], acc[q][b]);
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+    }
+
+    // ------------------------------ epilogue --------------------------------
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+        const int row = r0 + warp_row0 + q * 32 + lane;
+        if (warp_row0 + q * 32 >= rows_valid) continue;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            if (b >= p.B) continue;
+            if (p.ksplit == 1) {
+                if (row < p.F_out) {
+                    if (p.y_f32) reinterpret_cast<float*>(p.y)[(size_t)b * p.F_out + row] = acc[q][b];
+                    else reinterpret_cast<__half*>(p.y)[(size_t)b * p.F_out + row] = __float2half_rn(acc[q][b]);
+                }
+            } else {
+                p.partial[((size_t)ks * p.B + b) * p.F_out_pad + row] = acc[q][b];
+            }
+        }
+    }
+}
+
+// Fixed-order split-K merge: y[b][r] = sum_{ks ascending} partial[ks][b][r].
+__global__ void k_splitk_reduce(const float* __restrict__ partial, void* y, int ksplit, int B, int F_out,
+                                int F_out_pad, int y_f32) {
+    dev::pdl_wait();
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)B * F_out) return;
+    int b = (int)(t / F_out), r = (int)(t % F_out);
+    float s = 0.f;
+    for (int k = 0; k < ksplit; ++k) s += partial[((size_t)k * B + b) * F_out_pad + r];
+    if (y_f32) reinterpret_cast<float*>(y)[t] = s;
+    else reinterpret_cast<__half*>(y)[t] = __float2half_rn(s);
+}
+
+// ------------------------------- host side ----------------------------------
+static int g_num_sms = 0;
+static std::mutex g_mu;
+
+static int num_sms() {
+    if (g_num_sms == 0) {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        g_num_sms = n > 0 ? n : 148;
+    }
+    return g_num_sms;
+}
+
+struct GemvPlan {
+    int rpl, nw, R, row_tiles, ksplit, gmax;
+    size_t smem;
+};
+
+template <int D, int NB, int RPL, int NW>
+static fasq_status launch_gemv_t(const GemvParams& p0, const GemvPlan& pl, uint32_t flags, cudaStream_t st) {
+    constexpr int E = D <= 2 ? 4 : 2 * D;
+    auto kern = k_gemv<D, NB, RPL, NW>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        std::lock_guard<std::mutex> lk(g_mu);
+        FASQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_done = true;
+    }
+    (void)E;
+    GemvParams p = p0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pl.row_tiles, pl.ksplit, 1);
+    cfg.blockDim = dim3((NW + 1) * 32, 1, 1);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (flags & FASQ_FLAG_PDL) ? 1 : 0;
+    FASQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
+    return FASQ_OK;
+}
+
+template <int D, int NB>
+static fasq_status dispatch_cfg(const GemvParams& p, const GemvPlan& pl, uint32_t flags, cudaStream_t st) {
+    if (pl.rpl == 4 && pl.nw == 8) return launch_gemv_t<D, NB, 4, 8>(p, pl, flags, st);
+    if (pl.rpl == 2 && pl.nw == 8) return launch_gemv_t<D, NB, 2, 8>(p, pl, flags, st);
+    if (pl.rpl == 1 && pl.nw == 8) return launch_gemv_t<D, NB, 1, 8>(p, pl, flags, st);
+    return FASQ_E_UNSUPPORTED;
+}
+
+template <int D>
+static fasq_status dispatch_nb(int NB, const GemvParams& p, const GemvPlan& pl, uint32_t flags, cudaStream_t st) {
+    switch (NB) {
+        case 1: return dispatch_cfg<D, 1>(p, pl, flags, st);
+        case 2: return dispatch_cfg<D, 2>(p, pl, flags, st);
+        case 4: return dispatch_cfg<D, 4>(p, pl, flags, st);
+        case 8: return dispatch_cfg<D, 8>(p, pl, flags, st);
+    }
+    return FASQ_E_UNSUPPORTED;
+}
+
+static GemvPlan plan_gemv(const fasq_layer* L, int NB) {
+    GemvPlan pl{};
+    pl.nw = 8;
+    pl.rpl = NB <= 2 ? 4 : (NB == 4 ? 2 : 1);
+    pl.R = 32 * pl.nw * pl.rpl;
+    const int E = L->E;
+    pl.row_tiles = (L->F_out_pad + pl.R - 1) / pl.R;
+    const int sms = num_sms();
+    int ks = std::max(1, sms / pl.row_tiles);
+    ks = std::min(ks, L->n_groups);
+    // x staging budget: gmax * 64 * NB * E <= 32 KiB
+    const int xg = 64 * NB * E;
+    const int gcap = std::max(1, (32 * 1024) / xg);
+    while ((L->n_groups + ks - 1) / ks > gcap && ks < L->n_groups) ++ks;
+    pl.ksplit = ks;
+    pl.gmax = (L->n_groups + ks - 1) / ks;
+    pl.smem = (size_t)2 * L->C * 32 * E + (size_t)pl.gmax * xg + (size_t)2 * pl.R * 32 + 64;
+    return pl;
+}
+
+fasq_status gemv_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt, uint32_t flags,
+                        cudaStream_t st) {
+    const int NB = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;
+    GemvPlan pl = plan_gemv(L, NB);
+    GemvParams p{};
+    p.idx = L->idx;
+    p.cbimg = L->cbimg;
+    p.x = x;
+    p.y = y;
+    p.F_in = (int)L->F_in;
+    p.F_out = (int)L->F_out;
+    p.F_out_pad = L->F_out_pad;
+    p.N_ss = L->N_ss;
+    p.n_groups = L->n_groups;
+    p.C = L->C;
+    p.B = B;
+    p.ksplit = pl.ksplit;
+    p.y_f32 = yt == FASQ_F32;
+    p.gmax = pl.gmax;
+    float* partial = nullptr;
+    if (pl.ksplit > 1) {
+        size_t bytes = (size_t)pl.ksplit * B * L->F_out_pad * sizeof(float);
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&partial), bytes, st);
+        if (e != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
+    }
+    p.partial = partial;
+    fasq_status s;
+    switch (L->d) {
+        case 1: s = dispatch_nb<1>(NB, p, pl, flags, st); break;
+        case 2: s = dispatch_nb<2>(NB, p, pl, flags, st); break;
+        case 4: s = dispatch_nb<4>(NB, p, pl, flags, st); break;
+        case 8: s = dispatch_nb<8>(NB, p, pl, flags, st); break;
+        default: s = FASQ_E_UNSUPPORTED;
+    }
+    int launches = 1;
+    if (s == FASQ_OK && pl.ksplit > 1) {
+        int64_t n = (int64_t)B * L->F_out;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)((n + 255) / 256));
+        cfg.blockDim = dim3(256);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;   // always safe: it only waits for the GEMV's partials
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_splitk_reduce, (const float*)partial, y, pl.ksplit, B,
+                                           (int)L->F_out, L->F_out_pad, (int)(yt == FASQ_F32));
+        if (e != cudaSuccess) s = cuda_fail(e, "k_splitk_reduce");
+        launches = 2;
+    }
+    if (partial) cudaFreeAsync(partial, st);
+    if (s == FASQ_OK) set_launch_count(launches);
+    return s;
+}
+
+}  // namespace fasq

@@ -1,0 +1,139 @@
+// layout.cu -- logical <-> physical layout transforms for FASQ layers (sm_100a).
+//
+// Logical (ABI) layout: codebooks fp16 [N_cb][C][d], indices u8 [N_ss][F_out]
+// (Alg. 1 outputs T_cluster / T_index).  Physical layout: see
+// fasq_internal.cuh and DESIGN.md "Data layout in HBM".
+#include "fasq_internal.cuh"
+
+namespace fasq {
+
+fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
+                             int32_t group) {
+    if (F_out < 1 || F_in < 1 || d < 1 || C < 1 || group < 1) return FASQ_E_ARG;
+    if (d != 1 && d != 2 && d != 4 && d != 8) return FASQ_E_UNSUPPORTED;
+    if (C > 256) return FASQ_E_UNSUPPORTED;
+    if (F_in % d) return FASQ_E_NONDIVISIBLE;
+    int64_t N_ss = F_in / d;
+    if (N_ss % group) return FASQ_E_NONDIVISIBLE;
+    if (F_out > (1ll << 24) || N_ss > (1ll << 24)) return FASQ_E_UNSUPPORTED;
+    L->F_out = F_out;
+    L->F_in = F_in;
+    L->d = d;
+    L->C = C;
+    L->group = group;
+    L->N_ss = (int32_t)N_ss;
+    L->N_cb = (int32_t)(N_ss / group);
+    L->F_out_pad = (int32_t)((F_out + 31) / 32 * 32);
+    L->n_groups = (int32_t)((N_ss + kGroupSubs - 1) / kGroupSubs);
+    L->E = entry_bytes(d);
+    L->idx_bytes = (int64_t)L->n_groups * L->F_out_pad * kGroupSubs;
+    L->cbimg_bytes = (int64_t)L->n_groups * C * kGroupSubs * L->E;
+    L->cb_bytes = (int64_t)L->N_cb * C * d * 2;
+    return FASQ_OK;
+}
+
+fasq_status alloc_layer_storage(fasq_layer* L) {
+    cudaError_t e;
+    FASQ_CUDA_TRY(cudaGetDevice(&L->device));
+    e = cudaMalloc(&L->idx, (size_t)L->idx_bytes);
+    if (e != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
+    e = cudaMalloc(&L->cbimg, (size_t)L->cbimg_bytes);
+    if (e != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
+    e = cudaMalloc(&L->cb, (size_t)L->cb_bytes);
+    if (e != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
+    return FASQ_OK;
+}
+
+// One thread per (group g, padded row r): 32 output bytes.
+__global__ void k_idx_logical_to_phys(const uint8_t* __restrict__ idx_log, uint8_t* __restrict__ phys,
+                                      int F_out, int F_out_pad, int N_ss, int n_groups) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n_groups * F_out_pad) return;
+    int g = (int)(t / F_out_pad);
+    int r = (int)(t % F_out_pad);
+    uint32_t w[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) w[q] = 0;
+    if (r < F_out) {
+#pragma unroll
+        for (int p = 0; p < 32; ++p) {
+            int ss = g * kGroupSubs + ((p + r) & 31);
+            uint32_t v = ss < N_ss ? idx_log[(int64_t)ss * F_out + r] : 0u;
+            w[p >> 2] |= v << (8 * (p & 3));
+        }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(phys + t * 32);
+    dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
+__global__ void k_idx_phys_to_logical(const uint8_t* __restrict__ phys, uint8_t* __restrict__ idx_log,
+                                      int F_out, int F_out_pad, int N_ss, int n_groups) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n_groups * F_out_pad) return;
+    int g = (int)(t / F_out_pad);
+    int r = (int)(t % F_out_pad);
+    if (r >= F_out) return;
+    const uint8_t* src = phys + t * 32;
+#pragma unroll 4
+    for (int p = 0; p < 32; ++p) {
+        int ss = g * kGroupSubs + ((p + r) & 31);
+        if (ss < N_ss) idx_log[(int64_t)ss * F_out + r] = src[p];
+    }
+}
+
+// One thread per (group g, k, lane): entry of E bytes.
+__global__ void k_build_cbimg(const __half* __restrict__ cb, uint8_t* __restrict__ img, int C, int d,
+                              int group, int N_ss, int n_groups, int E) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = (int64_t)n_groups * C * kGroupSubs;
+    if (t >= total) return;
+    int lane = (int)(t % kGroupSubs);
+    int k = (int)((t / kGroupSubs) % C);
+    int g = (int)(t / ((int64_t)kGroupSubs * C));
+    int ss = g * kGroupSubs + lane;
+    uint16_t v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = 0;
+    if (ss < N_ss) {
+        const uint16_t* src = reinterpret_cast<const uint16_t*>(cb) + ((int64_t)(ss / group) * C + k) * d;
+        for (int e = 0; e < d; ++e) v[e] = src[e];
+    }
+    uint16_t* dst = reinterpret_cast<uint16_t*>(img + t * E);
+    for (int e = 0; e < E / 2; ++e) dst[e] = v[e];
+}
+
+static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+fasq_status build_physical_from_logical(fasq_layer* L, const __half* cb_logical, const uint8_t* idx_logical,
+                                        cudaStream_t st) {
+    if (cb_logical != L->cb)
+        FASQ_CUDA_TRY(cudaMemcpyAsync(L->cb, cb_logical, (size_t)L->cb_bytes, cudaMemcpyDeviceToDevice, st));
+    int64_t n = (int64_t)L->n_groups * L->F_out_pad;
+    k_idx_logical_to_phys<<<nblk(n, 256), 256, 0, st>>>(idx_logical, L->idx, (int)L->F_out, L->F_out_pad,
+                                                         L->N_ss, L->n_groups);
+    FASQ_CUDA_TRY(cudaGetLastError());
+    return build_cbimg(L, st);
+}
+
+fasq_status build_cbimg(fasq_layer* L, cudaStream_t st) {
+    int64_t n = (int64_t)L->n_groups * L->C * kGroupSubs;
+    k_build_cbimg<<<nblk(n, 256), 256, 0, st>>>(L->cb, L->cbimg, L->C, L->d, L->group, L->N_ss, L->n_groups,
+                                                 L->E);
+    FASQ_CUDA_TRY(cudaGetLastError());
+    return FASQ_OK;
+}
+
+fasq_status export_logical(const fasq_layer* L, __half* cb_out, uint8_t* idx_out, cudaStream_t st) {
+    if (cb_out)
+        FASQ_CUDA_TRY(cudaMemcpyAsync(cb_out, L->cb, (size_t)L->cb_bytes, cudaMemcpyDeviceToDevice, st));
+    if (idx_out) {
+        int64_t n = (int64_t)L->n_groups * L->F_out_pad;
+        k_idx_phys_to_logical<<<nblk(n, 256), 256, 0, st>>>(L->idx, idx_out, (int)L->F_out, L->F_out_pad,
+                                                             L->N_ss, L->n_groups);
+        FASQ_CUDA_TRY(cudaGetLastError());
+    }
+    return FASQ_OK;
+}
+
+}  // namespace fasq

@@ -65,3 +65,27 @@ def random_layer(F_out: int, F_in: int, d: int, C: int, group: int = 1, seed: in
     cb = g.normal(0.0, std, size=(N_cb, C, d)).astype(np.float16)
     idx = g.integers(0, C, size=(N_ss, F_out), dtype=np.uint8) if C <= 256 else None
     return cb, idx
+
+
+def torch_random_layer(F_out: int, F_in: int, d: int, C: int, group: int = 1, seed: int = 0,
+                       device: str = "cuda", std: float | None = None):
+    """Same recipe as :func:`random_layer` drawn with torch's generator on
+    ``device`` (fast for the full-size bench model; different stream of
+    random numbers than the numpy version)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    N_ss = F_in // d
+    N_cb = N_ss // group
+    if std is None:
+        std = 1.0 / float(np.sqrt(F_in))
+    cb = (torch.randn((N_cb, C, d), generator=g, device=device) * std).to(torch.float16)
+    idx = torch.randint(0, C, (N_ss, F_out), generator=g, device=device, dtype=torch.int32).to(torch.uint8)
+    return cb, idx
+
+
+def torch_activation(B: int, F_in: int, seed: int = 1, device: str = "cuda", std: float = 1.0):
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    return (torch.randn((B, F_in), generator=g, device=device) * std).to(torch.float16)

@@ -1,0 +1,59 @@
+"""The C-ABI library loads and exports every symbol include/fasq.h declares
+(no compute calls -- this runs without a GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "fasq.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fasq_[a-z_0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def fasq():
+    from paper_2605_04084_b200 import build
+    build.build()
+    import paper_2605_04084_b200 as F
+    return F
+
+
+def test_header_declares_expected(fasq):
+    decl = _declared()
+    assert set(decl) == set(fasq.EXPORTED), decl
+
+
+def test_library_exports_every_declared_symbol(fasq):
+    lib = ctypes.CDLL(fasq.LIB_PATH)
+    for name in _declared():
+        assert hasattr(lib, name), name
+
+
+def test_status_strings_and_version(fasq):
+    assert fasq.lib.fasq_abi_version() == 1
+    for code in (0, -1, -2, -3, -4, -5, -6, -7, -8):
+        s = fasq.lib.fasq_status_string(code).decode()
+        assert s.startswith("FASQ_"), s
+
+
+def test_argument_errors_are_synchronous(fasq):
+    out = ctypes.c_void_p()
+    # NULL pointers -> FASQ_E_ARG before touching any device
+    assert fasq.lib.fasq_import(None, None, 8, 8, 2, 4, 1, None, ctypes.byref(out)) == -1
+    assert fasq.lib.fasq_gemv(None, None, 1, None, 0, None) == -1
+    assert fasq.lib.fasq_gemm(None, None, 1, None, 0, 0, None) == -1
+    assert fasq.lib.fasq_export(None, None, None, None) == -1
+    info = fasq.LayerInfo()
+    assert fasq.lib.fasq_layer_info_get(None, ctypes.byref(info)) == -1
+
+
+def test_no_cpu_fallback_in_binding(fasq):
+    import torch
+    lay = object.__new__(fasq.Layer)
+    with pytest.raises(TypeError):
+        fasq._cuda(torch.zeros(4, dtype=torch.float16), torch.float16, "x")
