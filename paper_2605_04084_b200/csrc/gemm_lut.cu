@@ -1,7 +1,142 @@
-// gemm_lut.cu -- placeholder
+// gemm_lut.cu -- FASQ prefill GEMM, table-lookup variant (sm_100a).
+//
+// Alg. 3's math: for each token l and subspace ss a lookup table
+// LUT_ss[k] = dot(X[l]_ss, T_cluster[ss][k]) over all K_s centroids,
+// then Y[l][j] += LUT_ss[T_index[ss][j]].  The paper's design is output-
+// stationary with a double-buffered 257-float LUT per (token, subspace); here
+// one CTA owns 1024 weight rows x MT tokens, builds the LUTs of a whole
+// 32-subspace group at once in SMEM, [C][32 subspaces] fp32 per token laid out
+// like the GEMV codebook image, and every lane (= 4 weight rows, rotated
+// subspace order) gathers conflict-free with the one-`prmt` address.  The
+// gathers are pure FADD on CUDA cores -- no tensor cores --
+// which is why the EXPAND variant exists (gemm_tc.cu).
 #include "fasq_internal.cuh"
+
 namespace fasq {
-fasq_status gemm_lut_launch(const fasq_layer*, const __half*, int64_t, void*, fasq_dtype, cudaStream_t) {
-    return FASQ_E_UNSUPPORTED;
+
+namespace {
+
+constexpr int LUT_MT = 4;          // tokens per CTA
+constexpr int LUT_RPT = 4;         // weight rows per thread
+constexpr int LUT_THREADS = 256;
+constexpr int LUT_R = LUT_THREADS * LUT_RPT;   // 1024 rows per CTA
+
+struct LutParams {
+    const uint8_t* idx;       // [n_groups][F_out_pad][32]
+    const uint8_t* cbimg;     // [n_groups][C][32][4]   (d <= 2)
+    const __half* X;          // [M][F_in]
+    void* Y;
+    int M, F_in, F_out, F_out_pad, n_groups, N_ss, C, d, y_f32;
+};
+
+// LUT SMEM: token pair tp = t>>1 occupies C*256 B; row k = [t even: 32 x f32][t odd: 32 x f32]
+__global__ void __launch_bounds__(LUT_THREADS, 1) k_gemm_lut(LutParams p) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int C = p.C;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r_base = blockIdx.x * LUT_R;
+    const int m0 = blockIdx.y * LUT_MT;
+    const uint32_t lut_u = dev::smem_u32(smem);
+    const int rot = lane;   // natural byte order of the row-rotated index layout
+    uint32_t Lr[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v |= (uint32_t)(((4 * w + j + rot) & 31) * 4) << (8 * j);
+        Lr[w] = v;
+    }
+    float acc[LUT_RPT][LUT_MT];
+#pragma unroll
+    for (int q = 0; q < LUT_RPT; ++q)
+#pragma unroll
+        for (int t = 0; t < LUT_MT; ++t) acc[q][t] = 0.f;
+
+    for (int g = 0; g < p.n_groups; ++g) {
+        __syncthreads();   // previous group's gathers done
+        // build: entry (t, k, sub) = sum_e x[t][sub*d+e] * c[sub][k][e]  (fp32, exact fp16 products)
+        const uint32_t* cbg = reinterpret_cast<const uint32_t*>(p.cbimg + (size_t)g * C * 128);
+        for (int e = tid; e < C * 32; e += LUT_THREADS) {
+            const int k = e >> 5, sub = e & 31;
+            const uint32_t c = cbg[e];
+            const int ss = g * 32 + sub;
+#pragma unroll
+            for (int t = 0; t < LUT_MT; ++t) {
+                const int m = m0 + t;
+                uint32_t xv = 0;
+                if (m < p.M && ss < p.N_ss) {
+                    const uint16_t* xs = reinterpret_cast<const uint16_t*>(p.X) + (size_t)m * p.F_in + (size_t)ss * p.d;
+                    xv = p.d == 2 ? (uint32_t)xs[0] | ((uint32_t)xs[1] << 16) : (uint32_t)xs[0];
+                }
+                const float v = dev::fhfma2(c, xv, 0.f);
+                reinterpret_cast<float*>(smem)[((t >> 1) * C * 64) + k * 64 + (t & 1) * 32 + sub] = v;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < LUT_RPT; ++q) {
+            const int row = r_base + q * LUT_THREADS + warp * 32 + lane;
+            if (row >= p.F_out_pad) continue;
+            const uint4* ip = reinterpret_cast<const uint4*>(p.idx + ((size_t)g * p.F_out_pad + row) * 32);
+            const uint4 v0 = ip[0], v1 = ip[1];
+            const uint32_t iw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+            for (int st = 0; st < 32; ++st) {
+                const int j = st & 3;
+                const uint32_t sel = (uint32_t)(4 + j) | ((uint32_t)j << 4) | ((uint32_t)(12 + j) << 8) |
+                                     ((uint32_t)(12 + j) << 12);
+                const uint32_t a = dev::prmt(iw[st >> 2], Lr[st >> 2], sel);
+#pragma unroll
+                for (int t = 0; t < LUT_MT; ++t)
+                    acc[q][t] += __uint_as_float(dev::lds32(lut_u + (uint32_t)((t >> 1) * C * 256 + (t & 1) * 128) + a));
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < LUT_RPT; ++q) {
+        const int row = r_base + q * LUT_THREADS + warp * 32 + lane;
+        if (row >= p.F_out) continue;
+#pragma unroll
+        for (int t = 0; t < LUT_MT; ++t) {
+            const int m = m0 + t;
+            if (m >= p.M) continue;
+            if (p.y_f32) reinterpret_cast<float*>(p.Y)[(size_t)m * p.F_out + row] = acc[q][t];
+            else reinterpret_cast<__half*>(p.Y)[(size_t)m * p.F_out + row] = __float2half_rn(acc[q][t]);
+        }
+    }
 }
+
+}  // namespace
+
+fasq_status gemm_lut_launch(const fasq_layer* L, const __half* X, int64_t M, void* Y, fasq_dtype yt,
+                            cudaStream_t st) {
+    if (L->d > 2) { set_error("GEMM-LUT supports d <= 2"); return FASQ_E_UNSUPPORTED; }
+    if (M > (1ll << 30)) return FASQ_E_UNSUPPORTED;
+    LutParams p{};
+    p.idx = L->idx;
+    p.cbimg = L->cbimg;
+    p.X = X;
+    p.Y = Y;
+    p.M = (int)M;
+    p.F_in = (int)L->F_in;
+    p.F_out = (int)L->F_out;
+    p.F_out_pad = L->F_out_pad;
+    p.n_groups = L->n_groups;
+    p.N_ss = L->N_ss;
+    p.C = L->C;
+    p.d = L->d;
+    p.y_f32 = yt == FASQ_F32;
+    const size_t smem = (size_t)(LUT_MT / 2) * L->C * 256;
+    static bool attr = false;
+    if (!attr) {
+        FASQ_CUDA_TRY(cudaFuncSetAttribute(k_gemm_lut, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    dim3 grid((unsigned)((L->F_out_pad + LUT_R - 1) / LUT_R), (unsigned)((M + LUT_MT - 1) / LUT_MT));
+    k_gemm_lut<<<grid, LUT_THREADS, smem, st>>>(p);
+    FASQ_CUDA_TRY(cudaGetLastError());
+    set_launch_count(1);
+    return FASQ_OK;
+}
+
 }  // namespace fasq

@@ -1,8 +1,345 @@
-// gemm_tc.cu -- placeholder
+// gemm_tc.cu -- FASQ prefill GEMM, centroid-EXPAND variant on tcgen05 (sm_100a).
+//
+// Y[M][F_out] = X[M][F_in] . W_hat^T computed as a dense fp16 contraction on
+// the 5th-gen tensor cores WITHOUT materialising W_hat in HBM: the paper's
+// future-work direction (1), "a pipelined reconstruction kernel that rebuilds
+// FP16 weight tiles in parallel with tensor-core GEMM, avoiding full
+// materialization".  Per CTA tile (128 tokens x 256 weight rows)
+// and per K-chunk of 64 input features (= one group of 32 subspaces at d=2):
+//
+//   producer warp : TMA 2-D load of the X tile (128B swizzle) + bulk copies of
+//                   the group's codebook image and the tile's index chunk;
+//   8 expand warps: lane = weight row; gather the 32 centroids of the row from
+//                   the SMEM codebook image in the conflict-free rotated order
+//                   (same layout as the GEMV) and store them into the B tile
+//                   in the UMMA K-major SWIZZLE_128B layout (never to HBM);
+//   MMA thread    : 4 x tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256,
+//                   K=16) into a TMEM fp32 accumulator; tcgen05.commit frees
+//                   the stage;
+//   epilogue      : tcgen05.ld (32x32b) -> fp32/fp16 -> Y.
+#include <cuda.h>
+
+#include <mutex>
+
 #include "fasq_internal.cuh"
+
 namespace fasq {
-bool gemm_tc_supported(const fasq_layer*, int64_t) { return false; }
-fasq_status gemm_tc_launch(const fasq_layer*, const __half*, int64_t, void*, fasq_dtype, cudaStream_t) {
-    return FASQ_E_UNSUPPORTED;
+
+namespace {
+
+constexpr int TC_M = 128;          // tokens per CTA tile (UMMA M)
+constexpr int TC_N = 256;          // weight rows per CTA tile (UMMA N)
+constexpr int TC_K = 64;           // K elements per chunk (one 128B swizzle atom row)
+constexpr int TC_STAGES = 2;
+constexpr int TC_EXP_WARPS = 8;    // expansion warps (lane = weight row)
+constexpr int TC_THREADS = (2 + TC_EXP_WARPS) * 32;
+
+struct TcParams {
+    const uint8_t* idx;      // [n_groups][F_out_pad][32]
+    const uint8_t* cbimg;    // [n_groups][C][32][4]
+    void* Y;
+    int M, F_out, F_out_pad, n_groups, C, y_f32;
+};
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    // K-major, SWIZZLE_128B: start>>4 [0,14), LBO=0, SBO=1024>>4 [32,46),
+    // version=1 [46,48), layout_type=2 (128B) [61,64)
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)(1024u >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
 }
+
+// kind::f16 instruction descriptor: D=f32, A=B=f16, both K-major, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        :: "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar) : "memory");
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-B alignment for the swizzled tiles
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int C = p.C;
+    constexpr int A_BYTES = TC_M * TC_K * 2;      // 16 KiB
+    constexpr int B_BYTES = TC_N * TC_K * 2;      // 32 KiB
+    constexpr int IDX_BYTES = TC_N * 32;          // 8 KiB
+    const int CB_BYTES = C * 128;                 // per stage: [C][32][4]
+    uint8_t* sA = smem;                                   // STAGES * A
+    uint8_t* sB = sA + TC_STAGES * A_BYTES;               // STAGES * B
+    uint8_t* sI = sB + TC_STAGES * B_BYTES;               // STAGES * IDX
+    uint8_t* sC = sI + TC_STAGES * IDX_BYTES;             // [C][2 stages][32][4]: row k = 256 B
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sC + TC_STAGES * CB_BYTES);
+    // bars: full[S], bfull[S], empty[S], accum
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * TC_STAGES + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n0 = blockIdx.x * TC_N;          // weight-row tile
+    const int m0 = blockIdx.y * TC_M;          // token tile
+    const int nk = p.n_groups;
+    const uint32_t bar0 = dev::smem_u32(bars);
+    auto full_bar = [&](int s) { return bar0 + 8u * s; };
+    auto bfull_bar = [&](int s) { return bar0 + 8u * (TC_STAGES + s); };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (2 * TC_STAGES + s); };
+    const uint32_t accum_bar = bar0 + 8u * (3 * TC_STAGES);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) {
+            dev::mbar_init(full_bar(s), 1);
+            dev::mbar_init(bfull_bar(s), TC_EXP_WARPS);
+            dev::mbar_init(empty_bar(s), 1);
+        }
+        dev::mbar_init(accum_bar, 1);
+        dev::fence_barrier_init();
+    }
+    if (warp == 1) {   // TMEM allocation (256 fp32 columns = the 128x256 accumulator)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(dev::smem_u32(tmem_slot)), "n"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------ producer ------------------------------
+        if (lane == 0) asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+        const int rows = min(TC_N, p.F_out_pad - n0);          // idx rows present (multiple of 32)
+        const uint32_t idx_bytes = (uint32_t)rows * 32u;
+        const uint32_t cb_u = dev::smem_u32(sC);
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % TC_STAGES;
+            if (i >= TC_STAGES) dev::mbar_wait(empty_bar(s), ((i / TC_STAGES) + 1) & 1);
+            if (lane == 0) {
+                dev::mbar_arrive_expect_tx(full_bar(s), (uint32_t)A_BYTES + idx_bytes + (uint32_t)CB_BYTES);
+                tma_load_2d(dev::smem_u32(sA + s * A_BYTES), &xmap, i * TC_K, m0, full_bar(s));
+                dev::bulk_g2s(dev::smem_u32(sI + s * IDX_BYTES), p.idx + ((size_t)i * p.F_out_pad + n0) * 32,
+                              idx_bytes, full_bar(s));
+            }
+            __syncwarp();
+            const uint8_t* cbsrc = p.cbimg + (size_t)i * CB_BYTES;
+            for (int k = lane; k < C; k += 32)
+                dev::bulk_g2s(cb_u + (uint32_t)k * 256u + 128u * s, cbsrc + (size_t)k * 128, 128u, full_bar(s));
+        }
+    } else if (warp == 1) {
+        // ------------------------------ MMA issuer -----------------------------
+        constexpr uint32_t idesc = idesc_f16(TC_M, TC_N);
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % TC_STAGES;
+            const uint32_t ph = (i / TC_STAGES) & 1;
+            dev::mbar_wait(full_bar(s), ph);
+            dev::mbar_wait(bfull_bar(s), ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (lane == 0) {
+                const uint32_t a_base = dev::smem_u32(sA + s * A_BYTES);
+                const uint32_t b_base = dev::smem_u32(sB + s * B_BYTES);
+#pragma unroll
+                for (int kk = 0; kk < TC_K / 16; ++kk) {
+                    const uint64_t ad = umma_desc_sw128(a_base + kk * 32);
+                    const uint64_t bd = umma_desc_sw128(b_base + kk * 32);
+                    const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+                    asm volatile(
+                        "{.reg .pred p;\n\t"
+                        "setp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
+                        :: "r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                             :: "r"(empty_bar(s)) : "memory");
+                if (i == nk - 1)
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                                 :: "r"(accum_bar) : "memory");
+            }
+            __syncwarp();
+        }
+    } else {
+        // ------------------------------ expansion ------------------------------
+        const int ew = warp - 2;                 // 0..7
+        const int rl = ew * 32 + lane;           // local weight row 0..255
+        // natural byte order: register byte s holds subspace (s + rl) & 31
+        const int rot = rl & 31;
+        uint32_t Lr[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v |= (uint32_t)(((4 * w + j + rot) & 31) * 4) << (8 * j);
+            Lr[w] = v;
+        }
+        // B-tile STS offsets (SWIZZLE_128B K-major: 16-B chunk c of row r at c ^ (r & 7)):
+        // step st writes subspace (st + rot) & 31, i.e. k = 2*sub -> chunk sub>>2, word sub&3
+        uint32_t xo[32];
+#pragma unroll
+        for (int st = 0; st < 32; ++st) {
+            const int sub = (st + rot) & 31;
+            xo[st] = (uint32_t)rl * 128u + ((uint32_t)(((sub >> 2) ^ (rl & 7)) << 4) | ((uint32_t)(sub & 3) << 2));
+        }
+        const uint32_t cb_u = dev::smem_u32(sC);
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % TC_STAGES;
+            const uint32_t ph = (i / TC_STAGES) & 1;
+            dev::mbar_wait(full_bar(s), ph);
+            const uint32_t ia = dev::smem_u32(sI + s * IDX_BYTES) + (uint32_t)rl * 32u;
+            const uint4 v0 = dev::lds128(ia), v1 = dev::lds128(ia + 16);
+            const uint32_t iw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+            const uint32_t cbs = cb_u + 128u * s;
+            const uint32_t bst = dev::smem_u32(sB + s * B_BYTES);
+#pragma unroll
+            for (int st = 0; st < 32; ++st) {
+                const int j = st & 3;
+                // byte0 = 4*sub, byte1 = k, bytes 2,3 = 0  ->  k*256 + 4*sub
+                const uint32_t sel = (uint32_t)(4 + j) | ((uint32_t)j << 4) | ((uint32_t)(12 + j) << 8) |
+                                     ((uint32_t)(12 + j) << 12);
+                const uint32_t a = dev::prmt(iw[st >> 2], Lr[st >> 2], sel);
+                const uint32_t c = dev::lds32(cbs + a);
+                asm volatile("st.shared.u32 [%0], %1;" :: "r"(bst + xo[st]), "r"(c) : "memory");
+            }
+            dev::fence_proxy_async();      // generic-proxy STS -> visible to tcgen05 (async proxy)
+            __syncwarp();
+            if (lane == 0) dev::mbar_arrive(bfull_bar(s));
+        }
+        // ------------------------------ epilogue -------------------------------
+        if (ew < 4) {
+            dev::mbar_wait(accum_bar, 0);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int q = warp & 3;                    // TMEM lane quarter this warp may access
+            const int m = m0 + q * 32 + lane;          // token
+#pragma unroll 1
+            for (int c0 = 0; c0 < TC_N; c0 += 32) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+                    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                      "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+                      "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+                      "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+                      "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const int n = n0 + c0;
+                if (m < p.M && n < p.F_out) {
+                    const bool full = n + 32 <= p.F_out;
+                    if (p.y_f32) {
+                        float* yr = reinterpret_cast<float*>(p.Y) + (size_t)m * p.F_out + n;
+                        if (full && (p.F_out % 4 == 0)) {
+#pragma unroll
+                            for (int v = 0; v < 8; ++v)
+                                reinterpret_cast<float4*>(yr)[v] =
+                                    make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                                __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+                        } else {
+#pragma unroll
+                            for (int v = 0; v < 32; ++v)
+                                if (n + v < p.F_out) yr[v] = __uint_as_float(r[v]);
+                        }
+                    } else {
+                        __half* yr = reinterpret_cast<__half*>(p.Y) + (size_t)m * p.F_out + n;
+                        if (full && (p.F_out % 8 == 0)) {
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                uint4 o;
+                                __half2 h0 = __floats2half2_rn(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
+                                __half2 h1 = __floats2half2_rn(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
+                                __half2 h2 = __floats2half2_rn(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
+                                __half2 h3 = __floats2half2_rn(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
+                                o.x = *reinterpret_cast<uint32_t*>(&h0);
+                                o.y = *reinterpret_cast<uint32_t*>(&h1);
+                                o.z = *reinterpret_cast<uint32_t*>(&h2);
+                                o.w = *reinterpret_cast<uint32_t*>(&h3);
+                                reinterpret_cast<uint4*>(yr)[v] = o;
+                            }
+                        } else {
+#pragma unroll
+                            for (int v = 0; v < 32; ++v)
+                                if (n + v < p.F_out) yr[v] = __float2half_rn(__uint_as_float(r[v]));
+                        }
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(256));
+    }
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+        cudaGetLastError();
+    });
+    return fn;
+}
+
+size_t tc_smem_bytes(int C) {
+    return 1024 + (size_t)TC_STAGES * (TC_M * TC_K * 2 + TC_N * TC_K * 2 + TC_N * 32 + (size_t)C * 128) + 8 * 16 + 16;
+}
+
+}  // namespace
+
+bool gemm_tc_supported(const fasq_layer* L, int64_t M) {
+    return L->d == 2 && L->C <= 256 && (L->F_in % 64) == 0 && M >= 1 && M < (1ll << 31) &&
+           tc_smem_bytes(L->C) <= 227 * 1024 && get_encode() != nullptr;
+}
+
+fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void* Y, fasq_dtype yt, cudaStream_t st) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return FASQ_E_CUDA; }
+    if ((reinterpret_cast<uintptr_t>(X) & 15) != 0) return FASQ_E_ARG;
+    CUtensorMap map;
+    cuuint64_t gdim[2] = {(cuuint64_t)L->F_in, (cuuint64_t)M};
+    cuuint64_t gstride[1] = {(cuuint64_t)L->F_in * 2};
+    cuuint32_t box[2] = {TC_K, TC_M};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(X), gdim, gstride, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed"); return FASQ_E_CUDA; }
+    TcParams p{};
+    p.idx = L->idx;
+    p.cbimg = L->cbimg;
+    p.Y = Y;
+    p.M = (int)M;
+    p.F_out = (int)L->F_out;
+    p.F_out_pad = L->F_out_pad;
+    p.n_groups = L->n_groups;
+    p.C = L->C;
+    p.y_f32 = yt == FASQ_F32;
+    const size_t smem = tc_smem_bytes(L->C);
+    static std::once_flag once;
+    std::call_once(once, [] { cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); });
+    // F_out_pad rows of the idx table exist; tiles past F_out_pad read beyond it
+    // -> require the row tile grid to stay within F_out_pad (pad logic below).
+    dim3 grid((unsigned)((L->F_out_pad + TC_N - 1) / TC_N), (unsigned)((M + TC_M - 1) / TC_M));
+    k_gemm_tc<<<grid, TC_THREADS, smem, st>>>(map, p);
+    FASQ_CUDA_TRY(cudaGetLastError());
+    set_launch_count(1);
+    return FASQ_OK;
+}
+
 }  // namespace fasq

@@ -60,6 +60,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     constexpr int E = D <= 2 ? 4 : 2 * D;
     constexpr int R = 32 * NW * RPL;          // rows per CTA tile
     constexpr int XG = 64 * NB * E;           // x bytes per staged group
+    constexpr int CBS = (E == 16) ? 1 : 2;    // codebook slots (d=8, C=256: 128 KiB each)
     extern __shared__ __align__(1024) uint8_t smem[];
 
     const int C = p.C;
@@ -70,8 +71,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     const int r0 = rt * R;
     const int rows_valid = min(R, p.F_out_pad - r0);   // multiple of 32
 
-    uint8_t* s_cb = smem;                                     // 2*C*32*E
-    uint8_t* s_x = s_cb + 2 * C * 32 * E;                     // gmax*XG
+    uint8_t* s_cb = smem;                                     // CBS*C*32*E
+    uint8_t* s_x = s_cb + CBS * C * 32 * E;                   // gmax*XG
     uint8_t* s_idx = s_x + p.gmax * XG;                       // 2*R*32
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_idx + 2 * R * 32);  // full[2], empty[2]
     const uint32_t cb_u = dev::smem_u32(s_cb);
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
             const int slot = i & 1;
             const uint32_t full = full0 + 8 * slot, empty = empty0 + 8 * slot;
             if (i >= 2) dev::mbar_wait(empty, ((i >> 1) + 1) & 1);
+            if (CBS == 1 && i >= 1) dev::mbar_wait(empty0 + 8 * ((i - 1) & 1), ((i - 1) >> 1) & 1);
             const int g = g_begin + i;
             if (lane == 0) dev::mbar_arrive_expect_tx(full, idx_chunk + cb_bytes);
             __syncwarp();
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
                 for (int k = lane; k < C; k += 32)
                     dev::bulk_g2s(cb_u + (uint32_t)k * 256u + 128u * slot, cbsrc + (size_t)k * 128, 128u, full);
             } else if (lane == 0) {
-                dev::bulk_g2s(cb_u + CbGeom<E>::slot_off(slot, C), cbsrc, cb_bytes, full);
+                dev::bulk_g2s(cb_u + (CBS == 1 ? 0u : CbGeom<E>::slot_off(slot, C)), cbsrc, cb_bytes, full);
             }
             if (lane == 0)
                 dev::bulk_g2s(idx_u + (uint32_t)slot * R * 32u,
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
                 for (int w = 0; w < 8; ++w) iw[q][w] = 0u;
             }
         }
-        const uint32_t cbs = cb_u + CbGeom<E>::slot_off(slot, C);
+        const uint32_t cbs = cb_u + (CBS == 1 ? 0u : CbGeom<E>::slot_off(slot, C));
         const uint32_t xb = x_u + (uint32_t)i * XG + (uint32_t)rot * (NB * E);
 #pragma unroll
         for (int s = 0; s < 32; ++s) {
@@ -271,14 +273,25 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
 }
 
 // Fixed-order split-K merge: y[b][r] = sum_{ks ascending} partial[ks][b][r].
+// Loads are issued 8 at a time (independent) and summed in order.
 __global__ void k_splitk_reduce(const float* __restrict__ partial, void* y, int ksplit, int B, int F_out,
                                 int F_out_pad, int y_f32) {
     dev::pdl_wait();
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (int64_t)B * F_out) return;
     int b = (int)(t / F_out), r = (int)(t % F_out);
+    const size_t stride = (size_t)B * F_out_pad;
+    const float* src = partial + (size_t)b * F_out_pad + r;
     float s = 0.f;
-    for (int k = 0; k < ksplit; ++k) s += partial[((size_t)k * B + b) * F_out_pad + r];
+    int k = 0;
+    for (; k + 8 <= ksplit; k += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(k + u) * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; k < ksplit; ++k) s += __ldcg(src + (size_t)k * stride);
     if (y_f32) reinterpret_cast<float*>(y)[t] = s;
     else reinterpret_cast<__half*>(y)[t] = __float2half_rn(s);
 }
@@ -363,7 +376,8 @@ static GemvPlan plan_gemv(const fasq_layer* L, int NB) {
     while ((L->n_groups + ks - 1) / ks > gcap && ks < L->n_groups) ++ks;
     pl.ksplit = ks;
     pl.gmax = (L->n_groups + ks - 1) / ks;
-    pl.smem = (size_t)2 * L->C * 32 * E + (size_t)pl.gmax * xg + (size_t)2 * pl.R * 32 + 64;
+    const int cbs = E == 16 ? 1 : 2;
+    pl.smem = (size_t)cbs * L->C * 32 * E + (size_t)pl.gmax * xg + (size_t)2 * pl.R * 32 + 64;
     return pl;
 }
 

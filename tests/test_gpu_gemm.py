@@ -1,0 +1,87 @@
+"""GPU parity of the prefill GEMM (C-ABI fasq_gemm, LUT and EXPAND_TC
+variants) against the fp64 oracle (reconstruct-then-multiply)."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from fasq_testutil import parity_ok
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def F():
+    import paper_2605_04084_b200 as F
+    return F
+
+
+def _run(F, cb, idx, X, F_in, group, algo, out_dtype=torch.float32):
+    L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), F_in, group)
+    Y = F.gemm(L, torch.from_numpy(X).cuda(), out_dtype=out_dtype, algo=algo)
+    torch.cuda.synchronize()
+    return Y.float().cpu().numpy().astype(np.float64)
+
+
+CASES = [
+    # F_out, F_in, C, M
+    (256, 64, 256, 128),      # one tile
+    (512, 256, 256, 300),     # ragged M (3 token tiles)
+    (1000, 640, 128, 200),    # ragged rows (F_out_pad 1024 -> partial last tile)
+    (300, 128, 7, 33),        # odd C, rows not a multiple of 32
+    (2048, 1024, 256, 512),
+]
+
+
+@pytest.mark.parametrize("algo", ["tc", "lut"])
+@pytest.mark.parametrize("F_out,F_in,C,M", CASES)
+def test_gemm_small(F, oracle_lib, algo, F_out, F_in, C, M):
+    cb, idx = synth.random_layer(F_out, F_in, 2, C, seed=F_out + M)
+    X = synth.activation(M, F_in, seed=M)
+    a = F.GEMM_EXPAND_TC if algo == "tc" else F.GEMM_LUT
+    Y = _run(F, cb, idx, X, F_in, 1, a)
+    ref = oracle_lib.gemm(cb, idx, X)
+    ok, info = parity_ok(Y, ref, X, F_in)
+    assert ok, info
+
+
+def test_gemm_rows_match_gemv(F):
+    cb, idx = synth.random_layer(1024, 512, 2, 256, seed=1)
+    X = synth.activation(130, 512, seed=2)
+    L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), 512, 1)
+    Y = F.gemm(L, torch.from_numpy(X).cuda(), algo=F.GEMM_EXPAND_TC)
+    y = F.gemv(L, torch.from_numpy(X[129:130]).cuda())
+    torch.cuda.synchronize()
+    assert np.allclose(Y[129].cpu().numpy(), y[0].cpu().numpy(), rtol=1e-5, atol=1e-5)
+
+
+def test_gemm_fp16_out(F, oracle_lib):
+    cb, idx = synth.random_layer(512, 256, 2, 256, seed=3)
+    X = synth.activation(256, 256, seed=4)
+    for algo in (F.GEMM_EXPAND_TC, F.GEMM_LUT):
+        Y = _run(F, cb, idx, X, 256, 1, algo, out_dtype=torch.float16)
+        ok, info = parity_ok(Y, oracle_lib.gemm(cb, idx, X), X, 256)
+        assert ok, (algo, info)
+
+
+def test_gemm_saturated_exact_w(F, oracle_lib):
+    """Saturated codebook: W_hat == W, so Y == X . W^T (numpy fp64 matmul)."""
+    W = synth.structured_weight(512, 256, 2, 9, group=1, seed=5)
+    cb, idx, _ = oracle_lib.pack(W, d=2, C=16, group=1, seed=0)
+    X = synth.activation(128, 256, seed=6)
+    Y = _run(F, cb, idx, X, 256, 1, F.GEMM_EXPAND_TC)
+    ref = X.astype(np.float64) @ W.astype(np.float64).T
+    ok, info = parity_ok(Y, ref, X, 256)
+    assert ok, info
+
+
+@pytest.mark.parametrize("F_out,F_in", [(4096, 4096), (14336, 4096), (4096, 14336), (1024, 4096)])
+def test_gemm_llama_sampled(F, oracle_lib, F_out, F_in):
+    """Full Llama shapes at M=512 (bench configuration), sampled rows/tokens."""
+    cb, idx = synth.random_layer(F_out, F_in, 2, 256, seed=F_out + F_in)
+    X = synth.activation(512, F_in, seed=3)
+    Y = _run(F, cb, idx, X, F_in, 1, F.GEMM_EXPAND_TC)
+    for j0 in (0, F_out - 64):
+        ref = oracle_lib.gemm(cb, idx, X[::37], rows=(j0, j0 + 64))
+        ok, info = parity_ok(Y[::37, j0:j0 + 64], ref, X[::37], F_in)
+        assert ok, (j0, info)

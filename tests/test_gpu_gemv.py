@@ -8,7 +8,7 @@ import pytest
 import torch
 
 import synth
-from tests.util import parity_ok
+from fasq_testutil import parity_ok
 
 pytestmark = pytest.mark.gpu
 

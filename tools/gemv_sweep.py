@@ -17,7 +17,7 @@ import synth
 from oracle import sizemodel as sm
 
 
-def run(F_out, F_in, d, C, B, iters=50, flags=0, min_bytes=600e6):
+def run(F_out, F_in, d, C, B, iters=200, flags=0, min_bytes=600e6):
     lb = sm.gemv_algorithmic_bytes(F_out, F_in, d, C, 1, B, 4)
     nrep = max(2, int(min_bytes // lb) + 1)
     layers = []
@@ -30,12 +30,21 @@ def run(F_out, F_in, d, C, B, iters=50, flags=0, min_bytes=600e6):
     for i in range(2 * nrep):
         F.gemv(layers[i % nrep], x, out=ys[i % nrep], flags=flags)
     torch.cuda.synchronize()
-    st = torch.cuda.current_stream()
+    # capture `iters` launches in a CUDA graph so host overhead is excluded
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for i in range(iters):
+                F.gemv(layers[i % nrep], x, out=ys[i % nrep], flags=flags)
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for i in range(iters):
-        F.gemv(layers[i % nrep], x, out=ys[i % nrep], flags=flags)
-    e1.record(st)
+    e0.record()
+    g.replay()
+    e1.record()
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / iters
     return {"F_out": F_out, "F_in": F_in, "d": d, "C": C, "B": B, "us": round(us, 3),
