@@ -1,0 +1,444 @@
+"""FASQ B200 benchmark (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fasq|reference]
+
+Workload (BASELINE.json configs[1], the metric's headline configuration):
+one Llama-3-8B-shaped decode step through all 32 blocks x 7 product-quantized
+linear layers (q, k, v, o, gate, up, down) at the paper's effective 4-bit
+setting (d=2, C=256, uint8 indices, fp16 codebooks), batch 1.  Each GEMV's
+fp16 output feeds the next (q -> o, gate -> down, down -> next block), so the
+224 launches are a real dependency chain; weights are random-init with the
+paper's layer shapes (synthetic, data="synthetic"), 4.1 GB of PQ weights per
+step -- far larger than the 126 MB L2, so every step streams from HBM.
+
+At N > 1 GPUs every layer is row-sharded (F_out/N rows per rank, all
+codebooks replicated) and each of the 4 chain outputs per block
+(q, o, gate, down) is all-gathered over NCCL before it is consumed.
+
+value  = decode tokens/s of the PQ linear stack (1 token = 1 step), device
+         time via CUDA events around K graph replays, max over ranks.
+e2e    = the same step through the public API with HOST buffers: H2D of the
+         token's fp16 hidden state from pinned memory + the 224 GEMVs + D2H
+         of the last layer's output, inside the timed region.
+roofline: dominant kernel = the decode GEMV (k_gemv + its split-K merge),
+         algorithmic bytes = indices + codebooks + x + y of the 224 layers.
+cpu_baseline: the C oracle (fp64 reconstruct-then-multiply) timed on a
+         bounded row sample of each layer shape on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "Llama-3-8B PQ decode tok/s + GEMV HBM GB/s vs 8 TB/s; prefill GEMM TFLOP/s"
+D, C = 2, 256
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------
+# model
+# ----------------------------------------------------------------------------
+def build_model(rank: int, world: int, seed: int = 0):
+    """Row-sharded PQ layers of every block (random-init, paper shapes)."""
+    import torch
+
+    import paper_2605_04084_b200 as F
+    import synth
+
+    blocks = []
+    for b in range(synth.LLAMA3_8B_BLOCKS):
+        layers = {}
+        for li, (name, fo, fi) in enumerate(synth.LLAMA3_8B_LAYERS):
+            rows = fo // world
+            # draw the full layer deterministically, keep this rank's rows
+            cb, idx = synth.torch_random_layer(fo, fi, D, C, seed=seed * 1000 + b * 7 + li)
+            if world > 1:
+                idx = idx[:, rank * rows:(rank + 1) * rows].contiguous()
+            layers[name] = F.import_layer(cb, idx, fi)
+            del cb, idx
+        blocks.append(layers)
+    torch.cuda.synchronize()
+    return blocks
+
+
+def layer_bytes(world: int):
+    """Algorithmic bytes a decode step must move per rank:
+    uint8 indices N_ss*F_out + fp16 codebooks N_ss*C*d*2 + x (2*F_in) +
+    y (2*F_out), summed over the 224 layers."""
+    import synth
+    tot = 0
+    for (_, fo, fi) in synth.LLAMA3_8B_LAYERS:
+        n_ss = fi // D
+        tot += n_ss * (fo // world) + n_ss * C * D * 2 + 2 * fi + 2 * (fo // world)
+    return tot * synth.LLAMA3_8B_BLOCKS
+
+
+class DecodeStep:
+    """One decode step = 224 chained PQ GEMVs (+ all-gathers when sharded)."""
+
+    def __init__(self, blocks, rank, world, pg=None):
+        import torch
+        self.blocks, self.rank, self.world, self.pg = blocks, rank, world, pg
+        dev = torch.device("cuda", torch.cuda.current_device())
+        f16 = torch.float16
+        self.h = torch.zeros((1, 4096), dtype=f16, device=dev)
+        self.bufs = {}
+        for (name, fo, fi) in __import__("synth").LLAMA3_8B_LAYERS:
+            self.bufs[name] = torch.empty((1, fo // world), dtype=f16, device=dev)
+            self.bufs[name + "_full"] = torch.empty((1, fo), dtype=f16, device=dev)
+        self.launches = 0
+
+    def _gather(self, name):
+        import torch.distributed as dist
+        if self.world == 1:
+            return self.bufs[name]
+        out = self.bufs[name + "_full"]
+        dist.all_gather_into_tensor(out.view(-1), self.bufs[name].view(-1), group=self.pg)
+        return out
+
+    def run(self, flags=0):
+        import paper_2605_04084_b200 as F
+        n = 0
+        h = self.h
+        for layers in self.blocks:
+            for name in ("q_proj", "k_proj", "v_proj"):
+                F.gemv(layers[name], h, out=self.bufs[name], flags=flags)
+                n += F.last_launch_count()
+            q = self._gather("q_proj")
+            F.gemv(layers["o_proj"], q, out=self.bufs["o_proj"], flags=flags)
+            n += F.last_launch_count()
+            o = self._gather("o_proj")
+            for name in ("gate_proj", "up_proj"):
+                F.gemv(layers[name], o, out=self.bufs[name], flags=flags)
+                n += F.last_launch_count()
+            g = self._gather("gate_proj")
+            F.gemv(layers["down_proj"], g, out=self.bufs["down_proj"], flags=flags)
+            n += F.last_launch_count()
+            h = self._gather("down_proj")
+        self.out = h
+        self.launches = n
+        return h
+
+
+def capture(fn):
+    import torch
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()           # warm allocator / plans outside capture
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        fn()
+    torch.cuda.synchronize()
+    return g
+
+
+def timed(graph, steps, warmup, rank, world, pg=None):
+    import torch
+    import torch.distributed as dist
+    for _ in range(warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        graph.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms / steps
+
+
+# ----------------------------------------------------------------------------
+# CPU oracle baseline (bounded sample)
+# ----------------------------------------------------------------------------
+def oracle_decode_rate(budget_s: float = 15.0):
+    """Oracle fp64 reconstruct-then-multiply GEMV on a row sample of each
+    Llama layer shape, extrapolated to a full decode step.  Returns
+    (tok/s, threads, sample description, seconds spent)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    lib_threads = oracle.num_threads()
+    t_start = time.perf_counter()
+    per_row = {}
+    shapes = sorted({(fo, fi) for (_, fo, fi) in synth.LLAMA3_8B_LAYERS})
+    sample_rows = 1024
+    for (fo, fi) in shapes:
+        cb, idx = synth.random_layer(fo, fi, D, C, seed=7)
+        x = synth.activation(1, fi, seed=1)
+        rows = min(sample_rows, fo)
+        oracle.gemv(cb, idx, x, rows=(0, 64))               # warm
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            oracle.gemv(cb, idx, x, rows=(0, rows))
+            reps += 1
+            if time.perf_counter() - t0 > budget_s / (2 * len(shapes)) or reps >= 50:
+                break
+        per_row[(fo, fi)] = (time.perf_counter() - t0) / (reps * rows)
+    step_s = synth.LLAMA3_8B_BLOCKS * sum(per_row[(fo, fi)] * fo for (_, fo, fi) in synth.LLAMA3_8B_LAYERS)
+    spent = time.perf_counter() - t_start
+    sample = ("oracle fp64 GEMV (reconstruct-then-multiply) on the first %d rows of each Llama-3-8B "
+              "layer shape, repeated for ~%.0f s, extrapolated to 224 layers" % (sample_rows, budget_s))
+    return 1.0 / step_s, lib_threads, sample, spent
+
+
+# ----------------------------------------------------------------------------
+# side measurements (not part of the timed region)
+# ----------------------------------------------------------------------------
+def prefill_tflops(M=2048, iters=10):
+    import torch
+
+    import paper_2605_04084_b200 as F
+    import synth
+    out = {}
+    for (fo, fi) in [(4096, 4096), (14336, 4096), (4096, 14336)]:
+        cb, idx = synth.torch_random_layer(fo, fi, D, C, seed=3)
+        L = F.import_layer(cb, idx, fi)
+        X = synth.torch_activation(M, fi)
+        Y = torch.empty((M, fo), dtype=torch.float16, device="cuda")
+        res = {}
+        for name, algo in (("expand_tc", F.GEMM_EXPAND_TC), ("lut", F.GEMM_LUT)):
+            try:
+                n_it = iters if algo == F.GEMM_EXPAND_TC else 2
+                F.gemm(L, X, out=Y, algo=algo)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(n_it):
+                    F.gemm(L, X, out=Y, algo=algo)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / n_it
+                res[name] = {"ms": round(ms, 4), "tflops": round(2.0 * M * fo * fi / ms / 1e9, 2)}
+            except Exception as e:  # report, never hide
+                res[name] = {"error": str(e)[:200]}
+        out["%dx%d" % (fo, fi)] = res
+        L.free()
+    return out
+
+
+def pack_time():
+    import torch
+
+    import paper_2605_04084_b200 as F
+    import synth
+    W = synth.torch_activation(4096, 4096, seed=5, std=0.02)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    L = F.pack(W, d=D, C=C, group=1, seed=0, iters=25)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    L.free()
+    return {"layer": "4096x4096", "d": D, "C": C, "iters": 25, "seconds": round(dt, 3)}
+
+
+# ----------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    """--impl reference: the oracle on the host cores (bounded sample)."""
+    if rank != 0:
+        return
+    rates = []
+    spent_total = 0.0
+    threads = None
+    sample = None
+    for _ in range(args.warmup):
+        oracle_decode_rate(budget_s=3.0)
+    for _ in range(args.steps):
+        r, threads, sample, spent = oracle_decode_rate(budget_s=max(3.0, 60.0 / max(args.steps, 1)))
+        rates.append(r)
+        spent_total += spent
+    v = statistics.median(rates)
+    line = {"metric": METRIC, "value": v, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "llama3-8b-pq-decode-d2-C256-b1 (oracle, sampled rows)",
+                       "global_batch": 1, "seq_len": 1, "parallelism": "host-cores"},
+            "cpu_baseline": {"value": v, "unit": "tok/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="fasq", choices=["fasq", "reference"])
+    ap.add_argument("--no-side", action="store_true", help="skip prefill/pack/cpu side measurements")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist.group.WORLD
+
+    import paper_2605_04084_b200 as F
+
+    blocks = build_model(rank, world)
+    step = DecodeStep(blocks, rank, world, pg)
+    step.h.copy_(__import__("synth").torch_activation(1, 4096, seed=11))
+
+    # ---- device-resident timed region (graph of the whole step) ----
+    g = capture(lambda: step.run(flags=F.FLAG_PDL))
+    launches_per_step = step.launches
+    peaks, peak_src = _peaks()
+    with ClockSampler(local) as clk:
+        ms = timed(g, args.steps, args.warmup, rank, world, pg)
+    clocks = clk.summary()
+
+    # ---- e2e through the public API with host buffers ----
+    xh = torch.empty((1, 4096), dtype=torch.float16).pin_memory()
+    xh.copy_(step.h.cpu())
+    yh = torch.empty((1, 4096), dtype=torch.float16).pin_memory()
+
+    def e2e_fn():
+        step.h.copy_(xh, non_blocking=True)
+        out = step.run(flags=F.FLAG_PDL)
+        yh.copy_(out, non_blocking=True)
+
+    ge = capture(e2e_fn)
+    ms_e2e = timed(ge, args.steps, args.warmup, rank, world, pg)
+
+    tok_s = 1000.0 / ms
+    gbytes = layer_bytes(world)
+    achieved = gbytes / (ms * 1e-3) / 1e9
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+
+    side = {}
+    if rank == 0 and not args.no_side:
+        try:
+            side["prefill_gemm_M2048"] = prefill_tflops()
+        except Exception as e:
+            side["prefill_gemm_M2048"] = {"error": str(e)[:200]}
+        try:
+            side["gpu_pack"] = pack_time()
+        except Exception as e:
+            side["gpu_pack"] = {"error": str(e)[:200]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_side:
+        r, thr, sample, _ = oracle_decode_rate(budget_s=15.0)
+        cpu = {"value": r, "unit": "tok/s", "cores": thr, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": tok_s, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+            "config": {"workload": "llama3-8b-pq-decode-d2-C256-b1: 32 blocks x {q,k,v,o,gate,up,down} "
+                                   "PQ GEMVs, chained fp16 activations (attention/norm/lm_head excluded)",
+                       "global_batch": 1, "seq_len": 1,
+                       "parallelism": "row-shard-tp%d+nccl-allgather" % world if world > 1 else "single-gpu",
+                       "d": D, "C": C, "weights_bytes_per_step": gbytes,
+                       "l2": "inputs larger than L2 (%.2f GB of PQ weights per step vs 126 MB L2)" % (gbytes / 1e9),
+                       "timing": "CUDA graph of one step, K replays between CUDA events, max over ranks"},
+            "e2e": {"value": 1000.0 / ms_e2e, "unit": "tok/s", "h2d_bytes_per_step": 4096 * 2,
+                    "d2h_bytes_per_step": 4096 * 2},
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "k_gemv + k_splitk_reduce (decode GEMV op), algorithmic bytes of all "
+                                   "224 layers / step time; peak = %s hbm_gbs" % peak_src},
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+            "side": side,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -37,6 +37,8 @@ static void destroy(fasq_layer* L) {
     if (L->idx) cudaFree(L->idx);
     if (L->cbimg) cudaFree(L->cbimg);
     if (L->cb) cudaFree(L->cb);
+    if (L->ws) cudaFree(L->ws);
+    if (L->tickets) cudaFree(L->tickets);
     delete L;
 }
 

@@ -42,6 +42,12 @@ struct fasq_layer {
     uint8_t* cbimg = nullptr;  // GEMV codebook image
     __half* cb = nullptr;      // logical codebooks
     int64_t idx_bytes = 0, cbimg_bytes = 0, cb_bytes = 0;
+    // GEMV split-K workspace (partials + per-row-tile arrival tickets), grown
+    // lazily outside stream capture; see gemv.cu.
+    float* ws = nullptr;
+    int64_t ws_bytes = 0;
+    unsigned* tickets = nullptr;
+    int32_t n_tickets = 0;
 };
 
 namespace fasq {
@@ -59,6 +65,24 @@ void add_launch_count(int n);
     } while (0)
 
 inline int entry_bytes(int d) { return d <= 2 ? 4 : d * 2; }
+
+// Opt a kernel into the largest dynamic SMEM the device allows next to its
+// static SMEM; returns that byte count (0 on failure).
+template <class K>
+inline size_t set_max_dyn_smem(K kern) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) { cudaGetLastError(); return 0; }
+    const size_t lim = (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return lim;
+}
+constexpr size_t kSmemBudget = 227 * 1024 - 2048;   // dynamic-SMEM planning budget (static SMEM headroom)
 
 // ---- layout kernels (layout.cu) ---------------------------------------------
 fasq_status alloc_layer_storage(fasq_layer* L);

@@ -129,7 +129,7 @@ fasq_status gemm_lut_launch(const fasq_layer* L, const __half* X, int64_t M, voi
     const size_t smem = (size_t)(LUT_MT / 2) * L->C * 256;
     static bool attr = false;
     if (!attr) {
-        FASQ_CUDA_TRY(cudaFuncSetAttribute(k_gemm_lut, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        if (set_max_dyn_smem(k_gemm_lut) < smem) { set_error("gemm_lut: SMEM"); return FASQ_E_UNSUPPORTED; }
         attr = true;
     }
     dim3 grid((unsigned)((L->F_out_pad + LUT_R - 1) / LUT_R), (unsigned)((M + LUT_MT - 1) / LUT_MT));

@@ -189,7 +189,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
             const uint32_t ph = (i / TC_STAGES) & 1;
             dev::mbar_wait(full_bar(s), ph);
             const uint32_t ia = dev::smem_u32(sI + s * IDX_BYTES) + (uint32_t)rl * 32u;
-            const uint4 v0 = dev::lds128(ia), v1 = dev::lds128(ia + 16);
+            uint4 v0 = dev::lds128(ia), v1 = dev::lds128(ia + 16);
+            if (n0 + rl >= p.F_out_pad) { v0 = make_uint4(0, 0, 0, 0); v1 = v0; }   // rows not loaded
             const uint32_t iw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
             const uint32_t cbs = cb_u + 128u * s;
             const uint32_t bst = dev::smem_u32(sB + s * B_BYTES);
@@ -304,7 +305,7 @@ size_t tc_smem_bytes(int C) {
 
 bool gemm_tc_supported(const fasq_layer* L, int64_t M) {
     return L->d == 2 && L->C <= 256 && (L->F_in % 64) == 0 && M >= 1 && M < (1ll << 31) &&
-           tc_smem_bytes(L->C) <= 227 * 1024 && get_encode() != nullptr;
+           tc_smem_bytes(L->C) <= kSmemBudget && get_encode() != nullptr;
 }
 
 fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void* Y, fasq_dtype yt, cudaStream_t st) {
@@ -332,7 +333,9 @@ fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void
     p.y_f32 = yt == FASQ_F32;
     const size_t smem = tc_smem_bytes(L->C);
     static std::once_flag once;
-    std::call_once(once, [] { cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); });
+    static size_t lim = 0;
+    std::call_once(once, [] { lim = set_max_dyn_smem(k_gemm_tc); });
+    if (lim < smem) { set_error("gemm_tc: SMEM"); return FASQ_E_UNSUPPORTED; }
     // F_out_pad rows of the idx table exist; tiles past F_out_pad read beyond it
     // -> require the row tile grid to stay within F_out_pad (pad logic below).
     dim3 grid((unsigned)((L->F_out_pad + TC_N - 1) / TC_N), (unsigned)((M + TC_M - 1) / TC_M));

@@ -22,10 +22,13 @@
 //    group's codebook image into a 2-stage SMEM ring with the TMA bulk-copy
 //    engine (cp.async.bulk + mbarrier complete_tx); consumers never issue
 //    global loads in the hot loop;
-//  * split-K over subspace groups (grid.y) is merged deterministically:
-//    partial sums [ks][B][F_out] then a fixed-order reduce kernel (the
+//  * split-K over subspace groups (grid.y) is merged deterministically in
+//    the same kernel: every CTA publishes its partial sums, the last CTA of
+//    a row tile to arrive (atomic ticket) adds them in fixed ks order (the
 //    paper's atomicAdd merge, is order-nondeterministic).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "fasq_internal.cuh"
@@ -38,32 +41,28 @@ struct GemvParams {
     const __half* x;        // [B][F_in]
     void* y;                // [B][F_out]
     float* partial;         // [ksplit][B][F_out_pad] (ksplit > 1)
+    unsigned* tickets;      // [row_tiles] arrival counters (self-resetting)
     int F_in, F_out, F_out_pad, N_ss, n_groups, C, B;
     int ksplit, y_f32;
     int gmax;               // max groups per CTA (x staging capacity)
 };
 
-template <int E>
-struct CbGeom {  // SMEM codebook ring geometry (2 slots)
-    // E == 4: row k = [slot0: 32 x 4 B][slot1: 32 x 4 B] (256 B), so the
-    // prmt-built address k*256 + 4*sub needs only an immediate slot offset.
-    static __device__ __forceinline__ uint32_t row_bytes() { return E == 4 ? 256u : 32u * E; }
-    static __device__ __forceinline__ uint32_t slot_off(int slot, int C) {
-        return E == 4 ? 128u * slot : (uint32_t)slot * (uint32_t)C * 32u * E;
-    }
-};
-
 // x staging: per group, 64 entries (subspaces 0..31 twice, so the rotated
 // index (s + rot) needs no wrap) x NB batches x E bytes.
-template <int D, int NB, int RPL, int NW>
+//
+// SMEM layout: cb ring [ST][C][32][E] (one contiguous TMA bulk copy per
+// stage -- the microbenchmark in tools/mb_bulk.cu shows 128-B bulk copies
+// cap at ~0.6 TB/s while >=16 KiB copies reach ~7 TB/s), index ring
+// [ST][R][32], x [gmax][64][NB][E], mbarriers full[ST], empty[ST].
+template <int D, int NB, int RPL, int NW, int ST>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     constexpr int E = D <= 2 ? 4 : 2 * D;
     constexpr int R = 32 * NW * RPL;          // rows per CTA tile
     constexpr int XG = 64 * NB * E;           // x bytes per staged group
-    constexpr int CBS = (E == 16) ? 1 : 2;    // codebook slots (d=8, C=256: 128 KiB each)
     extern __shared__ __align__(1024) uint8_t smem[];
 
     const int C = p.C;
+    const uint32_t CBB = (uint32_t)C * 32u * E;   // codebook image bytes per group
     const int rt = blockIdx.x, ks = blockIdx.y;
     const int g_begin = (int)((int64_t)ks * p.n_groups / p.ksplit);
     const int g_end = (int)((int64_t)(ks + 1) * p.n_groups / p.ksplit);
@@ -71,51 +70,45 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     const int r0 = rt * R;
     const int rows_valid = min(R, p.F_out_pad - r0);   // multiple of 32
 
-    uint8_t* s_cb = smem;                                     // CBS*C*32*E
-    uint8_t* s_x = s_cb + CBS * C * 32 * E;                   // gmax*XG
-    uint8_t* s_idx = s_x + p.gmax * XG;                       // 2*R*32
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_idx + 2 * R * 32);  // full[2], empty[2]
+    uint8_t* s_cb = smem;                                     // ST*CBB
+    uint8_t* s_idx = s_cb + ST * CBB;                         // ST*R*32
+    uint8_t* s_x = s_idx + ST * R * 32;                       // gmax*XG
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_x + p.gmax * XG);   // full[ST], empty[ST]
     const uint32_t cb_u = dev::smem_u32(s_cb);
     const uint32_t x_u = dev::smem_u32(s_x);
     const uint32_t idx_u = dev::smem_u32(s_idx);
     const uint32_t full0 = dev::smem_u32(&bars[0]);
-    const uint32_t empty0 = dev::smem_u32(&bars[2]);
+    const uint32_t empty0 = dev::smem_u32(&bars[ST]);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        dev::mbar_init(full0, 1);
-        dev::mbar_init(full0 + 8, 1);
-        dev::mbar_init(empty0, NW);
-        dev::mbar_init(empty0 + 8, NW);
+#pragma unroll
+        for (int s = 0; s < ST; ++s) {
+            dev::mbar_init(full0 + 8 * s, 1);
+            dev::mbar_init(empty0 + 8 * s, NW);
+        }
         dev::fence_barrier_init();
     }
     __syncthreads();
 
     if (warp == NW) {
         // ------------------------- producer warp -------------------------
-        const uint32_t idx_chunk = (uint32_t)rows_valid * 32u;
-        const uint32_t cb_bytes = (uint32_t)C * 32u * E;
-        for (int i = 0; i < ng; ++i) {
-            const int slot = i & 1;
-            const uint32_t full = full0 + 8 * slot, empty = empty0 + 8 * slot;
-            if (i >= 2) dev::mbar_wait(empty, ((i >> 1) + 1) & 1);
-            if (CBS == 1 && i >= 1) dev::mbar_wait(empty0 + 8 * ((i - 1) & 1), ((i - 1) >> 1) & 1);
-            const int g = g_begin + i;
-            if (lane == 0) dev::mbar_arrive_expect_tx(full, idx_chunk + cb_bytes);
-            __syncwarp();
-            const uint8_t* cbsrc = p.cbimg + (size_t)g * cb_bytes;
-            if (E == 4) {
-                for (int k = lane; k < C; k += 32)
-                    dev::bulk_g2s(cb_u + (uint32_t)k * 256u + 128u * slot, cbsrc + (size_t)k * 128, 128u, full);
-            } else if (lane == 0) {
-                dev::bulk_g2s(cb_u + (CBS == 1 ? 0u : CbGeom<E>::slot_off(slot, C)), cbsrc, cb_bytes, full);
+        if (lane == 0) {
+            const uint32_t idx_chunk = (uint32_t)rows_valid * 32u;
+            for (int i = 0; i < ng; ++i) {
+                const int slot = i % ST;
+                if (i >= ST) dev::mbar_wait(empty0 + 8 * slot, ((i / ST) + 1) & 1);
+                const int g = g_begin + i;
+                const uint32_t full = full0 + 8 * slot;
+                dev::mbar_arrive_expect_tx(full, idx_chunk + CBB);
+                dev::bulk_g2s(cb_u + (uint32_t)slot * CBB, p.cbimg + (size_t)g * CBB, CBB, full);
+                dev::bulk_g2s(idx_u + (uint32_t)slot * R * 32u, p.idx + ((size_t)g * p.F_out_pad + r0) * 32,
+                              idx_chunk, full);
             }
-            if (lane == 0)
-                dev::bulk_g2s(idx_u + (uint32_t)slot * R * 32u,
-                              p.idx + ((size_t)g * p.F_out_pad + r0) * 32, idx_chunk, full);
         }
+        __syncwarp();
         dev::pdl_launch_dependents();
         return;
     }
@@ -146,18 +139,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
 
     const int hA = (lane >> 2) & 1;                 // conflict-free LDS.128 of 32-B rows
     const int rot = (lane + 16 * hA) & 31;          // lane's subspace rotation
-    // lowbyte constants: byte j of L[w] = E' * sub(4w + j) (E' = 4 or 8)
-    constexpr int LB = (E == 4) ? 4 : 8;            // lowbyte multiplier
-    constexpr int PER = (E == 4) ? 4 : 2;           // lowbytes per register
-    constexpr int NL = 32 / PER;
-    uint32_t Lr[NL];
+    // lowbyte constants: L[w] bytes = [8*sub(2w), 8*sub(2w+1), 0, 0];
+    // prmt(idx word, L, sel) = k*256 + 8*sub, then
+    //   E=4 : >>1  -> k*128 + 4*sub      E=8 : as is     E=16: <<1 -> k*512 + 16*sub
+    uint32_t Lr[16];
 #pragma unroll
-    for (int w = 0; w < NL; ++w) {
-        uint32_t v = 0;
-#pragma unroll
-        for (int j = 0; j < PER; ++j) v |= (uint32_t)(((4 * 0 + w * PER + j + rot) & 31) * LB) << (8 * j);
-        Lr[w] = v;
-    }
+    for (int w = 0; w < 16; ++w)
+        Lr[w] = (uint32_t)(((2 * w + rot) & 31) * 8) | ((uint32_t)(((2 * w + 1 + rot) & 31) * 8) << 8);
 
     float acc[RPL][NB];
 #pragma unroll
@@ -167,9 +155,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
 
     const int warp_row0 = warp * 32 * RPL;
     for (int i = 0; i < ng; ++i) {
-        const int slot = i & 1;
-        dev::mbar_wait(full0 + 8 * slot, (i >> 1) & 1);
-        // this lane's index words: [q][8]
+        const int slot = i % ST;
+        dev::mbar_wait(full0 + 8 * slot, (i / ST) & 1);
         uint32_t iw[RPL][8];
 #pragma unroll
         for (int q = 0; q < RPL; ++q) {
@@ -185,11 +172,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
                 for (int w = 0; w < 8; ++w) iw[q][w] = 0u;
             }
         }
-        const uint32_t cbs = cb_u + (CBS == 1 ? 0u : CbGeom<E>::slot_off(slot, C));
+        const uint32_t cbs = cb_u + (uint32_t)slot * CBB;
         const uint32_t xb = x_u + (uint32_t)i * XG + (uint32_t)rot * (NB * E);
 #pragma unroll
         for (int s = 0; s < 32; ++s) {
-            // x entries for this lane's subspace at step s, all batches
             uint32_t xv[NB][E / 4];
 #pragma unroll
             for (int b = 0; b < NB; ++b) {
@@ -205,45 +191,35 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
                     xv[b][2 % (E / 4)] = t4.z; xv[b][3 % (E / 4)] = t4.w;
                 }
             }
-            const int wi = s >> 2, j = s & 3;
+            const int wi = s >> 2, j = s & 3, lw = s >> 1, lj = s & 1;
+            // byte0 = L byte lj (8*sub), byte1 = idx byte j (k), bytes 2,3 = L byte 2 (0)
+            const uint32_t sel = (uint32_t)(4 + lj) | ((uint32_t)j << 4) | (6u << 8) | (6u << 12);
 #pragma unroll
             for (int q = 0; q < RPL; ++q) {
-                uint32_t addr;
+                if (warp_row0 + q * 32 >= rows_valid) continue;
+                uint32_t addr = dev::prmt(iw[q][wi], Lr[lw], sel);
+                if (E == 4) addr >>= 1;
+                if (E == 16) addr <<= 1;
                 if (E == 4) {
-                    // byte0 = 4*sub (L byte j), byte1 = k (idx byte j), bytes2,3 = sign of L byte (0)
-                    const uint32_t sel = (uint32_t)(4 + j) | ((uint32_t)j << 4) | ((uint32_t)(12 + j) << 8) |
-                                         ((uint32_t)(12 + j) << 12);
-                    addr = dev::prmt(iw[q][wi], Lr[wi], sel);
+                    const uint32_t c = dev::lds32(cbs + addr);
+#pragma unroll
+                    for (int b = 0; b < NB; ++b)
+                        acc[q][b] = (D == 1) ? dev::fhfma1(c, xv[b][0], acc[q][b]) : dev::fhfma2(c, xv[b][0], acc[q][b]);
+                } else if (E == 8) {
+                    const uint2 c = dev::lds64(cbs + addr);
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        acc[q][b] = dev::fhfma2(c.x, xv[b][0], acc[q][b]);
+                        acc[q][b] = dev::fhfma2(c.y, xv[b][1 % (E / 4)], acc[q][b]);
+                    }
                 } else {
-                    // L[w] bytes: [8*sub(2w), 8*sub(2w+1), 0, 0]
-                    const int lw = s >> 1, lj = s & 1;
-                    const uint32_t sel = (uint32_t)(4 + lj) | ((uint32_t)j << 4) | (6u << 8) | (6u << 12);
-                    addr = dev::prmt(iw[q][wi], Lr[lw], sel);
-                    if (E == 16) addr <<= 1;    // k*512 + 16*sub
-                }
-                if (warp_row0 + q * 32 < rows_valid) {
-                    if (E == 4) {
-                        const uint32_t c = dev::lds32(cbs + addr);
+                    const uint4 c = dev::lds128(cbs + addr);
 #pragma unroll
-                        for (int b = 0; b < NB; ++b)
-                            acc[q][b] = (D == 1) ? dev::fhfma1(c, xv[b][0], acc[q][b])
-                                                 : dev::fhfma2(c, xv[b][0], acc[q][b]);
-                    } else if (E == 8) {
-                        const uint2 c = dev::lds64(cbs + addr);
-#pragma unroll
-                        for (int b = 0; b < NB; ++b) {
-                            acc[q][b] = dev::fhfma2(c.x, xv[b][0], acc[q][b]);
-                            acc[q][b] = dev::fhfma2(c.y, xv[b][1 % (E / 4)], acc[q][b]);
-                        }
-                    } else {
-                        const uint4 c = dev::lds128(cbs + addr);
-#pragma unroll
-                        for (int b = 0; b < NB; ++b) {
-                            acc[q][b] = dev::fhfma2(c.x, xv[b][0], acc[q][b]);
-                            acc[q][b] = dev::fhfma2(c.y, xv[b][1 % (E / 4)], acc[q][b]);
-                            acc[q][b] = dev::fhfma2(c.z, xv[b][2 % (E / 4)], acc[q][b]);
-                            acc[q][b] = dev::fhfma2(c.w, xv[b][3 % (E / 4)], acc[q][b]);
-                        }
+                    for (int b = 0; b < NB; ++b) {
+                        acc[q][b] = dev::fhfma2(c.x, xv[b][0], acc[q][b]);
+                        acc[q][b] = dev::fhfma2(c.y, xv[b][1 % (E / 4)], acc[q][b]);
+                        acc[q][b] = dev::fhfma2(c.z, xv[b][2 % (E / 4)], acc[q][b]);
+                        acc[q][b] = dev::fhfma2(c.w, xv[b][3 % (E / 4)], acc[q][b]);
                     }
                 }
             }
@@ -253,47 +229,59 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     }
 
     // ------------------------------ epilogue --------------------------------
+    if (p.ksplit == 1) {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+            const int row = r0 + warp_row0 + q * 32 + lane;
+            if (warp_row0 + q * 32 >= rows_valid || row >= p.F_out) continue;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                if (b >= p.B) continue;
+                if (p.y_f32) reinterpret_cast<float*>(p.y)[(size_t)b * p.F_out + row] = acc[q][b];
+                else reinterpret_cast<__half*>(p.y)[(size_t)b * p.F_out + row] = __float2half_rn(acc[q][b]);
+            }
+        }
+        return;
+    }
+    // split-K: publish partials, the LAST CTA of this row tile to arrive sums
+    // them in fixed ks order (deterministic; the paper's merge is atomicAdd,
+    // P:278) -- one kernel, no second launch.
 #pragma unroll
     for (int q = 0; q < RPL; ++q) {
         const int row = r0 + warp_row0 + q * 32 + lane;
         if (warp_row0 + q * 32 >= rows_valid) continue;
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-            if (b >= p.B) continue;
-            if (p.ksplit == 1) {
-                if (row < p.F_out) {
-                    if (p.y_f32) reinterpret_cast<float*>(p.y)[(size_t)b * p.F_out + row] = acc[q][b];
-                    else reinterpret_cast<__half*>(p.y)[(size_t)b * p.F_out + row] = __float2half_rn(acc[q][b]);
-                }
-            } else {
-                p.partial[((size_t)ks * p.B + b) * p.F_out_pad + row] = acc[q][b];
-            }
+        for (int b = 0; b < NB; ++b)
+            if (b < p.B) __stcg(&p.partial[((size_t)ks * p.B + b) * p.F_out_pad + row], acc[q][b]);
+    }
+    __threadfence();
+    __shared__ unsigned s_last;
+    asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
+    if (threadIdx.x == 0) s_last = (atomicAdd(&p.tickets[rt], 1u) == (unsigned)(p.ksplit - 1));
+    asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
+    if (!s_last) return;
+    __threadfence();
+    const int n_out = rows_valid * p.B;
+    const size_t kstride = (size_t)p.B * p.F_out_pad;
+    for (int t = threadIdx.x; t < n_out; t += NW * 32) {
+        const int b = t / rows_valid, row = r0 + t % rows_valid;
+        const float* src = p.partial + (size_t)b * p.F_out_pad + row;
+        float sum = 0.f;
+        int k = 0;
+        for (; k + 8 <= p.ksplit; k += 8) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(k + u) * kstride);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) sum += v[u];
+        }
+        for (; k < p.ksplit; ++k) sum += __ldcg(src + (size_t)k * kstride);
+        if (row < p.F_out) {
+            if (p.y_f32) reinterpret_cast<float*>(p.y)[(size_t)b * p.F_out + row] = sum;
+            else reinterpret_cast<__half*>(p.y)[(size_t)b * p.F_out + row] = __float2half_rn(sum);
         }
     }
-}
-
-// Fixed-order split-K merge: y[b][r] = sum_{ks ascending} partial[ks][b][r].
-// Loads are issued 8 at a time (independent) and summed in order.
-__global__ void k_splitk_reduce(const float* __restrict__ partial, void* y, int ksplit, int B, int F_out,
-                                int F_out_pad, int y_f32) {
-    dev::pdl_wait();
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (int64_t)B * F_out) return;
-    int b = (int)(t / F_out), r = (int)(t % F_out);
-    const size_t stride = (size_t)B * F_out_pad;
-    const float* src = partial + (size_t)b * F_out_pad + r;
-    float s = 0.f;
-    int k = 0;
-    for (; k + 8 <= ksplit; k += 8) {
-        float v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(k + u) * stride);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s += v[u];
-    }
-    for (; k < ksplit; ++k) s += __ldcg(src + (size_t)k * stride);
-    if (y_f32) reinterpret_cast<float*>(y)[t] = s;
-    else reinterpret_cast<__half*>(y)[t] = __float2half_rn(s);
+    if (threadIdx.x == 0) p.tickets[rt] = 0u;     // ready for the next launch (stream order)
 }
 
 // ------------------------------- host side ----------------------------------
@@ -311,20 +299,18 @@ static int num_sms() {
 }
 
 struct GemvPlan {
-    int rpl, nw, R, row_tiles, ksplit, gmax;
+    int rpl, nw, st, R, row_tiles, ksplit, gmax;
     size_t smem;
 };
 
-template <int D, int NB, int RPL, int NW>
+template <int D, int NB, int RPL, int NW, int ST>
 static fasq_status launch_gemv_t(const GemvParams& p0, const GemvPlan& pl, uint32_t flags, cudaStream_t st) {
     constexpr int E = D <= 2 ? 4 : 2 * D;
-    auto kern = k_gemv<D, NB, RPL, NW>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        std::lock_guard<std::mutex> lk(g_mu);
-        FASQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_done = true;
-    }
+    auto kern = k_gemv<D, NB, RPL, NW, ST>;
+    static size_t lim = 0;
+    static std::once_flag once;
+    std::call_once(once, [&] { lim = set_max_dyn_smem(kern); });
+    if (lim < pl.smem) { set_error("gemv: dynamic SMEM plan exceeds the device limit"); return FASQ_E_UNSUPPORTED; }
     (void)E;
     GemvParams p = p0;
     cudaLaunchConfig_t cfg = {};
@@ -343,9 +329,13 @@ static fasq_status launch_gemv_t(const GemvParams& p0, const GemvPlan& pl, uint3
 
 template <int D, int NB>
 static fasq_status dispatch_cfg(const GemvParams& p, const GemvPlan& pl, uint32_t flags, cudaStream_t st) {
-    if (pl.rpl == 4 && pl.nw == 8) return launch_gemv_t<D, NB, 4, 8>(p, pl, flags, st);
-    if (pl.rpl == 2 && pl.nw == 8) return launch_gemv_t<D, NB, 2, 8>(p, pl, flags, st);
-    if (pl.rpl == 1 && pl.nw == 8) return launch_gemv_t<D, NB, 1, 8>(p, pl, flags, st);
+    if (pl.rpl == 2 && pl.nw == 16 && pl.st == 3) return launch_gemv_t<D, NB, 2, 16, 3>(p, pl, flags, st);
+    if (pl.rpl == 2 && pl.nw == 16 && pl.st == 2) return launch_gemv_t<D, NB, 2, 16, 2>(p, pl, flags, st);
+    if (pl.rpl == 1 && pl.nw == 16 && pl.st == 2) return launch_gemv_t<D, NB, 1, 16, 2>(p, pl, flags, st);
+    if (pl.rpl == 1 && pl.nw == 16 && pl.st == 3) return launch_gemv_t<D, NB, 1, 16, 3>(p, pl, flags, st);
+    if (pl.rpl == 1 && pl.nw == 16 && pl.st == 1) return launch_gemv_t<D, NB, 1, 16, 1>(p, pl, flags, st);
+    if (pl.rpl == 2 && pl.nw == 16 && pl.st == 1) return launch_gemv_t<D, NB, 2, 16, 1>(p, pl, flags, st);
+    if (pl.rpl == 1 && pl.nw == 8 && pl.st == 3) return launch_gemv_t<D, NB, 1, 8, 3>(p, pl, flags, st);
     return FASQ_E_UNSUPPORTED;
 }
 
@@ -360,29 +350,48 @@ static fasq_status dispatch_nb(int NB, const GemvParams& p, const GemvPlan& pl, 
     return FASQ_E_UNSUPPORTED;
 }
 
+// Tiling plan: R rows x a K-range of 32-subspace groups
+// per CTA, one CTA per SM; the K-split (grid.y) fills the 148 SMs.  Env
+// FASQ_GEMV_CFG="rpl,nw,stages" overrides the default (tuning only).
 static GemvPlan plan_gemv(const fasq_layer* L, int NB) {
     GemvPlan pl{};
-    pl.nw = 8;
-    pl.rpl = NB <= 2 ? 4 : (NB == 4 ? 2 : 1);
+    pl.nw = 16;
+    pl.rpl = NB <= 2 ? 2 : 1;
+    pl.st = 3;
+    if (const char* e = getenv("FASQ_GEMV_CFG")) {
+        int a = 0, b = 0, c = 0;
+        if (sscanf(e, "%d,%d,%d", &a, &b, &c) == 3) { pl.rpl = a; pl.nw = b; pl.st = c; }
+    }
     pl.R = 32 * pl.nw * pl.rpl;
     const int E = L->E;
     pl.row_tiles = (L->F_out_pad + pl.R - 1) / pl.R;
     const int sms = num_sms();
     int ks = std::max(1, sms / pl.row_tiles);
     ks = std::min(ks, L->n_groups);
-    // x staging budget: gmax * 64 * NB * E <= 32 KiB
+    // balance: every CTA gets the same number of groups (or one fewer)
+    const int gper = (L->n_groups + ks - 1) / ks;
+    ks = (L->n_groups + gper - 1) / gper;
+    // x staging budget: gmax * 64 * NB * E <= 16 KiB
     const int xg = 64 * NB * E;
-    const int gcap = std::max(1, (32 * 1024) / xg);
+    const int gcap = std::max(1, (16 * 1024) / xg);
     while ((L->n_groups + ks - 1) / ks > gcap && ks < L->n_groups) ++ks;
     pl.ksplit = ks;
     pl.gmax = (L->n_groups + ks - 1) / ks;
-    const int cbs = E == 16 ? 1 : 2;
-    pl.smem = (size_t)cbs * L->C * 32 * E + (size_t)pl.gmax * xg + (size_t)2 * pl.R * 32 + 64;
+    const size_t cbb = (size_t)L->C * 32 * E;
+    auto smem_for = [&](int st) { return (size_t)st * (cbb + (size_t)pl.R * 32) + (size_t)pl.gmax * xg + 16 * st; };
+    while (pl.st > 1 && smem_for(pl.st) > kSmemBudget) --pl.st;
+    if (smem_for(pl.st) > kSmemBudget && pl.rpl > 1) {   // d = 8, C = 256: 128 KiB codebook image
+        pl.rpl = 1;
+        pl.R = 32 * pl.nw;
+        pl.row_tiles = (L->F_out_pad + pl.R - 1) / pl.R;
+    }
+    pl.smem = smem_for(pl.st);
     return pl;
 }
 
-fasq_status gemv_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt, uint32_t flags,
+fasq_status gemv_launch(const fasq_layer* L_, const __half* x, int B, void* y, fasq_dtype yt, uint32_t flags,
                         cudaStream_t st) {
+    fasq_layer* L = const_cast<fasq_layer*>(L_);   // workspace only; the PQ data is immutable
     const int NB = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;
     GemvPlan pl = plan_gemv(L, NB);
     GemvParams p{};
@@ -400,13 +409,34 @@ fasq_status gemv_launch(const fasq_layer* L, const __half* x, int B, void* y, fa
     p.ksplit = pl.ksplit;
     p.y_f32 = yt == FASQ_F32;
     p.gmax = pl.gmax;
-    float* partial = nullptr;
     if (pl.ksplit > 1) {
-        size_t bytes = (size_t)pl.ksplit * B * L->F_out_pad * sizeof(float);
-        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&partial), bytes, st);
-        if (e != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
+        std::lock_guard<std::mutex> lk(g_mu);
+        const int64_t need = (int64_t)pl.ksplit * B * L->F_out_pad * (int64_t)sizeof(float);
+        if (need > L->ws_bytes || pl.row_tiles > L->n_tickets) {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            cudaStreamIsCapturing(st, &cs);
+            if (cs != cudaStreamCaptureStatusNone) {
+                set_error("fasq_gemv: split-K workspace must be sized by one uncaptured call with this B first");
+                return FASQ_E_ARG;
+            }
+            FASQ_CUDA_TRY(cudaStreamSynchronize(st));
+            if (L->ws) cudaFree(L->ws);
+            if (L->tickets) cudaFree(L->tickets);
+            L->ws = nullptr;
+            L->tickets = nullptr;
+            L->ws_bytes = 0;
+            L->n_tickets = 0;
+            const int64_t wsb = std::max<int64_t>(need, (int64_t)pl.ksplit * 2 * L->F_out_pad * 4);
+            if (cudaMalloc(&L->ws, (size_t)wsb) != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
+            const int nt = std::max(pl.row_tiles, 64);
+            if (cudaMalloc(&L->tickets, (size_t)nt * sizeof(unsigned)) != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
+            FASQ_CUDA_TRY(cudaMemset(L->tickets, 0, (size_t)nt * sizeof(unsigned)));
+            L->ws_bytes = wsb;
+            L->n_tickets = nt;
+        }
     }
-    p.partial = partial;
+    p.partial = L->ws;
+    p.tickets = L->tickets;
     fasq_status s;
     switch (L->d) {
         case 1: s = dispatch_nb<1>(NB, p, pl, flags, st); break;
@@ -415,25 +445,7 @@ fasq_status gemv_launch(const fasq_layer* L, const __half* x, int B, void* y, fa
         case 8: s = dispatch_nb<8>(NB, p, pl, flags, st); break;
         default: s = FASQ_E_UNSUPPORTED;
     }
-    int launches = 1;
-    if (s == FASQ_OK && pl.ksplit > 1) {
-        int64_t n = (int64_t)B * L->F_out;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)((n + 255) / 256));
-        cfg.blockDim = dim3(256);
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;   // always safe: it only waits for the GEMV's partials
-        cudaError_t e = cudaLaunchKernelEx(&cfg, k_splitk_reduce, (const float*)partial, y, pl.ksplit, B,
-                                           (int)L->F_out, L->F_out_pad, (int)(yt == FASQ_F32));
-        if (e != cudaSuccess) s = cuda_fail(e, "k_splitk_reduce");
-        launches = 2;
-    }
-    if (partial) cudaFreeAsync(partial, st);
-    if (s == FASQ_OK) set_launch_count(launches);
+    if (s == FASQ_OK) set_launch_count(1);
     return s;
 }
 

@@ -17,6 +17,28 @@ __device__ __forceinline__ void bulk(uint32_t dst, const void* src, uint32_t byt
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 
+// CTAs in groups of `share` read the SAME `region` bytes (L2-resident) in 32 KiB copies, `reps` times.
+__global__ void k_bulk_share(const uint8_t* src, size_t region, int share, int reps, unsigned long long* sink) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    __shared__ uint64_t bars[4];
+    const uint8_t* base = src + (size_t)(blockIdx.x / share) * region;
+    if (threadIdx.x == 0) { for (int s = 0; s < 4; ++s) mbar_init(smem_u32(&bars[s]), 1); asm volatile("fence.mbarrier_init.release.cluster;"); }
+    __syncthreads();
+    const uint32_t stage = 32768;
+    const int nst = (int)(region / stage) * reps;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nst; ++i) {
+            int s = i % 4;
+            if (i >= 4) { int j = i - 4; while (!try_wait(smem_u32(&bars[s]), (j / 4) & 1)) {} }
+            expect(smem_u32(&bars[s]), stage);
+            bulk(smem_u32(sm + s * stage), base + (size_t)(i % (region / stage)) * stage, stage, smem_u32(&bars[s]));
+        }
+        for (int j = nst - 4; j < nst; ++j) { if (j < 0) continue; while (!try_wait(smem_u32(&bars[j % 4]), (j / 4) & 1)) {} }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) sink[blockIdx.x] = sm[5];
+}
+
 // Each CTA streams `per_cta` bytes in chunks of `chunk` bytes through a STAGES ring of `stage` bytes.
 template <int STAGES>
 __global__ void k_bulk(const uint8_t* src, size_t per_cta, uint32_t stage, uint32_t chunk, int issuers, unsigned long long* sink) {
@@ -104,6 +126,19 @@ int main() {
             cudaEventSynchronize(b);
             float ms; cudaEventElapsedTime(&ms, a, b);
             if (rep == 2) printf("ldg L2-resident (64MiB x8): %.1f GB/s\n", 8.0 * pc * sms / ms / 1e6);
+        }
+    }
+    cudaFuncSetAttribute(k_bulk_share, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (int share : {1, 2, 4, 8, 37, 148}) {
+        size_t region = 256 * 1024;          // 256 KiB per sharing group (L2 resident)
+        int reps = 64;
+        for (int rep = 0; rep < 2; ++rep) {
+            cudaEventRecord(a);
+            k_bulk_share<<<sms, 32, 4 * 32768>>>(src, region, share, reps, sink);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms; cudaEventElapsedTime(&ms, a, b);
+            if (rep) printf("bulk shared-region share=%d : delivered %.1f GB/s (%s)\n", share, (double)region * reps * sms / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
         }
     }
     return 0;
