@@ -76,7 +76,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     uint8_t* sA = smem;                                   // STAGES * A
     uint8_t* sB = sA + TC_STAGES * A_BYTES;               // STAGES * B
     uint8_t* sI = sB + TC_STAGES * B_BYTES;               // STAGES * IDX
-    uint8_t* sC = sI + TC_STAGES * IDX_BYTES;             // [C][2 stages][32][4]: row k = 256 B
+    uint8_t* sC = sI + TC_STAGES * IDX_BYTES;             // STAGES * [C][32][4] (one bulk copy each)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sC + TC_STAGES * CB_BYTES);
     // bars: full[S], bfull[S], empty[S], accum
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * TC_STAGES + 1);
@@ -124,11 +124,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
                 tma_load_2d(dev::smem_u32(sA + s * A_BYTES), &xmap, i * TC_K, m0, full_bar(s));
                 dev::bulk_g2s(dev::smem_u32(sI + s * IDX_BYTES), p.idx + ((size_t)i * p.F_out_pad + n0) * 32,
                               idx_bytes, full_bar(s));
+                dev::bulk_g2s(cb_u + (uint32_t)s * (uint32_t)CB_BYTES, p.cbimg + (size_t)i * CB_BYTES,
+                              (uint32_t)CB_BYTES, full_bar(s));
             }
             __syncwarp();
-            const uint8_t* cbsrc = p.cbimg + (size_t)i * CB_BYTES;
-            for (int k = lane; k < C; k += 32)
-                dev::bulk_g2s(cb_u + (uint32_t)k * 256u + 128u * s, cbsrc + (size_t)k * 128, 128u, full_bar(s));
         }
     } else if (warp == 1) {
         // ------------------------------ MMA issuer -----------------------------
@@ -167,14 +166,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
         const int rl = ew * 32 + lane;           // local weight row 0..255
         // natural byte order: register byte s holds subspace (s + rl) & 31
         const int rot = rl & 31;
-        uint32_t Lr[8];
+        // L[w] bytes = [8*sub(2w), 8*sub(2w+1), 0, 0]: prmt -> k*256 + 8*sub, >>1 -> k*128 + 4*sub
+        uint32_t Lr[16];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            uint32_t v = 0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) v |= (uint32_t)(((4 * w + j + rot) & 31) * 4) << (8 * j);
-            Lr[w] = v;
-        }
+        for (int w = 0; w < 16; ++w)
+            Lr[w] = (uint32_t)(((2 * w + rot) & 31) * 8) | ((uint32_t)(((2 * w + 1 + rot) & 31) * 8) << 8);
         // B-tile STS offsets (SWIZZLE_128B K-major: 16-B chunk c of row r at c ^ (r & 7)):
         // step st writes subspace (st + rot) & 31, i.e. k = 2*sub -> chunk sub>>2, word sub&3
         uint32_t xo[32];
@@ -192,15 +188,13 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
             uint4 v0 = dev::lds128(ia), v1 = dev::lds128(ia + 16);
             if (n0 + rl >= p.F_out_pad) { v0 = make_uint4(0, 0, 0, 0); v1 = v0; }   // rows not loaded
             const uint32_t iw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-            const uint32_t cbs = cb_u + 128u * s;
+            const uint32_t cbs = cb_u + (uint32_t)s * (uint32_t)CB_BYTES;
             const uint32_t bst = dev::smem_u32(sB + s * B_BYTES);
 #pragma unroll
             for (int st = 0; st < 32; ++st) {
-                const int j = st & 3;
-                // byte0 = 4*sub, byte1 = k, bytes 2,3 = 0  ->  k*256 + 4*sub
-                const uint32_t sel = (uint32_t)(4 + j) | ((uint32_t)j << 4) | ((uint32_t)(12 + j) << 8) |
-                                     ((uint32_t)(12 + j) << 12);
-                const uint32_t a = dev::prmt(iw[st >> 2], Lr[st >> 2], sel);
+                const int j = st & 3, lj = st & 1;
+                const uint32_t sel = (uint32_t)(4 + lj) | ((uint32_t)j << 4) | (6u << 8) | (6u << 12);
+                const uint32_t a = dev::prmt(iw[st >> 2], Lr[st >> 1], sel) >> 1;
                 const uint32_t c = dev::lds32(cbs + a);
                 asm volatile("st.shared.u32 [%0], %1;" :: "r"(bst + xo[st]), "r"(c) : "memory");
             }

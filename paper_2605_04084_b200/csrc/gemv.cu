@@ -41,7 +41,7 @@ struct GemvParams {
     const __half* x;        // [B][F_in]
     void* y;                // [B][F_out]
     float* partial;         // [ksplit][B][F_out_pad] (ksplit > 1)
-    unsigned* tickets;      // [row_tiles] arrival counters (self-resetting)
+    unsigned long long* arrive;   // [row_tiles] monotonically increasing arrival counters
     int F_in, F_out, F_out_pad, N_ss, n_groups, C, B;
     int ksplit, y_f32;
     int gmax;               // max groups per CTA (x staging capacity)
@@ -243,9 +243,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
         }
         return;
     }
-    // split-K: publish partials, the LAST CTA of this row tile to arrive sums
-    // them in fixed ks order (deterministic; the paper's merge is atomicAdd,
-    // P:278) -- one kernel, no second launch.
+    // split-K: publish partials, wait until every CTA of this row tile has
+    // published (all CTAs are co-resident: grid <= #SMs, 1 CTA/SM, and PDL
+    // dependents launch only after every CTA started), then each CTA sums a
+    // 1/ksplit slice of the tile's rows over ks = 0..ksplit-1 in fixed order
+    // (deterministic; the paper's merge is atomicAdd).
 #pragma unroll
     for (int q = 0; q < RPL; ++q) {
         const int row = r0 + warp_row0 + q * 32 + lane;
@@ -255,16 +257,23 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
             if (b < p.B) __stcg(&p.partial[((size_t)ks * p.B + b) * p.F_out_pad + row], acc[q][b]);
     }
     __threadfence();
-    __shared__ unsigned s_last;
     asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
-    if (threadIdx.x == 0) s_last = (atomicAdd(&p.tickets[rt], 1u) == (unsigned)(p.ksplit - 1));
+    if (threadIdx.x == 0) {
+        unsigned long long* ctr = p.arrive + rt;
+        const unsigned long long old = atomicAdd(ctr, 1ull);
+        const unsigned long long target = (old / (unsigned long long)p.ksplit + 1ull) * (unsigned long long)p.ksplit;
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        } while (v < target);
+    }
     asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
-    if (!s_last) return;
-    __threadfence();
-    const int n_out = rows_valid * p.B;
+    const int rows_per = (rows_valid + p.ksplit - 1) / p.ksplit;
+    const int rb = ks * rows_per, re = min(rows_valid, rb + rows_per);
+    const int n_out = (re > rb ? re - rb : 0) * p.B;
     const size_t kstride = (size_t)p.B * p.F_out_pad;
     for (int t = threadIdx.x; t < n_out; t += NW * 32) {
-        const int b = t / rows_valid, row = r0 + t % rows_valid;
+        const int b = t / (re - rb), row = r0 + rb + t % (re - rb);
         const float* src = p.partial + (size_t)b * p.F_out_pad + row;
         float sum = 0.f;
         int k = 0;
@@ -281,7 +290,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
             else reinterpret_cast<__half*>(p.y)[(size_t)b * p.F_out + row] = __float2half_rn(sum);
         }
     }
-    if (threadIdx.x == 0) p.tickets[rt] = 0u;     // ready for the next launch (stream order)
 }
 
 // ------------------------------- host side ----------------------------------
@@ -336,6 +344,9 @@ static fasq_status dispatch_cfg(const GemvParams& p, const GemvPlan& pl, uint32_
     if (pl.rpl == 1 && pl.nw == 16 && pl.st == 1) return launch_gemv_t<D, NB, 1, 16, 1>(p, pl, flags, st);
     if (pl.rpl == 2 && pl.nw == 16 && pl.st == 1) return launch_gemv_t<D, NB, 2, 16, 1>(p, pl, flags, st);
     if (pl.rpl == 1 && pl.nw == 8 && pl.st == 3) return launch_gemv_t<D, NB, 1, 8, 3>(p, pl, flags, st);
+    if (pl.rpl == 4 && pl.nw == 8 && pl.st == 3) return launch_gemv_t<D, NB, 4, 8, 3>(p, pl, flags, st);
+    if (pl.rpl == 4 && pl.nw == 16 && pl.st == 2) return launch_gemv_t<D, NB, 4, 16, 2>(p, pl, flags, st);
+    if (pl.rpl == 2 && pl.nw == 8 && pl.st == 3) return launch_gemv_t<D, NB, 2, 8, 3>(p, pl, flags, st);
     return FASQ_E_UNSUPPORTED;
 }
 
@@ -377,6 +388,9 @@ static GemvPlan plan_gemv(const fasq_layer* L, int NB) {
     while ((L->n_groups + ks - 1) / ks > gcap && ks < L->n_groups) ++ks;
     pl.ksplit = ks;
     pl.gmax = (L->n_groups + ks - 1) / ks;
+    // the in-kernel split-K merge spins on its peers: all CTAs must be resident
+    while (pl.ksplit > 1 && pl.row_tiles * pl.ksplit > sms) --pl.ksplit;
+    pl.gmax = (L->n_groups + pl.ksplit - 1) / pl.ksplit;
     const size_t cbb = (size_t)L->C * 32 * E;
     auto smem_for = [&](int st) { return (size_t)st * (cbb + (size_t)pl.R * 32) + (size_t)pl.gmax * xg + 16 * st; };
     while (pl.st > 1 && smem_for(pl.st) > kSmemBudget) --pl.st;
@@ -429,14 +443,14 @@ fasq_status gemv_launch(const fasq_layer* L_, const __half* x, int B, void* y, f
             const int64_t wsb = std::max<int64_t>(need, (int64_t)pl.ksplit * 2 * L->F_out_pad * 4);
             if (cudaMalloc(&L->ws, (size_t)wsb) != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
             const int nt = std::max(pl.row_tiles, 64);
-            if (cudaMalloc(&L->tickets, (size_t)nt * sizeof(unsigned)) != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
-            FASQ_CUDA_TRY(cudaMemset(L->tickets, 0, (size_t)nt * sizeof(unsigned)));
+            if (cudaMalloc(&L->tickets, (size_t)nt * sizeof(unsigned long long)) != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
+            FASQ_CUDA_TRY(cudaMemset(L->tickets, 0, (size_t)nt * sizeof(unsigned long long)));
             L->ws_bytes = wsb;
             L->n_tickets = nt;
         }
     }
     p.partial = L->ws;
-    p.tickets = L->tickets;
+    p.arrive = reinterpret_cast<unsigned long long*>(L->tickets);
     fasq_status s;
     switch (L->d) {
         case 1: s = dispatch_nb<1>(NB, p, pl, flags, st); break;
