@@ -168,21 +168,33 @@ class DecodeStep:
         dist.all_gather_into_tensor(out.view(-1), self.bufs[name].view(-1), group=self.pg)
         return out
 
-    def run(self, flags=0):
+    def run(self, flags=0, grouped=True):
+        """q/k/v (same input) and gate/up (same input) are separately packed
+        layers launched together with fasq_gemv_grouped."""
         import paper_2605_04084_b200 as F
         n = 0
         h = self.h
         for layers in self.blocks:
-            for name in ("q_proj", "k_proj", "v_proj"):
-                F.gemv(layers[name], h, out=self.bufs[name], flags=flags)
+            if grouped:
+                F.gemv_grouped([layers[k] for k in ("q_proj", "k_proj", "v_proj")], h,
+                               outs=[self.bufs[k] for k in ("q_proj", "k_proj", "v_proj")], flags=flags)
                 n += F.last_launch_count()
+            else:
+                for name in ("q_proj", "k_proj", "v_proj"):
+                    F.gemv(layers[name], h, out=self.bufs[name], flags=flags)
+                    n += F.last_launch_count()
             q = self._gather("q_proj")
             F.gemv(layers["o_proj"], q, out=self.bufs["o_proj"], flags=flags)
             n += F.last_launch_count()
             o = self._gather("o_proj")
-            for name in ("gate_proj", "up_proj"):
-                F.gemv(layers[name], o, out=self.bufs[name], flags=flags)
+            if grouped:
+                F.gemv_grouped([layers["gate_proj"], layers["up_proj"]], o,
+                               outs=[self.bufs["gate_proj"], self.bufs["up_proj"]], flags=flags)
                 n += F.last_launch_count()
+            else:
+                for name in ("gate_proj", "up_proj"):
+                    F.gemv(layers[name], o, out=self.bufs[name], flags=flags)
+                    n += F.last_launch_count()
             g = self._gather("gate_proj")
             F.gemv(layers["down_proj"], g, out=self.bufs["down_proj"], flags=flags)
             n += F.last_launch_count()

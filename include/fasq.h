@@ -143,6 +143,13 @@ fasq_status fasq_gemv(const fasq_layer* layer, const void* x_dev, int32_t B, voi
 fasq_status fasq_gemv_ex(const fasq_layer* layer, const void* x_dev, int32_t B, void* y_dev,
                          fasq_dtype y_dtype, uint32_t flags, void* stream);
 
+/* Grouped decode GEMV: n (1..4) layers that share the input x (q/k/v or
+ * gate/up of a transformer block -- each packed separately) in ONE
+ * launch: ys[l] = W_hat_l . x.  All layers must have the same F_in and d
+ * (FASQ_E_SHAPE otherwise).  Same numerics as n separate fasq_gemv calls. */
+fasq_status fasq_gemv_grouped(const fasq_layer* const* layers, int32_t n, const void* x_dev, int32_t B,
+                              void* const* ys_dev, fasq_dtype y_dtype, uint32_t flags, void* stream);
+
 /* Same product with HOST buffers (end-to-end path): copies x_host (fp16
  * [B][F_in], ideally pinned) to the device, runs fasq_gemv and copies y back
  * to y_host.  Synchronous: returns after y_host is written. */

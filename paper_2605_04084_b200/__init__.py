@@ -29,7 +29,7 @@ _STATUS = {0: "FASQ_OK", -1: "FASQ_E_ARG", -2: "FASQ_E_NONDIVISIBLE", -3: "FASQ_
 
 # Every symbol include/fasq.h declares (checked by tests/test_abi.py).
 EXPORTED = ["fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
-            "fasq_free", "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_host", "fasq_gemm",
+            "fasq_free", "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_gemv_host", "fasq_gemm",
             "fasq_last_launch_count", "fasq_status_string", "fasq_last_error_message",
             "fasq_abi_version"]
 
@@ -74,11 +74,13 @@ def _load():
     L.fasq_gemv.argtypes = [vp, vp, i32, vp, i32, vp]
     L.fasq_gemv_ex.argtypes = [vp, vp, i32, vp, i32, u32, vp]
     L.fasq_gemv_host.argtypes = [vp, vp, i32, vp, i32, vp]
+    L.fasq_gemv_grouped.argtypes = [ctypes.POINTER(vp), i32, vp, i32, ctypes.POINTER(vp), i32, u32, vp]
     L.fasq_gemm.argtypes = [vp, vp, i64, vp, i32, i32, vp]
     L.fasq_status_string.restype = ctypes.c_char_p
     L.fasq_last_error_message.restype = ctypes.c_char_p
     for name in ("fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
-                 "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_host", "fasq_gemm", "fasq_last_launch_count",
+                 "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_gemv_host", "fasq_gemm",
+                 "fasq_last_launch_count",
                  "fasq_abi_version"):
         getattr(L, name).restype = ctypes.c_int32
     return L
@@ -190,6 +192,23 @@ def gemv(layer: Layer, x: torch.Tensor, out: torch.Tensor | None = None,
     yt = FASQ_F32 if out.dtype == torch.float32 else FASQ_F16
     _check(lib.fasq_gemv_ex(layer.handle, x.data_ptr(), B, out.data_ptr(), yt, flags, _stream(stream)))
     return out
+
+
+def gemv_grouped(layers, x: torch.Tensor, outs=None, out_dtype: torch.dtype = torch.float32,
+                 flags: int = 0, stream=None):
+    """One launch for up to 4 layers sharing x (e.g. q/k/v): returns [y_l]."""
+    x = _cuda(x, torch.float16, "x")
+    if x.dim() == 1:
+        x = x.unsqueeze(0)
+    B = x.shape[0]
+    n = len(layers)
+    if outs is None:
+        outs = [torch.empty((B, L.F_out), dtype=out_dtype, device=x.device) for L in layers]
+    hs = (ctypes.c_void_p * n)(*[L.handle.value for L in layers])
+    ys = (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs])
+    yt = FASQ_F32 if outs[0].dtype == torch.float32 else FASQ_F16
+    _check(lib.fasq_gemv_grouped(hs, n, x.data_ptr(), B, ys, yt, flags, _stream(stream)))
+    return outs
 
 
 def gemv_host(layer: Layer, x_host: torch.Tensor, y_host: torch.Tensor, stream=None) -> torch.Tensor:

@@ -193,6 +193,18 @@ fasq_status fasq_gemv_ex(const fasq_layer* L, const void* x_dev, int32_t B, void
     return gemv_launch(L, static_cast<const __half*>(x_dev), B, y_dev, yt, flags, (cudaStream_t)stream);
 }
 
+fasq_status fasq_gemv_grouped(const fasq_layer* const* layers, int32_t n, const void* x_dev, int32_t B,
+                              void* const* ys_dev, fasq_dtype yt, uint32_t flags, void* stream) {
+    if (!layers || !x_dev || !ys_dev || n < 1) return FASQ_E_ARG;
+    if (n > 4) return FASQ_E_UNSUPPORTED;
+    for (int i = 0; i < n; ++i)
+        if (!layers[i] || !ys_dev[i]) return FASQ_E_ARG;
+    if (B < 1 || B > 8) return FASQ_E_UNSUPPORTED;
+    if (yt != FASQ_F16 && yt != FASQ_F32) return FASQ_E_ARG;
+    return gemv_grouped_launch(layers, n, static_cast<const __half*>(x_dev), B, ys_dev, yt, flags,
+                               (cudaStream_t)stream);
+}
+
 fasq_status fasq_gemv(const fasq_layer* L, const void* x_dev, int32_t B, void* y_dev, fasq_dtype yt,
                       void* stream) {
     return fasq_gemv_ex(L, x_dev, B, y_dev, yt, 0u, stream);

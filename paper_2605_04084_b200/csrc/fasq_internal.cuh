@@ -97,6 +97,8 @@ fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t
 // ---- compute entry points ---------------------------------------------------
 fasq_status gemv_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt,
                         uint32_t flags, cudaStream_t st);
+fasq_status gemv_grouped_launch(const fasq_layer* const* Ls, int nl, const __half* x, int B, void* const* ys,
+                                fasq_dtype yt, uint32_t flags, cudaStream_t st);
 fasq_status gemm_lut_launch(const fasq_layer* L, const __half* X, int64_t M, void* Y,
                             fasq_dtype yt, cudaStream_t st);
 fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void* Y,

@@ -35,15 +35,22 @@
 
 namespace fasq {
 
-struct GemvParams {
+constexpr int kMaxGroup = 4;   // layers per grouped launch (q/k/v, gate/up)
+
+struct GemvLayerArgs {
     const uint8_t* idx;     // [n_groups][F_out_pad][32]
     const uint8_t* cbimg;   // [n_groups][C][32][E]
-    const __half* x;        // [B][F_in]
     void* y;                // [B][F_out]
     float* partial;         // [ksplit][B][F_out_pad] (ksplit > 1)
     unsigned long long* arrive;   // [row_tiles] monotonically increasing arrival counters
-    int F_in, F_out, F_out_pad, N_ss, n_groups, C, B;
-    int ksplit, y_f32;
+    int F_out, F_out_pad, N_ss, n_groups, C, ksplit, cta_begin;
+};
+
+struct GemvParams {
+    GemvLayerArgs L[kMaxGroup];   // layers sharing x (grouped launch); CTAs are laid out layer-major
+    int nl;
+    const __half* x;        // [B][F_in]
+    int F_in, B, y_f32;
     int gmax;               // max groups per CTA (x staging capacity)
 };
 
@@ -54,6 +61,10 @@ struct GemvParams {
 // stage -- the microbenchmark in tools/mb_bulk.cu shows 128-B bulk copies
 // cap at ~0.6 TB/s while >=16 KiB copies reach ~7 TB/s), index ring
 // [ST][R][32], x [gmax][64][NB][E], mbarriers full[ST], empty[ST].
+// Under programmatic dependent launch the NEXT layer's CTAs may become
+// resident as soon as SMEM allows and prefetch their codebook/index stages
+// (weights do not depend on x); they only wait (griddepcontrol.wait) before
+// touching x.
 template <int D, int NB, int RPL, int NW, int ST>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     constexpr int E = D <= 2 ? 4 : 2 * D;
@@ -61,14 +72,21 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     constexpr int XG = 64 * NB * E;           // x bytes per staged group
     extern __shared__ __align__(1024) uint8_t smem[];
 
-    const int C = p.C;
+    int li = 0;
+#pragma unroll
+    for (int l = 1; l < kMaxGroup; ++l)
+        if (l < p.nl && (int)blockIdx.x >= p.L[l].cta_begin) li = l;
+    const GemvLayerArgs& la = p.L[li];
+    const int C = la.C;
+    const int ksplit = la.ksplit, n_groups = la.n_groups, F_out = la.F_out, F_out_pad = la.F_out_pad;
     const uint32_t CBB = (uint32_t)C * 32u * E;   // codebook image bytes per group
-    const int rt = blockIdx.x, ks = blockIdx.y;
-    const int g_begin = (int)((int64_t)ks * p.n_groups / p.ksplit);
-    const int g_end = (int)((int64_t)(ks + 1) * p.n_groups / p.ksplit);
+    const int local = (int)blockIdx.x - la.cta_begin;
+    const int rt = local / ksplit, ks = local % ksplit;
+    const int g_begin = (int)((int64_t)ks * n_groups / ksplit);
+    const int g_end = (int)((int64_t)(ks + 1) * n_groups / ksplit);
     const int ng = g_end - g_begin;
     const int r0 = rt * R;
-    const int rows_valid = min(R, p.F_out_pad - r0);   // multiple of 32
+    const int rows_valid = min(R, F_out_pad - r0);   // multiple of 32
 
     uint8_t* s_cb = smem;                                     // ST*CBB
     uint8_t* s_idx = s_cb + ST * CBB;                         // ST*R*32
@@ -90,6 +108,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
             dev::mbar_init(empty0 + 8 * s, NW);
         }
         dev::fence_barrier_init();
+        dev::pdl_launch_dependents();   // let the next layer's CTAs start prefetching now
     }
     __syncthreads();
 
@@ -103,13 +122,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
                 const int g = g_begin + i;
                 const uint32_t full = full0 + 8 * slot;
                 dev::mbar_arrive_expect_tx(full, idx_chunk + CBB);
-                dev::bulk_g2s(cb_u + (uint32_t)slot * CBB, p.cbimg + (size_t)g * CBB, CBB, full);
-                dev::bulk_g2s(idx_u + (uint32_t)slot * R * 32u, p.idx + ((size_t)g * p.F_out_pad + r0) * 32,
+                dev::bulk_g2s(cb_u + (uint32_t)slot * CBB, la.cbimg + (size_t)g * CBB, CBB, full);
+                dev::bulk_g2s(idx_u + (uint32_t)slot * R * 32u, la.idx + ((size_t)g * F_out_pad + r0) * 32,
                               idx_chunk, full);
             }
         }
         __syncwarp();
-        dev::pdl_launch_dependents();
         return;
     }
 
@@ -119,20 +137,42 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     {
         const int tid = threadIdx.x;
         const int n_ent = ng * 64 * NB;   // entries of E bytes
-        for (int t = tid; t < n_ent; t += NW * 32) {
-            const int b = t % NB;
-            const int e64 = (t / NB) % 64;
-            const int gl = t / (NB * 64);
-            const int ss = (g_begin + gl) * 32 + (e64 & 31);
-            uint32_t w[4] = {0u, 0u, 0u, 0u};
-            if (b < p.B && ss < p.N_ss) {
-                const uint16_t* src = reinterpret_cast<const uint16_t*>(p.x) + (size_t)b * p.F_in + (size_t)ss * D;
+        // all global loads first (one round trip), then the SMEM stores
+        constexpr int XPT = 4;            // entries per thread per pass
+        for (int t0 = tid; t0 < n_ent; t0 += NW * 32 * XPT) {
+            uint32_t w[XPT][4];
 #pragma unroll
-                for (int e = 0; e < D; ++e) w[e >> 1] |= (uint32_t)src[e] << (16 * (e & 1));
+            for (int u = 0; u < XPT; ++u) {
+                const int t = t0 + u * NW * 32;
+                w[u][0] = w[u][1] = w[u][2] = w[u][3] = 0u;
+                if (t >= n_ent) continue;
+                const int b = t % NB;
+                const int e64 = (t / NB) % 64;
+                const int gl = t / (NB * 64);
+                const int ss = (g_begin + gl) * 32 + (e64 & 31);
+                if (b < p.B && ss < la.N_ss) {
+                    const __half* src = p.x + (size_t)b * p.F_in + (size_t)ss * D;
+                    if (D == 1) {
+                        w[u][0] = (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(src));
+                    } else if (D == 2) {
+                        w[u][0] = __ldg(reinterpret_cast<const unsigned int*>(src));
+                    } else if (D == 4) {
+                        const uint2 v = __ldg(reinterpret_cast<const uint2*>(src));
+                        w[u][0] = v.x; w[u][1] = v.y;
+                    } else {
+                        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src));
+                        w[u][0] = v.x; w[u][1] = v.y; w[u][2] = v.z; w[u][3] = v.w;
+                    }
+                }
             }
-            uint32_t* dst = reinterpret_cast<uint32_t*>(s_x + (size_t)t * E);
 #pragma unroll
-            for (int q = 0; q < E / 4; ++q) dst[q] = w[q];
+            for (int u = 0; u < XPT; ++u) {
+                const int t = t0 + u * NW * 32;
+                if (t >= n_ent) continue;
+                uint32_t* dst = reinterpret_cast<uint32_t*>(s_x + (size_t)t * E);
+#pragma unroll
+                for (int q = 0; q < E / 4; ++q) dst[q] = w[u][q];
+            }
         }
         asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
     }
@@ -229,16 +269,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     }
 
     // ------------------------------ epilogue --------------------------------
-    if (p.ksplit == 1) {
+    if (ksplit == 1) {
 #pragma unroll
         for (int q = 0; q < RPL; ++q) {
             const int row = r0 + warp_row0 + q * 32 + lane;
-            if (warp_row0 + q * 32 >= rows_valid || row >= p.F_out) continue;
+            if (warp_row0 + q * 32 >= rows_valid || row >= F_out) continue;
 #pragma unroll
             for (int b = 0; b < NB; ++b) {
                 if (b >= p.B) continue;
-                if (p.y_f32) reinterpret_cast<float*>(p.y)[(size_t)b * p.F_out + row] = acc[q][b];
-                else reinterpret_cast<__half*>(p.y)[(size_t)b * p.F_out + row] = __float2half_rn(acc[q][b]);
+                if (p.y_f32) reinterpret_cast<float*>(la.y)[(size_t)b * F_out + row] = acc[q][b];
+                else reinterpret_cast<__half*>(la.y)[(size_t)b * F_out + row] = __float2half_rn(acc[q][b]);
             }
         }
         return;
@@ -254,40 +294,40 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
         if (warp_row0 + q * 32 >= rows_valid) continue;
 #pragma unroll
         for (int b = 0; b < NB; ++b)
-            if (b < p.B) __stcg(&p.partial[((size_t)ks * p.B + b) * p.F_out_pad + row], acc[q][b]);
+            if (b < p.B) __stcg(&la.partial[((size_t)ks * p.B + b) * F_out_pad + row], acc[q][b]);
     }
     __threadfence();
     asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
     if (threadIdx.x == 0) {
-        unsigned long long* ctr = p.arrive + rt;
+        unsigned long long* ctr = la.arrive + rt;
         const unsigned long long old = atomicAdd(ctr, 1ull);
-        const unsigned long long target = (old / (unsigned long long)p.ksplit + 1ull) * (unsigned long long)p.ksplit;
+        const unsigned long long target = (old / (unsigned long long)ksplit + 1ull) * (unsigned long long)ksplit;
         unsigned long long v;
         do {
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
         } while (v < target);
     }
     asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
-    const int rows_per = (rows_valid + p.ksplit - 1) / p.ksplit;
+    const int rows_per = (rows_valid + ksplit - 1) / ksplit;
     const int rb = ks * rows_per, re = min(rows_valid, rb + rows_per);
     const int n_out = (re > rb ? re - rb : 0) * p.B;
-    const size_t kstride = (size_t)p.B * p.F_out_pad;
+    const size_t kstride = (size_t)p.B * F_out_pad;
     for (int t = threadIdx.x; t < n_out; t += NW * 32) {
         const int b = t / (re - rb), row = r0 + rb + t % (re - rb);
-        const float* src = p.partial + (size_t)b * p.F_out_pad + row;
+        const float* src = la.partial + (size_t)b * F_out_pad + row;
         float sum = 0.f;
         int k = 0;
-        for (; k + 8 <= p.ksplit; k += 8) {
+        for (; k + 8 <= ksplit; k += 8) {
             float v[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(k + u) * kstride);
 #pragma unroll
             for (int u = 0; u < 8; ++u) sum += v[u];
         }
-        for (; k < p.ksplit; ++k) sum += __ldcg(src + (size_t)k * kstride);
-        if (row < p.F_out) {
-            if (p.y_f32) reinterpret_cast<float*>(p.y)[(size_t)b * p.F_out + row] = sum;
-            else reinterpret_cast<__half*>(p.y)[(size_t)b * p.F_out + row] = __float2half_rn(sum);
+        for (; k < ksplit; ++k) sum += __ldcg(src + (size_t)k * kstride);
+        if (row < F_out) {
+            if (p.y_f32) reinterpret_cast<float*>(la.y)[(size_t)b * F_out + row] = sum;
+            else reinterpret_cast<__half*>(la.y)[(size_t)b * F_out + row] = __float2half_rn(sum);
         }
     }
 }
@@ -307,22 +347,22 @@ static int num_sms() {
 }
 
 struct GemvPlan {
-    int rpl, nw, st, R, row_tiles, ksplit, gmax;
+    int rpl, nw, st, R;
+    int nl;
+    int row_tiles[kMaxGroup], ksplit[kMaxGroup];
+    int gmax, grid;
     size_t smem;
 };
 
 template <int D, int NB, int RPL, int NW, int ST>
-static fasq_status launch_gemv_t(const GemvParams& p0, const GemvPlan& pl, uint32_t flags, cudaStream_t st) {
-    constexpr int E = D <= 2 ? 4 : 2 * D;
+static fasq_status launch_gemv_t(const GemvParams& p, const GemvPlan& pl, uint32_t flags, cudaStream_t st) {
     auto kern = k_gemv<D, NB, RPL, NW, ST>;
     static size_t lim = 0;
     static std::once_flag once;
     std::call_once(once, [&] { lim = set_max_dyn_smem(kern); });
     if (lim < pl.smem) { set_error("gemv: dynamic SMEM plan exceeds the device limit"); return FASQ_E_UNSUPPORTED; }
-    (void)E;
-    GemvParams p = p0;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(pl.row_tiles, pl.ksplit, 1);
+    cfg.gridDim = dim3(pl.grid, 1, 1);
     cfg.blockDim = dim3((NW + 1) * 32, 1, 1);
     cfg.dynamicSmemBytes = pl.smem;
     cfg.stream = st;
@@ -337,16 +377,25 @@ static fasq_status launch_gemv_t(const GemvParams& p0, const GemvPlan& pl, uint3
 
 template <int D, int NB>
 static fasq_status dispatch_cfg(const GemvParams& p, const GemvPlan& pl, uint32_t flags, cudaStream_t st) {
-    if (pl.rpl == 2 && pl.nw == 16 && pl.st == 3) return launch_gemv_t<D, NB, 2, 16, 3>(p, pl, flags, st);
-    if (pl.rpl == 2 && pl.nw == 16 && pl.st == 2) return launch_gemv_t<D, NB, 2, 16, 2>(p, pl, flags, st);
-    if (pl.rpl == 1 && pl.nw == 16 && pl.st == 2) return launch_gemv_t<D, NB, 1, 16, 2>(p, pl, flags, st);
-    if (pl.rpl == 1 && pl.nw == 16 && pl.st == 3) return launch_gemv_t<D, NB, 1, 16, 3>(p, pl, flags, st);
-    if (pl.rpl == 1 && pl.nw == 16 && pl.st == 1) return launch_gemv_t<D, NB, 1, 16, 1>(p, pl, flags, st);
-    if (pl.rpl == 2 && pl.nw == 16 && pl.st == 1) return launch_gemv_t<D, NB, 2, 16, 1>(p, pl, flags, st);
-    if (pl.rpl == 1 && pl.nw == 8 && pl.st == 3) return launch_gemv_t<D, NB, 1, 8, 3>(p, pl, flags, st);
-    if (pl.rpl == 4 && pl.nw == 8 && pl.st == 3) return launch_gemv_t<D, NB, 4, 8, 3>(p, pl, flags, st);
-    if (pl.rpl == 4 && pl.nw == 16 && pl.st == 2) return launch_gemv_t<D, NB, 4, 16, 2>(p, pl, flags, st);
-    if (pl.rpl == 2 && pl.nw == 8 && pl.st == 3) return launch_gemv_t<D, NB, 2, 8, 3>(p, pl, flags, st);
+#define FASQ_GEMV_CFG_CASE(RPL_, NW_, ST_) \
+    if (pl.rpl == RPL_ && pl.nw == NW_ && pl.st == ST_) return launch_gemv_t<D, NB, RPL_, NW_, ST_>(p, pl, flags, st);
+    FASQ_GEMV_CFG_CASE(2, 8, 2)
+    FASQ_GEMV_CFG_CASE(2, 8, 3)
+    FASQ_GEMV_CFG_CASE(1, 8, 2)
+    FASQ_GEMV_CFG_CASE(1, 8, 3)
+    FASQ_GEMV_CFG_CASE(4, 8, 2)
+    FASQ_GEMV_CFG_CASE(4, 8, 3)
+    FASQ_GEMV_CFG_CASE(2, 16, 2)
+    FASQ_GEMV_CFG_CASE(2, 16, 3)
+    FASQ_GEMV_CFG_CASE(1, 16, 3)
+    FASQ_GEMV_CFG_CASE(1, 8, 1)
+    FASQ_GEMV_CFG_CASE(8, 4, 3)
+    FASQ_GEMV_CFG_CASE(4, 4, 4)
+    FASQ_GEMV_CFG_CASE(2, 8, 4)
+    FASQ_GEMV_CFG_CASE(8, 8, 2)
+    FASQ_GEMV_CFG_CASE(2, 8, 1)
+#undef FASQ_GEMV_CFG_CASE
+    set_error("gemv: no kernel instantiated for this tiling");
     return FASQ_E_UNSUPPORTED;
 }
 
@@ -361,98 +410,131 @@ static fasq_status dispatch_nb(int NB, const GemvParams& p, const GemvPlan& pl, 
     return FASQ_E_UNSUPPORTED;
 }
 
-// Tiling plan: R rows x a K-range of 32-subspace groups
-// per CTA, one CTA per SM; the K-split (grid.y) fills the 148 SMs.  Env
-// FASQ_GEMV_CFG="rpl,nw,stages" overrides the default (tuning only).
-static GemvPlan plan_gemv(const fasq_layer* L, int NB) {
+// Tiling plan: each layer's work is split into R-row tiles
+// x K-ranges of 32-subspace groups; the CTAs of all layers of a (grouped)
+// launch add up to <= #SMs so they are co-resident (the split-K merge spins on
+// its peers) and each SM runs one CTA of this launch -- the second SM slot is
+// left for the NEXT launch's prefetch under PDL.  CTAs are shared between the
+// layers in proportion to their index bytes.  Env FASQ_GEMV_CFG="rpl,nw,stages"
+// overrides the default tiling (tuning only).
+static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB) {
     GemvPlan pl{};
-    pl.nw = 16;
-    pl.rpl = NB <= 2 ? 2 : 1;
+    pl.nw = 8;
+    pl.rpl = NB <= 2 ? 4 : (NB == 4 ? 2 : 1);
     pl.st = 3;
     if (const char* e = getenv("FASQ_GEMV_CFG")) {
         int a = 0, b = 0, c = 0;
         if (sscanf(e, "%d,%d,%d", &a, &b, &c) == 3) { pl.rpl = a; pl.nw = b; pl.st = c; }
     }
-    pl.R = 32 * pl.nw * pl.rpl;
-    const int E = L->E;
-    pl.row_tiles = (L->F_out_pad + pl.R - 1) / pl.R;
-    const int sms = num_sms();
-    int ks = std::max(1, sms / pl.row_tiles);
-    ks = std::min(ks, L->n_groups);
-    // balance: every CTA gets the same number of groups (or one fewer)
-    const int gper = (L->n_groups + ks - 1) / ks;
-    ks = (L->n_groups + gper - 1) / gper;
-    // x staging budget: gmax * 64 * NB * E <= 16 KiB
-    const int xg = 64 * NB * E;
-    const int gcap = std::max(1, (16 * 1024) / xg);
-    while ((L->n_groups + ks - 1) / ks > gcap && ks < L->n_groups) ++ks;
-    pl.ksplit = ks;
-    pl.gmax = (L->n_groups + ks - 1) / ks;
-    // the in-kernel split-K merge spins on its peers: all CTAs must be resident
-    while (pl.ksplit > 1 && pl.row_tiles * pl.ksplit > sms) --pl.ksplit;
-    pl.gmax = (L->n_groups + pl.ksplit - 1) / pl.ksplit;
-    const size_t cbb = (size_t)L->C * 32 * E;
-    auto smem_for = [&](int st) { return (size_t)st * (cbb + (size_t)pl.R * 32) + (size_t)pl.gmax * xg + 16 * st; };
-    while (pl.st > 1 && smem_for(pl.st) > kSmemBudget) --pl.st;
-    if (smem_for(pl.st) > kSmemBudget && pl.rpl > 1) {   // d = 8, C = 256: 128 KiB codebook image
-        pl.rpl = 1;
-        pl.R = 32 * pl.nw;
-        pl.row_tiles = (L->F_out_pad + pl.R - 1) / pl.R;
+    pl.nl = nl;
+    const int E = Ls[0]->E;
+    int maxC = 0;
+    for (int l = 0; l < nl; ++l) maxC = std::max(maxC, Ls[l]->C);
+    if ((size_t)maxC * 32 * E * pl.st + (size_t)32 * pl.nw * pl.rpl * 32 * pl.st > kSmemBudget) {
+        pl.st = 1;                                   // d = 8, C = 256: 128 KiB codebook image per group
+        if (pl.rpl > 1) pl.rpl = 1;
     }
-    pl.smem = smem_for(pl.st);
+    pl.R = 32 * pl.nw * pl.rpl;
+    const int sms = num_sms();
+    double W = 0;
+    for (int l = 0; l < nl; ++l) W += (double)Ls[l]->F_out_pad * Ls[l]->n_groups;
+    int total = 0;
+    for (int l = 0; l < nl; ++l) {
+        const fasq_layer* L = Ls[l];
+        pl.row_tiles[l] = (L->F_out_pad + pl.R - 1) / pl.R;
+        const double share = sms * ((double)L->F_out_pad * L->n_groups) / W;
+        int ks = std::max(1, (int)(share / pl.row_tiles[l]));
+        ks = std::min(ks, L->n_groups);
+        const int gper = (L->n_groups + ks - 1) / ks;   // balance: equal groups per CTA
+        ks = (L->n_groups + gper - 1) / gper;
+        pl.ksplit[l] = ks;
+        total += pl.row_tiles[l] * ks;
+    }
+    // co-residency: shrink the largest K-split until all CTAs fit on the SMs
+    while (total > sms) {
+        int lm = -1;
+        for (int l = 0; l < nl; ++l)
+            if (pl.ksplit[l] > 1 && (lm < 0 || pl.ksplit[l] * pl.row_tiles[l] > pl.ksplit[lm] * pl.row_tiles[lm])) lm = l;
+        if (lm < 0) break;                               // ksplit == 1 everywhere: no spin, waves are fine
+        total -= pl.row_tiles[lm];
+        pl.ksplit[lm] -= 1;
+    }
+    pl.grid = total;
+    pl.gmax = 1;
+    for (int l = 0; l < nl; ++l) pl.gmax = std::max(pl.gmax, (Ls[l]->n_groups + pl.ksplit[l] - 1) / pl.ksplit[l]);
+    const size_t xg = (size_t)64 * NB * E;
+    pl.smem = (size_t)pl.st * ((size_t)maxC * 32 * E + (size_t)pl.R * 32) + (size_t)pl.gmax * xg + 16 * pl.st;
     return pl;
 }
 
-fasq_status gemv_launch(const fasq_layer* L_, const __half* x, int B, void* y, fasq_dtype yt, uint32_t flags,
-                        cudaStream_t st) {
-    fasq_layer* L = const_cast<fasq_layer*>(L_);   // workspace only; the PQ data is immutable
+// Grows the layer's split-K workspace (outside stream capture only).
+static fasq_status ensure_workspace(fasq_layer* L, int ksplit, int row_tiles, int B, cudaStream_t st) {
+    if (ksplit <= 1) return FASQ_OK;
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int64_t need = (int64_t)ksplit * B * L->F_out_pad * (int64_t)sizeof(float);
+    if (need <= L->ws_bytes && row_tiles <= L->n_tickets) return FASQ_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone) {
+        set_error("fasq_gemv: split-K workspace must be sized by one uncaptured call with this B first");
+        return FASQ_E_ARG;
+    }
+    FASQ_CUDA_TRY(cudaStreamSynchronize(st));
+    if (L->ws) cudaFree(L->ws);
+    if (L->tickets) cudaFree(L->tickets);
+    L->ws = nullptr;
+    L->tickets = nullptr;
+    L->ws_bytes = 0;
+    L->n_tickets = 0;
+    const int64_t wsb = std::max<int64_t>(need, (int64_t)ksplit * 2 * L->F_out_pad * 4);
+    if (cudaMalloc(&L->ws, (size_t)wsb) != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
+    const int nt = std::max(row_tiles, 64);
+    if (cudaMalloc(&L->tickets, (size_t)nt * sizeof(unsigned long long)) != cudaSuccess) {
+        cudaGetLastError();
+        return FASQ_E_OOM;
+    }
+    FASQ_CUDA_TRY(cudaMemset(L->tickets, 0, (size_t)nt * sizeof(unsigned long long)));
+    L->ws_bytes = wsb;
+    L->n_tickets = nt;
+    return FASQ_OK;
+}
+
+fasq_status gemv_grouped_launch(const fasq_layer* const* Ls_, int nl, const __half* x, int B, void* const* ys,
+                                fasq_dtype yt, uint32_t flags, cudaStream_t st) {
+    if (nl < 1 || nl > kMaxGroup) return FASQ_E_UNSUPPORTED;
+    for (int l = 1; l < nl; ++l)
+        if (Ls_[l]->F_in != Ls_[0]->F_in || Ls_[l]->d != Ls_[0]->d) return FASQ_E_SHAPE;
     const int NB = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;
-    GemvPlan pl = plan_gemv(L, NB);
+    GemvPlan pl = plan_gemv(Ls_, nl, NB);
     GemvParams p{};
-    p.idx = L->idx;
-    p.cbimg = L->cbimg;
+    p.nl = nl;
     p.x = x;
-    p.y = y;
-    p.F_in = (int)L->F_in;
-    p.F_out = (int)L->F_out;
-    p.F_out_pad = L->F_out_pad;
-    p.N_ss = L->N_ss;
-    p.n_groups = L->n_groups;
-    p.C = L->C;
+    p.F_in = (int)Ls_[0]->F_in;
     p.B = B;
-    p.ksplit = pl.ksplit;
     p.y_f32 = yt == FASQ_F32;
     p.gmax = pl.gmax;
-    if (pl.ksplit > 1) {
-        std::lock_guard<std::mutex> lk(g_mu);
-        const int64_t need = (int64_t)pl.ksplit * B * L->F_out_pad * (int64_t)sizeof(float);
-        if (need > L->ws_bytes || pl.row_tiles > L->n_tickets) {
-            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-            cudaStreamIsCapturing(st, &cs);
-            if (cs != cudaStreamCaptureStatusNone) {
-                set_error("fasq_gemv: split-K workspace must be sized by one uncaptured call with this B first");
-                return FASQ_E_ARG;
-            }
-            FASQ_CUDA_TRY(cudaStreamSynchronize(st));
-            if (L->ws) cudaFree(L->ws);
-            if (L->tickets) cudaFree(L->tickets);
-            L->ws = nullptr;
-            L->tickets = nullptr;
-            L->ws_bytes = 0;
-            L->n_tickets = 0;
-            const int64_t wsb = std::max<int64_t>(need, (int64_t)pl.ksplit * 2 * L->F_out_pad * 4);
-            if (cudaMalloc(&L->ws, (size_t)wsb) != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
-            const int nt = std::max(pl.row_tiles, 64);
-            if (cudaMalloc(&L->tickets, (size_t)nt * sizeof(unsigned long long)) != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
-            FASQ_CUDA_TRY(cudaMemset(L->tickets, 0, (size_t)nt * sizeof(unsigned long long)));
-            L->ws_bytes = wsb;
-            L->n_tickets = nt;
-        }
+    int cta = 0;
+    for (int l = 0; l < nl; ++l) {
+        fasq_layer* L = const_cast<fasq_layer*>(Ls_[l]);   // workspace only; the PQ data is immutable
+        fasq_status s = ensure_workspace(L, pl.ksplit[l], pl.row_tiles[l], B, st);
+        if (s != FASQ_OK) return s;
+        GemvLayerArgs& a = p.L[l];
+        a.idx = L->idx;
+        a.cbimg = L->cbimg;
+        a.y = ys[l];
+        a.partial = L->ws;
+        a.arrive = reinterpret_cast<unsigned long long*>(L->tickets);
+        a.F_out = (int)L->F_out;
+        a.F_out_pad = L->F_out_pad;
+        a.N_ss = L->N_ss;
+        a.n_groups = L->n_groups;
+        a.C = L->C;
+        a.ksplit = pl.ksplit[l];
+        a.cta_begin = cta;
+        cta += pl.row_tiles[l] * pl.ksplit[l];
     }
-    p.partial = L->ws;
-    p.arrive = reinterpret_cast<unsigned long long*>(L->tickets);
     fasq_status s;
-    switch (L->d) {
+    switch (Ls_[0]->d) {
         case 1: s = dispatch_nb<1>(NB, p, pl, flags, st); break;
         case 2: s = dispatch_nb<2>(NB, p, pl, flags, st); break;
         case 4: s = dispatch_nb<4>(NB, p, pl, flags, st); break;
@@ -461,6 +543,12 @@ fasq_status gemv_launch(const fasq_layer* L_, const __half* x, int B, void* y, f
     }
     if (s == FASQ_OK) set_launch_count(1);
     return s;
+}
+
+fasq_status gemv_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt, uint32_t flags,
+                        cudaStream_t st) {
+    void* ys[1] = {y};
+    return gemv_grouped_launch(&L, 1, x, B, ys, yt, flags, st);
 }
 
 }  // namespace fasq

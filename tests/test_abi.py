@@ -17,8 +17,11 @@ def _declared():
 
 @pytest.fixture(scope="module")
 def fasq():
-    from paper_2605_04084_b200 import build
-    build.build()
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("fasq_build", os.path.join(ROOT, "paper_2605_04084_b200", "build.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    b.build()
     import paper_2605_04084_b200 as F
     return F
 

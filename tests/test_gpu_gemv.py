@@ -184,3 +184,21 @@ def test_errors(F):
     with pytest.raises(F.FasqError) as e:
         F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), 63, 1)
     assert e.value.code == -2
+
+
+def test_gemv_grouped_matches_separate(F, oracle_lib):
+    shapes = [(4096, 1024), (1024, 1024), (1024, 1024)]
+    x = synth.activation(1, 1024, seed=31)
+    layers, refs = [], []
+    for i, (fo, fi) in enumerate(shapes):
+        cb, idx = synth.random_layer(fo, fi, 2, 256, seed=40 + i)
+        layers.append(_import(F, cb, idx, fi, 1))
+        refs.append(oracle_lib.gemv(cb, idx, x))
+    ys = F.gemv_grouped(layers, torch.from_numpy(x).cuda(), flags=F.FLAG_PDL)
+    torch.cuda.synchronize()
+    for y, ref in zip(ys, refs):
+        ok, info = parity_ok(y.cpu().numpy(), ref, x, 1024)
+        assert ok, info
+    with pytest.raises(F.FasqError):
+        cb, idx = synth.random_layer(64, 512, 2, 16, seed=1)
+        F.gemv_grouped([layers[0], _import(F, cb, idx, 512, 1)], torch.from_numpy(x).cuda())
