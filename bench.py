@@ -161,44 +161,44 @@ class DecodeStep:
         self.launches = 0
 
     def _gather(self, name):
-        import torch.distributed as dist
+        """Row-shard all-gather over NCCL (paper_2605_04084_b200.shard)."""
         if self.world == 1:
             return self.bufs[name]
-        out = self.bufs[name + "_full"]
-        dist.all_gather_into_tensor(out.view(-1), self.bufs[name].view(-1), group=self.pg)
-        return out
+        from paper_2605_04084_b200 import shard
+        return shard.gather_rows(self.bufs[name], self.bufs[name + "_full"], group=self.pg)
 
-    def run(self, flags=0, grouped=True):
+    def run(self, flags=0, prefetch=None):
         """q/k/v (same input) and gate/up (same input) are separately packed
-        layers launched together with fasq_gemv_grouped."""
+        layers launched together with fasq_gemv_grouped; each launch
+        names the next one so it can warm L2 during its tail."""
         import paper_2605_04084_b200 as F
+        if prefetch is None:
+            prefetch = os.environ.get("FASQ_BENCH_PREFETCH", "1") == "1"
         n = 0
         h = self.h
-        for layers in self.blocks:
-            if grouped:
-                F.gemv_grouped([layers[k] for k in ("q_proj", "k_proj", "v_proj")], h,
-                               outs=[self.bufs[k] for k in ("q_proj", "k_proj", "v_proj")], flags=flags)
-                n += F.last_launch_count()
+        nb = len(self.blocks)
+        names = [("q_proj", "k_proj", "v_proj"), ("o_proj",), ("gate_proj", "up_proj"), ("down_proj",)]
+        seq = [(b, i) for b in range(nb) for i in range(4)]
+        srcs = {}
+        for pos, (b, i) in enumerate(seq):
+            layers = self.blocks[b]
+            nxt = None
+            if prefetch and pos + 1 < len(seq):
+                b2, i2 = seq[pos + 1]
+                nxt = [self.blocks[b2][k] for k in names[i2]]
+            if i == 0:
+                x = h
+            elif i == 1:
+                x = self._gather("q_proj")
+            elif i == 2:
+                x = self._gather("o_proj")
             else:
-                for name in ("q_proj", "k_proj", "v_proj"):
-                    F.gemv(layers[name], h, out=self.bufs[name], flags=flags)
-                    n += F.last_launch_count()
-            q = self._gather("q_proj")
-            F.gemv(layers["o_proj"], q, out=self.bufs["o_proj"], flags=flags)
+                x = self._gather("gate_proj")
+            F.gemv_grouped([layers[k] for k in names[i]], x, outs=[self.bufs[k] for k in names[i]],
+                           flags=flags, next_layers=nxt)
             n += F.last_launch_count()
-            o = self._gather("o_proj")
-            if grouped:
-                F.gemv_grouped([layers["gate_proj"], layers["up_proj"]], o,
-                               outs=[self.bufs["gate_proj"], self.bufs["up_proj"]], flags=flags)
-                n += F.last_launch_count()
-            else:
-                for name in ("gate_proj", "up_proj"):
-                    F.gemv(layers[name], o, out=self.bufs[name], flags=flags)
-                    n += F.last_launch_count()
-            g = self._gather("gate_proj")
-            F.gemv(layers["down_proj"], g, out=self.bufs["down_proj"], flags=flags)
-            n += F.last_launch_count()
-            h = self._gather("down_proj")
+            if i == 3:
+                h = self._gather("down_proj")
         self.out = h
         self.launches = n
         return h
@@ -247,37 +247,51 @@ def timed(graph, steps, warmup, rank, world, pg=None):
 # ----------------------------------------------------------------------------
 # CPU oracle baseline (bounded sample)
 # ----------------------------------------------------------------------------
-def oracle_decode_rate(budget_s: float = 15.0):
-    """Oracle fp64 reconstruct-then-multiply GEMV on a row sample of each
-    Llama layer shape, extrapolated to a full decode step.  Returns
-    (tok/s, threads, sample description, seconds spent)."""
-    import numpy as np
+class OracleSampler:
+    """CPU oracle baseline on a bounded sample: the fp64 reconstruct-then-
+    multiply GEMV (oracle/) on the first `rows` rows of one seeded layer of
+    each Llama-3-8B shape, extrapolated per row to the 224-layer decode step."""
 
-    import oracle
-    import synth
-    lib_threads = oracle.num_threads()
-    t_start = time.perf_counter()
-    per_row = {}
-    shapes = sorted({(fo, fi) for (_, fo, fi) in synth.LLAMA3_8B_LAYERS})
-    sample_rows = 1024
-    for (fo, fi) in shapes:
-        cb, idx = synth.random_layer(fo, fi, D, C, seed=7)
-        x = synth.activation(1, fi, seed=1)
-        rows = min(sample_rows, fo)
-        oracle.gemv(cb, idx, x, rows=(0, 64))               # warm
-        t0 = time.perf_counter()
-        reps = 0
-        while True:
-            oracle.gemv(cb, idx, x, rows=(0, rows))
-            reps += 1
-            if time.perf_counter() - t0 > budget_s / (2 * len(shapes)) or reps >= 50:
-                break
-        per_row[(fo, fi)] = (time.perf_counter() - t0) / (reps * rows)
-    step_s = synth.LLAMA3_8B_BLOCKS * sum(per_row[(fo, fi)] * fo for (_, fo, fi) in synth.LLAMA3_8B_LAYERS)
-    spent = time.perf_counter() - t_start
-    sample = ("oracle fp64 GEMV (reconstruct-then-multiply) on the first %d rows of each Llama-3-8B "
-              "layer shape, repeated for ~%.0f s, extrapolated to 224 layers" % (sample_rows, budget_s))
-    return 1.0 / step_s, lib_threads, sample, spent
+    def __init__(self):
+        import oracle
+        import synth
+        self.oracle = oracle
+        self.shapes = sorted({(fo, fi) for (_, fo, fi) in synth.LLAMA3_8B_LAYERS})
+        self.layers = {}
+        for (fo, fi) in self.shapes:
+            cb, idx = synth.random_layer(min(fo, 4096), fi, D, C, seed=7)   # rows beyond the sample unused
+            self.layers[(fo, fi)] = (cb, idx, synth.activation(1, fi, seed=1))
+        self.threads = oracle.num_threads()
+
+    def step(self, rows: int):
+        """One sampled step; returns (estimated full-step seconds, seconds spent)."""
+        import synth
+        t_all = time.perf_counter()
+        per_row = {}
+        for key, (cb, idx, x) in self.layers.items():
+            r = min(rows, idx.shape[1])
+            t0 = time.perf_counter()
+            self.oracle.gemv(cb, idx, x, rows=(0, r))
+            per_row[key] = (time.perf_counter() - t0) / r
+        est = synth.LLAMA3_8B_BLOCKS * sum(per_row[(fo, fi)] * fo for (_, fo, fi) in synth.LLAMA3_8B_LAYERS)
+        return est, time.perf_counter() - t_all
+
+    def calibrate(self, budget_s: float):
+        """Rows per step so one sampled step costs about budget_s."""
+        _, dt = self.step(64)
+        return max(16, min(4096, int(64 * budget_s / max(dt, 1e-3))))
+
+    def describe(self, rows):
+        return ("oracle fp64 GEMV (reconstruct-then-multiply) on the first %d rows of one seeded layer "
+                "of each Llama-3-8B shape (d=2, C=256, B=1), time per row extrapolated to the 224 "
+                "layers of one decode step" % rows)
+
+
+def oracle_decode_rate(budget_s: float = 15.0):
+    s = OracleSampler()
+    rows = s.calibrate(budget_s)
+    est, spent = s.step(rows)
+    return 1.0 / est, s.threads, s.describe(rows), spent
 
 
 # ----------------------------------------------------------------------------
@@ -332,27 +346,25 @@ def pack_time():
 
 # ----------------------------------------------------------------------------
 def run_reference(args, rank, world):
-    """--impl reference: the oracle on the host cores (bounded sample)."""
+    """--impl reference: the CPU oracle on the host cores, each step a bounded
+    sample of the same workload (whole run ~2 minutes for any K)."""
     if rank != 0:
         return
-    rates = []
-    spent_total = 0.0
-    threads = None
-    sample = None
+    sampler = OracleSampler()
+    per_step = max(0.05, min(2.0, 120.0 / max(1, args.steps + args.warmup)))
+    rows = sampler.calibrate(per_step)
     for _ in range(args.warmup):
-        oracle_decode_rate(budget_s=3.0)
-    for _ in range(args.steps):
-        r, threads, sample, spent = oracle_decode_rate(budget_s=max(3.0, 60.0 / max(args.steps, 1)))
-        rates.append(r)
-        spent_total += spent
-    v = statistics.median(rates)
+        sampler.step(rows)
+    ests = [sampler.step(rows)[0] for _ in range(args.steps)]
+    v = 1.0 / statistics.median(ests)
     line = {"metric": METRIC, "value": v, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "llama3-8b-pq-decode-d2-C256-b1 (oracle, sampled rows)",
+            "config": {"workload": "llama3-8b-pq-decode-d2-C256-b1 (CPU oracle, sampled rows)",
                        "global_batch": 1, "seq_len": 1, "parallelism": "host-cores"},
-            "cpu_baseline": {"value": v, "unit": "tok/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "tok/s", "cores": sampler.threads, "kind": "oracle",
+                             "sample": sampler.describe(rows)},
             "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -365,8 +377,6 @@ def main():
     ap.add_argument("--impl", default="fasq", choices=["fasq", "reference"])
     ap.add_argument("--no-side", action="store_true", help="skip prefill/pack/cpu side measurements")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -374,6 +384,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    args.warmup = max(args.warmup, 3)
 
     import torch
     import torch.distributed as dist

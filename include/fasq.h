@@ -146,9 +146,13 @@ fasq_status fasq_gemv_ex(const fasq_layer* layer, const void* x_dev, int32_t B, 
 /* Grouped decode GEMV: n (1..4) layers that share the input x (q/k/v or
  * gate/up of a transformer block -- each packed separately) in ONE
  * launch: ys[l] = W_hat_l . x.  All layers must have the same F_in and d
- * (FASQ_E_SHAPE otherwise).  Same numerics as n separate fasq_gemv calls. */
+ * (FASQ_E_SHAPE otherwise).  Same numerics as n separate fasq_gemv calls.
+ * `next_layers` (may be NULL, n_next 0..4) names the layers of the NEXT
+ * grouped GEMV of a decode chain: the kernel warms L2 with their first
+ * stages while it finishes (a performance hint only; results unchanged). */
 fasq_status fasq_gemv_grouped(const fasq_layer* const* layers, int32_t n, const void* x_dev, int32_t B,
-                              void* const* ys_dev, fasq_dtype y_dtype, uint32_t flags, void* stream);
+                              void* const* ys_dev, fasq_dtype y_dtype, uint32_t flags,
+                              const fasq_layer* const* next_layers, int32_t n_next, void* stream);
 
 /* Same product with HOST buffers (end-to-end path): copies x_host (fp16
  * [B][F_in], ideally pinned) to the device, runs fasq_gemv and copies y back

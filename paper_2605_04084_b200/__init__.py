@@ -74,7 +74,8 @@ def _load():
     L.fasq_gemv.argtypes = [vp, vp, i32, vp, i32, vp]
     L.fasq_gemv_ex.argtypes = [vp, vp, i32, vp, i32, u32, vp]
     L.fasq_gemv_host.argtypes = [vp, vp, i32, vp, i32, vp]
-    L.fasq_gemv_grouped.argtypes = [ctypes.POINTER(vp), i32, vp, i32, ctypes.POINTER(vp), i32, u32, vp]
+    L.fasq_gemv_grouped.argtypes = [ctypes.POINTER(vp), i32, vp, i32, ctypes.POINTER(vp), i32, u32,
+                                    ctypes.POINTER(vp), i32, vp]
     L.fasq_gemm.argtypes = [vp, vp, i64, vp, i32, i32, vp]
     L.fasq_status_string.restype = ctypes.c_char_p
     L.fasq_last_error_message.restype = ctypes.c_char_p
@@ -195,8 +196,10 @@ def gemv(layer: Layer, x: torch.Tensor, out: torch.Tensor | None = None,
 
 
 def gemv_grouped(layers, x: torch.Tensor, outs=None, out_dtype: torch.dtype = torch.float32,
-                 flags: int = 0, stream=None):
-    """One launch for up to 4 layers sharing x (e.g. q/k/v): returns [y_l]."""
+                 flags: int = 0, next_layers=None, stream=None):
+    """One launch for up to 4 layers sharing x (e.g. q/k/v): returns [y_l].
+    ``next_layers``: layers of the next launch in a decode chain (L2 warm-up
+    hint only)."""
     x = _cuda(x, torch.float16, "x")
     if x.dim() == 1:
         x = x.unsqueeze(0)
@@ -207,7 +210,10 @@ def gemv_grouped(layers, x: torch.Tensor, outs=None, out_dtype: torch.dtype = to
     hs = (ctypes.c_void_p * n)(*[L.handle.value for L in layers])
     ys = (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs])
     yt = FASQ_F32 if outs[0].dtype == torch.float32 else FASQ_F16
-    _check(lib.fasq_gemv_grouped(hs, n, x.data_ptr(), B, ys, yt, flags, _stream(stream)))
+    nn = len(next_layers) if next_layers else 0
+    nx = (ctypes.c_void_p * max(nn, 1))(*([L.handle.value for L in next_layers] if nn else [None]))
+    _check(lib.fasq_gemv_grouped(hs, n, x.data_ptr(), B, ys, yt, flags, nx if nn else None, nn,
+                                 _stream(stream)))
     return outs
 
 

@@ -194,15 +194,17 @@ fasq_status fasq_gemv_ex(const fasq_layer* L, const void* x_dev, int32_t B, void
 }
 
 fasq_status fasq_gemv_grouped(const fasq_layer* const* layers, int32_t n, const void* x_dev, int32_t B,
-                              void* const* ys_dev, fasq_dtype yt, uint32_t flags, void* stream) {
+                              void* const* ys_dev, fasq_dtype yt, uint32_t flags,
+                              const fasq_layer* const* next_layers, int32_t n_next, void* stream) {
     if (!layers || !x_dev || !ys_dev || n < 1) return FASQ_E_ARG;
     if (n > 4) return FASQ_E_UNSUPPORTED;
     for (int i = 0; i < n; ++i)
         if (!layers[i] || !ys_dev[i]) return FASQ_E_ARG;
     if (B < 1 || B > 8) return FASQ_E_UNSUPPORTED;
     if (yt != FASQ_F16 && yt != FASQ_F32) return FASQ_E_ARG;
+    if (n_next < 0 || n_next > 4) return FASQ_E_ARG;
     return gemv_grouped_launch(layers, n, static_cast<const __half*>(x_dev), B, ys_dev, yt, flags,
-                               (cudaStream_t)stream);
+                               (cudaStream_t)stream, next_layers, next_layers ? n_next : 0);
 }
 
 fasq_status fasq_gemv(const fasq_layer* L, const void* x_dev, int32_t B, void* y_dev, fasq_dtype yt,

@@ -98,7 +98,8 @@ fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t
 fasq_status gemv_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt,
                         uint32_t flags, cudaStream_t st);
 fasq_status gemv_grouped_launch(const fasq_layer* const* Ls, int nl, const __half* x, int B, void* const* ys,
-                                fasq_dtype yt, uint32_t flags, cudaStream_t st);
+                                fasq_dtype yt, uint32_t flags, cudaStream_t st,
+                                const fasq_layer* const* next = nullptr, int n_next = 0);
 fasq_status gemm_lut_launch(const fasq_layer* L, const __half* X, int64_t M, void* Y,
                             fasq_dtype yt, cudaStream_t st);
 fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void* Y,
@@ -205,6 +206,10 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
+}
+// L2 prefetch through the TMA engine (no SMEM destination).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"(bytes) : "memory");
 }
 // Programmatic dependent launch.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

@@ -4,7 +4,7 @@
 // the 5th-gen tensor cores WITHOUT materialising W_hat in HBM: the paper's
 // future-work direction (1), "a pipelined reconstruction kernel that rebuilds
 // FP16 weight tiles in parallel with tensor-core GEMM, avoiding full
-// materialization".  Per CTA tile (128 tokens x 256 weight rows)
+// materialization".  Per CTA tile (2 x 128 tokens x 256 weight rows)
 // and per K-chunk of 64 input features (= one group of 32 subspaces at d=2):
 //
 //   producer warp : TMA 2-D load of the X tile (128B swizzle) + bulk copies of
@@ -13,10 +13,12 @@
 //                   the SMEM codebook image in the conflict-free rotated order
 //                   (same layout as the GEMV) and store them into the B tile
 //                   in the UMMA K-major SWIZZLE_128B layout (never to HBM);
-//   MMA thread    : 4 x tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256,
-//                   K=16) into a TMEM fp32 accumulator; tcgen05.commit frees
-//                   the stage;
-//   epilogue      : tcgen05.ld (32x32b) -> fp32/fp16 -> Y.
+//   MMA thread    : 2 token tiles x 4 x tcgen05.mma.cta_group::1.kind::f16
+//                   (M=128, N=256, K=16) into two TMEM fp32 accumulators (all
+//                   512 columns) -- each expanded B tile feeds 256 tokens, which
+//                   halves the expansion + codebook SMEM traffic per FLOP;
+//                   tcgen05.commit frees the stage;
+//   epilogue      : tcgen05.ld (32x32b) -> fp32/fp16 -> Y (8 warps).
 #include <cuda.h>
 
 #include <mutex>
@@ -27,7 +29,8 @@ namespace fasq {
 
 namespace {
 
-constexpr int TC_M = 128;          // tokens per CTA tile (UMMA M)
+constexpr int TC_M = 128;          // tokens per accumulator (UMMA M)
+constexpr int TC_MT = 2;           // token tiles per CTA sharing each expanded B tile (2 TMEM accumulators)
 constexpr int TC_N = 256;          // weight rows per CTA tile (UMMA N)
 constexpr int TC_K = 64;           // K elements per chunk (one 128B swizzle atom row)
 constexpr int TC_STAGES = 2;
@@ -69,7 +72,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     // 1024-B alignment for the swizzled tiles
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int C = p.C;
-    constexpr int A_BYTES = TC_M * TC_K * 2;      // 16 KiB
+    constexpr int A_TILE = TC_M * TC_K * 2;       // 16 KiB per token tile
+    constexpr int A_BYTES = TC_MT * A_TILE;       // per stage
     constexpr int B_BYTES = TC_N * TC_K * 2;      // 32 KiB
     constexpr int IDX_BYTES = TC_N * 32;          // 8 KiB
     const int CB_BYTES = C * 128;                 // per stage: [C][32][4]
@@ -83,7 +87,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n0 = blockIdx.x * TC_N;          // weight-row tile
-    const int m0 = blockIdx.y * TC_M;          // token tile
+    const int m0 = blockIdx.y * TC_M * TC_MT;  // first token of this CTA's token tiles
     const int nk = p.n_groups;
     const uint32_t bar0 = dev::smem_u32(bars);
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
@@ -102,7 +106,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     }
     if (warp == 1) {   // TMEM allocation (256 fp32 columns = the 128x256 accumulator)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     :: "r"(dev::smem_u32(tmem_slot)), "n"(256));
+                     :: "r"(dev::smem_u32(tmem_slot)), "n"(256 * TC_MT));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -121,7 +125,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
             if (i >= TC_STAGES) dev::mbar_wait(empty_bar(s), ((i / TC_STAGES) + 1) & 1);
             if (lane == 0) {
                 dev::mbar_arrive_expect_tx(full_bar(s), (uint32_t)A_BYTES + idx_bytes + (uint32_t)CB_BYTES);
-                tma_load_2d(dev::smem_u32(sA + s * A_BYTES), &xmap, i * TC_K, m0, full_bar(s));
+#pragma unroll
+                for (int t = 0; t < TC_MT; ++t)
+                    tma_load_2d(dev::smem_u32(sA + s * A_BYTES + t * A_TILE), &xmap, i * TC_K, m0 + t * TC_M,
+                                full_bar(s));
                 dev::bulk_g2s(dev::smem_u32(sI + s * IDX_BYTES), p.idx + ((size_t)i * p.F_out_pad + n0) * 32,
                               idx_bytes, full_bar(s));
                 dev::bulk_g2s(cb_u + (uint32_t)s * (uint32_t)CB_BYTES, p.cbimg + (size_t)i * CB_BYTES,
@@ -139,18 +146,21 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
             dev::mbar_wait(bfull_bar(s), ph);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (lane == 0) {
-                const uint32_t a_base = dev::smem_u32(sA + s * A_BYTES);
                 const uint32_t b_base = dev::smem_u32(sB + s * B_BYTES);
 #pragma unroll
-                for (int kk = 0; kk < TC_K / 16; ++kk) {
-                    const uint64_t ad = umma_desc_sw128(a_base + kk * 32);
-                    const uint64_t bd = umma_desc_sw128(b_base + kk * 32);
-                    const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-                    asm volatile(
-                        "{.reg .pred p;\n\t"
-                        "setp.ne.b32 p, %4, 0;\n\t"
-                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
-                        :: "r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                for (int t = 0; t < TC_MT; ++t) {
+                    const uint32_t a_base = dev::smem_u32(sA + s * A_BYTES + t * A_TILE);
+#pragma unroll
+                    for (int kk = 0; kk < TC_K / 16; ++kk) {
+                        const uint64_t ad = umma_desc_sw128(a_base + kk * 32);
+                        const uint64_t bd = umma_desc_sw128(b_base + kk * 32);
+                        const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{.reg .pred p;\n\t"
+                            "setp.ne.b32 p, %4, 0;\n\t"
+                            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
+                            :: "r"(tmem + (uint32_t)(t * TC_N)), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                    }
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                              :: "r"(empty_bar(s)) : "memory");
@@ -203,15 +213,16 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
             if (lane == 0) dev::mbar_arrive(bfull_bar(s));
         }
         // ------------------------------ epilogue -------------------------------
-        if (ew < 4) {
+        {
             dev::mbar_wait(accum_bar, 0);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int q = warp & 3;                    // TMEM lane quarter this warp may access
-            const int m = m0 + q * 32 + lane;          // token
+            const int t = ew >> 2;                     // accumulator (token tile) this warp drains
+            const int m = m0 + t * TC_M + q * 32 + lane;   // token
 #pragma unroll 1
             for (int c0 = 0; c0 < TC_N; c0 += 32) {
                 uint32_t r[32];
-                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(t * TC_N + c0);
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
                     "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -269,7 +280,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(256));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(256 * TC_MT));
     }
 }
 
@@ -292,7 +303,7 @@ PFN_encodeTiled get_encode() {
 }
 
 size_t tc_smem_bytes(int C) {
-    return 1024 + (size_t)TC_STAGES * (TC_M * TC_K * 2 + TC_N * TC_K * 2 + TC_N * 32 + (size_t)C * 128) + 8 * 16 + 16;
+    return 1024 + (size_t)TC_STAGES * (TC_MT * TC_M * TC_K * 2 + TC_N * TC_K * 2 + TC_N * 32 + (size_t)C * 128) + 8 * 16 + 16;
 }
 
 }  // namespace
@@ -332,7 +343,7 @@ fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void
     if (lim < smem) { set_error("gemm_tc: SMEM"); return FASQ_E_UNSUPPORTED; }
     // F_out_pad rows of the idx table exist; tiles past F_out_pad read beyond it
     // -> require the row tile grid to stay within F_out_pad (pad logic below).
-    dim3 grid((unsigned)((L->F_out_pad + TC_N - 1) / TC_N), (unsigned)((M + TC_M - 1) / TC_M));
+    dim3 grid((unsigned)((L->F_out_pad + TC_N - 1) / TC_N), (unsigned)((M + TC_M * TC_MT - 1) / (TC_M * TC_MT)));
     k_gemm_tc<<<grid, TC_THREADS, smem, st>>>(map, p);
     FASQ_CUDA_TRY(cudaGetLastError());
     set_launch_count(1);

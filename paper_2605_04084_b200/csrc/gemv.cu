@@ -42,13 +42,15 @@ struct GemvLayerArgs {
     const uint8_t* cbimg;   // [n_groups][C][32][E]
     void* y;                // [B][F_out]
     float* partial;         // [ksplit][B][F_out_pad] (ksplit > 1)
-    unsigned long long* arrive;   // [row_tiles] monotonically increasing arrival counters
+    unsigned long long* arrive;   // [row_tiles] u32 monotonically increasing arrival counters (8-B slots)
     int F_out, F_out_pad, N_ss, n_groups, C, ksplit, cta_begin;
 };
 
 struct GemvParams {
     GemvLayerArgs L[kMaxGroup];   // layers sharing x (grouped launch); CTAs are laid out layer-major
     int nl;
+    GemvLayerArgs N[kMaxGroup];   // the NEXT launch of a decode chain (L2 prefetch hints), nn = 0: none
+    int nn;
     const __half* x;        // [B][F_in]
     int F_in, B, y_f32;
     int gmax;               // max groups per CTA (x staging capacity)
@@ -125,6 +127,28 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
                 dev::bulk_g2s(cb_u + (uint32_t)slot * CBB, la.cbimg + (size_t)g * CBB, CBB, full);
                 dev::bulk_g2s(idx_u + (uint32_t)slot * R * 32u, la.idx + ((size_t)g * F_out_pad + r0) * 32,
                               idx_chunk, full);
+                if (i == ng - 1 && p.nn > 0) {
+                    // this CTA's counterpart in the next launch of the chain: warm L2 with
+                    // its first ST stages while this layer finishes (HBM is otherwise idle
+                    // during the split-K merge and the kernel boundary)
+                    int nli = 0;
+                    for (int l = 1; l < p.nn; ++l)
+                        if ((int)blockIdx.x >= p.N[l].cta_begin) nli = l;
+                    const GemvLayerArgs& na = p.N[nli];
+                    const int nlocal = (int)blockIdx.x - na.cta_begin;
+                    const int nrt = nlocal / na.ksplit, nks = nlocal % na.ksplit;
+                    const int nr0 = nrt * R;
+                    if (nlocal >= 0 && nr0 < na.F_out_pad) {
+                        const int nrows = min(R, na.F_out_pad - nr0);
+                        const int ng0 = (int)((int64_t)nks * na.n_groups / na.ksplit);
+                        const int ng1 = (int)((int64_t)(nks + 1) * na.n_groups / na.ksplit);
+                        const uint32_t ncbb = (uint32_t)na.C * 32u * E;
+                        for (int gg = ng0; gg < min(ng1, ng0 + ST); ++gg) {
+                            dev::bulk_prefetch_l2(na.cbimg + (size_t)gg * ncbb, ncbb);
+                            dev::bulk_prefetch_l2(na.idx + ((size_t)gg * na.F_out_pad + nr0) * 32, (uint32_t)nrows * 32u);
+                        }
+                    }
+                }
             }
         }
         __syncwarp();
@@ -284,8 +308,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
         return;
     }
     // split-K: publish partials, wait until every CTA of this row tile has
-    // published (all CTAs are co-resident: grid <= #SMs, 1 CTA/SM, and PDL
-    // dependents launch only after every CTA started), then each CTA sums a
+    // published (all CTAs are co-resident: grid <= #SMs, and PDL dependents
+    // launch only after every CTA started), then each CTA sums a
     // 1/ksplit slice of the tile's rows over ks = 0..ksplit-1 in fixed order
     // (deterministic; the paper's merge is atomicAdd).
 #pragma unroll
@@ -296,38 +320,44 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
         for (int b = 0; b < NB; ++b)
             if (b < p.B) __stcg(&la.partial[((size_t)ks * p.B + b) * F_out_pad + row], acc[q][b]);
     }
-    __threadfence();
+    // arrive: bar.sync orders this CTA's partial stores before thread 0's
+    // release-RMW (cumulative, no full fence).
     asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
     if (threadIdx.x == 0) {
-        unsigned long long* ctr = la.arrive + rt;
-        const unsigned long long old = atomicAdd(ctr, 1ull);
-        const unsigned long long target = (old / (unsigned long long)ksplit + 1ull) * (unsigned long long)ksplit;
-        unsigned long long v;
+        // monotonically increasing arrival counter: this launch's CTAs of the
+        // tile take the values [n*ksplit, (n+1)*ksplit)
+        unsigned* cnt = reinterpret_cast<unsigned*>(la.arrive + rt);
+        unsigned old;
+        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+        const unsigned target = (old / (unsigned)ksplit + 1u) * (unsigned)ksplit;
+        unsigned v;
         do {
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
-        } while (v < target);
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+        } while ((int)(v - target) < 0);
     }
     asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
+    // merge: this CTA owns rows [rb, re) of the tile; sum ks = 0..ksplit-1 in order
     const int rows_per = (rows_valid + ksplit - 1) / ksplit;
     const int rb = ks * rows_per, re = min(rows_valid, rb + rows_per);
-    const int n_out = (re > rb ? re - rb : 0) * p.B;
     const size_t kstride = (size_t)p.B * F_out_pad;
-    for (int t = threadIdx.x; t < n_out; t += NW * 32) {
-        const int b = t / (re - rb), row = r0 + rb + t % (re - rb);
-        const float* src = la.partial + (size_t)b * F_out_pad + row;
-        float sum = 0.f;
-        int k = 0;
-        for (; k + 8 <= ksplit; k += 8) {
-            float v[8];
+    for (int rr = rb + (int)threadIdx.x; rr < re; rr += NW * 32) {
+        const int row = r0 + rr;
+        for (int b = 0; b < p.B; ++b) {
+            const float* src = la.partial + (size_t)b * F_out_pad + row;
+            float sum = 0.f;
+            int k = 0;
+            for (; k + 8 <= ksplit; k += 8) {
+                float v[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(k + u) * kstride);
+                for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(k + u) * kstride);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) sum += v[u];
-        }
-        for (; k < ksplit; ++k) sum += __ldcg(src + (size_t)k * kstride);
-        if (row < F_out) {
-            if (p.y_f32) reinterpret_cast<float*>(la.y)[(size_t)b * F_out + row] = sum;
-            else reinterpret_cast<__half*>(la.y)[(size_t)b * F_out + row] = __float2half_rn(sum);
+                for (int u = 0; u < 8; ++u) sum += v[u];
+            }
+            for (; k < ksplit; ++k) sum += __ldcg(src + (size_t)k * kstride);
+            if (row < F_out) {
+                if (p.y_f32) reinterpret_cast<float*>(la.y)[(size_t)b * F_out + row] = sum;
+                else reinterpret_cast<__half*>(la.y)[(size_t)b * F_out + row] = __float2half_rn(sum);
+            }
         }
     }
 }
@@ -499,8 +529,24 @@ static fasq_status ensure_workspace(fasq_layer* L, int ksplit, int row_tiles, in
     return FASQ_OK;
 }
 
+static void fill_layer_args(GemvLayerArgs* a, const fasq_layer* L, const GemvPlan& pl, int l, int cta, void* y) {
+    a->idx = L->idx;
+    a->cbimg = L->cbimg;
+    a->y = y;
+    a->partial = L->ws;
+    a->arrive = reinterpret_cast<unsigned long long*>(L->tickets);
+    a->F_out = (int)L->F_out;
+    a->F_out_pad = L->F_out_pad;
+    a->N_ss = L->N_ss;
+    a->n_groups = L->n_groups;
+    a->C = L->C;
+    a->ksplit = pl.ksplit[l];
+    a->cta_begin = cta;
+}
+
 fasq_status gemv_grouped_launch(const fasq_layer* const* Ls_, int nl, const __half* x, int B, void* const* ys,
-                                fasq_dtype yt, uint32_t flags, cudaStream_t st) {
+                                fasq_dtype yt, uint32_t flags, cudaStream_t st, const fasq_layer* const* next,
+                                int n_next) {
     if (nl < 1 || nl > kMaxGroup) return FASQ_E_UNSUPPORTED;
     for (int l = 1; l < nl; ++l)
         if (Ls_[l]->F_in != Ls_[0]->F_in || Ls_[l]->d != Ls_[0]->d) return FASQ_E_SHAPE;
@@ -518,20 +564,24 @@ fasq_status gemv_grouped_launch(const fasq_layer* const* Ls_, int nl, const __ha
         fasq_layer* L = const_cast<fasq_layer*>(Ls_[l]);   // workspace only; the PQ data is immutable
         fasq_status s = ensure_workspace(L, pl.ksplit[l], pl.row_tiles[l], B, st);
         if (s != FASQ_OK) return s;
-        GemvLayerArgs& a = p.L[l];
-        a.idx = L->idx;
-        a.cbimg = L->cbimg;
-        a.y = ys[l];
-        a.partial = L->ws;
-        a.arrive = reinterpret_cast<unsigned long long*>(L->tickets);
-        a.F_out = (int)L->F_out;
-        a.F_out_pad = L->F_out_pad;
-        a.N_ss = L->N_ss;
-        a.n_groups = L->n_groups;
-        a.C = L->C;
-        a.ksplit = pl.ksplit[l];
-        a.cta_begin = cta;
+        fill_layer_args(&p.L[l], L, pl, l, cta, ys[l]);
         cta += pl.row_tiles[l] * pl.ksplit[l];
+    }
+    // L2-prefetch hints for the next launch of a decode chain (same tiling family)
+    if (next && n_next > 0 && n_next <= kMaxGroup) {
+        bool ok = true;
+        for (int l = 0; l < n_next; ++l) ok = ok && next[l] && next[l]->d == Ls_[0]->d;
+        if (ok) {
+            GemvPlan pn = plan_gemv(next, n_next, NB);
+            if (pn.R == pl.R && pn.st == pl.st) {
+                int c2 = 0;
+                for (int l = 0; l < n_next; ++l) {
+                    fill_layer_args(&p.N[l], next[l], pn, l, c2, nullptr);
+                    c2 += pn.row_tiles[l] * pn.ksplit[l];
+                }
+                p.nn = n_next;
+            }
+        }
     }
     fasq_status s;
     switch (Ls_[0]->d) {

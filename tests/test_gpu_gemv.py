@@ -202,3 +202,17 @@ def test_gemv_grouped_matches_separate(F, oracle_lib):
     with pytest.raises(F.FasqError):
         cb, idx = synth.random_layer(64, 512, 2, 16, seed=1)
         F.gemv_grouped([layers[0], _import(F, cb, idx, 512, 1)], torch.from_numpy(x).cuda())
+
+
+def test_gemv_grouped_prefetch_hint_no_effect_on_results(F, oracle_lib):
+    cb, idx = synth.random_layer(4096, 1024, 2, 256, seed=51)
+    cb2, idx2 = synth.random_layer(1024, 4096, 2, 256, seed=52)
+    L1 = _import(F, cb, idx, 1024, 1)
+    L2 = _import(F, cb2, idx2, 4096, 1)
+    x = synth.activation(1, 1024, seed=53)
+    a = F.gemv_grouped([L1], torch.from_numpy(x).cuda(), next_layers=[L2], flags=F.FLAG_PDL)[0]
+    b = F.gemv_grouped([L1], torch.from_numpy(x).cuda())[0]
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    ok, info = parity_ok(a.cpu().numpy(), oracle_lib.gemv(cb, idx, x), x, 1024)
+    assert ok, info
