@@ -146,62 +146,93 @@ def layer_bytes(world: int):
 
 
 class DecodeStep:
-    """One decode step = 224 chained PQ GEMVs (+ all-gathers when sharded)."""
+    """One decode step = the 224 chained PQ GEMVs of the 32 blocks, launched as
+    4 grouped launches per block: {q,k,v} (same input), o, {gate,up} (same
+    input), down -- every layer packed separately.
+
+    N = 1: every launch writes FASQ_ACC_I64 accumulators (exact int64 fixed
+    point, deterministic, no split-K merge phase); the consumer rounds them to
+    fp16 x on load; each launch zeroes the accumulators of the launch two
+    steps back (no longer read) and warms L2 with the next launch's first
+    stages.  N > 1: rows are sharded and each chain output (q, o, gate, down)
+    is materialised as fp16 and all-gathered over NCCL."""
+
+    NAMES = [("q_proj", "k_proj", "v_proj"), ("o_proj",), ("gate_proj", "up_proj"), ("down_proj",)]
+    FEEDS = {1: "q_proj", 2: "o_proj", 3: "gate_proj"}   # launch i reads this output of launch i-1
 
     def __init__(self, blocks, rank, world, pg=None):
         import torch
+        import synth
         self.blocks, self.rank, self.world, self.pg = blocks, rank, world, pg
         dev = torch.device("cuda", torch.cuda.current_device())
         f16 = torch.float16
         self.h = torch.zeros((1, 4096), dtype=f16, device=dev)
-        self.bufs = {}
-        for (name, fo, fi) in __import__("synth").LLAMA3_8B_LAYERS:
-            self.bufs[name] = torch.empty((1, fo // world), dtype=f16, device=dev)
-            self.bufs[name + "_full"] = torch.empty((1, fo), dtype=f16, device=dev)
+        self.shapes = {n: (fo, fi) for (n, fo, fi) in synth.LLAMA3_8B_LAYERS}
+        self.seq = [(b, i) for b in range(len(blocks)) for i in range(4)]
+        self.acc_mode = world == 1
+        if self.acc_mode:
+            # one int64 accumulator slab per launch position of the token
+            self.acc = []
+            for (b, i) in self.seq:
+                tot = sum(self.shapes[n][0] for n in self.NAMES[i])
+                slab = torch.zeros((tot,), dtype=torch.int64, device=dev)
+                outs, off = {}, 0
+                for n in self.NAMES[i]:
+                    fo = self.shapes[n][0]
+                    outs[n] = slab[off:off + fo].view(1, fo)
+                    off += fo
+                self.acc.append((slab, outs))
+            self.out_f16 = torch.empty((1, 4096), dtype=f16, device=dev)
+        else:
+            self.bufs = {}
+            for (name, fo, fi) in synth.LLAMA3_8B_LAYERS:
+                self.bufs[name] = torch.empty((1, fo // world), dtype=f16, device=dev)
+                self.bufs[name + "_full"] = torch.empty((1, fo), dtype=f16, device=dev)
         self.launches = 0
 
     def _gather(self, name):
         """Row-shard all-gather over NCCL (paper_2605_04084_b200.shard)."""
-        if self.world == 1:
-            return self.bufs[name]
         from paper_2605_04084_b200 import shard
         return shard.gather_rows(self.bufs[name], self.bufs[name + "_full"], group=self.pg)
 
     def run(self, flags=0, prefetch=None):
-        """q/k/v (same input) and gate/up (same input) are separately packed
-        layers launched together with fasq_gemv_grouped; each launch
-        names the next one so it can warm L2 during its tail."""
         import paper_2605_04084_b200 as F
         if prefetch is None:
             prefetch = os.environ.get("FASQ_BENCH_PREFETCH", "1") == "1"
         n = 0
-        h = self.h
-        nb = len(self.blocks)
-        names = [("q_proj", "k_proj", "v_proj"), ("o_proj",), ("gate_proj", "up_proj"), ("down_proj",)]
-        seq = [(b, i) for b in range(nb) for i in range(4)]
-        srcs = {}
-        for pos, (b, i) in enumerate(seq):
-            layers = self.blocks[b]
+        T = len(self.seq)
+        for pos, (b, i) in enumerate(self.seq):
+            layers = [self.blocks[b][k] for k in self.NAMES[i]]
             nxt = None
-            if prefetch and pos + 1 < len(seq):
-                b2, i2 = seq[pos + 1]
-                nxt = [self.blocks[b2][k] for k in names[i2]]
-            if i == 0:
-                x = h
-            elif i == 1:
-                x = self._gather("q_proj")
-            elif i == 2:
-                x = self._gather("o_proj")
+            if prefetch and pos + 1 < T:
+                b2, i2 = self.seq[pos + 1]
+                nxt = [self.blocks[b2][k] for k in self.NAMES[i2]]
+            if self.acc_mode:
+                if pos == 0:
+                    x = self.h
+                else:
+                    x = self.acc[pos - 1][1][self.FEEDS[i] if i else "down_proj"]
+                F.gemv_grouped(layers, x, outs=[self.acc[pos][1][k] for k in self.NAMES[i]], flags=flags,
+                               next_layers=nxt, zero=self.acc[(pos - 2) % T][0])
+                n += F.last_launch_count()
             else:
-                x = self._gather("gate_proj")
-            F.gemv_grouped([layers[k] for k in names[i]], x, outs=[self.bufs[k] for k in names[i]],
-                           flags=flags, next_layers=nxt)
+                if pos == 0:
+                    x = self.h
+                elif i == 0:
+                    x = self._gather("down_proj")
+                else:
+                    x = self._gather(self.FEEDS[i])
+                F.gemv_grouped(layers, x, outs=[self.bufs[k] for k in self.NAMES[i]], flags=flags,
+                               next_layers=nxt)
+                n += F.last_launch_count()
+        if self.acc_mode:
+            F.acc_convert(self.acc[T - 1][1]["down_proj"], out=self.out_f16)
             n += F.last_launch_count()
-            if i == 3:
-                h = self._gather("down_proj")
-        self.out = h
+            self.out = self.out_f16
+        else:
+            self.out = self._gather("down_proj")
         self.launches = n
-        return h
+        return self.out
 
 
 def capture(fn):

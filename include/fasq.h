@@ -65,7 +65,14 @@ typedef enum {
     FASQ_E_OOM = -8               /* device allocation failed                            */
 } fasq_status;
 
-typedef enum { FASQ_F16 = 0, FASQ_F32 = 1 } fasq_dtype;
+typedef enum {
+    FASQ_F16 = 0,
+    FASQ_F32 = 1,
+    FASQ_ACC_I64 = 2   /* int64 fixed point in units of 2^-32.  As an OUTPUT of the GEMVs the
+                          result is ADDED into the caller-zeroed buffer with integer atomics
+                          (associative -> deterministic, no split-K merge phase); as an INPUT
+                          (FASQ_FLAG_X_ACC) it is rounded to fp16 once per element. */
+} fasq_dtype;
 
 typedef enum {
     FASQ_GEMM_AUTO = 0,      /* library picks (EXPAND_TC when shapes allow) */
@@ -79,6 +86,9 @@ typedef enum {
                                  kernel on the stream finishes (x is read only after
                                  griddepcontrol.wait).  Only valid when the layer was
                                  NOT written by the immediately preceding kernel. */
+
+#define FASQ_FLAG_X_ACC 2u   /* x_dev holds FASQ_ACC_I64 values [B][F_in] (a previous GEMV's
+                                 accumulator output) instead of fp16 */
 
 /* Pack parameters (Alg. 1). */
 typedef struct {
@@ -143,16 +153,32 @@ fasq_status fasq_gemv(const fasq_layer* layer, const void* x_dev, int32_t B, voi
 fasq_status fasq_gemv_ex(const fasq_layer* layer, const void* x_dev, int32_t B, void* y_dev,
                          fasq_dtype y_dtype, uint32_t flags, void* stream);
 
+/* Options of fasq_gemv_grouped (all fields may be zero / NULL). */
+typedef struct {
+    uint32_t flags;                          /* FASQ_FLAG_PDL | FASQ_FLAG_X_ACC                     */
+    const fasq_layer* const* next_layers;    /* layers of the NEXT launch of a decode chain: the
+                                                kernel warms L2 with their first stages while it
+                                                finishes (performance hint; results unchanged)   */
+    int32_t n_next;                          /* 0..4                                               */
+    void* zero_dev;                          /* side job: zero this device range during the launch
+                                                (e.g. the FASQ_ACC_I64 outputs of the launch two
+                                                steps back in a chain); must not alias this
+                                                launch's inputs or outputs                          */
+    int64_t zero_bytes;                      /* multiple of 8                                      */
+} fasq_gemv_opts;
+
 /* Grouped decode GEMV: n (1..4) layers that share the input x (q/k/v or
  * gate/up of a transformer block -- each packed separately) in ONE
  * launch: ys[l] = W_hat_l . x.  All layers must have the same F_in and d
- * (FASQ_E_SHAPE otherwise).  Same numerics as n separate fasq_gemv calls.
- * `next_layers` (may be NULL, n_next 0..4) names the layers of the NEXT
- * grouped GEMV of a decode chain: the kernel warms L2 with their first
- * stages while it finishes (a performance hint only; results unchanged). */
+ * (FASQ_E_SHAPE otherwise).  y_dtype FASQ_F16/F32: same numerics as n
+ * separate fasq_gemv calls.  y_dtype FASQ_ACC_I64: ys[l] are int64 [B][F_out]
+ * buffers the result is added to.  opts may be NULL. */
 fasq_status fasq_gemv_grouped(const fasq_layer* const* layers, int32_t n, const void* x_dev, int32_t B,
-                              void* const* ys_dev, fasq_dtype y_dtype, uint32_t flags,
-                              const fasq_layer* const* next_layers, int32_t n_next, void* stream);
+                              void* const* ys_dev, fasq_dtype y_dtype, const fasq_gemv_opts* opts,
+                              void* stream);
+
+/* Converts n FASQ_ACC_I64 values to fp16 / fp32 (out_dtype). */
+fasq_status fasq_acc_convert(const void* acc_dev, int64_t n, void* out_dev, fasq_dtype out_dtype, void* stream);
 
 /* Same product with HOST buffers (end-to-end path): copies x_host (fp16
  * [B][F_in], ideally pinned) to the device, runs fasq_gemv and copies y back

@@ -19,9 +19,11 @@ import torch
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libfasq.so")
 
-FASQ_F16, FASQ_F32 = 0, 1
+FASQ_F16, FASQ_F32, FASQ_ACC_I64 = 0, 1, 2
 GEMM_AUTO, GEMM_LUT, GEMM_EXPAND_TC = 0, 1, 2
 FLAG_PDL = 1
+FLAG_X_ACC = 2
+ACC_SCALE = 2.0 ** 32   # FASQ_ACC_I64 units
 
 _STATUS = {0: "FASQ_OK", -1: "FASQ_E_ARG", -2: "FASQ_E_NONDIVISIBLE", -3: "FASQ_E_CLUSTER_OVERFLOW",
            -4: "FASQ_E_NONFINITE", -5: "FASQ_E_SHAPE", -6: "FASQ_E_UNSUPPORTED", -7: "FASQ_E_CUDA",
@@ -29,7 +31,8 @@ _STATUS = {0: "FASQ_OK", -1: "FASQ_E_ARG", -2: "FASQ_E_NONDIVISIBLE", -3: "FASQ_
 
 # Every symbol include/fasq.h declares (checked by tests/test_abi.py).
 EXPORTED = ["fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
-            "fasq_free", "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_gemv_host", "fasq_gemm",
+            "fasq_free", "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_acc_convert",
+            "fasq_gemv_host", "fasq_gemm",
             "fasq_last_launch_count", "fasq_status_string", "fasq_last_error_message",
             "fasq_abi_version"]
 
@@ -43,6 +46,11 @@ class FasqError(RuntimeError):
 class _PackParams(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int32), ("C", ctypes.c_int32), ("group", ctypes.c_int32),
                 ("iters", ctypes.c_int32), ("seed", ctypes.c_uint64)]
+
+
+class GemvOpts(ctypes.Structure):
+    _fields_ = [("flags", ctypes.c_uint32), ("next_layers", ctypes.POINTER(ctypes.c_void_p)),
+                ("n_next", ctypes.c_int32), ("zero_dev", ctypes.c_void_p), ("zero_bytes", ctypes.c_int64)]
 
 
 class LayerInfo(ctypes.Structure):
@@ -74,14 +82,15 @@ def _load():
     L.fasq_gemv.argtypes = [vp, vp, i32, vp, i32, vp]
     L.fasq_gemv_ex.argtypes = [vp, vp, i32, vp, i32, u32, vp]
     L.fasq_gemv_host.argtypes = [vp, vp, i32, vp, i32, vp]
-    L.fasq_gemv_grouped.argtypes = [ctypes.POINTER(vp), i32, vp, i32, ctypes.POINTER(vp), i32, u32,
-                                    ctypes.POINTER(vp), i32, vp]
+    L.fasq_gemv_grouped.argtypes = [ctypes.POINTER(vp), i32, vp, i32, ctypes.POINTER(vp), i32,
+                                    ctypes.POINTER(GemvOpts), vp]
+    L.fasq_acc_convert.argtypes = [vp, i64, vp, i32, vp]
     L.fasq_gemm.argtypes = [vp, vp, i64, vp, i32, i32, vp]
     L.fasq_status_string.restype = ctypes.c_char_p
     L.fasq_last_error_message.restype = ctypes.c_char_p
     for name in ("fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
-                 "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_gemv_host", "fasq_gemm",
-                 "fasq_last_launch_count",
+                 "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_acc_convert", "fasq_gemv_host",
+                 "fasq_gemm", "fasq_last_launch_count",
                  "fasq_abi_version"):
         getattr(L, name).restype = ctypes.c_int32
     return L
@@ -196,25 +205,46 @@ def gemv(layer: Layer, x: torch.Tensor, out: torch.Tensor | None = None,
 
 
 def gemv_grouped(layers, x: torch.Tensor, outs=None, out_dtype: torch.dtype = torch.float32,
-                 flags: int = 0, next_layers=None, stream=None):
+                 flags: int = 0, next_layers=None, zero: torch.Tensor | None = None, stream=None):
     """One launch for up to 4 layers sharing x (e.g. q/k/v): returns [y_l].
+
+    ``out_dtype=torch.int64`` selects FASQ_ACC_I64 outputs (added into
+    caller-zeroed ``outs``); an int64 ``x`` is read as FASQ_ACC_I64.
     ``next_layers``: layers of the next launch in a decode chain (L2 warm-up
-    hint only)."""
-    x = _cuda(x, torch.float16, "x")
+    hint).  ``zero``: a device tensor to zero during the launch."""
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise TypeError("x must be a CUDA tensor (FASQ has no CPU path)")
+    if x.dtype == torch.int64:
+        flags |= FLAG_X_ACC
+    elif x.dtype != torch.float16:
+        raise TypeError("x must be fp16 or int64 (FASQ_ACC_I64)")
+    x = x.contiguous()
     if x.dim() == 1:
         x = x.unsqueeze(0)
     B = x.shape[0]
     n = len(layers)
     if outs is None:
-        outs = [torch.empty((B, L.F_out), dtype=out_dtype, device=x.device) for L in layers]
+        outs = [torch.zeros((B, L.F_out), dtype=out_dtype, device=x.device) for L in layers]
+    dt = outs[0].dtype
+    yt = FASQ_F32 if dt == torch.float32 else FASQ_F16 if dt == torch.float16 else FASQ_ACC_I64
     hs = (ctypes.c_void_p * n)(*[L.handle.value for L in layers])
     ys = (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs])
-    yt = FASQ_F32 if outs[0].dtype == torch.float32 else FASQ_F16
     nn = len(next_layers) if next_layers else 0
     nx = (ctypes.c_void_p * max(nn, 1))(*([L.handle.value for L in next_layers] if nn else [None]))
-    _check(lib.fasq_gemv_grouped(hs, n, x.data_ptr(), B, ys, yt, flags, nx if nn else None, nn,
-                                 _stream(stream)))
+    opts = GemvOpts(flags, nx if nn else None, nn, zero.data_ptr() if zero is not None else None,
+                    zero.numel() * zero.element_size() if zero is not None else 0)
+    _check(lib.fasq_gemv_grouped(hs, n, x.data_ptr(), B, ys, yt, ctypes.byref(opts), _stream(stream)))
     return outs
+
+
+def acc_convert(acc: torch.Tensor, out: torch.Tensor | None = None, out_dtype=torch.float16, stream=None):
+    """FASQ_ACC_I64 -> fp16/fp32."""
+    acc = _cuda(acc, torch.int64, "acc")
+    if out is None:
+        out = torch.empty(acc.shape, dtype=out_dtype, device=acc.device)
+    yt = FASQ_F32 if out.dtype == torch.float32 else FASQ_F16
+    _check(lib.fasq_acc_convert(acc.data_ptr(), acc.numel(), out.data_ptr(), yt, _stream(stream)))
+    return out
 
 
 def gemv_host(layer: Layer, x_host: torch.Tensor, y_host: torch.Tensor, stream=None) -> torch.Tensor:

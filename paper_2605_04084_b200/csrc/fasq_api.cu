@@ -194,17 +194,32 @@ fasq_status fasq_gemv_ex(const fasq_layer* L, const void* x_dev, int32_t B, void
 }
 
 fasq_status fasq_gemv_grouped(const fasq_layer* const* layers, int32_t n, const void* x_dev, int32_t B,
-                              void* const* ys_dev, fasq_dtype yt, uint32_t flags,
-                              const fasq_layer* const* next_layers, int32_t n_next, void* stream) {
+                              void* const* ys_dev, fasq_dtype yt, const fasq_gemv_opts* opts, void* stream) {
     if (!layers || !x_dev || !ys_dev || n < 1) return FASQ_E_ARG;
     if (n > 4) return FASQ_E_UNSUPPORTED;
     for (int i = 0; i < n; ++i)
         if (!layers[i] || !ys_dev[i]) return FASQ_E_ARG;
     if (B < 1 || B > 8) return FASQ_E_UNSUPPORTED;
-    if (yt != FASQ_F16 && yt != FASQ_F32) return FASQ_E_ARG;
-    if (n_next < 0 || n_next > 4) return FASQ_E_ARG;
-    return gemv_grouped_launch(layers, n, static_cast<const __half*>(x_dev), B, ys_dev, yt, flags,
-                               (cudaStream_t)stream, next_layers, next_layers ? n_next : 0);
+    if (yt != FASQ_F16 && yt != FASQ_F32 && yt != FASQ_ACC_I64) return FASQ_E_ARG;
+    GemvOpts o{};
+    if (opts) {
+        if (opts->n_next < 0 || opts->n_next > 4 || opts->zero_bytes < 0 || (opts->zero_bytes & 7)) return FASQ_E_ARG;
+        o.flags = opts->flags;
+        o.next = opts->next_layers;
+        o.n_next = opts->next_layers ? opts->n_next : 0;
+        o.zero_ptr = opts->zero_dev;
+        o.zero_bytes = opts->zero_dev ? opts->zero_bytes : 0;
+    }
+    o.x_acc = (o.flags & FASQ_FLAG_X_ACC) ? 1 : 0;
+    o.y_acc = yt == FASQ_ACC_I64;
+    return gemv_grouped_launch2(layers, n, x_dev, B, ys_dev, yt == FASQ_ACC_I64 ? FASQ_F32 : yt, o,
+                                (cudaStream_t)stream);
+}
+
+fasq_status fasq_acc_convert(const void* acc_dev, int64_t n, void* out_dev, fasq_dtype out_dtype, void* stream) {
+    if (!acc_dev || !out_dev || n < 0) return FASQ_E_ARG;
+    if (out_dtype != FASQ_F16 && out_dtype != FASQ_F32) return FASQ_E_ARG;
+    return acc_convert_launch(acc_dev, n, out_dev, out_dtype, (cudaStream_t)stream);
 }
 
 fasq_status fasq_gemv(const fasq_layer* L, const void* x_dev, int32_t B, void* y_dev, fasq_dtype yt,

@@ -97,6 +97,17 @@ fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t
 // ---- compute entry points ---------------------------------------------------
 fasq_status gemv_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt,
                         uint32_t flags, cudaStream_t st);
+struct GemvOpts {
+    uint32_t flags = 0;
+    int x_acc = 0, y_acc = 0;
+    void* zero_ptr = nullptr;
+    int64_t zero_bytes = 0;
+    const fasq_layer* const* next = nullptr;
+    int n_next = 0;
+};
+fasq_status gemv_grouped_launch2(const fasq_layer* const* Ls, int nl, const void* x, int B, void* const* ys,
+                                 fasq_dtype yt, const GemvOpts& o, cudaStream_t st);
+fasq_status acc_convert_launch(const void* acc, int64_t n, void* out, fasq_dtype yt, cudaStream_t st);
 fasq_status gemv_grouped_launch(const fasq_layer* const* Ls, int nl, const __half* x, int B, void* const* ys,
                                 fasq_dtype yt, uint32_t flags, cudaStream_t st,
                                 const fasq_layer* const* next = nullptr, int n_next = 0);

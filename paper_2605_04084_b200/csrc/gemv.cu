@@ -46,9 +46,20 @@ struct GemvLayerArgs {
     int F_out, F_out_pad, N_ss, n_groups, C, ksplit, cta_begin;
 };
 
+// Fixed-point accumulation mode (FASQ_ACC_I64): partial sums are converted
+// to int64 in units of 2^-32 (exact scaling, one RN rounding each) and
+// red.add'ed -- integer addition is associative, so the result is
+// deterministic whatever the arrival order, with no split-K merge phase.
+constexpr float kAccScale = 4294967296.0f;      // 2^32
+constexpr double kAccInv = 1.0 / 4294967296.0;   // 2^-32
+
 struct GemvParams {
     GemvLayerArgs L[kMaxGroup];   // layers sharing x (grouped launch); CTAs are laid out layer-major
     int nl;
+    int x_acc;                    // 1: x is int64 [B][F_in] in units of 2^-32 (FASQ_ACC_I64)
+    int y_acc;                    // 1: ys are int64 [B][F_out] accumulators (red.add, caller-zeroed)
+    unsigned long long* zero_ptr; // side job: zero these words (not used by this launch)
+    long long zero_words;
     GemvLayerArgs N[kMaxGroup];   // the NEXT launch of a decode chain (L2 prefetch hints), nn = 0: none
     int nn;
     const __half* x;        // [B][F_in]
@@ -174,7 +185,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
                 const int e64 = (t / NB) % 64;
                 const int gl = t / (NB * 64);
                 const int ss = (g_begin + gl) * 32 + (e64 & 31);
-                if (b < p.B && ss < la.N_ss) {
+                if (b < p.B && ss < la.N_ss && p.x_acc) {
+                    const long long* src = reinterpret_cast<const long long*>(p.x) + (size_t)b * p.F_in + (size_t)ss * D;
+#pragma unroll
+                    for (int e = 0; e < D; ++e) {
+                        const long long v = __ldcg(src + e);
+                        const uint32_t h = __half_as_ushort(__double2half((double)v * kAccInv));
+                        w[u][e >> 1] |= h << (16 * (e & 1));
+                    }
+                } else if (b < p.B && ss < la.N_ss) {
                     const __half* src = p.x + (size_t)b * p.F_in + (size_t)ss * D;
                     if (D == 1) {
                         w[u][0] = (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(src));
@@ -293,6 +312,26 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     }
 
     // ------------------------------ epilogue --------------------------------
+    if (p.zero_words > 0) {       // side job (e.g. the accumulators of the launch two steps back)
+        const long long per = (p.zero_words + gridDim.x - 1) / gridDim.x;
+        const long long zb = per * blockIdx.x, ze = min(p.zero_words, zb + per);
+        for (long long i = zb + threadIdx.x; i < ze; i += NW * 32) p.zero_ptr[i] = 0ull;
+    }
+    if (p.y_acc) {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+            const int row = r0 + warp_row0 + q * 32 + lane;
+            if (warp_row0 + q * 32 >= rows_valid || row >= F_out) continue;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                if (b >= p.B) continue;
+                const long long v = __float2ll_rn(acc[q][b] * kAccScale);
+                unsigned long long* dst = reinterpret_cast<unsigned long long*>(la.y) + (size_t)b * F_out + row;
+                asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(dst), "l"(v) : "memory");
+            }
+        }
+        return;
+    }
     if (ksplit == 1) {
 #pragma unroll
         for (int q = 0; q < RPL; ++q) {
@@ -447,7 +486,7 @@ static fasq_status dispatch_nb(int NB, const GemvParams& p, const GemvPlan& pl, 
 // left for the NEXT launch's prefetch under PDL.  CTAs are shared between the
 // layers in proportion to their index bytes.  Env FASQ_GEMV_CFG="rpl,nw,stages"
 // overrides the default tiling (tuning only).
-static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB) {
+static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB, bool spin_merge = true) {
     GemvPlan pl{};
     pl.nw = 8;
     pl.rpl = NB <= 2 ? 4 : (NB == 4 ? 2 : 1);
@@ -480,8 +519,9 @@ static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB) {
         pl.ksplit[l] = ks;
         total += pl.row_tiles[l] * ks;
     }
-    // co-residency: shrink the largest K-split until all CTAs fit on the SMs
-    while (total > sms) {
+    // co-residency (the dense-output merge spins on its peers): shrink the
+    // largest K-split until all CTAs fit on the SMs
+    while (spin_merge && total > sms) {
         int lm = -1;
         for (int l = 0; l < nl; ++l)
             if (pl.ksplit[l] > 1 && (lm < 0 || pl.ksplit[l] * pl.row_tiles[l] > pl.ksplit[lm] * pl.row_tiles[lm])) lm = l;
@@ -547,12 +587,29 @@ static void fill_layer_args(GemvLayerArgs* a, const fasq_layer* L, const GemvPla
 fasq_status gemv_grouped_launch(const fasq_layer* const* Ls_, int nl, const __half* x, int B, void* const* ys,
                                 fasq_dtype yt, uint32_t flags, cudaStream_t st, const fasq_layer* const* next,
                                 int n_next) {
+    GemvOpts o{};
+    o.flags = flags;
+    o.next = next;
+    o.n_next = n_next;
+    return gemv_grouped_launch2(Ls_, nl, x, B, ys, yt, o, st);
+}
+
+fasq_status gemv_grouped_launch2(const fasq_layer* const* Ls_, int nl, const void* x_, int B, void* const* ys,
+                                 fasq_dtype yt, const GemvOpts& o, cudaStream_t st) {
+    const __half* x = static_cast<const __half*>(x_);
+    const uint32_t flags = o.flags;
+    const fasq_layer* const* next = o.next;
+    const int n_next = o.n_next;
     if (nl < 1 || nl > kMaxGroup) return FASQ_E_UNSUPPORTED;
     for (int l = 1; l < nl; ++l)
         if (Ls_[l]->F_in != Ls_[0]->F_in || Ls_[l]->d != Ls_[0]->d) return FASQ_E_SHAPE;
     const int NB = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;
-    GemvPlan pl = plan_gemv(Ls_, nl, NB);
+    GemvPlan pl = plan_gemv(Ls_, nl, NB, !o.y_acc);
     GemvParams p{};
+    p.x_acc = o.x_acc;
+    p.y_acc = o.y_acc;
+    p.zero_ptr = static_cast<unsigned long long*>(o.zero_ptr);
+    p.zero_words = o.zero_ptr ? o.zero_bytes / 8 : 0;
     p.nl = nl;
     p.x = x;
     p.F_in = (int)Ls_[0]->F_in;
@@ -562,8 +619,10 @@ fasq_status gemv_grouped_launch(const fasq_layer* const* Ls_, int nl, const __ha
     int cta = 0;
     for (int l = 0; l < nl; ++l) {
         fasq_layer* L = const_cast<fasq_layer*>(Ls_[l]);   // workspace only; the PQ data is immutable
-        fasq_status s = ensure_workspace(L, pl.ksplit[l], pl.row_tiles[l], B, st);
-        if (s != FASQ_OK) return s;
+        if (!o.y_acc) {
+            fasq_status s = ensure_workspace(L, pl.ksplit[l], pl.row_tiles[l], B, st);
+            if (s != FASQ_OK) return s;
+        }
         fill_layer_args(&p.L[l], L, pl, l, cta, ys[l]);
         cta += pl.row_tiles[l] * pl.ksplit[l];
     }
@@ -572,7 +631,7 @@ fasq_status gemv_grouped_launch(const fasq_layer* const* Ls_, int nl, const __ha
         bool ok = true;
         for (int l = 0; l < n_next; ++l) ok = ok && next[l] && next[l]->d == Ls_[0]->d;
         if (ok) {
-            GemvPlan pn = plan_gemv(next, n_next, NB);
+            GemvPlan pn = plan_gemv(next, n_next, NB, !o.y_acc);
             if (pn.R == pl.R && pn.st == pl.st) {
                 int c2 = 0;
                 for (int l = 0; l < n_next; ++l) {
@@ -593,6 +652,23 @@ fasq_status gemv_grouped_launch(const fasq_layer* const* Ls_, int nl, const __ha
     }
     if (s == FASQ_OK) set_launch_count(1);
     return s;
+}
+
+__global__ void k_acc_convert(const long long* __restrict__ acc, int64_t n, void* out, int f32) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double v = (double)acc[i] * kAccInv;
+    if (f32) reinterpret_cast<float*>(out)[i] = (float)v;
+    else reinterpret_cast<__half*>(out)[i] = __double2half(v);
+}
+
+fasq_status acc_convert_launch(const void* acc, int64_t n, void* out, fasq_dtype yt, cudaStream_t st) {
+    if (n <= 0) return FASQ_OK;
+    k_acc_convert<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(static_cast<const long long*>(acc), n, out,
+                                                                 yt == FASQ_F32);
+    FASQ_CUDA_TRY(cudaGetLastError());
+    set_launch_count(1);
+    return FASQ_OK;
 }
 
 fasq_status gemv_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt, uint32_t flags,

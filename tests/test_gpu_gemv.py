@@ -216,3 +216,31 @@ def test_gemv_grouped_prefetch_hint_no_effect_on_results(F, oracle_lib):
     assert torch.equal(a, b)
     ok, info = parity_ok(a.cpu().numpy(), oracle_lib.gemv(cb, idx, x), x, 1024)
     assert ok, info
+
+
+def test_gemv_acc_mode_and_chain(F, oracle_lib):
+    """FASQ_ACC_I64 outputs (int64 fixed point, red.add) are deterministic and
+    match the oracle; an ACC output fed as the next layer's x matches the
+    oracle chain; the zero side job clears its range."""
+    cb1, idx1 = synth.random_layer(2048, 1024, 2, 256, seed=61)
+    cb2, idx2 = synth.random_layer(1024, 2048, 2, 256, seed=62)
+    L1 = _import(F, cb1, idx1, 1024, 1)
+    L2 = _import(F, cb2, idx2, 2048, 1)
+    x = synth.activation(1, 1024, seed=63)
+    xt = torch.from_numpy(x).cuda()
+    junk = torch.full((1000,), 7, dtype=torch.int64, device="cuda")
+    a1 = F.gemv_grouped([L1], xt, out_dtype=torch.int64, zero=junk)[0]
+    a1b = F.gemv_grouped([L1], xt, out_dtype=torch.int64)[0]
+    torch.cuda.synchronize()
+    assert torch.equal(a1, a1b)
+    assert int(junk.abs().sum()) == 0
+    y1 = F.acc_convert(a1, out_dtype=torch.float32).cpu().numpy()
+    ref1 = oracle_lib.gemv(cb1, idx1, x)
+    ok, info = parity_ok(y1, ref1, x, 1024)
+    assert ok, info
+    a2 = F.gemv_grouped([L2], a1, out_dtype=torch.int64)[0]      # x = ACC input
+    y2 = F.acc_convert(a2, out_dtype=torch.float32).cpu().numpy()
+    x2 = F.acc_convert(a1, out_dtype=torch.float16).cpu().numpy()  # the fp16 x the kernel used
+    ref2 = oracle_lib.gemv(cb2, idx2, x2)
+    ok, info = parity_ok(y2, ref2, x2, 2048)
+    assert ok, info
