@@ -462,6 +462,10 @@ static fasq_status dispatch_cfg(const GemvParams& p, const GemvPlan& pl, uint32_
     FASQ_GEMV_CFG_CASE(4, 4, 4)
     FASQ_GEMV_CFG_CASE(2, 8, 4)
     FASQ_GEMV_CFG_CASE(8, 8, 2)
+    FASQ_GEMV_CFG_CASE(4, 16, 2)
+    FASQ_GEMV_CFG_CASE(1, 16, 2)
+    FASQ_GEMV_CFG_CASE(4, 4, 2)
+    FASQ_GEMV_CFG_CASE(2, 16, 2)
     FASQ_GEMV_CFG_CASE(2, 8, 1)
 #undef FASQ_GEMV_CFG_CASE
     set_error("gemv: no kernel instantiated for this tiling");
@@ -488,8 +492,8 @@ static fasq_status dispatch_nb(int NB, const GemvParams& p, const GemvPlan& pl, 
 // overrides the default tiling (tuning only).
 static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB, bool spin_merge = true) {
     GemvPlan pl{};
-    pl.nw = 8;
-    pl.rpl = NB <= 2 ? 4 : (NB == 4 ? 2 : 1);
+    pl.nw = 16;
+    pl.rpl = NB <= 2 ? 2 : 1;
     pl.st = 3;
     if (const char* e = getenv("FASQ_GEMV_CFG")) {
         int a = 0, b = 0, c = 0;
@@ -504,7 +508,10 @@ static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB, bool spin
         if (pl.rpl > 1) pl.rpl = 1;
     }
     pl.R = 32 * pl.nw * pl.rpl;
-    const int sms = num_sms();
+    int sms = num_sms();
+    if (!spin_merge) {   // ACC outputs: no co-residency requirement; FASQ_GEMV_OCC = CTAs per SM to plan for
+        if (const char* e = getenv("FASQ_GEMV_OCC")) sms *= std::max(1, atoi(e));
+    }
     double W = 0;
     for (int l = 0; l < nl; ++l) W += (double)Ls[l]->F_out_pad * Ls[l]->n_groups;
     int total = 0;
