@@ -150,7 +150,9 @@ class DecodeStep:
     4 grouped launches per block: {q,k,v} (same input), o, {gate,up} (same
     input), down -- every layer packed separately.
 
-    N = 1: every launch writes FASQ_ACC_I64 accumulators (exact int64 fixed
+    N = 1 (default): the 128 grouped launches run as ONE persistent kernel
+    (fasq_chain_*); FASQ_BENCH_CHAIN=0 uses one launch per step instead, where
+    every launch writes FASQ_ACC_I64 accumulators (exact int64 fixed
     point, deterministic, no split-K merge phase); the consumer rounds them to
     fp16 x on load; each launch zeroes the accumulators of the launch two
     steps back (no longer read) and warms L2 with the next launch's first
@@ -170,7 +172,18 @@ class DecodeStep:
         self.shapes = {n: (fo, fi) for (n, fo, fi) in synth.LLAMA3_8B_LAYERS}
         self.seq = [(b, i) for b in range(len(blocks)) for i in range(4)]
         self.acc_mode = world == 1
-        if self.acc_mode:
+        self.chain = None
+        if self.acc_mode and os.environ.get("FASQ_BENCH_CHAIN", "1") == "1":
+            # the whole token as ONE persistent kernel (fasq_chain_*)
+            import paper_2605_04084_b200 as F
+            steps = []
+            for (b, i) in self.seq:
+                pos = len(steps)
+                src = None if pos == 0 else (pos - 1, 0)
+                steps.append(([blocks[b][k] for k in self.NAMES[i]], src))
+            self.chain = F.Chain(steps, B=1)
+            self.out_f16 = torch.empty((1, 4096), dtype=f16, device=dev)
+        elif self.acc_mode:
             # one int64 accumulator slab per launch position of the token
             self.acc = []
             for (b, i) in self.seq:
@@ -201,6 +214,14 @@ class DecodeStep:
             prefetch = os.environ.get("FASQ_BENCH_PREFETCH", "1") == "1"
         n = 0
         T = len(self.seq)
+        if self.chain is not None:
+            self.chain.run(self.h)
+            n += F.last_launch_count()
+            self.chain.output(T - 1, 0, out=self.out_f16)
+            n += 1
+            self.out = self.out_f16
+            self.launches = n
+            return self.out
         for pos, (b, i) in enumerate(self.seq):
             layers = [self.blocks[b][k] for k in self.NAMES[i]]
             nxt = None

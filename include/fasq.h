@@ -180,6 +180,42 @@ fasq_status fasq_gemv_grouped(const fasq_layer* const* layers, int32_t n, const 
 /* Converts n FASQ_ACC_I64 values to fp16 / fp32 (out_dtype). */
 fasq_status fasq_acc_convert(const void* acc_dev, int64_t n, void* out_dev, fasq_dtype out_dtype, void* stream);
 
+/* ---- decode chain (persistent executor) --------------------------------- */
+
+/* One step of a decode chain: 1..4 layers sharing one input (q/k/v, o,
+ * gate/up, down ...).  input_step = -1: the chain's external fp16 input x;
+ * otherwise the output of layer `input_layer` of the earlier step
+ * `input_step` (its F_out must equal this step's F_in). */
+typedef struct {
+    const fasq_layer* const* layers;
+    int32_t n_layers;
+    int32_t input_step;
+    int32_t input_layer;
+} fasq_chain_step;
+
+typedef struct fasq_chain fasq_chain; /* opaque */
+
+/* Plans a chain of grouped decode GEMVs (all layers: same d, B in 1..8) for
+ * ONE persistent kernel (one CTA per SM, cooperative launch): every CTA
+ * streams the codebook/index stages of all its steps through its SMEM ring
+ * without draining at step boundaries, and waits on a grid-wide counter only
+ * before reading a step's x.  Outputs are FASQ_ACC_I64 accumulators kept by
+ * the chain (same numerics as chained fasq_gemv_grouped calls with ACC
+ * outputs).  The layers must outlive the chain.  Synchronises `stream`. */
+fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int32_t B, void* stream,
+                              fasq_chain** out);
+
+/* Runs the whole chain on x_dev (fp16 [B][F_in of the external-input steps]):
+ * one memset node (accumulators + counter) and one kernel launch; graph
+ * capturable.  A chain instance must not run concurrently with itself. */
+fasq_status fasq_chain_run(fasq_chain* chain, const void* x_dev, void* stream);
+
+/* Output of layer `layer` of step `step` after a run, as fp16 / fp32 /
+ * FASQ_ACC_I64 [B][F_out] (valid until the next run). */
+fasq_status fasq_chain_output(const fasq_chain* chain, int32_t step, int32_t layer, void* y_dev,
+                              fasq_dtype dtype, void* stream);
+void fasq_chain_free(fasq_chain* chain);   /* synchronises the device; NULL is a no-op */
+
 /* Same product with HOST buffers (end-to-end path): copies x_host (fp16
  * [B][F_in], ideally pinned) to the device, runs fasq_gemv and copies y back
  * to y_host.  Synchronous: returns after y_host is written. */

@@ -32,6 +32,7 @@ _STATUS = {0: "FASQ_OK", -1: "FASQ_E_ARG", -2: "FASQ_E_NONDIVISIBLE", -3: "FASQ_
 # Every symbol include/fasq.h declares (checked by tests/test_abi.py).
 EXPORTED = ["fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
             "fasq_free", "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_acc_convert",
+            "fasq_chain_create", "fasq_chain_run", "fasq_chain_output", "fasq_chain_free",
             "fasq_gemv_host", "fasq_gemm",
             "fasq_last_launch_count", "fasq_status_string", "fasq_last_error_message",
             "fasq_abi_version"]
@@ -51,6 +52,11 @@ class _PackParams(ctypes.Structure):
 class GemvOpts(ctypes.Structure):
     _fields_ = [("flags", ctypes.c_uint32), ("next_layers", ctypes.POINTER(ctypes.c_void_p)),
                 ("n_next", ctypes.c_int32), ("zero_dev", ctypes.c_void_p), ("zero_bytes", ctypes.c_int64)]
+
+
+class _ChainStep(ctypes.Structure):
+    _fields_ = [("layers", ctypes.POINTER(ctypes.c_void_p)), ("n_layers", ctypes.c_int32),
+                ("input_step", ctypes.c_int32), ("input_layer", ctypes.c_int32)]
 
 
 class LayerInfo(ctypes.Structure):
@@ -85,11 +91,17 @@ def _load():
     L.fasq_gemv_grouped.argtypes = [ctypes.POINTER(vp), i32, vp, i32, ctypes.POINTER(vp), i32,
                                     ctypes.POINTER(GemvOpts), vp]
     L.fasq_acc_convert.argtypes = [vp, i64, vp, i32, vp]
+    L.fasq_chain_create.argtypes = [ctypes.POINTER(_ChainStep), i32, i32, vp, pp]
+    L.fasq_chain_run.argtypes = [vp, vp, vp]
+    L.fasq_chain_output.argtypes = [vp, i32, i32, vp, i32, vp]
+    L.fasq_chain_free.argtypes = [vp]
+    L.fasq_chain_free.restype = None
     L.fasq_gemm.argtypes = [vp, vp, i64, vp, i32, i32, vp]
     L.fasq_status_string.restype = ctypes.c_char_p
     L.fasq_last_error_message.restype = ctypes.c_char_p
     for name in ("fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
                  "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_acc_convert", "fasq_gemv_host",
+                 "fasq_chain_create", "fasq_chain_run", "fasq_chain_output",
                  "fasq_gemm", "fasq_last_launch_count",
                  "fasq_abi_version"):
         getattr(L, name).restype = ctypes.c_int32
@@ -245,6 +257,53 @@ def acc_convert(acc: torch.Tensor, out: torch.Tensor | None = None, out_dtype=to
     yt = FASQ_F32 if out.dtype == torch.float32 else FASQ_F16
     _check(lib.fasq_acc_convert(acc.data_ptr(), acc.numel(), out.data_ptr(), yt, _stream(stream)))
     return out
+
+
+class Chain:
+    """Persistent decode-chain executor (fasq_chain_*): a list of steps, each
+    ``(layers, input)`` with ``input = None`` (the external x) or
+    ``(step, layer)`` (an earlier step's output)."""
+
+    def __init__(self, steps, B: int = 1, stream=None):
+        self._keep = []
+        arr = (_ChainStep * len(steps))()
+        for i, (layers, src) in enumerate(steps):
+            hs = (ctypes.c_void_p * len(layers))(*[L.handle.value for L in layers])
+            self._keep.append((hs, list(layers)))
+            arr[i].layers = hs
+            arr[i].n_layers = len(layers)
+            arr[i].input_step, arr[i].input_layer = (-1, 0) if src is None else src
+        out = ctypes.c_void_p()
+        _check(lib.fasq_chain_create(arr, len(steps), B, _stream(stream), ctypes.byref(out)))
+        self._h = out
+        self.B = B
+        self.steps = [(list(l), s) for (l, s) in steps]
+
+    def run(self, x: torch.Tensor, stream=None):
+        x = _cuda(x, torch.float16, "x")
+        _check(lib.fasq_chain_run(self._h, x.data_ptr(), _stream(stream)))
+
+    def output(self, step: int, layer: int = 0, out: torch.Tensor | None = None,
+               out_dtype=torch.float16, stream=None) -> torch.Tensor:
+        F_out = self.steps[step][0][layer].F_out
+        if out is None:
+            out = torch.empty((self.B, F_out), dtype=out_dtype, device="cuda")
+        dt = out.dtype
+        yt = FASQ_F32 if dt == torch.float32 else FASQ_F16 if dt == torch.float16 else FASQ_ACC_I64
+        _check(lib.fasq_chain_output(self._h, step, layer, out.data_ptr(), yt, _stream(stream)))
+        return out
+
+    def free(self):
+        if self._h:
+            lib.fasq_chain_free(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib.fasq_chain_free(self._h)
+        except Exception:
+            pass
 
 
 def gemv_host(layer: Layer, x_host: torch.Tensor, y_host: torch.Tensor, stream=None) -> torch.Tensor:

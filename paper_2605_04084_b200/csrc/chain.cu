@@ -1,0 +1,419 @@
+// chain.cu -- persistent decode-chain executor (sm_100a).
+//
+// A decode token runs the PQ linear layers of a model as a chain of grouped
+// GEMVs (q/k/v, o, gate/up, down per block; every layer packed separately,
+// P:219).  Launching one kernel per step pays, per step, a launch, the first
+// stage's memory latency and a grid-wide completion before the next step may
+// read its x.  This executor runs the whole chain in ONE persistent kernel
+// (one CTA per SM, cooperative launch):
+//
+//  * the per-step work (row tile x K-range of groups, same tiling as gemv.cu)
+//    is planned once on the host into a [steps][CTAs] table of work items;
+//  * the producer warp of every CTA streams the codebook/index stages of ALL
+//    its steps back to back through the SMEM ring -- weights do not depend on
+//    x, so the ring keeps filling while the consumers wait for the previous
+//    step (no pipeline drain at step boundaries);
+//  * consumers wait on a grid-wide arrival counter (release/acquire) only
+//    before reading x; outputs are FASQ_ACC_I64 accumulators (exact int64
+//    fixed point -> deterministic, no split-K merge phase), read by the next
+//    step as x (rounded to fp16 once per element, as in FASQ_FLAG_X_ACC).
+//
+// Numerics are identical to chaining fasq_gemv_grouped calls with FASQ_ACC_I64
+// outputs.
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "fasq_internal.cuh"
+#include "gemv_core.cuh"
+
+struct fasq_chain {
+    int n_steps = 0, B = 0, d = 0, nctas = 0;
+    int rpl = 0, nw = 0, st = 0, R = 0, gmax = 1, maxC = 1;
+    size_t smem = 0;
+    std::vector<int> step_F_out_total;               // per step: sum of F_out of its layers
+    std::vector<std::vector<int64_t>> acc_off;       // per step, per layer: word offset in the arena
+    std::vector<std::vector<int64_t>> acc_Fout;
+    std::vector<int> step_F_in;
+    int ext_F_in = 0;
+    unsigned long long* arena = nullptr;             // [0]: grid counter (16 words), then accumulators
+    int64_t arena_words = 0;
+    void* items = nullptr;                           // device [n_steps][nctas] ChainItem
+    void* phases = nullptr;                          // device [n_steps] ChainPhase
+};
+
+namespace fasq {
+
+namespace {
+
+struct ChainItem {
+    const uint8_t* idx;
+    const uint8_t* cbimg;
+    unsigned long long* y;      // ACC output [B][F_out]
+    int F_out, F_out_pad, N_ss, C;
+    int r0, rows_valid, g_begin, g_end;
+};
+
+struct ChainPhase {
+    const long long* x_acc;     // ACC input (nullptr: the chain's external fp16 x)
+    int F_in, pad;
+};
+
+struct ChainParams {
+    const ChainItem* items;
+    const ChainPhase* phases;
+    const __half* x_ext;        // [B][F_in of the first step]
+    unsigned* counter;          // grid arrival counter (zeroed per run)
+    int n_steps, nctas, B, gmax, cbb_max;
+};
+
+template <int D, int NB, int RPL, int NW, int ST>
+__global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
+    constexpr int E = D <= 2 ? 4 : 2 * D;
+    constexpr int R = 32 * NW * RPL;
+    constexpr int XG = 64 * NB * E;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* s_cb = smem;                                       // ST * cbb_max
+    uint8_t* s_idx = s_cb + ST * p.cbb_max;                     // ST * R * 32
+    uint8_t* s_x = s_idx + ST * R * 32;                         // gmax * XG
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_x + p.gmax * XG);
+    const uint32_t cb_u = dev::smem_u32(s_cb), idx_u = dev::smem_u32(s_idx), x_u = dev::smem_u32(s_x);
+    const uint32_t full0 = dev::smem_u32(&bars[0]), empty0 = dev::smem_u32(&bars[ST]);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < ST; ++s) {
+            dev::mbar_init(full0 + 8 * s, 1);
+            dev::mbar_init(empty0 + 8 * s, NW);
+        }
+        dev::fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == NW) {
+        // producer: every step's stages, back to back (no dependence on x)
+        if (lane == 0) {
+            int it = 0;
+            for (int ph = 0; ph < p.n_steps; ++ph) {
+                const ChainItem& w = p.items[(size_t)ph * p.nctas + blockIdx.x];
+                if (w.rows_valid <= 0) continue;
+                const uint32_t cbb = (uint32_t)w.C * 32u * E;
+                const uint32_t chunk = (uint32_t)w.rows_valid * 32u;
+                for (int g = w.g_begin; g < w.g_end; ++g, ++it) {
+                    const int slot = it % ST;
+                    if (it >= ST) dev::mbar_wait(empty0 + 8 * slot, ((it / ST) + 1) & 1);
+                    const uint32_t full = full0 + 8 * slot;
+                    dev::mbar_arrive_expect_tx(full, chunk + cbb);
+                    dev::bulk_g2s(cb_u + (uint32_t)slot * (uint32_t)p.cbb_max, w.cbimg + (size_t)g * cbb, cbb, full);
+                    dev::bulk_g2s(idx_u + (uint32_t)slot * R * 32u, w.idx + ((size_t)g * w.F_out_pad + w.r0) * 32,
+                                  chunk, full);
+                }
+            }
+        }
+        __syncwarp();
+        return;
+    }
+
+    core::LaneConsts lc;
+    core::lane_consts(lane, lc);
+    const int warp_row0 = warp * 32 * RPL;
+    int it = 0;
+    for (int ph = 0; ph < p.n_steps; ++ph) {
+        const ChainItem& w = p.items[(size_t)ph * p.nctas + blockIdx.x];
+        const ChainPhase& phs = p.phases[ph];
+        if (ph > 0) {   // every CTA of the previous step has published its outputs
+            if (threadIdx.x == 0) {
+                const unsigned target = (unsigned)ph * (unsigned)p.nctas;
+                unsigned v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.counter) : "memory");
+                } while ((int)(v - target) < 0);
+            }
+            asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
+        }
+        if (w.rows_valid > 0) {
+            const int ng = w.g_end - w.g_begin;
+            const __half* xsrc = phs.x_acc ? reinterpret_cast<const __half*>(phs.x_acc) : p.x_ext;
+            core::stage_x<D, NB, NW>(s_x, xsrc, phs.x_acc != nullptr, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
+            asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
+            float acc[RPL][NB];
+#pragma unroll
+            for (int q = 0; q < RPL; ++q)
+#pragma unroll
+                for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
+            for (int i = 0; i < ng; ++i, ++it) {
+                const int slot = it % ST;
+                dev::mbar_wait(full0 + 8 * slot, (it / ST) & 1);
+                core::compute_group<D, NB, RPL>(acc, idx_u + (uint32_t)slot * R * 32u,
+                                                cb_u + (uint32_t)slot * (uint32_t)p.cbb_max, x_u + (uint32_t)i * XG,
+                                                warp_row0, w.rows_valid, lane, lc);
+                __syncwarp();
+                if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+            }
+            core::acc_store<RPL, NB>(acc, w.y, w.r0, warp_row0, w.rows_valid, w.F_out, p.B, lane);
+        }
+        // arrive: bar.sync orders this CTA's red.adds before thread 0's release
+        asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
+        if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(p.counter) : "memory");
+    }
+}
+
+struct ChainCfg {
+    int rpl, nw, st;
+};
+
+template <int D, int NB, int RPL, int NW, int ST>
+fasq_status launch_chain_t(const ChainParams& p, size_t smem, int grid, cudaStream_t st) {
+    auto kern = k_chain<D, NB, RPL, NW, ST>;
+    static size_t lim = 0;
+    static std::once_flag once;
+    std::call_once(once, [&] { lim = set_max_dyn_smem(kern); });
+    if (lim < smem) { set_error("chain: dynamic SMEM plan exceeds the device limit"); return FASQ_E_UNSUPPORTED; }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3((NW + 1) * 32, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident (grid-wide arrival counter)
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FASQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
+    return FASQ_OK;
+}
+
+template <int D, int NB>
+fasq_status chain_cfg(const fasq_chain* c, const ChainParams& p, cudaStream_t st) {
+#define FASQ_CHAIN_CASE(RPL_, NW_, ST_) \
+    if (c->rpl == RPL_ && c->nw == NW_ && c->st == ST_) return launch_chain_t<D, NB, RPL_, NW_, ST_>(p, c->smem, c->nctas, st);
+    FASQ_CHAIN_CASE(2, 16, 3)
+    FASQ_CHAIN_CASE(4, 8, 3)
+    FASQ_CHAIN_CASE(1, 16, 3)
+    FASQ_CHAIN_CASE(2, 8, 3)
+    FASQ_CHAIN_CASE(1, 16, 2)
+    FASQ_CHAIN_CASE(1, 8, 1)
+    FASQ_CHAIN_CASE(2, 16, 2)
+    FASQ_CHAIN_CASE(1, 16, 1)
+#undef FASQ_CHAIN_CASE
+    set_error("chain: no kernel instantiated for this tiling");
+    return FASQ_E_UNSUPPORTED;
+}
+
+template <int D>
+fasq_status chain_nb(const fasq_chain* c, const ChainParams& p, cudaStream_t st) {
+    switch (c->B <= 1 ? 1 : c->B <= 2 ? 2 : c->B <= 4 ? 4 : 8) {
+        case 1: return chain_cfg<D, 1>(c, p, st);
+        case 2: return chain_cfg<D, 2>(c, p, st);
+        case 4: return chain_cfg<D, 4>(c, p, st);
+        case 8: return chain_cfg<D, 8>(c, p, st);
+    }
+    return FASQ_E_UNSUPPORTED;
+}
+
+int sm_count() {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+
+void destroy_chain(fasq_chain* c) {
+    if (!c) return;
+    if (c->arena) cudaFree(c->arena);
+    if (c->items) cudaFree(c->items);
+    if (c->phases) cudaFree(c->phases);
+    delete c;
+}
+
+}  // namespace
+
+}  // namespace fasq
+
+using namespace fasq;
+
+extern "C" {
+
+fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int32_t B, void* stream,
+                              fasq_chain** out) {
+    if (!out) return FASQ_E_ARG;
+    *out = nullptr;
+    if (!steps || n_steps < 1) return FASQ_E_ARG;
+    if (B < 1 || B > 8) return FASQ_E_UNSUPPORTED;
+    const int NB = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;
+    fasq_chain* c = new fasq_chain();
+    c->n_steps = n_steps;
+    c->B = B;
+    c->nctas = sm_count();
+    // same tiling family as the per-launch GEMV default (gemv.cu plan_gemv)
+    c->nw = 16;
+    c->rpl = NB <= 2 ? 2 : 1;
+    c->st = 3;
+    c->R = 32 * c->nw * c->rpl;
+    // validate + output arena layout
+    int64_t words = 16;   // [0..15]: grid counter + padding
+    c->acc_off.resize(n_steps);
+    c->acc_Fout.resize(n_steps);
+    c->step_F_in.resize(n_steps);
+    for (int s = 0; s < n_steps; ++s) {
+        const fasq_chain_step& S = steps[s];
+        if (!S.layers || S.n_layers < 1 || S.n_layers > 4) { destroy_chain(c); return FASQ_E_ARG; }
+        const int64_t F_in = S.layers[0]->F_in;
+        for (int l = 0; l < S.n_layers; ++l) {
+            const fasq_layer* L = S.layers[l];
+            if (!L) { destroy_chain(c); return FASQ_E_ARG; }
+            if (L->F_in != F_in) { destroy_chain(c); return FASQ_E_SHAPE; }
+            if (c->d == 0) c->d = L->d;
+            if (L->d != c->d) { destroy_chain(c); return FASQ_E_UNSUPPORTED; }
+            c->maxC = std::max(c->maxC, L->C);
+            c->acc_off[s].push_back(words);
+            c->acc_Fout[s].push_back(L->F_out);
+            words += (int64_t)B * L->F_out;
+        }
+        c->step_F_in[s] = (int)F_in;
+        if (S.input_step < 0) {
+            if (c->ext_F_in == 0) c->ext_F_in = (int)F_in;
+            if (c->ext_F_in != F_in) { destroy_chain(c); return FASQ_E_SHAPE; }
+        } else {
+            if (S.input_step >= s || S.input_layer < 0 || S.input_layer >= steps[S.input_step].n_layers) {
+                destroy_chain(c);
+                return FASQ_E_ARG;
+            }
+            if (steps[S.input_step].layers[S.input_layer]->F_out != F_in) { destroy_chain(c); return FASQ_E_SHAPE; }
+        }
+    }
+    if (c->ext_F_in == 0) { destroy_chain(c); return FASQ_E_ARG; }   // the chain needs an external input
+    const int E = entry_bytes(c->d);
+    const size_t cbb_max = (size_t)c->maxC * 32 * E;
+    auto ring = [&](int st, int rpl) { return (size_t)st * (cbb_max + (size_t)32 * c->nw * rpl * 32) + 16 * 1024; };
+    while (c->st > 2 && ring(c->st, c->rpl) > kSmemBudget) --c->st;
+    if (ring(c->st, c->rpl) > kSmemBudget && c->rpl > 1) c->rpl = 1;
+    while (c->st > 1 && ring(c->st, c->rpl) > kSmemBudget) --c->st;
+    c->R = 32 * c->nw * c->rpl;
+    c->arena_words = words;
+    if (cudaMalloc(&c->arena, (size_t)words * 8) != cudaSuccess) { cudaGetLastError(); destroy_chain(c); return FASQ_E_OOM; }
+    // work plan
+    std::vector<ChainItem> items((size_t)n_steps * c->nctas);
+    std::vector<ChainPhase> phases(n_steps);
+    for (auto& w : items) w = ChainItem{};
+    for (int s = 0; s < n_steps; ++s) {
+        const fasq_chain_step& S = steps[s];
+        const int nl = S.n_layers;
+        double W = 0;
+        for (int l = 0; l < nl; ++l) W += (double)S.layers[l]->F_out_pad * S.layers[l]->n_groups;
+        std::vector<int> rt(nl), ks(nl);
+        int total = 0;
+        for (int l = 0; l < nl; ++l) {
+            const fasq_layer* L = S.layers[l];
+            rt[l] = (L->F_out_pad + c->R - 1) / c->R;
+            const double share = c->nctas * ((double)L->F_out_pad * L->n_groups) / W;
+            int k = std::max(1, (int)(share / rt[l]));
+            k = std::min(k, L->n_groups);
+            const int gper = (L->n_groups + k - 1) / k;
+            k = (L->n_groups + gper - 1) / gper;
+            ks[l] = k;
+            total += rt[l] * k;
+        }
+        while (total > c->nctas) {
+            int lm = -1;
+            for (int l = 0; l < nl; ++l)
+                if (ks[l] > 1 && (lm < 0 || ks[l] * rt[l] > ks[lm] * rt[lm])) lm = l;
+            if (lm < 0) break;
+            total -= rt[lm];
+            ks[lm] -= 1;
+        }
+        if (total > c->nctas) { destroy_chain(c); return FASQ_E_UNSUPPORTED; }   // > #SMs row tiles
+        int cta = 0;
+        for (int l = 0; l < nl; ++l) {
+            const fasq_layer* L = S.layers[l];
+            for (int r = 0; r < rt[l]; ++r)
+                for (int k = 0; k < ks[l]; ++k, ++cta) {
+                    ChainItem& w = items[(size_t)s * c->nctas + cta];
+                    w.idx = L->idx;
+                    w.cbimg = L->cbimg;
+                    w.y = c->arena + c->acc_off[s][l];
+                    w.F_out = (int)L->F_out;
+                    w.F_out_pad = L->F_out_pad;
+                    w.N_ss = L->N_ss;
+                    w.C = L->C;
+                    w.r0 = r * c->R;
+                    w.rows_valid = std::min(c->R, L->F_out_pad - w.r0);
+                    w.g_begin = (int)((int64_t)k * L->n_groups / ks[l]);
+                    w.g_end = (int)((int64_t)(k + 1) * L->n_groups / ks[l]);
+                    c->gmax = std::max(c->gmax, w.g_end - w.g_begin);
+                }
+        }
+        phases[s].F_in = c->step_F_in[s];
+        phases[s].x_acc = S.input_step < 0
+                              ? nullptr
+                              : reinterpret_cast<const long long*>(c->arena + c->acc_off[S.input_step][S.input_layer]);
+    }
+    const size_t xg = (size_t)64 * NB * E;
+    c->smem = (size_t)c->st * (cbb_max + (size_t)c->R * 32) + (size_t)c->gmax * xg + 16 * c->st;
+    if (c->smem > kSmemBudget) { destroy_chain(c); set_error("chain: SMEM plan too large"); return FASQ_E_UNSUPPORTED; }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMalloc(&c->items, items.size() * sizeof(ChainItem)) != cudaSuccess ||
+        cudaMalloc(&c->phases, phases.size() * sizeof(ChainPhase)) != cudaSuccess) {
+        cudaGetLastError();
+        destroy_chain(c);
+        return FASQ_E_OOM;
+    }
+    cudaError_t e = cudaMemcpyAsync(c->items, items.data(), items.size() * sizeof(ChainItem), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(c->phases, phases.data(), phases.size() * sizeof(ChainPhase), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);   // host vectors go out of scope
+    if (e != cudaSuccess) { fasq_status s = cuda_fail(e, "chain upload"); destroy_chain(c); return s; }
+    *out = c;
+    return FASQ_OK;
+}
+
+fasq_status fasq_chain_run(fasq_chain* c, const void* x_dev, void* stream) {
+    if (!c || !x_dev) return FASQ_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    // zero the grid counter and every step's accumulators (outputs stay
+    // readable until the next run)
+    FASQ_CUDA_TRY(cudaMemsetAsync(c->arena, 0, (size_t)c->arena_words * 8, st));
+    ChainParams p{};
+    p.items = static_cast<const ChainItem*>(c->items);
+    p.phases = static_cast<const ChainPhase*>(c->phases);
+    p.x_ext = static_cast<const __half*>(x_dev);
+    p.counter = reinterpret_cast<unsigned*>(c->arena);
+    p.n_steps = c->n_steps;
+    p.nctas = c->nctas;
+    p.B = c->B;
+    p.gmax = c->gmax;
+    p.cbb_max = c->maxC * 32 * entry_bytes(c->d);
+    fasq_status s;
+    switch (c->d) {
+        case 1: s = chain_nb<1>(c, p, st); break;
+        case 2: s = chain_nb<2>(c, p, st); break;
+        case 4: s = chain_nb<4>(c, p, st); break;
+        case 8: s = chain_nb<8>(c, p, st); break;
+        default: s = FASQ_E_UNSUPPORTED;
+    }
+    if (s == FASQ_OK) set_launch_count(1);   // + one memset node
+    return s;
+}
+
+fasq_status fasq_chain_output(const fasq_chain* c, int32_t step, int32_t layer, void* y_dev, fasq_dtype dtype,
+                              void* stream) {
+    if (!c || !y_dev || step < 0 || step >= c->n_steps) return FASQ_E_ARG;
+    if (layer < 0 || layer >= (int)c->acc_off[step].size()) return FASQ_E_ARG;
+    if (dtype == FASQ_ACC_I64) {
+        FASQ_CUDA_TRY(cudaMemcpyAsync(y_dev, c->arena + c->acc_off[step][layer],
+                                      (size_t)c->B * c->acc_Fout[step][layer] * 8, cudaMemcpyDeviceToDevice,
+                                      (cudaStream_t)stream));
+        return FASQ_OK;
+    }
+    return acc_convert_launch(c->arena + c->acc_off[step][layer], (int64_t)c->B * c->acc_Fout[step][layer], y_dev,
+                              dtype, (cudaStream_t)stream);
+}
+
+void fasq_chain_free(fasq_chain* c) {
+    if (!c) return;
+    cudaDeviceSynchronize();
+    destroy_chain(c);
+}
+
+}  // extern "C"

@@ -32,6 +32,7 @@
 #include <mutex>
 
 #include "fasq_internal.cuh"
+#include "gemv_core.cuh"
 
 namespace fasq {
 
@@ -50,8 +51,8 @@ struct GemvLayerArgs {
 // to int64 in units of 2^-32 (exact scaling, one RN rounding each) and
 // red.add'ed -- integer addition is associative, so the result is
 // deterministic whatever the arrival order, with no split-K merge phase.
-constexpr float kAccScale = 4294967296.0f;      // 2^32
-constexpr double kAccInv = 1.0 / 4294967296.0;   // 2^-32
+using core::kAccScale;
+using core::kAccInv;
 
 struct GemvParams {
     GemvLayerArgs L[kMaxGroup];   // layers sharing x (grouped launch); CTAs are laid out layer-major
@@ -170,65 +171,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     // x staging (after the previous kernel's writes are visible).
     dev::pdl_wait();
     {
-        const int tid = threadIdx.x;
-        const int n_ent = ng * 64 * NB;   // entries of E bytes
-        // all global loads first (one round trip), then the SMEM stores
-        constexpr int XPT = 4;            // entries per thread per pass
-        for (int t0 = tid; t0 < n_ent; t0 += NW * 32 * XPT) {
-            uint32_t w[XPT][4];
-#pragma unroll
-            for (int u = 0; u < XPT; ++u) {
-                const int t = t0 + u * NW * 32;
-                w[u][0] = w[u][1] = w[u][2] = w[u][3] = 0u;
-                if (t >= n_ent) continue;
-                const int b = t % NB;
-                const int e64 = (t / NB) % 64;
-                const int gl = t / (NB * 64);
-                const int ss = (g_begin + gl) * 32 + (e64 & 31);
-                if (b < p.B && ss < la.N_ss && p.x_acc) {
-                    const long long* src = reinterpret_cast<const long long*>(p.x) + (size_t)b * p.F_in + (size_t)ss * D;
-#pragma unroll
-                    for (int e = 0; e < D; ++e) {
-                        const long long v = __ldcg(src + e);
-                        const uint32_t h = __half_as_ushort(__double2half((double)v * kAccInv));
-                        w[u][e >> 1] |= h << (16 * (e & 1));
-                    }
-                } else if (b < p.B && ss < la.N_ss) {
-                    const __half* src = p.x + (size_t)b * p.F_in + (size_t)ss * D;
-                    if (D == 1) {
-                        w[u][0] = (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(src));
-                    } else if (D == 2) {
-                        w[u][0] = __ldg(reinterpret_cast<const unsigned int*>(src));
-                    } else if (D == 4) {
-                        const uint2 v = __ldg(reinterpret_cast<const uint2*>(src));
-                        w[u][0] = v.x; w[u][1] = v.y;
-                    } else {
-                        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src));
-                        w[u][0] = v.x; w[u][1] = v.y; w[u][2] = v.z; w[u][3] = v.w;
-                    }
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < XPT; ++u) {
-                const int t = t0 + u * NW * 32;
-                if (t >= n_ent) continue;
-                uint32_t* dst = reinterpret_cast<uint32_t*>(s_x + (size_t)t * E);
-#pragma unroll
-                for (int q = 0; q < E / 4; ++q) dst[q] = w[u][q];
-            }
-        }
+        core::stage_x<D, NB, NW>(s_x, p.x, p.x_acc, p.F_in, p.B, la.N_ss, g_begin, ng);
         asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
     }
 
-    const int hA = (lane >> 2) & 1;                 // conflict-free LDS.128 of 32-B rows
-    const int rot = (lane + 16 * hA) & 31;          // lane's subspace rotation
-    // lowbyte constants: L[w] bytes = [8*sub(2w), 8*sub(2w+1), 0, 0];
-    // prmt(idx word, L, sel) = k*256 + 8*sub, then
-    //   E=4 : >>1  -> k*128 + 4*sub      E=8 : as is     E=16: <<1 -> k*512 + 16*sub
-    uint32_t Lr[16];
-#pragma unroll
-    for (int w = 0; w < 16; ++w)
-        Lr[w] = (uint32_t)(((2 * w + rot) & 31) * 8) | ((uint32_t)(((2 * w + 1 + rot) & 31) * 8) << 8);
+    core::LaneConsts lc;
+    core::lane_consts(lane, lc);
 
     float acc[RPL][NB];
 #pragma unroll
@@ -240,73 +188,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     for (int i = 0; i < ng; ++i) {
         const int slot = i % ST;
         dev::mbar_wait(full0 + 8 * slot, (i / ST) & 1);
-        uint32_t iw[RPL][8];
-#pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-            const int rl = warp_row0 + q * 32 + lane;
-            const uint32_t a = idx_u + (uint32_t)slot * R * 32u + (uint32_t)rl * 32u;
-            if (warp_row0 + q * 32 < rows_valid) {
-                uint4 v0 = dev::lds128(a + 16u * hA);
-                uint4 v1 = dev::lds128(a + 16u * (1 - hA));
-                iw[q][0] = v0.x; iw[q][1] = v0.y; iw[q][2] = v0.z; iw[q][3] = v0.w;
-                iw[q][4] = v1.x; iw[q][5] = v1.y; iw[q][6] = v1.z; iw[q][7] = v1.w;
-            } else {
-#pragma unroll
-                for (int w = 0; w < 8; ++w) iw[q][w] = 0u;
-            }
-        }
-        const uint32_t cbs = cb_u + (uint32_t)slot * CBB;
-        const uint32_t xb = x_u + (uint32_t)i * XG + (uint32_t)rot * (NB * E);
-#pragma unroll
-        for (int s = 0; s < 32; ++s) {
-            uint32_t xv[NB][E / 4];
-#pragma unroll
-            for (int b = 0; b < NB; ++b) {
-                const uint32_t xa = xb + (uint32_t)(s * NB * E + b * E);
-                if (E == 4) {
-                    xv[b][0] = dev::lds32(xa);
-                } else if (E == 8) {
-                    uint2 t2 = dev::lds64(xa);
-                    xv[b][0] = t2.x; xv[b][1 % (E / 4)] = t2.y;
-                } else {
-                    uint4 t4 = dev::lds128(xa);
-                    xv[b][0] = t4.x; xv[b][1 % (E / 4)] = t4.y;
-                    xv[b][2 % (E / 4)] = t4.z; xv[b][3 % (E / 4)] = t4.w;
-                }
-            }
-            const int wi = s >> 2, j = s & 3, lw = s >> 1, lj = s & 1;
-            // byte0 = L byte lj (8*sub), byte1 = idx byte j (k), bytes 2,3 = L byte 2 (0)
-            const uint32_t sel = (uint32_t)(4 + lj) | ((uint32_t)j << 4) | (6u << 8) | (6u << 12);
-#pragma unroll
-            for (int q = 0; q < RPL; ++q) {
-                if (warp_row0 + q * 32 >= rows_valid) continue;
-                uint32_t addr = dev::prmt(iw[q][wi], Lr[lw], sel);
-                if (E == 4) addr >>= 1;
-                if (E == 16) addr <<= 1;
-                if (E == 4) {
-                    const uint32_t c = dev::lds32(cbs + addr);
-#pragma unroll
-                    for (int b = 0; b < NB; ++b)
-                        acc[q][b] = (D == 1) ? dev::fhfma1(c, xv[b][0], acc[q][b]) : dev::fhfma2(c, xv[b][0], acc[q][b]);
-                } else if (E == 8) {
-                    const uint2 c = dev::lds64(cbs + addr);
-#pragma unroll
-                    for (int b = 0; b < NB; ++b) {
-                        acc[q][b] = dev::fhfma2(c.x, xv[b][0], acc[q][b]);
-                        acc[q][b] = dev::fhfma2(c.y, xv[b][1 % (E / 4)], acc[q][b]);
-                    }
-                } else {
-                    const uint4 c = dev::lds128(cbs + addr);
-#pragma unroll
-                    for (int b = 0; b < NB; ++b) {
-                        acc[q][b] = dev::fhfma2(c.x, xv[b][0], acc[q][b]);
-                        acc[q][b] = dev::fhfma2(c.y, xv[b][1 % (E / 4)], acc[q][b]);
-                        acc[q][b] = dev::fhfma2(c.z, xv[b][2 % (E / 4)], acc[q][b]);
-                        acc[q][b] = dev::fhfma2(c.w, xv[b][3 % (E / 4)], acc[q][b]);
-                    }
-                }
-            }
-        }
+        core::compute_group<D, NB, RPL>(acc, idx_u + (uint32_t)slot * R * 32u, cb_u + (uint32_t)slot * CBB,
+                                         x_u + (uint32_t)i * XG, warp_row0, rows_valid, lane, lc);
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
     }
@@ -318,18 +201,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
         for (long long i = zb + threadIdx.x; i < ze; i += NW * 32) p.zero_ptr[i] = 0ull;
     }
     if (p.y_acc) {
-#pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-            const int row = r0 + warp_row0 + q * 32 + lane;
-            if (warp_row0 + q * 32 >= rows_valid || row >= F_out) continue;
-#pragma unroll
-            for (int b = 0; b < NB; ++b) {
-                if (b >= p.B) continue;
-                const long long v = __float2ll_rn(acc[q][b] * kAccScale);
-                unsigned long long* dst = reinterpret_cast<unsigned long long*>(la.y) + (size_t)b * F_out + row;
-                asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(dst), "l"(v) : "memory");
-            }
-        }
+        core::acc_store<RPL, NB>(acc, reinterpret_cast<unsigned long long*>(la.y), r0, warp_row0, rows_valid, F_out,
+                                 p.B, lane);
         return;
     }
     if (ksplit == 1) {
@@ -458,6 +331,8 @@ static fasq_status dispatch_cfg(const GemvParams& p, const GemvPlan& pl, uint32_
     FASQ_GEMV_CFG_CASE(2, 16, 3)
     FASQ_GEMV_CFG_CASE(1, 16, 3)
     FASQ_GEMV_CFG_CASE(1, 8, 1)
+    FASQ_GEMV_CFG_CASE(1, 16, 1)
+    FASQ_GEMV_CFG_CASE(2, 16, 1)
     FASQ_GEMV_CFG_CASE(8, 4, 3)
     FASQ_GEMV_CFG_CASE(4, 4, 4)
     FASQ_GEMV_CFG_CASE(2, 8, 4)
@@ -503,10 +378,14 @@ static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB, bool spin
     const int E = Ls[0]->E;
     int maxC = 0;
     for (int l = 0; l < nl; ++l) maxC = std::max(maxC, Ls[l]->C);
-    if ((size_t)maxC * 32 * E * pl.st + (size_t)32 * pl.nw * pl.rpl * 32 * pl.st > kSmemBudget) {
-        pl.st = 1;                                   // d = 8, C = 256: 128 KiB codebook image per group
-        if (pl.rpl > 1) pl.rpl = 1;
-    }
+    // large codebook images (d = 4/8 with C = 256: 64/128 KiB per group): fewer
+    // stages, then fewer rows per lane
+    auto ring = [&](int st, int rpl) {
+        return (size_t)st * ((size_t)maxC * 32 * E + (size_t)32 * pl.nw * rpl * 32) + 16 * 1024;
+    };
+    while (pl.st > 2 && ring(pl.st, pl.rpl) > kSmemBudget) --pl.st;
+    if (ring(pl.st, pl.rpl) > kSmemBudget && pl.rpl > 1) pl.rpl = 1;
+    while (pl.st > 1 && ring(pl.st, pl.rpl) > kSmemBudget) --pl.st;
     pl.R = 32 * pl.nw * pl.rpl;
     int sms = num_sms();
     if (!spin_merge) {   // ACC outputs: no co-residency requirement; FASQ_GEMV_OCC = CTAs per SM to plan for
