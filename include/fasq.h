@@ -214,6 +214,13 @@ fasq_status fasq_chain_run(fasq_chain* chain, const void* x_dev, void* stream);
  * FASQ_ACC_I64 [B][F_out] (valid until the next run). */
 fasq_status fasq_chain_output(const fasq_chain* chain, int32_t step, int32_t layer, void* y_dev,
                               fasq_dtype dtype, void* stream);
+/* Diagnostics: when trace_dev is not NULL, every later fasq_chain_run writes
+ * per (step, CTA) four %globaltimer stamps (ns) into it, uint64
+ * [n_steps][fasq_chain_ctas(chain)][4]: step entry, previous step complete
+ * (grid wait done), x staged, outputs stored.  The buffer is the caller's
+ * and must stay allocated while tracing is on; NULL turns tracing off. */
+fasq_status fasq_chain_trace(fasq_chain* chain, void* trace_dev);
+int32_t fasq_chain_ctas(const fasq_chain* chain);   /* CTAs (= SMs) the chain runs on; -1 for NULL */
 void fasq_chain_free(fasq_chain* chain);   /* synchronises the device; NULL is a no-op */
 
 /* Same product with HOST buffers (end-to-end path): copies x_host (fp16

@@ -32,8 +32,8 @@ _STATUS = {0: "FASQ_OK", -1: "FASQ_E_ARG", -2: "FASQ_E_NONDIVISIBLE", -3: "FASQ_
 # Every symbol include/fasq.h declares (checked by tests/test_abi.py).
 EXPORTED = ["fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
             "fasq_free", "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_acc_convert",
-            "fasq_chain_create", "fasq_chain_run", "fasq_chain_output", "fasq_chain_free",
-            "fasq_gemv_host", "fasq_gemm",
+            "fasq_chain_create", "fasq_chain_run", "fasq_chain_output", "fasq_chain_trace",
+            "fasq_chain_ctas", "fasq_chain_free", "fasq_gemv_host", "fasq_gemm",
             "fasq_last_launch_count", "fasq_status_string", "fasq_last_error_message",
             "fasq_abi_version"]
 
@@ -94,6 +94,8 @@ def _load():
     L.fasq_chain_create.argtypes = [ctypes.POINTER(_ChainStep), i32, i32, vp, pp]
     L.fasq_chain_run.argtypes = [vp, vp, vp]
     L.fasq_chain_output.argtypes = [vp, i32, i32, vp, i32, vp]
+    L.fasq_chain_trace.argtypes = [vp, vp]
+    L.fasq_chain_ctas.argtypes = [vp]
     L.fasq_chain_free.argtypes = [vp]
     L.fasq_chain_free.restype = None
     L.fasq_gemm.argtypes = [vp, vp, i64, vp, i32, i32, vp]
@@ -101,8 +103,8 @@ def _load():
     L.fasq_last_error_message.restype = ctypes.c_char_p
     for name in ("fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
                  "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_acc_convert", "fasq_gemv_host",
-                 "fasq_chain_create", "fasq_chain_run", "fasq_chain_output",
-                 "fasq_gemm", "fasq_last_launch_count",
+                 "fasq_chain_create", "fasq_chain_run", "fasq_chain_output", "fasq_chain_trace",
+                 "fasq_chain_ctas", "fasq_gemm", "fasq_last_launch_count",
                  "fasq_abi_version"):
         getattr(L, name).restype = ctypes.c_int32
     return L
@@ -292,6 +294,19 @@ class Chain:
         yt = FASQ_F32 if dt == torch.float32 else FASQ_F16 if dt == torch.float16 else FASQ_ACC_I64
         _check(lib.fasq_chain_output(self._h, step, layer, out.data_ptr(), yt, _stream(stream)))
         return out
+
+    @property
+    def ctas(self) -> int:
+        return int(lib.fasq_chain_ctas(self._h))
+
+    def trace(self, buf: torch.Tensor | None):
+        """Diagnostics: record %globaltimer stamps into ``buf`` (int64
+        [steps][ctas][4]) on every later run; None turns it off."""
+        if buf is not None:
+            if buf.dtype != torch.int64 or not buf.is_cuda or buf.numel() < len(self.steps) * self.ctas * 4:
+                raise ValueError("trace buffer: cuda int64 [steps][ctas][4]")
+        self._trace_buf = buf
+        _check(lib.fasq_chain_trace(self._h, None if buf is None else buf.data_ptr()))
 
     def free(self):
         if self._h:

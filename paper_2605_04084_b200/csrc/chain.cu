@@ -21,6 +21,8 @@
 // Numerics are identical to chaining fasq_gemv_grouped calls with FASQ_ACC_I64
 // outputs.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -29,7 +31,7 @@
 
 struct fasq_chain {
     int n_steps = 0, B = 0, d = 0, nctas = 0;
-    int rpl = 0, nw = 0, st = 0, R = 0, gmax = 1, maxC = 1;
+    int rw = 0, nw = 0, st = 0, R = 0, gmax = 1, maxC = 1;
     size_t smem = 0;
     std::vector<int> step_F_out_total;               // per step: sum of F_out of its layers
     std::vector<std::vector<int64_t>> acc_off;       // per step, per layer: word offset in the arena
@@ -40,6 +42,7 @@ struct fasq_chain {
     int64_t arena_words = 0;
     void* items = nullptr;                           // device [n_steps][nctas] ChainItem
     void* phases = nullptr;                          // device [n_steps] ChainPhase
+    unsigned long long* trace = nullptr;             // user buffer (fasq_chain_trace), not owned
 };
 
 namespace fasq {
@@ -64,14 +67,17 @@ struct ChainParams {
     const ChainPhase* phases;
     const __half* x_ext;        // [B][F_in of the first step]
     unsigned* counter;          // grid arrival counter (zeroed per run)
+    unsigned long long* trace;  // optional [n_steps][nctas][4] globaltimer stamps (fasq_chain_trace)
     int n_steps, nctas, B, gmax, cbb_max;
+    int pf;                     // producer: L2-prefetch this many groups of the next step's item
 };
 
-template <int D, int NB, int RPL, int NW, int ST>
+template <int D, int NB, int NW, int ST>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
-    constexpr int E = D <= 2 ? 4 : 2 * D;
-    constexpr int R = 32 * NW * RPL;
-    constexpr int XG = 64 * NB * E;
+    constexpr int E = core::Entry<D>::value;
+    constexpr int RW = core::RowsPerWarp<NB>::value;
+    constexpr int R = RW * NW;
+    constexpr int XG = 32 * NB * E;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* s_cb = smem;                                       // ST * cbb_max
     uint8_t* s_idx = s_cb + ST * p.cbb_max;                     // ST * R * 32
@@ -100,6 +106,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                 if (w.rows_valid <= 0) continue;
                 const uint32_t cbb = (uint32_t)w.C * 32u * E;
                 const uint32_t chunk = (uint32_t)w.rows_valid * 32u;
+                if (p.pf > 0 && ph + 1 < p.n_steps) {
+                    // warm L2 with the head of the next step's item: HBM keeps
+                    // streaming across the grid-wide wait between the steps
+                    const ChainItem& nw = p.items[(size_t)(ph + 1) * p.nctas + blockIdx.x];
+                    if (nw.rows_valid > 0) {
+                        const int ge = min(nw.g_end, nw.g_begin + p.pf);
+                        for (int g = nw.g_begin; g < ge; ++g)
+                            dev::bulk_prefetch_l2(nw.idx + ((size_t)g * nw.F_out_pad + nw.r0) * 32,
+                                                  (uint32_t)nw.rows_valid * 32u);
+                    }
+                }
                 for (int g = w.g_begin; g < w.g_end; ++g, ++it) {
                     const int slot = it % ST;
                     if (it >= ST) dev::mbar_wait(empty0 + 8 * slot, ((it / ST) + 1) & 1);
@@ -115,57 +132,74 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         return;
     }
 
-    core::LaneConsts lc;
-    core::lane_consts(lane, lc);
-    const int warp_row0 = warp * 32 * RPL;
+    const int wrow0 = warp * RW;
+    const uint8_t* idx_lane = s_idx + core::idx_lane_off(wrow0, lane);
     int it = 0;
+    unsigned arrived = 0;   // thread 0: counter value after its own last arrival
     for (int ph = 0; ph < p.n_steps; ++ph) {
-        const ChainItem& w = p.items[(size_t)ph * p.nctas + blockIdx.x];
-        const ChainPhase& phs = p.phases[ph];
+        // the work item and phase are read-only for the kernel's lifetime:
+        // load them into registers before the grid-wide wait (off the
+        // critical path that follows it)
+        const ChainItem w = p.items[(size_t)ph * p.nctas + blockIdx.x];
+        const ChainPhase phs = p.phases[ph];
+        unsigned long long* tr = p.trace ? p.trace + ((size_t)ph * p.nctas + blockIdx.x) * 4 : nullptr;
+        if (tr && threadIdx.x == 0) tr[0] = dev::globaltimer();
         if (ph > 0) {   // every CTA of the previous step has published its outputs
             if (threadIdx.x == 0) {
                 const unsigned target = (unsigned)ph * (unsigned)p.nctas;
-                unsigned v;
-                do {
+                unsigned v = arrived;
+                while ((int)(v - target) < 0)
                     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.counter) : "memory");
-                } while ((int)(v - target) < 0);
             }
             asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
         }
+        if (tr && threadIdx.x == 0) tr[1] = dev::globaltimer();
         if (w.rows_valid > 0) {
             const int ng = w.g_end - w.g_begin;
             const __half* xsrc = phs.x_acc ? reinterpret_cast<const __half*>(phs.x_acc) : p.x_ext;
             core::stage_x<D, NB, NW>(s_x, xsrc, phs.x_acc != nullptr, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
             asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
-            float acc[RPL][NB];
+            if (tr && threadIdx.x == 0) tr[2] = dev::globaltimer();
+            float acc[RW][NB];
 #pragma unroll
-            for (int q = 0; q < RPL; ++q)
+            for (int q = 0; q < RW; ++q)
 #pragma unroll
                 for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
+            const bool active = wrow0 < w.rows_valid;
             for (int i = 0; i < ng; ++i, ++it) {
                 const int slot = it % ST;
                 dev::mbar_wait(full0 + 8 * slot, (it / ST) & 1);
-                core::compute_group<D, NB, RPL>(acc, idx_u + (uint32_t)slot * R * 32u,
-                                                cb_u + (uint32_t)slot * (uint32_t)p.cbb_max, x_u + (uint32_t)i * XG,
-                                                warp_row0, w.rows_valid, lane, lc);
+                if (active) {
+                    uint32_t xv[NB][E / 4];
+                    core::load_x<D, NB>(xv, s_x + i * XG, lane);
+                    core::compute_group<D, NB, RW>(acc, idx_lane + slot * R * 32, s_cb + slot * p.cbb_max, xv,
+                                                   wrow0, lane);
+                }
                 __syncwarp();
                 if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
             }
-            core::acc_store<RPL, NB>(acc, w.y, w.r0, warp_row0, w.rows_valid, w.F_out, p.B, lane);
+            core::RowTotals<NB, RW> tot;
+            core::reduce_rows<NB, RW>(acc, tot, lane);
+            if (active) core::acc_store<NB, RW>(tot, w.y, w.r0 + wrow0, w.F_out, p.B);
         }
         // arrive: bar.sync orders this CTA's red.adds before thread 0's release
         asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
-        if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(p.counter) : "memory");
+        if (tr && threadIdx.x == 0) tr[3] = dev::globaltimer();
+        if (threadIdx.x == 0) {
+            // the returned count tells the last arriver it need not poll
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(p.counter) : "memory");
+            arrived += 1;
+        }
     }
 }
 
 struct ChainCfg {
-    int rpl, nw, st;
+    int rw, nw, st;
 };
 
-template <int D, int NB, int RPL, int NW, int ST>
+template <int D, int NB, int NW, int ST>
 fasq_status launch_chain_t(const ChainParams& p, size_t smem, int grid, cudaStream_t st) {
-    auto kern = k_chain<D, NB, RPL, NW, ST>;
+    auto kern = k_chain<D, NB, NW, ST>;
     static size_t lim = 0;
     static std::once_flag once;
     std::call_once(once, [&] { lim = set_max_dyn_smem(kern); });
@@ -186,16 +220,14 @@ fasq_status launch_chain_t(const ChainParams& p, size_t smem, int grid, cudaStre
 
 template <int D, int NB>
 fasq_status chain_cfg(const fasq_chain* c, const ChainParams& p, cudaStream_t st) {
-#define FASQ_CHAIN_CASE(RPL_, NW_, ST_) \
-    if (c->rpl == RPL_ && c->nw == NW_ && c->st == ST_) return launch_chain_t<D, NB, RPL_, NW_, ST_>(p, c->smem, c->nctas, st);
-    FASQ_CHAIN_CASE(2, 16, 3)
-    FASQ_CHAIN_CASE(4, 8, 3)
-    FASQ_CHAIN_CASE(1, 16, 3)
-    FASQ_CHAIN_CASE(2, 8, 3)
-    FASQ_CHAIN_CASE(1, 16, 2)
-    FASQ_CHAIN_CASE(1, 8, 1)
-    FASQ_CHAIN_CASE(2, 16, 2)
-    FASQ_CHAIN_CASE(1, 16, 1)
+#define FASQ_CHAIN_CASE(NW_, ST_) \
+    if (c->nw == NW_ && c->st == ST_) return launch_chain_t<D, NB, NW_, ST_>(p, c->smem, c->nctas, st);
+    FASQ_CHAIN_CASE(16, 3)
+    FASQ_CHAIN_CASE(16, 2)
+    FASQ_CHAIN_CASE(16, 1)
+    FASQ_CHAIN_CASE(8, 3)
+    FASQ_CHAIN_CASE(8, 2)
+    FASQ_CHAIN_CASE(8, 1)
 #undef FASQ_CHAIN_CASE
     set_error("chain: no kernel instantiated for this tiling");
     return FASQ_E_UNSUPPORTED;
@@ -248,9 +280,13 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
     c->nctas = sm_count();
     // same tiling family as the per-launch GEMV default (gemv.cu plan_gemv)
     c->nw = 16;
-    c->rpl = NB <= 2 ? 2 : 1;
+    c->rw = NB == 1 ? 64 : NB == 2 ? 32 : NB == 4 ? 16 : 8;   // core::RowsPerWarp
     c->st = 3;
-    c->R = 32 * c->nw * c->rpl;
+    if (const char* e = getenv("FASQ_CHAIN_CFG")) {   // experiments: "nw,st"
+        int a = 0, b = 0;
+        if (sscanf(e, "%d,%d", &a, &b) == 2) { c->nw = a; c->st = b; }
+    }
+    c->R = c->rw * c->nw;
     // validate + output arena layout
     int64_t words = 16;   // [0..15]: grid counter + padding
     c->acc_off.resize(n_steps);
@@ -286,11 +322,11 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
     if (c->ext_F_in == 0) { destroy_chain(c); return FASQ_E_ARG; }   // the chain needs an external input
     const int E = entry_bytes(c->d);
     const size_t cbb_max = (size_t)c->maxC * 32 * E;
-    auto ring = [&](int st, int rpl) { return (size_t)st * (cbb_max + (size_t)32 * c->nw * rpl * 32) + 16 * 1024; };
-    while (c->st > 2 && ring(c->st, c->rpl) > kSmemBudget) --c->st;
-    if (ring(c->st, c->rpl) > kSmemBudget && c->rpl > 1) c->rpl = 1;
-    while (c->st > 1 && ring(c->st, c->rpl) > kSmemBudget) --c->st;
-    c->R = 32 * c->nw * c->rpl;
+    auto ring = [&](int st, int nw) { return (size_t)st * (cbb_max + (size_t)c->rw * nw * 32) + 16 * 1024; };
+    while (c->st > 2 && ring(c->st, c->nw) > kSmemBudget) --c->st;
+    if (ring(c->st, c->nw) > kSmemBudget && c->nw > 8) c->nw = 8;
+    while (c->st > 1 && ring(c->st, c->nw) > kSmemBudget) --c->st;
+    c->R = c->rw * c->nw;
     c->arena_words = words;
     if (cudaMalloc(&c->arena, (size_t)words * 8) != cudaSuccess) { cudaGetLastError(); destroy_chain(c); return FASQ_E_OOM; }
     // work plan
@@ -349,7 +385,7 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
                               ? nullptr
                               : reinterpret_cast<const long long*>(c->arena + c->acc_off[S.input_step][S.input_layer]);
     }
-    const size_t xg = (size_t)64 * NB * E;
+    const size_t xg = (size_t)32 * NB * E;
     c->smem = (size_t)c->st * (cbb_max + (size_t)c->R * 32) + (size_t)c->gmax * xg + 16 * c->st;
     if (c->smem > kSmemBudget) { destroy_chain(c); set_error("chain: SMEM plan too large"); return FASQ_E_UNSUPPORTED; }
     cudaStream_t st = (cudaStream_t)stream;
@@ -379,6 +415,9 @@ fasq_status fasq_chain_run(fasq_chain* c, const void* x_dev, void* stream) {
     p.phases = static_cast<const ChainPhase*>(c->phases);
     p.x_ext = static_cast<const __half*>(x_dev);
     p.counter = reinterpret_cast<unsigned*>(c->arena);
+    p.trace = c->trace;
+    p.pf = 0;
+    if (const char* e = getenv("FASQ_CHAIN_PF")) p.pf = atoi(e);
     p.n_steps = c->n_steps;
     p.nctas = c->nctas;
     p.B = c->B;
@@ -409,6 +448,14 @@ fasq_status fasq_chain_output(const fasq_chain* c, int32_t step, int32_t layer, 
     return acc_convert_launch(c->arena + c->acc_off[step][layer], (int64_t)c->B * c->acc_Fout[step][layer], y_dev,
                               dtype, (cudaStream_t)stream);
 }
+
+fasq_status fasq_chain_trace(fasq_chain* c, void* trace_dev) {
+    if (!c) return FASQ_E_ARG;
+    c->trace = static_cast<unsigned long long*>(trace_dev);
+    return FASQ_OK;
+}
+
+int32_t fasq_chain_ctas(const fasq_chain* c) { return c ? c->nctas : -1; }
 
 void fasq_chain_free(fasq_chain* c) {
     if (!c) return;

@@ -12,29 +12,38 @@
 namespace fasq {
 
 constexpr int kGroupSubs = 32;   // subspaces per "group" = one per lane of a warp
+constexpr int kRowBlock = 64;    // rows per index block (F_out_pad is a multiple)
 
 // ---------------------------------------------------------------------------
 // The layer object (opaque behind the ABI).  Physical layout (DESIGN.md
 // "Data layout in HBM"):
 //
-//  idx    [n_groups][F_out_pad][32] uint8.  Byte p of (group g, row r) holds
-//         T_index[g*32 + ((p + r) & 31)][r]  (row-rotated so that lane l of a
-//         warp working on rows r = l (mod 32) reads subspace (s + l) & 31 at
-//         step s -> conflict-free codebook gathers).
-//         Padded subspaces (>= N_ss) and rows (>= F_out) hold 0.
+//  idx    [n_groups][F_out_pad/64][32 subspaces][64 rows] uint8: per group g
+//         and 64-row block, subspace-major, so that lane s of a warp (= the
+//         group's subspace s) loads the indices of 16 rows with one LDS.128.
+//         The four 16-row chunks of a (block, subspace) segment are rotated
+//         by s/2: chunk c (rows 16c..16c+15) sits at 16-B position
+//         (c + (s >> 1)) & 3, which makes the LDS.128 of a quarter-warp hit 8
+//         distinct 16-B bank groups (conflict-free).  Rows [r0, r0 + n) of a
+//         group with r0, n multiples of 64 are ONE contiguous range of n*32
+//         bytes at (g*F_out_pad + r0)*32.  Padded subspaces (>= N_ss) and rows
+//         (>= F_out) hold 0.  idx_offset() below is the definition.
 //  cbimg  [n_groups][C][32][E] bytes, E = entry bytes (4 for d<=2 -- d=1 is
 //         padded to (c,0) --, 8 for d=4, 16 for d=8): the codebook of each
-//         lane's subspace, k-major so that one k-row is 32*E contiguous bytes.
-//         Padded subspaces hold 0.
+//         lane's subspace, k-major so that one k-row is 32*E contiguous bytes
+//         and lane s reads bank(s) whatever k is.  Padded subspaces hold 0.
 //  cb     [N_cb][C][d] fp16, the logical codebooks (export / GEMM staging).
 // ---------------------------------------------------------------------------
+__host__ __device__ inline int64_t idx_offset(int64_t g, int64_t r, int s, int64_t F_out_pad) {
+    return (g * F_out_pad + (r & ~(int64_t)63)) * 32 + s * 64 + 16 * ((((r >> 4) & 3) + (s >> 1)) & 3) + (r & 15);
+}
 }  // namespace fasq
 
 struct fasq_layer {
     int64_t F_out = 0, F_in = 0;
     int32_t d = 0, C = 0, group = 0, N_ss = 0, N_cb = 0;
     int32_t row_offset = 0;
-    int32_t F_out_pad = 0;     // multiple of 32
+    int32_t F_out_pad = 0;     // multiple of kRowBlock (64)
     int32_t n_groups = 0;      // ceil(N_ss / 32)
     int32_t E = 0;             // cbimg entry bytes
     int device = 0;
@@ -228,6 +237,12 @@ __device__ __forceinline__ void pdl_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 }  // namespace dev
 }  // namespace fasq

@@ -8,6 +8,8 @@
 // 32-subspace group at once in SMEM, [C][32 subspaces] fp32 per token laid out
 // like the GEMV codebook image, and every lane (= 4 weight rows, rotated
 // subspace order) gathers conflict-free with the one-`prmt` address.  The
+// group's index block is first re-laid in SMEM from the subspace-major HBM
+// layout into row-rotated rows (byte p of row r = subspace (p + r) & 31).  The
 // gathers are pure FADD on CUDA cores -- no tensor cores --
 // which is why the EXPAND variant exists (gemm_tc.cu).
 #include "fasq_internal.cuh"
@@ -22,14 +24,15 @@ constexpr int LUT_THREADS = 256;
 constexpr int LUT_R = LUT_THREADS * LUT_RPT;   // 1024 rows per CTA
 
 struct LutParams {
-    const uint8_t* idx;       // [n_groups][F_out_pad][32]
+    const uint8_t* idx;       // [n_groups][F_out_pad/64][32][64] (fasq_internal.cuh)
     const uint8_t* cbimg;     // [n_groups][C][32][4]   (d <= 2)
     const __half* X;          // [M][F_in]
     void* Y;
     int M, F_in, F_out, F_out_pad, n_groups, N_ss, C, d, y_f32;
 };
 
-// LUT SMEM: token pair tp = t>>1 occupies C*256 B; row k = [t even: 32 x f32][t odd: 32 x f32]
+// LUT SMEM: token pair tp = t>>1 occupies C*256 B; row k = [t even: 32 x f32][t odd: 32 x f32];
+// then the row-rotated index block [LUT_R][32] bytes.
 __global__ void __launch_bounds__(LUT_THREADS, 1) k_gemm_lut(LutParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int C = p.C;
@@ -37,6 +40,7 @@ __global__ void __launch_bounds__(LUT_THREADS, 1) k_gemm_lut(LutParams p) {
     const int r_base = blockIdx.x * LUT_R;
     const int m0 = blockIdx.y * LUT_MT;
     const uint32_t lut_u = dev::smem_u32(smem);
+    uint8_t* s_idx = smem + (size_t)(LUT_MT / 2) * C * 256;
     const int rot = lane;   // natural byte order of the row-rotated index layout
     uint32_t Lr[8];
 #pragma unroll
@@ -72,12 +76,26 @@ __global__ void __launch_bounds__(LUT_THREADS, 1) k_gemm_lut(LutParams p) {
                 reinterpret_cast<float*>(smem)[((t >> 1) * C * 64) + k * 64 + (t & 1) * 32 + sub] = v;
             }
         }
+        // index block re-layout: 16-row chunks of subspace s -> rotated rows
+        for (int q = tid; q < (LUT_R / 16) * 32; q += LUT_THREADS) {
+            const int sub = q & 31, ch = q >> 5;
+            const int r0 = r_base + ch * 16;
+            if (r0 >= p.F_out_pad) continue;
+            const uint4 v = *reinterpret_cast<const uint4*>(p.idx + idx_offset(g, r0, sub, p.F_out_pad));
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int rl = ch * 16 + j;
+                s_idx[rl * 32 + ((sub - rl) & 31)] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
+            }
+        }
         __syncthreads();
 #pragma unroll
         for (int q = 0; q < LUT_RPT; ++q) {
-            const int row = r_base + q * LUT_THREADS + warp * 32 + lane;
+            const int rl = q * LUT_THREADS + warp * 32 + lane;
+            const int row = r_base + rl;
             if (row >= p.F_out_pad) continue;
-            const uint4* ip = reinterpret_cast<const uint4*>(p.idx + ((size_t)g * p.F_out_pad + row) * 32);
+            const uint4* ip = reinterpret_cast<const uint4*>(s_idx + rl * 32);
             const uint4 v0 = ip[0], v1 = ip[1];
             const uint32_t iw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
@@ -126,7 +144,7 @@ fasq_status gemm_lut_launch(const fasq_layer* L, const __half* X, int64_t M, voi
     p.C = L->C;
     p.d = L->d;
     p.y_f32 = yt == FASQ_F32;
-    const size_t smem = (size_t)(LUT_MT / 2) * L->C * 256;
+    const size_t smem = (size_t)(LUT_MT / 2) * L->C * 256 + (size_t)LUT_R * 32;
     static bool attr = false;
     if (!attr) {
         if (set_max_dyn_smem(k_gemm_lut) < smem) { set_error("gemm_lut: SMEM"); return FASQ_E_UNSUPPORTED; }

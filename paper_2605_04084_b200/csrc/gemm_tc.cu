@@ -9,9 +9,9 @@
 //
 //   producer warp : TMA 2-D load of the X tile (128B swizzle) + bulk copies of
 //                   the group's codebook image and the tile's index chunk;
-//   8 expand warps: lane = weight row; gather the 32 centroids of the row from
-//                   the SMEM codebook image in the conflict-free rotated order
-//                   (same layout as the GEMV) and store them into the B tile
+//   8 expand warps: lane = subspace (as in the GEMV); gather the centroids of
+//                   32 rows from the SMEM codebook image (lane s -> bank s,
+//                   conflict-free) and store them into the B tile
 //                   in the UMMA K-major SWIZZLE_128B layout (never to HBM);
 //   MMA thread    : 2 token tiles x 4 x tcgen05.mma.cta_group::1.kind::f16
 //                   (M=128, N=256, K=16) into two TMEM fp32 accumulators (all
@@ -38,7 +38,7 @@ constexpr int TC_EXP_WARPS = 8;    // expansion warps (lane = weight row)
 constexpr int TC_THREADS = (2 + TC_EXP_WARPS) * 32;
 
 struct TcParams {
-    const uint8_t* idx;      // [n_groups][F_out_pad][32]
+    const uint8_t* idx;      // [n_groups][F_out_pad/64][32][64] (fasq_internal.cuh)
     const uint8_t* cbimg;    // [n_groups][C][32][4]
     void* Y;
     int M, F_out, F_out_pad, n_groups, C, y_f32;
@@ -117,7 +117,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     if (warp == 0) {
         // ------------------------------ producer ------------------------------
         if (lane == 0) asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
-        const int rows = min(TC_N, p.F_out_pad - n0);          // idx rows present (multiple of 32)
+        const int rows = min(TC_N, p.F_out_pad - n0);          // idx rows present (multiple of 64)
         const uint32_t idx_bytes = (uint32_t)rows * 32u;
         const uint32_t cb_u = dev::smem_u32(sC);
         for (int i = 0; i < nk; ++i) {
@@ -172,41 +172,40 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
         }
     } else {
         // ------------------------------ expansion ------------------------------
+        // warp ew expands weight rows [32*ew, 32*ew + 32) of the tile; lane =
+        // subspace s (the GEMV's mapping, gemv_core.cuh): one LDS.128 gives the
+        // indices of 16 rows, lane s gathers c_s[k] from bank s (conflict-free
+        // whatever k is) and writes K columns (2s, 2s+1) of the row; the 32
+        // lanes of one STS fill one 128-B B-tile row (K-major SWIZZLE_128B:
+        // 16-B chunk c of row r at c ^ (r & 7)) -> conflict-free.
         const int ew = warp - 2;                 // 0..7
-        const int rl = ew * 32 + lane;           // local weight row 0..255
-        // natural byte order: register byte s holds subspace (s + rl) & 31
-        const int rot = rl & 31;
-        // L[w] bytes = [8*sub(2w), 8*sub(2w+1), 0, 0]: prmt -> k*256 + 8*sub, >>1 -> k*128 + 4*sub
-        uint32_t Lr[16];
+        uint32_t xo[8];
 #pragma unroll
-        for (int w = 0; w < 16; ++w)
-            Lr[w] = (uint32_t)(((2 * w + rot) & 31) * 8) | ((uint32_t)(((2 * w + 1 + rot) & 31) * 8) << 8);
-        // B-tile STS offsets (SWIZZLE_128B K-major: 16-B chunk c of row r at c ^ (r & 7)):
-        // step st writes subspace (st + rot) & 31, i.e. k = 2*sub -> chunk sub>>2, word sub&3
-        uint32_t xo[32];
-#pragma unroll
-        for (int st = 0; st < 32; ++st) {
-            const int sub = (st + rot) & 31;
-            xo[st] = (uint32_t)rl * 128u + ((uint32_t)(((sub >> 2) ^ (rl & 7)) << 4) | ((uint32_t)(sub & 3) << 2));
-        }
+        for (int q = 0; q < 8; ++q) xo[q] = ((uint32_t)(((lane >> 2) ^ q) << 4)) | ((uint32_t)(lane & 3) << 2);
         const uint32_t cb_u = dev::smem_u32(sC);
+        const uint32_t ib0 = (uint32_t)(ew >> 1) * 2048u + (uint32_t)lane * 64u;
+        const uint32_t rot = (uint32_t)(lane >> 1);
+        const bool have = n0 + ew * 32 < p.F_out_pad;   // this warp's rows were loaded (64-row blocks)
         for (int i = 0; i < nk; ++i) {
             const int s = i % TC_STAGES;
             const uint32_t ph = (i / TC_STAGES) & 1;
             dev::mbar_wait(full_bar(s), ph);
-            const uint32_t ia = dev::smem_u32(sI + s * IDX_BYTES) + (uint32_t)rl * 32u;
-            uint4 v0 = dev::lds128(ia), v1 = dev::lds128(ia + 16);
-            if (n0 + rl >= p.F_out_pad) { v0 = make_uint4(0, 0, 0, 0); v1 = v0; }   // rows not loaded
-            const uint32_t iw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-            const uint32_t cbs = cb_u + (uint32_t)s * (uint32_t)CB_BYTES;
-            const uint32_t bst = dev::smem_u32(sB + s * B_BYTES);
+            const uint32_t ia = dev::smem_u32(sI + s * IDX_BYTES) + ib0;
+            const uint32_t cbl = cb_u + (uint32_t)s * (uint32_t)CB_BYTES + (uint32_t)lane * 4u;
+            const uint32_t bst = dev::smem_u32(sB + s * B_BYTES) + (uint32_t)ew * 32u * 128u;
 #pragma unroll
-            for (int st = 0; st < 32; ++st) {
-                const int j = st & 3, lj = st & 1;
-                const uint32_t sel = (uint32_t)(4 + lj) | ((uint32_t)j << 4) | (6u << 8) | (6u << 12);
-                const uint32_t a = dev::prmt(iw[st >> 2], Lr[st >> 1], sel) >> 1;
-                const uint32_t c = dev::lds32(cbs + a);
-                asm volatile("st.shared.u32 [%0], %1;" :: "r"(bst + xo[st]), "r"(c) : "memory");
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t c = (uint32_t)(2 * (ew & 1) + h);
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (have) v = dev::lds128(ia + 16u * ((c + rot) & 3u));
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t k = dev::prmt(w[j >> 2], 0u, 0x4440u | (uint32_t)(j & 3));
+                    const uint32_t cv = dev::lds32(cbl + (k << 7));
+                    asm volatile("st.shared.u32 [%0], %1;" :: "r"(bst + (uint32_t)(h * 16 + j) * 128u + xo[j & 7]),
+                                 "r"(cv) : "memory");
+                }
             }
             dev::fence_proxy_async();      // generic-proxy STS -> visible to tcgen05 (async proxy)
             __syncwarp();

@@ -7,19 +7,18 @@
 // B200 its 32 lanes all gather from ONE 1 KiB codebook at random rows, i.e.
 // ~3 SMEM/L1 wavefronts per warp-gather.  This kernel instead:
 //
-//  * lane l of a warp owns output rows r = l (mod 32) and walks the 32
-//    subspaces of a group in a lane-ROTATED order (subspace (s + rot_l) & 31
-//    at step s); the codebook image of the 32 subspaces sits in SMEM k-major,
-//    [C][32 lanes][E bytes], so at every step the 32 lanes hit 32 distinct
-//    banks whatever the indices are -> one wavefront per warp-gather, and each
-//    lane accumulates whole rows in registers (no cross-lane reduction);
-//  * the index table is stored pre-rotated ([group][row][32] bytes, see
-//    layout.cu) so the byte for step s sits at a fixed register position and
-//    ONE `prmt` turns it into the SMEM address (k*256 | 4*sub) -- together
-//    with one LDS and two FHFMA (fma.rn.f32.f16: exact fp16 product, fp32
-//    accumulation) that is 4 instructions per index at d = 2;
+//  * lane s of a warp owns subspace s of the current 32-subspace group and
+//    keeps x_s in registers; the warp owns RW output rows (64 at B = 1).  The
+//    group's codebook image sits in SMEM k-major, [C][32 lanes][E bytes], so
+//    lane s gathers from bank s whatever the indices are: one wavefront per
+//    warp-gather.  The index table is stored subspace-major per 64-row block
+//    (layout.cu), so ONE LDS.128 gives a lane the indices of 16 rows; per
+//    index the lane issues PRMT (extract k), LEA (address), LDS and two FHFMA
+//    (fma.rn.f32.f16: exact fp16 product, fp32 accumulation) at d = 2.  The
+//    32 lanes' per-row partials are summed once per K range by a transposed
+//    butterfly (gemv_core.cuh);
 //  * a producer warp streams each (row tile, group) index chunk and the
-//    group's codebook image into a 2-stage SMEM ring with the TMA bulk-copy
+//    group's codebook image into a 3-stage SMEM ring with the TMA bulk-copy
 //    engine (cp.async.bulk + mbarrier complete_tx); consumers never issue
 //    global loads in the hot loop;
 //  * split-K over subspace groups (grid.y) is merged deterministically in
@@ -68,22 +67,20 @@ struct GemvParams {
     int gmax;               // max groups per CTA (x staging capacity)
 };
 
-// x staging: per group, 64 entries (subspaces 0..31 twice, so the rotated
-// index (s + rot) needs no wrap) x NB batches x E bytes.
-//
 // SMEM layout: cb ring [ST][C][32][E] (one contiguous TMA bulk copy per
 // stage -- the microbenchmark in tools/mb_bulk.cu shows 128-B bulk copies
 // cap at ~0.6 TB/s while >=16 KiB copies reach ~7 TB/s), index ring
-// [ST][R][32], x [gmax][64][NB][E], mbarriers full[ST], empty[ST].
+// [ST][R/64][32][64], x [gmax][32][NB][E], mbarriers full[ST], empty[ST].
 // Under programmatic dependent launch the NEXT layer's CTAs may become
 // resident as soon as SMEM allows and prefetch their codebook/index stages
 // (weights do not depend on x); they only wait (griddepcontrol.wait) before
 // touching x.
-template <int D, int NB, int RPL, int NW, int ST>
+template <int D, int NB, int NW, int ST>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
-    constexpr int E = D <= 2 ? 4 : 2 * D;
-    constexpr int R = 32 * NW * RPL;          // rows per CTA tile
-    constexpr int XG = 64 * NB * E;           // x bytes per staged group
+    constexpr int E = core::Entry<D>::value;
+    constexpr int RW = core::RowsPerWarp<NB>::value;   // rows per consumer warp
+    constexpr int R = RW * NW;                         // rows per CTA tile
+    constexpr int XG = 32 * NB * E;                    // x bytes per staged group
     extern __shared__ __align__(1024) uint8_t smem[];
 
     int li = 0;
@@ -100,7 +97,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     const int g_end = (int)((int64_t)(ks + 1) * n_groups / ksplit);
     const int ng = g_end - g_begin;
     const int r0 = rt * R;
-    const int rows_valid = min(R, F_out_pad - r0);   // multiple of 32
+    const int rows_valid = min(R, F_out_pad - r0);   // multiple of 64
 
     uint8_t* s_cb = smem;                                     // ST*CBB
     uint8_t* s_idx = s_cb + ST * CBB;                         // ST*R*32
@@ -175,21 +172,23 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
         asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
     }
 
-    core::LaneConsts lc;
-    core::lane_consts(lane, lc);
-
-    float acc[RPL][NB];
+    float acc[RW][NB];
 #pragma unroll
-    for (int q = 0; q < RPL; ++q)
+    for (int q = 0; q < RW; ++q)
 #pragma unroll
         for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
 
-    const int warp_row0 = warp * 32 * RPL;
+    const int wrow0 = warp * RW;
+    const bool active = wrow0 < rows_valid;          // rows_valid is a multiple of 64 >= RW
+    const uint8_t* idx_lane = s_idx + core::idx_lane_off(wrow0, lane);
     for (int i = 0; i < ng; ++i) {
         const int slot = i % ST;
         dev::mbar_wait(full0 + 8 * slot, (i / ST) & 1);
-        core::compute_group<D, NB, RPL>(acc, idx_u + (uint32_t)slot * R * 32u, cb_u + (uint32_t)slot * CBB,
-                                         x_u + (uint32_t)i * XG, warp_row0, rows_valid, lane, lc);
+        if (active) {
+            uint32_t xv[NB][E / 4];
+            core::load_x<D, NB>(xv, s_x + i * XG, lane);
+            core::compute_group<D, NB, RW>(acc, idx_lane + slot * R * 32, s_cb + slot * CBB, xv, wrow0, lane);
+        }
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
     }
@@ -200,21 +199,26 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
         const long long zb = per * blockIdx.x, ze = min(p.zero_words, zb + per);
         for (long long i = zb + threadIdx.x; i < ze; i += NW * 32) p.zero_ptr[i] = 0ull;
     }
+    core::RowTotals<NB, RW> tot;
+    core::reduce_rows<NB, RW>(acc, tot, lane);
+    constexpr int H = core::RowTotals<NB, RW>::H;
     if (p.y_acc) {
-        core::acc_store<RPL, NB>(acc, reinterpret_cast<unsigned long long*>(la.y), r0, warp_row0, rows_valid, F_out,
-                                 p.B, lane);
+        if (active)
+            core::acc_store<NB, RW>(tot, reinterpret_cast<unsigned long long*>(la.y), r0 + wrow0, F_out, p.B);
         return;
     }
     if (ksplit == 1) {
+        if (active && tot.own) {
 #pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-            const int row = r0 + warp_row0 + q * 32 + lane;
-            if (warp_row0 + q * 32 >= rows_valid || row >= F_out) continue;
+            for (int h = 0; h < H; ++h) {
+                const int row = r0 + wrow0 + h * 32 + tot.rsel;
+                if (row >= F_out) continue;
 #pragma unroll
-            for (int b = 0; b < NB; ++b) {
-                if (b >= p.B) continue;
-                if (p.y_f32) reinterpret_cast<float*>(la.y)[(size_t)b * F_out + row] = acc[q][b];
-                else reinterpret_cast<__half*>(la.y)[(size_t)b * F_out + row] = __float2half_rn(acc[q][b]);
+                for (int b = 0; b < NB; ++b) {
+                    if (b >= p.B) continue;
+                    if (p.y_f32) reinterpret_cast<float*>(la.y)[(size_t)b * F_out + row] = tot.v[h][b];
+                    else reinterpret_cast<__half*>(la.y)[(size_t)b * F_out + row] = __float2half_rn(tot.v[h][b]);
+                }
             }
         }
         return;
@@ -224,13 +228,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     // launch only after every CTA started), then each CTA sums a
     // 1/ksplit slice of the tile's rows over ks = 0..ksplit-1 in fixed order
     // (deterministic; the paper's merge is atomicAdd).
+    if (active && tot.own) {
 #pragma unroll
-    for (int q = 0; q < RPL; ++q) {
-        const int row = r0 + warp_row0 + q * 32 + lane;
-        if (warp_row0 + q * 32 >= rows_valid) continue;
+        for (int h = 0; h < H; ++h) {
+            const int row = r0 + wrow0 + h * 32 + tot.rsel;
 #pragma unroll
-        for (int b = 0; b < NB; ++b)
-            if (b < p.B) __stcg(&la.partial[((size_t)ks * p.B + b) * F_out_pad + row], acc[q][b]);
+            for (int b = 0; b < NB; ++b)
+                if (b < p.B) __stcg(&la.partial[((size_t)ks * p.B + b) * F_out_pad + row], tot.v[h][b]);
+        }
     }
     // arrive: bar.sync orders this CTA's partial stores before thread 0's
     // release-RMW (cumulative, no full fence).
@@ -289,16 +294,16 @@ static int num_sms() {
 }
 
 struct GemvPlan {
-    int rpl, nw, st, R;
+    int rw, nw, st, R;
     int nl;
     int row_tiles[kMaxGroup], ksplit[kMaxGroup];
     int gmax, grid;
     size_t smem;
 };
 
-template <int D, int NB, int RPL, int NW, int ST>
+template <int D, int NB, int NW, int ST>
 static fasq_status launch_gemv_t(const GemvParams& p, const GemvPlan& pl, uint32_t flags, cudaStream_t st) {
-    auto kern = k_gemv<D, NB, RPL, NW, ST>;
+    auto kern = k_gemv<D, NB, NW, ST>;
     static size_t lim = 0;
     static std::once_flag once;
     std::call_once(once, [&] { lim = set_max_dyn_smem(kern); });
@@ -319,29 +324,15 @@ static fasq_status launch_gemv_t(const GemvParams& p, const GemvPlan& pl, uint32
 
 template <int D, int NB>
 static fasq_status dispatch_cfg(const GemvParams& p, const GemvPlan& pl, uint32_t flags, cudaStream_t st) {
-#define FASQ_GEMV_CFG_CASE(RPL_, NW_, ST_) \
-    if (pl.rpl == RPL_ && pl.nw == NW_ && pl.st == ST_) return launch_gemv_t<D, NB, RPL_, NW_, ST_>(p, pl, flags, st);
-    FASQ_GEMV_CFG_CASE(2, 8, 2)
-    FASQ_GEMV_CFG_CASE(2, 8, 3)
-    FASQ_GEMV_CFG_CASE(1, 8, 2)
-    FASQ_GEMV_CFG_CASE(1, 8, 3)
-    FASQ_GEMV_CFG_CASE(4, 8, 2)
-    FASQ_GEMV_CFG_CASE(4, 8, 3)
-    FASQ_GEMV_CFG_CASE(2, 16, 2)
-    FASQ_GEMV_CFG_CASE(2, 16, 3)
-    FASQ_GEMV_CFG_CASE(1, 16, 3)
-    FASQ_GEMV_CFG_CASE(1, 8, 1)
-    FASQ_GEMV_CFG_CASE(1, 16, 1)
-    FASQ_GEMV_CFG_CASE(2, 16, 1)
-    FASQ_GEMV_CFG_CASE(8, 4, 3)
-    FASQ_GEMV_CFG_CASE(4, 4, 4)
-    FASQ_GEMV_CFG_CASE(2, 8, 4)
-    FASQ_GEMV_CFG_CASE(8, 8, 2)
-    FASQ_GEMV_CFG_CASE(4, 16, 2)
-    FASQ_GEMV_CFG_CASE(1, 16, 2)
-    FASQ_GEMV_CFG_CASE(4, 4, 2)
-    FASQ_GEMV_CFG_CASE(2, 16, 2)
-    FASQ_GEMV_CFG_CASE(2, 8, 1)
+#define FASQ_GEMV_CFG_CASE(NW_, ST_) \
+    if (pl.nw == NW_ && pl.st == ST_) return launch_gemv_t<D, NB, NW_, ST_>(p, pl, flags, st);
+    FASQ_GEMV_CFG_CASE(16, 3)
+    FASQ_GEMV_CFG_CASE(16, 2)
+    FASQ_GEMV_CFG_CASE(16, 1)
+    FASQ_GEMV_CFG_CASE(16, 4)
+    FASQ_GEMV_CFG_CASE(8, 3)
+    FASQ_GEMV_CFG_CASE(8, 2)
+    FASQ_GEMV_CFG_CASE(8, 1)
 #undef FASQ_GEMV_CFG_CASE
     set_error("gemv: no kernel instantiated for this tiling");
     return FASQ_E_UNSUPPORTED;
@@ -363,30 +354,32 @@ static fasq_status dispatch_nb(int NB, const GemvParams& p, const GemvPlan& pl, 
 // launch add up to <= #SMs so they are co-resident (the split-K merge spins on
 // its peers) and each SM runs one CTA of this launch -- the second SM slot is
 // left for the NEXT launch's prefetch under PDL.  CTAs are shared between the
-// layers in proportion to their index bytes.  Env FASQ_GEMV_CFG="rpl,nw,stages"
+// layers in proportion to their index bytes.  Env FASQ_GEMV_CFG="nw,stages"
 // overrides the default tiling (tuning only).
+static int gemv_rows_per_warp(int NB) { return NB == 1 ? 64 : NB == 2 ? 32 : NB == 4 ? 16 : 8; }
+
 static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB, bool spin_merge = true) {
     GemvPlan pl{};
     pl.nw = 16;
-    pl.rpl = NB <= 2 ? 2 : 1;
     pl.st = 3;
+    pl.rw = gemv_rows_per_warp(NB);
     if (const char* e = getenv("FASQ_GEMV_CFG")) {
-        int a = 0, b = 0, c = 0;
-        if (sscanf(e, "%d,%d,%d", &a, &b, &c) == 3) { pl.rpl = a; pl.nw = b; pl.st = c; }
+        int a = 0, b = 0;
+        if (sscanf(e, "%d,%d", &a, &b) == 2) { pl.nw = a; pl.st = b; }
     }
     pl.nl = nl;
     const int E = Ls[0]->E;
     int maxC = 0;
     for (int l = 0; l < nl; ++l) maxC = std::max(maxC, Ls[l]->C);
     // large codebook images (d = 4/8 with C = 256: 64/128 KiB per group): fewer
-    // stages, then fewer rows per lane
-    auto ring = [&](int st, int rpl) {
-        return (size_t)st * ((size_t)maxC * 32 * E + (size_t)32 * pl.nw * rpl * 32) + 16 * 1024;
+    // stages, then fewer rows per CTA
+    auto ring = [&](int st, int nw) {
+        return (size_t)st * ((size_t)maxC * 32 * E + (size_t)pl.rw * nw * 32) + 16 * 1024;
     };
-    while (pl.st > 2 && ring(pl.st, pl.rpl) > kSmemBudget) --pl.st;
-    if (ring(pl.st, pl.rpl) > kSmemBudget && pl.rpl > 1) pl.rpl = 1;
-    while (pl.st > 1 && ring(pl.st, pl.rpl) > kSmemBudget) --pl.st;
-    pl.R = 32 * pl.nw * pl.rpl;
+    while (pl.st > 2 && ring(pl.st, pl.nw) > kSmemBudget) --pl.st;
+    if (ring(pl.st, pl.nw) > kSmemBudget && pl.nw > 8) pl.nw = 8;
+    while (pl.st > 1 && ring(pl.st, pl.nw) > kSmemBudget) --pl.st;
+    pl.R = pl.rw * pl.nw;
     int sms = num_sms();
     if (!spin_merge) {   // ACC outputs: no co-residency requirement; FASQ_GEMV_OCC = CTAs per SM to plan for
         if (const char* e = getenv("FASQ_GEMV_OCC")) sms *= std::max(1, atoi(e));
@@ -418,7 +411,7 @@ static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB, bool spin
     pl.grid = total;
     pl.gmax = 1;
     for (int l = 0; l < nl; ++l) pl.gmax = std::max(pl.gmax, (Ls[l]->n_groups + pl.ksplit[l] - 1) / pl.ksplit[l]);
-    const size_t xg = (size_t)64 * NB * E;
+    const size_t xg = (size_t)32 * NB * E;
     pl.smem = (size_t)pl.st * ((size_t)maxC * 32 * E + (size_t)pl.R * 32) + (size_t)pl.gmax * xg + 16 * pl.st;
     return pl;
 }

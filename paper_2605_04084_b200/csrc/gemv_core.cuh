@@ -1,7 +1,16 @@
 // gemv_core.cuh -- device building blocks of the FASQ decode GEMV, shared by
 // the per-launch kernel (gemv.cu) and the persistent decode-chain kernel
-// (chain.cu).  See gemv.cu for the design; everything here is the hot loop
-// of Eq. 3 on the rotated lane = row layout.
+// (chain.cu): the hot loop of Eq. 3 on the lane = SUBSPACE
+// mapping.
+//
+// A warp owns RW output rows and, per 32-subspace group, lane s owns the
+// group's subspace s: it keeps x_s in registers, loads the indices of 16 rows
+// with one LDS.128 (sub-major index layout, fasq_internal.cuh), and for each
+// row gathers centroid T_cluster[s][k] from the SMEM codebook image
+// [C][32][E] -- lane s always hits bank s, so every warp-gather is one
+// wavefront whatever the indices are -- and accumulates dot(x_s, c) into the
+// row's register.  After the K range, the 32 lanes' per-row partial sums are
+// added by a transposed butterfly (fixed order -> deterministic).
 #pragma once
 #include "fasq_internal.cuh"
 
@@ -9,18 +18,35 @@ namespace fasq {
 namespace core {
 
 constexpr float kAccScale = 4294967296.0f;      // FASQ_ACC_I64 units: 2^-32
+
+// Plain C++ shared-memory loads (pointers derived from the kernel's
+// __shared__ buffer -> LDS): unlike asm volatile they can be scheduled freely
+// between the mbarrier waits/arrivals, which are asm volatile with a memory
+// clobber and therefore order them.
+template <class T>
+__device__ __forceinline__ T lds(const uint8_t* p) { return *reinterpret_cast<const T*>(p); }
 constexpr double kAccInv = 1.0 / 4294967296.0;
 
-// x staging for a K-range of ng groups: [gl][64 entries][NB][E] -- the 32
-// subspaces of each group twice so the rotated index (s + rot) needs no wrap.
+// Rows per consumer warp for an NB-wide batch (acc registers RW*NB = 64).
+template <int NB>
+struct RowsPerWarp {
+    static constexpr int value = NB == 1 ? 64 : NB == 2 ? 32 : NB == 4 ? 16 : 8;
+};
+
+template <int D>
+struct Entry {
+    static constexpr int value = D <= 2 ? 4 : 2 * D;
+};
+
+// x staging for a K-range of ng groups: [gl][32 subspaces][NB][E] bytes.
 // x is fp16 [B][F_in] or (x_acc) FASQ_ACC_I64 [B][F_in] rounded to fp16 here.
 template <int D, int NB, int NW>
 __device__ __forceinline__ void stage_x(uint8_t* s_x, const __half* x, int x_acc, int F_in, int B, int N_ss,
                                         int g_begin, int ng) {
-    constexpr int E = D <= 2 ? 4 : 2 * D;
+    constexpr int E = Entry<D>::value;
     const int tid = threadIdx.x;
-    const int n_ent = ng * 64 * NB;   // entries of E bytes
-    // all global loads first (one round trip), then the SMEM stores
+    const int n_ent = ng * 32 * NB;   // entries of E bytes
+    // all global loads of a pass first (one round trip), then the SMEM stores
     constexpr int XPT = 4;            // entries per thread per pass
     for (int t0 = tid; t0 < n_ent; t0 += NW * 32 * XPT) {
         uint32_t w[XPT][4];
@@ -30,15 +56,25 @@ __device__ __forceinline__ void stage_x(uint8_t* s_x, const __half* x, int x_acc
             w[u][0] = w[u][1] = w[u][2] = w[u][3] = 0u;
             if (t >= n_ent) continue;
             const int b = t % NB;
-            const int e64 = (t / NB) % 64;
-            const int gl = t / (NB * 64);
-            const int ss = (g_begin + gl) * 32 + (e64 & 31);
+            const int e32 = (t / NB) & 31;
+            const int gl = t / (NB * 32);
+            const int ss = (g_begin + gl) * 32 + e32;
             if (b < B && ss < N_ss && x_acc) {
                 const long long* src = reinterpret_cast<const long long*>(x) + (size_t)b * F_in + (size_t)ss * D;
+                long long v[D];
+                if (D == 1) {
+                    v[0] = __ldcg(src);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < D; e += 2) {
+                        const longlong2 t2 = __ldcg(reinterpret_cast<const longlong2*>(src + e));
+                        v[e] = t2.x;
+                        v[(e + 1) % D] = t2.y;
+                    }
+                }
 #pragma unroll
                 for (int e = 0; e < D; ++e) {
-                    const long long v = __ldcg(src + e);
-                    const uint32_t h = __half_as_ushort(__double2half((double)v * kAccInv));
+                    const uint32_t h = __half_as_ushort(__double2half((double)v[e] * kAccInv));
                     w[u][e >> 1] |= h << (16 * (e & 1));
                 }
             } else if (b < B && ss < N_ss) {
@@ -67,112 +103,186 @@ __device__ __forceinline__ void stage_x(uint8_t* s_x, const __half* x, int x_acc
     }
 }
 
-struct LaneConsts {
-    int hA, rot;
-    uint32_t Lr[16];
+// This lane's x_s for every batch row of staged group gl.
+template <int D, int NB>
+__device__ __forceinline__ void load_x(uint32_t (&xv)[NB][Entry<D>::value / 4], const uint8_t* x_grp, int lane) {
+    constexpr int E = Entry<D>::value;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const uint8_t* a = x_grp + (lane * NB + b) * E;
+        if (E == 4) {
+            xv[b][0] = lds<uint32_t>(a);
+        } else if (E == 8) {
+            const uint2 t = lds<uint2>(a);
+            xv[b][0] = t.x;
+            xv[b][1 % (E / 4)] = t.y;
+        } else {
+            const uint4 t = lds<uint4>(a);
+            xv[b][0] = t.x;
+            xv[b][1 % (E / 4)] = t.y;
+            xv[b][2 % (E / 4)] = t.z;
+            xv[b][3 % (E / 4)] = t.w;
+        }
+    }
+}
+
+// SMEM byte offset of this warp's first index chunk inside an index stage
+// (rows [wrow0, wrow0 + RW) of the stage's row tile, lane = subspace).
+__device__ __forceinline__ uint32_t idx_lane_off(int wrow0, int lane) {
+    return (uint32_t)(wrow0 >> 6) * 2048u + (uint32_t)lane * 64u;
+}
+
+// One 32-subspace group: acc[j][b] += dot(x[b]_s, c_s[k_s(row j)]) for the
+// warp's RW rows (lane s = subspace s).  idx_lane = idx_lane_base(...) +
+// stage base; cbs = codebook image stage base.
+template <int D, int NB, int RW>
+__device__ __forceinline__ void compute_group(float (&acc)[RW][NB], const uint8_t* idx_lane, const uint8_t* cbs,
+                                              const uint32_t (&xv)[NB][Entry<D>::value / 4], int wrow0, int lane) {
+    constexpr int E = Entry<D>::value;
+    constexpr int NCH = RW >= 16 ? RW / 16 : 1;        // 16-row chunks per warp
+    const int c0 = (wrow0 >> 4) & 3;                   // first chunk of the warp in its 64-row block
+    const uint32_t rot = (uint32_t)(lane >> 1);
+    // E = 4: address = cbs + 4*s + (k << 7)        (PRMT extracts k, LEA scales)
+    // E = 8: address = cbs + (k << 8 | 8*s)        (one PRMT)
+    // E = 16: address = cbs + (k << 8 | 8*s) << 1  (PRMT + shift)
+    const uint8_t* cbl = cbs + lane * 4;
+    const uint32_t L8 = (uint32_t)lane * 8u;
+#pragma unroll
+    for (int ci = 0; ci < NCH; ++ci) {
+        const uint8_t* ca = idx_lane + 16u * (((uint32_t)(c0 + ci) + rot) & 3u);
+        uint32_t w[4];
+        if (RW >= 16) {
+            const uint4 v = lds<uint4>(ca);
+            w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+        } else {   // RW = 8: half a chunk
+            const uint2 v = lds<uint2>(ca + (wrow0 & 8));
+            w[0] = v.x; w[1] = v.y; w[2] = 0u; w[3] = 0u;
+        }
+        // all gathers of a batch first, then the FMAs: keeps LDS_BATCH loads in
+        // flight per warp (ptxas otherwise serialises gather -> use)
+        constexpr int NJ = RW >= 16 ? 16 : RW;
+        constexpr int JB = E == 4 ? NJ : 8;                // rows per gather batch
+#pragma unroll
+        for (int j0 = 0; j0 < NJ; j0 += JB) {
+            if (E == 4) {
+                uint32_t c[JB];
+#pragma unroll
+                for (int j = 0; j < JB; ++j) {
+                    const uint32_t k = dev::prmt(w[(j0 + j) >> 2], 0u, 0x4440u | (uint32_t)((j0 + j) & 3));
+                    c[j] = lds<uint32_t>(cbl + (k << 7));
+                }
+#pragma unroll
+                for (int j = 0; j < JB; ++j)
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        float& a = acc[ci * 16 + j0 + j][b];
+                        a = (D == 1) ? dev::fhfma1(c[j], xv[b][0], a) : dev::fhfma2(c[j], xv[b][0], a);
+                    }
+            } else if (E == 8) {
+                uint2 c[JB];
+#pragma unroll
+                for (int j = 0; j < JB; ++j) {
+                    const uint32_t ad = dev::prmt(w[(j0 + j) >> 2], L8, 0x7704u | ((uint32_t)((j0 + j) & 3) << 4));
+                    c[j] = lds<uint2>(cbs + ad);
+                }
+#pragma unroll
+                for (int j = 0; j < JB; ++j)
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        float& a = acc[ci * 16 + j0 + j][b];
+                        a = dev::fhfma2(c[j].x, xv[b][0], a);
+                        a = dev::fhfma2(c[j].y, xv[b][1 % (E / 4)], a);
+                    }
+            } else {
+                uint4 c[JB];
+#pragma unroll
+                for (int j = 0; j < JB; ++j) {
+                    const uint32_t ad = dev::prmt(w[(j0 + j) >> 2], L8, 0x7704u | ((uint32_t)((j0 + j) & 3) << 4)) << 1;
+                    c[j] = lds<uint4>(cbs + ad);
+                }
+#pragma unroll
+                for (int j = 0; j < JB; ++j)
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        float& a = acc[ci * 16 + j0 + j][b];
+                        a = dev::fhfma2(c[j].x, xv[b][0], a);
+                        a = dev::fhfma2(c[j].y, xv[b][1 % (E / 4)], a);
+                        a = dev::fhfma2(c[j].z, xv[b][2 % (E / 4)], a);
+                        a = dev::fhfma2(c[j].w, xv[b][3 % (E / 4)], a);
+                    }
+            }
+        }
+    }
+}
+
+// Transposed butterfly over the 32 lanes: v[i] (i < N, N = 32/16/8) holds
+// this lane's partial of row i; afterwards v[0] holds the total of row
+// (lane >> (5 - log2 N)) (each row on 32/N lanes).  Fixed order.
+template <int N>
+__device__ __forceinline__ void transpose_reduce(float (&v)[N], int lane) {
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+        const int m = 16 >> r;
+        const int n = N >> r;          // live values before this round (compile-time after unrolling)
+        if (n > 1) {
+            const int half = n >> 1;
+            const bool up = (lane & m) != 0;
+#pragma unroll
+            for (int i = 0; i < half; ++i) {
+                const float send = up ? v[i] : v[i + half];
+                const float keep = up ? v[i + half] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+            }
+        } else {
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], m);
+        }
+    }
+}
+
+// Row totals of the warp: out[h][b] = total of row h*32 + rsel (RW = 64: two
+// halves) where rsel = lane >> shift; `own` = this lane writes those rows.
+template <int NB, int RW>
+struct RowTotals {
+    static constexpr int H = RW > 32 ? RW / 32 : 1;
+    static constexpr int N = RW > 32 ? 32 : RW;
+    float v[H][NB];
+    int rsel;
+    bool own;
 };
 
-// Lane constants: the conflict-free LDS.128 half order (hA), the lane's
-// subspace rotation, and the prmt lowbytes L[w] = [8*sub(2w), 8*sub(2w+1), 0, 0]
-// so that prmt(idx word, L, sel) = k*256 + 8*sub (E=4: >>1 -> k*128 + 4*sub;
-// E=8: as is; E=16: <<1 -> k*512 + 16*sub).
-__device__ __forceinline__ void lane_consts(int lane, LaneConsts& lc) {
-    lc.hA = (lane >> 2) & 1;
-    lc.rot = (lane + 16 * lc.hA) & 31;
+template <int NB, int RW>
+__device__ __forceinline__ void reduce_rows(const float (&acc)[RW][NB], RowTotals<NB, RW>& t, int lane) {
+    constexpr int H = RowTotals<NB, RW>::H, N = RowTotals<NB, RW>::N;
+    constexpr int shift = N == 32 ? 0 : N == 16 ? 1 : 2;
 #pragma unroll
-    for (int w = 0; w < 16; ++w)
-        lc.Lr[w] = (uint32_t)(((2 * w + lc.rot) & 31) * 8) | ((uint32_t)(((2 * w + 1 + lc.rot) & 31) * 8) << 8);
-}
-
-// One 32-subspace group for this lane's RPL rows: acc[q][b] += sum over the
-// group's subspaces of dot(x_ss, c[k]) (PRMT, LEA, LDS, FHFMA per index).
-template <int D, int NB, int RPL>
-__device__ __forceinline__ void compute_group(float (&acc)[RPL][NB], uint32_t idx_slot, uint32_t cbs, uint32_t x_grp,
-                                              int warp_row0, int rows_valid, int lane, const LaneConsts& lc) {
-    constexpr int E = D <= 2 ? 4 : 2 * D;
-    uint32_t iw[RPL][8];
-#pragma unroll
-    for (int q = 0; q < RPL; ++q) {
-        const int rl = warp_row0 + q * 32 + lane;
-        const uint32_t a = idx_slot + (uint32_t)rl * 32u;
-        if (warp_row0 + q * 32 < rows_valid) {
-            uint4 v0 = dev::lds128(a + 16u * lc.hA);
-            uint4 v1 = dev::lds128(a + 16u * (1 - lc.hA));
-            iw[q][0] = v0.x; iw[q][1] = v0.y; iw[q][2] = v0.z; iw[q][3] = v0.w;
-            iw[q][4] = v1.x; iw[q][5] = v1.y; iw[q][6] = v1.z; iw[q][7] = v1.w;
-        } else {
-#pragma unroll
-            for (int w = 0; w < 8; ++w) iw[q][w] = 0u;
-        }
-    }
-    const uint32_t xb = x_grp + (uint32_t)lc.rot * (NB * E);
-#pragma unroll
-    for (int s = 0; s < 32; ++s) {
-        uint32_t xv[NB][E / 4];
+    for (int h = 0; h < H; ++h)
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
-            const uint32_t xa = xb + (uint32_t)(s * NB * E + b * E);
-            if (E == 4) {
-                xv[b][0] = dev::lds32(xa);
-            } else if (E == 8) {
-                uint2 t2 = dev::lds64(xa);
-                xv[b][0] = t2.x; xv[b][1 % (E / 4)] = t2.y;
-            } else {
-                uint4 t4 = dev::lds128(xa);
-                xv[b][0] = t4.x; xv[b][1 % (E / 4)] = t4.y;
-                xv[b][2 % (E / 4)] = t4.z; xv[b][3 % (E / 4)] = t4.w;
-            }
+            float v[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) v[i] = acc[h * 32 + i][b];
+            transpose_reduce<N>(v, lane);
+            t.v[h][b] = v[0];
         }
-        const int wi = s >> 2, j = s & 3, lw = s >> 1, lj = s & 1;
-        // byte0 = L byte lj (8*sub), byte1 = idx byte j (k), bytes 2,3 = L byte 2 (0)
-        const uint32_t sel = (uint32_t)(4 + lj) | ((uint32_t)j << 4) | (6u << 8) | (6u << 12);
-#pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-            if (warp_row0 + q * 32 >= rows_valid) continue;
-            uint32_t addr = dev::prmt(iw[q][wi], lc.Lr[lw], sel);
-            if (E == 4) addr >>= 1;
-            if (E == 16) addr <<= 1;
-            if (E == 4) {
-                const uint32_t c = dev::lds32(cbs + addr);
-#pragma unroll
-                for (int b = 0; b < NB; ++b)
-                    acc[q][b] = (D == 1) ? dev::fhfma1(c, xv[b][0], acc[q][b]) : dev::fhfma2(c, xv[b][0], acc[q][b]);
-            } else if (E == 8) {
-                const uint2 c = dev::lds64(cbs + addr);
-#pragma unroll
-                for (int b = 0; b < NB; ++b) {
-                    acc[q][b] = dev::fhfma2(c.x, xv[b][0], acc[q][b]);
-                    acc[q][b] = dev::fhfma2(c.y, xv[b][1 % (E / 4)], acc[q][b]);
-                }
-            } else {
-                const uint4 c = dev::lds128(cbs + addr);
-#pragma unroll
-                for (int b = 0; b < NB; ++b) {
-                    acc[q][b] = dev::fhfma2(c.x, xv[b][0], acc[q][b]);
-                    acc[q][b] = dev::fhfma2(c.y, xv[b][1 % (E / 4)], acc[q][b]);
-                    acc[q][b] = dev::fhfma2(c.z, xv[b][2 % (E / 4)], acc[q][b]);
-                    acc[q][b] = dev::fhfma2(c.w, xv[b][3 % (E / 4)], acc[q][b]);
-                }
-            }
-        }
-    }
+    t.rsel = lane >> shift;
+    t.own = (lane & ((1 << shift) - 1)) == 0;
 }
 
-// FASQ_ACC_I64 output: round each fp32 partial to int64 units of 2^-32 and
+// FASQ_ACC_I64 output: round each fp32 row total to int64 units of 2^-32 and
 // red.add it (integer addition is associative -> deterministic).
-template <int RPL, int NB>
-__device__ __forceinline__ void acc_store(const float (&acc)[RPL][NB], unsigned long long* y, int r0, int warp_row0,
-                                          int rows_valid, int F_out, int B, int lane) {
+template <int NB, int RW>
+__device__ __forceinline__ void acc_store(const RowTotals<NB, RW>& t, unsigned long long* y, int row0, int F_out,
+                                          int B) {
+    if (!t.own) return;
 #pragma unroll
-    for (int q = 0; q < RPL; ++q) {
-        const int row = r0 + warp_row0 + q * 32 + lane;
-        if (warp_row0 + q * 32 >= rows_valid || row >= F_out) continue;
+    for (int h = 0; h < RowTotals<NB, RW>::H; ++h) {
+        const int row = row0 + h * 32 + t.rsel;
+        if (row >= F_out) continue;
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
             if (b >= B) continue;
-            const long long v = __float2ll_rn(acc[q][b] * kAccScale);
-            unsigned long long* dst = y + (size_t)b * F_out + row;
-            asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(dst), "l"(v) : "memory");
+            const long long v = __float2ll_rn(t.v[h][b] * kAccScale);
+            asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(y + (size_t)b * F_out + row), "l"(v) : "memory");
         }
     }
 }

@@ -23,7 +23,7 @@ fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t
     L->group = group;
     L->N_ss = (int32_t)N_ss;
     L->N_cb = (int32_t)(N_ss / group);
-    L->F_out_pad = (int32_t)((F_out + 31) / 32 * 32);
+    L->F_out_pad = (int32_t)((F_out + kRowBlock - 1) / kRowBlock * kRowBlock);
     L->n_groups = (int32_t)((N_ss + kGroupSubs - 1) / kGroupSubs);
     L->E = entry_bytes(d);
     L->idx_bytes = (int64_t)L->n_groups * L->F_out_pad * kGroupSubs;
@@ -44,41 +44,40 @@ fasq_status alloc_layer_storage(fasq_layer* L) {
     return FASQ_OK;
 }
 
-// One thread per (group g, padded row r): 32 output bytes.
+// One thread per (group g, 16-row chunk, subspace s): 16 output bytes.
 __global__ void k_idx_logical_to_phys(const uint8_t* __restrict__ idx_log, uint8_t* __restrict__ phys,
                                       int F_out, int F_out_pad, int N_ss, int n_groups) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (int64_t)n_groups * F_out_pad) return;
-    int g = (int)(t / F_out_pad);
-    int r = (int)(t % F_out_pad);
-    uint32_t w[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) w[q] = 0;
-    if (r < F_out) {
-#pragma unroll
-        for (int p = 0; p < 32; ++p) {
-            int ss = g * kGroupSubs + ((p + r) & 31);
-            uint32_t v = ss < N_ss ? idx_log[(int64_t)ss * F_out + r] : 0u;
-            w[p >> 2] |= v << (8 * (p & 3));
-        }
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n_chunks = (int64_t)F_out_pad / 16;
+    if (t >= (int64_t)n_groups * n_chunks * kGroupSubs) return;
+    const int s = (int)(t % kGroupSubs);
+    const int64_t ch = (t / kGroupSubs) % n_chunks;
+    const int64_t g = t / (kGroupSubs * n_chunks);
+    const int64_t ss = g * kGroupSubs + s;
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    for (int j = 0; j < 16; ++j) {
+        const int64_t r = ch * 16 + j;
+        const uint32_t v = (ss < N_ss && r < F_out) ? idx_log[ss * F_out + r] : 0u;
+        w[j >> 2] |= v << (8 * (j & 3));
     }
-    uint4* dst = reinterpret_cast<uint4*>(phys + t * 32);
-    dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-    dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    *reinterpret_cast<uint4*>(phys + idx_offset(g, ch * 16, s, F_out_pad)) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 __global__ void k_idx_phys_to_logical(const uint8_t* __restrict__ phys, uint8_t* __restrict__ idx_log,
                                       int F_out, int F_out_pad, int N_ss, int n_groups) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (int64_t)n_groups * F_out_pad) return;
-    int g = (int)(t / F_out_pad);
-    int r = (int)(t % F_out_pad);
-    if (r >= F_out) return;
-    const uint8_t* src = phys + t * 32;
-#pragma unroll 4
-    for (int p = 0; p < 32; ++p) {
-        int ss = g * kGroupSubs + ((p + r) & 31);
-        if (ss < N_ss) idx_log[(int64_t)ss * F_out + r] = src[p];
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n_chunks = (int64_t)F_out_pad / 16;
+    if (t >= (int64_t)n_groups * n_chunks * kGroupSubs) return;
+    const int s = (int)(t % kGroupSubs);
+    const int64_t ch = (t / kGroupSubs) % n_chunks;
+    const int64_t g = t / (kGroupSubs * n_chunks);
+    const int64_t ss = g * kGroupSubs + s;
+    if (ss >= N_ss) return;
+    const uint4 v = *reinterpret_cast<const uint4*>(phys + idx_offset(g, ch * 16, s, F_out_pad));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    for (int j = 0; j < 16; ++j) {
+        const int64_t r = ch * 16 + j;
+        if (r < F_out) idx_log[ss * F_out + r] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
     }
 }
 
@@ -109,7 +108,7 @@ fasq_status build_physical_from_logical(fasq_layer* L, const __half* cb_logical,
                                         cudaStream_t st) {
     if (cb_logical != L->cb)
         FASQ_CUDA_TRY(cudaMemcpyAsync(L->cb, cb_logical, (size_t)L->cb_bytes, cudaMemcpyDeviceToDevice, st));
-    int64_t n = (int64_t)L->n_groups * L->F_out_pad;
+    int64_t n = (int64_t)L->n_groups * (L->F_out_pad / 16) * kGroupSubs;
     k_idx_logical_to_phys<<<nblk(n, 256), 256, 0, st>>>(idx_logical, L->idx, (int)L->F_out, L->F_out_pad,
                                                          L->N_ss, L->n_groups);
     FASQ_CUDA_TRY(cudaGetLastError());
@@ -128,7 +127,7 @@ fasq_status export_logical(const fasq_layer* L, __half* cb_out, uint8_t* idx_out
     if (cb_out)
         FASQ_CUDA_TRY(cudaMemcpyAsync(cb_out, L->cb, (size_t)L->cb_bytes, cudaMemcpyDeviceToDevice, st));
     if (idx_out) {
-        int64_t n = (int64_t)L->n_groups * L->F_out_pad;
+        int64_t n = (int64_t)L->n_groups * (L->F_out_pad / 16) * kGroupSubs;
         k_idx_phys_to_logical<<<nblk(n, 256), 256, 0, st>>>(L->idx, idx_out, (int)L->F_out, L->F_out_pad,
                                                              L->N_ss, L->n_groups);
         FASQ_CUDA_TRY(cudaGetLastError());

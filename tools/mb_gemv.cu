@@ -1,0 +1,268 @@
+// GEMV main-loop microbenchmark (B200): separates the data-movement bound
+// from the SMEM/issue bound of candidate decode-GEMV inner loops.
+//
+//   VAR 0: retired (lane = row with row-rotated idx; see git history)
+//   VAR 1: lane = subspace (x in a register, idx sub-major per 64-row block,
+//          cb address = PRMT + LEA, transposed reduction at the end)
+//   MODE 0: full;  1: data movement only (consumers wait + release);
+//           2: compute only (the ring is filled once and re-read).
+//
+// Every CTA streams `ng` groups of its own idx tile (HBM) plus the shared
+// codebook image of each group (L2 after the first CTA).  Data are random
+// bytes; only throughput is measured.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/mb_gemv tools/mb_gemv.cu
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_2605_04084_b200/csrc/gemv_core.cuh"
+
+using namespace fasq;
+
+constexpr int D = 2, E = 4, C = 256;
+constexpr uint32_t CBB = C * 32 * E;   // 32 KiB per group
+
+template <int NW>
+__device__ __forceinline__ void transpose_reduce32(float (&v)[32], int lane) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+        const bool up = (lane & m) != 0;
+#pragma unroll
+        for (int i = 0; i < m; ++i) {
+            const float send = up ? v[i] : v[i + m];
+            const float keep = up ? v[i + m] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+        }
+    }
+}
+
+template <int VAR, int RPL, int NW, int ST, int MODE>
+__global__ void __launch_bounds__((NW + 1) * 32, 1)
+    k_mb(const uint8_t* __restrict__ idx, const uint8_t* __restrict__ cb, int ng, float* out) {
+    constexpr int R = VAR == 0 ? 32 * NW * RPL : 64 * NW;
+    constexpr uint32_t IDXB = R * 32;
+    static_assert(VAR != 3 || R == 64 * NW, "");
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* s_cb = smem;
+    uint8_t* s_idx = s_cb + (VAR >= 2 ? 2 * 65536 : ST * CBB);
+    uint8_t* s_x = s_idx + ST * IDXB;                     // [64][E] (VAR 0) / [32][E] (VAR 1)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_x + 64 * E);
+    const uint32_t cb_u = dev::smem_u32(s_cb), idx_u = dev::smem_u32(s_idx), x_u = dev::smem_u32(s_x);
+    const uint32_t full0 = dev::smem_u32(&bars[0]), empty0 = dev::smem_u32(&bars[ST]);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) {
+            dev::mbar_init(full0 + 8 * s, 1);
+            dev::mbar_init(empty0 + 8 * s, NW);
+        }
+        dev::fence_barrier_init();
+    }
+    if (threadIdx.x < 64) reinterpret_cast<uint32_t*>(s_x)[threadIdx.x] = 0x3c003c00u ^ (threadIdx.x * 0x00010001u);
+    __syncthreads();
+    const uint8_t* my_idx = idx + (size_t)blockIdx.x * ng * IDXB;
+    if (warp == NW) {
+        if (lane == 0) {
+            const int nload = MODE == 2 ? (ng < ST ? ng : ST) : ng;
+            for (int g = 0; g < nload; ++g) {
+                const int slot = g % ST;
+                if (g >= ST) dev::mbar_wait(empty0 + 8 * slot, ((g / ST) + 1) & 1);
+                const uint32_t full = full0 + 8 * slot;
+                dev::mbar_arrive_expect_tx(full, (MODE == 3 ? 0u : CBB) + IDXB);
+                if (MODE != 3) dev::bulk_g2s(cb_u + slot * CBB, cb + (size_t)g * CBB, CBB, full);
+                dev::bulk_g2s(idx_u + slot * IDXB, my_idx + (size_t)g * IDXB, IDXB, full);
+            }
+        }
+        return;
+    }
+    if (VAR == 0) {
+        // (the old lane = row loop was retired with the sub-major index layout)
+    } else if (VAR == 3) {
+        // hybrid: lane = (u = lane>>3: 8-subspace segment, q = lane&7: row slot);
+        // rows wrow0 + 8i + q; paired stride-256 codebook rows (address = PRMT)
+        const int q = lane & 7, u = lane >> 3;
+        float acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+        uint32_t Lr[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const uint32_t s0 = 8 * u + ((2 * h + q) & 7), s1 = 8 * u + ((2 * h + 1 + q) & 7);
+            Lr[h] = (s0 * 4u) | ((s1 * 4u) << 8);
+        }
+        const uint32_t wrow = (uint32_t)warp * 64u;
+        for (int g = 0; g < ng; ++g) {
+            const int slot = g % ST;
+            if (MODE != 2 || g < ST) dev::mbar_wait(full0 + 8 * slot, (g / ST) & 1);
+            if (MODE != 1 && MODE != 3) {
+                uint32_t xr[8];
+#pragma unroll
+                for (int pp = 0; pp < 8; ++pp) xr[pp] = dev::lds32(x_u + 4u * (uint32_t)(8 * u + ((pp + q) & 7)));
+                const uint32_t ib = idx_u + slot * IDXB + (wrow + (uint32_t)q) * 32u + 8u * (uint32_t)u;
+                const uint32_t cbl = cb_u + (slot & 1) * 65536u + (g & 1) * 128u;
+#pragma unroll
+                for (int i0 = 0; i0 < 8; i0 += 4) {
+                    uint32_t c[4][8];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint2 v = dev::lds64(ib + (uint32_t)(i0 + i) * 8u * 32u);
+                        const uint32_t w[2] = {v.x, v.y};
+#pragma unroll
+                        for (int pp = 0; pp < 8; ++pp) {
+                            const uint32_t sel = (uint32_t)(4 + (pp & 1)) | ((uint32_t)(pp & 3) << 4) | (6u << 8) | (6u << 12);
+                            const uint32_t a = dev::prmt(w[pp >> 2], Lr[pp >> 1], sel);
+                            c[i][pp] = dev::lds32(cbl + a);
+                        }
+                    }
+#pragma unroll
+                    for (int pp = 0; pp < 8; ++pp)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) acc[i0 + i] = dev::fhfma2(c[i][pp], xr[pp], acc[i0 + i]);
+                }
+            }
+            __syncwarp();
+            if (MODE != 2 && lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+        }
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += acc[i];
+        s += __shfl_xor_sync(0xffffffffu, s, 8);
+        s += __shfl_xor_sync(0xffffffffu, s, 16);
+        out[blockIdx.x * R + threadIdx.x] = s;
+    } else if (VAR == 2) {
+        float acc[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+        const uint32_t xv = dev::lds32(x_u + lane * 4);
+        const uint32_t wrow = (uint32_t)warp * 64u * 32u + (uint32_t)lane * 64u;
+        const uint32_t swz = (uint32_t)(lane >> 1);
+        const uint32_t Lc = (uint32_t)lane * 4u;
+        for (int g = 0; g < ng; ++g) {
+            const int slot = g % ST;
+            if (MODE != 2 || g < ST) dev::mbar_wait(full0 + 8 * slot, (g / ST) & 1);
+            if (MODE != 1 && MODE != 3) {
+                const uint32_t ib = idx_u + slot * IDXB + wrow;
+                const uint32_t cbl = cb_u + (slot & 1) * 65536u;   // stride-256 rows (fake 64 KiB image)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const uint4 v = dev::lds128(ib + 16u * ((c + swz) & 3u));
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const uint32_t a = dev::prmt(w[q >> 2], Lc, 0x7740u | ((uint32_t)(q & 3) << 4) | 4u);
+                        const uint32_t cv = dev::lds32(cbl + a);
+                        acc[c * 16 + q] = dev::fhfma2(cv, xv, acc[c * 16 + q]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (MODE != 2 && lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+        }
+        float lo[32], hi[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            lo[i] = acc[i];
+            hi[i] = acc[32 + i];
+        }
+        transpose_reduce32<NW>(lo, lane);
+        transpose_reduce32<NW>(hi, lane);
+        out[blockIdx.x * R + warp * 64 + lane] = lo[0];
+        out[blockIdx.x * R + warp * 64 + 32 + lane] = hi[0];
+    } else {
+        float acc[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+        const uint32_t xv = dev::lds32(x_u + lane * 4);
+        const uint32_t wrow = (uint32_t)warp * 64u * 32u + (uint32_t)lane * 64u;   // this lane's sub in the warp's block
+        const uint32_t swz = (uint32_t)(lane >> 1);
+        for (int g = 0; g < ng; ++g) {
+            const int slot = g % ST;
+            if (MODE != 2 || g < ST) dev::mbar_wait(full0 + 8 * slot, (g / ST) & 1);
+            if (MODE != 1 && MODE != 3) {
+                const uint32_t ib = idx_u + slot * IDXB + wrow;
+                const uint32_t cbl = cb_u + slot * CBB + (uint32_t)lane * 4u;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const uint4 v = dev::lds128(ib + 16u * ((c + swz) & 3u));
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const uint32_t k = dev::prmt(w[q >> 2], 0u, 0x4440u | (uint32_t)(q & 3));
+                        const uint32_t cv = dev::lds32(cbl + (k << 7));
+                        acc[c * 16 + q] = dev::fhfma2(cv, xv, acc[c * 16 + q]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (MODE != 2 && lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+        }
+        float lo[32], hi[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            lo[i] = acc[i];
+            hi[i] = acc[32 + i];
+        }
+        transpose_reduce32<NW>(lo, lane);
+        transpose_reduce32<NW>(hi, lane);
+        out[blockIdx.x * R + warp * 64 + lane] = lo[0];
+        out[blockIdx.x * R + warp * 64 + 32 + lane] = hi[0];
+    }
+}
+
+template <int VAR, int RPL, int NW, int ST, int MODE>
+void run(const uint8_t* idx, const uint8_t* cb, int ng, float* out, int nsm, const char* name) {
+    constexpr int R = VAR == 0 ? 32 * NW * RPL : 64 * NW;
+    const size_t smem = (VAR >= 2 ? 2 * 65536 - (long)ST * CBB : 0) + ST * (CBB + (size_t)R * 32) + 64 * E + 16 * ST;
+    auto kern = k_mb<VAR, RPL, NW, ST, MODE>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        printf("%-28s smem %zu too large\n", name, smem);
+        cudaGetLastError();
+        return;
+    }
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(a);
+        kern<<<nsm, (NW + 1) * 32, smem>>>(idx, cb, ng, out);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (rep > 0 && ms < best) best = ms;
+    }
+    const double idx_bytes = (double)nsm * ng * R * 32;
+    printf("%-28s R=%4d mode %d: %7.1f us  idx %6.0f GB/s  (idx+cb into SMEM %6.0f GB/s)\n", name, R, MODE,
+           best * 1e3, idx_bytes / (best * 1e-3) / 1e9, (idx_bytes + (double)nsm * ng * CBB) / (best * 1e-3) / 1e9);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
+}
+
+int main() {
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int ng = 48;
+    const size_t idx_bytes = (size_t)nsm * ng * 1024 * 32;
+    uint8_t *idx, *cb;
+    float* out;
+    cudaMalloc(&idx, idx_bytes);
+    cudaMalloc(&cb, (size_t)ng * CBB);
+    cudaMalloc(&out, (size_t)nsm * 2048 * 4);
+    std::vector<uint8_t> h(idx_bytes);
+    srand(1);
+    for (auto& v : h) v = (uint8_t)rand();
+    cudaMemcpy(idx, h.data(), idx_bytes, cudaMemcpyHostToDevice);
+    std::vector<uint8_t> hc((size_t)ng * CBB);
+    for (size_t i = 0; i < hc.size(); i += 2) { hc[i] = (uint8_t)rand(); hc[i + 1] = 0x3c; }
+    cudaMemcpy(cb, hc.data(), hc.size(), cudaMemcpyHostToDevice);
+#define RUN3(VAR, RPL, NW, ST, NAME)                          \
+    run<VAR, RPL, NW, ST, 0>(idx, cb, ng, out, nsm, NAME);    \
+    run<VAR, RPL, NW, ST, 1>(idx, cb, ng, out, nsm, NAME);    \
+    run<VAR, RPL, NW, ST, 2>(idx, cb, ng, out, nsm, NAME);    \
+    run<VAR, RPL, NW, ST, 3>(idx, cb, ng, out, nsm, NAME);
+    RUN3(1, 1, 16, 3, "sub  nw16 st3");
+    RUN3(2, 1, 16, 2, "sub256 nw16 st2");
+    RUN3(3, 1, 16, 2, "hyb256 nw16 st2");
+    RUN3(3, 1, 16, 3, "hyb256 nw16 st3");
+    return 0;
+}
