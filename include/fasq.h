@@ -198,15 +198,18 @@ typedef struct fasq_chain fasq_chain; /* opaque */
 /* Plans a chain of grouped decode GEMVs (all layers: same d, B in 1..8) for
  * ONE persistent kernel (one CTA per SM, cooperative launch): every CTA
  * streams the codebook/index stages of all its steps through its SMEM ring
- * without draining at step boundaries, and waits on a grid-wide counter only
- * before reading a step's x.  Outputs are FASQ_ACC_I64 accumulators kept by
- * the chain (same numerics as chained fasq_gemv_grouped calls with ACC
- * outputs).  The layers must outlive the chain.  Synchronises `stream`. */
+ * without draining at step boundaries.  There is no grid-wide barrier:
+ * every output element is a counted accumulator (int64 fixed-point sum in
+ * FASQ_ACC_I64 units plus the number of K-split contributions), and a step
+ * polls only the words of its own K range until they are final.  Same
+ * numerics as chained fasq_gemv_grouped calls with FASQ_ACC_I64 outputs.
+ * The layers must outlive the chain.  Synchronises `stream`.
+ * FASQ_E_UNSUPPORTED: a step needs more row tiles than SMs, or > 63 K-splits. */
 fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int32_t B, void* stream,
                               fasq_chain** out);
 
 /* Runs the whole chain on x_dev (fp16 [B][F_in of the external-input steps]):
- * one memset node (accumulators + counter) and one kernel launch; graph
+ * one memset node (the accumulators) and one kernel launch; graph
  * capturable.  A chain instance must not run concurrently with itself. */
 fasq_status fasq_chain_run(fasq_chain* chain, const void* x_dev, void* stream);
 
@@ -216,8 +219,9 @@ fasq_status fasq_chain_output(const fasq_chain* chain, int32_t step, int32_t lay
                               fasq_dtype dtype, void* stream);
 /* Diagnostics: when trace_dev is not NULL, every later fasq_chain_run writes
  * per (step, CTA) four %globaltimer stamps (ns) into it, uint64
- * [n_steps][fasq_chain_ctas(chain)][4]: step entry, previous step complete
- * (grid wait done), x staged, outputs stored.  The buffer is the caller's
+ * [n_steps][fasq_chain_ctas(chain)][4]: step entry, inputs final and staged
+ * (dataflow wait done), CTA synchronised, outputs stored (CTAs without work
+ * in a step write only the first).  The buffer is the caller's
  * and must stay allocated while tracing is on; NULL turns tracing off. */
 fasq_status fasq_chain_trace(fasq_chain* chain, void* trace_dev);
 int32_t fasq_chain_ctas(const fasq_chain* chain);   /* CTAs (= SMs) the chain runs on; -1 for NULL */

@@ -13,13 +13,17 @@
 //    its steps back to back through the SMEM ring -- weights do not depend on
 //    x, so the ring keeps filling while the consumers wait for the previous
 //    step (no pipeline drain at step boundaries);
-//  * consumers wait on a grid-wide arrival counter (release/acquire) only
-//    before reading x; outputs are FASQ_ACC_I64 accumulators (exact int64
-//    fixed point -> deterministic, no split-K merge phase), read by the next
-//    step as x (rounded to fp16 once per element, as in FASQ_FLAG_X_ACC).
+//  * there is NO grid-wide barrier between steps: every output element is a
+//    "counted accumulator" (gemv_core.cuh): an int64 red.add target that
+//    carries the fixed-point sum (units 2^-32, exact and order-independent
+//    -> deterministic) AND the number of K-split contributions; a consumer
+//    polls exactly the words of its K range until each shows count == ks of
+//    the producing layer, then rounds them to fp16 x (as FASQ_FLAG_X_ACC).
+//    One L2 round trip after the data is final instead of a barrier round
+//    trip plus a load round trip.
 //
 // Numerics are identical to chaining fasq_gemv_grouped calls with FASQ_ACC_I64
-// outputs.
+// outputs (same fixed-point units and rounding).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -36,9 +40,10 @@ struct fasq_chain {
     std::vector<int> step_F_out_total;               // per step: sum of F_out of its layers
     std::vector<std::vector<int64_t>> acc_off;       // per step, per layer: word offset in the arena
     std::vector<std::vector<int64_t>> acc_Fout;
+    std::vector<std::vector<int>> acc_ks;            // per step, per layer: K-split count (contributions per word)
     std::vector<int> step_F_in;
     int ext_F_in = 0;
-    unsigned long long* arena = nullptr;             // [0]: grid counter (16 words), then accumulators
+    unsigned long long* arena = nullptr;             // [0..15]: reserved, then counted accumulators
     int64_t arena_words = 0;
     void* items = nullptr;                           // device [n_steps][nctas] ChainItem
     void* phases = nullptr;                          // device [n_steps] ChainPhase
@@ -52,21 +57,20 @@ namespace {
 struct ChainItem {
     const uint8_t* idx;
     const uint8_t* cbimg;
-    unsigned long long* y;      // ACC output [B][F_out]
+    unsigned long long* y;      // counted-accumulator output [B][F_out]
     int F_out, F_out_pad, N_ss, C;
     int r0, rows_valid, g_begin, g_end;
 };
 
 struct ChainPhase {
-    const long long* x_acc;     // ACC input (nullptr: the chain's external fp16 x)
-    int F_in, pad;
+    const unsigned long long* x_cnt;   // counted-accumulator input (nullptr: the chain's external fp16 x)
+    int F_in, x_ks;                    // x_ks: contributions per input word (K-split of the producer)
 };
 
 struct ChainParams {
     const ChainItem* items;
     const ChainPhase* phases;
     const __half* x_ext;        // [B][F_in of the first step]
-    unsigned* counter;          // grid arrival counter (zeroed per run)
     unsigned long long* trace;  // optional [n_steps][nctas][4] globaltimer stamps (fasq_chain_trace)
     int n_steps, nctas, B, gmax, cbb_max;
     int pf;                     // producer: L2-prefetch this many groups of the next step's item
@@ -135,61 +139,45 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     const int wrow0 = warp * RW;
     const uint8_t* idx_lane = s_idx + core::idx_lane_off(wrow0, lane);
     int it = 0;
-    unsigned arrived = 0;   // thread 0: counter value after its own last arrival
     for (int ph = 0; ph < p.n_steps; ++ph) {
-        // the work item and phase are read-only for the kernel's lifetime:
-        // load them into registers before the grid-wide wait (off the
-        // critical path that follows it)
+        // the work item and phase are read-only for the kernel's lifetime
         const ChainItem w = p.items[(size_t)ph * p.nctas + blockIdx.x];
         const ChainPhase phs = p.phases[ph];
         unsigned long long* tr = p.trace ? p.trace + ((size_t)ph * p.nctas + blockIdx.x) * 4 : nullptr;
         if (tr && threadIdx.x == 0) tr[0] = dev::globaltimer();
-        if (ph > 0) {   // every CTA of the previous step has published its outputs
-            if (threadIdx.x == 0) {
-                const unsigned target = (unsigned)ph * (unsigned)p.nctas;
-                unsigned v = arrived;
-                while ((int)(v - target) < 0)
-                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.counter) : "memory");
-            }
-            asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
-        }
-        if (tr && threadIdx.x == 0) tr[1] = dev::globaltimer();
-        if (w.rows_valid > 0) {
-            const int ng = w.g_end - w.g_begin;
-            const __half* xsrc = phs.x_acc ? reinterpret_cast<const __half*>(phs.x_acc) : p.x_ext;
-            core::stage_x<D, NB, NW>(s_x, xsrc, phs.x_acc != nullptr, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
-            asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
-            if (tr && threadIdx.x == 0) tr[2] = dev::globaltimer();
-            float acc[RW][NB];
-#pragma unroll
-            for (int q = 0; q < RW; ++q)
-#pragma unroll
-                for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
-            const bool active = wrow0 < w.rows_valid;
-            for (int i = 0; i < ng; ++i, ++it) {
-                const int slot = it % ST;
-                dev::mbar_wait(full0 + 8 * slot, (it / ST) & 1);
-                if (active) {
-                    uint32_t xv[NB][E / 4];
-                    core::load_x<D, NB>(xv, s_x + i * XG, lane);
-                    core::compute_group<D, NB, RW>(acc, idx_lane + slot * R * 32, s_cb + slot * p.cbb_max, xv,
-                                                   wrow0, lane);
-                }
-                __syncwarp();
-                if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
-            }
-            core::RowTotals<NB, RW> tot;
-            core::reduce_rows<NB, RW>(acc, tot, lane);
-            if (active) core::acc_store<NB, RW>(tot, w.y, w.r0 + wrow0, w.F_out, p.B);
-        }
-        // arrive: bar.sync orders this CTA's red.adds before thread 0's release
+        if (w.rows_valid <= 0) continue;
+        // every consumer warp is done with the previous step's s_x
         asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
-        if (tr && threadIdx.x == 0) tr[3] = dev::globaltimer();
-        if (threadIdx.x == 0) {
-            // the returned count tells the last arriver it need not poll
-            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(p.counter) : "memory");
-            arrived += 1;
+        const int ng = w.g_end - w.g_begin;
+        if (phs.x_cnt)   // dataflow wait: poll this CTA's input words until final
+            core::stage_x_counted<D, NB, NW>(s_x, phs.x_cnt, phs.x_ks, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
+        else
+            core::stage_x<D, NB, NW>(s_x, p.x_ext, 0, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
+        if (tr && threadIdx.x == 0) tr[1] = dev::globaltimer();
+        asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
+        if (tr && threadIdx.x == 0) tr[2] = dev::globaltimer();
+        float acc[RW][NB];
+#pragma unroll
+        for (int q = 0; q < RW; ++q)
+#pragma unroll
+            for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
+        const bool active = wrow0 < w.rows_valid;
+        for (int i = 0; i < ng; ++i, ++it) {
+            const int slot = it % ST;
+            dev::mbar_wait(full0 + 8 * slot, (it / ST) & 1);
+            if (active) {
+                uint32_t xv[NB][E / 4];
+                core::load_x<D, NB>(xv, s_x + i * XG, lane);
+                core::compute_group<D, NB, RW>(acc, idx_lane + slot * R * 32, s_cb + slot * p.cbb_max, xv, wrow0,
+                                               lane);
+            }
+            __syncwarp();
+            if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
         }
+        core::RowTotals<NB, RW> tot;
+        core::reduce_rows<NB, RW>(acc, tot, lane);
+        if (active) core::counted_store<NB, RW>(tot, w.y, w.r0 + wrow0, w.F_out, p.B);
+        if (tr && lane == 0 && warp == 0) tr[3] = dev::globaltimer();
     }
 }
 
@@ -210,7 +198,7 @@ fasq_status launch_chain_t(const ChainParams& p, size_t smem, int grid, cudaStre
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident (grid-wide arrival counter)
+    attr[0].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident (consumers spin on producers' words)
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
@@ -242,6 +230,16 @@ fasq_status chain_nb(const fasq_chain* c, const ChainParams& p, cudaStream_t st)
         case 8: return chain_cfg<D, 8>(c, p, st);
     }
     return FASQ_E_UNSUPPORTED;
+}
+
+// counted accumulator words -> value (units 2^-32) -> fp16 / fp32 / FASQ_ACC_I64
+__global__ void k_counted_convert(const unsigned long long* __restrict__ w, int64_t n, int ks, void* out, int dtype) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long v = (long long)(w[i] & core::kCntMask) - (long long)ks * core::kCntBias;
+    if (dtype == FASQ_ACC_I64) reinterpret_cast<long long*>(out)[i] = v;
+    else if (dtype == FASQ_F32) reinterpret_cast<float*>(out)[i] = (float)((double)v * core::kAccInv);
+    else reinterpret_cast<__half*>(out)[i] = __double2half((double)v * core::kAccInv);
 }
 
 int sm_count() {
@@ -288,9 +286,10 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
     }
     c->R = c->rw * c->nw;
     // validate + output arena layout
-    int64_t words = 16;   // [0..15]: grid counter + padding
+    int64_t words = 16;   // [0..15]: reserved
     c->acc_off.resize(n_steps);
     c->acc_Fout.resize(n_steps);
+    c->acc_ks.resize(n_steps);
     c->step_F_in.resize(n_steps);
     for (int s = 0; s < n_steps; ++s) {
         const fasq_chain_step& S = steps[s];
@@ -360,6 +359,10 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
             ks[lm] -= 1;
         }
         if (total > c->nctas) { destroy_chain(c); return FASQ_E_UNSUPPORTED; }   // > #SMs row tiles
+        for (int l = 0; l < nl; ++l) {
+            if (ks[l] > 63) { destroy_chain(c); return FASQ_E_UNSUPPORTED; }   // counted-word count field
+            c->acc_ks[s].push_back(ks[l]);
+        }
         int cta = 0;
         for (int l = 0; l < nl; ++l) {
             const fasq_layer* L = S.layers[l];
@@ -381,9 +384,8 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
                 }
         }
         phases[s].F_in = c->step_F_in[s];
-        phases[s].x_acc = S.input_step < 0
-                              ? nullptr
-                              : reinterpret_cast<const long long*>(c->arena + c->acc_off[S.input_step][S.input_layer]);
+        phases[s].x_cnt = S.input_step < 0 ? nullptr : c->arena + c->acc_off[S.input_step][S.input_layer];
+        phases[s].x_ks = S.input_step < 0 ? 0 : c->acc_ks[S.input_step][S.input_layer];
     }
     const size_t xg = (size_t)32 * NB * E;
     c->smem = (size_t)c->st * (cbb_max + (size_t)c->R * 32) + (size_t)c->gmax * xg + 16 * c->st;
@@ -407,14 +409,13 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
 fasq_status fasq_chain_run(fasq_chain* c, const void* x_dev, void* stream) {
     if (!c || !x_dev) return FASQ_E_ARG;
     cudaStream_t st = (cudaStream_t)stream;
-    // zero the grid counter and every step's accumulators (outputs stay
-    // readable until the next run)
+    // zero every step's counted accumulators (outputs stay readable until
+    // the next run)
     FASQ_CUDA_TRY(cudaMemsetAsync(c->arena, 0, (size_t)c->arena_words * 8, st));
     ChainParams p{};
     p.items = static_cast<const ChainItem*>(c->items);
     p.phases = static_cast<const ChainPhase*>(c->phases);
     p.x_ext = static_cast<const __half*>(x_dev);
-    p.counter = reinterpret_cast<unsigned*>(c->arena);
     p.trace = c->trace;
     p.pf = 0;
     if (const char* e = getenv("FASQ_CHAIN_PF")) p.pf = atoi(e);
@@ -439,14 +440,14 @@ fasq_status fasq_chain_output(const fasq_chain* c, int32_t step, int32_t layer, 
                               void* stream) {
     if (!c || !y_dev || step < 0 || step >= c->n_steps) return FASQ_E_ARG;
     if (layer < 0 || layer >= (int)c->acc_off[step].size()) return FASQ_E_ARG;
-    if (dtype == FASQ_ACC_I64) {
-        FASQ_CUDA_TRY(cudaMemcpyAsync(y_dev, c->arena + c->acc_off[step][layer],
-                                      (size_t)c->B * c->acc_Fout[step][layer] * 8, cudaMemcpyDeviceToDevice,
-                                      (cudaStream_t)stream));
-        return FASQ_OK;
-    }
-    return acc_convert_launch(c->arena + c->acc_off[step][layer], (int64_t)c->B * c->acc_Fout[step][layer], y_dev,
-                              dtype, (cudaStream_t)stream);
+    if (dtype != FASQ_F16 && dtype != FASQ_F32 && dtype != FASQ_ACC_I64) return FASQ_E_ARG;
+    const int64_t n = (int64_t)c->B * c->acc_Fout[step][layer];
+    if (n <= 0) return FASQ_OK;
+    k_counted_convert<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        c->arena + c->acc_off[step][layer], n, c->acc_ks[step][layer], y_dev, (int)dtype);
+    FASQ_CUDA_TRY(cudaGetLastError());
+    set_launch_count(1);
+    return FASQ_OK;
 }
 
 fasq_status fasq_chain_trace(fasq_chain* c, void* trace_dev) {

@@ -287,5 +287,104 @@ __device__ __forceinline__ void acc_store(const RowTotals<NB, RW>& t, unsigned l
     }
 }
 
+// ---- counted accumulators (decode-chain dataflow, chain.cu) -----------------
+// A chain output word is an int64 red.add target holding BOTH the value and
+// the number of contributions: every K-split CTA adds
+//     (1 << kCntShift) + kCntBias + v,   v = rn(partial * 2^32), |v| < kCntBias,
+// so the low kCntShift bits stay positive and never carry into the count
+// (<= 63 contributions x 2^51 < 2^57), and a consumer that reads
+// count == ks knows the value is final: sum v = low bits - ks * kCntBias.
+// The word is self-validating -> no grid barrier between chain steps.
+constexpr int kCntShift = 58;
+constexpr long long kCntBias = 1ll << 50;
+constexpr unsigned long long kCntMask = (1ull << kCntShift) - 1;
+
+template <int NB, int RW>
+__device__ __forceinline__ void counted_store(const RowTotals<NB, RW>& t, unsigned long long* y, int row0, int F_out,
+                                              int B) {
+    if (!t.own) return;
+#pragma unroll
+    for (int h = 0; h < RowTotals<NB, RW>::H; ++h) {
+        const int row = row0 + h * 32 + t.rsel;
+        if (row >= F_out) continue;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            if (b >= B) continue;
+            long long v = __float2ll_rn(t.v[h][b] * kAccScale);
+            v = max(-(kCntBias - 1), min(kCntBias - 1, v));   // |partial| < 2^18 (fp16 range is 2^16)
+            const unsigned long long add = (1ull << kCntShift) + (unsigned long long)(kCntBias + v);
+            asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(y + (size_t)b * F_out + row), "l"(add) : "memory");
+        }
+    }
+}
+
+// x staging from counted accumulator words [B][F_in] produced by ks K-split
+// CTAs of the previous step: every thread polls its words until all carry
+// count == ks (one L2 round trip once they are final), then rounds the value
+// to fp16.  Layout of s_x as stage_x.
+template <int D, int NB, int NW>
+__device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned long long* x, int ks, int F_in, int B,
+                                                int N_ss, int g_begin, int ng) {
+    constexpr int E = Entry<D>::value;
+    const int tid = threadIdx.x;
+    const int n_ent = ng * 32 * NB;
+    const unsigned long long want = (unsigned long long)ks;
+    const long long bias = (long long)ks * kCntBias;
+    constexpr int XPT = 2;
+    for (int t0 = tid; t0 < n_ent; t0 += NW * 32 * XPT) {
+        unsigned long long v[XPT][D];
+        bool need[XPT];
+#pragma unroll
+        for (int u = 0; u < XPT; ++u) {
+            const int t = t0 + u * NW * 32;
+            const int b = t % NB;
+            const int ss = (g_begin + t / (NB * 32)) * 32 + ((t / NB) & 31);
+            need[u] = t < n_ent && b < B && ss < N_ss;
+#pragma unroll
+            for (int e = 0; e < D; ++e) v[u][e] = 0;
+        }
+        // poll: reload every word of this thread until all are final
+        bool done = false;
+        while (!done) {
+            done = true;
+#pragma unroll
+            for (int u = 0; u < XPT; ++u) {
+                if (!need[u]) continue;
+                const int t = t0 + u * NW * 32;
+                const int b = t % NB;
+                const int ss = (g_begin + t / (NB * 32)) * 32 + ((t / NB) & 31);
+                const unsigned long long* src = x + (size_t)b * F_in + (size_t)ss * D;
+#pragma unroll
+                for (int e = 0; e < D; ++e) {
+                    if ((v[u][e] >> kCntShift) == want) continue;
+                    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v[u][e]) : "l"(src + e) : "memory");
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < XPT; ++u)
+#pragma unroll
+                for (int e = 0; e < D; ++e)
+                    if (need[u] && (v[u][e] >> kCntShift) != want) done = false;
+        }
+#pragma unroll
+        for (int u = 0; u < XPT; ++u) {
+            const int t = t0 + u * NW * 32;
+            if (t >= n_ent) continue;
+            uint32_t w[4] = {0u, 0u, 0u, 0u};
+            if (need[u]) {
+#pragma unroll
+                for (int e = 0; e < D; ++e) {
+                    const long long val = (long long)(v[u][e] & kCntMask) - bias;
+                    const uint32_t h = __half_as_ushort(__double2half((double)val * kAccInv));
+                    w[e >> 1] |= h << (16 * (e & 1));
+                }
+            }
+            uint32_t* dst = reinterpret_cast<uint32_t*>(s_x + (size_t)t * E);
+#pragma unroll
+            for (int q = 0; q < E / 4; ++q) dst[q] = w[q];
+        }
+    }
+}
+
 }  // namespace core
 }  // namespace fasq

@@ -3,11 +3,12 @@
 
     python tools/chain_trace.py [--blocks 32] [--json out.json]
 
-Stamps per (step, CTA): t0 step entry, t1 grid wait done, t2 x staged,
-t3 outputs stored.  Reported per step kind (qkv, o, gateup, down), medians
-over blocks: step span (last t3 of the previous step -> last t3 of this
-step), barrier latency (last t3 of prev -> median t1), x staging, compute
-(t2 -> t3) min / median / max over CTAs, and the idle tail (max t3 - median t3).
+Stamps per (step, CTA): t0 step entry, t1 inputs final + staged (dataflow
+wait), t2 CTA synchronised, t3 outputs stored.  Reported per step kind (qkv,
+o, gateup, down), medians over blocks: step span (last t3 of the previous
+step -> last t3 of this step), "barrier" = input wait (last t3 of prev ->
+median t1), "xstage" = t2 - t1, compute (t2 -> t3) min / median / max over
+CTAs, and the idle tail (max t3 - median t3).
 """
 import argparse
 import json
