@@ -20,8 +20,12 @@ value  = decode tokens/s of the PQ linear stack (1 token = 1 step), device
 e2e    = the same step through the public API with HOST buffers: H2D of the
          token's fp16 hidden state from pinned memory + the 224 GEMVs + D2H
          of the last layer's output, inside the timed region.
-roofline: dominant kernel = the decode GEMV (k_gemv + its split-K merge),
-         algorithmic bytes = indices + codebooks + x + y of the 224 layers.
+roofline: dominant kernel = the persistent decode-chain kernel k_chain (N=1:
+         ONE launch per token runs all 224 GEMVs; its per-launch duration is
+         timed live with CUDA events around eager launches), algorithmic
+         bytes = indices + codebooks + x + y of the 224 layers; traffic =
+         dram bytes of one k_chain launch from the committed ncu --set full
+         capture (profiles/r01).
 cpu_baseline: the C oracle (fp64 reconstruct-then-multiply) timed on a
          bounded row sample of each layer shape on the host cores.
 """
@@ -41,6 +45,9 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 METRIC = "Llama-3-8B PQ decode tok/s + GEMV HBM GB/s vs 8 TB/s; prefill GEMM TFLOP/s"
+# dram__bytes_read.sum + dram__bytes_write.sum of ONE k_chain launch (32 blocks,
+# d=2, C=256, B=1) from `ncu --set full` (profiles/r01/ncu_chain_summary.txt)
+K_CHAIN_NCU_DRAM_BYTES = 4140526000 + 15484672
 D, C = 2, 256
 
 
@@ -476,8 +483,25 @@ def main():
 
     tok_s = 1000.0 / ms
     gbytes = layer_bytes(world)
-    achieved = gbytes / (ms * 1e-3) / 1e9
     peak = float(peaks.get("hbm_gbs", 6650.0))
+    # dominant kernel alone: k_chain launches (+ their accumulator memset node)
+    # timed with CUDA events on the launching stream, after the graph timing
+    kern_ms, kern_name, traffic = ms, "whole step (per-launch GEMVs)", None
+    if step.chain is not None:
+        for _ in range(3):
+            step.chain.run(step.h)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nk = max(10, args.steps // 4)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(nk):
+            step.chain.run(step.h)
+        e1.record()
+        torch.cuda.synchronize()
+        kern_ms = e0.elapsed_time(e1) / nk
+        kern_name = "k_chain (one launch = the 224 GEMVs of a token) + its accumulator memset"
+        traffic = K_CHAIN_NCU_DRAM_BYTES
+    achieved = gbytes / (kern_ms * 1e-3) / 1e9
 
     side = {}
     if rank == 0 and not args.no_side:
@@ -502,6 +526,8 @@ def main():
             "vs_baseline": None, "dtype": "f16", "data": "synthetic",
             "config": {"workload": "llama3-8b-pq-decode-d2-C256-b1: 32 blocks x {q,k,v,o,gate,up,down} "
                                    "PQ GEMVs, chained fp16 activations (attention/norm/lm_head excluded)",
+                       "executor": "persistent chain kernel (fasq_chain_*)" if step.chain is not None
+                                   else "one grouped GEMV launch per step",
                        "global_batch": 1, "seq_len": 1,
                        "parallelism": "row-shard-tp%d+nccl-allgather" % world if world > 1 else "single-gpu",
                        "d": D, "C": C, "weights_bytes_per_step": gbytes,
@@ -511,9 +537,9 @@ def main():
                     "d2h_bytes_per_step": 4096 * 2},
             "gpu_launches": launches_per_step * args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "k_gemv + k_splitk_reduce (decode GEMV op), algorithmic bytes of all "
-                                   "224 layers / step time; peak = %s hbm_gbs" % peak_src},
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": kern_name, "kernel_ms": kern_ms, "algorithmic_bytes": gbytes,
+                         "peak_source": "%s hbm_gbs" % peak_src},
             "clocks": clocks,
             "cpu_baseline": cpu,
             "side": side,
