@@ -137,8 +137,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     }
 
     const int wrow0 = warp * RW;
-    const uint8_t* idx_lane = s_idx + core::idx_lane_off(wrow0, lane);
-    int it = 0;
+    const auto co = core::chunk_offsets<RW>(wrow0, lane);
+    int slot = 0;            // ring position of the next stage (running across steps)
+    uint32_t par = 0;        // its mbarrier phase parity
     for (int ph = 0; ph < p.n_steps; ++ph) {
         // the work item and phase are read-only for the kernel's lifetime
         const ChainItem w = p.items[(size_t)ph * p.nctas + blockIdx.x];
@@ -162,17 +163,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
 #pragma unroll
             for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
         const bool active = wrow0 < w.rows_valid;
-        for (int i = 0; i < ng; ++i, ++it) {
-            const int slot = it % ST;
-            dev::mbar_wait(full0 + 8 * slot, (it / ST) & 1);
+        for (int i = 0; i < ng; ++i) {
+            dev::mbar_wait(full0 + 8 * slot, par);
             if (active) {
                 uint32_t xv[NB][E / 4];
                 core::load_x<D, NB>(xv, s_x + i * XG, lane);
-                core::compute_group<D, NB, RW>(acc, idx_lane + slot * R * 32, s_cb + slot * p.cbb_max, xv, wrow0,
-                                               lane);
+                core::compute_group<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb + slot * p.cbb_max, xv, lane);
             }
             __syncwarp();
             if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+            if (++slot == ST) { slot = 0; par ^= 1u; }
         }
         core::RowTotals<NB, RW> tot;
         core::reduce_rows<NB, RW>(acc, tot, lane);

@@ -180,17 +180,19 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
 
     const int wrow0 = warp * RW;
     const bool active = wrow0 < rows_valid;          // rows_valid is a multiple of 64 >= RW
-    const uint8_t* idx_lane = s_idx + core::idx_lane_off(wrow0, lane);
+    const auto co = core::chunk_offsets<RW>(wrow0, lane);
+    int slot = 0;
+    uint32_t par = 0;
     for (int i = 0; i < ng; ++i) {
-        const int slot = i % ST;
-        dev::mbar_wait(full0 + 8 * slot, (i / ST) & 1);
+        dev::mbar_wait(full0 + 8 * slot, par);
         if (active) {
             uint32_t xv[NB][E / 4];
             core::load_x<D, NB>(xv, s_x + i * XG, lane);
-            core::compute_group<D, NB, RW>(acc, idx_lane + slot * R * 32, s_cb + slot * CBB, xv, wrow0, lane);
+            core::compute_group<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb + slot * CBB, xv, lane);
         }
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+        if (++slot == ST) { slot = 0; par ^= 1u; }
     }
 
     // ------------------------------ epilogue --------------------------------

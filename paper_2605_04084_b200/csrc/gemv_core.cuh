@@ -132,16 +132,34 @@ __device__ __forceinline__ uint32_t idx_lane_off(int wrow0, int lane) {
     return (uint32_t)(wrow0 >> 6) * 2048u + (uint32_t)lane * 64u;
 }
 
+// Per-lane byte offsets of the warp's 16-row index chunks inside an index
+// stage (chunk c of the warp's 64-row block at 16 * ((c + s/2) & 3); RW = 8:
+// + 8 for the odd half).  Loop-invariant: computed once per kernel.
+template <int RW>
+struct ChunkOffs {
+    static constexpr int N = RW >= 16 ? RW / 16 : 1;
+    uint32_t o[N];
+};
+template <int RW>
+__device__ __forceinline__ ChunkOffs<RW> chunk_offsets(int wrow0, int lane) {
+    ChunkOffs<RW> c;
+    const int c0 = (wrow0 >> 4) & 3;
+#pragma unroll
+    for (int ci = 0; ci < ChunkOffs<RW>::N; ++ci)
+        c.o[ci] = idx_lane_off(wrow0, lane) + 16u * (((uint32_t)(c0 + ci) + (uint32_t)(lane >> 1)) & 3u) +
+                  (RW == 8 ? (uint32_t)(wrow0 & 8) : 0u);
+    return c;
+}
+
 // One 32-subspace group: acc[j][b] += dot(x[b]_s, c_s[k_s(row j)]) for the
-// warp's RW rows (lane s = subspace s).  idx_lane = idx_lane_base(...) +
-// stage base; cbs = codebook image stage base.
+// warp's RW rows (lane s = subspace s).  idx_stage = index stage base, co =
+// chunk_offsets(); cbs = codebook image stage base.
 template <int D, int NB, int RW>
-__device__ __forceinline__ void compute_group(float (&acc)[RW][NB], const uint8_t* idx_lane, const uint8_t* cbs,
-                                              const uint32_t (&xv)[NB][Entry<D>::value / 4], int wrow0, int lane) {
+__device__ __forceinline__ void compute_group(float (&acc)[RW][NB], const uint8_t* idx_stage, const ChunkOffs<RW>& co,
+                                              const uint8_t* cbs, const uint32_t (&xv)[NB][Entry<D>::value / 4],
+                                              int lane) {
     constexpr int E = Entry<D>::value;
-    constexpr int NCH = RW >= 16 ? RW / 16 : 1;        // 16-row chunks per warp
-    const int c0 = (wrow0 >> 4) & 3;                   // first chunk of the warp in its 64-row block
-    const uint32_t rot = (uint32_t)(lane >> 1);
+    constexpr int NCH = ChunkOffs<RW>::N;              // 16-row chunks per warp
     // E = 4: address = cbs + 4*s + (k << 7)        (PRMT extracts k, LEA scales)
     // E = 8: address = cbs + (k << 8 | 8*s)        (one PRMT)
     // E = 16: address = cbs + (k << 8 | 8*s) << 1  (PRMT + shift)
@@ -149,13 +167,13 @@ __device__ __forceinline__ void compute_group(float (&acc)[RW][NB], const uint8_
     const uint32_t L8 = (uint32_t)lane * 8u;
 #pragma unroll
     for (int ci = 0; ci < NCH; ++ci) {
-        const uint8_t* ca = idx_lane + 16u * (((uint32_t)(c0 + ci) + rot) & 3u);
+        const uint8_t* ca = idx_stage + co.o[ci];
         uint32_t w[4];
         if (RW >= 16) {
             const uint4 v = lds<uint4>(ca);
             w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
         } else {   // RW = 8: half a chunk
-            const uint2 v = lds<uint2>(ca + (wrow0 & 8));
+            const uint2 v = lds<uint2>(ca);
             w[0] = v.x; w[1] = v.y; w[2] = 0u; w[3] = 0u;
         }
         // all gathers of a batch first, then the FMAs: keeps LDS_BATCH loads in
