@@ -71,3 +71,79 @@ def test_chain_errors(F):
         F.Chain([([L1], None), ([L2], (0, 0))])     # F_out 256 != F_in 1024
     with pytest.raises(F.FasqError):
         F.Chain([([L1], (1, 0))])                  # forward reference
+
+
+def _chain_vs_oracle(F, oracle_lib, specs, B, d, C, seed0=300):
+    """specs: list of (layers [(F_out, F_in)], src) -> builds, runs, checks every layer."""
+    rng_seed = seed0
+    built = []
+    steps = []
+    for shapes, src in specs:
+        ls = []
+        for (fo, fi) in shapes:
+            cb, idx = synth.random_layer(fo, fi, d, C, seed=rng_seed)
+            rng_seed += 1
+            L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), fi, 1)
+            ls.append((L, cb, idx))
+        built.append(ls)
+        steps.append(([t[0] for t in ls], src))
+    chain = F.Chain(steps, B=B)
+    x = synth.activation(B, specs[0][0][0][1], seed=seed0)
+    chain.run(torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
+    for s, ls in enumerate(built):
+        src = steps[s][1]
+        xin = x if src is None else chain.output(src[0], src[1], out_dtype=torch.float16).cpu().numpy()
+        for l, (_, cb, idx) in enumerate(ls):
+            y = chain.output(s, l, out_dtype=torch.float32).cpu().numpy()
+            ref = oracle_lib.gemv(cb, idx, xin)
+            ok, info = parity_ok(y, ref, xin, xin.shape[1])
+            assert ok, (s, l, info)
+    chain.free()
+
+
+@pytest.mark.parametrize("d,C,B", [(1, 64, 1), (4, 256, 2), (8, 128, 1), (2, 256, 8), (2, 200, 4)])
+def test_chain_entry_sizes_and_batches(F, oracle_lib, d, C, B):
+    # ragged shapes: F_out not a multiple of 64, N_ss not a multiple of 32
+    specs = [([(1000, 1016), (88, 1016)], None), ([(1016, 1000)], (0, 0)), ([(472, 1016)], (1, 0))]
+    _chain_vs_oracle(F, oracle_lib, specs, B, d, C)
+
+
+def test_chain_input_from_other_layer_and_step(F, oracle_lib):
+    # a step may read any earlier step's output, including layer 1 of a grouped step
+    specs = [([(512, 768), (768, 768)], None), ([(768, 768)], (0, 1)), ([(640, 512)], (0, 0)),
+             ([(768, 640)], (2, 0))]
+    _chain_vs_oracle(F, oracle_lib, specs, 1, 2, 256)
+
+
+def test_chain_llama_block_sampled(F, oracle_lib):
+    """One Llama-3-8B-shaped block at full size (the bench's k_chain launch
+    configuration), checked on sampled rows of every layer."""
+    sh = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096), ("g", 14336, 4096),
+          ("u", 14336, 4096), ("d", 4096, 14336)]
+    Ls = {}
+    for i, (n, fo, fi) in enumerate(sh):
+        cb, idx = synth.torch_random_layer(fo, fi, 2, 256, seed=900 + i)
+        Ls[n] = (F.import_layer(cb, idx, fi), cb, idx)
+    steps = [([Ls["q"][0], Ls["k"][0], Ls["v"][0]], None), ([Ls["o"][0]], (0, 0)),
+             ([Ls["g"][0], Ls["u"][0]], (1, 0)), ([Ls["d"][0]], (2, 0))]
+    chain = F.Chain(steps, B=1)
+    x = synth.torch_activation(1, 4096, seed=5)
+    chain.run(x)
+    torch.cuda.synchronize()
+    names = [("q", "k", "v"), ("o",), ("g", "u"), ("d",)]
+    rng = np.random.default_rng(0)
+    for s, ns in enumerate(names):
+        src = steps[s][1]
+        xin = x.cpu().numpy() if src is None else chain.output(src[0], src[1], out_dtype=torch.float16).cpu().numpy()
+        for l, n in enumerate(ns):
+            _, cb, idx = Ls[n]
+            F_out = idx.shape[1]
+            yall = chain.output(s, l, out_dtype=torch.float32).cpu().numpy()
+            cbn, idxn = cb.cpu().numpy(), idx.cpu().numpy()
+            j = int(rng.integers(64, F_out - 128))
+            for (j0, j1) in ((0, 32), (j, j + 64), (F_out - 32, F_out)):   # first, random, last rows
+                ref = oracle_lib.gemv(cbn, idxn, xin, rows=(j0, j1))
+                ok, info = parity_ok(yall[:, j0:j1], ref, xin, xin.shape[1])
+                assert ok, (s, n, j0, info)
+    chain.free()
