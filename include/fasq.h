@@ -208,13 +208,39 @@ typedef struct fasq_chain fasq_chain; /* opaque */
 fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int32_t B, void* stream,
                               fasq_chain** out);
 
+/* Tensor-parallel chain (north_star "splitting output rows across GPUs with
+ * an all-gather"), one process (or chain) per GPU: every layer of
+ * `steps` is THIS rank's row shard (rows [rank*F_out, (rank+1)*F_out) of a
+ * layer with world*F_out rows, rank-major, all codebooks replicated -- as
+ * fasq_shard_rows produces), and every step's input is the full
+ * world*F_out-wide output of its producer.  The all-gather is fused into the
+ * GEMV: each rank red.adds its rows' counted accumulators into EVERY rank's
+ * arena (NVLink peer memory), so a step's consumers on every GPU wait only for
+ * their own K range -- no NCCL call and no host round trip between steps.
+ * world in 1..8; max_ctas > 0 caps the CTAs (e.g. several ranks sharing one
+ * GPU in tests), 0 = one per SM.  Before the first run every rank must call
+ * fasq_chain_set_peers (handles from every rank's fasq_chain_ipc_handle,
+ * exchanged by the caller) or, for chains of one process,
+ * fasq_chain_set_peer_chains.  All ranks must run their chains concurrently
+ * and the same number of times (the kernels spin-wait on each other; a rank
+ * that never delivers turns into a kernel error after ~4 s). */
+fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, int32_t B, int32_t world,
+                                 int32_t rank, int32_t max_ctas, void* stream, fasq_chain** out);
+/* Writes this chain's arena IPC handle (cudaIpcMemHandle_t, 64 bytes). */
+fasq_status fasq_chain_ipc_handle(const fasq_chain* chain, void* handle_out);
+/* handles: world x 64 bytes, rank-major (this rank's entry is ignored). */
+fasq_status fasq_chain_set_peers(fasq_chain* chain, const void* handles);
+/* In-process peers: chains[r] is rank r's chain (chains[rank] == chain). */
+fasq_status fasq_chain_set_peer_chains(fasq_chain* chain, const fasq_chain* const* chains);
+
 /* Runs the whole chain on x_dev (fp16 [B][F_in of the external-input steps]):
- * one memset node (the accumulators) and one kernel launch; graph
- * capturable.  A chain instance must not run concurrently with itself. */
+ * ONE kernel launch (the accumulators are double-buffered; each run zeroes the
+ * buffer of the next run in-kernel, the parity lives on the device, so graph
+ * replays work).  A chain instance must not run concurrently with itself. */
 fasq_status fasq_chain_run(fasq_chain* chain, const void* x_dev, void* stream);
 
-/* Output of layer `layer` of step `step` after a run, as fp16 / fp32 /
- * FASQ_ACC_I64 [B][F_out] (valid until the next run). */
+/* Output of layer `layer` of step `step` after the last run, as fp16 / fp32 /
+ * FASQ_ACC_I64 [B][world*F_out] (all ranks' rows; valid until the next run). */
 fasq_status fasq_chain_output(const fasq_chain* chain, int32_t step, int32_t layer, void* y_dev,
                               fasq_dtype dtype, void* stream);
 /* Diagnostics: when trace_dev is not NULL, every later fasq_chain_run writes

@@ -32,7 +32,8 @@ _STATUS = {0: "FASQ_OK", -1: "FASQ_E_ARG", -2: "FASQ_E_NONDIVISIBLE", -3: "FASQ_
 # Every symbol include/fasq.h declares (checked by tests/test_abi.py).
 EXPORTED = ["fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
             "fasq_free", "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_acc_convert",
-            "fasq_chain_create", "fasq_chain_run", "fasq_chain_output", "fasq_chain_trace",
+            "fasq_chain_create", "fasq_chain_create_tp", "fasq_chain_ipc_handle", "fasq_chain_set_peers",
+            "fasq_chain_set_peer_chains", "fasq_chain_run", "fasq_chain_output", "fasq_chain_trace",
             "fasq_chain_ctas", "fasq_chain_free", "fasq_gemv_host", "fasq_gemm",
             "fasq_last_launch_count", "fasq_status_string", "fasq_last_error_message",
             "fasq_abi_version"]
@@ -92,6 +93,10 @@ def _load():
                                     ctypes.POINTER(GemvOpts), vp]
     L.fasq_acc_convert.argtypes = [vp, i64, vp, i32, vp]
     L.fasq_chain_create.argtypes = [ctypes.POINTER(_ChainStep), i32, i32, vp, pp]
+    L.fasq_chain_create_tp.argtypes = [ctypes.POINTER(_ChainStep), i32, i32, i32, i32, i32, vp, pp]
+    L.fasq_chain_ipc_handle.argtypes = [vp, vp]
+    L.fasq_chain_set_peers.argtypes = [vp, vp]
+    L.fasq_chain_set_peer_chains.argtypes = [vp, ctypes.POINTER(vp)]
     L.fasq_chain_run.argtypes = [vp, vp, vp]
     L.fasq_chain_output.argtypes = [vp, i32, i32, vp, i32, vp]
     L.fasq_chain_trace.argtypes = [vp, vp]
@@ -103,7 +108,8 @@ def _load():
     L.fasq_last_error_message.restype = ctypes.c_char_p
     for name in ("fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
                  "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_acc_convert", "fasq_gemv_host",
-                 "fasq_chain_create", "fasq_chain_run", "fasq_chain_output", "fasq_chain_trace",
+                 "fasq_chain_create", "fasq_chain_create_tp", "fasq_chain_ipc_handle", "fasq_chain_set_peers",
+                 "fasq_chain_set_peer_chains", "fasq_chain_run", "fasq_chain_output", "fasq_chain_trace",
                  "fasq_chain_ctas", "fasq_gemm", "fasq_last_launch_count",
                  "fasq_abi_version"):
         getattr(L, name).restype = ctypes.c_int32
@@ -266,7 +272,7 @@ class Chain:
     ``(layers, input)`` with ``input = None`` (the external x) or
     ``(step, layer)`` (an earlier step's output)."""
 
-    def __init__(self, steps, B: int = 1, stream=None):
+    def __init__(self, steps, B: int = 1, stream=None, world: int = 1, rank: int = 0, max_ctas: int = 0):
         self._keep = []
         arr = (_ChainStep * len(steps))()
         for i, (layers, src) in enumerate(steps):
@@ -276,18 +282,38 @@ class Chain:
             arr[i].n_layers = len(layers)
             arr[i].input_step, arr[i].input_layer = (-1, 0) if src is None else src
         out = ctypes.c_void_p()
-        _check(lib.fasq_chain_create(arr, len(steps), B, _stream(stream), ctypes.byref(out)))
+        _check(lib.fasq_chain_create_tp(arr, len(steps), B, world, rank, max_ctas, _stream(stream),
+                                        ctypes.byref(out)))
         self._h = out
         self.B = B
+        self.world, self.rank = world, rank
         self.steps = [(list(l), s) for (l, s) in steps]
 
     def run(self, x: torch.Tensor, stream=None):
         x = _cuda(x, torch.float16, "x")
         _check(lib.fasq_chain_run(self._h, x.data_ptr(), _stream(stream)))
 
+    def ipc_handle(self) -> bytes:
+        """64-byte cudaIpcMemHandle of this chain's arena (exchange across ranks)."""
+        buf = ctypes.create_string_buffer(64)
+        _check(lib.fasq_chain_ipc_handle(self._h, buf))
+        return buf.raw
+
+    def set_peers(self, handles):
+        """handles: list of every rank's ipc_handle() (rank order)."""
+        blob = b"".join(handles)
+        if len(blob) != 64 * self.world:
+            raise ValueError("need world x 64-byte handles")
+        _check(lib.fasq_chain_set_peers(self._h, ctypes.create_string_buffer(blob, len(blob))))
+
+    def set_peer_chains(self, chains):
+        """In-process ranks: chains[r] is rank r's Chain (including self)."""
+        arr = (ctypes.c_void_p * len(chains))(*[c._h.value for c in chains])
+        _check(lib.fasq_chain_set_peer_chains(self._h, arr))
+
     def output(self, step: int, layer: int = 0, out: torch.Tensor | None = None,
                out_dtype=torch.float16, stream=None) -> torch.Tensor:
-        F_out = self.steps[step][0][layer].F_out
+        F_out = self.steps[step][0][layer].F_out * self.world
         if out is None:
             out = torch.empty((self.B, F_out), dtype=out_dtype, device="cuda")
         dt = out.dtype

@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <vector>
 
@@ -35,16 +36,23 @@
 
 struct fasq_chain {
     int n_steps = 0, B = 0, d = 0, nctas = 0;
+    int world = 1, rank = 0;                         // row-sharded tensor parallelism (fasq_chain_create_tp)
     int rw = 0, nw = 0, st = 0, R = 0, gmax = 1, maxC = 1;
     size_t smem = 0;
-    std::vector<int> step_F_out_total;               // per step: sum of F_out of its layers
-    std::vector<std::vector<int64_t>> acc_off;       // per step, per layer: word offset in the arena
-    std::vector<std::vector<int64_t>> acc_Fout;
+    std::vector<std::vector<int64_t>> acc_off;       // per step, per layer: word offset in one arena buffer
+    std::vector<std::vector<int64_t>> acc_Fout;      // per step, per layer: GLOBAL F_out (words per batch row)
     std::vector<std::vector<int>> acc_ks;            // per step, per layer: K-split count (contributions per word)
     std::vector<int> step_F_in;
     int ext_F_in = 0;
-    unsigned long long* arena = nullptr;             // [0..15]: reserved, then counted accumulators
-    int64_t arena_words = 0;
+    // two arena buffers (ONE allocation, IPC-exportable): run n accumulates into
+    // buffer parity(n) on every rank and zeroes its own buffer parity(n)^1 for
+    // run n+1 -- no memset node, no host round trip between tokens
+    unsigned long long* arenas = nullptr;
+    int64_t arena_words = 0;                         // words per buffer
+    unsigned* ctrl = nullptr;                        // device: [0] parity, [1] unused, [2] monotonic CTA entry counter
+    unsigned long long** peers_dev = nullptr;        // device [world]: every rank's `arenas` (own rank = local)
+    std::vector<void*> ipc_opened;                   // peer mappings opened by fasq_chain_set_peers
+    bool peers_ready = true;
     void* items = nullptr;                           // device [n_steps][nctas] ChainItem
     void* phases = nullptr;                          // device [n_steps] ChainPhase
     unsigned long long* trace = nullptr;             // user buffer (fasq_chain_trace), not owned
@@ -57,14 +65,15 @@ namespace {
 struct ChainItem {
     const uint8_t* idx;
     const uint8_t* cbimg;
-    unsigned long long* y;      // counted-accumulator output [B][F_out]
-    int F_out, F_out_pad, N_ss, C;
+    long long y_off;            // word offset of the layer's counted-accumulator output [B][F_out_g] in a buffer
+    int F_out, F_out_g, row0_g; // local rows of this rank's shard, global F_out, global row of local row 0
+    int F_out_pad, N_ss, C;
     int r0, rows_valid, g_begin, g_end;
 };
 
 struct ChainPhase {
-    const unsigned long long* x_cnt;   // counted-accumulator input (nullptr: the chain's external fp16 x)
-    int F_in, x_ks;                    // x_ks: contributions per input word (K-split of the producer)
+    long long x_off;            // word offset of the counted-accumulator input (< 0: the external fp16 x)
+    int F_in, x_ks;             // x_ks: contributions per input word (K-split of the producer)
 };
 
 struct ChainParams {
@@ -72,6 +81,10 @@ struct ChainParams {
     const ChainPhase* phases;
     const __half* x_ext;        // [B][F_in of the first step]
     unsigned long long* trace;  // optional [n_steps][nctas][4] globaltimer stamps (fasq_chain_trace)
+    unsigned* ctrl;             // [0] parity, [2] CTA entry counter
+    unsigned long long* const* peers;   // [world] arena bases (2 buffers each); peers[rank] = local
+    long long arena_words;      // words per buffer
+    int world, rank;
     int n_steps, nctas, B, gmax, cbb_max;
     int pf;                     // producer: L2-prefetch this many groups of the next step's item
 };
@@ -136,10 +149,43 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         return;
     }
 
+    // ---- run prologue: arena parity, zero the other buffer for the next run ----
+    __shared__ unsigned s_par, s_target;
+    if (threadIdx.x == 0) {
+        unsigned par, old;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(par) : "l"(p.ctrl) : "memory");
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.ctrl + 2) : "memory");
+        s_par = par & 1u;
+        s_target = (old / (unsigned)p.nctas + 1u) * (unsigned)p.nctas;
+    }
+    asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
+    const unsigned par = s_par;
+    unsigned long long* const cur = p.peers[p.rank] + (long long)par * p.arena_words;   // this run's buffer
+    {
+        unsigned long long* nxt = p.peers[p.rank] + (long long)(par ^ 1u) * p.arena_words;
+        const long long per = (p.arena_words + p.nctas - 1) / p.nctas;
+        const long long zb = per * blockIdx.x, ze = min(p.arena_words, zb + per);
+        for (long long i = zb + threadIdx.x; i < ze; i += NW * 32) nxt[i] = 0ull;
+    }
+    if (p.world > 1) {
+        // peers write into our next buffer only after they consumed this run's
+        // data; make the zeros visible system-wide and let every local CTA
+        // finish zeroing before any of this rank's outputs leave the GPU
+        __threadfence_system();
+        asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
+        if (threadIdx.x == 0) {
+            unsigned v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ctrl + 2) : "memory");
+            } while ((int)(v - s_target) < 0);
+        }
+        asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
+    }
+
     const int wrow0 = warp * RW;
     const auto co = core::chunk_offsets<RW>(wrow0, lane);
     int slot = 0;            // ring position of the next stage (running across steps)
-    uint32_t par = 0;        // its mbarrier phase parity
+    uint32_t par_ring = 0;   // its mbarrier phase parity
     for (int ph = 0; ph < p.n_steps; ++ph) {
         // the work item and phase are read-only for the kernel's lifetime
         const ChainItem w = p.items[(size_t)ph * p.nctas + blockIdx.x];
@@ -150,8 +196,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         // every consumer warp is done with the previous step's s_x
         asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
         const int ng = w.g_end - w.g_begin;
-        if (phs.x_cnt)   // dataflow wait: poll this CTA's input words until final
-            core::stage_x_counted<D, NB, NW>(s_x, phs.x_cnt, phs.x_ks, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
+        if (phs.x_off >= 0)   // dataflow wait: poll this CTA's input words until final
+            core::stage_x_counted<D, NB, NW>(s_x, cur + phs.x_off, phs.x_ks, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
         else
             core::stage_x<D, NB, NW>(s_x, p.x_ext, 0, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
         if (tr && threadIdx.x == 0) tr[1] = dev::globaltimer();
@@ -164,7 +210,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
         const bool active = wrow0 < w.rows_valid;
         for (int i = 0; i < ng; ++i) {
-            dev::mbar_wait(full0 + 8 * slot, par);
+            dev::mbar_wait(full0 + 8 * slot, par_ring);
             if (active) {
                 uint32_t xv[NB][E / 4];
                 core::load_x<D, NB>(xv, s_x + i * XG, lane);
@@ -172,12 +218,26 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             }
             __syncwarp();
             if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
-            if (++slot == ST) { slot = 0; par ^= 1u; }
+            if (++slot == ST) { slot = 0; par_ring ^= 1u; }
         }
         core::RowTotals<NB, RW> tot;
         core::reduce_rows<NB, RW>(acc, tot, lane);
-        if (active) core::counted_store<NB, RW>(tot, w.y, w.r0 + wrow0, w.F_out, p.B);
+        if (active) {
+            // this rank's rows go into EVERY rank's buffer (NVLink peer stores
+            // when world > 1): the row-shard all-gather fused into the GEMV
+            const long long off = (long long)par * p.arena_words + w.y_off + w.row0_g;
+            for (int q = 0; q < p.world; ++q)
+                core::counted_store<NB, RW>(tot, p.peers[q] + off, w.r0 + wrow0, w.F_out, w.F_out_g, p.B);
+        }
         if (tr && lane == 0 && warp == 0) tr[3] = dev::globaltimer();
+    }
+    // ---- run epilogue: flip the parity once every CTA has read it ----
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ctrl + 2) : "memory");
+        } while ((int)(v - s_target) < 0);
+        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" :: "l"(p.ctrl), "r"(par ^ 1u) : "memory");
     }
 }
 
@@ -232,11 +292,17 @@ fasq_status chain_nb(const fasq_chain* c, const ChainParams& p, cudaStream_t st)
     return FASQ_E_UNSUPPORTED;
 }
 
-// counted accumulator words -> value (units 2^-32) -> fp16 / fp32 / FASQ_ACC_I64
-__global__ void k_counted_convert(const unsigned long long* __restrict__ w, int64_t n, int ks, void* out, int dtype) {
+// counted accumulator words of the LAST run -> value (units 2^-32) -> fp16 /
+// fp32 / FASQ_ACC_I64.  The run flipped the parity at its end, so its buffer
+// is parity ^ 1 (read on the device: graph replays need no host bookkeeping).
+__global__ void k_counted_convert(const unsigned long long* __restrict__ arenas, long long arena_words,
+                                  const unsigned* __restrict__ ctrl, long long off, int64_t n, int ks, void* out,
+                                  int dtype) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const long long v = (long long)(w[i] & core::kCntMask) - (long long)ks * core::kCntBias;
+    const unsigned last = (ctrl[0] & 1u) ^ 1u;
+    const unsigned long long wv = arenas[(long long)last * arena_words + off + i];
+    const long long v = (long long)(wv & core::kCntMask) - (long long)ks * core::kCntBias;
     if (dtype == FASQ_ACC_I64) reinterpret_cast<long long*>(out)[i] = v;
     else if (dtype == FASQ_F32) reinterpret_cast<float*>(out)[i] = (float)((double)v * core::kAccInv);
     else reinterpret_cast<__half*>(out)[i] = __double2half((double)v * core::kAccInv);
@@ -251,10 +317,19 @@ int sm_count() {
 
 void destroy_chain(fasq_chain* c) {
     if (!c) return;
-    if (c->arena) cudaFree(c->arena);
+    for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
+    if (c->arenas) cudaFree(c->arenas);
+    if (c->ctrl) cudaFree(c->ctrl);
+    if (c->peers_dev) cudaFree(c->peers_dev);
     if (c->items) cudaFree(c->items);
     if (c->phases) cudaFree(c->phases);
     delete c;
+}
+
+fasq_status upload_peers(fasq_chain* c, const std::vector<unsigned long long*>& bases) {
+    FASQ_CUDA_TRY(cudaMemcpy(c->peers_dev, bases.data(), bases.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    c->peers_ready = true;
+    return FASQ_OK;
 }
 
 }  // namespace
@@ -265,17 +340,21 @@ using namespace fasq;
 
 extern "C" {
 
-fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int32_t B, void* stream,
-                              fasq_chain** out) {
+fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, int32_t B, int32_t world,
+                                 int32_t rank, int32_t max_ctas, void* stream, fasq_chain** out) {
     if (!out) return FASQ_E_ARG;
     *out = nullptr;
     if (!steps || n_steps < 1) return FASQ_E_ARG;
+    if (world < 1 || world > 8 || rank < 0 || rank >= world || max_ctas < 0) return FASQ_E_ARG;
     if (B < 1 || B > 8) return FASQ_E_UNSUPPORTED;
     const int NB = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;
     fasq_chain* c = new fasq_chain();
     c->n_steps = n_steps;
     c->B = B;
+    c->world = world;
+    c->rank = rank;
     c->nctas = sm_count();
+    if (max_ctas > 0) c->nctas = std::min(c->nctas, (int)max_ctas);
     // same tiling family as the per-launch GEMV default (gemv.cu plan_gemv)
     c->nw = 16;
     c->rw = NB == 1 ? 64 : NB == 2 ? 32 : NB == 4 ? 16 : 8;   // core::RowsPerWarp
@@ -285,7 +364,7 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
         if (sscanf(e, "%d,%d", &a, &b) == 2) { c->nw = a; c->st = b; }
     }
     c->R = c->rw * c->nw;
-    // validate + output arena layout
+    // validate + arena layout: every layer output is the FULL (all-rank) vector
     int64_t words = 16;   // [0..15]: reserved
     c->acc_off.resize(n_steps);
     c->acc_Fout.resize(n_steps);
@@ -303,8 +382,8 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
             if (L->d != c->d) { destroy_chain(c); return FASQ_E_UNSUPPORTED; }
             c->maxC = std::max(c->maxC, L->C);
             c->acc_off[s].push_back(words);
-            c->acc_Fout[s].push_back(L->F_out);
-            words += (int64_t)B * L->F_out;
+            c->acc_Fout[s].push_back(L->F_out * world);
+            words += (int64_t)B * L->F_out * world;
         }
         c->step_F_in[s] = (int)F_in;
         if (S.input_step < 0) {
@@ -315,7 +394,10 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
                 destroy_chain(c);
                 return FASQ_E_ARG;
             }
-            if (steps[S.input_step].layers[S.input_layer]->F_out != F_in) { destroy_chain(c); return FASQ_E_SHAPE; }
+            if (steps[S.input_step].layers[S.input_layer]->F_out * world != F_in) {
+                destroy_chain(c);
+                return FASQ_E_SHAPE;
+            }
         }
     }
     if (c->ext_F_in == 0) { destroy_chain(c); return FASQ_E_ARG; }   // the chain needs an external input
@@ -327,7 +409,13 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
     while (c->st > 1 && ring(c->st, c->nw) > kSmemBudget) --c->st;
     c->R = c->rw * c->nw;
     c->arena_words = words;
-    if (cudaMalloc(&c->arena, (size_t)words * 8) != cudaSuccess) { cudaGetLastError(); destroy_chain(c); return FASQ_E_OOM; }
+    if (cudaMalloc(&c->arenas, (size_t)words * 2 * 8) != cudaSuccess ||
+        cudaMalloc(&c->ctrl, 64) != cudaSuccess ||
+        cudaMalloc(&c->peers_dev, 8 * sizeof(void*)) != cudaSuccess) {
+        cudaGetLastError();
+        destroy_chain(c);
+        return FASQ_E_OOM;
+    }
     // work plan
     std::vector<ChainItem> items((size_t)n_steps * c->nctas);
     std::vector<ChainPhase> phases(n_steps);
@@ -358,7 +446,7 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
             total -= rt[lm];
             ks[lm] -= 1;
         }
-        if (total > c->nctas) { destroy_chain(c); return FASQ_E_UNSUPPORTED; }   // > #SMs row tiles
+        if (total > c->nctas) { destroy_chain(c); return FASQ_E_UNSUPPORTED; }   // > #CTAs row tiles
         for (int l = 0; l < nl; ++l) {
             if (ks[l] > 63) { destroy_chain(c); return FASQ_E_UNSUPPORTED; }   // counted-word count field
             c->acc_ks[s].push_back(ks[l]);
@@ -371,8 +459,10 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
                     ChainItem& w = items[(size_t)s * c->nctas + cta];
                     w.idx = L->idx;
                     w.cbimg = L->cbimg;
-                    w.y = c->arena + c->acc_off[s][l];
+                    w.y_off = c->acc_off[s][l];
                     w.F_out = (int)L->F_out;
+                    w.F_out_g = (int)(L->F_out * world);
+                    w.row0_g = (int)(L->F_out * rank);
                     w.F_out_pad = L->F_out_pad;
                     w.N_ss = L->N_ss;
                     w.C = L->C;
@@ -384,7 +474,7 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
                 }
         }
         phases[s].F_in = c->step_F_in[s];
-        phases[s].x_cnt = S.input_step < 0 ? nullptr : c->arena + c->acc_off[S.input_step][S.input_layer];
+        phases[s].x_off = S.input_step < 0 ? -1 : c->acc_off[S.input_step][S.input_layer];
         phases[s].x_ks = S.input_step < 0 ? 0 : c->acc_ks[S.input_step][S.input_layer];
     }
     const size_t xg = (size_t)32 * NB * E;
@@ -400,23 +490,74 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
     cudaError_t e = cudaMemcpyAsync(c->items, items.data(), items.size() * sizeof(ChainItem), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(c->phases, phases.data(), phases.size() * sizeof(ChainPhase), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->arenas, 0, (size_t)words * 2 * 8, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->ctrl, 0, 64, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);   // host vectors go out of scope
     if (e != cudaSuccess) { fasq_status s = cuda_fail(e, "chain upload"); destroy_chain(c); return s; }
+    std::vector<unsigned long long*> bases(world, nullptr);
+    bases[rank] = c->arenas;
+    fasq_status s = upload_peers(c, bases);
+    if (s != FASQ_OK) { destroy_chain(c); return s; }
+    c->peers_ready = world == 1;
     *out = c;
     return FASQ_OK;
 }
 
+fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int32_t B, void* stream,
+                              fasq_chain** out) {
+    return fasq_chain_create_tp(steps, n_steps, B, 1, 0, 0, stream, out);
+}
+
+fasq_status fasq_chain_ipc_handle(const fasq_chain* c, void* handle_out) {
+    if (!c || !handle_out) return FASQ_E_ARG;
+    cudaIpcMemHandle_t h;
+    FASQ_CUDA_TRY(cudaIpcGetMemHandle(&h, c->arenas));
+    std::memcpy(handle_out, &h, sizeof(h));
+    return FASQ_OK;
+}
+
+fasq_status fasq_chain_set_peers(fasq_chain* c, const void* handles) {
+    if (!c || !handles) return FASQ_E_ARG;
+    std::vector<unsigned long long*> bases(c->world, nullptr);
+    for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) { bases[r] = c->arenas; continue; }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const uint8_t*>(handles) + (size_t)r * sizeof(h), sizeof(h));
+        void* q = nullptr;
+        FASQ_CUDA_TRY(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_opened.push_back(q);
+        bases[r] = static_cast<unsigned long long*>(q);
+    }
+    return upload_peers(c, bases);
+}
+
+fasq_status fasq_chain_set_peer_chains(fasq_chain* c, const fasq_chain* const* chains) {
+    if (!c || !chains) return FASQ_E_ARG;
+    std::vector<unsigned long long*> bases(c->world, nullptr);
+    for (int r = 0; r < c->world; ++r) {
+        const fasq_chain* o = chains[r];
+        if (!o || o->world != c->world || o->arena_words != c->arena_words || o->n_steps != c->n_steps)
+            return FASQ_E_ARG;
+        bases[r] = o->arenas;
+    }
+    if (bases[c->rank] != c->arenas) return FASQ_E_ARG;
+    return upload_peers(c, bases);
+}
+
 fasq_status fasq_chain_run(fasq_chain* c, const void* x_dev, void* stream) {
     if (!c || !x_dev) return FASQ_E_ARG;
+    if (!c->peers_ready) { set_error("chain: world > 1 needs fasq_chain_set_peers first"); return FASQ_E_ARG; }
     cudaStream_t st = (cudaStream_t)stream;
-    // zero every step's counted accumulators (outputs stay readable until
-    // the next run)
-    FASQ_CUDA_TRY(cudaMemsetAsync(c->arena, 0, (size_t)c->arena_words * 8, st));
     ChainParams p{};
     p.items = static_cast<const ChainItem*>(c->items);
     p.phases = static_cast<const ChainPhase*>(c->phases);
     p.x_ext = static_cast<const __half*>(x_dev);
     p.trace = c->trace;
+    p.ctrl = c->ctrl;
+    p.peers = c->peers_dev;
+    p.arena_words = c->arena_words;
+    p.world = c->world;
+    p.rank = c->rank;
     p.pf = 0;
     if (const char* e = getenv("FASQ_CHAIN_PF")) p.pf = atoi(e);
     p.n_steps = c->n_steps;
@@ -432,7 +573,7 @@ fasq_status fasq_chain_run(fasq_chain* c, const void* x_dev, void* stream) {
         case 8: s = chain_nb<8>(c, p, st); break;
         default: s = FASQ_E_UNSUPPORTED;
     }
-    if (s == FASQ_OK) set_launch_count(1);   // + one memset node
+    if (s == FASQ_OK) set_launch_count(1);
     return s;
 }
 
@@ -444,7 +585,7 @@ fasq_status fasq_chain_output(const fasq_chain* c, int32_t step, int32_t layer, 
     const int64_t n = (int64_t)c->B * c->acc_Fout[step][layer];
     if (n <= 0) return FASQ_OK;
     k_counted_convert<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-        c->arena + c->acc_off[step][layer], n, c->acc_ks[step][layer], y_dev, (int)dtype);
+        c->arenas, c->arena_words, c->ctrl, c->acc_off[step][layer], n, c->acc_ks[step][layer], y_dev, (int)dtype);
     FASQ_CUDA_TRY(cudaGetLastError());
     set_launch_count(1);
     return FASQ_OK;

@@ -317,9 +317,12 @@ constexpr int kCntShift = 58;
 constexpr long long kCntBias = 1ll << 50;
 constexpr unsigned long long kCntMask = (1ull << kCntShift) - 1;
 
+// y points at this shard's row 0 inside a [B][ld] word array; rows >= F_out
+// (the shard's local rows) are padding and skipped.  System-scope reduction:
+// y may be a peer GPU's buffer (NVLink, fasq_chain_create_tp).
 template <int NB, int RW>
 __device__ __forceinline__ void counted_store(const RowTotals<NB, RW>& t, unsigned long long* y, int row0, int F_out,
-                                              int B) {
+                                              int ld, int B) {
     if (!t.own) return;
 #pragma unroll
     for (int h = 0; h < RowTotals<NB, RW>::H; ++h) {
@@ -331,7 +334,7 @@ __device__ __forceinline__ void counted_store(const RowTotals<NB, RW>& t, unsign
             long long v = __float2ll_rn(t.v[h][b] * kAccScale);
             v = max(-(kCntBias - 1), min(kCntBias - 1, v));   // |partial| < 2^18 (fp16 range is 2^16)
             const unsigned long long add = (1ull << kCntShift) + (unsigned long long)(kCntBias + v);
-            asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(y + (size_t)b * F_out + row), "l"(add) : "memory");
+            asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" :: "l"(y + (size_t)b * ld + row), "l"(add) : "memory");
         }
     }
 }
@@ -361,10 +364,13 @@ __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned lon
 #pragma unroll
             for (int e = 0; e < D; ++e) v[u][e] = 0;
         }
-        // poll: reload every word of this thread until all are final
+        // poll: reload every word of this thread until all are final (a
+        // watchdog turns a lost producer into a kernel error, not a hang)
         bool done = false;
+        const unsigned long long t_start = dev::globaltimer();
         while (!done) {
             done = true;
+            if (dev::globaltimer() - t_start > 4000000000ull) __trap();
 #pragma unroll
             for (int u = 0; u < XPT; ++u) {
                 if (!need[u]) continue;
@@ -375,7 +381,7 @@ __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned lon
 #pragma unroll
                 for (int e = 0; e < D; ++e) {
                     if ((v[u][e] >> kCntShift) == want) continue;
-                    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v[u][e]) : "l"(src + e) : "memory");
+                    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v[u][e]) : "l"(src + e) : "memory");
                 }
             }
 #pragma unroll

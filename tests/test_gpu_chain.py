@@ -147,3 +147,58 @@ def test_chain_llama_block_sampled(F, oracle_lib):
                 ok, info = parity_ok(yall[:, j0:j1], ref, xin, xin.shape[1])
                 assert ok, (s, n, j0, info)
     chain.free()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_chain_tensor_parallel_fused_gather(F, oracle_lib, world):
+    """fasq_chain_create_tp: `world` row-sharded ranks emulated as chains of
+    ONE process on one GPU (max_ctas = SMs / world each, concurrent streams),
+    peers wired with fasq_chain_set_peer_chains.  Every rank's outputs are the
+    full vectors (the fused all-gather) and match the oracle of the unsharded
+    layers; repeated runs are deterministic (arena parity flips)."""
+    h, ffn, kv = 1024, 2048, 256
+    names = [("q", h, h), ("k", kv, h), ("v", kv, h), ("o", h, h), ("g", ffn, h), ("u", ffn, h), ("d", h, ffn)]
+    full = {}
+    for i, (n, fo, fi) in enumerate(names):
+        full[n] = synth.random_layer(fo, fi, 2, 256, seed=700 + i)
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    chains, keep = [], []
+    for r in range(world):
+        L = {}
+        for (n, fo, fi) in names:
+            cb, idx = full[n]
+            rows = fo // world
+            L[n] = F.import_layer(torch.from_numpy(cb).cuda(),
+                                  torch.from_numpy(np.ascontiguousarray(idx[:, r * rows:(r + 1) * rows])).cuda(), fi)
+        keep.append(L)
+        steps = [([L["q"], L["k"], L["v"]], None), ([L["o"]], (0, 0)), ([L["g"], L["u"]], (1, 0)),
+                 ([L["d"]], (2, 0))]
+        chains.append(F.Chain(steps, B=1, world=world, rank=r, max_ctas=nsm // world))
+    for c in chains:
+        c.set_peer_chains(chains)
+    x = synth.activation(1, h, seed=3)
+    xd = torch.from_numpy(x).cuda()
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    outs = []
+    for rep in range(2):
+        torch.cuda.synchronize()
+        for c, s in zip(chains, streams):
+            c.run(xd, stream=s)
+        torch.cuda.synchronize()
+        outs.append([c.output(3, 0, out_dtype=torch.int64).clone() for c in chains])
+    torch.cuda.synchronize()
+    for r in range(1, world):
+        assert torch.equal(outs[0][0], outs[0][r])          # every rank holds the same gathered vector
+    assert torch.equal(outs[0][0], outs[1][0])              # deterministic across runs
+    flat = [("q", "k", "v"), ("o",), ("g", "u"), ("d",)]
+    srcs = [None, (0, 0), (1, 0), (2, 0)]
+    c0 = chains[world - 1]
+    for s, ns in enumerate(flat):
+        xin = x if srcs[s] is None else c0.output(srcs[s][0], srcs[s][1], out_dtype=torch.float16).cpu().numpy()
+        for l, n in enumerate(ns):
+            cb, idx = full[n]
+            y = c0.output(s, l, out_dtype=torch.float32).cpu().numpy()
+            ok, info = parity_ok(y, oracle_lib.gemv(cb, idx, xin), xin, xin.shape[1])
+            assert ok, (world, s, n, info)
+    for c in chains:
+        c.free()
