@@ -163,8 +163,13 @@ class DecodeStep:
     point, deterministic, no split-K merge phase); the consumer rounds them to
     fp16 x on load; each launch zeroes the accumulators of the launch two
     steps back (no longer read) and warms L2 with the next launch's first
-    stages.  N > 1: rows are sharded and each chain output (q, o, gate, down)
-    is materialised as fp16 and all-gathered over NCCL."""
+    stages.  N > 1: rows are sharded; by default the token still runs as ONE
+    chain kernel per GPU (fasq_chain_create_tp) whose GEMV epilogues red.add
+    every rank's rows into every rank's arena over NVLink peer memory (the
+    row-shard all-gather fused into the GEMV; arena IPC handles exchanged once
+    through torch.distributed).  FASQ_BENCH_TP=nccl selects the baseline:
+    per-launch GEMVs with each chain output (q, o, gate, down) materialised as
+    fp16 and all-gathered with NCCL."""
 
     NAMES = [("q_proj", "k_proj", "v_proj"), ("o_proj",), ("gate_proj", "up_proj"), ("down_proj",)]
     FEEDS = {1: "q_proj", 2: "o_proj", 3: "gate_proj"}   # launch i reads this output of launch i-1
@@ -180,16 +185,26 @@ class DecodeStep:
         self.seq = [(b, i) for b in range(len(blocks)) for i in range(4)]
         self.acc_mode = world == 1
         self.chain = None
-        if self.acc_mode and os.environ.get("FASQ_BENCH_CHAIN", "1") == "1":
-            # the whole token as ONE persistent kernel (fasq_chain_*)
+        use_chain = os.environ.get("FASQ_BENCH_CHAIN", "1") == "1"
+        if world > 1:
+            use_chain = use_chain and os.environ.get("FASQ_BENCH_TP", "fused") != "nccl"
+        self.tp_mode = "single-gpu" if world == 1 else "fused-p2p"
+        if use_chain:
+            # the whole token as ONE persistent kernel per GPU (fasq_chain_*)
             import paper_2605_04084_b200 as F
             steps = []
             for (b, i) in self.seq:
                 pos = len(steps)
                 src = None if pos == 0 else (pos - 1, 0)
                 steps.append(([blocks[b][k] for k in self.NAMES[i]], src))
-            self.chain = F.Chain(steps, B=1)
+            self.chain = F.Chain(steps, B=1, world=world, rank=rank)
+            if world > 1:
+                import torch.distributed as dist
+                handles = [None] * world
+                dist.all_gather_object(handles, self.chain.ipc_handle(), group=pg)
+                self.chain.set_peers(handles)
             self.out_f16 = torch.empty((1, 4096), dtype=f16, device=dev)
+            self.acc_mode = True
         elif self.acc_mode:
             # one int64 accumulator slab per launch position of the token
             self.acc = []
@@ -204,6 +219,7 @@ class DecodeStep:
                 self.acc.append((slab, outs))
             self.out_f16 = torch.empty((1, 4096), dtype=f16, device=dev)
         else:
+            self.tp_mode = "nccl-allgather"
             self.bufs = {}
             for (name, fo, fi) in synth.LLAMA3_8B_LAYERS:
                 self.bufs[name] = torch.empty((1, fo // world), dtype=f16, device=dev)
@@ -263,8 +279,12 @@ class DecodeStep:
         return self.out
 
 
-def capture(fn):
+def capture(fn, world=1):
     import torch
+    if world > 1:   # TP chain kernels spin-wait on their peers: start together
+        import torch.distributed as dist
+        torch.cuda.synchronize()
+        dist.barrier()
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
@@ -281,6 +301,9 @@ def capture(fn):
 def timed(graph, steps, warmup, rank, world, pg=None):
     import torch
     import torch.distributed as dist
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()
     for _ in range(warmup):
         graph.replay()
     torch.cuda.synchronize()
@@ -461,7 +484,7 @@ def main():
     step.h.copy_(__import__("synth").torch_activation(1, 4096, seed=11))
 
     # ---- device-resident timed region (graph of the whole step) ----
-    g = capture(lambda: step.run(flags=F.FLAG_PDL))
+    g = capture(lambda: step.run(flags=F.FLAG_PDL), world)
     launches_per_step = step.launches
     peaks, peak_src = _peaks()
     with ClockSampler(local) as clk:
@@ -478,7 +501,7 @@ def main():
         out = step.run(flags=F.FLAG_PDL)
         yh.copy_(out, non_blocking=True)
 
-    ge = capture(e2e_fn)
+    ge = capture(e2e_fn, world)
     ms_e2e = timed(ge, args.steps, args.warmup, rank, world, pg)
 
     tok_s = 1000.0 / ms
@@ -488,6 +511,9 @@ def main():
     # timed with CUDA events on the launching stream, after the graph timing
     kern_ms, kern_name, traffic = ms, "whole step (per-launch GEMVs)", None
     if step.chain is not None:
+        if world > 1:
+            torch.cuda.synchronize()
+            dist.barrier()
         for _ in range(3):
             step.chain.run(step.h)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -499,7 +525,8 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         kern_ms = e0.elapsed_time(e1) / nk
-        kern_name = "k_chain (one launch = the 224 GEMVs of a token) + its accumulator memset"
+        kern_name = "k_chain (one launch = the 224 GEMVs of a token%s)" % (
+            "" if world == 1 else ", this rank's row shard, all-gather fused over NVLink")
         traffic = K_CHAIN_NCU_DRAM_BYTES
     achieved = gbytes / (kern_ms * 1e-3) / 1e9
 
@@ -529,7 +556,7 @@ def main():
                        "executor": "persistent chain kernel (fasq_chain_*)" if step.chain is not None
                                    else "one grouped GEMV launch per step",
                        "global_batch": 1, "seq_len": 1,
-                       "parallelism": "row-shard-tp%d+nccl-allgather" % world if world > 1 else "single-gpu",
+                       "parallelism": ("row-shard-tp%d+%s" % (world, step.tp_mode)) if world > 1 else "single-gpu",
                        "d": D, "C": C, "weights_bytes_per_step": gbytes,
                        "l2": "inputs larger than L2 (%.2f GB of PQ weights per step vs 126 MB L2)" % (gbytes / 1e9),
                        "timing": "CUDA graph of one step, K replays between CUDA events, max over ranks"},

@@ -202,3 +202,48 @@ def test_chain_tensor_parallel_fused_gather(F, oracle_lib, world):
             assert ok, (world, s, n, info)
     for c in chains:
         c.free()
+
+
+def _ipc_worker(rank, world, port, q):
+    import os
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    import paper_2605_04084_b200 as F
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        cb, idx = synth.random_layer(512, 512, 2, 64, seed=rank)
+        L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), 512)
+        ch = F.Chain([([L], None)], B=1, world=world, rank=rank, max_ctas=8)
+        handles = [None] * world
+        dist.all_gather_object(handles, ch.ipc_handle())
+        ch.set_peers(handles)          # opens the peer arenas (cudaIpcOpenMemHandle)
+        dist.barrier()
+        ch.free()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as e:            # reported to the parent
+        q.put((rank, repr(e)))
+
+
+def test_chain_ipc_handles_between_processes():
+    """The multi-process plumbing of the TP chain: two ranks (processes) on one
+    GPU export their arena IPC handles, exchange them through
+    torch.distributed and open each other's arena.  (Running the TP kernels
+    needs one GPU per rank: two processes time-slice one GPU; the kernel path
+    is covered in-process by test_chain_tensor_parallel_fused_gather.)"""
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res
