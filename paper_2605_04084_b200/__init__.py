@@ -17,7 +17,7 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libfasq.so")
+LIB_PATH = os.environ.get("FASQ_LIB_PATH") or os.path.join(_PKG, "lib", "libfasq.so")   # override: A/B experiments only
 
 FASQ_F16, FASQ_F32, FASQ_ACC_I64 = 0, 1, 2
 GEMM_AUTO, GEMM_LUT, GEMM_EXPAND_TC = 0, 1, 2
