@@ -204,7 +204,8 @@ typedef struct fasq_chain fasq_chain; /* opaque */
  * polls only the words of its own K range until they are final.  Same
  * numerics as chained fasq_gemv_grouped calls with FASQ_ACC_I64 outputs.
  * The layers must outlive the chain.  Synchronises `stream`.
- * FASQ_E_UNSUPPORTED: a step needs more row tiles than SMs, or > 63 K-splits. */
+ * A step with more row tiles than SMs gives several work items per CTA.
+ * FASQ_E_UNSUPPORTED: the SMEM plan does not fit, or > 63 K-splits. */
 fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int32_t B, void* stream,
                               fasq_chain** out);
 

@@ -37,7 +37,7 @@
 struct fasq_chain {
     int n_steps = 0, B = 0, d = 0, nctas = 0;
     int world = 1, rank = 0;                         // row-sharded tensor parallelism (fasq_chain_create_tp)
-    int rw = 0, nw = 0, st = 0, R = 0, gmax = 1, maxC = 1;
+    int rw = 0, nw = 0, st = 0, R = 0, gmax = 1, maxC = 1, mi = 1;
     size_t smem = 0;
     std::vector<std::vector<int64_t>> acc_off;       // per step, per layer: word offset in one arena buffer
     std::vector<std::vector<int64_t>> acc_Fout;      // per step, per layer: GLOBAL F_out (words per batch row)
@@ -86,6 +86,7 @@ struct ChainParams {
     long long arena_words;      // words per buffer
     int world, rank;
     int n_steps, nctas, B, gmax, cbb_max;
+    int mi;                     // work items per (step, CTA): [n_steps][nctas][mi]
     int pf;                     // producer: L2-prefetch this many groups of the next step's item
 };
 
@@ -118,15 +119,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         // producer: every step's stages, back to back (no dependence on x)
         if (lane == 0) {
             int it = 0;
-            for (int ph = 0; ph < p.n_steps; ++ph) {
-                const ChainItem& w = p.items[(size_t)ph * p.nctas + blockIdx.x];
+            for (int phj = 0; phj < p.n_steps * p.mi; ++phj) {
+                const int ph = phj / p.mi;
+                const ChainItem& w = p.items[((size_t)ph * p.nctas + blockIdx.x) * p.mi + phj % p.mi];
                 if (w.rows_valid <= 0) continue;
                 const uint32_t cbb = (uint32_t)w.C * 32u * E;
                 const uint32_t chunk = (uint32_t)w.rows_valid * 32u;
-                if (p.pf > 0 && ph + 1 < p.n_steps) {
-                    // warm L2 with the head of the next step's item: HBM keeps
-                    // streaming across the grid-wide wait between the steps
-                    const ChainItem& nw = p.items[(size_t)(ph + 1) * p.nctas + blockIdx.x];
+                if (p.pf > 0 && ph + 1 < p.n_steps && phj % p.mi == 0) {
+                    // warm L2 with the head of the next step's first item
+                    const ChainItem& nw = p.items[((size_t)(ph + 1) * p.nctas + blockIdx.x) * p.mi];
                     if (nw.rows_valid > 0) {
                         const int ge = min(nw.g_end, nw.g_begin + p.pf);
                         for (int g = nw.g_begin; g < ge; ++g)
@@ -186,12 +187,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     const auto co = core::chunk_offsets<RW>(wrow0, lane);
     int slot = 0;            // ring position of the next stage (running across steps)
     uint32_t par_ring = 0;   // its mbarrier phase parity
-    for (int ph = 0; ph < p.n_steps; ++ph) {
+    for (int phj = 0; phj < p.n_steps * p.mi; ++phj) {
+        const int ph = phj / p.mi, j = phj % p.mi;
         // the work item and phase are read-only for the kernel's lifetime
-        const ChainItem w = p.items[(size_t)ph * p.nctas + blockIdx.x];
+        const ChainItem w = p.items[((size_t)ph * p.nctas + blockIdx.x) * p.mi + j];
         const ChainPhase phs = p.phases[ph];
+        // trace: t0 at the step's first item, t1/t2 of its first item, t3 after its last
         unsigned long long* tr = p.trace ? p.trace + ((size_t)ph * p.nctas + blockIdx.x) * 4 : nullptr;
-        if (tr && threadIdx.x == 0) tr[0] = dev::globaltimer();
+        if (tr && threadIdx.x == 0 && j == 0) tr[0] = dev::globaltimer();
         if (w.rows_valid <= 0) continue;
         // every consumer warp is done with the previous step's s_x
         asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
@@ -200,9 +203,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             core::stage_x_counted<D, NB, NW>(s_x, cur + phs.x_off, phs.x_ks, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
         else
             core::stage_x<D, NB, NW>(s_x, p.x_ext, 0, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
-        if (tr && threadIdx.x == 0) tr[1] = dev::globaltimer();
+        if (tr && threadIdx.x == 0 && j == 0) tr[1] = dev::globaltimer();
         asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
-        if (tr && threadIdx.x == 0) tr[2] = dev::globaltimer();
+        if (tr && threadIdx.x == 0 && j == 0) tr[2] = dev::globaltimer();
         float acc[RW][NB];
 #pragma unroll
         for (int q = 0; q < RW; ++q)
@@ -416,10 +419,11 @@ fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, 
         destroy_chain(c);
         return FASQ_E_OOM;
     }
-    // work plan
-    std::vector<ChainItem> items((size_t)n_steps * c->nctas);
+    // work plan: per step a list of items (row tile x K-range), dealt to the
+    // CTAs round-robin; more items than CTAs (e.g. B = 8: 128-row tiles) ->
+    // several items per CTA per step, [n_steps][nctas][mi]
+    std::vector<std::vector<ChainItem>> per_step(n_steps);
     std::vector<ChainPhase> phases(n_steps);
-    for (auto& w : items) w = ChainItem{};
     for (int s = 0; s < n_steps; ++s) {
         const fasq_chain_step& S = steps[s];
         const int nl = S.n_layers;
@@ -446,17 +450,15 @@ fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, 
             total -= rt[lm];
             ks[lm] -= 1;
         }
-        if (total > c->nctas) { destroy_chain(c); return FASQ_E_UNSUPPORTED; }   // > #CTAs row tiles
         for (int l = 0; l < nl; ++l) {
             if (ks[l] > 63) { destroy_chain(c); return FASQ_E_UNSUPPORTED; }   // counted-word count field
             c->acc_ks[s].push_back(ks[l]);
         }
-        int cta = 0;
         for (int l = 0; l < nl; ++l) {
             const fasq_layer* L = S.layers[l];
             for (int r = 0; r < rt[l]; ++r)
-                for (int k = 0; k < ks[l]; ++k, ++cta) {
-                    ChainItem& w = items[(size_t)s * c->nctas + cta];
+                for (int k = 0; k < ks[l]; ++k) {
+                    ChainItem w{};
                     w.idx = L->idx;
                     w.cbimg = L->cbimg;
                     w.y_off = c->acc_off[s][l];
@@ -471,12 +473,20 @@ fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, 
                     w.g_begin = (int)((int64_t)k * L->n_groups / ks[l]);
                     w.g_end = (int)((int64_t)(k + 1) * L->n_groups / ks[l]);
                     c->gmax = std::max(c->gmax, w.g_end - w.g_begin);
+                    per_step[s].push_back(w);
                 }
         }
         phases[s].F_in = c->step_F_in[s];
         phases[s].x_off = S.input_step < 0 ? -1 : c->acc_off[S.input_step][S.input_layer];
         phases[s].x_ks = S.input_step < 0 ? 0 : c->acc_ks[S.input_step][S.input_layer];
     }
+    c->mi = 1;
+    for (const auto& v : per_step) c->mi = std::max(c->mi, (int)((v.size() + c->nctas - 1) / c->nctas));
+    std::vector<ChainItem> items((size_t)n_steps * c->nctas * c->mi);
+    for (auto& w : items) w = ChainItem{};
+    for (int s = 0; s < n_steps; ++s)
+        for (size_t q = 0; q < per_step[s].size(); ++q)
+            items[((size_t)s * c->nctas + q % c->nctas) * c->mi + q / c->nctas] = per_step[s][q];
     const size_t xg = (size_t)32 * NB * E;
     c->smem = (size_t)c->st * (cbb_max + (size_t)c->R * 32) + (size_t)c->gmax * xg + 16 * c->st;
     if (c->smem > kSmemBudget) { destroy_chain(c); set_error("chain: SMEM plan too large"); return FASQ_E_UNSUPPORTED; }
@@ -564,6 +574,7 @@ fasq_status fasq_chain_run(fasq_chain* c, const void* x_dev, void* stream) {
     p.nctas = c->nctas;
     p.B = c->B;
     p.gmax = c->gmax;
+    p.mi = c->mi;
     p.cbb_max = c->maxC * 32 * entry_bytes(c->d);
     fasq_status s;
     switch (c->d) {

@@ -116,9 +116,11 @@ def test_chain_input_from_other_layer_and_step(F, oracle_lib):
     _chain_vs_oracle(F, oracle_lib, specs, 1, 2, 256)
 
 
-def test_chain_llama_block_sampled(F, oracle_lib):
+@pytest.mark.parametrize("B", [1, 8])
+def test_chain_llama_block_sampled(F, oracle_lib, B):
     """One Llama-3-8B-shaped block at full size (the bench's k_chain launch
-    configuration), checked on sampled rows of every layer."""
+    configuration; B = 8 uses 128-row tiles -> several items per CTA), checked
+    on sampled rows of every layer."""
     sh = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096), ("g", 14336, 4096),
           ("u", 14336, 4096), ("d", 4096, 14336)]
     Ls = {}
@@ -127,8 +129,8 @@ def test_chain_llama_block_sampled(F, oracle_lib):
         Ls[n] = (F.import_layer(cb, idx, fi), cb, idx)
     steps = [([Ls["q"][0], Ls["k"][0], Ls["v"][0]], None), ([Ls["o"][0]], (0, 0)),
              ([Ls["g"][0], Ls["u"][0]], (1, 0)), ([Ls["d"][0]], (2, 0))]
-    chain = F.Chain(steps, B=1)
-    x = synth.torch_activation(1, 4096, seed=5)
+    chain = F.Chain(steps, B=B)
+    x = synth.torch_activation(B, 4096, seed=5)
     chain.run(x)
     torch.cuda.synchronize()
     names = [("q", "k", "v"), ("o",), ("g", "u"), ("d",)]
