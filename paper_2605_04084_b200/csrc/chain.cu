@@ -55,6 +55,7 @@ struct fasq_chain {
     bool peers_ready = true;
     void* items = nullptr;                           // device [n_steps][nctas] ChainItem
     void* phases = nullptr;                          // device [n_steps] ChainPhase
+    void* maps = nullptr;                            // device CUtensorMap per layer (d <= 2: codebook pair boxes)
     unsigned long long* trace = nullptr;             // user buffer (fasq_chain_trace), not owned
 };
 
@@ -65,6 +66,7 @@ namespace {
 struct ChainItem {
     const uint8_t* idx;
     const uint8_t* cbimg;
+    const void* cbmap;          // d <= 2: 3-D tensor map {32 words, n_groups, C} over cbimg (pair boxes)
     long long y_off;            // word offset of the layer's counted-accumulator output [B][F_out_g] in a buffer
     int F_out, F_out_g, row0_g; // local rows of this rank's shard, global F_out, global row of local row 0
     int F_out_pad, N_ss, C;
@@ -88,7 +90,21 @@ struct ChainParams {
     int n_steps, nctas, B, gmax, cbb_max;
     int mi;                     // work items per (step, CTA): [n_steps][nctas][mi]
     int pf;                     // producer: L2-prefetch this many groups of the next step's item
+    int dbg;                    // experiments only (FASQ_CHAIN_DBG): bit 0 = consumers skip the gather
+                                // loop, bit 1 = producer skips the copies (compute on stale SMEM)
 };
+
+// d <= 2 (4-B codebook entries) runs on codebook PAIR stages: a separate
+// CS-deep ring of [C][2][32]-word slots, each filled by ONE 3-D TMA box that
+// interleaves groups g and g+1 of the [group][C][32] image into 256-B k-rows
+// (core::compute_group_pair: the gather address is one PRMT).  The index
+// chunks keep their own ST-deep ring (one group per stage).
+template <int D>
+struct ChainPair {
+    static constexpr bool value = D <= 2;
+};
+constexpr int kChainCS = 2;             // codebook pair slots
+constexpr uint32_t kPairSlot = 65536;   // pair slot stride: [<= 256][2][32] words
 
 template <int D, int NB, int NW, int ST>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
@@ -96,13 +112,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     constexpr int RW = core::RowsPerWarp<NB>::value;
     constexpr int R = RW * NW;
     constexpr int XG = 32 * NB * E;
+    constexpr bool PAIR = ChainPair<D>::value;
+    constexpr int CS = kChainCS;
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* s_cb = smem;                                       // ST * cbb_max
-    uint8_t* s_idx = s_cb + ST * p.cbb_max;                     // ST * R * 32
+    uint8_t* s_cb = smem;                                       // PAIR: CS * 64 KiB, else ST * cbb_max
+    uint8_t* s_idx = s_cb + (PAIR ? CS * kPairSlot : ST * p.cbb_max);   // ST * R * 32
     uint8_t* s_x = s_idx + ST * R * 32;                         // gmax * XG
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_x + p.gmax * XG);
     const uint32_t cb_u = dev::smem_u32(s_cb), idx_u = dev::smem_u32(s_idx), x_u = dev::smem_u32(s_x);
     const uint32_t full0 = dev::smem_u32(&bars[0]), empty0 = dev::smem_u32(&bars[ST]);
+    const uint32_t cfull0 = dev::smem_u32(&bars[2 * ST]), cempty0 = dev::smem_u32(&bars[2 * ST + CS]);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -111,6 +130,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             dev::mbar_init(full0 + 8 * s, 1);
             dev::mbar_init(empty0 + 8 * s, NW);
         }
+        if (PAIR) {
+#pragma unroll
+            for (int s = 0; s < CS; ++s) {
+                dev::mbar_init(cfull0 + 8 * s, 1);
+                dev::mbar_init(cempty0 + 8 * s, NW);
+            }
+        }
         dev::fence_barrier_init();
     }
     __syncthreads();
@@ -118,7 +144,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     if (warp == NW) {
         // producer: every step's stages, back to back (no dependence on x)
         if (lane == 0) {
-            int it = 0;
+            int it = 0, cit = 0;
             for (int phj = 0; phj < p.n_steps * p.mi; ++phj) {
                 const int ph = phj / p.mi;
                 const ChainItem& w = p.items[((size_t)ph * p.nctas + blockIdx.x) * p.mi + phj % p.mi];
@@ -136,11 +162,26 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                     }
                 }
                 for (int g = w.g_begin; g < w.g_end; ++g, ++it) {
+                    if (PAIR && ((g - w.g_begin) & 1) == 0) {
+                        // groups g, g+1 -> one pair slot (g+1 past the layer: zero fill)
+                        const int cs = cit % CS;
+                        if (cit >= CS) dev::mbar_wait(cempty0 + 8 * cs, ((cit / CS) + 1) & 1);
+                        if (p.dbg & 2) {
+                            dev::mbar_arrive(cfull0 + 8 * cs);
+                        } else {
+                            dev::mbar_arrive_expect_tx(cfull0 + 8 * cs, 2u * cbb);
+                            dev::tma_load_3d(cb_u + (uint32_t)cs * kPairSlot, w.cbmap, 0, g, 0, cfull0 + 8 * cs);
+                        }
+                        ++cit;
+                    }
                     const int slot = it % ST;
                     if (it >= ST) dev::mbar_wait(empty0 + 8 * slot, ((it / ST) + 1) & 1);
                     const uint32_t full = full0 + 8 * slot;
-                    dev::mbar_arrive_expect_tx(full, chunk + cbb);
-                    dev::bulk_g2s(cb_u + (uint32_t)slot * (uint32_t)p.cbb_max, w.cbimg + (size_t)g * cbb, cbb, full);
+                    if (p.dbg & 2) { dev::mbar_arrive(full); continue; }
+                    dev::mbar_arrive_expect_tx(full, PAIR ? chunk : chunk + cbb);
+                    if (!PAIR)
+                        dev::bulk_g2s(cb_u + (uint32_t)slot * (uint32_t)p.cbb_max, w.cbimg + (size_t)g * cbb, cbb,
+                                      full);
                     dev::bulk_g2s(idx_u + (uint32_t)slot * R * 32u, w.idx + ((size_t)g * w.F_out_pad + w.r0) * 32,
                                   chunk, full);
                 }
@@ -187,6 +228,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     const auto co = core::chunk_offsets<RW>(wrow0, lane);
     int slot = 0;            // ring position of the next stage (running across steps)
     uint32_t par_ring = 0;   // its mbarrier phase parity
+    int cslot = 0;           // PAIR: codebook pair slot and parity
+    uint32_t cpar = 0;
+    // PAIR gather constant = PRMT operand b: byte 0 = h*128 + 4*lane, byte 2 =
+    // pair slot (64 KiB stride), so the address is PRMT(idx word, lbv) + the
+    // ring base (uniform) -> LDS [R + UR]
+    const uint32_t lb = (uint32_t)lane * 4u;
     for (int phj = 0; phj < p.n_steps * p.mi; ++phj) {
         const int ph = phj / p.mi, j = phj % p.mi;
         // the work item and phase are read-only for the kernel's lifetime
@@ -213,15 +260,25 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
         const bool active = wrow0 < w.rows_valid;
         for (int i = 0; i < ng; ++i) {
+            if (PAIR && (i & 1) == 0) dev::mbar_wait(cfull0 + 8 * cslot, cpar);
             dev::mbar_wait(full0 + 8 * slot, par_ring);
-            if (active) {
+            if (active && !(p.dbg & 1)) {
                 uint32_t xv[NB][E / 4];
                 core::load_x<D, NB>(xv, s_x + i * XG, lane);
-                core::compute_group<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb + slot * p.cbb_max, xv, lane);
+                if constexpr (PAIR)
+                    core::compute_group_pair<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb,
+                                                        lb + ((uint32_t)(i & 1) << 7) + ((uint32_t)cslot << 16), xv);
+                else
+                    core::compute_group<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb + slot * p.cbb_max, xv,
+                                                   lane);
             }
             __syncwarp();
             if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
             if (++slot == ST) { slot = 0; par_ring ^= 1u; }
+            if (PAIR && ((i & 1) == 1 || i == ng - 1)) {
+                if (lane == 0) dev::mbar_arrive(cempty0 + 8 * cslot);
+                if (++cslot == CS) { cslot = 0; cpar ^= 1u; }
+            }
         }
         core::RowTotals<NB, RW> tot;
         core::reduce_rows<NB, RW>(acc, tot, lane);
@@ -243,6 +300,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" :: "l"(p.ctrl), "r"(par ^ 1u) : "memory");
     }
 }
+
+// dynamic SMEM the chain plans against: the sm_100 opt-in maximum (227 KiB)
+// minus headroom for the kernel's few bytes of static SMEM
+constexpr size_t kChainSmem = 227 * 1024 - 256;
 
 struct ChainCfg {
     int rw, nw, st;
@@ -326,6 +387,7 @@ void destroy_chain(fasq_chain* c) {
     if (c->peers_dev) cudaFree(c->peers_dev);
     if (c->items) cudaFree(c->items);
     if (c->phases) cudaFree(c->phases);
+    if (c->maps) cudaFree(c->maps);
     delete c;
 }
 
@@ -406,10 +468,12 @@ fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, 
     if (c->ext_F_in == 0) { destroy_chain(c); return FASQ_E_ARG; }   // the chain needs an external input
     const int E = entry_bytes(c->d);
     const size_t cbb_max = (size_t)c->maxC * 32 * E;
-    auto ring = [&](int st, int nw) { return (size_t)st * (cbb_max + (size_t)c->rw * nw * 32) + 16 * 1024; };
-    while (c->st > 2 && ring(c->st, c->nw) > kSmemBudget) --c->st;
-    if (ring(c->st, c->nw) > kSmemBudget && c->nw > 8) c->nw = 8;
-    while (c->st > 1 && ring(c->st, c->nw) > kSmemBudget) --c->st;
+    const bool pair = c->d <= 2;   // ChainPair: codebook pair ring next to the index ring
+    auto cbring = [&](int st) { return pair ? (size_t)kChainCS * kPairSlot : (size_t)st * cbb_max; };
+    auto ring = [&](int st, int nw) { return cbring(st) + (size_t)st * c->rw * nw * 32 + 2 * 1024; };
+    while (c->st > 2 && ring(c->st, c->nw) > kChainSmem) --c->st;
+    if (ring(c->st, c->nw) > kChainSmem && c->nw > 8) c->nw = 8;
+    while (c->st > 1 && ring(c->st, c->nw) > kChainSmem) --c->st;
     c->R = c->rw * c->nw;
     c->arena_words = words;
     if (cudaMalloc(&c->arenas, (size_t)words * 2 * 8) != cudaSuccess ||
@@ -419,6 +483,41 @@ fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, 
         destroy_chain(c);
         return FASQ_E_OOM;
     }
+    // d <= 2: one 3-D tensor map per distinct layer, {32 words, n_groups, C}
+    // with strides {C*128, 128} B over cbimg, box {32, 2, C}: a box at group g
+    // lands in SMEM as [C][g, g+1][32 words] (the pair layout)
+    std::vector<const fasq_layer*> map_layers;
+    if (pair) {
+        PFN_encodeTiled enc = get_encode();
+        if (!enc) { destroy_chain(c); set_error("chain: cuTensorMapEncodeTiled unavailable"); return FASQ_E_CUDA; }
+        for (int s = 0; s < n_steps; ++s)
+            for (int l = 0; l < steps[s].n_layers; ++l)
+                if (std::find(map_layers.begin(), map_layers.end(), steps[s].layers[l]) == map_layers.end())
+                    map_layers.push_back(steps[s].layers[l]);
+        std::vector<CUtensorMap> hm(map_layers.size());
+        for (size_t i = 0; i < map_layers.size(); ++i) {
+            const fasq_layer* L = map_layers[i];
+            cuuint64_t gdim[3] = {32, (cuuint64_t)L->n_groups, (cuuint64_t)L->C};
+            cuuint64_t gstr[2] = {(cuuint64_t)L->C * 128, 128};
+            cuuint32_t box[3] = {32, 2, (cuuint32_t)L->C};
+            cuuint32_t es[3] = {1, 1, 1};
+            CUresult r = enc(&hm[i], CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, L->cbimg, gdim, gstr, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) { destroy_chain(c); set_error("chain: codebook tensor map encode failed"); return FASQ_E_CUDA; }
+        }
+        if (cudaMalloc(&c->maps, hm.size() * sizeof(CUtensorMap)) != cudaSuccess ||
+            cudaMemcpy(c->maps, hm.data(), hm.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaGetLastError();
+            destroy_chain(c);
+            return FASQ_E_OOM;
+        }
+    }
+    auto map_of = [&](const fasq_layer* L) -> const void* {
+        if (!pair) return nullptr;
+        const size_t i = std::find(map_layers.begin(), map_layers.end(), L) - map_layers.begin();
+        return static_cast<const CUtensorMap*>(c->maps) + i;
+    };
     // work plan: per step a list of items (row tile x K-range), dealt to the
     // CTAs round-robin; more items than CTAs (e.g. B = 8: 128-row tiles) ->
     // several items per CTA per step, [n_steps][nctas][mi]
@@ -461,6 +560,7 @@ fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, 
                     ChainItem w{};
                     w.idx = L->idx;
                     w.cbimg = L->cbimg;
+                    w.cbmap = map_of(L);
                     w.y_off = c->acc_off[s][l];
                     w.F_out = (int)L->F_out;
                     w.F_out_g = (int)(L->F_out * world);
@@ -488,8 +588,12 @@ fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, 
         for (size_t q = 0; q < per_step[s].size(); ++q)
             items[((size_t)s * c->nctas + q % c->nctas) * c->mi + q / c->nctas] = per_step[s][q];
     const size_t xg = (size_t)32 * NB * E;
-    c->smem = (size_t)c->st * (cbb_max + (size_t)c->R * 32) + (size_t)c->gmax * xg + 16 * c->st;
-    if (c->smem > kSmemBudget) { destroy_chain(c); set_error("chain: SMEM plan too large"); return FASQ_E_UNSUPPORTED; }
+    auto smem_of = [&](int st) {
+        return cbring(st) + (size_t)st * c->R * 32 + (size_t)c->gmax * xg + 16 * (st + kChainCS);
+    };
+    while (c->st > 1 && smem_of(c->st) > kChainSmem) --c->st;
+    c->smem = smem_of(c->st);
+    if (c->smem > kChainSmem) { destroy_chain(c); set_error("chain: SMEM plan too large"); return FASQ_E_UNSUPPORTED; }
     cudaStream_t st = (cudaStream_t)stream;
     if (cudaMalloc(&c->items, items.size() * sizeof(ChainItem)) != cudaSuccess ||
         cudaMalloc(&c->phases, phases.size() * sizeof(ChainPhase)) != cudaSuccess) {
@@ -570,6 +674,8 @@ fasq_status fasq_chain_run(fasq_chain* c, const void* x_dev, void* stream) {
     p.rank = c->rank;
     p.pf = 0;
     if (const char* e = getenv("FASQ_CHAIN_PF")) p.pf = atoi(e);
+    p.dbg = 0;
+    if (const char* e = getenv("FASQ_CHAIN_DBG")) p.dbg = atoi(e);
     p.n_steps = c->n_steps;
     p.nctas = c->nctas;
     p.B = c->B;

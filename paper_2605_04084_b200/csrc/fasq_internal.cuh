@@ -1,6 +1,7 @@
 // fasq_internal.cuh -- shared definitions of the product library (CUDA, sm_100a).
 // Nothing here is shared with oracle/ (which is independent test infrastructure).
 #pragma once
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -125,6 +126,12 @@ fasq_status gemm_lut_launch(const fasq_layer* L, const __half* X, int64_t M, voi
 fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void* Y,
                            fasq_dtype yt, cudaStream_t st);
 bool gemm_tc_supported(const fasq_layer* L, int64_t M);
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda);
+// nullptr if unavailable (gemm_tc.cu).
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled get_encode();
 fasq_status pack_run(const __half* W, fasq_layer* L, const fasq_pack_params* p, cudaStream_t st,
                      __half* cb_logical_out, uint8_t* idx_logical_out);
 
@@ -239,6 +246,13 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
+}
+// 3-D tiled TMA load (tensor map in global memory, 64-B aligned), completion
+// on mbarrier.  Out-of-range box elements are zero-filled and still counted.
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* map, int c0, int c1, int c2, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        :: "r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar) : "memory");
 }
 // L2 prefetch through the TMA engine (no SMEM destination).
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {

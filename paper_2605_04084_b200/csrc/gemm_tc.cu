@@ -283,9 +283,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     }
 }
 
-typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+size_t tc_smem_bytes(int C) {
+    return 1024 + (size_t)TC_STAGES * (TC_MT * TC_M * TC_K * 2 + TC_N * TC_K * 2 + TC_N * 32 + (size_t)C * 128) + 8 * 16 + 16;
+}
+
+}  // namespace
 
 PFN_encodeTiled get_encode() {
     static PFN_encodeTiled fn = nullptr;
@@ -300,12 +302,6 @@ PFN_encodeTiled get_encode() {
     });
     return fn;
 }
-
-size_t tc_smem_bytes(int C) {
-    return 1024 + (size_t)TC_STAGES * (TC_MT * TC_M * TC_K * 2 + TC_N * TC_K * 2 + TC_N * 32 + (size_t)C * 128) + 8 * 16 + 16;
-}
-
-}  // namespace
 
 bool gemm_tc_supported(const fasq_layer* L, int64_t M) {
     return L->d == 2 && L->C <= 256 && (L->F_in % 64) == 0 && M >= 1 && M < (1ll << 31) &&

@@ -233,6 +233,44 @@ __device__ __forceinline__ void compute_group(float (&acc)[RW][NB], const uint8_
     }
 }
 
+// E = 4 (d <= 2) over a codebook PAIR stage: two consecutive groups staged
+// as [C][2][32] words (one 3-D TMA box, chain.cu), i.e. 256-B k-rows.  The
+// gather address (k << 8) | (h*128 + 4*s) is then ONE PRMT of the index word
+// with the lane constant lb = h*128 + 4*s (byte 0) -- no IMAD/LEA -- and the
+// LDS adds the uniform ring base cbs; lbv's byte 2 may carry the slot (64 KiB
+// units): PRMT, LDS, FHFMA x d per index.  Lane s still reads bank s for any
+// k (one wavefront per warp-gather).
+template <int D, int NB, int RW>
+__device__ __forceinline__ void compute_group_pair(float (&acc)[RW][NB], const uint8_t* idx_stage,
+                                                   const ChunkOffs<RW>& co, const uint8_t* cbs, uint32_t lbv,
+                                                   const uint32_t (&xv)[NB][1]) {
+    constexpr int NCH = ChunkOffs<RW>::N;
+#pragma unroll
+    for (int ci = 0; ci < NCH; ++ci) {
+        const uint8_t* ca = idx_stage + co.o[ci];
+        uint32_t w[4];
+        if (RW >= 16) {
+            const uint4 v = lds<uint4>(ca);
+            w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+        } else {
+            const uint2 v = lds<uint2>(ca);
+            w[0] = v.x; w[1] = v.y; w[2] = 0u; w[3] = 0u;
+        }
+        constexpr int NJ = RW >= 16 ? 16 : RW;
+        uint32_t c[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+            c[j] = lds<uint32_t>(cbs + dev::prmt(w[j >> 2], lbv, 0x7604u | ((uint32_t)(j & 3) << 4)));
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                float& a = acc[ci * 16 + j][b];
+                a = (D == 1) ? dev::fhfma1(c[j], xv[b][0], a) : dev::fhfma2(c[j], xv[b][0], a);
+            }
+    }
+}
+
 // Transposed butterfly over the 32 lanes: v[i] (i < N, N = 32/16/8) holds
 // this lane's partial of row i; afterwards v[0] holds the total of row
 // (lane >> (5 - log2 N)) (each row on 32/N lanes).  Fixed order.
