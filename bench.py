@@ -411,6 +411,94 @@ def prefill_tflops(M=2048, iters=10):
     return out
 
 
+KINDS = (("qkv", ("q_proj", "k_proj", "v_proj")), ("o", ("o_proj",)), ("gate_up", ("gate_proj", "up_proj")),
+         ("down", ("down_proj",)))
+
+
+def decode_sweep(peak, settings=((2, 256), (2, 128), (4, 256), (1, 256), (2, 64), (8, 256)), runs=30):
+    """configs[1]/[2]: the whole-model decode token through the chain kernel at
+    each (d, C) of the sweep (effective 4-bit (2,256), 3-bit (2,128), ...),
+    plus per-LAYER-SHAPE GEMV throughput measured inside the token: the
+    %globaltimer trace of one run gives every step's span (last output of the
+    previous step -> last output of this step, median over the 32 blocks), and
+    that step's algorithmic bytes / span is its GB/s.  Bytes per layer =
+    indices F_out*F_in/d + codebooks (F_in/d)*C*d*2 + x + y (counted
+    accumulator words, 8 B).  Model size fraction = (PQ bytes of the 224
+    layers + fp16 embedding, lm_head and norms) / fp16 model bytes."""
+    import numpy as np
+    import torch
+
+    import paper_2605_04084_b200 as F
+    import synth
+
+    shapes = {n: (fo, fi) for (n, fo, fi) in synth.LLAMA3_8B_LAYERS}
+    nb = synth.LLAMA3_8B_BLOCKS
+    dense_other = 2 * (2 * 128256 * 4096 + (2 * nb + 1) * 4096)   # embed + lm_head + norms, fp16 bytes
+    dense_lin = 2 * nb * sum(fo * fi for (fo, fi) in shapes.values())
+    out = {}
+    for (d, c) in settings:
+        blocks = []
+        for b in range(nb):
+            Ls = {}
+            for li, (name, fo, fi) in enumerate(synth.LLAMA3_8B_LAYERS):
+                cb, idx = synth.torch_random_layer(fo, fi, d, c, seed=7000 + b * 7 + li)
+                Ls[name] = F.import_layer(cb, idx, fi)
+                del cb, idx
+            blocks.append(Ls)
+
+        def lbytes(n):
+            fo, fi = shapes[n]
+            return fo * fi // d + (fi // d) * c * d * 2 + 2 * fi + 8 * fo
+        steps = []
+        for b in range(nb):
+            for (_, names) in KINDS:
+                steps.append(([blocks[b][n] for n in names], None if not steps else (len(steps) - 1, 0)))
+        ch = F.Chain(steps, B=1)
+        x = synth.torch_activation(1, 4096)
+        for _ in range(3):
+            ch.run(x)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(runs):
+            ch.run(x)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / runs
+        tok_bytes = nb * sum(lbytes(n) for n in shapes)
+        T = len(steps)
+        buf = torch.zeros((T, ch.ctas, 4), dtype=torch.int64, device="cuda")
+        ch.trace(buf)
+        ch.run(x)
+        torch.cuda.synchronize()
+        ch.trace(None)
+        t = buf.cpu().numpy().astype(np.int64)
+        ends = t[:, :, 3].max(axis=1)
+        spans = np.diff(np.concatenate([[t[0, :, 0][t[0, :, 0] > 0].min()], ends]))
+        per = {}
+        for k, (kind, names) in enumerate(KINDS):
+            us = float(np.median(spans[k::len(KINDS)])) / 1e3
+            bts = sum(lbytes(n) for n in names)
+            gbs = bts / (us * 1e-6) / 1e9
+            per[kind] = {"shapes": ["%dx%d" % shapes[n] for n in names], "us": round(us, 3),
+                         "GBps": round(gbs, 1), "frac": round(gbs / peak, 3)}
+        info = blocks[0]["q_proj"].info
+        pq = nb * sum(blocks[0][n].info["index_bytes"] + blocks[0][n].info["codebook_bytes"] for n in shapes)
+        out["d%d_C%d" % (d, c)] = {
+            "ms_per_token": round(ms, 4), "tok_s": round(1e3 / ms, 1),
+            "GBps": round(tok_bytes / (ms * 1e-3) / 1e9, 1), "frac": round(tok_bytes / (ms * 1e-3) / 1e9 / peak, 3),
+            "bits_per_weight_4096x4096": round(info["bits_per_weight"], 4),
+            "model_size_frac_of_fp16": round((pq + dense_other) / (dense_lin + dense_other), 4),
+            "per_layer_shape": per}
+        del ch
+        for Ls in blocks:
+            for L in Ls.values():
+                L.free()
+        del blocks
+        torch.cuda.synchronize()
+    return out
+
+
 def pack_time():
     import torch
 
@@ -516,15 +604,27 @@ def main():
             dist.barrier()
         for _ in range(3):
             step.chain.run(step.h)
+        # k_chain launches alone, replayed from a CUDA graph (as in the timed
+        # region) on the capture stream, CUDA events on that stream
+        nk = 10
+        ks = torch.cuda.Stream()
+        ks.wait_stream(torch.cuda.current_stream())
+        kg = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(ks):
+            with torch.cuda.graph(kg, stream=ks):
+                for _ in range(nk):
+                    step.chain.run(step.h)
+        torch.cuda.synchronize()
+        reps = max(2, args.steps // (4 * nk))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        nk = max(10, args.steps // 4)
+        with torch.cuda.stream(ks):
+            kg.replay()
+            e0.record(ks)
+            for _ in range(reps):
+                kg.replay()
+            e1.record(ks)
         torch.cuda.synchronize()
-        e0.record()
-        for _ in range(nk):
-            step.chain.run(step.h)
-        e1.record()
-        torch.cuda.synchronize()
-        kern_ms = e0.elapsed_time(e1) / nk
+        kern_ms = e0.elapsed_time(e1) / (reps * nk)
         kern_name = "k_chain (one launch = the 224 GEMVs of a token%s)" % (
             "" if world == 1 else ", this rank's row shard, all-gather fused over NVLink")
         traffic = K_CHAIN_NCU_DRAM_BYTES
@@ -536,6 +636,10 @@ def main():
             side["prefill_gemm_M2048"] = prefill_tflops()
         except Exception as e:
             side["prefill_gemm_M2048"] = {"error": str(e)[:200]}
+        try:
+            side["decode_sweep"] = decode_sweep(peak)
+        except Exception as e:
+            side["decode_sweep"] = {"error": str(e)[:200]}
         try:
             side["gpu_pack"] = pack_time()
         except Exception as e:

@@ -55,7 +55,6 @@ struct fasq_chain {
     bool peers_ready = true;
     void* items = nullptr;                           // device [n_steps][nctas] ChainItem
     void* phases = nullptr;                          // device [n_steps] ChainPhase
-    void* maps = nullptr;                            // device CUtensorMap per layer (d <= 2: codebook pair boxes)
     unsigned long long* trace = nullptr;             // user buffer (fasq_chain_trace), not owned
 };
 
@@ -103,8 +102,7 @@ template <int D>
 struct ChainPair {
     static constexpr bool value = D <= 2;
 };
-constexpr int kChainCS = 2;             // codebook pair slots
-constexpr uint32_t kPairSlot = 65536;   // pair slot stride: [<= 256][2][32] words
+constexpr int kChainCS = kPairSlots;
 
 template <int D, int NB, int NW, int ST>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
@@ -259,25 +257,41 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
 #pragma unroll
             for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
         const bool active = wrow0 < w.rows_valid;
-        for (int i = 0; i < ng; ++i) {
-            if (PAIR && (i & 1) == 0) dev::mbar_wait(cfull0 + 8 * cslot, cpar);
-            dev::mbar_wait(full0 + 8 * slot, par_ring);
-            if (active && !(p.dbg & 1)) {
-                uint32_t xv[NB][E / 4];
-                core::load_x<D, NB>(xv, s_x + i * XG, lane);
-                if constexpr (PAIR)
-                    core::compute_group_pair<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb,
-                                                        lb + ((uint32_t)(i & 1) << 7) + ((uint32_t)cslot << 16), xv);
-                else
-                    core::compute_group<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb + slot * p.cbb_max, xv,
-                                                   lane);
-            }
-            __syncwarp();
-            if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
-            if (++slot == ST) { slot = 0; par_ring ^= 1u; }
-            if (PAIR && ((i & 1) == 1 || i == ng - 1)) {
+        if constexpr (PAIR) {
+            // one iteration per codebook pair slot: groups i (h = 0), i+1 (h = 1)
+            const bool run = active && !(p.dbg & 1);
+            for (int i = 0; i < ng; i += 2) {
+                dev::mbar_wait(cfull0 + 8 * cslot, cpar);
+                const uint32_t lbs = lb + ((uint32_t)cslot << 16);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (h == 1 && i + 1 >= ng) break;
+                    dev::mbar_wait(full0 + 8 * slot, par_ring);
+                    if (run) {
+                        uint32_t xv[NB][E / 4];
+                        core::load_x<D, NB>(xv, s_x + (i + h) * XG, lane);
+                        core::compute_group_pair<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb,
+                                                            lbs + ((uint32_t)h << 7), xv);
+                    }
+                    __syncwarp();
+                    if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+                    if (++slot == ST) { slot = 0; par_ring ^= 1u; }
+                }
                 if (lane == 0) dev::mbar_arrive(cempty0 + 8 * cslot);
                 if (++cslot == CS) { cslot = 0; cpar ^= 1u; }
+            }
+        } else {
+            for (int i = 0; i < ng; ++i) {
+                dev::mbar_wait(full0 + 8 * slot, par_ring);
+                if (active && !(p.dbg & 1)) {
+                    uint32_t xv[NB][E / 4];
+                    core::load_x<D, NB>(xv, s_x + i * XG, lane);
+                    core::compute_group<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb + slot * p.cbb_max, xv,
+                                                   lane);
+                }
+                __syncwarp();
+                if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+                if (++slot == ST) { slot = 0; par_ring ^= 1u; }
             }
         }
         core::RowTotals<NB, RW> tot;
@@ -301,9 +315,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     }
 }
 
-// dynamic SMEM the chain plans against: the sm_100 opt-in maximum (227 KiB)
-// minus headroom for the kernel's few bytes of static SMEM
-constexpr size_t kChainSmem = 227 * 1024 - 256;
+constexpr size_t kChainSmem = kSmemMax;
 
 struct ChainCfg {
     int rw, nw, st;
@@ -387,7 +399,6 @@ void destroy_chain(fasq_chain* c) {
     if (c->peers_dev) cudaFree(c->peers_dev);
     if (c->items) cudaFree(c->items);
     if (c->phases) cudaFree(c->phases);
-    if (c->maps) cudaFree(c->maps);
     delete c;
 }
 
@@ -483,41 +494,6 @@ fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, 
         destroy_chain(c);
         return FASQ_E_OOM;
     }
-    // d <= 2: one 3-D tensor map per distinct layer, {32 words, n_groups, C}
-    // with strides {C*128, 128} B over cbimg, box {32, 2, C}: a box at group g
-    // lands in SMEM as [C][g, g+1][32 words] (the pair layout)
-    std::vector<const fasq_layer*> map_layers;
-    if (pair) {
-        PFN_encodeTiled enc = get_encode();
-        if (!enc) { destroy_chain(c); set_error("chain: cuTensorMapEncodeTiled unavailable"); return FASQ_E_CUDA; }
-        for (int s = 0; s < n_steps; ++s)
-            for (int l = 0; l < steps[s].n_layers; ++l)
-                if (std::find(map_layers.begin(), map_layers.end(), steps[s].layers[l]) == map_layers.end())
-                    map_layers.push_back(steps[s].layers[l]);
-        std::vector<CUtensorMap> hm(map_layers.size());
-        for (size_t i = 0; i < map_layers.size(); ++i) {
-            const fasq_layer* L = map_layers[i];
-            cuuint64_t gdim[3] = {32, (cuuint64_t)L->n_groups, (cuuint64_t)L->C};
-            cuuint64_t gstr[2] = {(cuuint64_t)L->C * 128, 128};
-            cuuint32_t box[3] = {32, 2, (cuuint32_t)L->C};
-            cuuint32_t es[3] = {1, 1, 1};
-            CUresult r = enc(&hm[i], CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, L->cbimg, gdim, gstr, box, es,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (r != CUDA_SUCCESS) { destroy_chain(c); set_error("chain: codebook tensor map encode failed"); return FASQ_E_CUDA; }
-        }
-        if (cudaMalloc(&c->maps, hm.size() * sizeof(CUtensorMap)) != cudaSuccess ||
-            cudaMemcpy(c->maps, hm.data(), hm.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice) != cudaSuccess) {
-            cudaGetLastError();
-            destroy_chain(c);
-            return FASQ_E_OOM;
-        }
-    }
-    auto map_of = [&](const fasq_layer* L) -> const void* {
-        if (!pair) return nullptr;
-        const size_t i = std::find(map_layers.begin(), map_layers.end(), L) - map_layers.begin();
-        return static_cast<const CUtensorMap*>(c->maps) + i;
-    };
     // work plan: per step a list of items (row tile x K-range), dealt to the
     // CTAs round-robin; more items than CTAs (e.g. B = 8: 128-row tiles) ->
     // several items per CTA per step, [n_steps][nctas][mi]
@@ -560,7 +536,7 @@ fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, 
                     ChainItem w{};
                     w.idx = L->idx;
                     w.cbimg = L->cbimg;
-                    w.cbmap = map_of(L);
+                    w.cbmap = L->cbmap;
                     w.y_off = c->acc_off[s][l];
                     w.F_out = (int)L->F_out;
                     w.F_out_g = (int)(L->F_out * world);

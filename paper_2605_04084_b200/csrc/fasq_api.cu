@@ -36,6 +36,7 @@ static void destroy(fasq_layer* L) {
     if (!L) return;
     if (L->idx) cudaFree(L->idx);
     if (L->cbimg) cudaFree(L->cbimg);
+    if (L->cbmap) cudaFree(L->cbmap);
     if (L->cb) cudaFree(L->cb);
     if (L->ws) cudaFree(L->ws);
     if (L->tickets) cudaFree(L->tickets);

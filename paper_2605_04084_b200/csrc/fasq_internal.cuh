@@ -50,6 +50,9 @@ struct fasq_layer {
     int device = 0;
     uint8_t* idx = nullptr;    // physical indices
     uint8_t* cbimg = nullptr;  // GEMV codebook image
+    void* cbmap = nullptr;     // d <= 2: device CUtensorMap {32 words, n_groups, C} over cbimg, strides
+                               // {C*128, 128} B: a box {32, 2, C} at group g lands in SMEM as the
+                               // codebook PAIR [C][g, g+1][32 words] (256-B k-rows, gemv_core.cuh)
     __half* cb = nullptr;      // logical codebooks
     int64_t idx_bytes = 0, cbimg_bytes = 0, cb_bytes = 0;
     // GEMV split-K workspace (partials + per-row-tile arrival tickets), grown
@@ -93,9 +96,14 @@ inline size_t set_max_dyn_smem(K kern) {
     return lim;
 }
 constexpr size_t kSmemBudget = 227 * 1024 - 2048;   // dynamic-SMEM planning budget (static SMEM headroom)
+constexpr size_t kSmemMax = 227 * 1024 - 256;       // opt-in maximum minus a few bytes of static SMEM
+// codebook PAIR ring (d <= 2): slots of [<= 256][2][32] words, 64 KiB stride so
+// that the slot is byte 2 of the gather's PRMT constant
+constexpr int kPairSlots = 2;
+constexpr uint32_t kPairSlot = 65536;
 
 // ---- layout kernels (layout.cu) ---------------------------------------------
-fasq_status alloc_layer_storage(fasq_layer* L);
+fasq_status alloc_layer_storage(fasq_layer* L);   // idx, cbimg, cb and (d <= 2) cbmap
 fasq_status build_physical_from_logical(fasq_layer* L, const __half* cb_logical,
                                         const uint8_t* idx_logical, cudaStream_t st);
 fasq_status build_cbimg(fasq_layer* L, cudaStream_t st);

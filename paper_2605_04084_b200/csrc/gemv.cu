@@ -40,6 +40,7 @@ constexpr int kMaxGroup = 4;   // layers per grouped launch (q/k/v, gate/up)
 struct GemvLayerArgs {
     const uint8_t* idx;     // [n_groups][F_out_pad][32]
     const uint8_t* cbimg;   // [n_groups][C][32][E]
+    const void* cbmap;      // d <= 2: codebook PAIR tensor map (fasq_layer::cbmap)
     void* y;                // [B][F_out]
     float* partial;         // [ksplit][B][F_out_pad] (ksplit > 1)
     unsigned long long* arrive;   // [row_tiles] u32 monotonically increasing arrival counters (8-B slots)
@@ -81,6 +82,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     constexpr int RW = core::RowsPerWarp<NB>::value;   // rows per consumer warp
     constexpr int R = RW * NW;                         // rows per CTA tile
     constexpr int XG = 32 * NB * E;                    // x bytes per staged group
+    constexpr bool PAIR = D <= 2;                      // codebook PAIR ring (gemv_core.cuh)
+    constexpr int CS = kPairSlots;
     extern __shared__ __align__(1024) uint8_t smem[];
 
     int li = 0;
@@ -99,15 +102,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     const int r0 = rt * R;
     const int rows_valid = min(R, F_out_pad - r0);   // multiple of 64
 
-    uint8_t* s_cb = smem;                                     // ST*CBB
-    uint8_t* s_idx = s_cb + ST * CBB;                         // ST*R*32
+    uint8_t* s_cb = smem;                                     // PAIR: CS*64 KiB, else ST*CBB
+    uint8_t* s_idx = s_cb + (PAIR ? CS * kPairSlot : ST * CBB);   // ST*R*32
     uint8_t* s_x = s_idx + ST * R * 32;                       // gmax*XG
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_x + p.gmax * XG);   // full[ST], empty[ST]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_x + p.gmax * XG);   // full[ST], empty[ST], cfull[CS], cempty[CS]
     const uint32_t cb_u = dev::smem_u32(s_cb);
     const uint32_t x_u = dev::smem_u32(s_x);
     const uint32_t idx_u = dev::smem_u32(s_idx);
     const uint32_t full0 = dev::smem_u32(&bars[0]);
     const uint32_t empty0 = dev::smem_u32(&bars[ST]);
+    const uint32_t cfull0 = dev::smem_u32(&bars[2 * ST]), cempty0 = dev::smem_u32(&bars[2 * ST + CS]);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -117,6 +121,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
         for (int s = 0; s < ST; ++s) {
             dev::mbar_init(full0 + 8 * s, 1);
             dev::mbar_init(empty0 + 8 * s, NW);
+        }
+        if (PAIR) {
+#pragma unroll
+            for (int s = 0; s < CS; ++s) {
+                dev::mbar_init(cfull0 + 8 * s, 1);
+                dev::mbar_init(cempty0 + 8 * s, NW);
+            }
         }
         dev::fence_barrier_init();
         dev::pdl_launch_dependents();   // let the next layer's CTAs start prefetching now
@@ -128,12 +139,18 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
         if (lane == 0) {
             const uint32_t idx_chunk = (uint32_t)rows_valid * 32u;
             for (int i = 0; i < ng; ++i) {
+                const int g = g_begin + i;
+                if (PAIR && (i & 1) == 0) {   // groups g, g+1 -> one pair slot (one 3-D TMA box)
+                    const int cs = (i >> 1) % CS;
+                    if ((i >> 1) >= CS) dev::mbar_wait(cempty0 + 8 * cs, (((i >> 1) / CS) + 1) & 1);
+                    dev::mbar_arrive_expect_tx(cfull0 + 8 * cs, 2u * CBB);
+                    dev::tma_load_3d(cb_u + (uint32_t)cs * kPairSlot, la.cbmap, 0, g, 0, cfull0 + 8 * cs);
+                }
                 const int slot = i % ST;
                 if (i >= ST) dev::mbar_wait(empty0 + 8 * slot, ((i / ST) + 1) & 1);
-                const int g = g_begin + i;
                 const uint32_t full = full0 + 8 * slot;
-                dev::mbar_arrive_expect_tx(full, idx_chunk + CBB);
-                dev::bulk_g2s(cb_u + (uint32_t)slot * CBB, la.cbimg + (size_t)g * CBB, CBB, full);
+                dev::mbar_arrive_expect_tx(full, PAIR ? idx_chunk : idx_chunk + CBB);
+                if (!PAIR) dev::bulk_g2s(cb_u + (uint32_t)slot * CBB, la.cbimg + (size_t)g * CBB, CBB, full);
                 dev::bulk_g2s(idx_u + (uint32_t)slot * R * 32u, la.idx + ((size_t)g * F_out_pad + r0) * 32,
                               idx_chunk, full);
                 if (i == ng - 1 && p.nn > 0) {
@@ -183,16 +200,42 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     const auto co = core::chunk_offsets<RW>(wrow0, lane);
     int slot = 0;
     uint32_t par = 0;
-    for (int i = 0; i < ng; ++i) {
-        dev::mbar_wait(full0 + 8 * slot, par);
-        if (active) {
-            uint32_t xv[NB][E / 4];
-            core::load_x<D, NB>(xv, s_x + i * XG, lane);
-            core::compute_group<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb + slot * CBB, xv, lane);
+    if constexpr (PAIR) {
+        int cslot = 0;
+        uint32_t cpar = 0;
+        const uint32_t lb = (uint32_t)lane * 4u;
+        for (int i = 0; i < ng; i += 2) {
+            dev::mbar_wait(cfull0 + 8 * cslot, cpar);
+            const uint32_t lbs = lb + ((uint32_t)cslot << 16);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (h == 1 && i + 1 >= ng) break;
+                dev::mbar_wait(full0 + 8 * slot, par);
+                if (active) {
+                    uint32_t xv[NB][E / 4];
+                    core::load_x<D, NB>(xv, s_x + (i + h) * XG, lane);
+                    core::compute_group_pair<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb,
+                                                        lbs + ((uint32_t)h << 7), xv);
+                }
+                __syncwarp();
+                if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+                if (++slot == ST) { slot = 0; par ^= 1u; }
+            }
+            if (lane == 0) dev::mbar_arrive(cempty0 + 8 * cslot);
+            if (++cslot == CS) { cslot = 0; cpar ^= 1u; }
         }
-        __syncwarp();
-        if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
-        if (++slot == ST) { slot = 0; par ^= 1u; }
+    } else {
+        for (int i = 0; i < ng; ++i) {
+            dev::mbar_wait(full0 + 8 * slot, par);
+            if (active) {
+                uint32_t xv[NB][E / 4];
+                core::load_x<D, NB>(xv, s_x + i * XG, lane);
+                core::compute_group<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb + slot * CBB, xv, lane);
+            }
+            __syncwarp();
+            if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+            if (++slot == ST) { slot = 0; par ^= 1u; }
+        }
     }
 
     // ------------------------------ epilogue --------------------------------
@@ -375,12 +418,12 @@ static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB, bool spin
     for (int l = 0; l < nl; ++l) maxC = std::max(maxC, Ls[l]->C);
     // large codebook images (d = 4/8 with C = 256: 64/128 KiB per group): fewer
     // stages, then fewer rows per CTA
-    auto ring = [&](int st, int nw) {
-        return (size_t)st * ((size_t)maxC * 32 * E + (size_t)pl.rw * nw * 32) + 16 * 1024;
-    };
-    while (pl.st > 2 && ring(pl.st, pl.nw) > kSmemBudget) --pl.st;
-    if (ring(pl.st, pl.nw) > kSmemBudget && pl.nw > 8) pl.nw = 8;
-    while (pl.st > 1 && ring(pl.st, pl.nw) > kSmemBudget) --pl.st;
+    const bool pair = E == 4;   // codebook PAIR ring (d <= 2)
+    auto cbring = [&](int st) { return pair ? (size_t)kPairSlots * kPairSlot : (size_t)st * maxC * 32 * E; };
+    auto ring = [&](int st, int nw) { return cbring(st) + (size_t)st * pl.rw * nw * 32 + 2 * 1024; };
+    while (pl.st > 2 && ring(pl.st, pl.nw) > kSmemMax) --pl.st;
+    if (ring(pl.st, pl.nw) > kSmemMax && pl.nw > 8) pl.nw = 8;
+    while (pl.st > 1 && ring(pl.st, pl.nw) > kSmemMax) --pl.st;
     pl.R = pl.rw * pl.nw;
     int sms = num_sms();
     if (!spin_merge) {   // ACC outputs: no co-residency requirement; FASQ_GEMV_OCC = CTAs per SM to plan for
@@ -414,7 +457,11 @@ static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB, bool spin
     pl.gmax = 1;
     for (int l = 0; l < nl; ++l) pl.gmax = std::max(pl.gmax, (Ls[l]->n_groups + pl.ksplit[l] - 1) / pl.ksplit[l]);
     const size_t xg = (size_t)32 * NB * E;
-    pl.smem = (size_t)pl.st * ((size_t)maxC * 32 * E + (size_t)pl.R * 32) + (size_t)pl.gmax * xg + 16 * pl.st;
+    auto smem_of = [&](int st) {
+        return cbring(st) + (size_t)st * pl.R * 32 + (size_t)pl.gmax * xg + 16 * (st + kPairSlots);
+    };
+    while (pl.st > 1 && smem_of(pl.st) > kSmemMax) --pl.st;
+    pl.smem = smem_of(pl.st);
     return pl;
 }
 
@@ -453,6 +500,7 @@ static fasq_status ensure_workspace(fasq_layer* L, int ksplit, int row_tiles, in
 static void fill_layer_args(GemvLayerArgs* a, const fasq_layer* L, const GemvPlan& pl, int l, int cta, void* y) {
     a->idx = L->idx;
     a->cbimg = L->cbimg;
+    a->cbmap = L->cbmap;
     a->y = y;
     a->partial = L->ws;
     a->arrive = reinterpret_cast<unsigned long long*>(L->tickets);

@@ -41,6 +41,26 @@ fasq_status alloc_layer_storage(fasq_layer* L) {
     if (e != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
     e = cudaMalloc(&L->cb, (size_t)L->cb_bytes);
     if (e != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
+    if (L->E == 4) {
+        // codebook PAIR tensor map (the map only depends on the cbimg pointer and
+        // shape, so it is encoded now and stays valid for the layer's lifetime)
+        PFN_encodeTiled enc = get_encode();
+        if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return FASQ_E_CUDA; }
+        CUtensorMap m;
+        cuuint64_t gdim[3] = {32, (cuuint64_t)L->n_groups, (cuuint64_t)L->C};
+        cuuint64_t gstr[2] = {(cuuint64_t)L->C * 128, 128};
+        cuuint32_t box[3] = {32, 2, (cuuint32_t)L->C};
+        cuuint32_t es[3] = {1, 1, 1};
+        if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, L->cbimg, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            set_error("codebook pair tensor map: encode failed");
+            return FASQ_E_CUDA;
+        }
+        e = cudaMalloc(&L->cbmap, sizeof(CUtensorMap));
+        if (e != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
+        FASQ_CUDA_TRY(cudaMemcpy(L->cbmap, &m, sizeof(m), cudaMemcpyHostToDevice));
+    }
     return FASQ_OK;
 }
 

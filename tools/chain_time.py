@@ -20,7 +20,7 @@ blocks, nbytes = [], 0
 for b in range(nb):
     Ls = {}
     for li, (name, fo, fi) in enumerate(synth.LLAMA3_8B_LAYERS):
-        cb, idx = synth.torch_random_layer(fo, fi, d, C, seed=b * 7 + li)
+        cb, idx = synth.torch_random_layer(fo, fi, d, C, seed=int(os.environ.get("SEEDBASE", "0")) + b * 7 + li)
         Ls[name] = F.import_layer(cb, idx, fi)
         nbytes += fo * fi // d + (fi // d) * C * d * 2 + 2 * B * fi + 4 * B * fo
     blocks.append(Ls)
@@ -30,11 +30,13 @@ for b in range(nb):
         steps.append(([blocks[b][n] for n in NAMES[i]], None if not steps else (len(steps) - 1, 0)))
 ch = F.Chain(steps, B=B)
 x = synth.torch_activation(B, 4096)
-for _ in range(5):
+if os.environ.get("XZERO"):
+    x.zero_()
+for _ in range(int(os.environ.get("WARM", "5"))):
     ch.run(x)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-n = 50
+n = int(os.environ.get("NRUN", "50"))
 e0.record()
 for _ in range(n):
     ch.run(x)
