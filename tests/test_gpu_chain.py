@@ -73,7 +73,7 @@ def test_chain_errors(F):
         F.Chain([([L1], (1, 0))])                  # forward reference
 
 
-def _chain_vs_oracle(F, oracle_lib, specs, B, d, C, seed0=300):
+def _chain_vs_oracle(F, oracle_lib, specs, B, d, C, seed0=300, max_ctas=0, runs=1):
     """specs: list of (layers [(F_out, F_in)], src) -> builds, runs, checks every layer."""
     rng_seed = seed0
     built = []
@@ -87,9 +87,10 @@ def _chain_vs_oracle(F, oracle_lib, specs, B, d, C, seed0=300):
             ls.append((L, cb, idx))
         built.append(ls)
         steps.append(([t[0] for t in ls], src))
-    chain = F.Chain(steps, B=B)
+    chain = F.Chain(steps, B=B, max_ctas=max_ctas)
     x = synth.activation(B, specs[0][0][0][1], seed=seed0)
-    chain.run(torch.from_numpy(x).cuda())
+    for _ in range(runs):
+        chain.run(torch.from_numpy(x).cuda())
     torch.cuda.synchronize()
     for s, ls in enumerate(built):
         src = steps[s][1]
@@ -107,6 +108,16 @@ def test_chain_entry_sizes_and_batches(F, oracle_lib, d, C, B):
     # ragged shapes: F_out not a multiple of 64, N_ss not a multiple of 32
     specs = [([(1000, 1016), (88, 1016)], None), ([(1016, 1000)], (0, 0)), ([(472, 1016)], (1, 0))]
     _chain_vs_oracle(F, oracle_lib, specs, B, d, C)
+
+
+@pytest.mark.parametrize("d,C,ctas", [(2, 256, 3), (2, 128, 5), (1, 256, 2)])
+def test_chain_long_k_ranges_codebook_pairs(F, oracle_lib, d, C, ctas):
+    """Few CTAs -> every item spans many groups (odd and even counts, items
+    starting at odd groups, a last group whose pair partner lies past the
+    layer): the codebook PAIR ring (d <= 2) wraps many times; three runs in a
+    row also cycle the double-buffered arenas."""
+    specs = [([(640, 4096), (192, 4096)], None), ([(4096, 640)], (0, 0)), ([(704, 4096)], (1, 0))]
+    _chain_vs_oracle(F, oracle_lib, specs, 1, d, C, seed0=900, max_ctas=ctas, runs=3)
 
 
 def test_chain_input_from_other_layer_and_step(F, oracle_lib):

@@ -67,6 +67,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
                 const int slot = g % ST;
                 if (g >= ST) dev::mbar_wait(empty0 + 8 * slot, ((g / ST) + 1) & 1);
                 const uint32_t full = full0 + 8 * slot;
+                if (VAR == 4) {   // indices bypass SMEM (LDG by the consumers): codebook only
+                    dev::mbar_arrive_expect_tx(full, CBB);
+                    dev::bulk_g2s(cb_u + (slot & 1) * 65536u, cb + (size_t)g * CBB, CBB, full);
+                    continue;
+                }
                 dev::mbar_arrive_expect_tx(full, (MODE == 3 ? 0u : CBB) + IDXB);
                 if (MODE != 3) dev::bulk_g2s(cb_u + slot * CBB, cb + (size_t)g * CBB, CBB, full);
                 dev::bulk_g2s(idx_u + slot * IDXB, my_idx + (size_t)g * IDXB, IDXB, full);
@@ -128,6 +133,54 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
         s += __shfl_xor_sync(0xffffffffu, s, 8);
         s += __shfl_xor_sync(0xffffffffu, s, 16);
         out[blockIdx.x * R + threadIdx.x] = s;
+    } else if (VAR == 4) {
+        // pair addressing (one PRMT per gather) + indices streamed with LDG.128
+        // straight into registers one group ahead (lane-contiguous 512-B chunks)
+        float acc[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+        const uint32_t xv = dev::lds32(x_u + lane * 4);
+        const uint32_t Lc = (uint32_t)lane * 4u;
+        const uint8_t* gb = my_idx + (size_t)warp * 2048 + (size_t)lane * 16;
+        uint4 cur[4], nxt[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cur[c] = __ldcs(reinterpret_cast<const uint4*>(gb + c * 512));
+        for (int g = 0; g < ng; ++g) {
+            const int slot = g % ST;
+            if (MODE != 2 || g < ST) dev::mbar_wait(full0 + 8 * slot, (g / ST) & 1);
+            if (g + 1 < ng) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    nxt[c] = __ldcs(reinterpret_cast<const uint4*>(gb + (size_t)(g + 1) * IDXB + c * 512));
+            }
+            if (MODE != 1 && MODE != 3) {
+                const uint32_t cbl = cb_u + (slot & 1) * 65536u;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const uint32_t w[4] = {cur[c].x, cur[c].y, cur[c].z, cur[c].w};
+                    uint32_t cv[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q)
+                        cv[q] = dev::lds32(cbl + dev::prmt(w[q >> 2], Lc, 0x7740u | ((uint32_t)(q & 3) << 4) | 4u));
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) acc[c * 16 + q] = dev::fhfma2(cv[q], xv, acc[c * 16 + q]);
+                }
+            }
+            __syncwarp();
+            if (MODE != 2 && lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) cur[c] = nxt[c];
+        }
+        float lo[32], hi[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            lo[i] = acc[i];
+            hi[i] = acc[32 + i];
+        }
+        transpose_reduce32<NW>(lo, lane);
+        transpose_reduce32<NW>(hi, lane);
+        out[blockIdx.x * R + warp * 64 + lane] = lo[0];
+        out[blockIdx.x * R + warp * 64 + 32 + lane] = hi[0];
     } else if (VAR == 2) {
         float acc[64];
 #pragma unroll
@@ -262,7 +315,9 @@ int main() {
     run<VAR, RPL, NW, ST, 3>(idx, cb, ng, out, nsm, NAME);
     RUN3(1, 1, 16, 3, "sub  nw16 st3");
     RUN3(2, 1, 16, 2, "sub256 nw16 st2");
-    RUN3(3, 1, 16, 2, "hyb256 nw16 st2");
-    RUN3(3, 1, 16, 3, "hyb256 nw16 st3");
+    RUN3(4, 1, 16, 2, "pair+ldg nw16 st2");
+    RUN3(4, 1, 15, 2, "pair+ldg nw15 st2");
+    RUN3(2, 1, 15, 2, "sub256 nw15 st2");
+    RUN3(2, 1, 16, 3, "sub256 nw16 st3");
     return 0;
 }
