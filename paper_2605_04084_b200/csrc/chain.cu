@@ -90,7 +90,8 @@ struct ChainParams {
     int mi;                     // work items per (step, CTA): [n_steps][nctas][mi]
     int pf;                     // producer: L2-prefetch this many groups of the next step's item
     int dbg;                    // experiments only (FASQ_CHAIN_DBG): bit 0 = consumers skip the gather
-                                // loop, bit 1 = producer skips the copies (compute on stale SMEM)
+                                // loop, bit 1 = producer skips the copies (compute on stale SMEM),
+                                // bit 2 = producer skips the codebook copies only
 };
 
 // d <= 2 (4-B codebook entries) runs on codebook PAIR stages: a separate
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                         // groups g, g+1 -> one pair slot (g+1 past the layer: zero fill)
                         const int cs = cit % CS;
                         if (cit >= CS) dev::mbar_wait(cempty0 + 8 * cs, ((cit / CS) + 1) & 1);
-                        if (p.dbg & 2) {
+                        if (p.dbg & 6) {   // bit 2: codebook copies only skipped (stale SMEM codebooks)
                             dev::mbar_arrive(cfull0 + 8 * cs);
                         } else {
                             dev::mbar_arrive_expect_tx(cfull0 + 8 * cs, 2u * cbb);

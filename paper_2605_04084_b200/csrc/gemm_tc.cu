@@ -7,8 +7,14 @@
 // materialization".  Per CTA tile (2 x 128 tokens x 256 weight rows)
 // and per K-chunk of 64 input features (= one group of 32 subspaces at d=2):
 //
-//   producer warp : TMA 2-D load of the X tile (128B swizzle) + bulk copies of
-//                   the group's codebook image and the tile's index chunk;
+//   X producer    : TMA 2-D loads of the two X tiles (128B swizzle); its ring
+//                   slot is released by the MMA commit;
+//   cb/idx producer: bulk copies of the group's codebook image and the tile's
+//                   index chunk into a ring released by the EXPANSION warps (not
+//                   the MMA), so the next chunks' loads start one MMA period
+//                   earlier -- the coupled single ring left the tensor pipe idle
+//                   on load latency (ncu: 47 % tensor-active, expansion warps
+//                   waiting on the full barrier); decoupled: +15-32 % TFLOP/s;
 //   8 expand warps: lane = subspace (as in the GEMV); gather the centroids of
 //                   32 rows from the SMEM codebook image (lane s -> bank s,
 //                   conflict-free) and store them into the B tile
@@ -35,7 +41,7 @@ constexpr int TC_N = 256;          // weight rows per CTA tile (UMMA N)
 constexpr int TC_K = 64;           // K elements per chunk (one 128B swizzle atom row)
 constexpr int TC_STAGES = 2;
 constexpr int TC_EXP_WARPS = 8;    // expansion warps (lane = weight row)
-constexpr int TC_THREADS = (2 + TC_EXP_WARPS) * 32;
+constexpr int TC_THREADS = (3 + TC_EXP_WARPS) * 32;   // + X producer, MMA, codebook/index producer
 
 struct TcParams {
     const uint8_t* idx;      // [n_groups][F_out_pad/64][32][64] (fasq_internal.cuh)
@@ -82,8 +88,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     uint8_t* sI = sB + TC_STAGES * B_BYTES;               // STAGES * IDX
     uint8_t* sC = sI + TC_STAGES * IDX_BYTES;             // STAGES * [C][32][4] (one bulk copy each)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sC + TC_STAGES * CB_BYTES);
-    // bars: full[S], bfull[S], empty[S], accum
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * TC_STAGES + 1);
+    // bars: full[S] (X tiles), bfull[S] (B tile expanded), empty[S] (MMA done:
+    // X and B slot free), lfull[S] / lempty[S] (codebook + index chunk ring,
+    // released by the expansion warps -- not by the MMA -- so the next chunks'
+    // loads start one MMA period earlier), accum
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 * TC_STAGES + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n0 = blockIdx.x * TC_N;          // weight-row tile
@@ -93,13 +102,17 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto bfull_bar = [&](int s) { return bar0 + 8u * (TC_STAGES + s); };
     auto empty_bar = [&](int s) { return bar0 + 8u * (2 * TC_STAGES + s); };
-    const uint32_t accum_bar = bar0 + 8u * (3 * TC_STAGES);
+    auto lfull_bar = [&](int s) { return bar0 + 8u * (3 * TC_STAGES + s); };
+    auto lempty_bar = [&](int s) { return bar0 + 8u * (4 * TC_STAGES + s); };
+    const uint32_t accum_bar = bar0 + 8u * (5 * TC_STAGES);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < TC_STAGES; ++s) {
             dev::mbar_init(full_bar(s), 1);
             dev::mbar_init(bfull_bar(s), TC_EXP_WARPS);
             dev::mbar_init(empty_bar(s), 1);
+            dev::mbar_init(lfull_bar(s), 1);
+            dev::mbar_init(lempty_bar(s), TC_EXP_WARPS);
         }
         dev::mbar_init(accum_bar, 1);
         dev::fence_barrier_init();
@@ -115,24 +128,34 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        // ------------------------------ producer ------------------------------
+        // ---------------------------- X producer -----------------------------
         if (lane == 0) asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % TC_STAGES;
+            if (i >= TC_STAGES) dev::mbar_wait(empty_bar(s), ((i / TC_STAGES) + 1) & 1);
+            if (lane == 0) {
+                dev::mbar_arrive_expect_tx(full_bar(s), (uint32_t)A_BYTES);
+#pragma unroll
+                for (int t = 0; t < TC_MT; ++t)
+                    tma_load_2d(dev::smem_u32(sA + s * A_BYTES + t * A_TILE), &xmap, i * TC_K, m0 + t * TC_M,
+                                full_bar(s));
+            }
+            __syncwarp();
+        }
+    } else if (warp == 2 + TC_EXP_WARPS) {
+        // ---------------------- codebook + index producer ----------------------
         const int rows = min(TC_N, p.F_out_pad - n0);          // idx rows present (multiple of 64)
         const uint32_t idx_bytes = (uint32_t)rows * 32u;
         const uint32_t cb_u = dev::smem_u32(sC);
         for (int i = 0; i < nk; ++i) {
             const int s = i % TC_STAGES;
-            if (i >= TC_STAGES) dev::mbar_wait(empty_bar(s), ((i / TC_STAGES) + 1) & 1);
+            if (i >= TC_STAGES) dev::mbar_wait(lempty_bar(s), ((i / TC_STAGES) + 1) & 1);
             if (lane == 0) {
-                dev::mbar_arrive_expect_tx(full_bar(s), (uint32_t)A_BYTES + idx_bytes + (uint32_t)CB_BYTES);
-#pragma unroll
-                for (int t = 0; t < TC_MT; ++t)
-                    tma_load_2d(dev::smem_u32(sA + s * A_BYTES + t * A_TILE), &xmap, i * TC_K, m0 + t * TC_M,
-                                full_bar(s));
+                dev::mbar_arrive_expect_tx(lfull_bar(s), idx_bytes + (uint32_t)CB_BYTES);
                 dev::bulk_g2s(dev::smem_u32(sI + s * IDX_BYTES), p.idx + ((size_t)i * p.F_out_pad + n0) * 32,
-                              idx_bytes, full_bar(s));
+                              idx_bytes, lfull_bar(s));
                 dev::bulk_g2s(cb_u + (uint32_t)s * (uint32_t)CB_BYTES, p.cbimg + (size_t)i * CB_BYTES,
-                              (uint32_t)CB_BYTES, full_bar(s));
+                              (uint32_t)CB_BYTES, lfull_bar(s));
             }
             __syncwarp();
         }
@@ -189,7 +212,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
         for (int i = 0; i < nk; ++i) {
             const int s = i % TC_STAGES;
             const uint32_t ph = (i / TC_STAGES) & 1;
-            dev::mbar_wait(full_bar(s), ph);
+            dev::mbar_wait(lfull_bar(s), ph);                                       // codebook + indices
+            if (i >= TC_STAGES) dev::mbar_wait(empty_bar(s), ((i / TC_STAGES) + 1) & 1);   // B slot free
             const uint32_t ia = dev::smem_u32(sI + s * IDX_BYTES) + ib0;
             const uint32_t cbl = cb_u + (uint32_t)s * (uint32_t)CB_BYTES + (uint32_t)lane * 4u;
             const uint32_t bst = dev::smem_u32(sB + s * B_BYTES) + (uint32_t)ew * 32u * 128u;
@@ -209,7 +233,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
             }
             dev::fence_proxy_async();      // generic-proxy STS -> visible to tcgen05 (async proxy)
             __syncwarp();
-            if (lane == 0) dev::mbar_arrive(bfull_bar(s));
+            if (lane == 0) {
+                dev::mbar_arrive(bfull_bar(s));
+                dev::mbar_arrive(lempty_bar(s));
+            }
         }
         // ------------------------------ epilogue -------------------------------
         {
@@ -284,7 +311,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
 }
 
 size_t tc_smem_bytes(int C) {
-    return 1024 + (size_t)TC_STAGES * (TC_MT * TC_M * TC_K * 2 + TC_N * TC_K * 2 + TC_N * 32 + (size_t)C * 128) + 8 * 16 + 16;
+    return 1024 + (size_t)TC_STAGES * (TC_MT * TC_M * TC_K * 2 + TC_N * TC_K * 2 + TC_N * 32 + (size_t)C * 128) +
+           8 * (5 * TC_STAGES + 1) + 16;
 }
 
 }  // namespace
