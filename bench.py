@@ -380,7 +380,12 @@ def oracle_decode_rate(budget_s: float = 15.0):
 # side measurements (not part of the timed region)
 # ----------------------------------------------------------------------------
 def prefill_tflops(M=2048, iters=10):
+    """configs[3]: prefill PQ GEMM on the Llama-3-8B shapes, EXPAND (tcgen05)
+    vs LUT; EXPAND's fraction is against the measured dense bf16 peak (fp16
+    tensor-core rate = bf16 rate, MEASURED_PEAKS.json)."""
     import torch
+    pk, _ = _peaks()
+    dense_peak = float(pk.get("bf16_tflops", 1692.0))
 
     import paper_2605_04084_b200 as F
     import synth
@@ -394,16 +399,31 @@ def prefill_tflops(M=2048, iters=10):
         for name, algo in (("expand_tc", F.GEMM_EXPAND_TC), ("lut", F.GEMM_LUT)):
             try:
                 n_it = iters if algo == F.GEMM_EXPAND_TC else 2
-                F.gemm(L, X, out=Y, algo=algo)
+                F.gemm(L, X, out=Y, algo=algo)   # sizes workspaces outside capture
+                torch.cuda.synchronize()
+                # device time: n_it launches replayed from a CUDA graph (the
+                # ~40 us of Python/ctypes/tensor-map host work per call would
+                # otherwise starve the GPU at these sizes)
+                gs = torch.cuda.Stream()
+                gs.wait_stream(torch.cuda.current_stream())
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.stream(gs):
+                    with torch.cuda.graph(gr, stream=gs):
+                        for _ in range(n_it):
+                            F.gemm(L, X, out=Y, algo=algo)
+                torch.cuda.synchronize()
+                gr.replay()
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                for _ in range(n_it):
-                    F.gemm(L, X, out=Y, algo=algo)
+                gr.replay()
                 e1.record()
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1) / n_it
-                res[name] = {"ms": round(ms, 4), "tflops": round(2.0 * M * fo * fi / ms / 1e9, 2)}
+                tf = 2.0 * M * fo * fi / ms / 1e9
+                res[name] = {"ms": round(ms, 4), "tflops": round(tf, 2)}
+                if algo == F.GEMM_EXPAND_TC:
+                    res[name]["frac_of_dense_peak"] = round(tf / dense_peak, 3)
             except Exception as e:  # report, never hide
                 res[name] = {"error": str(e)[:200]}
         out["%dx%d" % (fo, fi)] = res
@@ -632,10 +652,11 @@ def main():
 
     side = {}
     if rank == 0 and not args.no_side:
-        try:
-            side["prefill_gemm_M2048"] = prefill_tflops()
-        except Exception as e:
-            side["prefill_gemm_M2048"] = {"error": str(e)[:200]}
+        for pm in (512, 2048):   # configs[3]: prefill M = 512 and 2048 tokens
+            try:
+                side["prefill_gemm_M%d" % pm] = prefill_tflops(M=pm)
+            except Exception as e:
+                side["prefill_gemm_M%d" % pm] = {"error": str(e)[:200]}
         try:
             side["decode_sweep"] = decode_sweep(peak)
         except Exception as e:

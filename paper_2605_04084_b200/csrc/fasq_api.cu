@@ -40,6 +40,8 @@ static void destroy(fasq_layer* L) {
     if (L->cb) cudaFree(L->cb);
     if (L->ws) cudaFree(L->ws);
     if (L->tickets) cudaFree(L->tickets);
+    if (L->gws) cudaFree(L->gws);
+    if (L->gtickets) cudaFree(L->gtickets);
     delete L;
 }
 

@@ -61,6 +61,11 @@ struct fasq_layer {
     int64_t ws_bytes = 0;
     unsigned* tickets = nullptr;
     int32_t n_tickets = 0;
+    // GEMM-EXPAND split-K workspace (small M; gemm_tc.cu), same rules
+    float* gws = nullptr;
+    int64_t gws_bytes = 0;
+    unsigned* gtickets = nullptr;
+    int32_t n_gtickets = 0;
 };
 
 namespace fasq {

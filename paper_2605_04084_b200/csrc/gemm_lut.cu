@@ -60,19 +60,26 @@ __global__ void __launch_bounds__(LUT_THREADS, 1) k_gemm_lut(LutParams p) {
         __syncthreads();   // previous group's gathers done
         // build: entry (t, k, sub) = sum_e x[t][sub*d+e] * c[sub][k][e]  (fp32, exact fp16 products)
         const uint32_t* cbg = reinterpret_cast<const uint32_t*>(p.cbimg + (size_t)g * C * 128);
+        // this thread's subspace is fixed (LUT_THREADS is a multiple of 32): its
+        // x slices for the MT tokens are loaded once per group
+        const int sub = tid & 31, ss = g * 32 + sub;
+        uint32_t xv[LUT_MT];
+#pragma unroll
+        for (int t = 0; t < LUT_MT; ++t) {
+            const int m = m0 + t;
+            xv[t] = 0;
+            if (m < p.M && ss < p.N_ss) {
+                const uint16_t* xs = reinterpret_cast<const uint16_t*>(p.X) + (size_t)m * p.F_in + (size_t)ss * p.d;
+                xv[t] = p.d == 2 ? (uint32_t)xs[0] | ((uint32_t)xs[1] << 16) : (uint32_t)xs[0];
+            }
+        }
+#pragma unroll 4
         for (int e = tid; e < C * 32; e += LUT_THREADS) {
-            const int k = e >> 5, sub = e & 31;
+            const int k = e >> 5;
             const uint32_t c = cbg[e];
-            const int ss = g * 32 + sub;
 #pragma unroll
             for (int t = 0; t < LUT_MT; ++t) {
-                const int m = m0 + t;
-                uint32_t xv = 0;
-                if (m < p.M && ss < p.N_ss) {
-                    const uint16_t* xs = reinterpret_cast<const uint16_t*>(p.X) + (size_t)m * p.F_in + (size_t)ss * p.d;
-                    xv = p.d == 2 ? (uint32_t)xs[0] | ((uint32_t)xs[1] << 16) : (uint32_t)xs[0];
-                }
-                const float v = dev::fhfma2(c, xv, 0.f);
+                const float v = dev::fhfma2(c, xv[t], 0.f);
                 reinterpret_cast<float*>(smem)[((t >> 1) * C * 64) + k * 64 + (t & 1) * 32 + sub] = v;
             }
         }

@@ -27,6 +27,8 @@
 //   epilogue      : tcgen05.ld (32x32b) -> fp32/fp16 -> Y (8 warps).
 #include <cuda.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "fasq_internal.cuh"
@@ -47,6 +49,8 @@ struct TcParams {
     const uint8_t* idx;      // [n_groups][F_out_pad/64][32][64] (fasq_internal.cuh)
     const uint8_t* cbimg;    // [n_groups][C][32][4]
     void* Y;
+    float* ws;               // split-K (gridDim.z > 1): fp32 partial tiles [ks][tiles][256 tokens][256 rows]
+    unsigned* tickets;       // [tiles][2] arrive / depart counters (zero between launches)
     int M, F_out, F_out_pad, n_groups, C, y_f32;
 };
 
@@ -97,7 +101,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n0 = blockIdx.x * TC_N;          // weight-row tile
     const int m0 = blockIdx.y * TC_M * TC_MT;  // first token of this CTA's token tiles
-    const int nk = p.n_groups;
+    // split-K (small M: too few tiles for the SMs): this CTA's K chunks [kb, kb + nk)
+    const int ksplit = (int)gridDim.z, kz = (int)blockIdx.z;
+    const int kb = (int)((int64_t)kz * p.n_groups / ksplit);
+    const int nk = (int)((int64_t)(kz + 1) * p.n_groups / ksplit) - kb;
     const uint32_t bar0 = dev::smem_u32(bars);
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto bfull_bar = [&](int s) { return bar0 + 8u * (TC_STAGES + s); };
@@ -137,7 +144,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
                 dev::mbar_arrive_expect_tx(full_bar(s), (uint32_t)A_BYTES);
 #pragma unroll
                 for (int t = 0; t < TC_MT; ++t)
-                    tma_load_2d(dev::smem_u32(sA + s * A_BYTES + t * A_TILE), &xmap, i * TC_K, m0 + t * TC_M,
+                    tma_load_2d(dev::smem_u32(sA + s * A_BYTES + t * A_TILE), &xmap, (kb + i) * TC_K, m0 + t * TC_M,
                                 full_bar(s));
             }
             __syncwarp();
@@ -152,9 +159,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
             if (i >= TC_STAGES) dev::mbar_wait(lempty_bar(s), ((i / TC_STAGES) + 1) & 1);
             if (lane == 0) {
                 dev::mbar_arrive_expect_tx(lfull_bar(s), idx_bytes + (uint32_t)CB_BYTES);
-                dev::bulk_g2s(dev::smem_u32(sI + s * IDX_BYTES), p.idx + ((size_t)i * p.F_out_pad + n0) * 32,
+                dev::bulk_g2s(dev::smem_u32(sI + s * IDX_BYTES), p.idx + ((size_t)(kb + i) * p.F_out_pad + n0) * 32,
                               idx_bytes, lfull_bar(s));
-                dev::bulk_g2s(cb_u + (uint32_t)s * (uint32_t)CB_BYTES, p.cbimg + (size_t)i * CB_BYTES,
+                dev::bulk_g2s(cb_u + (uint32_t)s * (uint32_t)CB_BYTES, p.cbimg + (size_t)(kb + i) * CB_BYTES,
                               (uint32_t)CB_BYTES, lfull_bar(s));
             }
             __syncwarp();
@@ -244,7 +251,44 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int q = warp & 3;                    // TMEM lane quarter this warp may access
             const int t = ew >> 2;                     // accumulator (token tile) this warp drains
-            const int m = m0 + t * TC_M + q * 32 + lane;   // token
+            const int ml = t * TC_M + q * 32 + lane;   // token within the CTA tile
+            const int m = m0 + ml;                     // token
+            const int tile = (int)(blockIdx.y * gridDim.x + blockIdx.x);
+            // 32 consecutive outputs (rows n .. n+31) of token m -> Y (fp32 / fp16)
+            auto store32 = [&](int n, const float* r) {
+                if (m >= p.M || n >= p.F_out) return;
+                const bool full = n + 32 <= p.F_out;
+                if (p.y_f32) {
+                    float* yr = reinterpret_cast<float*>(p.Y) + (size_t)m * p.F_out + n;
+                    if (full && (p.F_out % 4 == 0)) {
+#pragma unroll
+                        for (int v = 0; v < 8; ++v)
+                            reinterpret_cast<float4*>(yr)[v] = make_float4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+                    } else {
+                        for (int v = 0; v < 32; ++v)
+                            if (n + v < p.F_out) yr[v] = r[v];
+                    }
+                } else {
+                    __half* yr = reinterpret_cast<__half*>(p.Y) + (size_t)m * p.F_out + n;
+                    if (full && (p.F_out % 8 == 0)) {
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            __half2 h[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) h[u] = __floats2half2_rn(r[8 * v + 2 * u], r[8 * v + 2 * u + 1]);
+                            uint4 o;
+                            o.x = *reinterpret_cast<uint32_t*>(&h[0]);
+                            o.y = *reinterpret_cast<uint32_t*>(&h[1]);
+                            o.z = *reinterpret_cast<uint32_t*>(&h[2]);
+                            o.w = *reinterpret_cast<uint32_t*>(&h[3]);
+                            reinterpret_cast<uint4*>(yr)[v] = o;
+                        }
+                    } else {
+                        for (int v = 0; v < 32; ++v)
+                            if (n + v < p.F_out) yr[v] = __float2half_rn(r[v]);
+                    }
+                }
+            };
 #pragma unroll 1
             for (int c0 = 0; c0 < TC_N; c0 += 32) {
                 uint32_t r[32];
@@ -260,44 +304,61 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
                       "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
                     : "r"(taddr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                const int n = n0 + c0;
-                if (m < p.M && n < p.F_out) {
-                    const bool full = n + 32 <= p.F_out;
-                    if (p.y_f32) {
-                        float* yr = reinterpret_cast<float*>(p.Y) + (size_t)m * p.F_out + n;
-                        if (full && (p.F_out % 4 == 0)) {
+                float f[32];
 #pragma unroll
-                            for (int v = 0; v < 8; ++v)
-                                reinterpret_cast<float4*>(yr)[v] =
-                                    make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                                __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-                        } else {
+                for (int v = 0; v < 32; ++v) f[v] = __uint_as_float(r[v]);
+                if (ksplit > 1) {
+                    // partial tile -> workspace, merged below in fixed ks order (deterministic)
+                    float* wr = p.ws + (((size_t)kz * gridDim.x * gridDim.y + tile) * (TC_M * TC_MT) + ml) * TC_N + c0;
 #pragma unroll
-                            for (int v = 0; v < 32; ++v)
-                                if (n + v < p.F_out) yr[v] = __uint_as_float(r[v]);
-                        }
-                    } else {
-                        __half* yr = reinterpret_cast<__half*>(p.Y) + (size_t)m * p.F_out + n;
-                        if (full && (p.F_out % 8 == 0)) {
+                    for (int v = 0; v < 8; ++v)
+                        __stcg(reinterpret_cast<float4*>(wr) + v, make_float4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]));
+                } else {
+                    store32(n0 + c0, f);
+                }
+            }
+            if (ksplit > 1) {
+                // all ks CTAs of the tile are co-resident (grid <= #SMs): arrive,
+                // wait for the others, then each sums a 1/ks slice of the tile's
+                // columns over z = 0..ks-1 in fixed order (deterministic).  The
+                // last CTA to leave resets both counters for the next launch.
+                __threadfence();
+                asm volatile("bar.sync 1, %0;" :: "n"(TC_EXP_WARPS * 32) : "memory");
+                unsigned* arrive = p.tickets + 2 * tile;
+                unsigned* depart = arrive + 1;
+                if (ew == 0 && lane == 0) {
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(arrive) : "memory");
+                    unsigned v;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(arrive) : "memory");
+                    } while (v < (unsigned)ksplit);
+                    unsigned old;
+                    asm volatile("atom.add.relaxed.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(depart) : "memory");
+                    if (old == (unsigned)ksplit - 1u) {   // everyone has seen arrive == ks
+                        *arrive = 0u;
+                        *depart = 0u;
+                    }
+                }
+                asm volatile("bar.sync 1, %0;" :: "n"(TC_EXP_WARPS * 32) : "memory");
+                const int cw = TC_N / ksplit;     // ks in {2, 4, 8}: multiples of 32 columns
+#pragma unroll 1
+                for (int c0 = kz * cw; c0 < (kz + 1) * cw; c0 += 32) {
+                    float f[32];
 #pragma unroll
-                            for (int v = 0; v < 4; ++v) {
-                                uint4 o;
-                                __half2 h0 = __floats2half2_rn(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
-                                __half2 h1 = __floats2half2_rn(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
-                                __half2 h2 = __floats2half2_rn(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
-                                __half2 h3 = __floats2half2_rn(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
-                                o.x = *reinterpret_cast<uint32_t*>(&h0);
-                                o.y = *reinterpret_cast<uint32_t*>(&h1);
-                                o.z = *reinterpret_cast<uint32_t*>(&h2);
-                                o.w = *reinterpret_cast<uint32_t*>(&h3);
-                                reinterpret_cast<uint4*>(yr)[v] = o;
-                            }
-                        } else {
+                    for (int v = 0; v < 32; ++v) f[v] = 0.f;
+                    for (int z = 0; z < ksplit; ++z) {
+                        const float4* rd = reinterpret_cast<const float4*>(
+                            p.ws + (((size_t)z * gridDim.x * gridDim.y + tile) * (TC_M * TC_MT) + ml) * TC_N + c0);
 #pragma unroll
-                            for (int v = 0; v < 32; ++v)
-                                if (n + v < p.F_out) yr[v] = __float2half_rn(__uint_as_float(r[v]));
+                        for (int v = 0; v < 8; ++v) {
+                            const float4 w = __ldcg(rd + v);
+                            f[4 * v] += w.x;
+                            f[4 * v + 1] += w.y;
+                            f[4 * v + 2] += w.z;
+                            f[4 * v + 3] += w.w;
                         }
                     }
+                    store32(n0 + c0, f);
                 }
             }
         }
@@ -367,6 +428,56 @@ fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void
     // F_out_pad rows of the idx table exist; tiles past F_out_pad read beyond it
     // -> require the row tile grid to stay within F_out_pad (pad logic below).
     dim3 grid((unsigned)((L->F_out_pad + TC_N - 1) / TC_N), (unsigned)((M + TC_M * TC_MT - 1) / (TC_M * TC_MT)));
+    // small M: fewer tiles than SMs -> split K over gridDim.z (>= 8 chunks
+    // each); partial tiles go through an fp32 workspace and are summed by the
+    // last CTA of each tile in fixed ks order (deterministic)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int tiles = (int)(grid.x * grid.y);
+    int ks = 1;
+    if (const char* e = getenv("FASQ_GEMM_KSPLIT")) ks = atoi(e);
+    else if (tiles < sms) ks = std::min(sms / tiles, L->n_groups / 8);
+    ks = ks >= 8 ? 8 : ks >= 4 ? 4 : ks >= 2 ? 2 : 1;          // the merge splits 256 columns by ks
+    while (ks > 1 && (tiles * ks > sms || ks > L->n_groups)) ks >>= 1;   // co-resident, >= 1 chunk each
+    if (ks > 1) {
+        // per-layer workspace (like the GEMV's): grown outside stream capture
+        static std::mutex mu;
+        std::lock_guard<std::mutex> lk(mu);
+        fasq_layer* Lw = const_cast<fasq_layer*>(L);   // workspace only; the PQ data is immutable
+        const int64_t need = (int64_t)ks * tiles * (TC_M * TC_MT) * TC_N * (int64_t)sizeof(float);
+        if (need > Lw->gws_bytes || 2 * tiles > Lw->n_gtickets) {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            cudaStreamIsCapturing(st, &cs);
+            if (cs != cudaStreamCaptureStatusNone) {
+                set_error("fasq_gemm: split-K workspace must be sized by one uncaptured call with this M first");
+                return FASQ_E_ARG;
+            }
+            FASQ_CUDA_TRY(cudaStreamSynchronize(st));
+            if (need > Lw->gws_bytes) {
+                if (Lw->gws) cudaFree(Lw->gws);
+                Lw->gws = nullptr;
+                Lw->gws_bytes = 0;
+                if (cudaMalloc(&Lw->gws, (size_t)need) != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
+                Lw->gws_bytes = need;
+            }
+            if (2 * tiles > Lw->n_gtickets) {
+                if (Lw->gtickets) cudaFree(Lw->gtickets);
+                Lw->gtickets = nullptr;
+                Lw->n_gtickets = 0;
+                const int nt = std::max(2 * tiles, 128);   // [tiles][arrive, depart]
+                if (cudaMalloc(&Lw->gtickets, (size_t)nt * sizeof(unsigned)) != cudaSuccess) {
+                    cudaGetLastError();
+                    return FASQ_E_OOM;
+                }
+                FASQ_CUDA_TRY(cudaMemset(Lw->gtickets, 0, (size_t)nt * sizeof(unsigned)));
+                Lw->n_gtickets = nt;
+            }
+        }
+        p.ws = Lw->gws;
+        p.tickets = Lw->gtickets;
+        grid.z = (unsigned)ks;
+    }
     k_gemm_tc<<<grid, TC_THREADS, smem, st>>>(map, p);
     FASQ_CUDA_TRY(cudaGetLastError());
     set_launch_count(1);

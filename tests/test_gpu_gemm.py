@@ -85,3 +85,24 @@ def test_gemm_llama_sampled(F, oracle_lib, F_out, F_in):
         ref = oracle_lib.gemm(cb, idx, X[::37], rows=(j0, j0 + 64))
         ok, info = parity_ok(Y[::37, j0:j0 + 64], ref, X[::37], F_in)
         assert ok, (j0, info)
+
+
+@pytest.mark.parametrize("F_out,F_in,M,ks", [(512, 2048, 100, 0), (1000, 2496, 300, 4), (256, 4096, 17, 0)])
+def test_gemm_tc_split_k(F, oracle_lib, monkeypatch, F_out, F_in, M, ks):
+    """Small M -> fewer tiles than SMs -> split-K over gridDim.z with an fp32
+    workspace merged by the last CTA of each tile in fixed order (ks = 0: the
+    library's choice; 4: forced, uneven chunk counts (39 chunks)).  Two calls in a row also
+    check the per-tile ticket reset, and the result must be bit-identical."""
+    if ks:
+        monkeypatch.setenv("FASQ_GEMM_KSPLIT", str(ks))
+    cb, idx = synth.random_layer(F_out, F_in, 2, 256, seed=F_out + M + 7)
+    X = synth.activation(M, F_in, seed=M + 1)
+    L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), F_in, 1)
+    Xd = torch.from_numpy(X).cuda()
+    Y1 = F.gemm(L, Xd, out_dtype=torch.float32, algo=F.GEMM_EXPAND_TC)
+    Y2 = F.gemm(L, Xd, out_dtype=torch.float32, algo=F.GEMM_EXPAND_TC)
+    torch.cuda.synchronize()
+    assert torch.equal(Y1, Y2)
+    ref = oracle_lib.gemm(cb, idx, X)
+    ok, info = parity_ok(Y1.cpu().numpy().astype(np.float64), ref, X, F_in)
+    assert ok, info
