@@ -112,6 +112,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     constexpr int R = RW * NW;
     constexpr int XG = 32 * NB * E;
     constexpr bool PAIR = ChainPair<D>::value;
+    constexpr bool QUAD = PAIR && NB == 1;   // quarter-lane mapping (gemv_core.cuh)
     constexpr int CS = kChainCS;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* s_cb = smem;                                       // PAIR: CS * 64 KiB, else ST * cbb_max
@@ -225,6 +226,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
 
     const int wrow0 = warp * RW;
     const auto co = core::chunk_offsets<RW>(wrow0, lane);
+    const auto qm = core::quarter_map(wrow0, lane);
     int slot = 0;            // ring position of the next stage (running across steps)
     uint32_t par_ring = 0;   // its mbarrier phase parity
     int cslot = 0;           // PAIR: codebook pair slot and parity
@@ -252,12 +254,43 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         if (tr && threadIdx.x == 0 && j == 0) tr[1] = dev::globaltimer();
         asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
         if (tr && threadIdx.x == 0 && j == 0) tr[2] = dev::globaltimer();
+        const bool active = wrow0 < w.rows_valid;
+        if constexpr (QUAD) {
+            // B = 1 on pair stages: quarter-lane mapping (gemv_core.cuh), 16
+            // accumulators per lane, 8-lane row reduction
+            float acc[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc[q] = 0.f;
+            const bool run = active && !(p.dbg & 1);
+            for (int i = 0; i < ng; i += 2) {
+                dev::mbar_wait(cfull0 + 8 * cslot, cpar);
+                const uint32_t lbs = (uint32_t)cslot << 16;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (h == 1 && i + 1 >= ng) break;
+                    dev::mbar_wait(full0 + 8 * slot, par_ring);
+                    if (run)
+                        core::compute_group_pair_q<D>(acc, s_idx + slot * R * 32, qm, s_cb, lbs + ((uint32_t)h << 7),
+                                                      s_x + (i + h) * XG);
+                    __syncwarp();
+                    if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+                    if (++slot == ST) { slot = 0; par_ring ^= 1u; }
+                }
+                if (lane == 0) dev::mbar_arrive(cempty0 + 8 * cslot);
+                if (++cslot == CS) { cslot = 0; cpar ^= 1u; }
+            }
+            core::reduce_quarter(acc, lane);
+            if (active) {
+                const long long off = (long long)par * p.arena_words + w.y_off + w.row0_g;
+                for (int q = 0; q < p.world; ++q)
+                    core::counted_store_q(acc, p.peers[q] + off, w.r0 + wrow0, lane, w.F_out);
+            }
+        } else {
         float acc[RW][NB];
 #pragma unroll
         for (int q = 0; q < RW; ++q)
 #pragma unroll
             for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
-        const bool active = wrow0 < w.rows_valid;
         if constexpr (PAIR) {
             // one iteration per codebook pair slot: groups i (h = 0), i+1 (h = 1)
             const bool run = active && !(p.dbg & 1);
@@ -303,6 +336,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             const long long off = (long long)par * p.arena_words + w.y_off + w.row0_g;
             for (int q = 0; q < p.world; ++q)
                 core::counted_store<NB, RW>(tot, p.peers[q] + off, w.r0 + wrow0, w.F_out, w.F_out_g, p.B);
+        }
         }
         if (tr && lane == 0 && warp == 0) tr[3] = dev::globaltimer();
     }

@@ -271,6 +271,81 @@ __device__ __forceinline__ void compute_group_pair(float (&acc)[RW][NB], const u
     }
 }
 
+// ---- quarter-lane mapping (B = 1, pair stages) ----------------------------
+// The 32-lane reduction of the lane = subspace mapping moves 31 values per row
+// through SHFL (SHFL-bound, ~0.5 us per work item on a full CTA).  Here lane
+// l = 8q + u of a warp owns the 16 rows {8q + t, 32 + 8q + t : t < 8} of the
+// warp's 64 and, in phase p = 0..3, subspace sigma_p = 8*((q + p) & 3) + u of
+// the group.  In every phase the 32 lanes still read 32 DISTINCT subspaces ->
+// 32 distinct banks (one wavefront per warp-gather); each row is covered by
+// the 8 lanes of its quarter x 4 phases; a lane accumulates 16 rows (not 64)
+// and a row total is a reduction over 8 lanes (3 butterfly rounds, 14 SHFL per
+// lane instead of 62), after which lane l holds rows l and 32 + l (contiguous
+// counted stores).  The index bytes of (sigma_p, 8 rows) are 8 B of the
+// existing layout: two LDS.64 per phase, conflict-free over each half-warp
+// (checked exhaustively for the s/2 chunk rotation).
+struct QuarterMap {
+    uint32_t ia[4], ib[4];   // index bytes of rows 8q.. / 32+8q.. per phase inside an index stage
+    uint32_t lb[4];          // PRMT lane constant per phase: 4*sigma_p (byte 0)
+};
+__device__ __forceinline__ QuarterMap quarter_map(int wrow0, int lane) {
+    QuarterMap m;
+    const uint32_t q = (uint32_t)lane >> 3, u = (uint32_t)lane & 7u;
+    const uint32_t hh = q & 1u, c0 = q >> 1, c1 = 2u + (q >> 1);
+#pragma unroll
+    for (int ph = 0; ph < 4; ++ph) {
+        const uint32_t sg = 8u * ((q + (uint32_t)ph) & 3u) + u;
+        const uint32_t seg = (uint32_t)(wrow0 >> 6) * 2048u + sg * 64u + 8u * hh;
+        m.ia[ph] = seg + 16u * ((c0 + (sg >> 1)) & 3u);
+        m.ib[ph] = seg + 16u * ((c1 + (sg >> 1)) & 3u);
+        m.lb[ph] = sg * 4u;
+    }
+    return m;
+}
+
+// One group on a codebook pair stage (half h and slot bits in lbs): register
+// 2*(j & 7) + (j >> 3) accumulates quarter row j (j < 8: row 8q + j, else
+// 32 + 8q + j - 8) over the 4 phases.  x_grp: the group's staged x [32][4 B].
+template <int D>
+__device__ __forceinline__ void compute_group_pair_q(float (&acc)[16], const uint8_t* idx_stage, const QuarterMap& m,
+                                                     const uint8_t* cbs, uint32_t lbs, const uint8_t* x_grp) {
+#pragma unroll
+    for (int ph = 0; ph < 4; ++ph) {
+        const uint32_t xv = lds<uint32_t>(x_grp + m.lb[ph]);
+        const uint2 va = lds<uint2>(idx_stage + m.ia[ph]);
+        const uint2 vb = lds<uint2>(idx_stage + m.ib[ph]);
+        const uint32_t w[4] = {va.x, va.y, vb.x, vb.y};
+        const uint32_t lbv = lbs + m.lb[ph];
+        uint32_t c[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            c[j] = lds<uint32_t>(cbs + dev::prmt(w[j >> 2], lbv, 0x7604u | ((uint32_t)(j & 3) << 4)));
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            float& a = acc[2 * (j & 7) + (j >> 3)];
+            a = (D == 1) ? dev::fhfma1(c[j], xv, a) : dev::fhfma2(c[j], xv, a);
+        }
+    }
+}
+
+// Row totals of a quarter: transposed butterfly over the 8 lanes of the
+// quarter (xor 4, 2, 1; fixed order).  Afterwards v[0], v[1] hold the warp's
+// rows lane and 32 + lane.
+__device__ __forceinline__ void reduce_quarter(float (&v)[16], int lane) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const int msk = 4 >> r;
+        const int half = 8 >> r;
+        const bool up = (lane & msk) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+            const float send = up ? v[i] : v[i + half];
+            const float keep = up ? v[i + half] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, msk);
+        }
+    }
+}
+
 // Transposed butterfly over the 32 lanes: v[i] (i < N, N = 32/16/8) holds
 // this lane's partial of row i; afterwards v[0] holds the total of row
 // (lane >> (5 - log2 N)) (each row on 32/N lanes).  Fixed order.
@@ -374,6 +449,21 @@ __device__ __forceinline__ void counted_store(const RowTotals<NB, RW>& t, unsign
             const unsigned long long add = (1ull << kCntShift) + (unsigned long long)(kCntBias + v);
             asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" :: "l"(y + (size_t)b * ld + row), "l"(add) : "memory");
         }
+    }
+}
+
+// Counted store of the quarter mapping's two row totals (B = 1): rows
+// row0w + lane and row0w + 32 + lane.
+__device__ __forceinline__ void counted_store_q(const float (&v)[16], unsigned long long* y, int row0w, int lane,
+                                                int F_out) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int row = row0w + 32 * i + lane;
+        if (row >= F_out) continue;
+        long long t = __float2ll_rn(v[i] * kAccScale);
+        t = max(-(kCntBias - 1), min(kCntBias - 1, t));
+        const unsigned long long add = (1ull << kCntShift) + (unsigned long long)(kCntBias + t);
+        asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" :: "l"(y + row), "l"(add) : "memory");
     }
 }
 
