@@ -108,11 +108,12 @@ constexpr int kChainCS = kPairSlots;
 template <int D, int NB, int NW, int ST>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     constexpr int E = core::Entry<D>::value;
-    constexpr int RW = core::RowsPerWarp<NB>::value;
+    constexpr bool PAIR = ChainPair<D>::value;
+    // d <= 2: row-set mapping, 64 rows per warp at any B (gemv_core.cuh)
+    constexpr int RW = PAIR ? 64 : core::RowsPerWarp<NB>::value;
     constexpr int R = RW * NW;
     constexpr int XG = 32 * NB * E;
-    constexpr bool PAIR = ChainPair<D>::value;
-    constexpr bool QUAD = PAIR && NB == 1;   // quarter-lane mapping (gemv_core.cuh)
+    constexpr int G = NB <= 2 ? 8 : NB == 4 ? 4 : 2;   // lanes per row set (<= 32 accumulators)
     constexpr int CS = kChainCS;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* s_cb = smem;                                       // PAIR: CS * 64 KiB, else ST * cbb_max
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
 
     const int wrow0 = warp * RW;
     const auto co = core::chunk_offsets<RW>(wrow0, lane);
-    const auto qm = core::quarter_map(wrow0, lane);
+    const auto qm = core::set_map<G>(wrow0, lane);
     int slot = 0;            // ring position of the next stage (running across steps)
     uint32_t par_ring = 0;   // its mbarrier phase parity
     int cslot = 0;           // PAIR: codebook pair slot and parity
@@ -255,12 +256,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
         if (tr && threadIdx.x == 0 && j == 0) tr[2] = dev::globaltimer();
         const bool active = wrow0 < w.rows_valid;
-        if constexpr (QUAD) {
-            // B = 1 on pair stages: quarter-lane mapping (gemv_core.cuh), 16
-            // accumulators per lane, 8-lane row reduction
-            float acc[16];
+        if constexpr (PAIR) {
+            // pair stages: row-set mapping (gemv_core.cuh), 2G*NB accumulators
+            // per lane, G-lane row reduction
+            float acc[2 * G * NB];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) acc[q] = 0.f;
+            for (int q = 0; q < 2 * G * NB; ++q) acc[q] = 0.f;
             const bool run = active && !(p.dbg & 1);
             for (int i = 0; i < ng; i += 2) {
                 dev::mbar_wait(cfull0 + 8 * cslot, cpar);
@@ -270,8 +271,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                     if (h == 1 && i + 1 >= ng) break;
                     dev::mbar_wait(full0 + 8 * slot, par_ring);
                     if (run)
-                        core::compute_group_pair_q<D>(acc, s_idx + slot * R * 32, qm, s_cb, lbs + ((uint32_t)h << 7),
-                                                      s_x + (i + h) * XG);
+                        core::compute_group_set<D, NB, G>(acc, s_idx + slot * R * 32, qm, s_cb,
+                                                          lbs + ((uint32_t)h << 7), s_x + (i + h) * XG);
                     __syncwarp();
                     if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
                     if (++slot == ST) { slot = 0; par_ring ^= 1u; }
@@ -279,11 +280,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                 if (lane == 0) dev::mbar_arrive(cempty0 + 8 * cslot);
                 if (++cslot == CS) { cslot = 0; cpar ^= 1u; }
             }
-            core::reduce_quarter(acc, lane);
+            core::reduce_set<NB, G>(acc, lane);
             if (active) {
                 const long long off = (long long)par * p.arena_words + w.y_off + w.row0_g;
                 for (int q = 0; q < p.world; ++q)
-                    core::counted_store_q(acc, p.peers[q] + off, w.r0 + wrow0, lane, w.F_out);
+                    core::counted_store_set<NB, G>(acc, p.peers[q] + off, w.r0 + wrow0, lane, w.F_out, w.F_out_g,
+                                                   p.B);
             }
         } else {
         float acc[RW][NB];
@@ -468,7 +470,7 @@ fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, 
     if (max_ctas > 0) c->nctas = std::min(c->nctas, (int)max_ctas);
     // same tiling family as the per-launch GEMV default (gemv.cu plan_gemv)
     c->nw = 16;
-    c->rw = NB == 1 ? 64 : NB == 2 ? 32 : NB == 4 ? 16 : 8;   // core::RowsPerWarp
+    c->rw = NB == 1 ? 64 : NB == 2 ? 32 : NB == 4 ? 16 : 8;   // core::RowsPerWarp (d = 4, 8)
     c->st = 3;
     if (const char* e = getenv("FASQ_CHAIN_CFG")) {   // experiments: "nw,st"
         int a = 0, b = 0;
@@ -512,6 +514,7 @@ fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, 
         }
     }
     if (c->ext_F_in == 0) { destroy_chain(c); return FASQ_E_ARG; }   // the chain needs an external input
+    if (c->d <= 2) c->rw = 64;   // pair stages: row-set mapping, 64 rows per warp at any B
     const int E = entry_bytes(c->d);
     const size_t cbb_max = (size_t)c->maxC * 32 * E;
     const bool pair = c->d <= 2;   // ChainPair: codebook pair ring next to the index ring

@@ -271,71 +271,105 @@ __device__ __forceinline__ void compute_group_pair(float (&acc)[RW][NB], const u
     }
 }
 
-// ---- quarter-lane mapping (B = 1, pair stages) ----------------------------
+// ---- row-set mapping (decode chain, pair stages, any B) ---------------------
 // The 32-lane reduction of the lane = subspace mapping moves 31 values per row
-// through SHFL (SHFL-bound, ~0.5 us per work item on a full CTA).  Here lane
-// l = 8q + u of a warp owns the 16 rows {8q + t, 32 + 8q + t : t < 8} of the
-// warp's 64 and, in phase p = 0..3, subspace sigma_p = 8*((q + p) & 3) + u of
-// the group.  In every phase the 32 lanes still read 32 DISTINCT subspaces ->
-// 32 distinct banks (one wavefront per warp-gather); each row is covered by
-// the 8 lanes of its quarter x 4 phases; a lane accumulates 16 rows (not 64)
-// and a row total is a reduction over 8 lanes (3 butterfly rounds, 14 SHFL per
-// lane instead of 62), after which lane l holds rows l and 32 + l (contiguous
-// counted stores).  The index bytes of (sigma_p, 8 rows) are 8 B of the
-// existing layout: two LDS.64 per phase, conflict-free over each half-warp
-// (checked exhaustively for the s/2 chunk rotation).
-struct QuarterMap {
-    uint32_t ia[4], ib[4];   // index bytes of rows 8q.. / 32+8q.. per phase inside an index stage
-    uint32_t lb[4];          // PRMT lane constant per phase: 4*sigma_p (byte 0)
-};
-__device__ __forceinline__ QuarterMap quarter_map(int wrow0, int lane) {
-    QuarterMap m;
-    const uint32_t q = (uint32_t)lane >> 3, u = (uint32_t)lane & 7u;
-    const uint32_t hh = q & 1u, c0 = q >> 1, c1 = 2u + (q >> 1);
-#pragma unroll
-    for (int ph = 0; ph < 4; ++ph) {
-        const uint32_t sg = 8u * ((q + (uint32_t)ph) & 3u) + u;
-        const uint32_t seg = (uint32_t)(wrow0 >> 6) * 2048u + sg * 64u + 8u * hh;
-        m.ia[ph] = seg + 16u * ((c0 + (sg >> 1)) & 3u);
-        m.ib[ph] = seg + 16u * ((c1 + (sg >> 1)) & 3u);
-        m.lb[ph] = sg * 4u;
+// through SHFL (SHFL-bound, ~0.5 us per work item on a full CTA), and at B > 1
+// the 64-accumulator budget shrank the rows per warp (RW = 64/B) and with them
+// the rows per codebook stage.  Here a warp always owns 64 rows, split into
+// K = 32/G row sets: lane l = G*a + u owns the 2G rows {G*a + t, 32 + G*a + t :
+// t < G} and, in phase p = 0..K-1 of every group, subspace
+// sigma_p = G*((a + p) % K) + u.  Every phase is a permutation of the 32
+// subspaces over the 32 lanes -> 32 distinct banks per warp-gather; a lane
+// keeps 2G x B accumulators (G = 8 for B <= 2, 4 for B = 4, 2 for B = 8: <= 32); a row
+// total is a reduction over the G lanes of its set (log2 G butterfly rounds),
+// after which lane l holds rows l and 32 + l for every token (contiguous
+// counted stores).  The index bytes of (sigma_p, G rows) are G bytes of the
+// existing layout (two LDS per phase; G = 8 conflict-free per half-warp, G = 4
+// and 2 at most 2-way -- checked exhaustively for the s/2 chunk rotation).
+template <int G>
+struct SetMap {
+    static constexpr int K = 32 / G;
+    uint32_t blk;   // byte offset of the warp's 64-row block inside an index stage
+    uint32_t a, u;  // row set, lane within the set
+    // phase ph: subspace, and the index-byte offsets of the set's two row runs
+    __device__ __forceinline__ uint32_t sg(int ph) const { return G * ((a + (uint32_t)ph) % K) + u; }
+    __device__ __forceinline__ uint32_t ia(uint32_t s) const {
+        const uint32_t r0 = G * a;
+        return blk + s * 64u + 16u * (((r0 >> 4) + (s >> 1)) & 3u) + (r0 & 15u);
     }
+    __device__ __forceinline__ uint32_t ib(uint32_t s) const {
+        const uint32_t r1 = 32u + G * a;
+        return blk + s * 64u + 16u * (((r1 >> 4) + (s >> 1)) & 3u) + (r1 & 15u);
+    }
+};
+template <int G>
+__device__ __forceinline__ SetMap<G> set_map(int wrow0, int lane) {
+    SetMap<G> m;
+    m.blk = (uint32_t)(wrow0 >> 6) * 2048u;
+    m.a = (uint32_t)lane / G;
+    m.u = (uint32_t)lane % G;
     return m;
 }
 
-// One group on a codebook pair stage (half h and slot bits in lbs): register
-// 2*(j & 7) + (j >> 3) accumulates quarter row j (j < 8: row 8q + j, else
-// 32 + 8q + j - 8) over the 4 phases.  x_grp: the group's staged x [32][4 B].
-template <int D>
-__device__ __forceinline__ void compute_group_pair_q(float (&acc)[16], const uint8_t* idx_stage, const QuarterMap& m,
-                                                     const uint8_t* cbs, uint32_t lbs, const uint8_t* x_grp) {
+// One group on a codebook pair stage (half h and slot bits in lbs).  Value
+// (row t of the set, token b) accumulates in register (2*(t % G) + t / G)*NB + b
+// (t < G: row G*a + t, else 32 + G*a + t - G).  x_grp: the group's staged x
+// [32 subspaces][NB][4 B].
+template <int D, int NB, int G>
+__device__ __forceinline__ void compute_group_set(float (&acc)[2 * G * NB], const uint8_t* idx_stage,
+                                                  const SetMap<G>& m, const uint8_t* cbs, uint32_t lbs,
+                                                  const uint8_t* x_grp) {
+    constexpr int K = 32 / G;
 #pragma unroll
-    for (int ph = 0; ph < 4; ++ph) {
-        const uint32_t xv = lds<uint32_t>(x_grp + m.lb[ph]);
-        const uint2 va = lds<uint2>(idx_stage + m.ia[ph]);
-        const uint2 vb = lds<uint2>(idx_stage + m.ib[ph]);
-        const uint32_t w[4] = {va.x, va.y, vb.x, vb.y};
-        const uint32_t lbv = lbs + m.lb[ph];
-        uint32_t c[16];
+    for (int ph = 0; ph < K; ++ph) {
+        const uint32_t sg = m.sg(ph);
+        uint32_t xv[NB];
+        const uint8_t* xa = x_grp + sg * 4u * NB;
+        if (NB == 1) {
+            xv[0] = lds<uint32_t>(xa);
+        } else if (NB == 2) {
+            const uint2 t = lds<uint2>(xa);
+            xv[0] = t.x; xv[1 % NB] = t.y;
+        } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            c[j] = lds<uint32_t>(cbs + dev::prmt(w[j >> 2], lbv, 0x7604u | ((uint32_t)(j & 3) << 4)));
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            float& a = acc[2 * (j & 7) + (j >> 3)];
-            a = (D == 1) ? dev::fhfma1(c[j], xv, a) : dev::fhfma2(c[j], xv, a);
+            for (int b = 0; b < NB; b += 4) {
+                const uint4 t = lds<uint4>(xa + 4 * b);
+                xv[b] = t.x; xv[(b + 1) % NB] = t.y; xv[(b + 2) % NB] = t.z; xv[(b + 3) % NB] = t.w;
+            }
         }
+        constexpr int NWD = G >= 4 ? G / 2 : 1;   // index words: rows t < G in the first G/4 (or half) words
+        uint32_t w[NWD];
+        if (G == 8) {
+            const uint2 va = lds<uint2>(idx_stage + m.ia(sg));
+            const uint2 vb = lds<uint2>(idx_stage + m.ib(sg));
+            w[0] = va.x; w[1 % NWD] = va.y; w[2 % NWD] = vb.x; w[3 % NWD] = vb.y;
+        } else if (G == 4) {
+            w[0] = lds<uint32_t>(idx_stage + m.ia(sg));
+            w[1 % NWD] = lds<uint32_t>(idx_stage + m.ib(sg));
+        } else {   // G = 2: two 16-bit halves in one word
+            w[0] = (uint32_t)lds<uint16_t>(idx_stage + m.ia(sg)) | ((uint32_t)lds<uint16_t>(idx_stage + m.ib(sg)) << 16);
+        }
+        const uint32_t lbv = lbs + sg * 4u;
+        uint32_t c[2 * G];
+#pragma unroll
+        for (int t = 0; t < 2 * G; ++t)
+            c[t] = lds<uint32_t>(cbs + dev::prmt(w[t >> 2], lbv, 0x7604u | ((uint32_t)(t & 3) << 4)));
+#pragma unroll
+        for (int t = 0; t < 2 * G; ++t)
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                float& r = acc[(2 * (t % G) + t / G) * NB + b];
+                r = (D == 1) ? dev::fhfma1(c[t], xv[b], r) : dev::fhfma2(c[t], xv[b], r);
+            }
     }
 }
 
-// Row totals of a quarter: transposed butterfly over the 8 lanes of the
-// quarter (xor 4, 2, 1; fixed order).  Afterwards v[0], v[1] hold the warp's
-// rows lane and 32 + lane.
-__device__ __forceinline__ void reduce_quarter(float (&v)[16], int lane) {
+// Row totals of a set: transposed butterfly over its G lanes (xor G/2 .. 1,
+// fixed order).  Afterwards v[h*NB + b] = row (lane + 32h) of the warp, token b.
+template <int NB, int G>
+__device__ __forceinline__ void reduce_set(float (&v)[2 * G * NB], int lane) {
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-        const int msk = 4 >> r;
-        const int half = 8 >> r;
+    for (int msk = G / 2, half = G * NB; msk >= 1; msk >>= 1, half >>= 1) {
         const bool up = (lane & msk) != 0;
 #pragma unroll
         for (int i = 0; i < half; ++i) {
@@ -452,18 +486,23 @@ __device__ __forceinline__ void counted_store(const RowTotals<NB, RW>& t, unsign
     }
 }
 
-// Counted store of the quarter mapping's two row totals (B = 1): rows
-// row0w + lane and row0w + 32 + lane.
-__device__ __forceinline__ void counted_store_q(const float (&v)[16], unsigned long long* y, int row0w, int lane,
-                                                int F_out) {
+// Counted stores of the row-set mapping's totals: rows row0w + lane and
+// row0w + 32 + lane of every token b < B (word b*ld + row).
+template <int NB, int G>
+__device__ __forceinline__ void counted_store_set(const float (&v)[2 * G * NB], unsigned long long* y, int row0w,
+                                                  int lane, int F_out, int ld, int B) {
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const int row = row0w + 32 * i + lane;
+    for (int h = 0; h < 2; ++h) {
+        const int row = row0w + 32 * h + lane;
         if (row >= F_out) continue;
-        long long t = __float2ll_rn(v[i] * kAccScale);
-        t = max(-(kCntBias - 1), min(kCntBias - 1, t));
-        const unsigned long long add = (1ull << kCntShift) + (unsigned long long)(kCntBias + t);
-        asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" :: "l"(y + row), "l"(add) : "memory");
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            if (b >= B) continue;
+            long long t = __float2ll_rn(v[h * NB + b] * kAccScale);
+            t = max(-(kCntBias - 1), min(kCntBias - 1, t));
+            const unsigned long long add = (1ull << kCntShift) + (unsigned long long)(kCntBias + t);
+            asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" :: "l"(y + (size_t)b * ld + row), "l"(add) : "memory");
+        }
     }
 }
 
