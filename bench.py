@@ -435,6 +435,54 @@ KINDS = (("qkv", ("q_proj", "k_proj", "v_proj")), ("o", ("o_proj",)), ("gate_up"
          ("down", ("down_proj",)))
 
 
+def decode_batch(peak, batches=(2, 4, 8), runs=20):
+    """decode batch B in {2, 4, 8} at (2,256) through the
+    chain kernel (one step = B tokens through the 224 layers).  Bytes per step
+    = indices + codebooks + B x (x + y accumulator words)."""
+    import torch
+
+    import paper_2605_04084_b200 as F
+    import synth
+
+    nb = synth.LLAMA3_8B_BLOCKS
+    blocks = []
+    for b in range(nb):
+        Ls = {}
+        for li, (name, fo, fi) in enumerate(synth.LLAMA3_8B_LAYERS):
+            cb, idx = synth.torch_random_layer(fo, fi, D, C, seed=9000 + b * 7 + li)
+            Ls[name] = F.import_layer(cb, idx, fi)
+            del cb, idx
+        blocks.append(Ls)
+    out = {}
+    for B in batches:
+        steps = []
+        for b in range(nb):
+            for (_, names) in KINDS:
+                steps.append(([blocks[b][n] for n in names], None if not steps else (len(steps) - 1, 0)))
+        ch = F.Chain(steps, B=B)
+        x = synth.torch_activation(B, 4096)
+        for _ in range(3):
+            ch.run(x)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(runs):
+            ch.run(x)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / runs
+        bts = nb * sum(fo * fi // D + (fi // D) * C * D * 2 + B * (2 * fi + 8 * fo)
+                       for (_, fo, fi) in synth.LLAMA3_8B_LAYERS)
+        out["B%d" % B] = {"ms_per_step": round(ms, 4), "tok_s": round(B * 1e3 / ms, 1),
+                          "GBps": round(bts / (ms * 1e-3) / 1e9, 1), "frac": round(bts / (ms * 1e-3) / 1e9 / peak, 3)}
+        del ch
+    for Ls in blocks:
+        for L in Ls.values():
+            L.free()
+    torch.cuda.synchronize()
+    return out
+
+
 def decode_sweep(peak, settings=((2, 256), (2, 128), (4, 256), (1, 256), (2, 64), (8, 256)), runs=30):
     """configs[1]/[2]: the whole-model decode token through the chain kernel at
     each (d, C) of the sweep (effective 4-bit (2,256), 3-bit (2,128), ...),
@@ -661,6 +709,10 @@ def main():
             side["decode_sweep"] = decode_sweep(peak)
         except Exception as e:
             side["decode_sweep"] = {"error": str(e)[:200]}
+        try:
+            side["decode_batch"] = decode_batch(peak)
+        except Exception as e:
+            side["decode_batch"] = {"error": str(e)[:200]}
         try:
             side["gpu_pack"] = pack_time()
         except Exception as e:

@@ -79,7 +79,14 @@ struct GemvParams {
 template <int D, int NB, int NW, int ST>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
     constexpr int E = core::Entry<D>::value;
+    // d <= 2, B = 1: row-set mapping (gemv_core.cuh, G = 8 lanes per row set).
+    // B > 1 keeps lane = subspace with 64/B rows per warp here: a per-launch
+    // GEMV is dominated by per-CTA fixed costs and wants the finer row tiles
+    // (measured: the row-set mapping's 1024-row tiles were 15-30 % slower at
+    // B = 2..8 per launch; the decode chain uses row sets at every B).
+    constexpr bool PAIR_ = D <= 2 && NB == 1;
     constexpr int RW = core::RowsPerWarp<NB>::value;   // rows per consumer warp
+    constexpr int G = 8;
     constexpr int R = RW * NW;                         // rows per CTA tile
     constexpr int XG = 32 * NB * E;                    // x bytes per staged group
     constexpr bool PAIR = D <= 2;                      // codebook PAIR ring (gemv_core.cuh)
@@ -189,33 +196,41 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
         asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
     }
 
-    float acc[RW][NB];
+    float acc[PAIR_ ? 1 : RW][NB];        // lane = subspace mapping (d = 4, 8)
+    float accs[PAIR_ ? 2 * G * NB : 1];   // row-set mapping (d <= 2)
 #pragma unroll
-    for (int q = 0; q < RW; ++q)
+    for (int q = 0; q < (PAIR_ ? 1 : RW); ++q)
 #pragma unroll
         for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
+#pragma unroll
+    for (int q = 0; q < (PAIR_ ? 2 * G * NB : 1); ++q) accs[q] = 0.f;
 
     const int wrow0 = warp * RW;
     const bool active = wrow0 < rows_valid;          // rows_valid is a multiple of 64 >= RW
     const auto co = core::chunk_offsets<RW>(wrow0, lane);
+    const auto sm = core::set_map<G>(wrow0, lane);
     int slot = 0;
     uint32_t par = 0;
     if constexpr (PAIR) {
         int cslot = 0;
         uint32_t cpar = 0;
-        const uint32_t lb = (uint32_t)lane * 4u;
         for (int i = 0; i < ng; i += 2) {
             dev::mbar_wait(cfull0 + 8 * cslot, cpar);
-            const uint32_t lbs = lb + ((uint32_t)cslot << 16);
+            const uint32_t lbs = (uint32_t)cslot << 16;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 if (h == 1 && i + 1 >= ng) break;
                 dev::mbar_wait(full0 + 8 * slot, par);
                 if (active) {
-                    uint32_t xv[NB][E / 4];
-                    core::load_x<D, NB>(xv, s_x + (i + h) * XG, lane);
-                    core::compute_group_pair<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb,
-                                                        lbs + ((uint32_t)h << 7), xv);
+                    if constexpr (PAIR_) {
+                        core::compute_group_set<D, NB, G>(accs, s_idx + slot * R * 32, sm, s_cb,
+                                                          lbs + ((uint32_t)h << 7), s_x + (i + h) * XG);
+                    } else {
+                        uint32_t xv[NB][E / 4];
+                        core::load_x<D, NB>(xv, s_x + (i + h) * XG, lane);
+                        core::compute_group_pair<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb,
+                                                            (uint32_t)lane * 4u + lbs + ((uint32_t)h << 7), xv);
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
@@ -245,7 +260,18 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
         for (long long i = zb + threadIdx.x; i < ze; i += NW * 32) p.zero_ptr[i] = 0ull;
     }
     core::RowTotals<NB, RW> tot;
-    core::reduce_rows<NB, RW>(acc, tot, lane);
+    if constexpr (PAIR_) {
+        // row sets: lane holds rows lane and 32 + lane of the warp (RowTotals of RW = 64)
+        core::reduce_set<NB, G>(accs, lane);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int b = 0; b < NB; ++b) tot.v[h][b] = accs[h * NB + b];
+        tot.rsel = lane;
+        tot.own = true;
+    } else {
+        core::reduce_rows<NB, RW>(acc, tot, lane);
+    }
     constexpr int H = core::RowTotals<NB, RW>::H;
     if (p.y_acc) {
         if (active)
