@@ -29,6 +29,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "fasq_internal.cuh"
@@ -112,8 +113,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     // d <= 2: row-set mapping, 64 rows per warp at any B (gemv_core.cuh)
     constexpr int RW = PAIR ? 64 : core::RowsPerWarp<NB>::value;
     constexpr int R = RW * NW;
-    constexpr int XG = 32 * NB * E;
     constexpr int G = NB <= 2 ? 8 : NB == 4 ? 4 : 2;   // lanes per row set (<= 32 accumulators)
+    constexpr bool XF = PAIR && NB == 8;               // x staged as fp32 (FFMA2 path, compute_group_set)
+    constexpr int XG = XF ? 32 * NB * D * 4 : 32 * NB * E;
     constexpr int CS = kChainCS;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* s_cb = smem;                                       // PAIR: CS * 64 KiB, else ST * cbb_max
@@ -249,9 +251,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
         const int ng = w.g_end - w.g_begin;
         if (phs.x_off >= 0)   // dataflow wait: poll this CTA's input words until final
-            core::stage_x_counted<D, NB, NW>(s_x, cur + phs.x_off, phs.x_ks, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
+            core::stage_x_counted<D, NB, NW, XF>(s_x, cur + phs.x_off, phs.x_ks, phs.F_in, p.B, w.N_ss, w.g_begin,
+                                                 ng);
         else
-            core::stage_x<D, NB, NW>(s_x, p.x_ext, 0, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
+            core::stage_x<D, NB, NW, XF>(s_x, p.x_ext, 0, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
         if (tr && threadIdx.x == 0 && j == 0) tr[1] = dev::globaltimer();
         asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
         if (tr && threadIdx.x == 0 && j == 0) tr[2] = dev::globaltimer();
@@ -364,7 +367,11 @@ fasq_status launch_chain_t(const ChainParams& p, size_t smem, int grid, cudaStre
     static size_t lim = 0;
     static std::once_flag once;
     std::call_once(once, [&] { lim = set_max_dyn_smem(kern); });
-    if (lim < smem) { set_error("chain: dynamic SMEM plan exceeds the device limit"); return FASQ_E_UNSUPPORTED; }
+    if (lim < smem) {
+        set_error("chain: dynamic SMEM plan (" + std::to_string(smem) + " B) exceeds the device limit (" +
+                  std::to_string(lim) + " B)");
+        return FASQ_E_UNSUPPORTED;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid, 1, 1);
     cfg.blockDim = dim3((NW + 1) * 32, 1, 1);
@@ -519,7 +526,8 @@ fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, 
     const size_t cbb_max = (size_t)c->maxC * 32 * E;
     const bool pair = c->d <= 2;   // ChainPair: codebook pair ring next to the index ring
     auto cbring = [&](int st) { return pair ? (size_t)kChainCS * kPairSlot : (size_t)st * cbb_max; };
-    auto ring = [&](int st, int nw) { return cbring(st) + (size_t)st * c->rw * nw * 32 + 2 * 1024; };
+    // (x staging is added after the work plan, smem_of below)
+    auto ring = [&](int st, int nw) { return cbring(st) + (size_t)st * c->rw * nw * 32; };
     while (c->st > 2 && ring(c->st, c->nw) > kChainSmem) --c->st;
     if (ring(c->st, c->nw) > kChainSmem && c->nw > 8) c->nw = 8;
     while (c->st > 1 && ring(c->st, c->nw) > kChainSmem) --c->st;
@@ -601,7 +609,7 @@ fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, 
     for (int s = 0; s < n_steps; ++s)
         for (size_t q = 0; q < per_step[s].size(); ++q)
             items[((size_t)s * c->nctas + q % c->nctas) * c->mi + q / c->nctas] = per_step[s][q];
-    const size_t xg = (size_t)32 * NB * E;
+    const size_t xg = (pair && NB == 8) ? (size_t)32 * NB * c->d * 4 : (size_t)32 * NB * E;   // k_chain XG
     auto smem_of = [&](int st) {
         return cbring(st) + (size_t)st * c->R * 32 + (size_t)c->gmax * xg + 16 * (st + kChainCS);
     };

@@ -101,7 +101,7 @@ inline size_t set_max_dyn_smem(K kern) {
     return lim;
 }
 constexpr size_t kSmemBudget = 227 * 1024 - 2048;   // dynamic-SMEM planning budget (static SMEM headroom)
-constexpr size_t kSmemMax = 227 * 1024 - 256;       // opt-in maximum minus a few bytes of static SMEM
+constexpr size_t kSmemMax = 226 * 1024 - 64;        // opt-in maximum (227 KiB) minus the 1 KiB the kernels report as static SMEM
 // codebook PAIR ring (d <= 2): slots of [<= 256][2][32] words, 64 KiB stride so
 // that the slot is byte 2 of the gather's PRMT constant
 constexpr int kPairSlots = 2;
@@ -185,6 +185,16 @@ __device__ __forceinline__ float fhfma2(uint32_t c, uint32_t x, float acc) {
         "fma.rn.f32.f16 %0, b, f, %0;}"
         : "+f"(acc) : "r"(c), "r"(x));
     return acc;
+}
+// (a0, a1) += c * (x0, x1): fma.rn.f32x2 with a scalar broadcast (SASS FFMA2).
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float c, float x0, float x1) {
+    asm("{.reg .b64 a, b, d;\n\t"
+        "mov.b64 a, {%2, %2};\n\t"
+        "mov.b64 b, {%3, %4};\n\t"
+        "mov.b64 d, {%0, %1};\n\t"
+        "fma.rn.f32x2 d, a, b, d;\n\t"
+        "mov.b64 {%0, %1}, d;}"
+        : "+f"(a0), "+f"(a1) : "f"(c), "f"(x0), "f"(x1));
 }
 __device__ __forceinline__ float fhfma1(uint32_t c, uint32_t x, float acc) {
     asm("{.reg .f16 a, b, e, f;\n\t"

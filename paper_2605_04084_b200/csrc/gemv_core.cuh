@@ -40,7 +40,21 @@ struct Entry {
 
 // x staging for a K-range of ng groups: [gl][32 subspaces][NB][E] bytes.
 // x is fp16 [B][F_in] or (x_acc) FASQ_ACC_I64 [B][F_in] rounded to fp16 here.
-template <int D, int NB, int NW>
+// XF (row-set FFMA2 path, B = 8): instead store x as fp32
+// [gl][e < D][NB/4][32 subspaces][4 tokens] (the fp16 values converted
+// exactly): one LDS.128 per (e, 4 tokens) and the 32 lanes' subspaces are
+// consecutive 16-B blocks -> conflict-free.  See compute_group_set.
+template <int D, int NB>
+__device__ __forceinline__ void store_x_f32(uint8_t* s_x, int t, const uint32_t (&w)[4]) {
+    const int b = t % NB, e32 = (t / NB) & 31, gl = t / (NB * 32);
+    float* g = reinterpret_cast<float*>(s_x) + (size_t)gl * 32 * D * NB;
+#pragma unroll
+    for (int e = 0; e < D; ++e)
+        g[((e * (NB / 4) + b / 4) * 32 + e32) * 4 + (b & 3)] =
+            __half2float(__ushort_as_half((unsigned short)(w[e >> 1] >> (16 * (e & 1)))));
+}
+
+template <int D, int NB, int NW, bool XF = false>
 __device__ __forceinline__ void stage_x(uint8_t* s_x, const __half* x, int x_acc, int F_in, int B, int N_ss,
                                         int g_begin, int ng) {
     constexpr int E = Entry<D>::value;
@@ -96,6 +110,10 @@ __device__ __forceinline__ void stage_x(uint8_t* s_x, const __half* x, int x_acc
         for (int u = 0; u < XPT; ++u) {
             const int t = t0 + u * NW * 32;
             if (t >= n_ent) continue;
+            if (XF) {
+                store_x_f32<D, NB>(s_x, t, w[u]);
+                continue;
+            }
             uint32_t* dst = reinterpret_cast<uint32_t*>(s_x + (size_t)t * E);
 #pragma unroll
             for (int q = 0; q < E / 4; ++q) dst[q] = w[u][q];
@@ -320,6 +338,56 @@ __device__ __forceinline__ void compute_group_set(float (&acc)[2 * G * NB], cons
                                                   const SetMap<G>& m, const uint8_t* cbs, uint32_t lbs,
                                                   const uint8_t* x_grp) {
     constexpr int K = 32 / G;
+    if constexpr (NB == 8) {
+        // B = 8: x staged as fp32 (store_x_f32 layout); each centroid half is converted
+        // once (HADD2.F32) and FFMA2 (fma.rn.f32x2, scalar broadcast) updates
+        // two tokens per instruction -- the same exact products and fp32 sums
+        // in the same order as the FHFMA path, half the FMA instructions
+        // (measured: 3.49 -> 3.39 ms per B = 8 step; at B = 4 the FHFMA path
+        // is faster, 1.85 vs 2.09 ms).
+#pragma unroll
+        for (int ph = 0; ph < K; ++ph) {
+            const uint32_t sg = m.sg(ph);
+            float xf[D][NB];
+            const float4* xa = reinterpret_cast<const float4*>(x_grp) + sg;
+#pragma unroll
+            for (int e = 0; e < D; ++e)
+#pragma unroll
+                for (int b = 0; b < NB; b += 4) {
+                    const float4 t = *(xa + (e * (NB / 4) + b / 4) * 32);
+                    xf[e][b] = t.x; xf[e][b + 1] = t.y; xf[e][b + 2] = t.z; xf[e][b + 3] = t.w;
+                }
+            constexpr int NWD = G >= 4 ? G / 2 : 1;
+            uint32_t w[NWD];
+            if (G == 8) {
+                const uint2 va = lds<uint2>(idx_stage + m.ia(sg));
+                const uint2 vb = lds<uint2>(idx_stage + m.ib(sg));
+                w[0] = va.x; w[1 % NWD] = va.y; w[2 % NWD] = vb.x; w[3 % NWD] = vb.y;
+            } else if (G == 4) {
+                w[0] = lds<uint32_t>(idx_stage + m.ia(sg));
+                w[1 % NWD] = lds<uint32_t>(idx_stage + m.ib(sg));
+            } else {
+                w[0] = (uint32_t)lds<uint16_t>(idx_stage + m.ia(sg)) |
+                       ((uint32_t)lds<uint16_t>(idx_stage + m.ib(sg)) << 16);
+            }
+            const uint32_t lbv = lbs + sg * 4u;
+            uint32_t c[2 * G];
+#pragma unroll
+            for (int t = 0; t < 2 * G; ++t)
+                c[t] = lds<uint32_t>(cbs + dev::prmt(w[t >> 2], lbv, 0x7604u | ((uint32_t)(t & 3) << 4)));
+#pragma unroll
+            for (int t = 0; t < 2 * G; ++t) {
+                const int base = (2 * (t % G) + t / G) * NB;
+#pragma unroll
+                for (int e = 0; e < D; ++e) {
+                    const float ce = __half2float(__ushort_as_half((unsigned short)(c[t] >> (16 * e))));
+#pragma unroll
+                    for (int b = 0; b < NB; b += 2) dev::ffma2(acc[base + b], acc[base + b + 1], ce, xf[e][b], xf[e][b + 1]);
+                }
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int ph = 0; ph < K; ++ph) {
         const uint32_t sg = m.sg(ph);
@@ -510,7 +578,7 @@ __device__ __forceinline__ void counted_store_set(const float (&v)[2 * G * NB], 
 // CTAs of the previous step: every thread polls its words until all carry
 // count == ks (one L2 round trip once they are final), then rounds the value
 // to fp16.  Layout of s_x as stage_x.
-template <int D, int NB, int NW>
+template <int D, int NB, int NW, bool XF = false>
 __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned long long* x, int ks, int F_in, int B,
                                                 int N_ss, int g_begin, int ng) {
     constexpr int E = Entry<D>::value;
@@ -569,6 +637,10 @@ __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned lon
                     const uint32_t h = __half_as_ushort(__double2half((double)val * kAccInv));
                     w[e >> 1] |= h << (16 * (e & 1));
                 }
+            }
+            if (XF) {
+                store_x_f32<D, NB>(s_x, t, w);
+                continue;
             }
             uint32_t* dst = reinterpret_cast<uint32_t*>(s_x + (size_t)t * E);
 #pragma unroll
