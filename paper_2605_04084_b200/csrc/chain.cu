@@ -252,7 +252,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         const int ng = w.g_end - w.g_begin;
         if (phs.x_off >= 0)   // dataflow wait: poll this CTA's input words until final
             core::stage_x_counted<D, NB, NW, XF>(s_x, cur + phs.x_off, phs.x_ks, phs.F_in, p.B, w.N_ss, w.g_begin,
-                                                 ng);
+                                                 ng, p.world > 1);
         else
             core::stage_x<D, NB, NW, XF>(s_x, p.x_ext, 0, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
         if (tr && threadIdx.x == 0 && j == 0) tr[1] = dev::globaltimer();
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                 const long long off = (long long)par * p.arena_words + w.y_off + w.row0_g;
                 for (int q = 0; q < p.world; ++q)
                     core::counted_store_set<NB, G>(acc, p.peers[q] + off, w.r0 + wrow0, lane, w.F_out, w.F_out_g,
-                                                   p.B);
+                                                   p.B, p.world > 1);
             }
         } else {
         float acc[RW][NB];

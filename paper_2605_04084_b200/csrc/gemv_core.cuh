@@ -558,7 +558,7 @@ __device__ __forceinline__ void counted_store(const RowTotals<NB, RW>& t, unsign
 // row0w + 32 + lane of every token b < B (word b*ld + row).
 template <int NB, int G>
 __device__ __forceinline__ void counted_store_set(const float (&v)[2 * G * NB], unsigned long long* y, int row0w,
-                                                  int lane, int F_out, int ld, int B) {
+                                                  int lane, int F_out, int ld, int B, bool sys) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int row = row0w + 32 * h + lane;
@@ -569,7 +569,10 @@ __device__ __forceinline__ void counted_store_set(const float (&v)[2 * G * NB], 
             long long t = __float2ll_rn(v[h * NB + b] * kAccScale);
             t = max(-(kCntBias - 1), min(kCntBias - 1, t));
             const unsigned long long add = (1ull << kCntShift) + (unsigned long long)(kCntBias + t);
-            asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" :: "l"(y + (size_t)b * ld + row), "l"(add) : "memory");
+            if (sys)   // peer GPU arenas (tensor parallel): system scope
+                asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" :: "l"(y + (size_t)b * ld + row), "l"(add) : "memory");
+            else
+                asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(y + (size_t)b * ld + row), "l"(add) : "memory");
         }
     }
 }
@@ -580,7 +583,7 @@ __device__ __forceinline__ void counted_store_set(const float (&v)[2 * G * NB], 
 // to fp16.  Layout of s_x as stage_x.
 template <int D, int NB, int NW, bool XF = false>
 __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned long long* x, int ks, int F_in, int B,
-                                                int N_ss, int g_begin, int ng) {
+                                                int N_ss, int g_begin, int ng, bool sys = true) {
     constexpr int E = Entry<D>::value;
     const int tid = threadIdx.x;
     const int n_ent = ng * 32 * NB;
@@ -616,7 +619,10 @@ __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned lon
 #pragma unroll
                 for (int e = 0; e < D; ++e) {
                     if ((v[u][e] >> kCntShift) == want) continue;
-                    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v[u][e]) : "l"(src + e) : "memory");
+                    if (sys)
+                        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v[u][e]) : "l"(src + e) : "memory");
+                    else
+                        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v[u][e]) : "l"(src + e) : "memory");
                 }
             }
 #pragma unroll
