@@ -84,6 +84,10 @@ def main():
             "comp_max": (st[have, 3] - st[have, 2]).max(),
             "active": int(have.sum()) * 1000,
             "tail": end - np.median(st[:, 3]),
+            # staging latency of CTAs whose inputs were already final when they
+            # started polling (t0 after the previous step's end): ~ one poll round trip
+            "stage_min": (st[have, 1] - st[have, 0]).min(),
+            "stage_med": np.median(st[have, 1] - st[have, 0]),
         }
         rows[KINDS[s % 4]].append(rec)
         prev_end = end
