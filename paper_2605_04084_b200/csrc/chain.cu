@@ -90,6 +90,7 @@ struct ChainParams {
     int n_steps, nctas, B, gmax, cbb_max;
     int mi;                     // work items per (step, CTA): [n_steps][nctas][mi]
     int pf;                     // producer: L2-prefetch this many groups of the next step's item
+    int backoff;                // ns slept between input polls (FASQ_CHAIN_BACKOFF, default 0)
     int dbg;                    // experiments only (FASQ_CHAIN_DBG): bit 0 = consumers skip the gather
                                 // loop, bit 1 = producer skips the copies (compute on stale SMEM),
                                 // bit 2 = producer skips the codebook copies only
@@ -252,7 +253,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         const int ng = w.g_end - w.g_begin;
         if (phs.x_off >= 0)   // dataflow wait: poll this CTA's input words until final
             core::stage_x_counted<D, NB, NW, XF>(s_x, cur + phs.x_off, phs.x_ks, phs.F_in, p.B, w.N_ss, w.g_begin,
-                                                 ng, p.world > 1);
+                                                 ng, p.world > 1, p.backoff);
         else
             core::stage_x<D, NB, NW, XF>(s_x, p.x_ext, 0, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
         if (tr && threadIdx.x == 0 && j == 0) tr[1] = dev::globaltimer();
@@ -698,6 +699,8 @@ fasq_status fasq_chain_run(fasq_chain* c, const void* x_dev, void* stream) {
     if (const char* e = getenv("FASQ_CHAIN_PF")) p.pf = atoi(e);
     p.dbg = 0;
     if (const char* e = getenv("FASQ_CHAIN_DBG")) p.dbg = atoi(e);
+    p.backoff = 0;
+    if (const char* e = getenv("FASQ_CHAIN_BACKOFF")) p.backoff = atoi(e);
     p.n_steps = c->n_steps;
     p.nctas = c->nctas;
     p.B = c->B;

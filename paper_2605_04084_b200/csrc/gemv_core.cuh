@@ -583,7 +583,7 @@ __device__ __forceinline__ void counted_store_set(const float (&v)[2 * G * NB], 
 // to fp16.  Layout of s_x as stage_x.
 template <int D, int NB, int NW, bool XF = false>
 __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned long long* x, int ks, int F_in, int B,
-                                                int N_ss, int g_begin, int ng, bool sys = true) {
+                                                int N_ss, int g_begin, int ng, bool sys = true, int backoff = 0) {
     constexpr int E = Entry<D>::value;
     const int tid = threadIdx.x;
     const int n_ent = ng * 32 * NB;
@@ -606,9 +606,10 @@ __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned lon
         // watchdog turns a lost producer into a kernel error, not a hang)
         bool done = false;
         const unsigned long long t_start = dev::globaltimer();
-        while (!done) {
+        for (int round = 0; !done; ++round) {
             done = true;
             if (dev::globaltimer() - t_start > 4000000000ull) __trap();
+            if (round > 0 && backoff > 0) __nanosleep(backoff);
 #pragma unroll
             for (int u = 0; u < XPT; ++u) {
                 if (!need[u]) continue;
