@@ -22,7 +22,7 @@ def _layer(F, fo, fi, seed, C=256):
     return F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), fi, 1), cb, idx
 
 
-@pytest.mark.parametrize("B", [1, 3])
+@pytest.mark.parametrize("B", [1, 3, 8])
 def test_chain_matches_oracle(F, oracle_lib, B):
     h, ffn, kv = 1024, 2048, 256
     blocks = []
