@@ -4,7 +4,9 @@
 // LUT_ss[k] = dot(X[l]_ss, T_cluster[ss][k]) over all K_s centroids,
 // then Y[l][j] += LUT_ss[T_index[ss][j]].  The paper's design is output-
 // stationary with a double-buffered 257-float LUT per (token, subspace); here
-// one CTA owns 1024 weight rows x MT tokens, builds the LUTs of a whole
+// one CTA (16 warps, 2 rows per thread) owns 1024 weight rows x MT = 6 tokens
+// (3 token-pair LUT images = 192 KiB at C = 256: the per-group LUT build and
+// index re-layout are amortised over 6 tokens), builds the LUTs of a whole
 // 32-subspace group at once in SMEM, [C][32 subspaces] fp32 per token laid out
 // like the GEMV codebook image, and every lane (= 4 weight rows, rotated
 // subspace order) gathers conflict-free with the one-`prmt` address.  The
@@ -18,9 +20,9 @@ namespace fasq {
 
 namespace {
 
-constexpr int LUT_MT = 4;          // tokens per CTA
-constexpr int LUT_RPT = 4;         // weight rows per thread
-constexpr int LUT_THREADS = 256;
+constexpr int LUT_MT = 6;          // tokens per CTA
+constexpr int LUT_RPT = 2;         // weight rows per thread
+constexpr int LUT_THREADS = 512;
 constexpr int LUT_R = LUT_THREADS * LUT_RPT;   // 1024 rows per CTA
 
 struct LutParams {
