@@ -52,6 +52,7 @@ struct TcParams {
     float* ws;               // split-K (gridDim.z > 1): fp32 partial tiles [ks][tiles][256 tokens][256 rows]
     unsigned* tickets;       // [tiles][2] arrive / depart counters (zero between launches)
     int M, F_out, F_out_pad, n_groups, C, y_f32;
+    int tile0, ntx;          // this launch covers tiles tile0 + blockIdx.x (row tile = tile % ntx)
 };
 
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
@@ -99,8 +100,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 * TC_STAGES + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * TC_N;          // weight-row tile
-    const int m0 = blockIdx.y * TC_M * TC_MT;  // first token of this CTA's token tiles
+    const int tile_g = p.tile0 + (int)blockIdx.x;            // tile of the whole problem
+    const int n0 = (tile_g % p.ntx) * TC_N;                  // weight-row tile
+    const int m0 = (tile_g / p.ntx) * TC_M * TC_MT;          // first token of this CTA's token tiles
     // split-K (small M: too few tiles for the SMs): this CTA's K chunks [kb, kb + nk)
     const int ksplit = (int)gridDim.z, kz = (int)blockIdx.z;
     const int kb = (int)((int64_t)kz * p.n_groups / ksplit);
@@ -253,7 +255,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
             const int t = ew >> 2;                     // accumulator (token tile) this warp drains
             const int ml = t * TC_M + q * 32 + lane;   // token within the CTA tile
             const int m = m0 + ml;                     // token
-            const int tile = (int)(blockIdx.y * gridDim.x + blockIdx.x);
+            const int tile = (int)blockIdx.x;         // tile within this launch (workspace / tickets)
             // 32 consecutive outputs (rows n .. n+31) of token m -> Y (fp32 / fp16)
             auto store32 = [&](int n, const float* r) {
                 if (m >= p.M || n >= p.F_out) return;
@@ -309,7 +311,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
                 for (int v = 0; v < 32; ++v) f[v] = __uint_as_float(r[v]);
                 if (ksplit > 1) {
                     // partial tile -> workspace, merged below in fixed ks order (deterministic)
-                    float* wr = p.ws + (((size_t)kz * gridDim.x * gridDim.y + tile) * (TC_M * TC_MT) + ml) * TC_N + c0;
+                    float* wr = p.ws + (((size_t)kz * gridDim.x + tile) * (TC_M * TC_MT) + ml) * TC_N + c0;
 #pragma unroll
                     for (int v = 0; v < 8; ++v)
                         __stcg(reinterpret_cast<float4*>(wr) + v, make_float4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]));
@@ -348,7 +350,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
                     for (int v = 0; v < 32; ++v) f[v] = 0.f;
                     for (int z = 0; z < ksplit; ++z) {
                         const float4* rd = reinterpret_cast<const float4*>(
-                            p.ws + (((size_t)z * gridDim.x * gridDim.y + tile) * (TC_M * TC_MT) + ml) * TC_N + c0);
+                            p.ws + (((size_t)z * gridDim.x + tile) * (TC_M * TC_MT) + ml) * TC_N + c0);
 #pragma unroll
                         for (int v = 0; v < 8; ++v) {
                             const float4 w = __ldcg(rd + v);
@@ -427,60 +429,83 @@ fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void
     if (lim < smem) { set_error("gemm_tc: SMEM"); return FASQ_E_UNSUPPORTED; }
     // F_out_pad rows of the idx table exist; tiles past F_out_pad read beyond it
     // -> require the row tile grid to stay within F_out_pad (pad logic below).
-    dim3 grid((unsigned)((L->F_out_pad + TC_N - 1) / TC_N), (unsigned)((M + TC_M * TC_MT - 1) / (TC_M * TC_MT)));
-    // small M: fewer tiles than SMs -> split K over gridDim.z (>= 8 chunks
-    // each); partial tiles go through an fp32 workspace and are summed by the
-    // last CTA of each tile in fixed ks order (deterministic)
+    const int ntx = (L->F_out_pad + TC_N - 1) / TC_N;
+    const int nty = (int)((M + TC_M * TC_MT - 1) / (TC_M * TC_MT));
+    const int tiles_all = ntx * nty;
+    p.ntx = ntx;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int tiles = (int)(grid.x * grid.y);
-    int ks = 1;
-    if (const char* e = getenv("FASQ_GEMM_KSPLIT")) ks = atoi(e);
-    else if (tiles < sms) ks = std::min(sms / tiles, L->n_groups / 8);
-    ks = ks >= 8 ? 8 : ks >= 4 ? 4 : ks >= 2 ? 2 : 1;          // the merge splits 256 columns by ks
-    while (ks > 1 && (tiles * ks > sms || ks > L->n_groups)) ks >>= 1;   // co-resident, >= 1 chunk each
-    if (ks > 1) {
-        // per-layer workspace (like the GEMV's): grown outside stream capture
-        static std::mutex mu;
-        std::lock_guard<std::mutex> lk(mu);
-        fasq_layer* Lw = const_cast<fasq_layer*>(L);   // workspace only; the PQ data is immutable
-        const int64_t need = (int64_t)ks * tiles * (TC_M * TC_MT) * TC_N * (int64_t)sizeof(float);
-        if (need > Lw->gws_bytes || 2 * tiles > Lw->n_gtickets) {
-            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-            cudaStreamIsCapturing(st, &cs);
-            if (cs != cudaStreamCaptureStatusNone) {
-                set_error("fasq_gemm: split-K workspace must be sized by one uncaptured call with this M first");
-                return FASQ_E_ARG;
-            }
-            FASQ_CUDA_TRY(cudaStreamSynchronize(st));
-            if (need > Lw->gws_bytes) {
-                if (Lw->gws) cudaFree(Lw->gws);
-                Lw->gws = nullptr;
-                Lw->gws_bytes = 0;
-                if (cudaMalloc(&Lw->gws, (size_t)need) != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
-                Lw->gws_bytes = need;
-            }
-            if (2 * tiles > Lw->n_gtickets) {
-                if (Lw->gtickets) cudaFree(Lw->gtickets);
-                Lw->gtickets = nullptr;
-                Lw->n_gtickets = 0;
-                const int nt = std::max(2 * tiles, 128);   // [tiles][arrive, depart]
-                if (cudaMalloc(&Lw->gtickets, (size_t)nt * sizeof(unsigned)) != cudaSuccess) {
-                    cudaGetLastError();
-                    return FASQ_E_OOM;
-                }
-                FASQ_CUDA_TRY(cudaMemset(Lw->gtickets, 0, (size_t)nt * sizeof(unsigned)));
-                Lw->n_gtickets = nt;
-            }
-        }
-        p.ws = Lw->gws;
-        p.tickets = Lw->gtickets;
-        grid.z = (unsigned)ks;
+    // Tile scheduling (one CTA per SM; 1-D grids over tile ranges):
+    //  * fewer tiles than SMs (small M): split K over gridDim.z for all tiles;
+    //  * several waves with a small last wave (e.g. 14336 rows x M = 2048: 448
+    //    tiles = 3 x 148 + 4): the full waves in one launch, the tail tiles in
+    //    a second launch split over K so the tail takes ~1/ks of a tile.
+    // Split-K: fp32 partial tiles through a per-layer workspace, merged in
+    // fixed ks order (deterministic), see the kernel epilogue.
+    auto pick_ks = [&](int tiles) {
+        int ks = 1;
+        if (const char* e = getenv("FASQ_GEMM_KSPLIT")) ks = atoi(e);
+        else if (tiles < sms) ks = std::min(sms / tiles, L->n_groups / 8);
+        ks = ks >= 8 ? 8 : ks >= 4 ? 4 : ks >= 2 ? 2 : 1;          // the merge splits 256 columns by ks
+        while (ks > 1 && (tiles * ks > sms || ks > L->n_groups)) ks >>= 1;   // co-resident, >= 1 chunk each
+        return ks;
+    };
+    int launches[2][3];   // {tile0, tiles, ks}
+    int nl = 0;
+    const int tail = tiles_all > sms ? tiles_all % sms : 0;
+    if (tail > 0 && tail <= sms / 4 && getenv("FASQ_GEMM_KSPLIT") == nullptr) {
+        launches[nl][0] = 0; launches[nl][1] = tiles_all - tail; launches[nl][2] = 1; ++nl;
+        launches[nl][0] = tiles_all - tail; launches[nl][1] = tail; launches[nl][2] = pick_ks(tail); ++nl;
+    } else {
+        launches[nl][0] = 0; launches[nl][1] = tiles_all; launches[nl][2] = pick_ks(tiles_all); ++nl;
     }
-    k_gemm_tc<<<grid, TC_THREADS, smem, st>>>(map, p);
-    FASQ_CUDA_TRY(cudaGetLastError());
-    set_launch_count(1);
+    for (int li = 0; li < nl; ++li) {
+        const int tiles = launches[li][1], ks = launches[li][2];
+        dim3 grid((unsigned)tiles, 1, 1);
+        p.tile0 = launches[li][0];
+        if (ks > 1) {
+            // per-layer workspace (like the GEMV's): grown outside stream capture
+            static std::mutex mu;
+            std::lock_guard<std::mutex> lk(mu);
+            fasq_layer* Lw = const_cast<fasq_layer*>(L);   // workspace only; the PQ data is immutable
+            const int64_t need = (int64_t)ks * tiles * (TC_M * TC_MT) * TC_N * (int64_t)sizeof(float);
+            if (need > Lw->gws_bytes || 2 * tiles > Lw->n_gtickets) {
+                cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+                cudaStreamIsCapturing(st, &cs);
+                if (cs != cudaStreamCaptureStatusNone) {
+                    set_error("fasq_gemm: split-K workspace must be sized by one uncaptured call with this M first");
+                    return FASQ_E_ARG;
+                }
+                FASQ_CUDA_TRY(cudaStreamSynchronize(st));
+                if (need > Lw->gws_bytes) {
+                    if (Lw->gws) cudaFree(Lw->gws);
+                    Lw->gws = nullptr;
+                    Lw->gws_bytes = 0;
+                    if (cudaMalloc(&Lw->gws, (size_t)need) != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
+                    Lw->gws_bytes = need;
+                }
+                if (2 * tiles > Lw->n_gtickets) {
+                    if (Lw->gtickets) cudaFree(Lw->gtickets);
+                    Lw->gtickets = nullptr;
+                    Lw->n_gtickets = 0;
+                    const int nt = std::max(2 * tiles, 128);   // [tiles][arrive, depart]
+                    if (cudaMalloc(&Lw->gtickets, (size_t)nt * sizeof(unsigned)) != cudaSuccess) {
+                        cudaGetLastError();
+                        return FASQ_E_OOM;
+                    }
+                    FASQ_CUDA_TRY(cudaMemset(Lw->gtickets, 0, (size_t)nt * sizeof(unsigned)));
+                    Lw->n_gtickets = nt;
+                }
+            }
+            p.ws = Lw->gws;
+            p.tickets = Lw->gtickets;
+            grid.z = (unsigned)ks;
+        }
+        k_gemm_tc<<<grid, TC_THREADS, smem, st>>>(map, p);
+        FASQ_CUDA_TRY(cudaGetLastError());
+    }
+    set_launch_count(nl);
     return FASQ_OK;
 }
 

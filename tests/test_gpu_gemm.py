@@ -106,3 +106,25 @@ def test_gemm_tc_split_k(F, oracle_lib, monkeypatch, F_out, F_in, M, ks):
     ref = oracle_lib.gemm(cb, idx, X)
     ok, info = parity_ok(Y1.cpu().numpy().astype(np.float64), ref, X, F_in)
     assert ok, info
+
+
+def test_gemm_tc_tail_wave_split_k(F, oracle_lib, monkeypatch):
+    """More tiles than SMs with a small last wave (5 row tiles x 30 token tiles =
+    150 tiles on 148 SMs): the full waves run as one launch, the 2 tail tiles as a
+    split-K launch.  The tail tiles (last 256 tokens) are checked against the
+    oracle, the whole output against the single-launch path."""
+    F_out, F_in, M = 1280, 1024, 7680
+    cb, idx = synth.random_layer(F_out, F_in, 2, 256, seed=77)
+    X = synth.activation(M, F_in, seed=78)
+    L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), F_in, 1)
+    Xd = torch.from_numpy(X).cuda()
+    Y = F.gemm(L, Xd, out_dtype=torch.float32, algo=F.GEMM_EXPAND_TC)
+    monkeypatch.setenv("FASQ_GEMM_KSPLIT", "1")
+    Y1 = F.gemm(L, Xd, out_dtype=torch.float32, algo=F.GEMM_EXPAND_TC)
+    torch.cuda.synchronize()
+    tail = slice(M - 256, M)
+    ref = oracle_lib.gemm(cb, idx, X[tail])
+    ok, info = parity_ok(Y[tail].cpu().numpy().astype(np.float64), ref, X[tail], F_in)
+    assert ok, info
+    d = (Y - Y1).abs().max().item()
+    assert d <= 1e-3 * max(1.0, Y1.abs().max().item()), d
