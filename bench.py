@@ -435,6 +435,72 @@ KINDS = (("qkv", ("q_proj", "k_proj", "v_proj")), ("o", ("o_proj",)), ("gate_up"
          ("down", ("down_proj",)))
 
 
+def prefill_model(dense_peak, Ms=(512, 2048), reps=3):
+    """configs[4] at N = 1: the prefill pass of the whole PQ linear stack --
+    M tokens through the 224 Llama-3-8B-shaped PQ layers with fasq_gemm
+    (EXPAND, tcgen05), fp16 activations chained block to block like the decode
+    chain (q/k/v and gate/up read the same input); attention/norms excluded.
+    Replayed from a CUDA graph; tok/s = M / pass time."""
+    import torch
+
+    import paper_2605_04084_b200 as F
+    import synth
+
+    nb = synth.LLAMA3_8B_BLOCKS
+    shapes = {n: (fo, fi) for (n, fo, fi) in synth.LLAMA3_8B_LAYERS}
+    blocks = []
+    for b in range(nb):
+        Ls = {}
+        for li, (name, fo, fi) in enumerate(synth.LLAMA3_8B_LAYERS):
+            cb, idx = synth.torch_random_layer(fo, fi, D, C, seed=11000 + b * 7 + li)
+            Ls[name] = F.import_layer(cb, idx, fi)
+            del cb, idx
+        blocks.append(Ls)
+    flops = 2.0 * nb * sum(fo * fi for (fo, fi) in shapes.values())
+    out = {}
+    for M in Ms:
+        x0 = synth.torch_activation(M, 4096)
+        bufs = {n: torch.empty((M, fo), dtype=torch.float16, device="cuda") for n, (fo, fi) in shapes.items()}
+
+        def one_pass():
+            h = x0
+            for Ls in blocks:
+                for n in ("q_proj", "k_proj", "v_proj"):
+                    F.gemm(Ls[n], h, out=bufs[n], algo=F.GEMM_EXPAND_TC)
+                F.gemm(Ls["o_proj"], bufs["q_proj"], out=bufs["o_proj"], algo=F.GEMM_EXPAND_TC)
+                for n in ("gate_proj", "up_proj"):
+                    F.gemm(Ls[n], bufs["o_proj"], out=bufs[n], algo=F.GEMM_EXPAND_TC)
+                F.gemm(Ls["down_proj"], bufs["gate_proj"], out=bufs["down_proj"], algo=F.GEMM_EXPAND_TC)
+                h = bufs["down_proj"]
+        one_pass()                      # sizes split-K workspaces outside capture
+        torch.cuda.synchronize()
+        gs = torch.cuda.Stream()
+        gs.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(gs):
+            with torch.cuda.graph(g, stream=gs):
+                one_pass()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        tf = flops * M / (ms * 1e-3) / 1e12
+        out["M%d" % M] = {"ms_per_pass": round(ms, 3), "tok_s": round(M * 1e3 / ms, 1), "tflops": round(tf, 1),
+                          "frac_of_dense_peak": round(tf / dense_peak, 3)}
+        del g, bufs
+    for Ls in blocks:
+        for L in Ls.values():
+            L.free()
+    torch.cuda.synchronize()
+    return out
+
+
 def decode_batch(peak, batches=(2, 4, 8), runs=20):
     """decode batch B in {2, 4, 8} at (2,256) through the
     chain kernel (one step = B tokens through the 224 layers).  Bytes per step
@@ -713,6 +779,10 @@ def main():
             side["decode_batch"] = decode_batch(peak)
         except Exception as e:
             side["decode_batch"] = {"error": str(e)[:200]}
+        try:
+            side["prefill_model"] = prefill_model(float(peaks.get("bf16_tflops", 1692.0)))
+        except Exception as e:
+            side["prefill_model"] = {"error": str(e)[:200]}
         try:
             side["gpu_pack"] = pack_time()
         except Exception as e:
