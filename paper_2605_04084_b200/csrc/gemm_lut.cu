@@ -14,6 +14,8 @@
 // layout into row-rotated rows (byte p of row r = subspace (p + r) & 31).  The
 // gathers are pure FADD on CUDA cores -- no tensor cores --
 // which is why the EXPAND variant exists (gemm_tc.cu).
+#include <mutex>
+
 #include "fasq_internal.cuh"
 
 namespace fasq {
@@ -27,7 +29,7 @@ constexpr int LUT_R = LUT_THREADS * LUT_RPT;   // 1024 rows per CTA
 
 struct LutParams {
     const uint8_t* idx;       // [n_groups][F_out_pad/64][32][64] (fasq_internal.cuh)
-    const uint8_t* cbimg;     // [n_groups][C][32][4]   (d <= 2)
+    const uint8_t* cbimg;     // [n_groups][C][32][E], E = 4*EW bytes (d <= 2: 4, d = 4: 8, d = 8: 16)
     const __half* X;          // [M][F_in]
     void* Y;
     int M, F_in, F_out, F_out_pad, n_groups, N_ss, C, d, y_f32;
@@ -35,6 +37,9 @@ struct LutParams {
 
 // LUT SMEM: token pair tp = t>>1 occupies C*256 B; row k = [t even: 32 x f32][t odd: 32 x f32];
 // then the row-rotated index block [LUT_R][32] bytes.
+// EW = 32-bit words per codebook entry / x slice (1: d <= 2, 2: d = 4, 4: d = 8):
+// LUT entry = dot(x_ss, c_k) accumulated word by word in the GEMV's order.
+template <int EW>
 __global__ void __launch_bounds__(LUT_THREADS, 1) k_gemm_lut(LutParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int C = p.C;
@@ -61,27 +66,37 @@ __global__ void __launch_bounds__(LUT_THREADS, 1) k_gemm_lut(LutParams p) {
     for (int g = 0; g < p.n_groups; ++g) {
         __syncthreads();   // previous group's gathers done
         // build: entry (t, k, sub) = sum_e x[t][sub*d+e] * c[sub][k][e]  (fp32, exact fp16 products)
-        const uint32_t* cbg = reinterpret_cast<const uint32_t*>(p.cbimg + (size_t)g * C * 128);
+        const uint32_t* cbg = reinterpret_cast<const uint32_t*>(p.cbimg + (size_t)g * C * 128 * EW);
         // this thread's subspace is fixed (LUT_THREADS is a multiple of 32): its
         // x slices for the MT tokens are loaded once per group
         const int sub = tid & 31, ss = g * 32 + sub;
-        uint32_t xv[LUT_MT];
+        uint32_t xv[LUT_MT][EW];
 #pragma unroll
         for (int t = 0; t < LUT_MT; ++t) {
             const int m = m0 + t;
-            xv[t] = 0;
+#pragma unroll
+            for (int q = 0; q < EW; ++q) xv[t][q] = 0;
             if (m < p.M && ss < p.N_ss) {
                 const uint16_t* xs = reinterpret_cast<const uint16_t*>(p.X) + (size_t)m * p.F_in + (size_t)ss * p.d;
-                xv[t] = p.d == 2 ? (uint32_t)xs[0] | ((uint32_t)xs[1] << 16) : (uint32_t)xs[0];
+                if (EW == 1) {
+                    xv[t][0] = p.d == 2 ? (uint32_t)xs[0] | ((uint32_t)xs[1] << 16) : (uint32_t)xs[0];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < EW; ++q) xv[t][q] = (uint32_t)xs[2 * q] | ((uint32_t)xs[2 * q + 1] << 16);
+                }
             }
         }
 #pragma unroll 4
         for (int e = tid; e < C * 32; e += LUT_THREADS) {
             const int k = e >> 5;
-            const uint32_t c = cbg[e];
+            uint32_t c[EW];
+#pragma unroll
+            for (int q = 0; q < EW; ++q) c[q] = cbg[(size_t)e * EW + q];
 #pragma unroll
             for (int t = 0; t < LUT_MT; ++t) {
-                const float v = dev::fhfma2(c, xv[t], 0.f);
+                float v = 0.f;
+#pragma unroll
+                for (int q = 0; q < EW; ++q) v = dev::fhfma2(c[q], xv[t][q], v);
                 reinterpret_cast<float*>(smem)[((t >> 1) * C * 64) + k * 64 + (t & 1) * 32 + sub] = v;
             }
         }
@@ -133,11 +148,21 @@ __global__ void __launch_bounds__(LUT_THREADS, 1) k_gemm_lut(LutParams p) {
     }
 }
 
+template <int EW>
+fasq_status launch_lut(const LutParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+    static std::once_flag once;   // per instantiation
+    static size_t lim = 0;
+    std::call_once(once, [] { lim = set_max_dyn_smem(k_gemm_lut<EW>); });
+    if (lim < smem) { set_error("gemm_lut: SMEM"); return FASQ_E_UNSUPPORTED; }
+    k_gemm_lut<EW><<<grid, LUT_THREADS, smem, st>>>(p);
+    return FASQ_OK;
+}
+
 }  // namespace
 
 fasq_status gemm_lut_launch(const fasq_layer* L, const __half* X, int64_t M, void* Y, fasq_dtype yt,
                             cudaStream_t st) {
-    if (L->d > 2) { set_error("GEMM-LUT supports d <= 2"); return FASQ_E_UNSUPPORTED; }
+
     if (M > (1ll << 30)) return FASQ_E_UNSUPPORTED;
     LutParams p{};
     p.idx = L->idx;
@@ -154,13 +179,10 @@ fasq_status gemm_lut_launch(const fasq_layer* L, const __half* X, int64_t M, voi
     p.d = L->d;
     p.y_f32 = yt == FASQ_F32;
     const size_t smem = (size_t)(LUT_MT / 2) * L->C * 256 + (size_t)LUT_R * 32;
-    static bool attr = false;
-    if (!attr) {
-        if (set_max_dyn_smem(k_gemm_lut) < smem) { set_error("gemm_lut: SMEM"); return FASQ_E_UNSUPPORTED; }
-        attr = true;
-    }
     dim3 grid((unsigned)((L->F_out_pad + LUT_R - 1) / LUT_R), (unsigned)((M + LUT_MT - 1) / LUT_MT));
-    k_gemm_lut<<<grid, LUT_THREADS, smem, st>>>(p);
+    fasq_status s = L->d <= 2 ? launch_lut<1>(p, grid, smem, st)
+                  : L->d == 4 ? launch_lut<2>(p, grid, smem, st) : launch_lut<4>(p, grid, smem, st);
+    if (s != FASQ_OK) return s;
     FASQ_CUDA_TRY(cudaGetLastError());
     set_launch_count(1);
     return FASQ_OK;

@@ -128,3 +128,17 @@ def test_gemm_tc_tail_wave_split_k(F, oracle_lib, monkeypatch):
     assert ok, info
     d = (Y - Y1).abs().max().item()
     assert d <= 1e-3 * max(1.0, Y1.abs().max().item()), d
+
+
+@pytest.mark.parametrize("d,C,F_out,F_in,M", [(4, 256, 512, 1024, 100), (8, 128, 300, 512, 37), (1, 64, 256, 256, 50),
+                                              (4, 16, 1000, 2048, 7)])
+def test_gemm_lut_all_subvector_sizes(F, oracle_lib, d, C, F_out, F_in, M):
+    """GEMM-LUT (and AUTO, which routes d != 2 to it) for every sub-vector size:
+    the LUT entry is dot(x_ss, c_k) over d elements, gathered by index."""
+    cb, idx = synth.random_layer(F_out, F_in, d, C, seed=F_out + d + M)
+    X = synth.activation(M, F_in, seed=M + d)
+    ref = oracle_lib.gemm(cb, idx, X)
+    for algo in (F.GEMM_LUT, F.GEMM_AUTO):
+        Y = _run(F, cb, idx, X, F_in, 1, algo)
+        ok, info = parity_ok(Y, ref, X, F_in)
+        assert ok, (algo, info)
