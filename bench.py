@@ -634,18 +634,31 @@ def decode_sweep(peak, settings=((2, 256), (2, 128), (4, 256), (1, 256), (2, 64)
 
 
 def pack_time():
+    """GPU k-means pack (Alg. 1, 25 Lloyd rounds, d=2, C=256) of one seeded
+    layer of each Llama-3-8B shape, and the whole-model estimate (x 32 blocks);
+    the paper quotes ~10 minutes for all layers on one GPU."""
     import torch
 
     import paper_2605_04084_b200 as F
     import synth
-    W = synth.torch_activation(4096, 4096, seed=5, std=0.02)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    L = F.pack(W, d=D, C=C, group=1, seed=0, iters=25)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    L.free()
-    return {"layer": "4096x4096", "d": D, "C": C, "iters": 25, "seconds": round(dt, 3)}
+    per = {}
+    block_s = 0.0
+    for (name, fo, fi) in synth.LLAMA3_8B_LAYERS:
+        key = "%dx%d" % (fo, fi)
+        if key not in per:
+            W = synth.torch_activation(fo, fi, seed=5, std=0.02)
+            F.pack(synth.torch_activation(64, fi, seed=6, std=0.02), d=D, C=min(C, 64), group=1, seed=0,
+                   iters=1).free()   # warm-up (allocations, CUB temp storage)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            L = F.pack(W, d=D, C=C, group=1, seed=0, iters=25)
+            torch.cuda.synchronize()
+            per[key] = round(time.perf_counter() - t0, 4)
+            L.free()
+            del W
+        block_s += per[key]
+    return {"d": D, "C": C, "iters": 25, "seconds_per_layer_shape": per,
+            "whole_model_seconds_est": round(block_s * synth.LLAMA3_8B_BLOCKS, 2)}
 
 
 # ----------------------------------------------------------------------------
