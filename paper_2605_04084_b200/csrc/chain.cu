@@ -235,10 +235,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     uint32_t par_ring = 0;   // its mbarrier phase parity
     int cslot = 0;           // PAIR: codebook pair slot and parity
     uint32_t cpar = 0;
-    // PAIR gather constant = PRMT operand b: byte 0 = h*128 + 4*lane, byte 2 =
+    // PAIR gather constant = PRMT operand b: byte 0 = h*128 + 4*sigma, byte 2 =
     // pair slot (64 KiB stride), so the address is PRMT(idx word, lbv) + the
-    // ring base (uniform) -> LDS [R + UR]
-    const uint32_t lb = (uint32_t)lane * 4u;
+    // ring base (uniform) -> LDS [R + UR] (gemv_core.cuh compute_group_set)
     for (int phj = 0; phj < p.n_steps * p.mi; ++phj) {
         const int ph = phj / p.mi, j = phj % p.mi;
         // the work item and phase are read-only for the kernel's lifetime
@@ -297,30 +296,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         for (int q = 0; q < RW; ++q)
 #pragma unroll
             for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
-        if constexpr (PAIR) {
-            // one iteration per codebook pair slot: groups i (h = 0), i+1 (h = 1)
-            const bool run = active && !(p.dbg & 1);
-            for (int i = 0; i < ng; i += 2) {
-                dev::mbar_wait(cfull0 + 8 * cslot, cpar);
-                const uint32_t lbs = lb + ((uint32_t)cslot << 16);
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (h == 1 && i + 1 >= ng) break;
-                    dev::mbar_wait(full0 + 8 * slot, par_ring);
-                    if (run) {
-                        uint32_t xv[NB][E / 4];
-                        core::load_x<D, NB>(xv, s_x + (i + h) * XG, lane);
-                        core::compute_group_pair<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb,
-                                                            lbs + ((uint32_t)h << 7), xv);
-                    }
-                    __syncwarp();
-                    if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
-                    if (++slot == ST) { slot = 0; par_ring ^= 1u; }
-                }
-                if (lane == 0) dev::mbar_arrive(cempty0 + 8 * cslot);
-                if (++cslot == CS) { cslot = 0; cpar ^= 1u; }
-            }
-        } else {
+        {   // d = 4, 8: lane = subspace over 64/B rows per warp
             for (int i = 0; i < ng; ++i) {
                 dev::mbar_wait(full0 + 8 * slot, par_ring);
                 if (active && !(p.dbg & 1)) {
