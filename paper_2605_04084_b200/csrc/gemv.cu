@@ -464,8 +464,10 @@ static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB, bool spin
         const double share = sms * ((double)L->F_out_pad * L->n_groups) / W;
         int ks = std::max(1, (int)(share / pl.row_tiles[l]));
         ks = std::min(ks, L->n_groups);
-        const int gper = (L->n_groups + ks - 1) / ks;   // balance: equal groups per CTA
-        ks = (L->n_groups + gper - 1) / gper;
+        if (getenv("FASQ_GEMV_UNEVEN") == nullptr) {     // balance: equal groups per CTA
+            const int gper = (L->n_groups + ks - 1) / ks;
+            ks = (L->n_groups + gper - 1) / gper;
+        }
         pl.ksplit[l] = ks;
         total += pl.row_tiles[l] * ks;
     }
