@@ -47,7 +47,7 @@ if ROOT not in sys.path:
 METRIC = "Llama-3-8B PQ decode tok/s + GEMV HBM GB/s vs 8 TB/s; prefill GEMM TFLOP/s"
 # dram__bytes_read.sum + dram__bytes_write.sum of ONE k_chain launch (32 blocks,
 # d=2, C=256, B=1) from `ncu --set full` (profiles/r01/ncu_chain_final_summary.txt)
-K_CHAIN_NCU_DRAM_BYTES = 4140843000 + 26033920
+K_CHAIN_NCU_DRAM_BYTES = 4143973000 + 26200576
 D, C = 2, 256
 
 
