@@ -271,3 +271,49 @@ def test_nonfinite_rejected(oracle_lib):
     with pytest.raises(oracle_lib.OracleError) as e:
         oracle_lib.pack(W, d=2, C=2)
     assert e.value.code == -4
+
+
+def test_tie_rule_lowest_k_duplicated_centroids(oracle_lib):
+    """Reading R5 / SPEC S:145: an exact distance tie goes to the LOWEST k.
+    With fewer distinct sub-vectors than C, init slots >= m copy slot 0
+    (reading R3), so every point equal to codebook[0] is at distance 0 from
+    slots 0 and m..C-1 at once: the lowest-k rule must pick 0 and no index
+    may ever point at a duplicate slot (a '<=' slip would pick C-1)."""
+    d, C, n_distinct = 2, 16, 5
+    W = synth.structured_weight(64, 8 * d, d, n_distinct, group=1, seed=77)
+    cb, idx, _ = oracle_lib.pack(W, d=d, C=C, group=1, seed=3, iters=0)
+    for g in range(cb.shape[0]):
+        pts = _points_of(W, d, 1, g)
+        m = len({tuple(p) for p in pts})
+        assert m < C
+        c = cb[g].astype(np.float64)
+        assert all(np.array_equal(c[k], c[0]) for k in range(m, C))   # slots >= m duplicate slot 0
+        assert idx[g].max() < m
+        at0 = np.all(pts == c[0], axis=1)
+        assert at0.any() and np.all(idx[g][at0] == 0)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_tie_rule_lowest_k_equidistant_point(oracle_lib, seed):
+    """Exact equidistance between two DISTINCT centroids: 1-D points
+    {0, 1, 2} (x64 rows), C = 2, no Lloyd round (iters = 0, the codebook is
+    the seeded init).  Whenever the init picked {0, 2}, point 1 lies at
+    distance exactly 1 from both and must take the lower of their two slots."""
+    W = np.repeat(np.array([0.0, 1.0, 2.0], np.float16), 64)[:, None]
+    cb, idx, _ = oracle_lib.pack(W, d=1, C=2, group=1, seed=seed, iters=0)
+    cents = [float(v) for v in cb[0, :, 0]]
+    one = idx[0][W[:, 0] == 1.0]
+    if sorted(cents) == [0.0, 2.0]:
+        assert np.all(one == 0)
+    else:   # 1 is itself a centroid: exact match wins
+        assert np.all(one == cents.index(1.0))
+
+
+def test_tie_rule_case_occurs():
+    """Guard for the parametrised test above: some seed in range(6) must hit
+    the {0, 2} init (otherwise the tie branch is untested)."""
+    import oracle
+    W = np.repeat(np.array([0.0, 1.0, 2.0], np.float16), 64)[:, None]
+    hits = [s for s in range(6)
+            if sorted(float(v) for v in oracle.pack(W, d=1, C=2, group=1, seed=s, iters=0)[0][0, :, 0]) == [0.0, 2.0]]
+    assert hits, "no seed produced the equidistant init"
