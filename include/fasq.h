@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define FASQ_ABI_VERSION 1
+#define FASQ_ABI_VERSION 2
 
 typedef enum {
     FASQ_OK = 0,
@@ -62,7 +62,8 @@ typedef enum {
     FASQ_E_SHAPE = -5,            /* operand shape mismatch          */
     FASQ_E_UNSUPPORTED = -6,      /* d not in {1,2,4,8}, C > 256, B > 8, n_pts > 2^23    */
     FASQ_E_CUDA = -7,             /* CUDA runtime / launch error, or no device           */
-    FASQ_E_OOM = -8               /* device allocation failed                            */
+    FASQ_E_OOM = -8,              /* device allocation failed                            */
+    FASQ_E_RANGE = -9             /* a counted partial left its |v| < 2^18 range (fasq_chain_check) */
 } fasq_status;
 
 typedef enum {
@@ -201,11 +202,13 @@ typedef struct fasq_chain fasq_chain; /* opaque */
  * without draining at step boundaries.  There is no grid-wide barrier:
  * every output element is a counted accumulator (int64 fixed-point sum in
  * FASQ_ACC_I64 units plus the number of K-split contributions), and a step
- * polls only the words of its own K range until they are final.  Same
- * numerics as chained fasq_gemv_grouped calls with FASQ_ACC_I64 outputs.
+ * polls only the words of its own K range until they are final.  Each K
+ * range's fp32 partial is rounded once to FASQ_ACC_I64 units, so results
+ * depend on the K-range plan (SM count; see fasq_chain_plan_ks) but not on
+ * arrival order: repeated runs are bit-identical.
  * The layers must outlive the chain.  Synchronises `stream`.
  * A step with more row tiles than SMs gives several work items per CTA.
- * FASQ_E_UNSUPPORTED: the SMEM plan does not fit, or > 63 K-splits. */
+ * FASQ_E_UNSUPPORTED: the SMEM plan does not fit. */
 fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int32_t B, void* stream,
                               fasq_chain** out);
 
@@ -218,13 +221,19 @@ fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int
  * GEMV: each rank red.adds its rows' counted accumulators into EVERY rank's
  * arena (NVLink peer memory), so a step's consumers on every GPU wait only for
  * their own K range -- no NCCL call and no host round trip between steps.
+ * Deterministic by default: the K ranges are those the unsharded (world = 1)
+ * chain would use on this GPU, so when every shard's F_out is a multiple of 64
+ * the gathered outputs are bit-identical to the single-GPU chain's
+ * (environment FASQ_CHAIN_FAST=1: plan each rank on its own shard instead).
  * world in 1..8; max_ctas > 0 caps the CTAs (e.g. several ranks sharing one
  * GPU in tests), 0 = one per SM.  Before the first run every rank must call
  * fasq_chain_set_peers (handles from every rank's fasq_chain_ipc_handle,
  * exchanged by the caller) or, for chains of one process,
- * fasq_chain_set_peer_chains.  All ranks must run their chains concurrently
- * and the same number of times (the kernels spin-wait on each other; a rank
- * that never delivers turns into a kernel error after ~4 s). */
+ * fasq_chain_set_peer_chains.  All ranks must run their chains the same
+ * number of times; run n on a rank starts writing only after every rank
+ * finished run n-1 (a per-run DONE word every rank increments in every rank's
+ * arena tail), and a rank that never delivers turns into a kernel error
+ * (trap) after ~4 s instead of a hang. */
 fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, int32_t B, int32_t world,
                                  int32_t rank, int32_t max_ctas, void* stream, fasq_chain** out);
 /* Writes this chain's arena IPC handle (cudaIpcMemHandle_t, 64 bytes). */
@@ -236,14 +245,32 @@ fasq_status fasq_chain_set_peer_chains(fasq_chain* chain, const fasq_chain* cons
 
 /* Runs the whole chain on x_dev (fp16 [B][F_in of the external-input steps]):
  * ONE kernel launch (the accumulators are double-buffered; each run zeroes the
- * buffer of the next run in-kernel, the parity lives on the device, so graph
- * replays work).  A chain instance must not run concurrently with itself. */
+ * buffer of the next run in-kernel, the run index lives on the device, so
+ * graph replays work).  A chain instance must not run concurrently with itself. */
 fasq_status fasq_chain_run(fasq_chain* chain, const void* x_dev, void* stream);
 
+/* End-to-end run with HOST buffers: copies x_host (fp16 [B][F_in], ideally
+ * pinned) to the device, runs the chain, converts the output of (step, layer)
+ * to fp16/fp32 and copies it to y_host.  Synchronous. */
+fasq_status fasq_chain_run_host(fasq_chain* chain, const void* x_host, void* y_host, int32_t step, int32_t layer,
+                                fasq_dtype dtype, void* stream);
+
 /* Output of layer `layer` of step `step` after the last run, as fp16 / fp32 /
- * FASQ_ACC_I64 [B][world*F_out] (all ranks' rows; valid until the next run). */
+ * FASQ_ACC_I64 [B][width] (width = world*F_out for gathered row shards;
+ * valid until the next run).  Waits on the device until every word carries
+ * all its contributions (peers' stores of the last step may still be in
+ * flight).  fp16/fp32 outputs of a run that raised the range flag are NaN. */
 fasq_status fasq_chain_output(const fasq_chain* chain, int32_t step, int32_t layer, void* y_dev,
                               fasq_dtype dtype, void* stream);
+/* Synchronises `stream`; FASQ_E_RANGE if any run since the last check had a
+ * K-split partial outside |v| < 2^18 (its values were clamped and its float
+ * outputs poisoned with NaN); clears the flag. */
+fasq_status fasq_chain_check(fasq_chain* chain, void* stream);
+/* Host-only planner query: K-split count per layer of one grouped step of
+ * n layers (F_out, n_groups = ceil(F_in/d/32)) on nctas CTAs at batch B
+ * (what fasq_chain_create uses; <= 63 per layer, the counted-word field). */
+int32_t fasq_chain_plan_ks(const int64_t* F_out, const int64_t* n_groups, int32_t n, int32_t nctas, int32_t d,
+                           int32_t B, int32_t* ks_out);
 /* Diagnostics: when trace_dev is not NULL, every later fasq_chain_run writes
  * per (step, CTA) four %globaltimer stamps (ns) into it, uint64
  * [n_steps][fasq_chain_ctas(chain)][4]: step entry, inputs final and staged
@@ -253,6 +280,79 @@ fasq_status fasq_chain_output(const fasq_chain* chain, int32_t step, int32_t lay
 fasq_status fasq_chain_trace(fasq_chain* chain, void* trace_dev);
 int32_t fasq_chain_ctas(const fasq_chain* chain);   /* CTAs (= SMs) the chain runs on; -1 for NULL */
 void fasq_chain_free(fasq_chain* chain);   /* synchronises the device; NULL is a no-op */
+
+/* ---- whole-model decode (Llama-shaped; the paper's E2E setting) ---- */
+
+/* A decoder-only model whose every linear layer is a FASQ layer (the
+ * embedding, norms and lm_head stay fp16).  HF Llama semantics: pre-norm
+ * blocks h' = h + o(Attn(RMSNorm(h))), h'' = h' + down(silu(gate(x)) * up(x))
+ * with x = RMSNorm(h'); RoPE rotate-half with theta; GQA (n_heads / n_kv_heads
+ * query heads per KV head); greedy argmax over the lm_head logits.
+ * Tensor parallelism (world > 1, Megatron): q/k/v are row shards holding
+ * this rank's n_heads/world heads (n_kv_heads/world KV heads), o is a K shard
+ * (its F_in = this rank's heads x head_dim), gate/up row shards of ffn/world,
+ * down a K shard (F_in = ffn/world); embed is the full table, lm_head this
+ * rank's vocab/world rows.  Pointer arrays have n_layers entries; every
+ * pointer is a device pointer owned by the caller and must outlive the model. */
+typedef struct {
+    int32_t n_layers, hidden, n_heads, n_kv_heads, head_dim, ffn, vocab;
+    float rms_eps, rope_theta;
+    int32_t max_T;       /* KV-cache positions per sequence                                   */
+    int32_t pos_wrap;    /* a step at position max_T-1 is followed by pos_wrap (benchmarks)   */
+    int32_t B;           /* sequences decoded together, 1..8                                  */
+    int32_t world, rank;
+    const fasq_layer* const* q;
+    const fasq_layer* const* k;
+    const fasq_layer* const* v;
+    const fasq_layer* const* o;
+    const fasq_layer* const* gate;
+    const fasq_layer* const* up;
+    const fasq_layer* const* down;
+    const void* const* attn_norm;   /* fp16 [hidden] per layer */
+    const void* const* mlp_norm;    /* fp16 [hidden] per layer */
+    const void* final_norm;         /* fp16 [hidden]           */
+    const void* embed;              /* fp16 [vocab][hidden]    */
+    const void* lm_head;            /* fp16 [vocab/world][hidden] */
+    int32_t max_ctas;               /* 0 = one CTA per SM; > 0 caps the CTAs (ranks sharing a GPU in tests) */
+} fasq_llama_desc;
+
+typedef struct fasq_llama fasq_llama; /* opaque */
+
+/* Builds the decode executor: one persistent chain (EMBED, then per block
+ * qkv <- RMSNorm, ATTN, o + residual, gate/up <- RMSNorm, down <- SwiGLU +
+ * residual) and the lm_head kernel; allocates the fp16 KV caches
+ * ([B][n_kv_heads/world][max_T][head_dim] per layer, zeroed).  Chain step
+ * numbering (fasq_llama_chain + fasq_chain_output): 0 = embedding h0; block l:
+ * 1+5l = q/k/v (layers 0/1/2), 2+5l = attention output, 3+5l = h after the
+ * attention residual, 4+5l = gate/up, 5+5l = h after the MLP residual.
+ * Synchronises `stream`. */
+fasq_status fasq_llama_create(const fasq_llama_desc* desc, void* stream, fasq_llama** out);
+fasq_status fasq_llama_ipc_handle(const fasq_llama* model, void* handle_out);   /* world > 1: as fasq_chain_* */
+fasq_status fasq_llama_set_peers(fasq_llama* model, const void* handles);
+/* In-process peers: models[r] is rank r's model (models[rank] == model). */
+fasq_status fasq_llama_set_peer_models(fasq_llama* model, const fasq_llama* const* models);
+const fasq_chain* fasq_llama_chain(const fasq_llama* model);
+/* This rank's KV cache of a layer: fp16 [B][n_kv_heads/world][max_T][head_dim]. */
+fasq_status fasq_llama_kv_cache(const fasq_llama* model, int32_t layer, void** k_dev, void** v_dev);
+/* The next step decodes tokens_host[b] (B entries) at position pos (pos < 0:
+ * keep the current position); positions < pos must be in the KV cache.
+ * Synchronous. */
+fasq_status fasq_llama_reset(fasq_llama* model, const int32_t* tokens_host, int32_t pos, void* stream);
+/* One greedy decode step of every sequence: TWO launches (chain, lm_head);
+ * the chosen tokens feed the next step on the device (graph-replayable). */
+fasq_status fasq_llama_step(fasq_llama* model, void* stream);
+/* The tokens the last step chose (int32 [B], device). */
+fasq_status fasq_llama_tokens(const fasq_llama* model, int32_t* tokens_dev, void* stream);
+/* End to end with a HOST buffer: one step, then the chosen tokens are copied
+ * to tokens_out_host (int32 [B]).  Synchronous. */
+fasq_status fasq_llama_step_host(fasq_llama* model, int32_t* tokens_out_host, void* stream);
+/* Diagnostics: enable (1) / disable (0) writing the lm_head logits (fp32
+ * [B][vocab/world]) of every later step; *logits_dev receives the buffer. */
+fasq_status fasq_llama_logits(fasq_llama* model, int32_t enable, void** logits_dev);
+/* Copies the token history (int32 [B][max_T]: the token each step embedded,
+ * at its position) to hist_dev. */
+fasq_status fasq_llama_token_history(const fasq_llama* model, int32_t* hist_dev, void* stream);
+void fasq_llama_free(fasq_llama* model);   /* synchronises the device; NULL is a no-op */
 
 /* Same product with HOST buffers (end-to-end path): copies x_host (fp16
  * [B][F_in], ideally pinned) to the device, runs fasq_gemv and copies y back

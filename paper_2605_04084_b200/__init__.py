@@ -27,14 +27,19 @@ ACC_SCALE = 2.0 ** 32   # FASQ_ACC_I64 units
 
 _STATUS = {0: "FASQ_OK", -1: "FASQ_E_ARG", -2: "FASQ_E_NONDIVISIBLE", -3: "FASQ_E_CLUSTER_OVERFLOW",
            -4: "FASQ_E_NONFINITE", -5: "FASQ_E_SHAPE", -6: "FASQ_E_UNSUPPORTED", -7: "FASQ_E_CUDA",
-           -8: "FASQ_E_OOM"}
+           -8: "FASQ_E_OOM", -9: "FASQ_E_RANGE"}
 
 # Every symbol include/fasq.h declares (checked by tests/test_abi.py).
 EXPORTED = ["fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
             "fasq_free", "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_acc_convert",
             "fasq_chain_create", "fasq_chain_create_tp", "fasq_chain_ipc_handle", "fasq_chain_set_peers",
             "fasq_chain_set_peer_chains", "fasq_chain_run", "fasq_chain_output", "fasq_chain_trace",
-            "fasq_chain_ctas", "fasq_chain_free", "fasq_gemv_host", "fasq_gemm",
+            "fasq_chain_ctas", "fasq_chain_free", "fasq_chain_run_host", "fasq_chain_check",
+            "fasq_chain_plan_ks", "fasq_gemv_host", "fasq_gemm",
+            "fasq_llama_create", "fasq_llama_ipc_handle", "fasq_llama_set_peers", "fasq_llama_set_peer_models",
+            "fasq_llama_chain",
+            "fasq_llama_kv_cache", "fasq_llama_reset", "fasq_llama_step", "fasq_llama_tokens",
+            "fasq_llama_step_host", "fasq_llama_logits", "fasq_llama_token_history", "fasq_llama_free",
             "fasq_last_launch_count", "fasq_status_string", "fasq_last_error_message",
             "fasq_abi_version"]
 
@@ -58,6 +63,20 @@ class GemvOpts(ctypes.Structure):
 class _ChainStep(ctypes.Structure):
     _fields_ = [("layers", ctypes.POINTER(ctypes.c_void_p)), ("n_layers", ctypes.c_int32),
                 ("input_step", ctypes.c_int32), ("input_layer", ctypes.c_int32)]
+
+
+class LlamaDesc(ctypes.Structure):
+    _fields_ = [("n_layers", ctypes.c_int32), ("hidden", ctypes.c_int32), ("n_heads", ctypes.c_int32),
+                ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32), ("ffn", ctypes.c_int32),
+                ("vocab", ctypes.c_int32), ("rms_eps", ctypes.c_float), ("rope_theta", ctypes.c_float),
+                ("max_T", ctypes.c_int32), ("pos_wrap", ctypes.c_int32), ("B", ctypes.c_int32),
+                ("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("q", ctypes.POINTER(ctypes.c_void_p)), ("k", ctypes.POINTER(ctypes.c_void_p)),
+                ("v", ctypes.POINTER(ctypes.c_void_p)), ("o", ctypes.POINTER(ctypes.c_void_p)),
+                ("gate", ctypes.POINTER(ctypes.c_void_p)), ("up", ctypes.POINTER(ctypes.c_void_p)),
+                ("down", ctypes.POINTER(ctypes.c_void_p)), ("attn_norm", ctypes.POINTER(ctypes.c_void_p)),
+                ("mlp_norm", ctypes.POINTER(ctypes.c_void_p)), ("final_norm", ctypes.c_void_p),
+                ("embed", ctypes.c_void_p), ("lm_head", ctypes.c_void_p), ("max_ctas", ctypes.c_int32)]
 
 
 class LayerInfo(ctypes.Structure):
@@ -103,6 +122,25 @@ def _load():
     L.fasq_chain_ctas.argtypes = [vp]
     L.fasq_chain_free.argtypes = [vp]
     L.fasq_chain_free.restype = None
+    L.fasq_chain_run_host.argtypes = [vp, vp, vp, i32, i32, i32, vp]
+    L.fasq_chain_check.argtypes = [vp, vp]
+    L.fasq_chain_plan_ks.argtypes = [ctypes.POINTER(i64), ctypes.POINTER(i64), i32, i32, i32, i32,
+                                     ctypes.POINTER(i32)]
+    L.fasq_llama_create.argtypes = [ctypes.POINTER(LlamaDesc), vp, pp]
+    L.fasq_llama_ipc_handle.argtypes = [vp, vp]
+    L.fasq_llama_set_peers.argtypes = [vp, vp]
+    L.fasq_llama_set_peer_models.argtypes = [vp, ctypes.POINTER(vp)]
+    L.fasq_llama_chain.argtypes = [vp]
+    L.fasq_llama_chain.restype = vp
+    L.fasq_llama_kv_cache.argtypes = [vp, i32, pp, pp]
+    L.fasq_llama_reset.argtypes = [vp, ctypes.POINTER(i32), i32, vp]
+    L.fasq_llama_step.argtypes = [vp, vp]
+    L.fasq_llama_tokens.argtypes = [vp, vp, vp]
+    L.fasq_llama_step_host.argtypes = [vp, ctypes.POINTER(i32), vp]
+    L.fasq_llama_logits.argtypes = [vp, i32, pp]
+    L.fasq_llama_token_history.argtypes = [vp, vp, vp]
+    L.fasq_llama_free.argtypes = [vp]
+    L.fasq_llama_free.restype = None
     L.fasq_gemm.argtypes = [vp, vp, i64, vp, i32, i32, vp]
     L.fasq_status_string.restype = ctypes.c_char_p
     L.fasq_last_error_message.restype = ctypes.c_char_p
@@ -110,7 +148,10 @@ def _load():
                  "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_acc_convert", "fasq_gemv_host",
                  "fasq_chain_create", "fasq_chain_create_tp", "fasq_chain_ipc_handle", "fasq_chain_set_peers",
                  "fasq_chain_set_peer_chains", "fasq_chain_run", "fasq_chain_output", "fasq_chain_trace",
-                 "fasq_chain_ctas", "fasq_gemm", "fasq_last_launch_count",
+                 "fasq_chain_ctas", "fasq_gemm", "fasq_last_launch_count", "fasq_chain_run_host",
+                 "fasq_chain_check", "fasq_chain_plan_ks", "fasq_llama_create", "fasq_llama_ipc_handle",
+                 "fasq_llama_set_peers", "fasq_llama_kv_cache", "fasq_llama_reset", "fasq_llama_step",
+                 "fasq_llama_tokens", "fasq_llama_set_peer_models", "fasq_llama_step_host", "fasq_llama_logits", "fasq_llama_token_history",
                  "fasq_abi_version"):
         getattr(L, name).restype = ctypes.c_int32
     return L
@@ -128,6 +169,16 @@ def _stream(stream=None) -> int:
     if stream is None:
         stream = torch.cuda.current_stream()
     return stream.cuda_stream
+
+
+def _check_out(out: torch.Tensor, shape, dtypes=(torch.float16, torch.float32, torch.int64)):
+    """Caller-supplied output buffers: CUDA, contiguous, exact shape, known dtype."""
+    if not isinstance(out, torch.Tensor) or not out.is_cuda:
+        raise TypeError("out must be a CUDA tensor")
+    if out.dtype not in dtypes:
+        raise TypeError("out dtype %s not in %s" % (out.dtype, dtypes))
+    if tuple(out.shape) != tuple(shape) or not out.is_contiguous():
+        raise FasqError(-5, "out must be contiguous %s, got %s" % (tuple(shape), tuple(out.shape)))
 
 
 def _cuda(t: torch.Tensor, dtype, name: str) -> torch.Tensor:
@@ -219,6 +270,7 @@ def gemv(layer: Layer, x: torch.Tensor, out: torch.Tensor | None = None,
         raise FasqError(-5, "x has %d columns, layer F_in=%d" % (x.shape[1], layer.F_in))
     if out is None:
         out = torch.empty((B, layer.F_out), dtype=out_dtype, device=x.device)
+    _check_out(out, (B, layer.F_out), (torch.float16, torch.float32))
     yt = FASQ_F32 if out.dtype == torch.float32 else FASQ_F16
     _check(lib.fasq_gemv_ex(layer.handle, x.data_ptr(), B, out.data_ptr(), yt, flags, _stream(stream)))
     return out
@@ -289,9 +341,41 @@ class Chain:
         self.world, self.rank = world, rank
         self.steps = [(list(l), s) for (l, s) in steps]
 
+    @property
+    def in_features(self) -> int:
+        for layers, src in self.steps:
+            if src is None:
+                return layers[0].F_in
+        raise ValueError("chain has no external-input step")
+
     def run(self, x: torch.Tensor, stream=None):
         x = _cuda(x, torch.float16, "x")
+        if x.dim() == 1:
+            x = x.unsqueeze(0)
+        if tuple(x.shape) != (self.B, self.in_features):
+            raise FasqError(-5, "x must be [%d][%d], got %s" % (self.B, self.in_features, tuple(x.shape)))
         _check(lib.fasq_chain_run(self._h, x.data_ptr(), _stream(stream)))
+
+    def run_host(self, x_host: torch.Tensor, y_host: torch.Tensor, step: int, layer: int = 0, stream=None):
+        """End to end with HOST buffers (H2D of x, the chain, conversion, D2H of y)."""
+        if x_host.is_cuda or y_host.is_cuda:
+            raise TypeError("run_host takes host tensors")
+        if x_host.dtype != torch.float16 or tuple(x_host.shape) != (self.B, self.in_features):
+            raise FasqError(-5, "x_host must be fp16 [%d][%d]" % (self.B, self.in_features))
+        width = self.steps[step][0][layer].F_out * self.world
+        if tuple(y_host.shape) != (self.B, width) or y_host.dtype not in (torch.float16, torch.float32):
+            raise FasqError(-5, "y_host must be fp16/fp32 [%d][%d]" % (self.B, width))
+        if not (x_host.is_contiguous() and y_host.is_contiguous()):
+            raise ValueError("host buffers must be contiguous")
+        yt = FASQ_F32 if y_host.dtype == torch.float32 else FASQ_F16
+        _check(lib.fasq_chain_run_host(self._h, x_host.data_ptr(), y_host.data_ptr(), step, layer, yt,
+                                       _stream(stream)))
+        return y_host
+
+    def check(self, stream=None):
+        """Raises FasqError(FASQ_E_RANGE) if a run since the last check had an
+        out-of-range counted partial (synchronises the stream)."""
+        _check(lib.fasq_chain_check(self._h, _stream(stream)))
 
     def ipc_handle(self) -> bytes:
         """64-byte cudaIpcMemHandle of this chain's arena (exchange across ranks)."""
@@ -316,6 +400,7 @@ class Chain:
         F_out = self.steps[step][0][layer].F_out * self.world
         if out is None:
             out = torch.empty((self.B, F_out), dtype=out_dtype, device="cuda")
+        _check_out(out, (self.B, F_out))
         dt = out.dtype
         yt = FASQ_F32 if dt == torch.float32 else FASQ_F16 if dt == torch.float16 else FASQ_ACC_I64
         _check(lib.fasq_chain_output(self._h, step, layer, out.data_ptr(), yt, _stream(stream)))
@@ -335,13 +420,13 @@ class Chain:
         _check(lib.fasq_chain_trace(self._h, None if buf is None else buf.data_ptr()))
 
     def free(self):
-        if self._h:
+        if self._h and getattr(self, "_owned", True):
             lib.fasq_chain_free(self._h)
-            self._h = ctypes.c_void_p(0)
+        self._h = ctypes.c_void_p(0)
 
     def __del__(self):
         try:
-            if getattr(self, "_h", None):
+            if getattr(self, "_h", None) and getattr(self, "_owned", True):
                 lib.fasq_chain_free(self._h)
         except Exception:
             pass
@@ -366,6 +451,175 @@ def gemm(layer: Layer, X: torch.Tensor, out: torch.Tensor | None = None,
         raise FasqError(-5, "X has %d columns, layer F_in=%d" % (X.shape[1], layer.F_in))
     if out is None:
         out = torch.empty((M, layer.F_out), dtype=out_dtype, device=X.device)
+    _check_out(out, (M, layer.F_out), (torch.float16, torch.float32))
     yt = FASQ_F32 if out.dtype == torch.float32 else FASQ_F16
     _check(lib.fasq_gemm(layer.handle, X.data_ptr(), M, out.data_ptr(), yt, algo, _stream(stream)))
     return out
+
+
+def plan_ks(shapes, nctas: int = 148, d: int = 2, B: int = 1):
+    """Host-only query of the chain planner: K-split count per layer of one
+    grouped step; shapes = [(F_out, F_in)]."""
+    n = len(shapes)
+    fo = (ctypes.c_int64 * n)(*[s[0] for s in shapes])
+    ng = (ctypes.c_int64 * n)(*[-(-(s[1] // d) // 32) for s in shapes])
+    ks = (ctypes.c_int32 * n)()
+    _check(lib.fasq_chain_plan_ks(fo, ng, n, nctas, d, B, ks))
+    return list(ks)
+
+
+class Llama:
+    """Whole-model greedy decode (fasq_llama_*): a Llama-shaped decoder whose
+    every linear layer is a FASQ Layer.  ``layers`` is a list (n_layers) of
+    dicts with keys q, k, v, o, gate, up, down (Layer, this rank's shard) and
+    attn_norm, mlp_norm (fp16 CUDA tensors [hidden]).  Chain step numbering:
+    0 = h0 (embedding); block l: 1+5l q/k/v, 2+5l attention output, 3+5l h
+    after the attention residual, 4+5l gate/up, 5+5l h after the MLP residual."""
+
+    def __init__(self, layers, final_norm, embed, lm_head, n_heads, n_kv_heads, head_dim, vocab,
+                 rms_eps=1e-5, rope_theta=500000.0, max_T=2048, pos_wrap=0, B=1, world=1, rank=0,
+                 max_ctas=0, stream=None):
+        self._keep = [final_norm, embed, lm_head, layers]
+        n = len(layers)
+        hidden = embed.shape[1]
+        for t, name in ((final_norm, "final_norm"), (embed, "embed"), (lm_head, "lm_head")):
+            _cuda(t, torch.float16, name)
+            if not t.is_contiguous():
+                raise ValueError(name + " must be contiguous")
+        if tuple(embed.shape) != (vocab, hidden) or tuple(lm_head.shape) != (vocab // world, hidden):
+            raise FasqError(-5, "embed must be [vocab][hidden] and lm_head [vocab/world][hidden]")
+
+        def arr(key):
+            a = (ctypes.c_void_p * n)()
+            for i, L in enumerate(layers):
+                v = L[key]
+                if isinstance(v, Layer):
+                    a[i] = v.handle.value
+                else:
+                    _cuda(v, torch.float16, key)
+                    if tuple(v.shape) != (hidden,) or not v.is_contiguous():
+                        raise FasqError(-5, "%s[%d] must be fp16 [%d]" % (key, i, hidden))
+                    a[i] = v.data_ptr()
+            self._keep.append(a)
+            return a
+        ffn = layers[0]["gate"].F_out * world
+        self.desc = LlamaDesc(n, hidden, n_heads, n_kv_heads, head_dim, ffn, vocab, rms_eps, rope_theta, max_T,
+                              pos_wrap, B, world, rank, arr("q"), arr("k"), arr("v"), arr("o"), arr("gate"),
+                              arr("up"), arr("down"), arr("attn_norm"), arr("mlp_norm"), final_norm.data_ptr(),
+                              embed.data_ptr(), lm_head.data_ptr(), max_ctas)
+        out = ctypes.c_void_p()
+        _check(lib.fasq_llama_create(ctypes.byref(self.desc), _stream(stream), ctypes.byref(out)))
+        self._h = out
+        self.B, self.world, self.rank = B, world, rank
+        self.n_layers, self.hidden, self.vocab, self.max_T = n, hidden, vocab, max_T
+        self.n_kv_local, self.head_dim = n_kv_heads // world, head_dim
+        # a non-owning view of the model's chain (fasq_chain_output etc.)
+        self.chain = Chain.__new__(Chain)
+        self.chain._h = ctypes.c_void_p(lib.fasq_llama_chain(self._h))
+        self.chain._owned = False
+        self.chain.B, self.chain.world, self.chain.rank = B, world, rank
+        self._logits = None
+
+    def kv_cache(self, layer: int):
+        """(K, V) fp16 views [B][n_kv/world][max_T][head_dim] of a layer's cache."""
+        kp, vp = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib.fasq_llama_kv_cache(self._h, layer, ctypes.byref(kp), ctypes.byref(vp)))
+        shape = (self.B, self.n_kv_local, self.max_T, self.head_dim)
+        return _wrap_dev(kp.value, shape, torch.float16), _wrap_dev(vp.value, shape, torch.float16)
+
+    def reset(self, tokens, pos: int, stream=None):
+        arr = (ctypes.c_int32 * self.B)(*[int(t) for t in tokens])
+        _check(lib.fasq_llama_reset(self._h, arr, pos, _stream(stream)))
+
+    def step(self, stream=None):
+        _check(lib.fasq_llama_step(self._h, _stream(stream)))
+
+    def tokens(self, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((self.B,), dtype=torch.int32, device="cuda")
+        _check_out(out, (self.B,), (torch.int32,))
+        _check(lib.fasq_llama_tokens(self._h, out.data_ptr(), _stream(stream)))
+        return out
+
+    def step_host(self, stream=None):
+        """One step end to end; returns the chosen tokens (host list)."""
+        arr = (ctypes.c_int32 * self.B)()
+        _check(lib.fasq_llama_step_host(self._h, arr, _stream(stream)))
+        return list(arr)
+
+    def enable_logits(self, on: bool = True):
+        p = ctypes.c_void_p()
+        _check(lib.fasq_llama_logits(self._h, 1 if on else 0, ctypes.byref(p)))
+        self._logits = _wrap_dev(p.value, (self.B, self.vocab // self.world), torch.float32) if on else None
+        return self._logits
+
+    def token_history(self, stream=None) -> torch.Tensor:
+        out = torch.empty((self.B, self.max_T), dtype=torch.int32, device="cuda")
+        _check(lib.fasq_llama_token_history(self._h, out.data_ptr(), _stream(stream)))
+        return out
+
+    def output(self, step: int, layer: int = 0, out_dtype=torch.float32, width: int | None = None, stream=None):
+        """Chain output (see the class docstring for the step numbering)."""
+        if width is None:
+            width = self._width(step, layer)
+        out = torch.empty((self.B, width), dtype=out_dtype, device="cuda")
+        yt = FASQ_F32 if out_dtype == torch.float32 else FASQ_F16 if out_dtype == torch.float16 else FASQ_ACC_I64
+        _check(lib.fasq_chain_output(self.chain._h, step, layer, out.data_ptr(), yt, _stream(stream)))
+        return out
+
+    def _width(self, step, layer):
+        if step == 0:
+            return self.hidden
+        k = (step - 1) % 5
+        L = self._keep[3][(step - 1) // 5]
+        if k == 0:
+            return (L["q"], L["k"], L["v"])[layer].F_out
+        if k == 1:
+            return L["q"].F_out
+        if k == 3:
+            return L["gate"].F_out
+        return self.hidden
+
+    def ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        _check(lib.fasq_llama_ipc_handle(self._h, buf))
+        return buf.raw
+
+    def set_peer_models(self, models):
+        """In-process ranks (tests): models[r] is rank r's Llama (including self)."""
+        arr = (ctypes.c_void_p * len(models))(*[m._h.value for m in models])
+        _check(lib.fasq_llama_set_peer_models(self._h, arr))
+
+    def set_peers(self, handles):
+        blob = b"".join(handles)
+        if len(blob) != 64 * self.world:
+            raise ValueError("need world x 64-byte handles")
+        _check(lib.fasq_llama_set_peers(self._h, ctypes.create_string_buffer(blob, len(blob))))
+
+    def free(self):
+        if self._h:
+            lib.fasq_llama_free(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib.fasq_llama_free(self._h)
+        except Exception:
+            pass
+
+
+def _wrap_dev(ptr: int, shape, dtype) -> torch.Tensor:
+    """A torch view of library-owned device memory (valid while its owner lives)."""
+    n = 1
+    for v in shape:
+        n *= v
+    es = torch.empty((), dtype=dtype).element_size()
+
+    class _A:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": {torch.float16: "<f2", torch.float32: "<f4",
+                                                                       torch.int32: "<i4"}[dtype],
+                                    "data": (ptr, False), "version": 2}
+    t = torch.as_tensor(_A(), device="cuda")
+    assert t.numel() * es == n * es
+    return t

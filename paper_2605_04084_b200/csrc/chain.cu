@@ -7,8 +7,8 @@
 // read its x.  This executor runs the whole chain in ONE persistent kernel
 // (one CTA per SM, cooperative launch):
 //
-//  * the per-step work (row tile x K-range of groups, same tiling as gemv.cu)
-//    is planned once on the host into a [steps][CTAs] table of work items;
+//  * the per-step work (row tile x K-range of groups) is planned once on the
+//    host into a [steps][CTAs][items] table;
 //  * the producer warp of every CTA streams the codebook/index stages of ALL
 //    its steps back to back through the SMEM ring -- weights do not depend on
 //    x, so the ring keeps filling while the consumers wait for the previous
@@ -16,15 +16,26 @@
 //  * there is NO grid-wide barrier between steps: every output element is a
 //    "counted accumulator" (gemv_core.cuh): an int64 red.add target that
 //    carries the fixed-point sum (units 2^-32, exact and order-independent
-//    -> deterministic) AND the number of K-split contributions; a consumer
-//    polls exactly the words of its K range until each shows count == ks of
-//    the producing layer, then rounds them to fp16 x (as FASQ_FLAG_X_ACC).
-//    One L2 round trip after the data is final instead of a barrier round
-//    trip plus a load round trip.
+//    -> deterministic) AND the number of contributions; a consumer polls
+//    exactly the words it needs until each shows the producer's count.
 //
-// Numerics are identical to chaining fasq_gemv_grouped calls with FASQ_ACC_I64
-// outputs (same fixed-point units and rounding).
+// Besides PQ GEMV steps the kernel runs the non-linear glue of a decoder
+// block (whole-model decode, llama.cu): an EMBED step (the embedding row of
+// the token the previous run's lm_head chose), RMSNorm and SwiGLU as input
+// transforms of a PQ step, the residual connection fused into the PQ epilogue
+// (an exact integer add of the residual words), and an ATTN step (RoPE,
+// KV-cache append, softmax attention, split over the cache length).
+//
+// Cross-run / cross-rank protocol (tail words of the arena allocation):
+//  * run index r = (CTA entry counter) / nctas; parity r & 1 selects the
+//    arena buffer the run accumulates into; the run zeroes the other buffer
+//    for run r+1 (no memset node, graph replays need no host bookkeeping);
+//  * world > 1: a rank starts zeroing only after EVERY rank finished run r-1
+//    (each rank adds 1 to every rank's DONE word when its last CTA exits),
+//    so a slow peer's late stores can never hit a zeroed buffer and a fast
+//    peer can never write into a buffer before it was zeroed.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -32,32 +43,8 @@
 #include <string>
 #include <vector>
 
-#include "fasq_internal.cuh"
+#include "chain_internal.cuh"
 #include "gemv_core.cuh"
-
-struct fasq_chain {
-    int n_steps = 0, B = 0, d = 0, nctas = 0;
-    int world = 1, rank = 0;                         // row-sharded tensor parallelism (fasq_chain_create_tp)
-    int rw = 0, nw = 0, st = 0, R = 0, gmax = 1, maxC = 1, mi = 1;
-    size_t smem = 0;
-    std::vector<std::vector<int64_t>> acc_off;       // per step, per layer: word offset in one arena buffer
-    std::vector<std::vector<int64_t>> acc_Fout;      // per step, per layer: GLOBAL F_out (words per batch row)
-    std::vector<std::vector<int>> acc_ks;            // per step, per layer: K-split count (contributions per word)
-    std::vector<int> step_F_in;
-    int ext_F_in = 0;
-    // two arena buffers (ONE allocation, IPC-exportable): run n accumulates into
-    // buffer parity(n) on every rank and zeroes its own buffer parity(n)^1 for
-    // run n+1 -- no memset node, no host round trip between tokens
-    unsigned long long* arenas = nullptr;
-    int64_t arena_words = 0;                         // words per buffer
-    unsigned* ctrl = nullptr;                        // device: [0] parity, [1] unused, [2] monotonic CTA entry counter
-    unsigned long long** peers_dev = nullptr;        // device [world]: every rank's `arenas` (own rank = local)
-    std::vector<void*> ipc_opened;                   // peer mappings opened by fasq_chain_set_peers
-    bool peers_ready = true;
-    void* items = nullptr;                           // device [n_steps][nctas] ChainItem
-    void* phases = nullptr;                          // device [n_steps] ChainPhase
-    unsigned long long* trace = nullptr;             // user buffer (fasq_chain_trace), not owned
-};
 
 namespace fasq {
 
@@ -67,15 +54,35 @@ struct ChainItem {
     const uint8_t* idx;
     const uint8_t* cbimg;
     const void* cbmap;          // d <= 2: 3-D tensor map {32 words, n_groups, C} over cbimg (pair boxes)
-    long long y_off;            // word offset of the layer's counted-accumulator output [B][F_out_g] in a buffer
-    int F_out, F_out_g, row0_g; // local rows of this rank's shard, global F_out, global row of local row 0
+    long long y_off;            // word offset of the output [B][ld] in a buffer
+    int F_out, ld, row0_g;      // local rows, words per batch row of the output, output index of local row 0
     int F_out_pad, N_ss, C;
     int r0, rows_valid, g_begin, g_end;
+    int kidx;                   // PQ: K-range index in its row tile (0 adds the residual); ATTN: cache part
+    int head;                   // ATTN: local q head
+    int kind;                   // -1: no item
 };
 
 struct ChainPhase {
-    long long x_off;            // word offset of the counted-accumulator input (< 0: the external fp16 x)
-    int F_in, x_ks;             // x_ks: contributions per input word (K-split of the producer)
+    int kind, in_mode, F_in;
+    long long x_off, x2_off;    // input words (WORDS/NORM: x; SILU: gate x, up x2)
+    int x_ks, x2_ks;
+    int x_sys;                  // input words written by peers (system-scope polls)
+    const __half* gamma;
+    float eps;
+    long long res_off;          // residual words (< 0: none), same [B][ld] indexing as the output
+    int res_ks, res_here, res_sys;
+    int out_all;                // outputs red.add'ed into every rank's arena
+    // ATTN
+    long long q_off, k_off, v_off, o_off;
+    int q_ks, k_ks, v_ks, q_ld, kv_ld, o_ld;
+    __half* kc;
+    __half* vc;
+    int n_heads, n_kv, hd, parts;
+    // EMBED
+    const __half* embed;
+    long long e_off;
+    int hidden;
 };
 
 struct ChainParams {
@@ -83,8 +90,7 @@ struct ChainParams {
     const ChainPhase* phases;
     const __half* x_ext;        // [B][F_in of the first step]
     unsigned long long* trace;  // optional [n_steps][nctas][4] globaltimer stamps (fasq_chain_trace)
-    unsigned* ctrl;             // [0] parity, [2] CTA entry counter
-    unsigned long long* const* peers;   // [world] arena bases (2 buffers each); peers[rank] = local
+    unsigned long long* const* peers;   // [world] allocation bases (2 buffers + tail each); peers[rank] = local
     long long arena_words;      // words per buffer
     int world, rank;
     int n_steps, nctas, B, gmax, cbb_max;
@@ -94,18 +100,251 @@ struct ChainParams {
     int dbg;                    // experiments only (FASQ_CHAIN_DBG): bit 0 = consumers skip the gather
                                 // loop, bit 1 = producer skips the copies (compute on stale SMEM),
                                 // bit 2 = producer skips the codebook copies only
+    // model (llama.cu)
+    int model;
+    const float2* rope;
+    int max_T, pos_wrap;
+    int* tok_hist;
+    long long tok_expect;
+    float* part_buf;
+    unsigned* part_cnt;
 };
 
-// d <= 2 (4-B codebook entries) runs on codebook PAIR stages: a separate
-// CS-deep ring of [C][2][32]-word slots, each filled by ONE 3-D TMA box that
-// interleaves groups g and g+1 of the [group][C][32] image into 256-B k-rows
-// (core::compute_group_pair: the gather address is one PRMT).  The index
-// chunks keep their own ST-deep ring (one group per stage).
 template <int D>
 struct ChainPair {
     static constexpr bool value = D <= 2;
 };
 constexpr int kChainCS = kPairSlots;
+
+__device__ __forceinline__ void consumer_bar(int nt) { asm volatile("bar.sync 1, %0;" :: "r"(nt) : "memory"); }
+
+__device__ __forceinline__ unsigned long long cnt_word(long long v) {
+    return (1ull << core::kCntShift) + (unsigned long long)(core::kCntBias + v);
+}
+
+// ---- EMBED: h0[b] = embed[token_b] as counted words (count 1) ---------------
+// token_b = the key the previous run's lm_head red.max'ed into token slot
+// (par_prev, b), once all its contributions arrived; the slot is cleared for
+// the run after next and the token is appended to the history.
+__device__ __noinline__ void embed_item(const ChainPhase* ph, unsigned long long* cur, unsigned long long* tail,
+                                        int B, unsigned run, int pos, int max_T, int* tok_hist,
+                                        long long tok_expect, int NT, int* s_tok) {
+    const int tid = threadIdx.x;
+    const unsigned pp = (run - 1u) & 1u;
+    if (tid < B) {
+        unsigned long long* slot = tail + T_TOK + (pp * 8 + tid) * 2;
+        unsigned long long cnt;
+        const unsigned long long t0 = dev::globaltimer();
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(cnt) : "l"(slot + 1) : "memory");
+            if (dev::globaltimer() - t0 > 4000000000ull) __trap();
+        } while ((long long)cnt != tok_expect);
+        unsigned long long key;
+        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(key) : "l"(slot) : "memory");
+        const unsigned tok = tok_of_key(key);
+        s_tok[tid] = (int)tok;
+        tok_hist[(size_t)tid * max_T + pos] = (int)tok;
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(slot), "l"(0ull) : "memory");
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(slot + 1), "l"(0ull) : "memory");
+    }
+    consumer_bar(NT);
+    const int n = ph->hidden;
+    for (int i = tid; i < B * n; i += NT) {
+        const int b = i / n, c = i - b * n;
+        const float v = __half2float(ph->embed[(size_t)s_tok[b] * n + c]);
+        const long long q = __float2ll_rn(v * core::kAccScale);
+        asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(cur + ph->e_off + i), "l"(cnt_word(q)) : "memory");
+    }
+}
+
+// ---- ATTN: one (local q head, cache part) item ------------------------------
+// Llama attention for the token at `pos` (HF LlamaAttention semantics):
+// RoPE (rotate-half, cos/sin table) on q and k, the new fp16 k/v appended to
+// the KV cache at pos (by the first q head of each KV group), scores
+// q.k_t / sqrt(hd) over t <= pos, softmax, o = sum_t p_t v_t.  The cache
+// length is split into `parts` ranges over CTAs; each writes (max, sum,
+// unnormalised o) partials and the last of a head's parts to arrive merges
+// them in FIXED part order (deterministic) into counted output words.
+// scr: >= 48 KiB of SMEM scratch (a codebook pair slot handed over by the producer).
+__device__ __noinline__ void attn_item(const ChainPhase* ph, int head, int part, unsigned long long* cur, int B,
+                                       int pos, int max_T, const float2* rope, float* part_buf, unsigned* part_cnt,
+                                       float* scr, int NT, bool sys, unsigned* s_last) {
+    const int tid = threadIdx.x;
+    const int hd = ph->hd, half = hd / 2;
+    const int n_heads = ph->n_heads, n_kv = ph->n_kv, P = ph->parts;
+    const int grp = n_heads / n_kv, kvh = head / grp;
+    const int Tn = pos + 1;
+    const int t0 = (int)((long long)part * Tn / P), t1 = (int)((long long)(part + 1) * Tn / P);
+    const int nrow = t1 - t0;
+    const float qk_scale = 1.0f / sqrtf((float)hd);
+    float* s_q = scr;                 // [hd] raw q, then rotated q
+    float* s_k = s_q + 256;           // [hd] raw k
+    float* s_v = s_k + 256;           // [hd] raw v
+    __half* s_kn = reinterpret_cast<__half*>(s_v + 256);   // [hd] new k (rotated, fp16)
+    __half* s_vn = s_kn + 256;                              // [hd] new v (fp16)
+    float* s_red = reinterpret_cast<float*>(s_vn + 256);    // [32][hd] row-group partials of o (16 KiB at hd=128)
+    float* s_sc = s_red + 32 * 256;                         // [nrow] scores / probabilities
+    float* s_w = s_sc + ((nrow + 3) & ~3);                  // [32] block-reduction scratch
+    const int nwarp = NT / 32, lane = tid & 31, warp = tid >> 5;
+    for (int b = 0; b < B; ++b) {
+        // 1. q (this head), k and v (its KV head) from the counted words
+        if (tid < 3 * hd) {
+            const int which = tid / hd, e = tid - which * hd;
+            const unsigned long long* a =
+                which == 0 ? cur + ph->q_off + (size_t)b * ph->q_ld + (size_t)head * hd + e
+                           : cur + (which == 1 ? ph->k_off : ph->v_off) + (size_t)b * ph->kv_ld + (size_t)kvh * hd + e;
+            const int ks = which == 0 ? ph->q_ks : which == 1 ? ph->k_ks : ph->v_ks;
+            const float f = (float)((double)core::poll_value(a, ks, sys) * core::kAccInv);
+            (which == 0 ? s_q : which == 1 ? s_k : s_v)[e] = f;
+        }
+        consumer_bar(NT);
+        // 2. RoPE (rotate half): x'[i] = x[i] c - x[i+half] s, x'[i+half] = x[i+half] c + x[i] s
+        float qr0 = 0.f, qr1 = 0.f;
+        if (tid < half) {
+            const float2 cs = rope[(size_t)pos * half + tid];
+            const float q0 = s_q[tid], q1 = s_q[tid + half], k0 = s_k[tid], k1 = s_k[tid + half];
+            qr0 = q0 * cs.x - q1 * cs.y;
+            qr1 = q1 * cs.x + q0 * cs.y;
+            s_kn[tid] = __float2half_rn(k0 * cs.x - k1 * cs.y);
+            s_kn[tid + half] = __float2half_rn(k1 * cs.x + k0 * cs.y);
+        }
+        if (tid < hd) s_vn[tid] = __float2half_rn(s_v[tid]);
+        consumer_bar(NT);
+        if (tid < half) { s_q[tid] = qr0; s_q[tid + half] = qr1; }
+        __half* kc = ph->kc + ((size_t)b * n_kv + kvh) * (size_t)max_T * hd;
+        __half* vc = ph->vc + ((size_t)b * n_kv + kvh) * (size_t)max_T * hd;
+        // 3. cache append at pos (one writer per KV head: the group's first q head, last part)
+        if (head % grp == 0 && t1 == Tn && tid < hd) {
+            kc[(size_t)pos * hd + tid] = s_kn[tid];
+            vc[(size_t)pos * hd + tid] = s_vn[tid];
+        }
+        consumer_bar(NT);
+        // 4. scores: thread (row group r = tid / 16, chunk c = tid % 16 of 8 dims)
+        const int nch = hd / 8;          // 16-B chunks per row (hd <= 128 -> <= 16)
+        const int rpi = NT / 16;         // rows per iteration (32 with 512 threads)
+        const int c = tid & 15, r = tid >> 4;
+        float qv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) qv[i] = c < nch ? s_q[c * 8 + i] : 0.f;
+        for (int base = 0; base < nrow; base += 4 * rpi) {
+            uint4 kv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = t0 + base + r + u * rpi;
+                kv[u] = make_uint4(0u, 0u, 0u, 0u);
+                if (c < nch && t < t1)
+                    kv[u] = t == pos ? *reinterpret_cast<const uint4*>(s_kn + c * 8)
+                                     : __ldcg(reinterpret_cast<const uint4*>(kc + (size_t)t * hd + c * 8));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const __half* kh = reinterpret_cast<const __half*>(&kv[u]);
+                float dsum = 0.f;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) dsum += qv[i] * __half2float(kh[i]);
+#pragma unroll
+                for (int m = 8; m >= 1; m >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, m);
+                const int t = t0 + base + r + u * rpi;
+                if (c == 0 && t < t1) s_sc[t - t0] = dsum * qk_scale;
+            }
+        }
+        consumer_bar(NT);
+        // 5. max and sum (fixed order: strided per thread, warp butterfly, warps in order)
+        float mx = -INFINITY;
+        for (int i = tid; i < nrow; i += NT) mx = fmaxf(mx, s_sc[i]);
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, m));
+        if (lane == 0) s_w[warp] = mx;
+        consumer_bar(NT);
+        mx = -INFINITY;
+        for (int w = 0; w < nwarp; ++w) mx = fmaxf(mx, s_w[w]);
+        float sm = 0.f;
+        for (int i = tid; i < nrow; i += NT) {
+            const float pe = expf(s_sc[i] - mx);
+            s_sc[i] = pe;
+            sm += pe;
+        }
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, m);
+        consumer_bar(NT);
+        if (lane == 0) s_w[warp] = sm;
+        consumer_bar(NT);
+        float l = 0.f;
+        for (int w = 0; w < nwarp; ++w) l += s_w[w];
+        // 6. o partials: thread (r, c) sums rows t0 + r + k*rpi for its 8 dims
+        float o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = 0.f;
+        for (int base = 0; base < nrow; base += 4 * rpi) {
+            uint4 vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = t0 + base + r + u * rpi;
+                vv[u] = make_uint4(0u, 0u, 0u, 0u);
+                if (c < nch && t < t1)
+                    vv[u] = t == pos ? *reinterpret_cast<const uint4*>(s_vn + c * 8)
+                                     : __ldcg(reinterpret_cast<const uint4*>(vc + (size_t)t * hd + c * 8));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = t0 + base + r + u * rpi;
+                if (t >= t1) continue;
+                const float pt = s_sc[t - t0];
+                const __half* vh = reinterpret_cast<const __half*>(&vv[u]);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o[i] += pt * __half2float(vh[i]);
+            }
+        }
+        if (c < nch) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s_red[r * hd + c * 8 + i] = o[i];
+        }
+        consumer_bar(NT);
+        if (tid < hd) {
+            float od = 0.f;
+            for (int rr = 0; rr < rpi; ++rr) od += s_red[rr * hd + tid];
+            if (P == 1) {
+                const long long q = __float2ll_rn(od / l * core::kAccScale);
+                asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;"
+                             :: "l"(cur + ph->o_off + (size_t)b * ph->o_ld + (size_t)head * hd + tid), "l"(cnt_word(q))
+                             : "memory");
+            } else {
+                float* pb = part_buf + (((size_t)head * P + part) * B + b) * (hd + 2);
+                __stcg(pb + tid, od);
+                if (tid == 0) { __stcg(pb + hd, mx); __stcg(pb + hd + 1, l); }
+            }
+        }
+        consumer_bar(NT);
+    }
+    if (P == 1) return;
+    // last part of this head to arrive merges all parts in fixed order
+    if (tid == 0) {
+        __threadfence();
+        unsigned old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(part_cnt + head) : "memory");
+        *s_last = ((old + 1u) & (unsigned)(P - 1)) == 0u;   // P is a power of two (2^32 % P == 0)
+    }
+    consumer_bar(NT);
+    if (!*s_last) return;
+    for (int b = 0; b < B; ++b) {
+        if (tid < hd) {
+            float M = -INFINITY;
+            for (int q = 0; q < P; ++q) M = fmaxf(M, __ldcg(part_buf + (((size_t)head * P + q) * B + b) * (hd + 2) + hd));
+            float L = 0.f, od = 0.f;
+            for (int q = 0; q < P; ++q) {
+                const float* pb = part_buf + (((size_t)head * P + q) * B + b) * (hd + 2);
+                const float m_q = __ldcg(pb + hd);
+                const float f = m_q == -INFINITY ? 0.f : expf(m_q - M);
+                L += f * __ldcg(pb + hd + 1);
+                od += f * __ldcg(pb + tid);
+            }
+            const long long q = __float2ll_rn(od / L * core::kAccScale);
+            asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;"
+                         :: "l"(cur + ph->o_off + (size_t)b * ph->o_ld + (size_t)head * hd + tid), "l"(cnt_word(q))
+                         : "memory");
+        }
+    }
+}
 
 template <int D, int NB, int NW, int ST>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
@@ -118,15 +357,23 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     constexpr bool XF = PAIR && NB == 8;               // x staged as fp32 (FFMA2 path, compute_group_set)
     constexpr int XG = XF ? 32 * NB * D * 4 : 32 * NB * E;
     constexpr int CS = kChainCS;
+    constexpr int NT = NW * 32;                        // consumer threads
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* s_cb = smem;                                       // PAIR: CS * 64 KiB, else ST * cbb_max
     uint8_t* s_idx = s_cb + (PAIR ? CS * kPairSlot : ST * p.cbb_max);   // ST * R * 32
     uint8_t* s_x = s_idx + ST * R * 32;                         // gmax * XG
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_x + p.gmax * XG);
-    const uint32_t cb_u = dev::smem_u32(s_cb), idx_u = dev::smem_u32(s_idx), x_u = dev::smem_u32(s_x);
+    float* s_red = reinterpret_cast<float*>(bars + 2 * (ST + CS));   // [NW][8] norm reduction scratch
+    float* s_scale = s_red + NW * 8;                                 // [8] RMSNorm scales
+    int* s_tok = reinterpret_cast<int*>(s_scale + 8);                // [8] EMBED tokens
+    unsigned& s_run = *reinterpret_cast<unsigned*>(s_tok + 8);       // run index
+    int& s_pos = *reinterpret_cast<int*>(s_tok + 9);                 // model position
+    unsigned* s_flag = reinterpret_cast<unsigned*>(s_tok + 10);      // attention merge flag
+    const uint32_t cb_u = dev::smem_u32(s_cb), idx_u = dev::smem_u32(s_idx);
     const uint32_t full0 = dev::smem_u32(&bars[0]), empty0 = dev::smem_u32(&bars[ST]);
     const uint32_t cfull0 = dev::smem_u32(&bars[2 * ST]), cempty0 = dev::smem_u32(&bars[2 * ST + CS]);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long* const tail = p.peers[p.rank] + 2 * p.arena_words;
 
     if (threadIdx.x == 0) {
 #pragma unroll
@@ -152,13 +399,22 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             for (int phj = 0; phj < p.n_steps * p.mi; ++phj) {
                 const int ph = phj / p.mi;
                 const ChainItem& w = p.items[((size_t)ph * p.nctas + blockIdx.x) * p.mi + phj % p.mi];
-                if (w.rows_valid <= 0) continue;
+                if (w.kind == SK_ATTN) {
+                    if (PAIR) {   // hand a pair slot to the consumers as attention scratch
+                        const int cs = cit % CS;
+                        if (cit >= CS) dev::mbar_wait(cempty0 + 8 * cs, ((cit / CS) + 1) & 1);
+                        dev::mbar_arrive(cfull0 + 8 * cs);
+                        ++cit;
+                    }
+                    continue;
+                }
+                if (w.kind != SK_PQ || w.rows_valid <= 0) continue;
                 const uint32_t cbb = (uint32_t)w.C * 32u * E;
                 const uint32_t chunk = (uint32_t)w.rows_valid * 32u;
                 if (p.pf > 0 && ph + 1 < p.n_steps && phj % p.mi == 0) {
                     // warm L2 with the head of the next step's first item
                     const ChainItem& nw = p.items[((size_t)(ph + 1) * p.nctas + blockIdx.x) * p.mi];
-                    if (nw.rows_valid > 0) {
+                    if (nw.kind == SK_PQ && nw.rows_valid > 0) {
                         const int ge = min(nw.g_end, nw.g_begin + p.pf);
                         for (int g = nw.g_begin; g < ge; ++g)
                             dev::bulk_prefetch_l2(nw.idx + ((size_t)g * nw.F_out_pad + nw.r0) * 32,
@@ -195,38 +451,39 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         return;
     }
 
-    // ---- run prologue: arena parity, zero the other buffer for the next run ----
-    __shared__ unsigned s_par, s_target;
+    // ---- run prologue ----
     if (threadIdx.x == 0) {
-        unsigned par, old;
-        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(par) : "l"(p.ctrl) : "memory");
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.ctrl + 2) : "memory");
-        s_par = par & 1u;
-        s_target = (old / (unsigned)p.nctas + 1u) * (unsigned)p.nctas;
+        unsigned long long old;
+        asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(tail + T_ENTRY) : "memory");
+        const unsigned run = (unsigned)(old / (unsigned long long)p.nctas);
+        s_run = run;
+        if (p.world > 1) {
+            // every rank finished run - 1 (its stores into our buffers landed) before we zero
+            const unsigned long long want = (unsigned long long)p.world * run, t0 = dev::globaltimer();
+            unsigned long long v;
+            for (;;) {
+                asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(tail + T_DONE) : "memory");
+                if (v >= want) break;
+                if (dev::globaltimer() - t0 > 4000000000ull) __trap();
+            }
+        }
+        if (p.model) {
+            unsigned long long v;
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(tail + T_POS) : "memory");
+            s_pos = (int)v;
+        }
     }
-    asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
-    const unsigned par = s_par;
+    consumer_bar(NT);
+    const unsigned run = s_run;
+    const unsigned par = run & 1u;
     unsigned long long* const cur = p.peers[p.rank] + (long long)par * p.arena_words;   // this run's buffer
     {
         unsigned long long* nxt = p.peers[p.rank] + (long long)(par ^ 1u) * p.arena_words;
         const long long per = (p.arena_words + p.nctas - 1) / p.nctas;
         const long long zb = per * blockIdx.x, ze = min(p.arena_words, zb + per);
-        for (long long i = zb + threadIdx.x; i < ze; i += NW * 32) nxt[i] = 0ull;
+        for (long long i = zb + threadIdx.x; i < ze; i += NT) nxt[i] = 0ull;
     }
-    if (p.world > 1) {
-        // peers write into our next buffer only after they consumed this run's
-        // data; make the zeros visible system-wide and let every local CTA
-        // finish zeroing before any of this rank's outputs leave the GPU
-        __threadfence_system();
-        asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
-        if (threadIdx.x == 0) {
-            unsigned v;
-            do {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ctrl + 2) : "memory");
-            } while ((int)(v - s_target) < 0);
-        }
-        asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
-    }
+    const bool sys_out = p.world > 1;
 
     const int wrow0 = warp * RW;
     const auto co = core::chunk_offsets<RW>(wrow0, lane);
@@ -235,37 +492,65 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     uint32_t par_ring = 0;   // its mbarrier phase parity
     int cslot = 0;           // PAIR: codebook pair slot and parity
     uint32_t cpar = 0;
-    // PAIR gather constant = PRMT operand b: byte 0 = h*128 + 4*sigma, byte 2 =
-    // pair slot (64 KiB stride), so the address is PRMT(idx word, lbv) + the
-    // ring base (uniform) -> LDS [R + UR] (gemv_core.cuh compute_group_set)
     for (int phj = 0; phj < p.n_steps * p.mi; ++phj) {
         const int ph = phj / p.mi, j = phj % p.mi;
-        // the work item and phase are read-only for the kernel's lifetime
         const ChainItem w = p.items[((size_t)ph * p.nctas + blockIdx.x) * p.mi + j];
-        const ChainPhase phs = p.phases[ph];
-        // trace: t0 at the step's first item, t1/t2 of its first item, t3 after its last
+        const ChainPhase* phs = p.phases + ph;
         unsigned long long* tr = p.trace ? p.trace + ((size_t)ph * p.nctas + blockIdx.x) * 4 : nullptr;
         if (tr && threadIdx.x == 0 && j == 0) tr[0] = dev::globaltimer();
-        if (w.rows_valid <= 0) continue;
-        // every consumer warp is done with the previous step's s_x
-        asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
+        if (w.kind < 0) continue;
+        // every consumer warp is done with the previous item's SMEM
+        consumer_bar(NT);
+        if (w.kind == SK_EMBED) {
+            embed_item(phs, cur, tail, p.B, run, s_pos, p.max_T, p.tok_hist, p.tok_expect, NT, s_tok);
+            if (tr && lane == 0 && warp == 0) { tr[1] = tr[2] = tr[3] = dev::globaltimer(); }
+            continue;
+        }
+        if (w.kind == SK_ATTN) {
+            if constexpr (PAIR) {
+                dev::mbar_wait(cfull0 + 8 * cslot, cpar);
+                if (tr && threadIdx.x == 0 && j == 0) tr[1] = tr[2] = dev::globaltimer();
+                attn_item(phs, w.head, w.kidx, cur, p.B, s_pos, p.max_T, p.rope, p.part_buf, p.part_cnt,
+                          reinterpret_cast<float*>(s_cb + (size_t)cslot * kPairSlot), NT, false, s_flag);
+                __syncwarp();
+                if (lane == 0) dev::mbar_arrive(cempty0 + 8 * cslot);
+                if (++cslot == CS) { cslot = 0; cpar ^= 1u; }
+            }
+            if (tr && lane == 0 && warp == 0) tr[3] = dev::globaltimer();
+            continue;
+        }
         const int ng = w.g_end - w.g_begin;
-        if (phs.x_off >= 0)   // dataflow wait: poll this CTA's input words until final
-            core::stage_x_counted<D, NB, NW, XF>(s_x, cur + phs.x_off, phs.x_ks, phs.F_in, p.B, w.N_ss, w.g_begin,
-                                                 ng, p.world > 1, p.backoff);
-        else
-            core::stage_x<D, NB, NW, XF>(s_x, p.x_ext, 0, phs.F_in, p.B, w.N_ss, w.g_begin, ng);
+        const int in_mode = phs->in_mode;
+        const bool xsys = phs->x_sys != 0;
+        if (in_mode == IN_EXT) {
+            core::stage_x<D, NB, NW, XF>(s_x, p.x_ext, 0, phs->F_in, p.B, w.N_ss, w.g_begin, ng);
+        } else if (in_mode == IN_WORDS) {
+            core::stage_x_counted<D, NB, NW, XF>(s_x, cur + phs->x_off, phs->x_ks, phs->F_in, p.B, w.N_ss, w.g_begin,
+                                                 ng, xsys, p.backoff);
+        } else if constexpr (PAIR) {
+            if (in_mode == IN_RMSNORM) {
+                core::norm_scale<NB, NW>(cur + phs->x_off, phs->x_ks, phs->F_in, p.B, phs->eps, xsys, s_red, s_scale);
+                core::stage_x_counted<D, NB, NW, XF, core::XM_NORM>(s_x, cur + phs->x_off, phs->x_ks, phs->F_in, p.B,
+                                                                    w.N_ss, w.g_begin, ng, xsys, 0, nullptr, 0,
+                                                                    s_scale, phs->gamma);
+            } else {
+                core::stage_x_counted<D, NB, NW, XF, core::XM_SILU>(s_x, cur + phs->x_off, phs->x_ks, phs->F_in, p.B,
+                                                                    w.N_ss, w.g_begin, ng, xsys, 0,
+                                                                    cur + phs->x2_off, phs->x2_ks);
+            }
+        }
         if (tr && threadIdx.x == 0 && j == 0) tr[1] = dev::globaltimer();
-        asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
+        consumer_bar(NT);
         if (tr && threadIdx.x == 0 && j == 0) tr[2] = dev::globaltimer();
         const bool active = wrow0 < w.rows_valid;
+        unsigned long long* const ovf = tail + T_OVF;
         if constexpr (PAIR) {
             // pair stages: row-set mapping (gemv_core.cuh), 2G*NB accumulators
             // per lane, G-lane row reduction
             float acc[2 * G * NB];
 #pragma unroll
             for (int q = 0; q < 2 * G * NB; ++q) acc[q] = 0.f;
-            const bool run = active && !(p.dbg & 1);
+            const bool run_loop = active && !(p.dbg & 1);
             for (int i = 0; i < ng; i += 2) {
                 dev::mbar_wait(cfull0 + 8 * cslot, cpar);
                 const uint32_t lbs = (uint32_t)cslot << 16;
@@ -273,7 +558,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                 for (int h = 0; h < 2; ++h) {
                     if (h == 1 && i + 1 >= ng) break;
                     dev::mbar_wait(full0 + 8 * slot, par_ring);
-                    if (run)
+                    if (run_loop)
                         core::compute_group_set<D, NB, G>(acc, s_idx + slot * R * 32, qm, s_cb,
                                                           lbs + ((uint32_t)h << 7), s_x + (i + h) * XG);
                     __syncwarp();
@@ -285,58 +570,74 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             }
             core::reduce_set<NB, G>(acc, lane);
             if (active) {
+                const bool add_res = phs->res_off >= 0 && phs->res_here && w.kidx == 0;
+                long long qv[2 * NB];
                 const long long off = (long long)par * p.arena_words + w.y_off + w.row0_g;
-                for (int q = 0; q < p.world; ++q)
-                    core::counted_store_set<NB, G>(acc, p.peers[q] + off, w.r0 + wrow0, lane, w.F_out, w.F_out_g,
-                                                   p.B, p.world > 1);
+                core::set_values<NB, G>(acc, qv, w.r0 + wrow0, lane, w.F_out, p.B,
+                                        add_res ? cur + phs->res_off + w.row0_g : nullptr, w.ld, phs->res_ks,
+                                        phs->res_sys != 0, ovf);
+                if (phs->out_all) {
+                    for (int q = 0; q < p.world; ++q)
+                        core::counted_store_q<NB>(qv, p.peers[q] + off, w.r0 + wrow0, lane, w.F_out, w.ld, p.B,
+                                                  sys_out);
+                } else {
+                    core::counted_store_q<NB>(qv, p.peers[p.rank] + off, w.r0 + wrow0, lane, w.F_out, w.ld, p.B,
+                                              false);
+                }
             }
         } else {
-        float acc[RW][NB];
+            float acc[RW][NB];
 #pragma unroll
-        for (int q = 0; q < RW; ++q)
+            for (int q = 0; q < RW; ++q)
 #pragma unroll
-            for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
-        {   // d = 4, 8: lane = subspace over 64/B rows per warp
+                for (int b = 0; b < NB; ++b) acc[q][b] = 0.f;
+            // d = 4, 8: lane = subspace over 64/B rows per warp
             for (int i = 0; i < ng; ++i) {
                 dev::mbar_wait(full0 + 8 * slot, par_ring);
                 if (active && !(p.dbg & 1)) {
                     uint32_t xv[NB][E / 4];
                     core::load_x<D, NB>(xv, s_x + i * XG, lane);
-                    core::compute_group<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb + slot * p.cbb_max, xv,
-                                                   lane);
+                    core::compute_group<D, NB, RW>(acc, s_idx + slot * R * 32, co, s_cb + slot * p.cbb_max, xv, lane);
                 }
                 __syncwarp();
                 if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
                 if (++slot == ST) { slot = 0; par_ring ^= 1u; }
             }
-        }
-        core::RowTotals<NB, RW> tot;
-        core::reduce_rows<NB, RW>(acc, tot, lane);
-        if (active) {
-            // this rank's rows go into EVERY rank's buffer (NVLink peer stores
-            // when world > 1): the row-shard all-gather fused into the GEMV
-            const long long off = (long long)par * p.arena_words + w.y_off + w.row0_g;
-            for (int q = 0; q < p.world; ++q)
-                core::counted_store<NB, RW>(tot, p.peers[q] + off, w.r0 + wrow0, w.F_out, w.F_out_g, p.B);
-        }
+            core::RowTotals<NB, RW> tot;
+            core::reduce_rows<NB, RW>(acc, tot, lane);
+            if (active) {
+                const long long off = (long long)par * p.arena_words + w.y_off + w.row0_g;
+                const int nq = phs->out_all ? p.world : 1;
+                for (int q = 0; q < nq; ++q)
+                    core::counted_store<NB, RW>(tot, p.peers[phs->out_all ? q : p.rank] + off, w.r0 + wrow0, w.F_out,
+                                                w.ld, p.B, ovf);
+            }
         }
         if (tr && lane == 0 && warp == 0) tr[3] = dev::globaltimer();
     }
-    // ---- run epilogue: flip the parity once every CTA has read it ----
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        unsigned v;
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ctrl + 2) : "memory");
-        } while ((int)(v - s_target) < 0);
-        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" :: "l"(p.ctrl), "r"(par ^ 1u) : "memory");
+    // ---- run epilogue: exit count; the last CTA publishes the run to every rank ----
+    consumer_bar(NT);
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        unsigned long long old;
+        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(tail + T_EXIT) : "memory");
+        if (old + 1 == (unsigned long long)(run + 1) * (unsigned long long)p.nctas) {
+            if (p.model) {
+                const int np = s_pos + 1 < p.max_T ? s_pos + 1 : p.pos_wrap;
+                asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(tail + T_POS), "l"((unsigned long long)np)
+                             : "memory");
+            }
+            __threadfence_system();
+            for (int q = 0; q < p.world; ++q) {
+                unsigned long long* dn = p.peers[q] + 2 * p.arena_words + T_DONE;
+                asm volatile("red.release.sys.global.add.u64 [%0], %1;" :: "l"(dn), "l"(1ull) : "memory");
+            }
+        }
     }
 }
 
 constexpr size_t kChainSmem = kSmemMax;
-
-struct ChainCfg {
-    int rw, nw, st;
-};
+constexpr size_t kChainScratch = 16 * 8 * 4 + 128;   // s_red, s_scale, s_tok, run/pos/flag words (after the mbarriers)
 
 template <int D, int NB, int NW, int ST>
 fasq_status launch_chain_t(const ChainParams& p, size_t smem, int grid, cudaStream_t st) {
@@ -390,33 +691,29 @@ fasq_status chain_nb(const fasq_chain* c, const ChainParams& p, cudaStream_t st)
 }
 
 // counted accumulator words of the LAST run -> value (units 2^-32) -> fp16 /
-// fp32 / FASQ_ACC_I64.  The run flipped the parity at its end, so its buffer
-// is parity ^ 1 (read on the device: graph replays need no host bookkeeping).
-__global__ void k_counted_convert(const unsigned long long* __restrict__ arenas, long long arena_words,
-                                  const unsigned* __restrict__ ctrl, long long off, int64_t n, int ks, void* out,
-                                  int dtype) {
+// fp32 / FASQ_ACC_I64.  The last run is (entry counter / nctas) - 1 (read on
+// the device: graph replays need no host bookkeeping).  Every word is polled
+// until it carries its `ks` contributions (peers' red.adds of the last step
+// may still be in flight when this rank's kernel ends).  A run that raised
+// the out-of-range flag yields NaN (float outputs).
+__global__ void k_counted_convert(const unsigned long long* __restrict__ arenas, long long arena_words, int nctas,
+                                  long long off, int64_t n, int ks, void* out, int dtype, int sys) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const unsigned last = (ctrl[0] & 1u) ^ 1u;
-    const unsigned long long wv = arenas[(long long)last * arena_words + off + i];
-    const long long v = (long long)(wv & core::kCntMask) - (long long)ks * core::kCntBias;
+    const unsigned long long* tail = arenas + 2 * arena_words;
+    const unsigned long long runs = tail[T_ENTRY] / (unsigned long long)nctas;
+    const unsigned last = (unsigned)((runs + 1ull) & 1ull);   // parity of run (runs - 1)
+    const long long v = core::poll_value(arenas + (long long)last * arena_words + off + i, ks, sys != 0);
+    const bool bad = tail[T_OVF] != 0ull;
     if (dtype == FASQ_ACC_I64) reinterpret_cast<long long*>(out)[i] = v;
-    else if (dtype == FASQ_F32) reinterpret_cast<float*>(out)[i] = (float)((double)v * core::kAccInv);
-    else reinterpret_cast<__half*>(out)[i] = __double2half((double)v * core::kAccInv);
-}
-
-int sm_count() {
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n > 0 ? n : 148;
+    else if (dtype == FASQ_F32) reinterpret_cast<float*>(out)[i] = bad ? __int_as_float(0x7fc00000) : (float)((double)v * core::kAccInv);
+    else reinterpret_cast<__half*>(out)[i] = bad ? __ushort_as_half((unsigned short)0x7e00) : __double2half((double)v * core::kAccInv);
 }
 
 void destroy_chain(fasq_chain* c) {
     if (!c) return;
     for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
     if (c->arenas) cudaFree(c->arenas);
-    if (c->ctrl) cudaFree(c->ctrl);
     if (c->peers_dev) cudaFree(c->peers_dev);
     if (c->items) cudaFree(c->items);
     if (c->phases) cudaFree(c->phases);
@@ -431,6 +728,386 @@ fasq_status upload_peers(fasq_chain* c, const std::vector<unsigned long long*>& 
 
 }  // namespace
 
+int sm_count() {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+
+// ---- planner (host only) ------------------------------------------------------
+// K-split count per layer of one step: every layer's work (row tiles x groups)
+// gets a share of the `nctas` CTAs proportional to its index bytes; a layer
+// with rt row tiles is split into k = share / rt K-ranges (K ranges may differ
+// by one group), capped by its group count and by the 6-bit count field of the
+// counted words (<= 63).  While the step needs more CTAs than it has, the
+// largest split shrinks.
+std::vector<int> plan_step_ks(const std::vector<int64_t>& F_out_pad, const std::vector<int>& n_groups, int nctas,
+                              int R, bool even) {
+    const int nl = (int)F_out_pad.size();
+    double W = 0;
+    for (int l = 0; l < nl; ++l) W += (double)F_out_pad[l] * n_groups[l];
+    std::vector<int> rt(nl), ks(nl);
+    int total = 0;
+    for (int l = 0; l < nl; ++l) {
+        rt[l] = (int)((F_out_pad[l] + R - 1) / R);
+        const double share = nctas * ((double)F_out_pad[l] * n_groups[l]) / W;
+        int k = std::max(1, (int)(share / rt[l]));
+        k = std::min(k, n_groups[l]);
+        k = std::min(k, 63);
+        if (even) {
+            const int gper = (n_groups[l] + k - 1) / k;
+            k = (n_groups[l] + gper - 1) / gper;
+        }
+        ks[l] = k;
+        total += rt[l] * k;
+    }
+    while (total > nctas) {
+        int lm = -1;
+        for (int l = 0; l < nl; ++l)
+            if (ks[l] > 1 && (lm < 0 || ks[l] * rt[l] > ks[lm] * rt[lm])) lm = l;
+        if (lm < 0) break;
+        total -= rt[lm];
+        ks[lm] -= 1;
+    }
+    return ks;
+}
+
+static int chain_rows_per_cta(int d, int B, int nw) {
+    const int NB = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;
+    const int rw = d <= 2 ? 64 : (NB == 1 ? 64 : NB == 2 ? 32 : NB == 4 ? 16 : 8);
+    return rw * nw;
+}
+
+fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, int rank, int max_ctas, bool det,
+                        const ChainModel* model, cudaStream_t st, fasq_chain** out) {
+    *out = nullptr;
+    const int n_steps = (int)steps.size();
+    if (n_steps < 1) return FASQ_E_ARG;
+    if (world < 1 || world > 8 || rank < 0 || rank >= world || max_ctas < 0) return FASQ_E_ARG;
+    if (B < 1 || B > 8) return FASQ_E_UNSUPPORTED;
+    const int NB = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;
+    fasq_chain* c = new fasq_chain();
+    auto fail = [&](fasq_status s, const std::string& msg) {
+        if (!msg.empty()) set_error("chain: " + msg);
+        destroy_chain(c);
+        return s;
+    };
+    c->n_steps = n_steps;
+    c->B = B;
+    c->world = world;
+    c->rank = rank;
+    const int sms = sm_count();
+    c->nctas = sms;
+    if (max_ctas > 0) c->nctas = std::min(c->nctas, (int)max_ctas);
+    c->nw = 16;
+    c->st = 3;
+    if (const char* e = getenv("FASQ_CHAIN_CFG")) {   // experiments: "nw,st"
+        int a = 0, b = 0;
+        if (sscanf(e, "%d,%d", &a, &b) == 2) { c->nw = a; c->st = b; }
+    }
+    if (model) { c->model = *model; c->has_model = true; }
+    // ---- validate + arena layout ----
+    int64_t words = 0;
+    c->acc_off.resize(n_steps);
+    c->acc_ld.resize(n_steps);
+    c->acc_ks.resize(n_steps);
+    c->kinds.resize(n_steps);
+    std::vector<int> pq_F_in(n_steps, 0);
+    for (int s = 0; s < n_steps; ++s) {
+        const StepDesc& S = steps[s];
+        c->kinds[s] = S.kind;
+        if (S.kind == SK_PQ) {
+            if (S.layers.empty() || S.layers.size() > 4) return fail(FASQ_E_ARG, "a PQ step needs 1..4 layers");
+            const int64_t F_in = S.layers[0]->F_in;
+            for (const fasq_layer* L : S.layers) {
+                if (!L) return fail(FASQ_E_ARG, "null layer");
+                if (L->F_in != F_in) return fail(FASQ_E_SHAPE, "layers of a step must share F_in");
+                if (c->d == 0) c->d = L->d;
+                if (L->d != c->d) return fail(FASQ_E_UNSUPPORTED, "all layers of a chain need the same d");
+                c->maxC = std::max(c->maxC, L->C);
+                const int64_t ld = S.kshard ? L->F_out : (S.out_all ? L->F_out * world : L->F_out);
+                c->acc_off[s].push_back(words);
+                c->acc_ld[s].push_back(ld);
+                words += (int64_t)B * ld;
+            }
+            pq_F_in[s] = (int)F_in;
+        } else if (S.kind == SK_EMBED) {
+            if (!model || !S.embed || S.hidden < 1) return fail(FASQ_E_ARG, "EMBED step needs a model and a table");
+            c->acc_off[s].push_back(words);
+            c->acc_ld[s].push_back(S.hidden);
+            c->acc_ks[s].push_back(1);
+            words += (int64_t)B * S.hidden;
+        } else if (S.kind == SK_ATTN) {
+            if (!model || !S.kc || !S.vc || S.head_dim < 8 || S.head_dim > 128 || S.head_dim % 8 || S.n_kv < 1 ||
+                S.n_heads % S.n_kv)
+                return fail(FASQ_E_UNSUPPORTED, "ATTN step: head_dim must be a multiple of 8 in 8..128");
+            if (S.q_step < 0 || S.q_step >= s || steps[S.q_step].kind != SK_PQ || steps[S.q_step].layers.size() != 3)
+                return fail(FASQ_E_ARG, "ATTN step needs an earlier q/k/v step");
+            c->acc_off[s].push_back(words);
+            c->acc_ld[s].push_back((int64_t)S.n_heads * S.head_dim);
+            c->acc_ks[s].push_back(1);
+            words += (int64_t)B * S.n_heads * S.head_dim;
+        } else {
+            return fail(FASQ_E_ARG, "unknown step kind");
+        }
+    }
+    if (c->d == 0) return fail(FASQ_E_ARG, "a chain needs at least one PQ step");
+    const bool pair = c->d <= 2;
+    if (model && !pair) return fail(FASQ_E_UNSUPPORTED, "whole-model chains need d <= 2");
+    c->rw = pair ? 64 : (NB == 1 ? 64 : NB == 2 ? 32 : NB == 4 ? 16 : 8);
+    const int E = entry_bytes(c->d);
+    const size_t cbb_max = (size_t)c->maxC * 32 * E;
+    auto cbring = [&](int stg) { return pair ? (size_t)kChainCS * kPairSlot : (size_t)stg * cbb_max; };
+    auto ring = [&](int stg, int nw) { return cbring(stg) + (size_t)stg * c->rw * nw * 32; };
+    while (c->st > 2 && ring(c->st, c->nw) > kChainSmem) --c->st;
+    if (ring(c->st, c->nw) > kChainSmem && c->nw > 8) c->nw = 8;
+    while (c->st > 1 && ring(c->st, c->nw) > kChainSmem) --c->st;
+    c->R = c->rw * c->nw;
+    c->arena_words = words;
+    // ---- work plan: per step a list of items, dealt to the CTAs round-robin ----
+    std::vector<std::vector<ChainItem>> per_step(n_steps);
+    std::vector<ChainPhase> phases(n_steps);
+    for (int s = 0; s < n_steps; ++s) {
+        const StepDesc& S = steps[s];
+        ChainPhase& P = phases[s];
+        std::memset(&P, 0, sizeof(P));
+        P.kind = S.kind;
+        P.res_off = -1;
+        if (S.kind == SK_EMBED) {
+            P.embed = S.embed;
+            P.e_off = c->acc_off[s][0];
+            P.hidden = S.hidden;
+            ChainItem w{};
+            w.kind = SK_EMBED;
+            per_step[s].push_back(w);
+            continue;
+        }
+        if (S.kind == SK_ATTN) {
+            const StepDesc& Q = steps[S.q_step];
+            const int hd = S.head_dim;
+            for (int l = 0; l < 3; ++l) {
+                const int64_t want = (int64_t)(l == 0 ? S.n_heads : S.n_kv) * hd;
+                if (c->acc_ld[S.q_step][l] != want) return fail(FASQ_E_SHAPE, "q/k/v widths do not match the heads");
+            }
+            P.q_off = c->acc_off[S.q_step][0];
+            P.k_off = c->acc_off[S.q_step][1];
+            P.v_off = c->acc_off[S.q_step][2];
+            P.q_ks = c->acc_ks[S.q_step][0];
+            P.k_ks = c->acc_ks[S.q_step][1];
+            P.v_ks = c->acc_ks[S.q_step][2];
+            P.q_ld = S.n_heads * hd;
+            P.kv_ld = S.n_kv * hd;
+            P.o_off = c->acc_off[s][0];
+            P.o_ld = S.n_heads * hd;
+            P.kc = S.kc;
+            P.vc = S.vc;
+            P.n_heads = S.n_heads;
+            P.n_kv = S.n_kv;
+            P.hd = hd;
+            P.parts = model->attn_parts;
+            (void)Q;
+            for (int h = 0; h < S.n_heads; ++h)
+                for (int q = 0; q < P.parts; ++q) {
+                    ChainItem w{};
+                    w.kind = SK_ATTN;
+                    w.head = h;
+                    w.kidx = q;
+                    per_step[s].push_back(w);
+                }
+            continue;
+        }
+        // ---- PQ ----
+        const int nl = (int)S.layers.size();
+        std::vector<int64_t> fop(nl), fop_plan(nl);
+        std::vector<int> ngr(nl);
+        for (int l = 0; l < nl; ++l) {
+            fop[l] = S.layers[l]->F_out_pad;
+            ngr[l] = S.layers[l]->n_groups;
+            // deterministic TP: K ranges as the unsharded (world 1) plan on a full
+            // GPU would cut them -> bit-identical to one GPU
+            fop_plan[l] = det && world > 1 && !S.kshard
+                              ? (S.layers[l]->F_out * world + kRowBlock - 1) / kRowBlock * kRowBlock
+                              : fop[l];
+        }
+        const bool even = getenv("FASQ_CHAIN_EVEN") != nullptr;
+        std::vector<int> ks = plan_step_ks(fop_plan, ngr, det && world > 1 ? sms : c->nctas, c->R, even);
+        for (int l = 0; l < nl; ++l) c->acc_ks[s].push_back(S.kshard ? ks[l] * world : ks[l]);
+        // input
+        P.F_in = pq_F_in[s];
+        P.in_mode = S.in_mode;
+        if (S.in_mode == IN_EXT) {
+            if (c->ext_F_in == 0) c->ext_F_in = P.F_in;
+            if (c->ext_F_in != P.F_in) return fail(FASQ_E_SHAPE, "external-input steps need the same F_in");
+        } else {
+            const int src = S.src_step;
+            if (src < 0 || src >= s) return fail(FASQ_E_ARG, "input must come from an earlier step");
+            if (S.in_mode == IN_SILU) {
+                if (steps[src].kind != SK_PQ || steps[src].layers.size() < 2) return fail(FASQ_E_ARG, "SILU input needs gate/up");
+                if (c->acc_ld[src][0] != P.F_in || c->acc_ld[src][1] != P.F_in) return fail(FASQ_E_SHAPE, "gate/up width != F_in");
+                P.x_off = c->acc_off[src][0];
+                P.x_ks = c->acc_ks[src][0];
+                P.x2_off = c->acc_off[src][1];
+                P.x2_ks = c->acc_ks[src][1];
+                P.x_sys = steps[src].out_all && world > 1;
+            } else {
+                if (S.src_layer < 0 || S.src_layer >= (int)c->acc_off[src].size())
+                    return fail(FASQ_E_ARG, "input layer out of range");
+                if (c->acc_ld[src][S.src_layer] != P.F_in) return fail(FASQ_E_SHAPE, "input width != F_in");
+                P.x_off = c->acc_off[src][S.src_layer];
+                P.x_ks = c->acc_ks[src][S.src_layer];
+                P.x_sys = steps[src].kind == SK_PQ && steps[src].out_all && world > 1;
+                if (S.in_mode == IN_RMSNORM) {
+                    if (!pair || !S.gamma) return fail(FASQ_E_UNSUPPORTED, "RMSNorm input needs d <= 2 and gamma");
+                    P.gamma = S.gamma;
+                    P.eps = S.eps;
+                }
+            }
+            if (S.in_mode != IN_WORDS && !pair) return fail(FASQ_E_UNSUPPORTED, "input transforms need d <= 2");
+        }
+        if (S.res_step >= 0) {
+            if (!pair) return fail(FASQ_E_UNSUPPORTED, "residual epilogue needs d <= 2");
+            if (S.res_step >= s || S.res_layer >= (int)c->acc_off[S.res_step].size())
+                return fail(FASQ_E_ARG, "residual must come from an earlier step");
+            if (c->acc_ld[S.res_step][S.res_layer] != c->acc_ld[s][0] || nl != 1)
+                return fail(FASQ_E_SHAPE, "residual width != output width (single-layer steps only)");
+            P.res_off = c->acc_off[S.res_step][S.res_layer];
+            P.res_ks = c->acc_ks[S.res_step][S.res_layer];
+            P.res_here = S.res_here ? 1 : 0;
+            P.res_sys = steps[S.res_step].kind == SK_PQ && steps[S.res_step].out_all && world > 1;
+        }
+        P.out_all = S.out_all && world > 1;
+        for (int l = 0; l < nl; ++l) {
+            const fasq_layer* L = S.layers[l];
+            const int rt = (L->F_out_pad + c->R - 1) / c->R;
+            for (int r = 0; r < rt; ++r)
+                for (int k = 0; k < ks[l]; ++k) {
+                    ChainItem w{};
+                    w.kind = SK_PQ;
+                    w.idx = L->idx;
+                    w.cbimg = L->cbimg;
+                    w.cbmap = L->cbmap;
+                    w.y_off = c->acc_off[s][l];
+                    w.F_out = (int)L->F_out;
+                    w.ld = (int)c->acc_ld[s][l];
+                    w.row0_g = (S.out_all && !S.kshard) ? (int)(L->F_out * rank) : 0;
+                    w.F_out_pad = L->F_out_pad;
+                    w.N_ss = L->N_ss;
+                    w.C = L->C;
+                    w.r0 = r * c->R;
+                    w.rows_valid = std::min(c->R, L->F_out_pad - w.r0);
+                    w.g_begin = (int)((int64_t)k * L->n_groups / ks[l]);
+                    w.g_end = (int)((int64_t)(k + 1) * L->n_groups / ks[l]);
+                    w.kidx = k;
+                    c->gmax = std::max(c->gmax, w.g_end - w.g_begin);
+                    per_step[s].push_back(w);
+                }
+        }
+    }
+    if (c->ext_F_in == 0 && !model) return fail(FASQ_E_ARG, "the chain needs an external input");
+    c->mi = 1;
+    for (const auto& v : per_step) c->mi = std::max(c->mi, (int)((v.size() + c->nctas - 1) / c->nctas));
+    std::vector<ChainItem> items((size_t)n_steps * c->nctas * c->mi);
+    for (auto& w : items) { w = ChainItem{}; w.kind = -1; }
+    for (int s = 0; s < n_steps; ++s)
+        for (size_t q = 0; q < per_step[s].size(); ++q)
+            items[((size_t)s * c->nctas + q % c->nctas) * c->mi + q / c->nctas] = per_step[s][q];
+    const size_t xg = (pair && NB == 8) ? (size_t)32 * NB * c->d * 4 : (size_t)32 * NB * E;   // k_chain XG
+    auto smem_of = [&](int stg) {
+        return cbring(stg) + (size_t)stg * c->R * 32 + (size_t)c->gmax * xg + 16 * (stg + kChainCS) + kChainScratch;
+    };
+    while (c->st > 1 && smem_of(c->st) > kChainSmem) --c->st;
+    c->smem = smem_of(c->st);
+    if (c->smem > kChainSmem) return fail(FASQ_E_UNSUPPORTED, "SMEM plan too large");
+    if (model) {   // attention scratch lives in a 64 KiB pair slot
+        for (int s = 0; s < n_steps; ++s)
+            if (steps[s].kind == SK_ATTN) {
+                const int Tp = (model->max_T + model->attn_parts - 1) / model->attn_parts;
+                const size_t need = (3 * 256) * 4 + 2 * 256 * 2 + 32 * 256 * 4 + ((Tp + 3) & ~3) * 4 + 32 * 4;
+                if (need > kPairSlot) return fail(FASQ_E_UNSUPPORTED, "attention scratch exceeds a pair slot (max_T)");
+            }
+    }
+    const size_t bytes = ((size_t)words * 2 + kTailWords) * 8;
+    if (cudaMalloc(&c->arenas, bytes) != cudaSuccess || cudaMalloc(&c->peers_dev, 8 * sizeof(void*)) != cudaSuccess ||
+        cudaMalloc(&c->items, items.size() * sizeof(ChainItem)) != cudaSuccess ||
+        cudaMalloc(&c->phases, phases.size() * sizeof(ChainPhase)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FASQ_E_OOM, "");
+    }
+    cudaError_t e = cudaMemcpyAsync(c->items, items.data(), items.size() * sizeof(ChainItem), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(c->phases, phases.data(), phases.size() * sizeof(ChainPhase), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->arenas, 0, bytes, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);   // host vectors go out of scope
+    if (e != cudaSuccess) { fasq_status s = cuda_fail(e, "chain upload"); destroy_chain(c); return s; }
+    std::vector<unsigned long long*> bases(world, nullptr);
+    bases[rank] = c->arenas;
+    fasq_status s = upload_peers(c, bases);
+    if (s != FASQ_OK) { destroy_chain(c); return s; }
+    c->peers_ready = world == 1;
+    *out = c;
+    return FASQ_OK;
+}
+
+fasq_status chain_launch(fasq_chain* c, const void* x_dev, cudaStream_t st) {
+    if (!c->peers_ready) { set_error("chain: world > 1 needs fasq_chain_set_peers first"); return FASQ_E_ARG; }
+    ChainParams p{};
+    p.items = static_cast<const ChainItem*>(c->items);
+    p.phases = static_cast<const ChainPhase*>(c->phases);
+    p.x_ext = static_cast<const __half*>(x_dev);
+    p.trace = c->trace;
+    p.peers = c->peers_dev;
+    p.arena_words = c->arena_words;
+    p.world = c->world;
+    p.rank = c->rank;
+    p.pf = 0;
+    if (const char* e = getenv("FASQ_CHAIN_PF")) p.pf = atoi(e);
+    p.dbg = 0;
+    if (const char* e = getenv("FASQ_CHAIN_DBG")) p.dbg = atoi(e);
+    p.backoff = 0;
+    if (const char* e = getenv("FASQ_CHAIN_BACKOFF")) p.backoff = atoi(e);
+    p.n_steps = c->n_steps;
+    p.nctas = c->nctas;
+    p.B = c->B;
+    p.gmax = c->gmax;
+    p.mi = c->mi;
+    p.cbb_max = c->maxC * 32 * entry_bytes(c->d);
+    if (c->has_model) {
+        p.model = 1;
+        p.rope = c->model.rope;
+        p.max_T = c->model.max_T;
+        p.pos_wrap = c->model.pos_wrap;
+        p.tok_hist = c->model.tok_hist;
+        p.tok_expect = c->model.tok_expect;
+        p.part_buf = c->model.part_buf;
+        p.part_cnt = c->model.part_cnt;
+    }
+    fasq_status s;
+    switch (c->d) {
+        case 1: s = chain_nb<1>(c, p, st); break;
+        case 2: s = chain_nb<2>(c, p, st); break;
+        case 4: s = chain_nb<4>(c, p, st); break;
+        case 8: s = chain_nb<8>(c, p, st); break;
+        default: s = FASQ_E_UNSUPPORTED;
+    }
+    return s;
+}
+
+fasq_status chain_output(const fasq_chain* c, int step, int layer, void* y_dev, fasq_dtype dtype, cudaStream_t st) {
+    if (step < 0 || step >= c->n_steps) return FASQ_E_ARG;
+    if (layer < 0 || layer >= (int)c->acc_off[step].size()) return FASQ_E_ARG;
+    if (dtype != FASQ_F16 && dtype != FASQ_F32 && dtype != FASQ_ACC_I64) return FASQ_E_ARG;
+    const int64_t n = (int64_t)c->B * c->acc_ld[step][layer];
+    if (n <= 0) return FASQ_OK;
+    k_counted_convert<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(c->arenas, c->arena_words, c->nctas,
+                                                                  c->acc_off[step][layer], n, c->acc_ks[step][layer],
+                                                                  y_dev, (int)dtype, c->world > 1);
+    FASQ_CUDA_TRY(cudaGetLastError());
+    return FASQ_OK;
+}
+
+void chain_destroy(fasq_chain* c) { destroy_chain(c); }
+
 }  // namespace fasq
 
 using namespace fasq;
@@ -442,185 +1119,28 @@ fasq_status fasq_chain_create_tp(const fasq_chain_step* steps, int32_t n_steps, 
     if (!out) return FASQ_E_ARG;
     *out = nullptr;
     if (!steps || n_steps < 1) return FASQ_E_ARG;
-    if (world < 1 || world > 8 || rank < 0 || rank >= world || max_ctas < 0) return FASQ_E_ARG;
-    if (B < 1 || B > 8) return FASQ_E_UNSUPPORTED;
-    const int NB = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;
-    fasq_chain* c = new fasq_chain();
-    c->n_steps = n_steps;
-    c->B = B;
-    c->world = world;
-    c->rank = rank;
-    c->nctas = sm_count();
-    if (max_ctas > 0) c->nctas = std::min(c->nctas, (int)max_ctas);
-    // same tiling family as the per-launch GEMV default (gemv.cu plan_gemv)
-    c->nw = 16;
-    c->rw = NB == 1 ? 64 : NB == 2 ? 32 : NB == 4 ? 16 : 8;   // core::RowsPerWarp (d = 4, 8)
-    c->st = 3;
-    if (const char* e = getenv("FASQ_CHAIN_CFG")) {   // experiments: "nw,st"
-        int a = 0, b = 0;
-        if (sscanf(e, "%d,%d", &a, &b) == 2) { c->nw = a; c->st = b; }
-    }
-    c->R = c->rw * c->nw;
-    // validate + arena layout: every layer output is the FULL (all-rank) vector
-    int64_t words = 16;   // [0..15]: reserved
-    c->acc_off.resize(n_steps);
-    c->acc_Fout.resize(n_steps);
-    c->acc_ks.resize(n_steps);
-    c->step_F_in.resize(n_steps);
+    std::vector<StepDesc> v(n_steps);
     for (int s = 0; s < n_steps; ++s) {
         const fasq_chain_step& S = steps[s];
-        if (!S.layers || S.n_layers < 1 || S.n_layers > 4) { destroy_chain(c); return FASQ_E_ARG; }
-        const int64_t F_in = S.layers[0]->F_in;
-        for (int l = 0; l < S.n_layers; ++l) {
-            const fasq_layer* L = S.layers[l];
-            if (!L) { destroy_chain(c); return FASQ_E_ARG; }
-            if (L->F_in != F_in) { destroy_chain(c); return FASQ_E_SHAPE; }
-            if (c->d == 0) c->d = L->d;
-            if (L->d != c->d) { destroy_chain(c); return FASQ_E_UNSUPPORTED; }
-            c->maxC = std::max(c->maxC, L->C);
-            c->acc_off[s].push_back(words);
-            c->acc_Fout[s].push_back(L->F_out * world);
-            words += (int64_t)B * L->F_out * world;
-        }
-        c->step_F_in[s] = (int)F_in;
+        if (!S.layers || S.n_layers < 1 || S.n_layers > 4) return FASQ_E_ARG;
+        v[s].kind = SK_PQ;
+        v[s].layers.assign(S.layers, S.layers + S.n_layers);
+        for (const fasq_layer* L : v[s].layers)
+            if (!L) return FASQ_E_ARG;
         if (S.input_step < 0) {
-            if (c->ext_F_in == 0) c->ext_F_in = (int)F_in;
-            if (c->ext_F_in != F_in) { destroy_chain(c); return FASQ_E_SHAPE; }
+            v[s].in_mode = IN_EXT;
         } else {
-            if (S.input_step >= s || S.input_layer < 0 || S.input_layer >= steps[S.input_step].n_layers) {
-                destroy_chain(c);
-                return FASQ_E_ARG;
-            }
-            if (steps[S.input_step].layers[S.input_layer]->F_out * world != F_in) {
-                destroy_chain(c);
-                return FASQ_E_SHAPE;
-            }
+            if (S.input_step >= s) return FASQ_E_ARG;
+            v[s].in_mode = IN_WORDS;
+            v[s].src_step = S.input_step;
+            v[s].src_layer = S.input_layer;
         }
+        v[s].out_all = world > 1;   // row shards, gathered into every rank's arena
     }
-    if (c->ext_F_in == 0) { destroy_chain(c); return FASQ_E_ARG; }   // the chain needs an external input
-    if (c->d <= 2) c->rw = 64;   // pair stages: row-set mapping, 64 rows per warp at any B
-    const int E = entry_bytes(c->d);
-    const size_t cbb_max = (size_t)c->maxC * 32 * E;
-    const bool pair = c->d <= 2;   // ChainPair: codebook pair ring next to the index ring
-    auto cbring = [&](int st) { return pair ? (size_t)kChainCS * kPairSlot : (size_t)st * cbb_max; };
-    // (x staging is added after the work plan, smem_of below)
-    auto ring = [&](int st, int nw) { return cbring(st) + (size_t)st * c->rw * nw * 32; };
-    while (c->st > 2 && ring(c->st, c->nw) > kChainSmem) --c->st;
-    if (ring(c->st, c->nw) > kChainSmem && c->nw > 8) c->nw = 8;
-    while (c->st > 1 && ring(c->st, c->nw) > kChainSmem) --c->st;
-    c->R = c->rw * c->nw;
-    c->arena_words = words;
-    if (cudaMalloc(&c->arenas, (size_t)words * 2 * 8) != cudaSuccess ||
-        cudaMalloc(&c->ctrl, 64) != cudaSuccess ||
-        cudaMalloc(&c->peers_dev, 8 * sizeof(void*)) != cudaSuccess) {
-        cudaGetLastError();
-        destroy_chain(c);
-        return FASQ_E_OOM;
-    }
-    // work plan: per step a list of items (row tile x K-range), dealt to the
-    // CTAs round-robin; more items than CTAs (e.g. B = 8: 128-row tiles) ->
-    // several items per CTA per step, [n_steps][nctas][mi]
-    std::vector<std::vector<ChainItem>> per_step(n_steps);
-    std::vector<ChainPhase> phases(n_steps);
-    for (int s = 0; s < n_steps; ++s) {
-        const fasq_chain_step& S = steps[s];
-        const int nl = S.n_layers;
-        double W = 0;
-        for (int l = 0; l < nl; ++l) W += (double)S.layers[l]->F_out_pad * S.layers[l]->n_groups;
-        std::vector<int> rt(nl), ks(nl);
-        int total = 0;
-        for (int l = 0; l < nl; ++l) {
-            const fasq_layer* L = S.layers[l];
-            rt[l] = (L->F_out_pad + c->R - 1) / c->R;
-            const double share = c->nctas * ((double)L->F_out_pad * L->n_groups) / W;
-            int k = std::max(1, (int)(share / rt[l]));
-            k = std::min(k, L->n_groups);
-            // use every CTA the share allows even when the K ranges then differ by
-            // one group (e.g. down: 37 x 6-7 groups instead of 32 x 7): the
-            // dataflow lets short items hand their outputs over early, and
-            // measured 0.92-0.95 -> 0.90 ms/token; FASQ_CHAIN_EVEN=1 restores
-            // equal-sized K ranges
-            if (getenv("FASQ_CHAIN_EVEN") != nullptr) {
-                const int gper = (L->n_groups + k - 1) / k;
-                k = (L->n_groups + gper - 1) / gper;
-            }
-            ks[l] = k;
-            total += rt[l] * k;
-        }
-        while (total > c->nctas) {
-            int lm = -1;
-            for (int l = 0; l < nl; ++l)
-                if (ks[l] > 1 && (lm < 0 || ks[l] * rt[l] > ks[lm] * rt[lm])) lm = l;
-            if (lm < 0) break;
-            total -= rt[lm];
-            ks[lm] -= 1;
-        }
-        for (int l = 0; l < nl; ++l) {
-            if (ks[l] > 63) { destroy_chain(c); return FASQ_E_UNSUPPORTED; }   // counted-word count field
-            c->acc_ks[s].push_back(ks[l]);
-        }
-        for (int l = 0; l < nl; ++l) {
-            const fasq_layer* L = S.layers[l];
-            for (int r = 0; r < rt[l]; ++r)
-                for (int k = 0; k < ks[l]; ++k) {
-                    ChainItem w{};
-                    w.idx = L->idx;
-                    w.cbimg = L->cbimg;
-                    w.cbmap = L->cbmap;
-                    w.y_off = c->acc_off[s][l];
-                    w.F_out = (int)L->F_out;
-                    w.F_out_g = (int)(L->F_out * world);
-                    w.row0_g = (int)(L->F_out * rank);
-                    w.F_out_pad = L->F_out_pad;
-                    w.N_ss = L->N_ss;
-                    w.C = L->C;
-                    w.r0 = r * c->R;
-                    w.rows_valid = std::min(c->R, L->F_out_pad - w.r0);
-                    w.g_begin = (int)((int64_t)k * L->n_groups / ks[l]);
-                    w.g_end = (int)((int64_t)(k + 1) * L->n_groups / ks[l]);
-                    c->gmax = std::max(c->gmax, w.g_end - w.g_begin);
-                    per_step[s].push_back(w);
-                }
-        }
-        phases[s].F_in = c->step_F_in[s];
-        phases[s].x_off = S.input_step < 0 ? -1 : c->acc_off[S.input_step][S.input_layer];
-        phases[s].x_ks = S.input_step < 0 ? 0 : c->acc_ks[S.input_step][S.input_layer];
-    }
-    c->mi = 1;
-    for (const auto& v : per_step) c->mi = std::max(c->mi, (int)((v.size() + c->nctas - 1) / c->nctas));
-    std::vector<ChainItem> items((size_t)n_steps * c->nctas * c->mi);
-    for (auto& w : items) w = ChainItem{};
-    for (int s = 0; s < n_steps; ++s)
-        for (size_t q = 0; q < per_step[s].size(); ++q)
-            items[((size_t)s * c->nctas + q % c->nctas) * c->mi + q / c->nctas] = per_step[s][q];
-    const size_t xg = (pair && NB == 8) ? (size_t)32 * NB * c->d * 4 : (size_t)32 * NB * E;   // k_chain XG
-    auto smem_of = [&](int st) {
-        return cbring(st) + (size_t)st * c->R * 32 + (size_t)c->gmax * xg + 16 * (st + kChainCS);
-    };
-    while (c->st > 1 && smem_of(c->st) > kChainSmem) --c->st;
-    c->smem = smem_of(c->st);
-    if (c->smem > kChainSmem) { destroy_chain(c); set_error("chain: SMEM plan too large"); return FASQ_E_UNSUPPORTED; }
-    cudaStream_t st = (cudaStream_t)stream;
-    if (cudaMalloc(&c->items, items.size() * sizeof(ChainItem)) != cudaSuccess ||
-        cudaMalloc(&c->phases, phases.size() * sizeof(ChainPhase)) != cudaSuccess) {
-        cudaGetLastError();
-        destroy_chain(c);
-        return FASQ_E_OOM;
-    }
-    cudaError_t e = cudaMemcpyAsync(c->items, items.data(), items.size() * sizeof(ChainItem), cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(c->phases, phases.data(), phases.size() * sizeof(ChainPhase), cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(c->arenas, 0, (size_t)words * 2 * 8, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(c->ctrl, 0, 64, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);   // host vectors go out of scope
-    if (e != cudaSuccess) { fasq_status s = cuda_fail(e, "chain upload"); destroy_chain(c); return s; }
-    std::vector<unsigned long long*> bases(world, nullptr);
-    bases[rank] = c->arenas;
-    fasq_status s = upload_peers(c, bases);
-    if (s != FASQ_OK) { destroy_chain(c); return s; }
-    c->peers_ready = world == 1;
-    *out = c;
-    return FASQ_OK;
+    // deterministic TP (default): K ranges of the unsharded plan -> sharded
+    // outputs bit-identical to one GPU; FASQ_CHAIN_FAST=1 plans per rank
+    const bool det = getenv("FASQ_CHAIN_FAST") == nullptr;
+    return chain_build(v, B, world, rank, max_ctas, det, nullptr, (cudaStream_t)stream, out);
 }
 
 fasq_status fasq_chain_create(const fasq_chain_step* steps, int32_t n_steps, int32_t B, void* stream,
@@ -666,53 +1186,75 @@ fasq_status fasq_chain_set_peer_chains(fasq_chain* c, const fasq_chain* const* c
 
 fasq_status fasq_chain_run(fasq_chain* c, const void* x_dev, void* stream) {
     if (!c || !x_dev) return FASQ_E_ARG;
-    if (!c->peers_ready) { set_error("chain: world > 1 needs fasq_chain_set_peers first"); return FASQ_E_ARG; }
-    cudaStream_t st = (cudaStream_t)stream;
-    ChainParams p{};
-    p.items = static_cast<const ChainItem*>(c->items);
-    p.phases = static_cast<const ChainPhase*>(c->phases);
-    p.x_ext = static_cast<const __half*>(x_dev);
-    p.trace = c->trace;
-    p.ctrl = c->ctrl;
-    p.peers = c->peers_dev;
-    p.arena_words = c->arena_words;
-    p.world = c->world;
-    p.rank = c->rank;
-    p.pf = 0;
-    if (const char* e = getenv("FASQ_CHAIN_PF")) p.pf = atoi(e);
-    p.dbg = 0;
-    if (const char* e = getenv("FASQ_CHAIN_DBG")) p.dbg = atoi(e);
-    p.backoff = 0;
-    if (const char* e = getenv("FASQ_CHAIN_BACKOFF")) p.backoff = atoi(e);
-    p.n_steps = c->n_steps;
-    p.nctas = c->nctas;
-    p.B = c->B;
-    p.gmax = c->gmax;
-    p.mi = c->mi;
-    p.cbb_max = c->maxC * 32 * entry_bytes(c->d);
-    fasq_status s;
-    switch (c->d) {
-        case 1: s = chain_nb<1>(c, p, st); break;
-        case 2: s = chain_nb<2>(c, p, st); break;
-        case 4: s = chain_nb<4>(c, p, st); break;
-        case 8: s = chain_nb<8>(c, p, st); break;
-        default: s = FASQ_E_UNSUPPORTED;
-    }
+    fasq_status s = chain_launch(c, x_dev, (cudaStream_t)stream);
     if (s == FASQ_OK) set_launch_count(1);
+    return s;
+}
+
+fasq_status fasq_chain_run_host(fasq_chain* c, const void* x_host, void* y_host, int32_t step, int32_t layer,
+                                fasq_dtype dtype, void* stream) {
+    if (!c || !x_host || !y_host) return FASQ_E_ARG;
+    if (step < 0 || step >= c->n_steps || layer < 0 || layer >= (int)c->acc_off[step].size()) return FASQ_E_ARG;
+    if (dtype != FASQ_F16 && dtype != FASQ_F32) return FASQ_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t xb = (size_t)c->B * c->ext_F_in * 2;
+    const size_t yb = (size_t)c->B * c->acc_ld[step][layer] * (dtype == FASQ_F32 ? 4 : 2);
+    void *xd = nullptr, *yd = nullptr;
+    if (cudaMallocAsync(&xd, xb, st) != cudaSuccess || cudaMallocAsync(&yd, yb, st) != cudaSuccess) {
+        cudaGetLastError();
+        return FASQ_E_OOM;
+    }
+    fasq_status s = FASQ_OK;
+    cudaError_t e = cudaMemcpyAsync(xd, x_host, xb, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) s = cuda_fail(e, "H2D x");
+    if (s == FASQ_OK) s = chain_launch(c, xd, st);
+    if (s == FASQ_OK) s = chain_output(c, step, layer, yd, dtype, st);
+    if (s == FASQ_OK) {
+        e = cudaMemcpyAsync(y_host, yd, yb, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) s = cuda_fail(e, "D2H y");
+    }
+    cudaFreeAsync(xd, st);
+    cudaFreeAsync(yd, st);
+    e = cudaStreamSynchronize(st);
+    if (s == FASQ_OK && e != cudaSuccess) s = cuda_fail(e, "chain_run_host sync");
+    if (s == FASQ_OK) set_launch_count(2);
     return s;
 }
 
 fasq_status fasq_chain_output(const fasq_chain* c, int32_t step, int32_t layer, void* y_dev, fasq_dtype dtype,
                               void* stream) {
-    if (!c || !y_dev || step < 0 || step >= c->n_steps) return FASQ_E_ARG;
-    if (layer < 0 || layer >= (int)c->acc_off[step].size()) return FASQ_E_ARG;
-    if (dtype != FASQ_F16 && dtype != FASQ_F32 && dtype != FASQ_ACC_I64) return FASQ_E_ARG;
-    const int64_t n = (int64_t)c->B * c->acc_Fout[step][layer];
-    if (n <= 0) return FASQ_OK;
-    k_counted_convert<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-        c->arenas, c->arena_words, c->ctrl, c->acc_off[step][layer], n, c->acc_ks[step][layer], y_dev, (int)dtype);
-    FASQ_CUDA_TRY(cudaGetLastError());
-    set_launch_count(1);
+    if (!c || !y_dev) return FASQ_E_ARG;
+    fasq_status s = chain_output(c, step, layer, y_dev, dtype, (cudaStream_t)stream);
+    if (s == FASQ_OK) set_launch_count(1);
+    return s;
+}
+
+fasq_status fasq_chain_check(fasq_chain* c, void* stream) {
+    if (!c) return FASQ_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long f = 0;
+    FASQ_CUDA_TRY(cudaMemcpyAsync(&f, c->tail() + T_OVF, 8, cudaMemcpyDeviceToHost, st));
+    FASQ_CUDA_TRY(cudaStreamSynchronize(st));
+    if (f) {
+        FASQ_CUDA_TRY(cudaMemsetAsync(c->tail() + T_OVF, 0, 8, st));
+        FASQ_CUDA_TRY(cudaStreamSynchronize(st));
+        set_error("chain: a counted partial exceeded |v| < 2^18 (outputs of that run are NaN)");
+        return FASQ_E_RANGE;
+    }
+    return FASQ_OK;
+}
+
+int32_t fasq_chain_plan_ks(const int64_t* F_out, const int64_t* n_groups, int32_t n, int32_t nctas, int32_t d,
+                           int32_t B, int32_t* ks_out) {
+    if (!F_out || !n_groups || !ks_out || n < 1 || nctas < 1) return FASQ_E_ARG;
+    std::vector<int64_t> fop(n);
+    std::vector<int> ngr(n);
+    for (int i = 0; i < n; ++i) {
+        fop[i] = (F_out[i] + kRowBlock - 1) / kRowBlock * kRowBlock;
+        ngr[i] = (int)n_groups[i];
+    }
+    std::vector<int> ks = plan_step_ks(fop, ngr, nctas, chain_rows_per_cta(d, B, 16), false);
+    for (int i = 0; i < n; ++i) ks_out[i] = ks[i];
     return FASQ_OK;
 }
 

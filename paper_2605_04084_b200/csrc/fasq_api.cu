@@ -64,6 +64,7 @@ const char* fasq_status_string(fasq_status s) {
         case FASQ_E_UNSUPPORTED: return "FASQ_E_UNSUPPORTED: parameter outside the supported range";
         case FASQ_E_CUDA: return "FASQ_E_CUDA: CUDA error";
         case FASQ_E_OOM: return "FASQ_E_OOM: device allocation failed";
+        case FASQ_E_RANGE: return "FASQ_E_RANGE: a counted partial left its |v| < 2^18 range";
     }
     return "FASQ: unknown status";
 }

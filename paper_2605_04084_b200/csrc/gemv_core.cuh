@@ -532,12 +532,41 @@ constexpr int kCntShift = 58;
 constexpr long long kCntBias = 1ll << 50;
 constexpr unsigned long long kCntMask = (1ull << kCntShift) - 1;
 
+// Out-of-range partials: the value field holds |v| < kCntBias (2^18 in value
+// units).  A partial outside it is clamped AND raises the sticky flag *ovf,
+// which poisons the run's converted outputs (NaN) and makes fasq_chain_check
+// return FASQ_E_RANGE -- never a silently wrong finite number.
+__device__ __forceinline__ long long cnt_clamp(long long v, unsigned long long* ovf) {
+    if (v >= kCntBias || v <= -kCntBias) {
+        if (ovf) asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(ovf), "l"(1ull) : "memory");
+        v = max(-(kCntBias - 1), min(kCntBias - 1, v));
+    }
+    return v;
+}
+
+// Polls one counted word until it carries `ks` contributions; returns its
+// value (units 2^-32).  The watchdog turns a lost producer into a kernel
+// error (trap) after 4 s instead of a hang.
+__device__ __forceinline__ long long poll_value(const unsigned long long* a, int ks, bool sys) {
+    unsigned long long v;
+    const unsigned long long t0 = dev::globaltimer();
+    for (;;) {
+        if (sys)
+            asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+        else
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+        if ((v >> kCntShift) == (unsigned long long)ks) break;
+        if (dev::globaltimer() - t0 > 4000000000ull) __trap();
+    }
+    return (long long)(v & kCntMask) - (long long)ks * kCntBias;
+}
+
 // y points at this shard's row 0 inside a [B][ld] word array; rows >= F_out
 // (the shard's local rows) are padding and skipped.  System-scope reduction:
 // y may be a peer GPU's buffer (NVLink, fasq_chain_create_tp).
 template <int NB, int RW>
 __device__ __forceinline__ void counted_store(const RowTotals<NB, RW>& t, unsigned long long* y, int row0, int F_out,
-                                              int ld, int B) {
+                                              int ld, int B, unsigned long long* ovf) {
     if (!t.own) return;
 #pragma unroll
     for (int h = 0; h < RowTotals<NB, RW>::H; ++h) {
@@ -546,19 +575,39 @@ __device__ __forceinline__ void counted_store(const RowTotals<NB, RW>& t, unsign
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
             if (b >= B) continue;
-            long long v = __float2ll_rn(t.v[h][b] * kAccScale);
-            v = max(-(kCntBias - 1), min(kCntBias - 1, v));   // |partial| < 2^18 (fp16 range is 2^16)
+            const long long v = cnt_clamp(__float2ll_rn(t.v[h][b] * kAccScale), ovf);
             const unsigned long long add = (1ull << kCntShift) + (unsigned long long)(kCntBias + v);
             asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" :: "l"(y + (size_t)b * ld + row), "l"(add) : "memory");
         }
     }
 }
 
-// Counted stores of the row-set mapping's totals: rows row0w + lane and
-// row0w + 32 + lane of every token b < B (word b*ld + row).
+// Row totals of the row-set mapping -> fixed-point values: v[h*NB + b] is
+// row row0w + 32h + lane, token b.  With `res` (residual words of the same
+// [B][ld] indexing, `res_ks` contributions each), the residual value is added
+// exactly (integer) to the partial -- the transformer's residual connection
+// fused into the GEMV epilogue of ONE K-split CTA per row.
 template <int NB, int G>
-__device__ __forceinline__ void counted_store_set(const float (&v)[2 * G * NB], unsigned long long* y, int row0w,
-                                                  int lane, int F_out, int ld, int B, bool sys) {
+__device__ __forceinline__ void set_values(const float (&v)[2 * G * NB], long long (&q)[2 * NB], int row0w, int lane,
+                                           int F_out, int B, const unsigned long long* res, int res_ld, int res_ks,
+                                           bool res_sys, unsigned long long* ovf) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int row = row0w + 32 * h + lane;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            long long t = __float2ll_rn(v[h * NB + b] * kAccScale);
+            if (res && row < F_out && b < B) t += poll_value(res + (size_t)b * res_ld + row, res_ks, res_sys);
+            q[h * NB + b] = cnt_clamp(t, ovf);
+        }
+    }
+}
+
+// Counted stores of set_values' results: rows row0w + lane and row0w + 32 +
+// lane of every token b < B (word b*ld + row).
+template <int NB>
+__device__ __forceinline__ void counted_store_q(const long long (&q)[2 * NB], unsigned long long* y, int row0w,
+                                                int lane, int F_out, int ld, int B, bool sys) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int row = row0w + 32 * h + lane;
@@ -566,9 +615,7 @@ __device__ __forceinline__ void counted_store_set(const float (&v)[2 * G * NB], 
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
             if (b >= B) continue;
-            long long t = __float2ll_rn(v[h * NB + b] * kAccScale);
-            t = max(-(kCntBias - 1), min(kCntBias - 1, t));
-            const unsigned long long add = (1ull << kCntShift) + (unsigned long long)(kCntBias + t);
+            const unsigned long long add = (1ull << kCntShift) + (unsigned long long)(kCntBias + q[h * NB + b]);
             if (sys)   // peer GPU arenas (tensor parallel): system scope
                 asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" :: "l"(y + (size_t)b * ld + row), "l"(add) : "memory");
             else
@@ -579,19 +626,25 @@ __device__ __forceinline__ void counted_store_set(const float (&v)[2 * G * NB], 
 
 // x staging from counted accumulator words [B][F_in] produced by ks K-split
 // CTAs of the previous step: every thread polls its words until all carry
-// count == ks (one L2 round trip once they are final), then rounds the value
-// to fp16.  Layout of s_x as stage_x.
-template <int D, int NB, int NW, bool XF = false>
+// count == ks (one L2 round trip once they are final), then forms fp16 x.
+// Layout of s_x as stage_x.  MODE:
+//   XM_WORDS  x = fp16(value)                                  (one RN rounding)
+//   XM_NORM   x = fp16(fp32(value) * scale[b] * gamma[col])    (RMSNorm; scale from norm_scale)
+//   XM_SILU   x = fp16(silu(g) * u), g/u = values of x / x2    (SwiGLU gate * up, fp32)
+constexpr int XM_WORDS = 0, XM_NORM = 1, XM_SILU = 2;
+
+template <int D, int NB, int NW, bool XF = false, int MODE = XM_WORDS>
 __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned long long* x, int ks, int F_in, int B,
-                                                int N_ss, int g_begin, int ng, bool sys = true, int backoff = 0) {
+                                                int N_ss, int g_begin, int ng, bool sys = true, int backoff = 0,
+                                                const unsigned long long* x2 = nullptr, int ks2 = 0,
+                                                const float* scale = nullptr, const __half* gamma = nullptr) {
     constexpr int E = Entry<D>::value;
+    constexpr int NX = MODE == XM_SILU ? 2 : 1;     // words per element
     const int tid = threadIdx.x;
     const int n_ent = ng * 32 * NB;
-    const unsigned long long want = (unsigned long long)ks;
-    const long long bias = (long long)ks * kCntBias;
-    constexpr int XPT = 2;
+    constexpr int XPT = MODE == XM_SILU ? 1 : 2;
     for (int t0 = tid; t0 < n_ent; t0 += NW * 32 * XPT) {
-        unsigned long long v[XPT][D];
+        unsigned long long v[XPT][NX][D];
         bool need[XPT];
 #pragma unroll
         for (int u = 0; u < XPT; ++u) {
@@ -600,7 +653,9 @@ __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned lon
             const int ss = (g_begin + t / (NB * 32)) * 32 + ((t / NB) & 31);
             need[u] = t < n_ent && b < B && ss < N_ss;
 #pragma unroll
-            for (int e = 0; e < D; ++e) v[u][e] = 0;
+            for (int q = 0; q < NX; ++q)
+#pragma unroll
+                for (int e = 0; e < D; ++e) v[u][q][e] = 0;
         }
         // poll: reload every word of this thread until all are final (a
         // watchdog turns a lost producer into a kernel error, not a hang)
@@ -616,21 +671,27 @@ __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned lon
                 const int t = t0 + u * NW * 32;
                 const int b = t % NB;
                 const int ss = (g_begin + t / (NB * 32)) * 32 + ((t / NB) & 31);
-                const unsigned long long* src = x + (size_t)b * F_in + (size_t)ss * D;
 #pragma unroll
-                for (int e = 0; e < D; ++e) {
-                    if ((v[u][e] >> kCntShift) == want) continue;
-                    if (sys)
-                        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v[u][e]) : "l"(src + e) : "memory");
-                    else
-                        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v[u][e]) : "l"(src + e) : "memory");
+                for (int q = 0; q < NX; ++q) {
+                    const unsigned long long* src = (q == 0 ? x : x2) + (size_t)b * F_in + (size_t)ss * D;
+                    const unsigned long long want = (unsigned long long)(q == 0 ? ks : ks2);
+#pragma unroll
+                    for (int e = 0; e < D; ++e) {
+                        if ((v[u][q][e] >> kCntShift) == want) continue;
+                        if (sys)
+                            asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v[u][q][e]) : "l"(src + e) : "memory");
+                        else
+                            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v[u][q][e]) : "l"(src + e) : "memory");
+                    }
                 }
             }
 #pragma unroll
             for (int u = 0; u < XPT; ++u)
 #pragma unroll
-                for (int e = 0; e < D; ++e)
-                    if (need[u] && (v[u][e] >> kCntShift) != want) done = false;
+                for (int q = 0; q < NX; ++q)
+#pragma unroll
+                    for (int e = 0; e < D; ++e)
+                        if (need[u] && (v[u][q][e] >> kCntShift) != (unsigned long long)(q == 0 ? ks : ks2)) done = false;
         }
 #pragma unroll
         for (int u = 0; u < XPT; ++u) {
@@ -638,10 +699,23 @@ __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned lon
             if (t >= n_ent) continue;
             uint32_t w[4] = {0u, 0u, 0u, 0u};
             if (need[u]) {
+                const int b = t % NB;
+                const int ss = (g_begin + t / (NB * 32)) * 32 + ((t / NB) & 31);
 #pragma unroll
                 for (int e = 0; e < D; ++e) {
-                    const long long val = (long long)(v[u][e] & kCntMask) - bias;
-                    const uint32_t h = __half_as_ushort(__double2half((double)val * kAccInv));
+                    const long long val = (long long)(v[u][0][e] & kCntMask) - (long long)ks * kCntBias;
+                    uint32_t h;
+                    if (MODE == XM_WORDS) {
+                        h = __half_as_ushort(__double2half((double)val * kAccInv));
+                    } else if (MODE == XM_NORM) {
+                        const float f = (float)((double)val * kAccInv) * scale[b];
+                        h = __half_as_ushort(__float2half_rn(f * __half2float(gamma[(size_t)ss * D + e])));
+                    } else {
+                        const long long val2 = (long long)(v[u][NX - 1][e] & kCntMask) - (long long)ks2 * kCntBias;
+                        const float g = (float)((double)val * kAccInv);
+                        const float uu = (float)((double)val2 * kAccInv);
+                        h = __half_as_ushort(__float2half_rn(g / (1.0f + expf(-g)) * uu));
+                    }
                     w[e >> 1] |= h << (16 * (e & 1));
                 }
             }
@@ -654,6 +728,70 @@ __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned lon
             for (int q = 0; q < E / 4; ++q) dst[q] = w[q];
         }
     }
+}
+
+// RMSNorm scale of the counted vector x [B][n] (ks contributions per word):
+// scale[b] = 1 / sqrt(mean_i value_i^2 + eps), fp32 sums in a FIXED order
+// (per-thread strided partials, warp butterfly, warps in order) so that every
+// CTA computes bit-identical scales.  Polls every word (the whole vector
+// must be final).  red: NW*8 floats of SMEM; scale: 8 floats of SMEM.
+template <int NB, int NW>
+__device__ __noinline__ void norm_scale(const unsigned long long* x, int ks, int n, int B, float eps, bool sys,
+                                        float* red, float* scale) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NT = NW * 32;
+    float acc[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[b] = 0.f;
+    constexpr int U = 8;   // words in flight per thread
+    const int total = B * n;
+    for (int i0 = tid; i0 < total; i0 += NT * U) {
+        unsigned long long v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = 0;
+        bool done = false;
+        const unsigned long long t_start = dev::globaltimer();
+        while (!done) {
+            done = true;
+            if (dev::globaltimer() - t_start > 4000000000ull) __trap();
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * NT;
+                if (i >= total || (v[u] >> kCntShift) == (unsigned long long)ks) continue;
+                if (sys)
+                    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v[u]) : "l"(x + i) : "memory");
+                else
+                    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v[u]) : "l"(x + i) : "memory");
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (i0 + u * NT < total && (v[u] >> kCntShift) != (unsigned long long)ks) done = false;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * NT;
+            if (i >= total) continue;
+            const float f = (float)((double)((long long)(v[u] & kCntMask) - (long long)ks * kCntBias) * kAccInv);
+            const int b = i / n;
+#pragma unroll
+            for (int bb = 0; bb < NB; ++bb)
+                if (bb == b) acc[bb] += f * f;
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        float a = acc[b];
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) a += __shfl_xor_sync(0xffffffffu, a, m);
+        if (lane == 0) red[warp * 8 + b] = a;
+    }
+    asm volatile("bar.sync 1, %0;" :: "n"(NT) : "memory");
+    if (tid < NB) {
+        float a = 0.f;
+        for (int w = 0; w < NW; ++w) a += red[w * 8 + tid];
+        scale[tid] = 1.0f / sqrtf(a / (float)n + eps);
+    }
+    asm volatile("bar.sync 1, %0;" :: "n"(NT) : "memory");
 }
 
 }  // namespace core

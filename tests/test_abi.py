@@ -38,8 +38,8 @@ def test_library_exports_every_declared_symbol(fasq):
 
 
 def test_status_strings_and_version(fasq):
-    assert fasq.lib.fasq_abi_version() == 1
-    for code in (0, -1, -2, -3, -4, -5, -6, -7, -8):
+    assert fasq.lib.fasq_abi_version() == 2
+    for code in (0, -1, -2, -3, -4, -5, -6, -7, -8, -9):
         s = fasq.lib.fasq_status_string(code).decode()
         assert s.startswith("FASQ_"), s
 
@@ -60,3 +60,29 @@ def test_no_cpu_fallback_in_binding(fasq):
     lay = object.__new__(fasq.Layer)
     with pytest.raises(TypeError):
         fasq._cuda(torch.zeros(4, dtype=torch.float16), torch.float16, "x")
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_chain_planner_llama_shapes(fasq, world):
+    """Host-only planner query at the bench's row-sharded Llama-3-8B shapes:
+    every K split fits the 6-bit count field of the counted words (<= 63) and
+    every step fits on the 148 CTAs (round-1 advisor finding: world 2 gave 64/74,
+    world 4/8 148 for o/down)."""
+    steps = [[(4096 // world, 4096), (1024 // world, 4096), (1024 // world, 4096)], [(4096 // world, 4096)],
+             [(14336 // world, 4096), (14336 // world, 4096)], [(4096 // world, 14336)]]
+    for shapes in steps:
+        for B in (1, 8):
+            ks = fasq.plan_ks(shapes, nctas=148, d=2, B=B)
+            assert all(1 <= k <= 63 for k in ks), (shapes, ks)
+            rows = 1024
+            assert sum(-(-fo // rows) * k for (fo, _), k in zip(shapes, ks)) <= 148
+
+
+def test_llama_argument_errors(fasq):
+    out = ctypes.c_void_p()
+    assert fasq.lib.fasq_llama_create(None, None, ctypes.byref(out)) == -1
+    d = fasq.LlamaDesc()
+    d.n_layers = 0
+    assert fasq.lib.fasq_llama_create(ctypes.byref(d), None, ctypes.byref(out)) == -1
+    assert fasq.lib.fasq_llama_step(None, None) == -1
+    assert fasq.lib.fasq_chain_check(None, None) == -1

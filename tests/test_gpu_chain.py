@@ -217,6 +217,93 @@ def test_chain_tensor_parallel_fused_gather(F, oracle_lib, world):
         c.free()
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_chain_tp_bit_identical_to_single_gpu(F, world):
+    """in the deterministic (default) TP plan the K ranges are the
+    unsharded chain's, so every rank's gathered outputs equal the world-1
+    chain's outputs byte for byte (shard F_out multiples of 64)."""
+    h, ffn, kv = 1024, 2048, 256
+    names = [("q", h, h), ("k", kv, h), ("v", kv, h), ("o", h, h), ("g", ffn, h), ("u", ffn, h), ("d", h, ffn)]
+    full = {n: synth.random_layer(fo, fi, 2, 256, seed=800 + i) for i, (n, fo, fi) in enumerate(names)}
+    x = torch.from_numpy(synth.activation(1, h, seed=4)).cuda()
+
+    def steps_of(L):
+        return [([L["q"], L["k"], L["v"]], None), ([L["o"]], (0, 0)), ([L["g"], L["u"]], (1, 0)), ([L["d"]], (2, 0)),
+                ([L["q"], L["k"]], (3, 0))]
+    L1 = {n: F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), idx.shape[0] * 2)
+          for n, (cb, idx) in full.items()}
+    single = F.Chain(steps_of(L1), B=1)
+    single.run(x)
+    torch.cuda.synchronize()
+    ref = [[single.output(s, l, out_dtype=torch.int64).clone() for l in range(len(st[0]))]
+           for s, st in enumerate(steps_of(L1))]
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    chains, keep = [], []
+    for r in range(world):
+        L = {}
+        for (n, fo, fi) in names:
+            cb, idx = full[n]
+            rows = fo // world
+            L[n] = F.import_layer(torch.from_numpy(cb).cuda(),
+                                  torch.from_numpy(np.ascontiguousarray(idx[:, r * rows:(r + 1) * rows])).cuda(), fi)
+        keep.append(L)
+        chains.append(F.Chain(steps_of(L), B=1, world=world, rank=r, max_ctas=nsm // world))
+    for c in chains:
+        c.set_peer_chains(chains)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    for rep in range(3):   # arena parity cycles; the DONE protocol orders the runs
+        for c, s in zip(chains, streams):
+            c.run(x, stream=s)
+    torch.cuda.synchronize()
+    for c in chains:
+        for s, outs in enumerate(ref):
+            for l, want in enumerate(outs):
+                got = c.output(s, l, out_dtype=torch.int64)
+                assert torch.equal(got, want), (world, s, l)
+    for c in chains:
+        c.free()
+    single.free()
+
+
+def test_chain_out_of_range_partial_is_flagged(F):
+    """A K-split partial beyond |v| < 2^18 (value units) is not silently
+    clamped: the run's float outputs are NaN and check() raises FASQ_E_RANGE;
+    the flag clears and the next in-range run is clean."""
+    fo, fi = 256, 512
+    cb = np.full((fi // 2, 16, 2), 60000.0, np.float16)
+    idx = np.zeros((fi // 2, fo), np.uint8)
+    L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), fi)
+    ch = F.Chain([([L], None)], B=1)
+    x = torch.full((1, fi), 8.0, dtype=torch.float16, device="cuda")   # 512 * 60000 * 8 >> 2^18
+    ch.run(x)
+    y = ch.output(0, 0, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert torch.isnan(y).all()
+    with pytest.raises(F.FasqError) as e:
+        ch.check()
+    assert e.value.code == -9
+    ch.run(torch.full((1, fi), 1e-4, dtype=torch.float16, device="cuda"))
+    y = ch.output(0, 0, out_dtype=torch.float32)
+    ch.check()
+    assert torch.isfinite(y).all()
+    ch.free()
+
+
+def test_chain_run_host_end_to_end(F, oracle_lib):
+    """fasq_chain_run_host: host x in, host y out (H2D, chain, D2H)."""
+    cb, idx = synth.random_layer(768, 1024, 2, 256, seed=61)
+    L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), 1024)
+    ch = F.Chain([([L], None)], B=2)
+    x = synth.activation(2, 1024, seed=62)
+    y = torch.empty((2, 768), dtype=torch.float32).pin_memory()
+    ch.run_host(torch.from_numpy(x).pin_memory(), y, 0, 0)
+    ok, info = parity_ok(y.numpy(), oracle_lib.gemv(cb, idx, x), x, 1024)
+    assert ok, info
+    with pytest.raises(F.FasqError):
+        ch.run(torch.zeros((2, 1000), dtype=torch.float16, device="cuda"))   # shape checked in the binding
+    ch.free()
+
+
 def _ipc_worker(rank, world, port, q):
     import os
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))

@@ -1,0 +1,324 @@
+"""Whole-model greedy decode (fasq_llama_*) vs the fp64 oracle (oracle/llama.py).
+
+The oracle runs the same seeded model end to end on its own (no value from
+the CUDA path enters it): embedding of the start token, every decoder block
+(RMSNorm -> PQ q/k/v -> RoPE + KV cache + attention -> PQ o + residual ->
+RMSNorm -> PQ gate/up -> SwiGLU -> PQ down + residual), final RMSNorm, fp16
+lm_head, greedy argmax -- for several steps with the KV cache growing.  The
+GPU executor's intermediates (chain outputs) and logits are compared at every
+step; tokens must match (the seeds give clear top-1 margins, asserted).
+
+Tolerances: the PQ products keep north_star's
+rel-L2 <= 1e-3 / max-abs <= 5e-3*||x||_inf*sqrt(K) against the oracle's own
+fp16 input; hidden states, attention outputs and logits rel-L2 <= 1e-3.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from fasq_testutil import parity_ok
+from oracle import llama as ol
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def F():
+    import paper_2605_04084_b200 as F
+    return F
+
+
+def make_model(cfg, seed):
+    """Seeded synthetic Llama-shaped model (numpy): PQ layers with uniform
+    random indices and N(0, 1/F_in) codebooks (synth.random_layer), fp16 norm
+    weights ~ 1 + N(0, 0.1^2), embedding ~ N(0, 1), lm_head ~ N(0, 1/hidden)."""
+    rng = np.random.default_rng(seed)
+    hd, H, KV, hid, ffn = cfg["head_dim"], cfg["n_heads"], cfg["n_kv"], cfg["hidden"], cfg["ffn"]
+    shapes = {"q": (H * hd, hid), "k": (KV * hd, hid), "v": (KV * hd, hid), "o": (hid, H * hd),
+              "gate": (ffn, hid), "up": (ffn, hid), "down": (hid, ffn)}
+    layers = []
+    s = seed * 1000
+    for _ in range(cfg["n_layers"]):
+        L = {}
+        for n, (fo, fi) in shapes.items():
+            L[n] = synth.random_layer(fo, fi, cfg["d"], cfg["C"], seed=s)
+            s += 1
+        L["attn_norm"] = (1.0 + 0.1 * rng.normal(size=hid)).astype(np.float16)
+        L["mlp_norm"] = (1.0 + 0.1 * rng.normal(size=hid)).astype(np.float16)
+        layers.append(L)
+    final_norm = (1.0 + 0.1 * rng.normal(size=hid)).astype(np.float16)
+    embed = rng.normal(size=(cfg["vocab"], hid)).astype(np.float16)
+    lm_head = (rng.normal(size=(cfg["vocab"], hid)) / np.sqrt(hid)).astype(np.float16)
+    return layers, final_norm, embed, lm_head
+
+
+def prompt_cache(cfg, B, P0, seed):
+    """Seeded KV cache of the prompt positions [0, P0): fp16 N(0, 1)."""
+    rng = np.random.default_rng(seed)
+    n = (cfg["n_layers"], B, cfg["n_kv"], P0, cfg["head_dim"])
+    return rng.normal(size=n).astype(np.float16), rng.normal(size=n).astype(np.float16)
+
+
+def shard(cfg, layers, lm_head, rank, world):
+    """This rank's Megatron shards of the numpy model (heads / ffn / vocab)."""
+    hd, d = cfg["head_dim"], cfg["d"]
+    Hl, KVl, Fl = cfg["n_heads"] // world, cfg["n_kv"] // world, cfg["ffn"] // world
+    out = []
+    for L in layers:
+        S = dict(L)
+        for n, rows in (("q", Hl * hd), ("k", KVl * hd), ("v", KVl * hd), ("gate", Fl), ("up", Fl)):
+            cb, idx = L[n]
+            S[n] = (cb, np.ascontiguousarray(idx[:, rank * rows:(rank + 1) * rows]))
+        for n, cols in (("o", Hl * hd), ("down", Fl)):
+            cb, idx = L[n]
+            s0, s1 = rank * cols // d, (rank + 1) * cols // d
+            S[n] = (np.ascontiguousarray(cb[s0:s1]), np.ascontiguousarray(idx[s0:s1]))
+        out.append(S)
+    V = cfg["vocab"] // world
+    return out, np.ascontiguousarray(lm_head[rank * V:(rank + 1) * V])
+
+
+def build_gpu(F, cfg, layers, final_norm, embed, lm_head, B, world=1, rank=0, max_ctas=0, max_T=64):
+    glayers = []
+    for L in layers:
+        G = {}
+        for n in ("q", "k", "v", "o", "gate", "up", "down"):
+            cb, idx = L[n]
+            G[n] = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), idx.shape[0] * cfg["d"])
+        G["attn_norm"] = torch.from_numpy(L["attn_norm"]).cuda()
+        G["mlp_norm"] = torch.from_numpy(L["mlp_norm"]).cuda()
+        glayers.append(G)
+    return F.Llama(glayers, torch.from_numpy(final_norm).cuda(), torch.from_numpy(embed).cuda(),
+                   torch.from_numpy(lm_head).cuda(), cfg["n_heads"], cfg["n_kv"], cfg["head_dim"], cfg["vocab"],
+                   rms_eps=1e-5, rope_theta=cfg["theta"], max_T=max_T, B=B, world=world, rank=rank,
+                   max_ctas=max_ctas)
+
+
+def oracle_decode(cfg, layers, final_norm, embed, lm_head, kc, vc, tokens, P0, n_steps):
+    """The oracle's greedy decode of B sequences for n_steps steps from the
+    prompt cache; returns per step the intermediates, logits and tokens."""
+    B = len(tokens)
+    kc = [[list(kc[l, b]) for b in range(B)] for l in range(cfg["n_layers"])]
+    vc = [[list(vc[l, b]) for b in range(B)] for l in range(cfg["n_layers"])]
+    # caches as per-(layer, b, kv) python lists of rows
+    kcache = [[[list(np.asarray(kc[l][b][j], np.float64)) for j in range(cfg["n_kv"])] for b in range(B)]
+              for l in range(cfg["n_layers"])]
+    vcache = [[[list(np.asarray(vc[l][b][j], np.float64)) for j in range(cfg["n_kv"])] for b in range(B)]
+              for l in range(cfg["n_layers"])]
+    steps = []
+    toks = list(tokens)
+    for st in range(n_steps):
+        pos = P0 + st
+        rec = {"blocks": [], "h0": [], "tok_in": list(toks)}
+        hs = [np.asarray(embed[t], np.float64) for t in toks]
+        rec["h0"] = [h.copy() for h in hs]
+        for l, L in enumerate(layers):
+            rb = []
+            for b in range(B):
+                K = [np.array(kcache[l][b][j]) for j in range(cfg["n_kv"])]
+                V = [np.array(vcache[l][b][j]) for j in range(cfg["n_kv"])]
+                r = ol.block_decode(hs[b], L, pos, K, V, cfg["n_heads"], cfg["n_kv"], 1e-5, cfg["theta"])
+                for j in range(cfg["n_kv"]):
+                    kcache[l][b][j].append(r["k_new"][j])
+                    vcache[l][b][j].append(r["v_new"][j])
+                hs[b] = r["h_out"]
+                rb.append(r)
+            rec["blocks"].append(rb)
+        rec["logits"] = [ol.lm_head_logits(hs[b], final_norm, lm_head, 1e-5) for b in range(B)]
+        toks = [ol.greedy(lg) for lg in rec["logits"]]
+        rec["tok_out"] = list(toks)
+        steps.append(rec)
+    return steps
+
+
+def _rel(y, ref):
+    y, ref = np.asarray(y, np.float64), np.asarray(ref, np.float64)
+    return float(np.linalg.norm(y - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+def check_step(model, rec, cfg, B, tol=1e-3):
+    """Compares every chain output of the last GPU step with the oracle's step."""
+    acc = lambda s, l=0: model.output(s, l, out_dtype=torch.int64).cpu().numpy().astype(np.float64) * 2.0 ** -32
+    h0 = acc(0)
+    for b in range(B):
+        assert np.array_equal(h0[b], np.asarray(rec["h0"][b], np.float64)), "embedding row"
+    for l in range(cfg["n_layers"]):
+        base = 1 + 5 * l
+        for b in range(B):
+            r = rec["blocks"][l][b]
+            for li, n in enumerate(("q", "k", "v")):
+                y = acc(base, li)[b]
+                ok, info = parity_ok(y, r[n], r["x"], cfg["hidden"])
+                assert ok, (l, b, n, info)
+            assert _rel(acc(base + 1)[b], r["attn"]) <= tol, (l, b, "attn", _rel(acc(base + 1)[b], r["attn"]))
+            assert _rel(acc(base + 2)[b], r["h_mid"]) <= tol, (l, b, "h_mid")
+            for li, n in enumerate(("gate", "up")):
+                ok, info = parity_ok(acc(base + 3, li)[b], r[n], r["xm"], cfg["hidden"])
+                assert ok, (l, b, n, info)
+            assert _rel(acc(base + 4)[b], r["h_out"]) <= tol, (l, b, "h_out")
+
+
+SMALL = dict(n_layers=2, hidden=256, n_heads=4, n_kv=2, head_dim=64, ffn=512, vocab=1000, d=2, C=64,
+             theta=10000.0)
+
+
+@pytest.mark.parametrize("B", [1, 2])
+def test_llama_decode_matches_oracle(F, B):
+    cfg = SMALL
+    layers, fn, emb, lm = make_model(cfg, seed=11)
+    P0, n_steps = 5, 3
+    kc, vc = prompt_cache(cfg, B, P0, seed=12)
+    tokens = [17, 503][:B]
+    ref = oracle_decode(cfg, layers, fn, emb, lm, kc, vc, tokens, P0, n_steps)
+    model = build_gpu(F, cfg, layers, fn, emb, lm, B)
+    for l in range(cfg["n_layers"]):
+        K, V = model.kv_cache(l)
+        K[:, :, :P0].copy_(torch.from_numpy(kc[l]).cuda())
+        V[:, :, :P0].copy_(torch.from_numpy(vc[l]).cuda())
+    logits = model.enable_logits(True)
+    model.reset(tokens, P0)
+    for st in range(n_steps):
+        model.step()
+        torch.cuda.synchronize()
+        rec = ref[st]
+        check_step(model, rec, cfg, B)
+        lg = logits.cpu().numpy()
+        for b in range(B):
+            assert _rel(lg[b], rec["logits"][b]) <= 1e-3
+            top2 = np.sort(rec["logits"][b])[-2:]
+            assert top2[1] - top2[0] > 1e-2, "seed gives a near tie; pick another"
+        assert model.tokens().cpu().tolist() == rec["tok_out"], (st, rec["tok_out"])
+    hist = model.token_history().cpu().numpy()
+    for st in range(n_steps):
+        assert hist[:, P0 + st].tolist() == ref[st]["tok_in"]
+    # the KV cache holds the oracle's new rows (fp16)
+    K, _ = model.kv_cache(0)
+    kn = K[:, :, P0].cpu().numpy().astype(np.float64)
+    for b in range(B):
+        assert _rel(kn[b], ref[0]["blocks"][0][b]["k_new"]) <= 2e-3
+    model.free()
+
+
+def test_llama_decode_deterministic_and_replayable(F):
+    """Same start -> bit-identical outputs; the whole step replays from a CUDA
+    graph (the position and tokens advance on the device)."""
+    cfg = SMALL
+    layers, fn, emb, lm = make_model(cfg, seed=21)
+    model = build_gpu(F, cfg, layers, fn, emb, lm, 1)
+    runs = []
+    for rep in range(2):
+        model.reset([5], 0)
+        for _ in range(4):
+            model.step()
+        torch.cuda.synchronize()
+        runs.append((model.output(5 * cfg["n_layers"], 0, out_dtype=torch.int64).clone(),
+                     model.token_history()[:, :4].clone()))
+    assert torch.equal(runs[0][0], runs[1][0]) and torch.equal(runs[0][1], runs[1][1])
+    # graph replay of 4 steps from the same start gives the same tokens
+    model.reset([5], 0)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            model.step(stream=s)
+    torch.cuda.synchronize()
+    model.reset([5], 0)
+    for _ in range(4):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(model.token_history()[:, :4], runs[0][1])
+    # step_host (end-to-end host API) continues the sequence
+    t = model.step_host()
+    assert 0 <= t[0] < cfg["vocab"]
+    model.free()
+
+
+@pytest.mark.parametrize("parts", ["1", "2", "8"])
+def test_llama_attention_split_invariance(F, monkeypatch, parts):
+    """The cache-length split (FASQ_ATTN_PARTS) changes only rounding."""
+    cfg = SMALL
+    layers, fn, emb, lm = make_model(cfg, seed=31)
+    P0 = 40
+    kc, vc = prompt_cache(cfg, 1, P0, seed=32)
+    ref = oracle_decode(cfg, layers, fn, emb, lm, kc, vc, [9], P0, 1)
+    monkeypatch.setenv("FASQ_ATTN_PARTS", parts)
+    model = build_gpu(F, cfg, layers, fn, emb, lm, 1)
+    for l in range(cfg["n_layers"]):
+        K, V = model.kv_cache(l)
+        K[:, :, :P0].copy_(torch.from_numpy(kc[l]).cuda())
+        V[:, :, :P0].copy_(torch.from_numpy(vc[l]).cuda())
+    model.reset([9], P0)
+    model.step()
+    torch.cuda.synchronize()
+    check_step(model, ref[0], cfg, 1)
+    model.free()
+
+
+def test_llama_tensor_parallel_emulated(F):
+    """world = 2 Megatron shards as two models of one process on one GPU
+    (max_ctas = SMs / 2 each, concurrent streams, peers wired in-process):
+    the fused all-reduce (o, down) and the cross-rank argmax give the oracle's
+    tokens and hidden states on both ranks."""
+    cfg = SMALL
+    world = 2
+    layers, fn, emb, lm = make_model(cfg, seed=41)
+    P0, n_steps = 6, 2
+    kc, vc = prompt_cache(cfg, 1, P0, seed=42)
+    ref = oracle_decode(cfg, layers, fn, emb, lm, kc, vc, [33], P0, n_steps)
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    models = []
+    for r in range(world):
+        sl, slm = shard(cfg, layers, lm, r, world)
+        m = build_gpu(F, cfg, sl, fn, emb, slm, 1, world=world, rank=r, max_ctas=nsm // world)
+        kvl = cfg["n_kv"] // world
+        for l in range(cfg["n_layers"]):
+            K, V = m.kv_cache(l)
+            K[:, :, :P0].copy_(torch.from_numpy(kc[l][:, r * kvl:(r + 1) * kvl]).cuda())
+            V[:, :, :P0].copy_(torch.from_numpy(vc[l][:, r * kvl:(r + 1) * kvl]).cuda())
+        models.append(m)
+    for m in models:
+        m.set_peer_models(models)
+    for m in models:
+        m.reset([33], P0)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    for st in range(n_steps):
+        torch.cuda.synchronize()
+        for m, s in zip(models, streams):
+            m.step(stream=s)
+        torch.cuda.synchronize()
+        for m in models:
+            assert m.tokens().cpu().tolist() == ref[st]["tok_out"], st
+            h = m.output(5 + 5 * (cfg["n_layers"] - 1), 0, out_dtype=torch.float32).cpu().numpy()[0]
+            assert _rel(h, ref[st]["blocks"][-1][0]["h_out"]) <= 1e-3
+    for m in models:
+        m.free()
+
+
+LLAMA3 = dict(n_layers=1, hidden=4096, n_heads=32, n_kv=8, head_dim=128, ffn=14336, vocab=128256, d=2, C=256,
+              theta=500000.0)
+
+
+def test_llama3_block_full_size(F):
+    """One Llama-3-8B-shaped block at full size with the full 128256-token fp16
+    lm_head (the bench's kernel configuration: 148 CTAs, attention split over
+    the cache), prompt of 128 positions, two decode steps."""
+    cfg = LLAMA3
+    layers, fn, emb, lm = make_model(cfg, seed=51)
+    P0 = 128
+    kc, vc = prompt_cache(cfg, 1, P0, seed=52)
+    ref = oracle_decode(cfg, layers, fn, emb, lm, kc, vc, [128000], P0, 2)
+    model = build_gpu(F, cfg, layers, fn, emb, lm, 1, max_T=256)
+    K, V = model.kv_cache(0)
+    K[:, :, :P0].copy_(torch.from_numpy(kc[0]).cuda())
+    V[:, :, :P0].copy_(torch.from_numpy(vc[0]).cuda())
+    logits = model.enable_logits(True)
+    model.reset([128000], P0)
+    for st in range(2):
+        model.step()
+        torch.cuda.synchronize()
+        check_step(model, ref[st], cfg, 1)
+        assert _rel(logits.cpu().numpy()[0], ref[st]["logits"][0]) <= 1e-3
+        assert model.tokens().cpu().tolist() == ref[st]["tok_out"]
+    model.free()
