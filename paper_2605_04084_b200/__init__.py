@@ -340,6 +340,7 @@ class Chain:
         self.B = B
         self.world, self.rank = world, rank
         self.steps = [(list(l), s) for (l, s) in steps]
+        self.n_steps = len(self.steps)
 
     @property
     def in_features(self) -> int:
@@ -414,7 +415,7 @@ class Chain:
         """Diagnostics: record %globaltimer stamps into ``buf`` (int64
         [steps][ctas][4]) on every later run; None turns it off."""
         if buf is not None:
-            if buf.dtype != torch.int64 or not buf.is_cuda or buf.numel() < len(self.steps) * self.ctas * 4:
+            if buf.dtype != torch.int64 or not buf.is_cuda or buf.numel() < self.n_steps * self.ctas * 4:
                 raise ValueError("trace buffer: cuda int64 [steps][ctas][4]")
         self._trace_buf = buf
         _check(lib.fasq_chain_trace(self._h, None if buf is None else buf.data_ptr()))
@@ -517,6 +518,7 @@ class Llama:
         self.chain = Chain.__new__(Chain)
         self.chain._h = ctypes.c_void_p(lib.fasq_llama_chain(self._h))
         self.chain._owned = False
+        self.chain.n_steps = 1 + 5 * n
         self.chain.B, self.chain.world, self.chain.rank = B, world, rank
         self._logits = None
 

@@ -362,9 +362,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     uint8_t* s_cb = smem;                                       // PAIR: CS * 64 KiB, else ST * cbb_max
     uint8_t* s_idx = s_cb + (PAIR ? CS * kPairSlot : ST * p.cbb_max);   // ST * R * 32
     uint8_t* s_x = s_idx + ST * R * 32;                         // gmax * XG
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_x + p.gmax * XG);
-    float* s_red = reinterpret_cast<float*>(bars + 2 * (ST + CS));   // [NW][8] norm reduction scratch
-    float* s_scale = s_red + NW * 8;                                 // [8] RMSNorm scales
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_x + max(p.gmax * XG, NW * 8 * 4));
+    // RMSNorm reduction scratch [NW][8] aliases the x staging area: norm_scale
+    // finishes (bar.sync) before stage_x writes s_x, and every warp is past
+    // the previous item (consumer_bar at the item start).  The planner sizes
+    // s_x >= NW*8 floats.  The fixed scratch stays <= 96 B: at gmax = 13 the
+    // d = 2 plan has 240 B left for a 3-deep ring.
+    float* s_red = reinterpret_cast<float*>(s_x);
+    float* s_scale = reinterpret_cast<float*>(bars + 2 * (ST + CS));  // [8] RMSNorm scales
     int* s_tok = reinterpret_cast<int*>(s_scale + 8);                // [8] EMBED tokens
     unsigned& s_run = *reinterpret_cast<unsigned*>(s_tok + 8);       // run index
     int& s_pos = *reinterpret_cast<int*>(s_tok + 9);                 // model position
@@ -496,6 +501,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         const int ph = phj / p.mi, j = phj % p.mi;
         const ChainItem w = p.items[((size_t)ph * p.nctas + blockIdx.x) * p.mi + j];
         const ChainPhase* phs = p.phases + ph;
+        // the PQ fields of the phase by value: their loads issue here, next to
+        // the item's, before the barrier -- not as dependent L2 round trips
+        // after it (~1 us per step when they were pointer reads)
+        const ChainPhase pv = *phs;
         unsigned long long* tr = p.trace ? p.trace + ((size_t)ph * p.nctas + blockIdx.x) * 4 : nullptr;
         if (tr && threadIdx.x == 0 && j == 0) tr[0] = dev::globaltimer();
         if (w.kind < 0) continue;
@@ -520,23 +529,23 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             continue;
         }
         const int ng = w.g_end - w.g_begin;
-        const int in_mode = phs->in_mode;
-        const bool xsys = phs->x_sys != 0;
+        const int in_mode = pv.in_mode;
+        const bool xsys = pv.x_sys != 0;
         if (in_mode == IN_EXT) {
-            core::stage_x<D, NB, NW, XF>(s_x, p.x_ext, 0, phs->F_in, p.B, w.N_ss, w.g_begin, ng);
+            core::stage_x<D, NB, NW, XF>(s_x, p.x_ext, 0, pv.F_in, p.B, w.N_ss, w.g_begin, ng);
         } else if (in_mode == IN_WORDS) {
-            core::stage_x_counted<D, NB, NW, XF>(s_x, cur + phs->x_off, phs->x_ks, phs->F_in, p.B, w.N_ss, w.g_begin,
+            core::stage_x_counted<D, NB, NW, XF>(s_x, cur + pv.x_off, pv.x_ks, pv.F_in, p.B, w.N_ss, w.g_begin,
                                                  ng, xsys, p.backoff);
         } else if constexpr (PAIR) {
             if (in_mode == IN_RMSNORM) {
-                core::norm_scale<NB, NW>(cur + phs->x_off, phs->x_ks, phs->F_in, p.B, phs->eps, xsys, s_red, s_scale);
-                core::stage_x_counted<D, NB, NW, XF, core::XM_NORM>(s_x, cur + phs->x_off, phs->x_ks, phs->F_in, p.B,
+                core::norm_scale<NB, NW>(cur + pv.x_off, pv.x_ks, pv.F_in, p.B, pv.eps, xsys, s_red, s_scale);
+                core::stage_x_counted<D, NB, NW, XF, core::XM_NORM>(s_x, cur + pv.x_off, pv.x_ks, pv.F_in, p.B,
                                                                     w.N_ss, w.g_begin, ng, xsys, 0, nullptr, 0,
-                                                                    s_scale, phs->gamma);
+                                                                    s_scale, pv.gamma);
             } else {
-                core::stage_x_counted<D, NB, NW, XF, core::XM_SILU>(s_x, cur + phs->x_off, phs->x_ks, phs->F_in, p.B,
+                core::stage_x_counted<D, NB, NW, XF, core::XM_SILU>(s_x, cur + pv.x_off, pv.x_ks, pv.F_in, p.B,
                                                                     w.N_ss, w.g_begin, ng, xsys, 0,
-                                                                    cur + phs->x2_off, phs->x2_ks);
+                                                                    cur + pv.x2_off, pv.x2_ks);
             }
         }
         if (tr && threadIdx.x == 0 && j == 0) tr[1] = dev::globaltimer();
@@ -570,13 +579,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             }
             core::reduce_set<NB, G>(acc, lane);
             if (active) {
-                const bool add_res = phs->res_off >= 0 && phs->res_here && w.kidx == 0;
+                const bool add_res = pv.res_off >= 0 && pv.res_here && w.kidx == 0;
                 long long qv[2 * NB];
                 const long long off = (long long)par * p.arena_words + w.y_off + w.row0_g;
                 core::set_values<NB, G>(acc, qv, w.r0 + wrow0, lane, w.F_out, p.B,
-                                        add_res ? cur + phs->res_off + w.row0_g : nullptr, w.ld, phs->res_ks,
-                                        phs->res_sys != 0, ovf);
-                if (phs->out_all) {
+                                        add_res ? cur + pv.res_off + w.row0_g : nullptr, w.ld, pv.res_ks,
+                                        pv.res_sys != 0, ovf);
+                if (pv.out_all) {
                     for (int q = 0; q < p.world; ++q)
                         core::counted_store_q<NB>(qv, p.peers[q] + off, w.r0 + wrow0, lane, w.F_out, w.ld, p.B,
                                                   sys_out);
@@ -607,9 +616,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             core::reduce_rows<NB, RW>(acc, tot, lane);
             if (active) {
                 const long long off = (long long)par * p.arena_words + w.y_off + w.row0_g;
-                const int nq = phs->out_all ? p.world : 1;
+                const int nq = pv.out_all ? p.world : 1;
                 for (int q = 0; q < nq; ++q)
-                    core::counted_store<NB, RW>(tot, p.peers[phs->out_all ? q : p.rank] + off, w.r0 + wrow0, w.F_out,
+                    core::counted_store<NB, RW>(tot, p.peers[pv.out_all ? q : p.rank] + off, w.r0 + wrow0, w.F_out,
                                                 w.ld, p.B, ovf);
             }
         }
@@ -637,7 +646,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
 }
 
 constexpr size_t kChainSmem = kSmemMax;
-constexpr size_t kChainScratch = 16 * 8 * 4 + 128;   // s_red, s_scale, s_tok, run/pos/flag words (after the mbarriers)
+constexpr size_t kChainScratch = 8 * 4 + 8 * 4 + 16;   // s_scale, s_tok, run/pos/flag words (after the mbarriers)
 
 template <int D, int NB, int NW, int ST>
 fasq_status launch_chain_t(const ChainParams& p, size_t smem, int grid, cudaStream_t st) {
@@ -1014,11 +1023,15 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
             items[((size_t)s * c->nctas + q % c->nctas) * c->mi + q / c->nctas] = per_step[s][q];
     const size_t xg = (pair && NB == 8) ? (size_t)32 * NB * c->d * 4 : (size_t)32 * NB * E;   // k_chain XG
     auto smem_of = [&](int stg) {
-        return cbring(stg) + (size_t)stg * c->R * 32 + (size_t)c->gmax * xg + 16 * (stg + kChainCS) + kChainScratch;
+        const size_t sx = std::max((size_t)c->gmax * xg, (size_t)c->nw * 8 * 4);   // x staging / norm scratch
+        return cbring(stg) + (size_t)stg * c->R * 32 + sx + 16 * (stg + kChainCS) + kChainScratch;
     };
     while (c->st > 1 && smem_of(c->st) > kChainSmem) --c->st;
     c->smem = smem_of(c->st);
     if (c->smem > kChainSmem) return fail(FASQ_E_UNSUPPORTED, "SMEM plan too large");
+    if (getenv("FASQ_CHAIN_VERBOSE"))
+        fprintf(stderr, "chain plan: %d steps, %d CTAs, nw=%d st=%d R=%d gmax=%d mi=%d smem=%zu arena_words=%lld\n",
+                n_steps, c->nctas, c->nw, c->st, c->R, c->gmax, c->mi, c->smem, (long long)words);
     if (model) {   // attention scratch lives in a 64 KiB pair slot
         for (int s = 0; s < n_steps; ++s)
             if (steps[s].kind == SK_ATTN) {
