@@ -50,32 +50,38 @@ namespace fasq {
 
 namespace {
 
-struct ChainItem {
+// Work item of one CTA in one step.  The consumer fields come first (loaded
+// by value at the item start, next to the phase); the epilogue fields are
+// re-read through the item pointer after the gather loop (same 128-B line,
+// an L1 hit) instead of occupying registers across it.
+struct alignas(128) ChainItem {
+    int kind;                   // SK_* ; -1: no item
+    int g_begin, g_end, rows_valid;
+    int N_ss, r0, kidx, head;   // kidx: PQ K-range index in its row tile (0 adds the residual); ATTN: cache part
+    int nsq;                    // PQ: RMSNorm sum-of-squares slot this item contributes (-1: none)
+    int F_out, ld, row0_g;      // local rows, words per batch row of the output, output index of local row 0
+    long long y_off;            // word offset of the output [B][ld] in a buffer
+    // producer
     const uint8_t* idx;
     const uint8_t* cbimg;
     const void* cbmap;          // d <= 2: 3-D tensor map {32 words, n_groups, C} over cbimg (pair boxes)
-    long long y_off;            // word offset of the output [B][ld] in a buffer
-    int F_out, ld, row0_g;      // local rows, words per batch row of the output, output index of local row 0
-    int F_out_pad, N_ss, C;
-    int r0, rows_valid, g_begin, g_end;
-    int kidx;                   // PQ: K-range index in its row tile (0 adds the residual); ATTN: cache part
-    int head;                   // ATTN: local q head
-    int kind;                   // -1: no item
+    int F_out_pad, C;
 };
 
-struct ChainPhase {
-    int kind, in_mode, F_in;
-    long long x_off, x2_off;    // input words (WORDS/NORM: x; SILU: gate x, up x2)
-    int x_ks, x2_ks;
-    int x_sys;                  // input words written by peers (system-scope polls)
-    const __half* gamma;
-    float eps;
+// Per-step description.  The PQ fields fill the first 128-B line.
+struct alignas(128) ChainPhase {
+    int kind, in_mode, F_in, x_ks;
+    long long x_off, x2_off;    // input words (WORDS/NORM/ATTN: x; SILU: gate x, up x2)
+    int x2_ks, x_sys, res_ks, res_here;   // x_sys: input words written by peers (system-scope polls)
+    const __half* gamma;        // IN_RMSNORM
     long long res_off;          // residual words (< 0: none), same [B][ld] indexing as the output
-    int res_ks, res_here, res_sys;
-    int out_all;                // outputs red.add'ed into every rank's arena
+    long long nsq_off;          // IN_RMSNORM: sum-of-squares slots [B][64]
+    int nsq_n, res_sys, out_all, a_heads;   // out_all: outputs red.add'ed into every rank's arena
+    float eps;
+    int a_hd, a_parts;          // IN_ATTN: layout of the source attention partials
     // ATTN
     long long q_off, k_off, v_off, o_off;
-    int q_ks, k_ks, v_ks, q_ld, kv_ld, o_ld;
+    int q_ks, k_ks, v_ks, q_ld, kv_ld;
     __half* kc;
     __half* vc;
     int n_heads, n_kv, hd, parts;
@@ -83,6 +89,19 @@ struct ChainPhase {
     const __half* embed;
     long long e_off;
     int hidden;
+};
+
+// Epilogue parameters of the current item, kept in SMEM (one copy per CTA)
+// rather than in 512 threads' registers across the gather loop: with 227 KiB
+// of SMEM the L1 left for register spills is small, and spills in the loop
+// cost more than the loop saves.
+struct EpiParams {
+    long long y_off, res_off, nsq_off;
+    int row0_g, ld, F_out, r0;
+    int add_res, res_ks, res_sys, out_all;
+    int nsq_n, F_in;
+    float eps;
+    int in_mode;
 };
 
 struct ChainParams {
@@ -106,8 +125,6 @@ struct ChainParams {
     int max_T, pos_wrap;
     int* tok_hist;
     long long tok_expect;
-    float* part_buf;
-    unsigned* part_cnt;
 };
 
 template <int D>
@@ -115,18 +132,56 @@ struct ChainPair {
     static constexpr bool value = D <= 2;
 };
 constexpr int kChainCS = kPairSlots;
+// ATTN items: a codebook pair slot (64 KiB) holds the item's K/V cache rows
+// (prefetched by the producer warp while earlier steps run) in its first
+// kAttnKV bytes and the attention scratch after them.
+constexpr uint32_t kAttnKV = 40 * 1024;
+constexpr uint32_t kAttnScratchFixed = 5 * 128 * 4 + 4 * 128 * 4 + 64;   // q, k, v, q', k/v new, o row groups, m/l
 
 __device__ __forceinline__ void consumer_bar(int nt) { asm volatile("bar.sync 1, %0;" :: "r"(nt) : "memory"); }
 
 __device__ __forceinline__ unsigned long long cnt_word(long long v) {
     return (1ull << core::kCntShift) + (unsigned long long)(core::kCntBias + v);
 }
+// A single-contributor counted word carrying fp32 bits (count 1).
+__device__ __forceinline__ unsigned long long f32_word(float f) {
+    return (1ull << core::kCntShift) | (unsigned long long)__float_as_uint(f);
+}
+__device__ __forceinline__ float word_f32(unsigned long long v) { return __uint_as_float((unsigned)(v & 0xffffffffull)); }
+__device__ __forceinline__ void st_word(unsigned long long* a, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_word(const unsigned long long* a, bool sys) {
+    unsigned long long v;
+    if (sys) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    else asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+
+// Cache rows [t0, t1) of part `part` of P over Tn = pos + 1 positions, and the
+// rows [t0, te) (te = min(t1, pos)) that already sit in the cache; whether they
+// are staged in SMEM (same decision on the producer and the consumer side).
+struct AttnRows {
+    int t0, t1, te;
+    bool smem;
+};
+__device__ __forceinline__ AttnRows attn_rows(int part, int P, int pos, int B, int hd) {
+    AttnRows r;
+    const int Tn = pos + 1;
+    r.t0 = (int)((long long)part * Tn / P);
+    r.t1 = (int)((long long)(part + 1) * Tn / P);
+    r.te = min(r.t1, pos);
+    const long long kv = (long long)B * max(0, r.te - r.t0) * hd * 4;
+    r.smem = r.te > r.t0 && kv <= (long long)kAttnKV &&
+             kAttnKV + kAttnScratchFixed + (uint32_t)(r.t1 - r.t0 + 4) * 4u <= kPairSlot;
+    return r;
+}
 
 // ---- EMBED: h0[b] = embed[token_b] as counted words (count 1) ---------------
 // token_b = the key the previous run's lm_head red.max'ed into token slot
 // (par_prev, b), once all its contributions arrived; the slot is cleared for
 // the run after next and the token is appended to the history.
-__device__ __noinline__ void embed_item(const ChainPhase* ph, unsigned long long* cur, unsigned long long* tail,
+__device__ __forceinline__ void embed_item(const ChainPhase* ph, unsigned long long* cur, unsigned long long* tail,
                                         int B, unsigned run, int pos, int max_T, int* tok_hist,
                                         long long tok_expect, int NT, int* s_tok) {
     const int tid = threadIdx.x;
@@ -153,40 +208,55 @@ __device__ __noinline__ void embed_item(const ChainPhase* ph, unsigned long long
         const int b = i / n, c = i - b * n;
         const float v = __half2float(ph->embed[(size_t)s_tok[b] * n + c]);
         const long long q = __float2ll_rn(v * core::kAccScale);
-        asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(cur + ph->e_off + i), "l"(cnt_word(q)) : "memory");
+        st_word(cur + ph->e_off + i, cnt_word(q));
     }
 }
 
 // ---- ATTN: one (local q head, cache part) item ------------------------------
 // Llama attention for the token at `pos` (HF LlamaAttention semantics):
 // RoPE (rotate-half, cos/sin table) on q and k, the new fp16 k/v appended to
-// the KV cache at pos (by the first q head of each KV group), scores
-// q.k_t / sqrt(hd) over t <= pos, softmax, o = sum_t p_t v_t.  The cache
-// length is split into `parts` ranges over CTAs; each writes (max, sum,
-// unnormalised o) partials and the last of a head's parts to arrive merges
-// them in FIXED part order (deterministic) into counted output words.
-// scr: >= 48 KiB of SMEM scratch (a codebook pair slot handed over by the producer).
-__device__ __noinline__ void attn_item(const ChainPhase* ph, int head, int part, unsigned long long* cur, int B,
-                                       int pos, int max_T, const float2* rope, float* part_buf, unsigned* part_cnt,
-                                       float* scr, int NT, bool sys, unsigned* s_last) {
-    const int tid = threadIdx.x;
+// the KV cache at pos (by the first q head of each KV group, last part),
+// scores q.k_t / sqrt(hd) over t <= pos, softmax, o = sum_t p_t v_t.  The
+// cache length is split into `parts` ranges over CTAs; each writes its
+// unnormalised partial o, max m and sum l (fp32 bits in counted words); the
+// consumer (the o projection's x staging, stage_x_attn) merges the parts in
+// FIXED order -- no merge round trip here.  slot: a 64 KiB codebook pair slot
+// handed over by the producer, holding this item's cache rows [t0, te) for
+// every token b (K [B][nk][hd] then V) when r.smem.
+__device__ __forceinline__ void attn_item(const ChainPhase* ph, int head, int part, unsigned long long* cur, int B,
+                                       int pos, int max_T, const float2* rope, uint8_t* slot, int NT) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int hd = ph->hd, half = hd / 2;
     const int n_heads = ph->n_heads, n_kv = ph->n_kv, P = ph->parts;
     const int grp = n_heads / n_kv, kvh = head / grp;
-    const int Tn = pos + 1;
-    const int t0 = (int)((long long)part * Tn / P), t1 = (int)((long long)(part + 1) * Tn / P);
-    const int nrow = t1 - t0;
+    const AttnRows r = attn_rows(part, P, pos, B, hd);
+    const int nrow = r.t1 - r.t0, nk = max(0, r.te - r.t0);
     const float qk_scale = 1.0f / sqrtf((float)hd);
-    float* s_q = scr;                 // [hd] raw q, then rotated q
-    float* s_k = s_q + 256;           // [hd] raw k
-    float* s_v = s_k + 256;           // [hd] raw v
-    __half* s_kn = reinterpret_cast<__half*>(s_v + 256);   // [hd] new k (rotated, fp16)
-    __half* s_vn = s_kn + 256;                              // [hd] new v (fp16)
-    float* s_red = reinterpret_cast<float*>(s_vn + 256);    // [32][hd] row-group partials of o (16 KiB at hd=128)
-    float* s_sc = s_red + 32 * 256;                         // [nrow] scores / probabilities
-    float* s_w = s_sc + ((nrow + 3) & ~3);                  // [32] block-reduction scratch
-    const int nwarp = NT / 32, lane = tid & 31, warp = tid >> 5;
+    float* s_q = reinterpret_cast<float*>(slot + kAttnKV);   // [128] raw q
+    float* s_k = s_q + 128;                                  // [128] raw k
+    float* s_v = s_k + 128;                                  // [128] raw v
+    float* s_qr = s_v + 128;                                 // [128] rotated q
+    __half* s_kn = reinterpret_cast<__half*>(s_qr + 128);    // [128] new k (rotated, fp16)
+    __half* s_vn = s_kn + 128;                               // [128] new v (fp16)
+    float* s_o = reinterpret_cast<float*>(s_vn + 128);       // [4][128] row-group partials of o
+    float* s_ml = s_o + 4 * 128;                             // [2] m, l  (+ pad)
+    float* s_sc = s_ml + 16;                                 // [nrow] scores / probabilities
+    const __half* kv_k = reinterpret_cast<const __half*>(slot);
+    const __half* kv_v = kv_k + (size_t)B * nk * hd;
+    unsigned long long* out_base = cur + ph->o_off + (size_t)head * P * (hd + 2) + (size_t)part * (hd + 2);
+    const size_t out_bstride = (size_t)n_heads * P * (hd + 2);
     for (int b = 0; b < B; ++b) {
+        unsigned long long* ob = out_base + (size_t)b * out_bstride;
+        if (nrow <= 0) {   // empty part (Tn < parts): contributes nothing
+            if (tid < hd) st_word(ob + tid, f32_word(0.f));
+            if (tid == 0) st_word(ob + hd, f32_word(-INFINITY));
+            consumer_bar(NT);
+            if (tid == 0) {
+                __threadfence();
+                asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(ob + hd + 1), "l"(f32_word(0.f)) : "memory");
+            }
+            continue;
+        }
         // 1. q (this head), k and v (its KV head) from the counted words
         if (tid < 3 * hd) {
             const int which = tid / hd, e = tid - which * hd;
@@ -194,159 +264,206 @@ __device__ __noinline__ void attn_item(const ChainPhase* ph, int head, int part,
                 which == 0 ? cur + ph->q_off + (size_t)b * ph->q_ld + (size_t)head * hd + e
                            : cur + (which == 1 ? ph->k_off : ph->v_off) + (size_t)b * ph->kv_ld + (size_t)kvh * hd + e;
             const int ks = which == 0 ? ph->q_ks : which == 1 ? ph->k_ks : ph->v_ks;
-            const float f = (float)((double)core::poll_value(a, ks, sys) * core::kAccInv);
+            const float f = (float)((double)core::poll_value(a, ks, false) * core::kAccInv);
             (which == 0 ? s_q : which == 1 ? s_k : s_v)[e] = f;
         }
         consumer_bar(NT);
         // 2. RoPE (rotate half): x'[i] = x[i] c - x[i+half] s, x'[i+half] = x[i+half] c + x[i] s
-        float qr0 = 0.f, qr1 = 0.f;
+        __half* kc = ph->kc + ((size_t)b * n_kv + kvh) * (size_t)max_T * hd;
+        __half* vc = ph->vc + ((size_t)b * n_kv + kvh) * (size_t)max_T * hd;
+        const bool writer = head % grp == 0 && r.t1 == pos + 1;   // one cache writer per KV head
         if (tid < half) {
             const float2 cs = rope[(size_t)pos * half + tid];
             const float q0 = s_q[tid], q1 = s_q[tid + half], k0 = s_k[tid], k1 = s_k[tid + half];
-            qr0 = q0 * cs.x - q1 * cs.y;
-            qr1 = q1 * cs.x + q0 * cs.y;
-            s_kn[tid] = __float2half_rn(k0 * cs.x - k1 * cs.y);
-            s_kn[tid + half] = __float2half_rn(k1 * cs.x + k0 * cs.y);
-        }
-        if (tid < hd) s_vn[tid] = __float2half_rn(s_v[tid]);
-        consumer_bar(NT);
-        if (tid < half) { s_q[tid] = qr0; s_q[tid + half] = qr1; }
-        __half* kc = ph->kc + ((size_t)b * n_kv + kvh) * (size_t)max_T * hd;
-        __half* vc = ph->vc + ((size_t)b * n_kv + kvh) * (size_t)max_T * hd;
-        // 3. cache append at pos (one writer per KV head: the group's first q head, last part)
-        if (head % grp == 0 && t1 == Tn && tid < hd) {
-            kc[(size_t)pos * hd + tid] = s_kn[tid];
-            vc[(size_t)pos * hd + tid] = s_vn[tid];
+            s_qr[tid] = q0 * cs.x - q1 * cs.y;
+            s_qr[tid + half] = q1 * cs.x + q0 * cs.y;
+            const __half kn0 = __float2half_rn(k0 * cs.x - k1 * cs.y), kn1 = __float2half_rn(k1 * cs.x + k0 * cs.y);
+            s_kn[tid] = kn0;
+            s_kn[tid + half] = kn1;
+            if (writer) { kc[(size_t)pos * hd + tid] = kn0; kc[(size_t)pos * hd + tid + half] = kn1; }
+        } else if (tid < half + hd) {
+            const int e = tid - half;
+            const __half vn = __float2half_rn(s_v[e]);
+            s_vn[e] = vn;
+            if (writer) vc[(size_t)pos * hd + e] = vn;
         }
         consumer_bar(NT);
-        // 4. scores: thread (row group r = tid / 16, chunk c = tid % 16 of 8 dims)
-        const int nch = hd / 8;          // 16-B chunks per row (hd <= 128 -> <= 16)
-        const int rpi = NT / 16;         // rows per iteration (32 with 512 threads)
-        const int c = tid & 15, r = tid >> 4;
-        float qv[8];
+        // 3. scores: 16 lanes per row (8 dims each), NT/16 rows per pass
+        {
+            const int nch = hd / 8;
+            const int c = tid & 15, rr = tid >> 4, rpi = NT / 16;
+            float qv[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) qv[i] = c < nch ? s_q[c * 8 + i] : 0.f;
-        for (int base = 0; base < nrow; base += 4 * rpi) {
-            uint4 kv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int t = t0 + base + r + u * rpi;
-                kv[u] = make_uint4(0u, 0u, 0u, 0u);
-                if (c < nch && t < t1)
-                    kv[u] = t == pos ? *reinterpret_cast<const uint4*>(s_kn + c * 8)
-                                     : __ldcg(reinterpret_cast<const uint4*>(kc + (size_t)t * hd + c * 8));
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const __half* kh = reinterpret_cast<const __half*>(&kv[u]);
+            for (int i = 0; i < 8; ++i) qv[i] = c < nch ? s_qr[c * 8 + i] : 0.f;
+            for (int base = 0; base < nrow; base += rpi) {
+                const int t = r.t0 + base + rr;
+                uint4 kv = make_uint4(0u, 0u, 0u, 0u);
+                if (c < nch && t < r.t1) {
+                    if (t == pos) kv = *reinterpret_cast<const uint4*>(s_kn + c * 8);
+                    else if (r.smem) kv = *reinterpret_cast<const uint4*>(kv_k + ((size_t)b * nk + (t - r.t0)) * hd + c * 8);
+                    else kv = __ldcg(reinterpret_cast<const uint4*>(kc + (size_t)t * hd + c * 8));
+                }
+                const __half* kh = reinterpret_cast<const __half*>(&kv);
                 float dsum = 0.f;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) dsum += qv[i] * __half2float(kh[i]);
 #pragma unroll
                 for (int m = 8; m >= 1; m >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, m);
-                const int t = t0 + base + r + u * rpi;
-                if (c == 0 && t < t1) s_sc[t - t0] = dsum * qk_scale;
+                if (c == 0 && t < r.t1) s_sc[t - r.t0] = dsum * qk_scale;
             }
         }
         consumer_bar(NT);
-        // 5. max and sum (fixed order: strided per thread, warp butterfly, warps in order)
-        float mx = -INFINITY;
-        for (int i = tid; i < nrow; i += NT) mx = fmaxf(mx, s_sc[i]);
+        // 4. softmax statistics (warp 0; fixed order: strided per lane, xor tree)
+        if (warp == 0) {
+            float mx = -INFINITY;
+            for (int i = lane; i < nrow; i += 32) mx = fmaxf(mx, s_sc[i]);
 #pragma unroll
-        for (int m = 16; m >= 1; m >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, m));
-        if (lane == 0) s_w[warp] = mx;
-        consumer_bar(NT);
-        mx = -INFINITY;
-        for (int w = 0; w < nwarp; ++w) mx = fmaxf(mx, s_w[w]);
-        float sm = 0.f;
-        for (int i = tid; i < nrow; i += NT) {
-            const float pe = expf(s_sc[i] - mx);
-            s_sc[i] = pe;
-            sm += pe;
-        }
-#pragma unroll
-        for (int m = 16; m >= 1; m >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, m);
-        consumer_bar(NT);
-        if (lane == 0) s_w[warp] = sm;
-        consumer_bar(NT);
-        float l = 0.f;
-        for (int w = 0; w < nwarp; ++w) l += s_w[w];
-        // 6. o partials: thread (r, c) sums rows t0 + r + k*rpi for its 8 dims
-        float o[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = 0.f;
-        for (int base = 0; base < nrow; base += 4 * rpi) {
-            uint4 vv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int t = t0 + base + r + u * rpi;
-                vv[u] = make_uint4(0u, 0u, 0u, 0u);
-                if (c < nch && t < t1)
-                    vv[u] = t == pos ? *reinterpret_cast<const uint4*>(s_vn + c * 8)
-                                     : __ldcg(reinterpret_cast<const uint4*>(vc + (size_t)t * hd + c * 8));
+            for (int m = 16; m >= 1; m >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, m));
+            float sm = 0.f;
+            for (int i = lane; i < nrow; i += 32) {
+                const float pe = expf(s_sc[i] - mx);
+                s_sc[i] = pe;
+                sm += pe;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int t = t0 + base + r + u * rpi;
-                if (t >= t1) continue;
-                const float pt = s_sc[t - t0];
-                const __half* vh = reinterpret_cast<const __half*>(&vv[u]);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) o[i] += pt * __half2float(vh[i]);
-            }
-        }
-        if (c < nch) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) s_red[r * hd + c * 8 + i] = o[i];
+            for (int m = 16; m >= 1; m >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, m);
+            if (lane == 0) { s_ml[0] = mx; s_ml[1] = sm; }
         }
         consumer_bar(NT);
-        if (tid < hd) {
-            float od = 0.f;
-            for (int rr = 0; rr < rpi; ++rr) od += s_red[rr * hd + tid];
-            if (P == 1) {
-                const long long q = __float2ll_rn(od / l * core::kAccScale);
-                asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;"
-                             :: "l"(cur + ph->o_off + (size_t)b * ph->o_ld + (size_t)head * hd + tid), "l"(cnt_word(q))
-                             : "memory");
-            } else {
-                float* pb = part_buf + (((size_t)head * P + part) * B + b) * (hd + 2);
-                __stcg(pb + tid, od);
-                if (tid == 0) { __stcg(pb + hd, mx); __stcg(pb + hd + 1, l); }
+        // 5. o partial: thread (dim, row group) sums p_t v_t[dim] over its rows
+        {
+            const int rgs = min(NT / hd, 4);       // row groups (4 at hd >= 128 with 512 threads)
+            const int dim = tid % hd, rg = tid / hd;
+            float o = 0.f;
+            if (rg < rgs) {
+                for (int t = r.t0 + rg; t < r.t1; t += rgs) {
+                    __half vh;
+                    if (t == pos) vh = s_vn[dim];
+                    else if (r.smem) vh = kv_v[((size_t)b * nk + (t - r.t0)) * hd + dim];
+                    else vh = __ldcg(vc + (size_t)t * hd + dim);
+                    o += s_sc[t - r.t0] * __half2float(vh);
+                }
+                s_o[rg * 128 + dim] = o;
             }
+            consumer_bar(NT);
+            if (tid < hd) {
+                float od = 0.f;
+                for (int g = 0; g < rgs; ++g) od += s_o[g * 128 + tid];
+                st_word(ob + tid, f32_word(od));
+            }
+            if (tid == 0) st_word(ob + hd, f32_word(s_ml[0]));
         }
         consumer_bar(NT);
-    }
-    if (P == 1) return;
-    // last part of this head to arrive merges all parts in fixed order
-    if (tid == 0) {
-        __threadfence();
-        unsigned old;
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(part_cnt + head) : "memory");
-        *s_last = ((old + 1u) & (unsigned)(P - 1)) == 0u;   // P is a power of two (2^32 % P == 0)
-    }
-    consumer_bar(NT);
-    if (!*s_last) return;
-    for (int b = 0; b < B; ++b) {
-        if (tid < hd) {
-            float M = -INFINITY;
-            for (int q = 0; q < P; ++q) M = fmaxf(M, __ldcg(part_buf + (((size_t)head * P + q) * B + b) * (hd + 2) + hd));
-            float L = 0.f, od = 0.f;
-            for (int q = 0; q < P; ++q) {
-                const float* pb = part_buf + (((size_t)head * P + q) * B + b) * (hd + 2);
-                const float m_q = __ldcg(pb + hd);
-                const float f = m_q == -INFINITY ? 0.f : expf(m_q - M);
-                L += f * __ldcg(pb + hd + 1);
-                od += f * __ldcg(pb + tid);
-            }
-            const long long q = __float2ll_rn(od / L * core::kAccScale);
-            asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;"
-                         :: "l"(cur + ph->o_off + (size_t)b * ph->o_ld + (size_t)head * hd + tid), "l"(cnt_word(q))
-                         : "memory");
+        if (tid == 0) {   // l last, with release: a reader that sees l final sees this part's o and m
+            __threadfence();
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(ob + hd + 1), "l"(f32_word(s_ml[1])) : "memory");
         }
     }
 }
 
-template <int D, int NB, int NW, int ST>
+// x staging of the o projection from the attention partials of an ATTN step
+// (counted words [B][heads][P][hd + 2], count 1): element col of token b is
+// head col / hd, dim col % hd; x = fp16(sum_q e_q o_q / sum_q e_q l_q) with
+// e_q = exp(m_q - max_q m_q), parts in fixed order (deterministic).  Layout of
+// s_x as core::stage_x.
+template <int D, int NB, int NW, bool XF>
+__device__ __forceinline__ void stage_x_attn(uint8_t* s_x, const unsigned long long* a, int B, int N_ss, int g_begin,
+                                             int ng, int heads, int hd, int P) {
+    constexpr int E = core::Entry<D>::value;
+    const int n_ent = ng * 32 * NB;
+    for (int t = threadIdx.x; t < n_ent; t += NW * 32) {
+        const int b = t % NB;
+        const int ss = (g_begin + t / (NB * 32)) * 32 + ((t / NB) & 31);
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+        if (b < B && ss < N_ss) {
+            const int col = ss * D, head = col / hd, e0 = col - head * hd;
+            const unsigned long long* hb = a + ((size_t)b * heads + head) * P * (hd + 2);
+            // poll only the l words (written with release after the part's o and m
+            // words, attn_item), all parts in flight; then o and m are final
+            unsigned long long lv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) lv[q] = 0ull;
+            const unsigned long long t_start = dev::globaltimer();
+            for (bool done = false; !done;) {
+                done = true;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (q < P && (lv[q] >> core::kCntShift) != 1ull) {
+                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(lv[q]) : "l"(hb + (size_t)q * (hd + 2) + hd + 1) : "memory");
+                        if ((lv[q] >> core::kCntShift) != 1ull) done = false;
+                    }
+                if (!done && dev::globaltimer() - t_start > 4000000000ull) __trap();
+            }
+            float m[8], l[8], o[8][D];   // P <= 8, fully unrolled (registers, not local memory)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const unsigned long long* pb = hb + (size_t)q * (hd + 2);
+                m[q] = q < P ? word_f32(ld_word(pb + hd, false)) : -INFINITY;
+                l[q] = q < P ? word_f32(lv[q]) : 0.f;
+#pragma unroll
+                for (int e = 0; e < D; ++e) o[q][e] = q < P ? word_f32(ld_word(pb + e0 + e, false)) : 0.f;
+            }
+            float M = -INFINITY;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) M = fmaxf(M, m[q]);
+            float den = 0.f, num[D];
+#pragma unroll
+            for (int e = 0; e < D; ++e) num[e] = 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (q >= P) continue;
+                const float f = m[q] == -INFINITY ? 0.f : expf(m[q] - M);
+                den += f * l[q];
+#pragma unroll
+                for (int e = 0; e < D; ++e) num[e] += f * o[q][e];
+            }
+#pragma unroll
+            for (int e = 0; e < D; ++e)
+                w[e >> 1] |= (uint32_t)__half_as_ushort(__float2half_rn(num[e] / den)) << (16 * (e & 1));
+        }
+        if (XF) {
+            core::store_x_f32<D, NB>(s_x, t, w);
+        } else {
+            uint32_t* dst = reinterpret_cast<uint32_t*>(s_x + (size_t)t * E);
+#pragma unroll
+            for (int q = 0; q < E / 4; ++q) dst[q] = w[q];
+        }
+    }
+}
+
+// RMSNorm scale s[b] = 1/sqrt(sum_k slot[b][k] / n + eps) from the n_slots
+// sum-of-squares slots of a norm step; every warp computes it the same way
+// (lane k and k + 32, xor tree) -> identical in every warp and CTA.
+template <int NB>
+__device__ __forceinline__ void warp_norm_scale(float (&sc)[NB], const unsigned long long* slots, int n_slots, int n,
+                                                float eps, int B, int lane) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        float a = 0.f;
+        if (b < B) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int k = lane + 32 * h;
+                if (k < n_slots) {
+                    unsigned long long v;
+                    const unsigned long long t0 = dev::globaltimer();
+                    while (((v = ld_word(slots + b * 64 + k, false)) >> core::kCntShift) != 1ull)
+                        if (dev::globaltimer() - t0 > 4000000000ull) __trap();
+                    a += word_f32(v);
+                }
+            }
+        }
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) a += __shfl_xor_sync(0xffffffffu, a, m);
+        sc[b] = 1.0f / sqrtf(a / (float)n + eps);
+    }
+}
+
+// MODEL: the whole-model step kinds and input transforms (EMBED, ATTN,
+// RMSNorm / SwiGLU / attention inputs, residual epilogue) are compiled in;
+// plain GEMV chains use the MODEL = false instance (fewer live registers in
+// the gather loop: the kernel runs at the 96-register cap of 17 warps).
+template <int D, int NB, int NW, int ST, bool MODEL>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     constexpr int E = core::Entry<D>::value;
     constexpr bool PAIR = ChainPair<D>::value;
@@ -362,23 +479,19 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     uint8_t* s_cb = smem;                                       // PAIR: CS * 64 KiB, else ST * cbb_max
     uint8_t* s_idx = s_cb + (PAIR ? CS * kPairSlot : ST * p.cbb_max);   // ST * R * 32
     uint8_t* s_x = s_idx + ST * R * 32;                         // gmax * XG
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_x + max(p.gmax * XG, NW * 8 * 4));
-    // RMSNorm reduction scratch [NW][8] aliases the x staging area: norm_scale
-    // finishes (bar.sync) before stage_x writes s_x, and every warp is past
-    // the previous item (consumer_bar at the item start).  The planner sizes
-    // s_x >= NW*8 floats.  The fixed scratch stays <= 96 B: at gmax = 13 the
-    // d = 2 plan has 240 B left for a 3-deep ring.
-    float* s_red = reinterpret_cast<float*>(s_x);
-    float* s_scale = reinterpret_cast<float*>(bars + 2 * (ST + CS));  // [8] RMSNorm scales
-    int* s_tok = reinterpret_cast<int*>(s_scale + 8);                // [8] EMBED tokens
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_x + p.gmax * XG);
+    float* s_sq = reinterpret_cast<float*>(bars + 2 * (ST + CS));   // [NW][NB] RMSNorm sum-of-squares partials
+    int* s_tok = reinterpret_cast<int*>(s_sq + NW * NB);             // [8] EMBED tokens
     unsigned& s_run = *reinterpret_cast<unsigned*>(s_tok + 8);       // run index
     int& s_pos = *reinterpret_cast<int*>(s_tok + 9);                 // model position
-    unsigned* s_flag = reinterpret_cast<unsigned*>(s_tok + 10);      // attention merge flag
+    unsigned long long*& s_tail = *reinterpret_cast<unsigned long long**>(s_tok + 10);   // this rank's tail words
+    EpiParams& s_ep = *reinterpret_cast<EpiParams*>(s_tok + 12);     // the current item's epilogue parameters
     const uint32_t cb_u = dev::smem_u32(s_cb), idx_u = dev::smem_u32(s_idx);
     const uint32_t full0 = dev::smem_u32(&bars[0]), empty0 = dev::smem_u32(&bars[ST]);
     const uint32_t cfull0 = dev::smem_u32(&bars[2 * ST]), cempty0 = dev::smem_u32(&bars[2 * ST + CS]);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned long long* const tail = p.peers[p.rank] + 2 * p.arena_words;
+    // (the tail pointer is not kept live across the loop: register pressure)
+    auto tail_ptr = [&]() { return p.peers[p.rank] + 2 * p.arena_words; };
 
     if (threadIdx.x == 0) {
 #pragma unroll
@@ -400,15 +513,31 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     if (warp == NW) {
         // producer: every step's stages, back to back (no dependence on x)
         if (lane == 0) {
+            int pos = 0;
+            if (p.model) pos = (int)ld_word(tail_ptr() + T_POS, false);
             int it = 0, cit = 0;
             for (int phj = 0; phj < p.n_steps * p.mi; ++phj) {
                 const int ph = phj / p.mi;
                 const ChainItem& w = p.items[((size_t)ph * p.nctas + blockIdx.x) * p.mi + phj % p.mi];
-                if (w.kind == SK_ATTN) {
-                    if (PAIR) {   // hand a pair slot to the consumers as attention scratch
+                if (MODEL && w.kind == SK_ATTN) {
+                    if (PAIR) {   // a pair slot for the consumers: cache rows + attention scratch
                         const int cs = cit % CS;
                         if (cit >= CS) dev::mbar_wait(cempty0 + 8 * cs, ((cit / CS) + 1) & 1);
-                        dev::mbar_arrive(cfull0 + 8 * cs);
+                        const ChainPhase& P = p.phases[ph];
+                        const AttnRows r = attn_rows(w.kidx, P.parts, pos, p.B, P.hd);
+                        if (r.smem) {
+                            const int nk = r.te - r.t0, kvh = w.head / (P.n_heads / P.n_kv);
+                            const uint32_t rb = (uint32_t)nk * P.hd * 2u;
+                            const uint32_t dst = cb_u + (uint32_t)cs * kPairSlot;
+                            dev::mbar_arrive_expect_tx(cfull0 + 8 * cs, 2u * rb * (uint32_t)p.B);
+                            for (int b = 0; b < p.B; ++b) {
+                                const size_t src = (((size_t)b * P.n_kv + kvh) * p.max_T + r.t0) * P.hd;
+                                dev::bulk_g2s(dst + (uint32_t)b * rb, P.kc + src, rb, cfull0 + 8 * cs);
+                                dev::bulk_g2s(dst + (uint32_t)(p.B + b) * rb, P.vc + src, rb, cfull0 + 8 * cs);
+                            }
+                        } else {
+                            dev::mbar_arrive(cfull0 + 8 * cs);
+                        }
                         ++cit;
                     }
                     continue;
@@ -458,6 +587,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
 
     // ---- run prologue ----
     if (threadIdx.x == 0) {
+        unsigned long long* const tail = tail_ptr();
+        s_tail = tail;
         unsigned long long old;
         asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(tail + T_ENTRY) : "memory");
         const unsigned run = (unsigned)(old / (unsigned long long)p.nctas);
@@ -472,21 +603,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                 if (dev::globaltimer() - t0 > 4000000000ull) __trap();
             }
         }
-        if (p.model) {
-            unsigned long long v;
-            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(tail + T_POS) : "memory");
-            s_pos = (int)v;
-        }
+        if (p.model) s_pos = (int)ld_word(tail + T_POS, false);
     }
     consumer_bar(NT);
     const unsigned run = s_run;
     const unsigned par = run & 1u;
     unsigned long long* const cur = p.peers[p.rank] + (long long)par * p.arena_words;   // this run's buffer
-    {
-        unsigned long long* nxt = p.peers[p.rank] + (long long)(par ^ 1u) * p.arena_words;
-        const long long per = (p.arena_words + p.nctas - 1) / p.nctas;
-        const long long zb = per * blockIdx.x, ze = min(p.arena_words, zb + per);
-        for (long long i = zb + threadIdx.x; i < ze; i += NT) nxt[i] = 0ull;
+    {   // zero this CTA's share of the other buffer for run + 1 (16-B stores; arena_words is even)
+        ulonglong2* nxt = reinterpret_cast<ulonglong2*>(p.peers[p.rank] + (long long)(par ^ 1u) * p.arena_words);
+        const long long n2 = p.arena_words / 2, per = (n2 + p.nctas - 1) / p.nctas;
+        const long long zb = per * blockIdx.x, ze = min(n2, zb + per);
+        for (long long i = zb + threadIdx.x; i < ze; i += NT) nxt[i] = make_ulonglong2(0ull, 0ull);
     }
     const bool sys_out = p.world > 1;
 
@@ -499,33 +626,33 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     uint32_t cpar = 0;
     for (int phj = 0; phj < p.n_steps * p.mi; ++phj) {
         const int ph = phj / p.mi, j = phj % p.mi;
-        const ChainItem w = p.items[((size_t)ph * p.nctas + blockIdx.x) * p.mi + j];
+        const ChainItem* wp = p.items + ((size_t)ph * p.nctas + blockIdx.x) * p.mi + j;
         const ChainPhase* phs = p.phases + ph;
-        // the PQ fields of the phase by value: their loads issue here, next to
-        // the item's, before the barrier -- not as dependent L2 round trips
-        // after it (~1 us per step when they were pointer reads)
+        // item and phase fields by value: their loads issue here, before the
+        // barrier -- not as dependent L2 round trips after it
+        const ChainItem w = *wp;
         const ChainPhase pv = *phs;
-        unsigned long long* tr = p.trace ? p.trace + ((size_t)ph * p.nctas + blockIdx.x) * 4 : nullptr;
-        if (tr && threadIdx.x == 0 && j == 0) tr[0] = dev::globaltimer();
+#define FASQ_TR(k) (p.trace + ((size_t)ph * p.nctas + blockIdx.x) * 4 + (k))
+        const bool tr = p.trace != nullptr;   // trace stamps (the pointer is recomputed: register pressure)
+        if (tr && threadIdx.x == 0 && j == 0) *FASQ_TR(0) = dev::globaltimer();
         if (w.kind < 0) continue;
         // every consumer warp is done with the previous item's SMEM
         consumer_bar(NT);
-        if (w.kind == SK_EMBED) {
-            embed_item(phs, cur, tail, p.B, run, s_pos, p.max_T, p.tok_hist, p.tok_expect, NT, s_tok);
-            if (tr && lane == 0 && warp == 0) { tr[1] = tr[2] = tr[3] = dev::globaltimer(); }
+        if (MODEL && w.kind == SK_EMBED) {
+            embed_item(phs, cur, s_tail, p.B, s_run, s_pos, p.max_T, p.tok_hist, p.tok_expect, NT, s_tok);
+            if (tr && lane == 0 && warp == 0) { *FASQ_TR(1) = *FASQ_TR(2) = *FASQ_TR(3) = dev::globaltimer(); }
             continue;
         }
-        if (w.kind == SK_ATTN) {
+        if (MODEL && w.kind == SK_ATTN) {
             if constexpr (PAIR) {
                 dev::mbar_wait(cfull0 + 8 * cslot, cpar);
-                if (tr && threadIdx.x == 0 && j == 0) tr[1] = tr[2] = dev::globaltimer();
-                attn_item(phs, w.head, w.kidx, cur, p.B, s_pos, p.max_T, p.rope, p.part_buf, p.part_cnt,
-                          reinterpret_cast<float*>(s_cb + (size_t)cslot * kPairSlot), NT, false, s_flag);
+                if (tr && threadIdx.x == 0 && j == 0) *FASQ_TR(1) = *FASQ_TR(2) = dev::globaltimer();
+                attn_item(phs, w.head, w.kidx, cur, p.B, s_pos, p.max_T, p.rope, s_cb + (size_t)cslot * kPairSlot, NT);
                 __syncwarp();
                 if (lane == 0) dev::mbar_arrive(cempty0 + 8 * cslot);
                 if (++cslot == CS) { cslot = 0; cpar ^= 1u; }
             }
-            if (tr && lane == 0 && warp == 0) tr[3] = dev::globaltimer();
+            if (tr && lane == 0 && warp == 0) *FASQ_TR(3) = dev::globaltimer();
             continue;
         }
         const int ng = w.g_end - w.g_begin;
@@ -536,23 +663,49 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         } else if (in_mode == IN_WORDS) {
             core::stage_x_counted<D, NB, NW, XF>(s_x, cur + pv.x_off, pv.x_ks, pv.F_in, p.B, w.N_ss, w.g_begin,
                                                  ng, xsys, p.backoff);
-        } else if constexpr (PAIR) {
+        } else if constexpr (PAIR && MODEL) {
             if (in_mode == IN_RMSNORM) {
-                core::norm_scale<NB, NW>(cur + pv.x_off, pv.x_ks, pv.F_in, p.B, pv.eps, xsys, s_red, s_scale);
-                core::stage_x_counted<D, NB, NW, XF, core::XM_NORM>(s_x, cur + pv.x_off, pv.x_ks, pv.F_in, p.B,
-                                                                    w.N_ss, w.g_begin, ng, xsys, 0, nullptr, 0,
-                                                                    s_scale, pv.gamma);
-            } else {
+                core::stage_x_counted<D, NB, NW, XF, core::XM_GAMMA>(s_x, cur + pv.x_off, pv.x_ks, pv.F_in, p.B,
+                                                                     w.N_ss, w.g_begin, ng, xsys, 0, nullptr, 0,
+                                                                     w.nsq >= 0 ? s_sq : nullptr, pv.gamma);
+            } else if (in_mode == IN_SILU) {
                 core::stage_x_counted<D, NB, NW, XF, core::XM_SILU>(s_x, cur + pv.x_off, pv.x_ks, pv.F_in, p.B,
                                                                     w.N_ss, w.g_begin, ng, xsys, 0,
                                                                     cur + pv.x2_off, pv.x2_ks);
+            } else {
+                stage_x_attn<D, NB, NW, XF>(s_x, cur + pv.x_off, p.B, w.N_ss, w.g_begin, ng, pv.a_heads, pv.a_hd,
+                                            pv.a_parts);
             }
         }
-        if (tr && threadIdx.x == 0 && j == 0) tr[1] = dev::globaltimer();
+        if (tr && threadIdx.x == 0 && j == 0) *FASQ_TR(1) = dev::globaltimer();
+        if (threadIdx.x == 0) {   // epilogue parameters -> SMEM (read after the gather loop)
+            EpiParams e;
+            e.y_off = wp->y_off;
+            e.res_off = phs->res_off;
+            e.nsq_off = phs->nsq_off;
+            e.row0_g = wp->row0_g;
+            e.ld = wp->ld;
+            e.F_out = wp->F_out;
+            e.r0 = wp->r0;
+            e.add_res = e.res_off >= 0 && phs->res_here && w.kidx == 0;
+            e.res_ks = phs->res_ks;
+            e.res_sys = phs->res_sys;
+            e.out_all = phs->out_all;
+            e.nsq_n = phs->nsq_n;
+            e.F_in = phs->F_in;
+            e.eps = phs->eps;
+            e.in_mode = in_mode;
+            s_ep = e;
+        }
         consumer_bar(NT);
-        if (tr && threadIdx.x == 0 && j == 0) tr[2] = dev::globaltimer();
+        if (tr && threadIdx.x == 0 && j == 0) *FASQ_TR(2) = dev::globaltimer();
+        if (PAIR && MODEL && in_mode == IN_RMSNORM && w.nsq >= 0 && threadIdx.x < p.B) {
+            // this K range's sum of squares of h (all warps' partials, fixed order)
+            float a = 0.f;
+            for (int q = 0; q < NW; ++q) a += s_sq[q * NB + threadIdx.x];
+            st_word(cur + pv.nsq_off + threadIdx.x * 64 + w.nsq, f32_word(a));
+        }
         const bool active = wrow0 < w.rows_valid;
-        unsigned long long* const ovf = tail + T_OVF;
         if constexpr (PAIR) {
             // pair stages: row-set mapping (gemv_core.cuh), 2G*NB accumulators
             // per lane, G-lane row reduction
@@ -579,19 +732,25 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             }
             core::reduce_set<NB, G>(acc, lane);
             if (active) {
-                const bool add_res = pv.res_off >= 0 && pv.res_here && w.kidx == 0;
+                if (MODEL && s_ep.in_mode == IN_RMSNORM) {
+                    float sc[NB];
+                    warp_norm_scale<NB>(sc, cur + s_ep.nsq_off, s_ep.nsq_n, s_ep.F_in, s_ep.eps, p.B, lane);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) acc[h * NB + b] *= sc[b];
+                }
+                const int row0_g = s_ep.row0_g, ld = s_ep.ld, F_out = s_ep.F_out, r0 = s_ep.r0;
                 long long qv[2 * NB];
-                const long long off = (long long)par * p.arena_words + w.y_off + w.row0_g;
-                core::set_values<NB, G>(acc, qv, w.r0 + wrow0, lane, w.F_out, p.B,
-                                        add_res ? cur + pv.res_off + w.row0_g : nullptr, w.ld, pv.res_ks,
-                                        pv.res_sys != 0, ovf);
-                if (pv.out_all) {
+                const long long off = (long long)(s_run & 1u) * p.arena_words + s_ep.y_off + row0_g;
+                core::set_values<NB, G>(acc, qv, r0 + wrow0, lane, F_out, p.B,
+                                        MODEL && s_ep.add_res ? cur + s_ep.res_off + row0_g : nullptr, ld,
+                                        s_ep.res_ks, s_ep.res_sys != 0, s_tail + T_OVF);
+                if (s_ep.out_all) {
                     for (int q = 0; q < p.world; ++q)
-                        core::counted_store_q<NB>(qv, p.peers[q] + off, w.r0 + wrow0, lane, w.F_out, w.ld, p.B,
-                                                  sys_out);
+                        core::counted_store_q<NB>(qv, p.peers[q] + off, r0 + wrow0, lane, F_out, ld, p.B, sys_out);
                 } else {
-                    core::counted_store_q<NB>(qv, p.peers[p.rank] + off, w.r0 + wrow0, lane, w.F_out, w.ld, p.B,
-                                              false);
+                    core::counted_store_q<NB>(qv, p.peers[p.rank] + off, r0 + wrow0, lane, F_out, ld, p.B, false);
                 }
             }
         } else {
@@ -615,18 +774,21 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             core::RowTotals<NB, RW> tot;
             core::reduce_rows<NB, RW>(acc, tot, lane);
             if (active) {
-                const long long off = (long long)par * p.arena_words + w.y_off + w.row0_g;
-                const int nq = pv.out_all ? p.world : 1;
+                const long long off = (long long)(s_run & 1u) * p.arena_words + s_ep.y_off + s_ep.row0_g;
+                const bool oa = s_ep.out_all != 0;
+                const int nq = oa ? p.world : 1;
                 for (int q = 0; q < nq; ++q)
-                    core::counted_store<NB, RW>(tot, p.peers[pv.out_all ? q : p.rank] + off, w.r0 + wrow0, w.F_out,
-                                                w.ld, p.B, ovf);
+                    core::counted_store<NB, RW>(tot, p.peers[oa ? q : p.rank] + off, s_ep.r0 + wrow0, s_ep.F_out,
+                                                s_ep.ld, p.B, s_tail + T_OVF);
             }
         }
-        if (tr && lane == 0 && warp == 0) tr[3] = dev::globaltimer();
+        if (tr && lane == 0 && warp == 0) *FASQ_TR(3) = dev::globaltimer();
     }
+#undef FASQ_TR
     // ---- run epilogue: exit count; the last CTA publishes the run to every rank ----
     consumer_bar(NT);
     if (threadIdx.x == 0) {
+        unsigned long long* const tail = s_tail;
         __threadfence_system();
         unsigned long long old;
         asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(tail + T_EXIT) : "memory");
@@ -646,11 +808,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
 }
 
 constexpr size_t kChainSmem = kSmemMax;
-constexpr size_t kChainScratch = 8 * 4 + 8 * 4 + 16;   // s_scale, s_tok, run/pos/flag words (after the mbarriers)
+constexpr size_t kChainScratch = 8 * 4 + 16 + sizeof(EpiParams);   // s_tok, run/pos words, s_ep (after the mbarriers and s_sq)
 
-template <int D, int NB, int NW, int ST>
+template <int D, int NB, int NW, int ST, bool MODEL>
 fasq_status launch_chain_t(const ChainParams& p, size_t smem, int grid, cudaStream_t st) {
-    auto kern = k_chain<D, NB, NW, ST>;
+    auto kern = k_chain<D, NB, NW, ST, MODEL>;
     static size_t lim = 0;
     static std::once_flag once;
     std::call_once(once, [&] { lim = set_max_dyn_smem(kern); });
@@ -675,8 +837,12 @@ fasq_status launch_chain_t(const ChainParams& p, size_t smem, int grid, cudaStre
 
 template <int D, int NB>
 fasq_status chain_cfg(const fasq_chain* c, const ChainParams& p, cudaStream_t st) {
-#define FASQ_CHAIN_CASE(NW_, ST_) \
-    if (c->nw == NW_ && c->st == ST_) return launch_chain_t<D, NB, NW_, ST_>(p, c->smem, c->nctas, st);
+#define FASQ_CHAIN_CASE(NW_, ST_)                                                                \
+    if (c->nw == NW_ && c->st == ST_) {                                                          \
+        if constexpr (D <= 2)                                                                    \
+            if (c->has_model) return launch_chain_t<D, NB, NW_, ST_, true>(p, c->smem, c->nctas, st); \
+        return launch_chain_t<D, NB, NW_, ST_, false>(p, c->smem, c->nctas, st);                 \
+    }
     FASQ_CHAIN_CASE(16, 3)
     FASQ_CHAIN_CASE(16, 2)
     FASQ_CHAIN_CASE(16, 1)
@@ -717,6 +883,36 @@ __global__ void k_counted_convert(const unsigned long long* __restrict__ arenas,
     if (dtype == FASQ_ACC_I64) reinterpret_cast<long long*>(out)[i] = v;
     else if (dtype == FASQ_F32) reinterpret_cast<float*>(out)[i] = bad ? __int_as_float(0x7fc00000) : (float)((double)v * core::kAccInv);
     else reinterpret_cast<__half*>(out)[i] = bad ? __ushort_as_half((unsigned short)0x7e00) : __double2half((double)v * core::kAccInv);
+}
+
+// Attention output of the LAST run (ATTN step partials [B][heads][P][hd + 2])
+// merged exactly as stage_x_attn merges them, as fp16 / fp32 / FASQ_ACC_I64
+// [B][heads * hd].
+__global__ void k_attn_convert(const unsigned long long* __restrict__ arenas, long long arena_words, int nctas,
+                               long long off, int B, int heads, int hd, int P, void* out, int dtype) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = (int64_t)B * heads * hd;
+    if (i >= n) return;
+    const unsigned long long* tail = arenas + 2 * arena_words;
+    const unsigned long long runs = tail[T_ENTRY] / (unsigned long long)nctas;
+    const unsigned last = (unsigned)((runs + 1ull) & 1ull);
+    const int b = (int)(i / ((int64_t)heads * hd)), col = (int)(i % ((int64_t)heads * hd));
+    const int head = col / hd, e = col - head * hd;
+    const unsigned long long* hb = arenas + (long long)last * arena_words + off + ((size_t)b * heads + head) * P * (hd + 2);
+    float M = -INFINITY;
+    for (int q = 0; q < P; ++q) M = fmaxf(M, word_f32(hb[(size_t)q * (hd + 2) + hd]));
+    float den = 0.f, num = 0.f;
+    for (int q = 0; q < P; ++q) {
+        const unsigned long long* pb = hb + (size_t)q * (hd + 2);
+        const float m = word_f32(pb[hd]);
+        const float f = m == -INFINITY ? 0.f : expf(m - M);
+        den += f * word_f32(pb[hd + 1]);
+        num += f * word_f32(pb[e]);
+    }
+    const float v = num / den;
+    if (dtype == FASQ_ACC_I64) reinterpret_cast<long long*>(out)[i] = __float2ll_rn(v * core::kAccScale);
+    else if (dtype == FASQ_F32) reinterpret_cast<float*>(out)[i] = v;
+    else reinterpret_cast<__half*>(out)[i] = __float2half_rn(v);
 }
 
 void destroy_chain(fasq_chain* c) {
@@ -822,6 +1018,10 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
     c->acc_ld.resize(n_steps);
     c->acc_ks.resize(n_steps);
     c->kinds.resize(n_steps);
+    c->nsq_off.assign(n_steps, -1);
+    c->nsq_n.assign(n_steps, 0);
+    c->attn_hd.assign(n_steps, 0);
+    c->attn_heads.assign(n_steps, 0);
     std::vector<int> pq_F_in(n_steps, 0);
     for (int s = 0; s < n_steps; ++s) {
         const StepDesc& S = steps[s];
@@ -841,6 +1041,10 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
                 words += (int64_t)B * ld;
             }
             pq_F_in[s] = (int)F_in;
+            if (S.in_mode == IN_RMSNORM) {   // sum-of-squares slots [B][64]
+                c->nsq_off[s] = words;
+                words += (int64_t)B * 64;
+            }
         } else if (S.kind == SK_EMBED) {
             if (!model || !S.embed || S.hidden < 1) return fail(FASQ_E_ARG, "EMBED step needs a model and a table");
             c->acc_off[s].push_back(words);
@@ -853,10 +1057,13 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
                 return fail(FASQ_E_UNSUPPORTED, "ATTN step: head_dim must be a multiple of 8 in 8..128");
             if (S.q_step < 0 || S.q_step >= s || steps[S.q_step].kind != SK_PQ || steps[S.q_step].layers.size() != 3)
                 return fail(FASQ_E_ARG, "ATTN step needs an earlier q/k/v step");
+            // partials [B][heads][parts][hd + 2] (logical output width heads * hd)
             c->acc_off[s].push_back(words);
             c->acc_ld[s].push_back((int64_t)S.n_heads * S.head_dim);
             c->acc_ks[s].push_back(1);
-            words += (int64_t)B * S.n_heads * S.head_dim;
+            c->attn_hd[s] = S.head_dim;
+            c->attn_heads[s] = S.n_heads;
+            words += (int64_t)B * S.n_heads * model->attn_parts * (S.head_dim + 2);
         } else {
             return fail(FASQ_E_ARG, "unknown step kind");
         }
@@ -873,6 +1080,7 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
     if (ring(c->st, c->nw) > kChainSmem && c->nw > 8) c->nw = 8;
     while (c->st > 1 && ring(c->st, c->nw) > kChainSmem) --c->st;
     c->R = c->rw * c->nw;
+    words = (words + 1) & ~(int64_t)1;   // 16-B zeroing stores
     c->arena_words = words;
     // ---- work plan: per step a list of items, dealt to the CTAs round-robin ----
     std::vector<std::vector<ChainItem>> per_step(n_steps);
@@ -908,7 +1116,6 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
             P.q_ld = S.n_heads * hd;
             P.kv_ld = S.n_kv * hd;
             P.o_off = c->acc_off[s][0];
-            P.o_ld = S.n_heads * hd;
             P.kc = S.kc;
             P.vc = S.vc;
             P.n_heads = S.n_heads;
@@ -922,6 +1129,7 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
                     w.kind = SK_ATTN;
                     w.head = h;
                     w.kidx = q;
+                    w.nsq = -1;
                     per_step[s].push_back(w);
                 }
             continue;
@@ -959,6 +1167,13 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
                 P.x2_off = c->acc_off[src][1];
                 P.x2_ks = c->acc_ks[src][1];
                 P.x_sys = steps[src].out_all && world > 1;
+            } else if (S.in_mode == IN_ATTN) {
+                if (steps[src].kind != SK_ATTN) return fail(FASQ_E_ARG, "ATTN input needs an ATTN step");
+                if (c->acc_ld[src][0] != P.F_in) return fail(FASQ_E_SHAPE, "attention width != F_in");
+                P.x_off = c->acc_off[src][0];
+                P.a_heads = c->attn_heads[src];
+                P.a_hd = c->attn_hd[src];
+                P.a_parts = model->attn_parts;
             } else {
                 if (S.src_layer < 0 || S.src_layer >= (int)c->acc_off[src].size())
                     return fail(FASQ_E_ARG, "input layer out of range");
@@ -970,6 +1185,9 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
                     if (!pair || !S.gamma) return fail(FASQ_E_UNSUPPORTED, "RMSNorm input needs d <= 2 and gamma");
                     P.gamma = S.gamma;
                     P.eps = S.eps;
+                    P.nsq_off = c->nsq_off[s];
+                    P.nsq_n = ks[0];
+                    c->nsq_n[s] = ks[0];
                 }
             }
             if (S.in_mode != IN_WORDS && !pair) return fail(FASQ_E_UNSUPPORTED, "input transforms need d <= 2");
@@ -1008,6 +1226,8 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
                     w.g_begin = (int)((int64_t)k * L->n_groups / ks[l]);
                     w.g_end = (int)((int64_t)(k + 1) * L->n_groups / ks[l]);
                     w.kidx = k;
+                    // (layer 0, row tile 0) K ranges cover F_in once: they contribute the RMSNorm sum of squares
+                    w.nsq = (S.in_mode == IN_RMSNORM && l == 0 && r == 0) ? k : -1;
                     c->gmax = std::max(c->gmax, w.g_end - w.g_begin);
                     per_step[s].push_back(w);
                 }
@@ -1022,9 +1242,9 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
         for (size_t q = 0; q < per_step[s].size(); ++q)
             items[((size_t)s * c->nctas + q % c->nctas) * c->mi + q / c->nctas] = per_step[s][q];
     const size_t xg = (pair && NB == 8) ? (size_t)32 * NB * c->d * 4 : (size_t)32 * NB * E;   // k_chain XG
-    auto smem_of = [&](int stg) {
-        const size_t sx = std::max((size_t)c->gmax * xg, (size_t)c->nw * 8 * 4);   // x staging / norm scratch
-        return cbring(stg) + (size_t)stg * c->R * 32 + sx + 16 * (stg + kChainCS) + kChainScratch;
+    auto smem_of = [&](int stg) {   // k_chain's layout: rings, x staging, mbarriers, s_sq [nw][NB], scratch
+        return cbring(stg) + (size_t)stg * c->R * 32 + (size_t)c->gmax * xg + 16 * (stg + kChainCS) +
+               (size_t)c->nw * NB * 4 + kChainScratch;
     };
     while (c->st > 1 && smem_of(c->st) > kChainSmem) --c->st;
     c->smem = smem_of(c->st);
@@ -1035,8 +1255,10 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
     if (model) {   // attention scratch lives in a 64 KiB pair slot
         for (int s = 0; s < n_steps; ++s)
             if (steps[s].kind == SK_ATTN) {
-                const int Tp = (model->max_T + model->attn_parts - 1) / model->attn_parts;
-                const size_t need = (3 * 256) * 4 + 2 * 256 * 2 + 32 * 256 * 4 + ((Tp + 3) & ~3) * 4 + 32 * 4;
+                // attn_item's scratch after the staged cache rows (the rows fall back to
+                // global loads when they do not fit; the scratch must)
+                const int Tp = (model->max_T + model->attn_parts - 1) / model->attn_parts + 1;
+                const size_t need = kAttnKV + kAttnScratchFixed + (size_t)(Tp + 4) * 4;
                 if (need > kPairSlot) return fail(FASQ_E_UNSUPPORTED, "attention scratch exceeds a pair slot (max_T)");
             }
     }
@@ -1092,8 +1314,6 @@ fasq_status chain_launch(fasq_chain* c, const void* x_dev, cudaStream_t st) {
         p.pos_wrap = c->model.pos_wrap;
         p.tok_hist = c->model.tok_hist;
         p.tok_expect = c->model.tok_expect;
-        p.part_buf = c->model.part_buf;
-        p.part_cnt = c->model.part_cnt;
     }
     fasq_status s;
     switch (c->d) {
@@ -1112,6 +1332,14 @@ fasq_status chain_output(const fasq_chain* c, int step, int layer, void* y_dev, 
     if (dtype != FASQ_F16 && dtype != FASQ_F32 && dtype != FASQ_ACC_I64) return FASQ_E_ARG;
     const int64_t n = (int64_t)c->B * c->acc_ld[step][layer];
     if (n <= 0) return FASQ_OK;
+    if (c->kinds[step] == SK_ATTN) {
+        k_attn_convert<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(c->arenas, c->arena_words, c->nctas,
+                                                                     c->acc_off[step][0], c->B, c->attn_heads[step],
+                                                                     c->attn_hd[step], c->model.attn_parts, y_dev,
+                                                                     (int)dtype);
+        FASQ_CUDA_TRY(cudaGetLastError());
+        return FASQ_OK;
+    }
     k_counted_convert<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(c->arenas, c->arena_words, c->nctas,
                                                                   c->acc_off[step][layer], n, c->acc_ks[step][layer],
                                                                   y_dev, (int)dtype, c->world > 1);

@@ -18,9 +18,20 @@ enum ChainStepKind : int {
 enum ChainInMode : int {
     IN_EXT = 0,     // the chain's external fp16 input x
     IN_WORDS = 1,   // output words of (src_step, src_layer), rounded to fp16
-    IN_RMSNORM = 2, // RMSNorm(words of src) * gamma (the whole vector is read for the scale)
-    IN_SILU = 3     // silu(layer 0 of src_step) * (layer 1 of src_step) (gate/up)
+    IN_RMSNORM = 2, // RMSNorm(words of src) * gamma, the scale folded into the epilogue (below)
+    IN_SILU = 3,    // silu(layer 0 of src_step) * (layer 1 of src_step) (gate/up)
+    IN_ATTN = 4     // the merged attention partials of an ATTN step (src_step)
 };
+// RMSNorm folding (IN_RMSNORM): RMSNorm(h) = s * (h (.) gamma) with the scalar
+// s = 1/sqrt(mean(h^2) + eps) per token, and the PQ product is linear in x
+// (Eq. 3), so a step stages x = fp16(h (.) gamma) over its own K range only and
+// multiplies its fp32 partials by s in the epilogue.  The sum of squares is
+// contributed by the K ranges of (layer 0, row tile 0) -- they cover F_in
+// exactly once -- into per-range slots (fp32 bits in counted words, count 1);
+// every warp sums the slots in a fixed order, so every CTA applies the same s.
+// Attention output (SK_ATTN): per (token, head, cache part) the unnormalised
+// o [hd], the running max m and the sum l, fp32 bits in counted words
+// [B][heads][parts][hd + 2]; the consumer merges the parts in fixed order.
 
 struct StepDesc {
     int kind = SK_PQ;
@@ -53,9 +64,7 @@ struct ChainModel {
     int max_T = 0, pos_wrap = 0;
     int* tok_hist = nullptr;                 // [B][max_T] tokens chosen by the runs (int32)
     long long tok_expect = 0;                // contributions per token slot (all ranks' lm_head CTAs)
-    float* part_buf = nullptr;               // attention split-T partials
-    unsigned* part_cnt = nullptr;            // per-head merge counters
-    int attn_parts = 1;
+    int attn_parts = 1;                      // cache parts per head (items per head of an ATTN step)
 };
 
 fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, int rank, int max_ctas, bool det,
@@ -97,6 +106,9 @@ struct fasq_chain {
     std::vector<std::vector<int64_t>> acc_off;   // per step, per output: word offset in one arena buffer
     std::vector<std::vector<int64_t>> acc_ld;    // per step, per output: words per batch row
     std::vector<std::vector<int>> acc_ks;        // per step, per output: contributions per word
+    std::vector<long long> nsq_off;              // per step: RMSNorm sum-of-squares slots [B][64] (-1: none)
+    std::vector<int> nsq_n;                      // per step: slots per token (K ranges of layer 0)
+    std::vector<int> attn_hd, attn_heads;        // per ATTN step: head dim, local heads (output layout)
     int ext_F_in = 0;
     unsigned long long* arenas = nullptr;        // [2][arena_words] + tail (ONE allocation, IPC-exportable)
     int64_t arena_words = 0;

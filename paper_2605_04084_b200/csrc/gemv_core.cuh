@@ -629,16 +629,21 @@ __device__ __forceinline__ void counted_store_q(const long long (&q)[2 * NB], un
 // count == ks (one L2 round trip once they are final), then forms fp16 x.
 // Layout of s_x as stage_x.  MODE:
 //   XM_WORDS  x = fp16(value)                                  (one RN rounding)
-//   XM_NORM   x = fp16(fp32(value) * scale[b] * gamma[col])    (RMSNorm; scale from norm_scale)
+//   XM_GAMMA  x = fp16(fp32(value) * gamma[col])               (RMSNorm with the scale folded into
+//             the epilogue, chain_internal.cuh); with sq != NULL also the sum of fp32(value)^2 per
+//             token over this K range: sq[warp * NB + b] = the warp's partial (fixed order)
 //   XM_SILU   x = fp16(silu(g) * u), g/u = values of x / x2    (SwiGLU gate * up, fp32)
-constexpr int XM_WORDS = 0, XM_NORM = 1, XM_SILU = 2;
+constexpr int XM_WORDS = 0, XM_GAMMA = 1, XM_SILU = 2;
 
 template <int D, int NB, int NW, bool XF = false, int MODE = XM_WORDS>
 __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned long long* x, int ks, int F_in, int B,
                                                 int N_ss, int g_begin, int ng, bool sys = true, int backoff = 0,
                                                 const unsigned long long* x2 = nullptr, int ks2 = 0,
-                                                const float* scale = nullptr, const __half* gamma = nullptr) {
+                                                float* sq = nullptr, const __half* gamma = nullptr) {
     constexpr int E = Entry<D>::value;
+    float sqa[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) sqa[b] = 0.f;
     constexpr int NX = MODE == XM_SILU ? 2 : 1;     // words per element
     const int tid = threadIdx.x;
     const int n_ent = ng * 32 * NB;
@@ -707,8 +712,11 @@ __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned lon
                     uint32_t h;
                     if (MODE == XM_WORDS) {
                         h = __half_as_ushort(__double2half((double)val * kAccInv));
-                    } else if (MODE == XM_NORM) {
-                        const float f = (float)((double)val * kAccInv) * scale[b];
+                    } else if (MODE == XM_GAMMA) {
+                        const float f = (float)((double)val * kAccInv);
+#pragma unroll
+                        for (int bb = 0; bb < NB; ++bb)
+                            if (bb == b) sqa[bb] += f * f;
                         h = __half_as_ushort(__float2half_rn(f * __half2float(gamma[(size_t)ss * D + e])));
                     } else {
                         const long long val2 = (long long)(v[u][NX - 1][e] & kCntMask) - (long long)ks2 * kCntBias;
@@ -726,6 +734,16 @@ __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned lon
             uint32_t* dst = reinterpret_cast<uint32_t*>(s_x + (size_t)t * E);
 #pragma unroll
             for (int q = 0; q < E / 4; ++q) dst[q] = w[q];
+        }
+    }
+    if (MODE == XM_GAMMA && sq) {
+        const int lane = tid & 31;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            float a = sqa[b];
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) a += __shfl_xor_sync(0xffffffffu, a, m);
+            if (lane == 0) sq[(tid >> 5) * NB + b] = a;
         }
     }
 }

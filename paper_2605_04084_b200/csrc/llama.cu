@@ -41,8 +41,6 @@ struct fasq_llama {
     std::vector<__half*> kc, vc;       // per layer [B][n_kv_local][max_T][hd]
     float2* rope = nullptr;
     int* tok_hist = nullptr;
-    float* part_buf = nullptr;
-    unsigned* part_cnt = nullptr;
     float* logits = nullptr;           // optional debug output (fasq_llama_logits)
     int* tok_dev = nullptr;            // staging for fasq_llama_step_host / reset
     int lm_ctas = 0;
@@ -209,8 +207,6 @@ void destroy_model(fasq_llama* m) {
     for (__half* p : m->vc) if (p) cudaFree(p);
     if (m->rope) cudaFree(m->rope);
     if (m->tok_hist) cudaFree(m->tok_hist);
-    if (m->part_buf) cudaFree(m->part_buf);
-    if (m->part_cnt) cudaFree(m->part_cnt);
     if (m->logits) cudaFree(m->logits);
     if (m->tok_dev) cudaFree(m->tok_dev);
     delete m;
@@ -310,18 +306,14 @@ fasq_status fasq_llama_create(const fasq_llama_desc* d, void* stream, fasq_llama
             return fail(FASQ_E_CUDA, "rope upload");
     }
     const int sms = D.max_ctas > 0 ? std::min(D.max_ctas, sm_count()) : sm_count();
-    int parts = 1;   // split the cache length so that heads x parts fill the GPU (power of two, <= 8)
+    int parts = 1;   // split the cache length so that heads x parts fill the GPU (<= 8)
     while (parts < 8 && m->n_heads_l * parts * 2 <= sms) parts *= 2;
     if (const char* e = getenv("FASQ_ATTN_PARTS")) parts = std::max(1, std::min(8, atoi(e)));
-    if (parts & (parts - 1)) parts = 1;
-    if (cudaMalloc(&m->tok_hist, (size_t)D.B * D.max_T * 4) != cudaSuccess ||
-        cudaMalloc(&m->part_buf, (size_t)m->n_heads_l * parts * D.B * (hd + 2) * 4) != cudaSuccess ||
-        cudaMalloc(&m->part_cnt, (size_t)m->n_heads_l * 4) != cudaSuccess || cudaMalloc(&m->tok_dev, 64) != cudaSuccess) {
+    if (cudaMalloc(&m->tok_hist, (size_t)D.B * D.max_T * 4) != cudaSuccess || cudaMalloc(&m->tok_dev, 64) != cudaSuccess) {
         cudaGetLastError();
         return fail(FASQ_E_OOM, "");
     }
     cudaMemsetAsync(m->tok_hist, 0, (size_t)D.B * D.max_T * 4, st);
-    cudaMemsetAsync(m->part_cnt, 0, (size_t)m->n_heads_l * 4, st);
     // step list: 0 = EMBED; block l: 1+5l qkv, 2+5l attn, 3+5l o(+h), 4+5l gate/up, 5+5l down(+h')
     std::vector<StepDesc> steps;
     StepDesc e;
@@ -353,7 +345,7 @@ fasq_status fasq_llama_create(const fasq_llama_desc* d, void* stream, fasq_llama
         StepDesc o;
         o.kind = SK_PQ;
         o.layers = {D.o[l]};
-        o.in_mode = IN_WORDS;
+        o.in_mode = IN_ATTN;
         o.src_step = s_at;
         o.res_step = h_step;
         o.res_here = D.rank == 0;
@@ -390,8 +382,6 @@ fasq_status fasq_llama_create(const fasq_llama_desc* d, void* stream, fasq_llama
     cm.pos_wrap = std::max(0, std::min(D.pos_wrap, D.max_T - 1));
     cm.tok_hist = m->tok_hist;
     cm.tok_expect = (long long)W * m->lm_ctas;
-    cm.part_buf = m->part_buf;
-    cm.part_cnt = m->part_cnt;
     cm.attn_parts = parts;
     fasq_status s = chain_build(steps, D.B, W, D.rank, D.max_ctas, false, &cm, st, &m->chain);
     if (s != FASQ_OK) return fail(s, "");
