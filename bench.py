@@ -2,30 +2,31 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fasq|reference]
 
-Workload (BASELINE.json configs[1], the metric's headline configuration):
-one Llama-3-8B-shaped decode step through all 32 blocks x 7 product-quantized
-linear layers (q, k, v, o, gate, up, down) at the paper's effective 4-bit
-setting (d=2, C=256, uint8 indices, fp16 codebooks), batch 1.  Each GEMV's
-fp16 output feeds the next (q -> o, gate -> down, down -> next block), so the
-224 launches are a real dependency chain; weights are random-init with the
-paper's layer shapes (synthetic, data="synthetic"), 4.1 GB of PQ weights per
-step -- far larger than the 126 MB L2, so every step streams from HBM.
+Workload (BASELINE.json configs[4] / north_star "whole-model Llama-3-8B-shaped
+decode"; metric "Llama-3-8B PQ decode tok/s"): greedy decode of a random-init
+Llama-3-8B-shaped model whose 224 linear layers (32 blocks x q, k, v, o, gate,
+up, down) are FASQ layers at the paper's effective 4-bit setting (d=2, C=256,
+uint8 indices, fp16 codebooks), batch 1, with the fp16 embedding, RMSNorms,
+RoPE + KV-cache attention, SwiGLU, residuals, fp16 lm_head and argmax -- the
+paper's E2E setting (prompt 128, 128 generated tokens; the KV cache of
+the 128 prompt positions is seeded, decode cycles over positions 128..255).
+One step = one token: 5.2 GB of weights, far larger than the 126 MB L2.
 
-At N > 1 GPUs every layer is row-sharded (F_out/N rows per rank, all
-codebooks replicated) and each of the 4 chain outputs per block
-(q, o, gate, down) is all-gathered over NCCL before it is consumed.
+At N > 1 GPUs the model is Megatron-sharded (q/k/v, gate/up: heads / ffn rows;
+o, down: K slices; lm_head: vocab rows); the all-reduces / gathers are fused
+into the chain kernel's counted stores over NVLink peer memory (no NCCL on the
+data path), the argmax is reduced across ranks by red.max.
 
-value  = decode tokens/s of the PQ linear stack (1 token = 1 step), device
-         time via CUDA events around K graph replays, max over ranks.
-e2e    = the same step through the public API with HOST buffers: H2D of the
-         token's fp16 hidden state from pinned memory + the 224 GEMVs + D2H
-         of the last layer's output, inside the timed region.
-roofline: dominant kernel = the persistent decode-chain kernel k_chain (N=1:
-         ONE launch per token runs all 224 GEMVs; its per-launch duration is
-         timed live with CUDA events around eager launches), algorithmic
-         bytes = indices + codebooks + x + y of the 224 layers; traffic =
-         dram bytes of one k_chain launch from the committed ncu --set full
-         capture (profiles/r01).
+value  = decode tokens/s (1 token per step at B = 1), device time via CUDA
+         events around K graph replays, max over ranks.
+e2e    = the same through the public C-ABI calls with HOST buffers (token
+         H2D + step + chosen-token D2H per step), wall clock.
+roofline: dominant kernel = k_chain (the persistent whole-model chain, one
+         launch per token), timed live with CUDA events around eager launches
+         on the launch stream; algorithmic bytes = PQ indices + codebooks +
+         fp16 activations of the 224 layers + embedding row + the KV rows
+         attention reads; traffic = ncu dram bytes of one launch from the
+         committed capture (profiles/r02/ncu_traffic.json) or null.
 cpu_baseline: the C oracle (fp64 reconstruct-then-multiply) timed on a
          bounded row sample of each layer shape on the host cores.
 """
@@ -45,9 +46,6 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 METRIC = "Llama-3-8B PQ decode tok/s + GEMV HBM GB/s vs 8 TB/s; prefill GEMM TFLOP/s"
-# dram__bytes_read.sum + dram__bytes_write.sum of ONE k_chain launch (32 blocks,
-# d=2, C=256, B=1) from `ncu --set full` (profiles/r01/ncu_chain_final_summary.txt)
-K_CHAIN_NCU_DRAM_BYTES = 4143973000 + 26200576
 D, C = 2, 256
 
 
@@ -115,7 +113,146 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------
-# model
+# whole model (the headline): Llama-3-8B-shaped greedy decode, fasq_llama_*
+# ----------------------------------------------------------------------------
+LLAMA = dict(n_layers=32, hidden=4096, n_heads=32, n_kv=8, head_dim=128, ffn=14336, vocab=128256)
+PROMPT, MAX_T = 128, 256   # the paper's E2E protocol: prompt 128, 128 generated tokens
+
+
+def build_llama(rank: int, world: int, d: int = D, c: int = C, B: int = 1, seed: int = 0, n_layers=None):
+    """Random-init Llama-3-8B-shaped model whose 224 linear layers are FASQ
+    layers (uniform random uint8 indices, N(0, 1/F_in) fp16 codebooks -- the
+    synth recipe), fp16 embedding / lm_head / norm weights, and this rank's
+    Megatron shards (q/k/v and gate/up: heads / ffn rows; o and down: K
+    slices; lm_head: vocab rows).  Every rank draws the same full layers from
+    the same seeds and keeps its shard, so the model does not depend on the
+    world size.  The KV cache of the first PROMPT positions is seeded N(0, 1)
+    (the state after a 128-token prompt); decoding cycles over positions
+    [PROMPT, MAX_T) (pos_wrap).  Returns (model, bytes dict)."""
+    import torch
+
+    import paper_2605_04084_b200 as F
+    import synth
+    m = LLAMA
+    nl = m["n_layers"] if n_layers is None else n_layers
+    hid, H, KV, hd, ffn, V = m["hidden"], m["n_heads"], m["n_kv"], m["head_dim"], m["ffn"], m["vocab"]
+    Hl, KVl, Fl, Vl = H // world, KV // world, ffn // world, V // world
+    shapes = {"q": (H * hd, hid), "k": (KV * hd, hid), "v": (KV * hd, hid), "o": (hid, H * hd),
+              "gate": (ffn, hid), "up": (ffn, hid), "down": (hid, ffn)}
+    rows = {"q": Hl * hd, "k": KVl * hd, "v": KVl * hd, "gate": Fl, "up": Fl}
+    kcols = {"o": Hl * hd, "down": Fl}
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed * 7919 + 17)
+    layers, pq_bytes = [], 0
+    for l in range(nl):
+        L = {}
+        for i, (n, (fo, fi)) in enumerate(shapes.items()):
+            cb, idx = synth.torch_random_layer(fo, fi, d, c, seed=seed * 1000 + l * 7 + i)
+            if world > 1 and n in rows:
+                r = rows[n]
+                idx = idx[:, rank * r:(rank + 1) * r].contiguous()
+                fi_l = fi
+            elif world > 1:
+                s0, s1 = rank * kcols[n] // d, (rank + 1) * kcols[n] // d
+                cb, idx = cb[s0:s1].contiguous(), idx[s0:s1].contiguous()
+                fi_l = kcols[n]
+            else:
+                fi_l = fi
+            L[n] = F.import_layer(cb, idx, fi_l)
+            pq_bytes += idx.numel() + cb.numel() * 2
+            del cb, idx
+        L["attn_norm"] = (1 + 0.1 * torch.randn(hid, generator=g, device="cuda")).half()
+        L["mlp_norm"] = (1 + 0.1 * torch.randn(hid, generator=g, device="cuda")).half()
+        layers.append(L)
+    fn = (1 + 0.1 * torch.randn(hid, generator=g, device="cuda")).half()
+    emb = torch.randn((V, hid), generator=g, device="cuda").half()
+    lm = (torch.randn((V, hid), generator=g, device="cuda") / hid ** 0.5).half()
+    lm = lm[rank * Vl:(rank + 1) * Vl].contiguous()
+    torch.cuda.synchronize()
+    model = F.Llama(layers, fn, emb, lm, H, KV, hd, V, max_T=MAX_T, pos_wrap=PROMPT, B=B, world=world, rank=rank)
+    gk = torch.Generator(device="cuda")
+    gk.manual_seed(seed * 31 + 5)
+    for l in range(nl):
+        K_, V_ = model.kv_cache(l)
+        K_.normal_(generator=gk)
+        V_.normal_(generator=gk)
+    torch.cuda.synchronize()
+    model._bench_keep = (layers, fn, emb, lm)
+    # algorithmic bytes per step (this rank): PQ weights (indices + codebooks),
+    # fp16 activations in/out of every PQ layer, the embedding row, the KV rows
+    # attention reads (T = positions incl. the new one, averaged over the
+    # decode cycle [PROMPT, MAX_T)), and the lm_head (separate kernel)
+    act = 0
+    for n, (fo, fi) in shapes.items():
+        fo_l = rows.get(n, fo) if world > 1 else fo
+        fi_l = kcols.get(n, fi) if world > 1 else fi
+        act += 2 * B * (fo_l + fi_l)
+    t_avg = (PROMPT + 1 + MAX_T) / 2.0
+    kv = 2 * KVl * t_avg * hd * 2 * B
+    chain = pq_bytes + nl * (act + kv) + 2 * hid * B
+    lm_b = Vl * hid * 2 + 2 * hid * B
+    return model, {"pq": pq_bytes, "chain": chain, "lm_head": lm_b, "step": chain + lm_b, "kv_t_avg": t_avg}
+
+
+def llama_timed(model, steps, warmup, rank, world):
+    """ms per decode step (device time: CUDA graph of one step, K replays
+    between CUDA events, max over ranks)."""
+    model.reset([128000 + b for b in range(model.B)], PROMPT)
+    g = capture(lambda: model.step(), world)
+    return timed(g, steps, warmup, rank, world), g
+
+
+def llama_kernel_ms(model, reps, world):
+    """Per-kernel device time of the two launches of a step (chain, lm_head):
+    eager steps with CUDA events before / between (fasq_llama_step_ex
+    parts 1 and 2) / after, on the launch stream, averaged."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(reps)]
+    for e in evs:
+        e[0].record()
+        model.step_part(1)
+        e[1].record()
+        model.step_part(2)
+        e[2].record()
+    torch.cuda.synchronize()
+    ch = sum(e[0].elapsed_time(e[1]) for e in evs) / reps
+    lm = sum(e[1].elapsed_time(e[2]) for e in evs) / reps
+    return ch, lm
+
+
+def llama_e2e(model, steps, warmup, rank, world):
+    """End to end through the public C-ABI calls with HOST buffers: every step
+    copies the B tokens to decode from pinned host memory (fasq_llama_reset,
+    H2D) and runs fasq_llama_step_host (chain + lm_head + D2H of the chosen
+    tokens); wall clock around K synchronous steps, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    toks = [128000 + b for b in range(model.B)]
+    model.reset(toks, PROMPT)
+    for _ in range(warmup):
+        toks = model.step_host()
+        model.reset(toks, -1)
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        model.reset(toks, -1)
+        toks = model.step_host()
+    dt = (time.perf_counter() - t0) * 1e3 / steps
+    if world > 1:
+        t = torch.tensor([dt], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    return dt
+
+
+# ----------------------------------------------------------------------------
+# PQ linear stack only (the round-1 headline; side measurement now)
 # ----------------------------------------------------------------------------
 def build_model(rank: int, world: int, seed: int = 0):
     """Row-sharded PQ layers of every block (random-init, paper shapes)."""
@@ -678,12 +815,74 @@ def run_reference(args, rank, world):
             "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "llama3-8b-pq-decode-d2-C256-b1 (CPU oracle, sampled rows)",
+            "config": {"workload": "llama3-8b-pq-greedy-decode-d2-C256-b1 (CPU oracle: sampled rows of the PQ "
+                                   "products, which are > 99% of its per-token time)",
                        "global_batch": 1, "seq_len": 1, "parallelism": "host-cores"},
             "cpu_baseline": {"value": v, "unit": "tok/s", "cores": sampler.threads, "kind": "oracle",
                              "sample": sampler.describe(rows)},
             "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def pq_chain_side(peak, steps=50):
+    """The PQ linear stack alone (the round-1 headline): 224 chained PQ GEMVs
+    of a token in the persistent chain kernel, N = 1."""
+    import torch
+    blocks = build_model(0, 1, seed=3)
+    step = DecodeStep(blocks, 0, 1, None)
+    step.h.copy_(__import__("synth").torch_activation(1, 4096, seed=11))
+    for _ in range(3):
+        step.chain.run(step.h)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step.chain.run(step.h)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    gb = layer_bytes(1)
+    out = {"ms_per_token": round(ms, 4), "tok_s": round(1e3 / ms, 1), "GBps": round(gb / ms / 1e6, 1),
+           "frac": round(gb / ms / 1e6 / peak, 3), "algorithmic_bytes": gb}
+    step.chain.free()
+    for Ls in blocks:
+        for L in Ls.values():
+            L.free()
+    torch.cuda.synchronize()
+    return out
+
+
+def llama_side(peak, settings=((2, 128, 1), (2, 256, 8)), steps=30):
+    """Whole-model decode at effective 3-bit (2,128) and at batch 8, N = 1."""
+    import torch
+    out = {}
+    for (d, c, B) in settings:
+        model, by = build_llama(0, 1, d=d, c=c, B=B, seed=1)
+        ms, g = llama_timed(model, steps, 3, 0, 1)
+        ch, lm = llama_kernel_ms(model, 10, 1)
+        out["d%d_C%d_B%d" % (d, c, B)] = {
+            "ms_per_step": round(ms, 4), "tok_s": round(B * 1e3 / ms, 1),
+            "chain_ms": round(ch, 4), "chain_frac": round(by["chain"] / ch / 1e6 / peak, 3),
+            "lm_head_ms": round(lm, 4), "step_GBps": round(by["step"] / ms / 1e6, 1),
+            "step_frac": round(by["step"] / ms / 1e6 / peak, 3)}
+        del g
+        model.free()
+        torch.cuda.synchronize()
+    return out
+
+
+def _ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel`
+    from the committed `ncu --set full` capture summary (profiles/), or None."""
+    for path in (os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json"),):
+        try:
+            with open(path) as f:
+                v = json.load(f).get(kernel)
+            if v:
+                return v
+        except Exception:
+            pass
+    return None
 
 
 def main():
@@ -714,119 +913,82 @@ def main():
 
     import paper_2605_04084_b200 as F
 
-    blocks = build_model(rank, world)
-    step = DecodeStep(blocks, rank, world, pg)
-    step.h.copy_(__import__("synth").torch_activation(1, 4096, seed=11))
-
-    # ---- device-resident timed region (graph of the whole step) ----
-    g = capture(lambda: step.run(flags=F.FLAG_PDL), world)
-    launches_per_step = step.launches
+    B = 1
+    model, by = build_llama(rank, world, B=B)
+    if world > 1:
+        handles = [None] * world
+        dist.all_gather_object(handles, model.ipc_handle(), group=pg)
+        model.set_peers(handles)
     peaks, peak_src = _peaks()
-    with ClockSampler(local) as clk:
-        ms = timed(g, args.steps, args.warmup, rank, world, pg)
-    clocks = clk.summary()
-
-    # ---- e2e through the public API with host buffers ----
-    xh = torch.empty((1, 4096), dtype=torch.float16).pin_memory()
-    xh.copy_(step.h.cpu())
-    yh = torch.empty((1, 4096), dtype=torch.float16).pin_memory()
-
-    def e2e_fn():
-        step.h.copy_(xh, non_blocking=True)
-        out = step.run(flags=F.FLAG_PDL)
-        yh.copy_(out, non_blocking=True)
-
-    ge = capture(e2e_fn, world)
-    ms_e2e = timed(ge, args.steps, args.warmup, rank, world, pg)
-
-    tok_s = 1000.0 / ms
-    gbytes = layer_bytes(world)
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    # dominant kernel alone: k_chain launches (+ their accumulator memset node)
-    # timed with CUDA events on the launching stream, after the graph timing
-    kern_ms, kern_name, traffic = ms, "whole step (per-launch GEMVs)", None
-    if step.chain is not None:
-        if world > 1:
-            torch.cuda.synchronize()
-            dist.barrier()
-        for _ in range(3):
-            step.chain.run(step.h)
-        # k_chain launches alone, replayed from a CUDA graph (as in the timed
-        # region) on the capture stream, CUDA events on that stream
-        nk = 10
-        ks = torch.cuda.Stream()
-        ks.wait_stream(torch.cuda.current_stream())
-        kg = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(ks):
-            with torch.cuda.graph(kg, stream=ks):
-                for _ in range(nk):
-                    step.chain.run(step.h)
-        torch.cuda.synchronize()
-        reps = max(2, args.steps // (4 * nk))
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(ks):
-            kg.replay()
-            e0.record(ks)
-            for _ in range(reps):
-                kg.replay()
-            e1.record(ks)
-        torch.cuda.synchronize()
-        kern_ms = e0.elapsed_time(e1) / (reps * nk)
-        kern_name = "k_chain (one launch = the 224 GEMVs of a token%s)" % (
-            "" if world == 1 else ", this rank's row shard, all-gather fused over NVLink")
-        traffic = K_CHAIN_NCU_DRAM_BYTES
-    achieved = gbytes / (kern_ms * 1e-3) / 1e9
+
+    # ---- device-resident timed region: CUDA graph of one decode step ----
+    with ClockSampler(local) as clk:
+        ms, g = llama_timed(model, args.steps, args.warmup, rank, world)
+    clocks = clk.summary()
+    # ---- the two kernels of a step, timed separately on the launch stream ----
+    ch_ms, lm_ms = llama_kernel_ms(model, max(10, min(50, args.steps)), world)
+    # ---- e2e through the public API with host buffers ----
+    ms_e2e = llama_e2e(model, args.steps, args.warmup, rank, world)
+
+    tok_s = B * 1000.0 / ms
+    achieved = by["chain"] / (ch_ms * 1e-3) / 1e9
+    lm_gbs = by["lm_head"] / (lm_ms * 1e-3) / 1e9
 
     side = {}
     if rank == 0 and not args.no_side:
-        for pm in (512, 2048):   # configs[3]: prefill M = 512 and 2048 tokens
+        del g
+        for name, fn in (("pq_chain", lambda: pq_chain_side(peak)),
+                         ("llama_variants", lambda: llama_side(peak)),
+                         ("prefill_gemm_M512", lambda: prefill_tflops(M=512)),
+                         ("prefill_gemm_M2048", lambda: prefill_tflops(M=2048)),
+                         ("decode_sweep", lambda: decode_sweep(peak)),
+                         ("decode_batch", lambda: decode_batch(peak)),
+                         ("prefill_model", lambda: prefill_model(float(peaks.get("bf16_tflops", 1692.0)))),
+                         ("gpu_pack", pack_time)):
             try:
-                side["prefill_gemm_M%d" % pm] = prefill_tflops(M=pm)
-            except Exception as e:
-                side["prefill_gemm_M%d" % pm] = {"error": str(e)[:200]}
-        try:
-            side["decode_sweep"] = decode_sweep(peak)
-        except Exception as e:
-            side["decode_sweep"] = {"error": str(e)[:200]}
-        try:
-            side["decode_batch"] = decode_batch(peak)
-        except Exception as e:
-            side["decode_batch"] = {"error": str(e)[:200]}
-        try:
-            side["prefill_model"] = prefill_model(float(peaks.get("bf16_tflops", 1692.0)))
-        except Exception as e:
-            side["prefill_model"] = {"error": str(e)[:200]}
-        try:
-            side["gpu_pack"] = pack_time()
-        except Exception as e:
-            side["gpu_pack"] = {"error": str(e)[:200]}
+                side[name] = fn()
+            except Exception as e:  # report, never hide
+                side[name] = {"error": str(e)[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_side:
         r, thr, sample, _ = oracle_decode_rate(budget_s=15.0)
-        cpu = {"value": r, "unit": "tok/s", "cores": thr, "kind": "oracle", "sample": sample}
+        cpu = {"value": r, "unit": "tok/s", "cores": thr, "kind": "oracle", "sample": sample,
+               "cpu": _cpu_model()}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": tok_s, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f16", "data": "synthetic",
-            "config": {"workload": "llama3-8b-pq-decode-d2-C256-b1: 32 blocks x {q,k,v,o,gate,up,down} "
-                                   "PQ GEMVs, chained fp16 activations (attention/norm/lm_head excluded)",
-                       "executor": "persistent chain kernel (fasq_chain_*)" if step.chain is not None
-                                   else "one grouped GEMV launch per step",
-                       "global_batch": 1, "seq_len": 1,
-                       "parallelism": ("row-shard-tp%d+%s" % (world, step.tp_mode)) if world > 1 else "single-gpu",
-                       "d": D, "C": C, "weights_bytes_per_step": gbytes,
-                       "l2": "inputs larger than L2 (%.2f GB of PQ weights per step vs 126 MB L2)" % (gbytes / 1e9),
-                       "timing": "CUDA graph of one step, K replays between CUDA events, max over ranks"},
-            "e2e": {"value": 1000.0 / ms_e2e, "unit": "tok/s", "h2d_bytes_per_step": 4096 * 2,
-                    "d2h_bytes_per_step": 4096 * 2},
-            "gpu_launches": launches_per_step * args.steps,
+            "config": {"workload": "llama3-8b-pq-greedy-decode-d2-C256-b1: whole Llama-3-8B-shaped model "
+                                   "(embedding, 32 x {RMSNorm, PQ q/k/v, RoPE + KV cache + attention, PQ o + "
+                                   "residual, RMSNorm, PQ gate/up, SwiGLU, PQ down + residual}, final RMSNorm, "
+                                   "fp16 lm_head, greedy argmax), KV positions %d..%d (prompt %d, gen %d, P:438)"
+                                   % (PROMPT, MAX_T - 1, PROMPT, MAX_T - PROMPT),
+                       "executor": "fasq_llama: persistent chain kernel (all 161 steps) + lm_head/argmax kernel",
+                       "global_batch": B, "seq_len": 1,
+                       "parallelism": ("megatron-tp%d (fused NVLink all-reduce/gather in the counted stores)"
+                                       % world) if world > 1 else "single-gpu",
+                       "d": D, "C": C, "pq_bytes_per_step": by["pq"], "bytes_per_step": by["step"],
+                       "l2": "inputs larger than L2 (%.2f GB per step vs 126 MB L2)" % (by["step"] / 1e9),
+                       "timing": "CUDA graph of one step (2 launches), K replays between CUDA events, max over ranks"},
+            "e2e": {"value": B * 1000.0 / ms_e2e, "unit": "tok/s", "h2d_bytes_per_step": 4 * B,
+                    "d2h_bytes_per_step": 4 * B,
+                    "how": "per step fasq_llama_reset (H2D of the B tokens from pinned host memory) + "
+                           "fasq_llama_step_host (chain + lm_head + D2H of the chosen tokens), wall clock"},
+            "gpu_launches": 2 * args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": kern_name, "kernel_ms": kern_ms, "algorithmic_bytes": gbytes,
-                         "peak_source": "%s hbm_gbs" % peak_src},
+                         "frac": achieved / peak, "traffic": _ncu_traffic("k_chain"),
+                         "kernel": "k_chain (whole-model decode chain; %.1f%% of the step)"
+                                   % (100.0 * ch_ms / (ch_ms + lm_ms)),
+                         "kernel_ms": ch_ms, "algorithmic_bytes": by["chain"],
+                         "peak_source": "%s hbm_gbs" % peak_src,
+                         "lm_head": {"kernel": "k_lm_head", "ms": lm_ms, "algorithmic_bytes": by["lm_head"],
+                                     "GBps": lm_gbs, "frac": lm_gbs / peak,
+                                     "traffic": _ncu_traffic("k_lm_head")},
+                         "step_frac": by["step"] / (ms * 1e-3) / 1e9 / peak},
             "clocks": clocks,
             "cpu_baseline": cpu,
             "side": side,
@@ -835,6 +997,17 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 if __name__ == "__main__":

@@ -341,6 +341,12 @@ fasq_status fasq_llama_reset(fasq_llama* model, const int32_t* tokens_host, int3
 /* One greedy decode step of every sequence: TWO launches (chain, lm_head);
  * the chosen tokens feed the next step on the device (graph-replayable). */
 fasq_status fasq_llama_step(fasq_llama* model, void* stream);
+/* One step in parts, for per-kernel timing: part 0 = both launches
+ * (fasq_llama_step), 1 = the chain kernel only, 2 = the lm_head kernel only.
+ * A part-1 call must be followed by a part-2 call on the same stream before
+ * the next step (the next chain run waits for the lm_head's token).
+ * FASQ_E_ARG for another part. */
+fasq_status fasq_llama_step_ex(fasq_llama* model, void* stream, int32_t part);
 /* The tokens the last step chose (int32 [B], device). */
 fasq_status fasq_llama_tokens(const fasq_llama* model, int32_t* tokens_dev, void* stream);
 /* End to end with a HOST buffer: one step, then the chosen tokens are copied

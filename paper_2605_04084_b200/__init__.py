@@ -38,7 +38,7 @@ EXPORTED = ["fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_
             "fasq_chain_plan_ks", "fasq_gemv_host", "fasq_gemm",
             "fasq_llama_create", "fasq_llama_ipc_handle", "fasq_llama_set_peers", "fasq_llama_set_peer_models",
             "fasq_llama_chain",
-            "fasq_llama_kv_cache", "fasq_llama_reset", "fasq_llama_step", "fasq_llama_tokens",
+            "fasq_llama_kv_cache", "fasq_llama_reset", "fasq_llama_step", "fasq_llama_step_ex", "fasq_llama_tokens",
             "fasq_llama_step_host", "fasq_llama_logits", "fasq_llama_token_history", "fasq_llama_free",
             "fasq_last_launch_count", "fasq_status_string", "fasq_last_error_message",
             "fasq_abi_version"]
@@ -136,6 +136,7 @@ def _load():
     L.fasq_llama_reset.argtypes = [vp, ctypes.POINTER(i32), i32, vp]
     L.fasq_llama_step.argtypes = [vp, vp]
     L.fasq_llama_tokens.argtypes = [vp, vp, vp]
+    L.fasq_llama_step_ex.argtypes = [vp, vp, i32]
     L.fasq_llama_step_host.argtypes = [vp, ctypes.POINTER(i32), vp]
     L.fasq_llama_logits.argtypes = [vp, i32, pp]
     L.fasq_llama_token_history.argtypes = [vp, vp, vp]
@@ -151,7 +152,7 @@ def _load():
                  "fasq_chain_ctas", "fasq_gemm", "fasq_last_launch_count", "fasq_chain_run_host",
                  "fasq_chain_check", "fasq_chain_plan_ks", "fasq_llama_create", "fasq_llama_ipc_handle",
                  "fasq_llama_set_peers", "fasq_llama_kv_cache", "fasq_llama_reset", "fasq_llama_step",
-                 "fasq_llama_tokens", "fasq_llama_set_peer_models", "fasq_llama_step_host", "fasq_llama_logits", "fasq_llama_token_history",
+                 "fasq_llama_tokens", "fasq_llama_step_ex", "fasq_llama_set_peer_models", "fasq_llama_step_host", "fasq_llama_logits", "fasq_llama_token_history",
                  "fasq_abi_version"):
         getattr(L, name).restype = ctypes.c_int32
     return L
@@ -535,6 +536,10 @@ class Llama:
 
     def step(self, stream=None):
         _check(lib.fasq_llama_step(self._h, _stream(stream)))
+
+    def step_part(self, part: int, stream=None):
+        """part 1: the chain kernel of a step, 2: its lm_head kernel (per-kernel timing)."""
+        _check(lib.fasq_llama_step_ex(self._h, _stream(stream), part))
 
     def tokens(self, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         if out is None:

@@ -444,6 +444,16 @@ fasq_status fasq_llama_step(fasq_llama* m, void* stream) {
     return s;
 }
 
+fasq_status fasq_llama_step_ex(fasq_llama* m, void* stream, int32_t part) {
+    if (!m || part < 0 || part > 2) return FASQ_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    fasq_status s = FASQ_OK;
+    if (part != 2) s = chain_launch(m->chain, m->rope /* unused external input */, st);
+    if (s == FASQ_OK && part != 1) s = lm_launch(m, st);
+    if (s == FASQ_OK) set_launch_count(part == 0 ? 2 : 1);
+    return s;
+}
+
 fasq_status fasq_llama_tokens(const fasq_llama* m, int32_t* tokens_dev, void* stream) {
     if (!m || !tokens_dev) return FASQ_E_ARG;
     k_llama_tokens<<<1, 32, 0, (cudaStream_t)stream>>>(m->chain->tail(), m->chain->nctas, m->desc.B,
