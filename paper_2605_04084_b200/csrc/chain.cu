@@ -56,18 +56,42 @@ namespace {
 // until it carries its `ks` contributions (peers' red.adds of the last step
 // may still be in flight when this rank's kernel ends).  A run that raised
 // the out-of-range flag yields NaN (float outputs).
+// With a lazy base (off2 >= 0) the value is the sum of both words; with
+// RMSNorm slots (sc_off >= 0) it is multiplied by the scale every consumer
+// applies (warp_norm_scale's fixed summation order, emulated serially).
 __global__ void k_counted_convert(const unsigned long long* __restrict__ arenas, long long arena_words, int nctas,
-                                  long long off, int64_t n, int ks, void* out, int dtype, int sys) {
+                                  long long off, int64_t n, int ks, void* out, int dtype, int sys, long long off2,
+                                  int ks2, long long sc_off, int sc_n, int sc_F, float sc_eps, int64_t ld) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const unsigned long long* tail = arenas + 2 * arena_words;
     const unsigned long long runs = tail[T_ENTRY] / (unsigned long long)nctas;
     const unsigned last = (unsigned)((runs + 1ull) & 1ull);   // parity of run (runs - 1)
-    const long long v = core::poll_value(arenas + (long long)last * arena_words + off + i, ks, sys != 0);
+    const unsigned long long* buf = arenas + (long long)last * arena_words;
+    long long v = core::poll_value(buf + off + i, ks, sys != 0);
+    if (off2 >= 0) v += core::poll_value(buf + off2 + i, ks2, sys != 0);
+    double sc = 1.0;
+    if (sc_off >= 0) {
+        const int b = (int)(i / ld);
+        float a[32];
+        for (int k = 0; k < 32; ++k) {
+            float t = 0.f;
+            if (k < sc_n) t += word_f32(buf[sc_off + b * 64 + k]);
+            if (k + 32 < sc_n) t += word_f32(buf[sc_off + b * 64 + k + 32]);
+            a[k] = t;
+        }
+        for (int m = 16; m >= 1; m >>= 1) {
+            float na[32];
+            for (int k = 0; k < 32; ++k) na[k] = a[k] + a[k ^ m];
+            for (int k = 0; k < 32; ++k) a[k] = na[k];
+        }
+        sc = (double)(1.0f / sqrtf(a[0] / (float)sc_F + sc_eps));
+    }
     const bool bad = tail[T_OVF] != 0ull;
-    if (dtype == FASQ_ACC_I64) reinterpret_cast<long long*>(out)[i] = v;
-    else if (dtype == FASQ_F32) reinterpret_cast<float*>(out)[i] = bad ? __int_as_float(0x7fc00000) : (float)((double)v * core::kAccInv);
-    else reinterpret_cast<__half*>(out)[i] = bad ? __ushort_as_half((unsigned short)0x7e00) : __double2half((double)v * core::kAccInv);
+    const double val = (double)v * core::kAccInv * sc;
+    if (dtype == FASQ_ACC_I64) reinterpret_cast<long long*>(out)[i] = sc_off >= 0 ? __double2ll_rn(val * 4294967296.0) : v;
+    else if (dtype == FASQ_F32) reinterpret_cast<float*>(out)[i] = bad ? __int_as_float(0x7fc00000) : (float)val;
+    else reinterpret_cast<__half*>(out)[i] = bad ? __ushort_as_half((unsigned short)0x7e00) : __double2half(val);
 }
 
 // Attention output of the LAST run (ATTN step partials [B][heads][P][hd + 2])
@@ -205,6 +229,10 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
     c->kinds.resize(n_steps);
     c->nsq_off.assign(n_steps, -1);
     c->nsq_n.assign(n_steps, 0);
+    c->nsq_F.assign(n_steps, 0);
+    c->nsq_eps.assign(n_steps, 0.f);
+    c->nsq_epi.assign(n_steps, 0);
+    c->lazy.assign(n_steps, -1);
     c->attn_hd.assign(n_steps, 0);
     c->attn_heads.assign(n_steps, 0);
     std::vector<int> pq_F_in(n_steps, 0);
@@ -226,6 +254,11 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
                 words += (int64_t)B * ld;
             }
             pq_F_in[s] = (int)F_in;
+            if (S.lazy_step >= 0) {
+                if (S.lazy_step >= s || S.layers.size() != 1 || steps[S.lazy_step].kind == SK_ATTN)
+                    return fail(FASQ_E_ARG, "lazy residual base must be an earlier PQ/EMBED step (1-layer steps)");
+                c->lazy[s] = S.lazy_step;
+            }
             if (S.in_mode == IN_RMSNORM) {   // sum-of-squares slots [B][64]
                 c->nsq_off[s] = words;
                 words += (int64_t)B * 64;
@@ -275,6 +308,18 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
         std::memset(&P, 0, sizeof(P));
         P.kind = S.kind;
         P.res_off = -1;
+        P.res2_off = -1;
+        P.x2_off = -1;
+        P.sc_off = -1;
+        // the RMSNorm scale of a normed source step (applied by this consumer)
+        auto set_scale = [&](int src) {
+            if (src >= 0 && c->nsq_off[src] >= 0 && !c->nsq_epi[src]) {
+                P.sc_off = c->nsq_off[src];
+                P.sc_n = c->nsq_n[src];
+                P.sc_F = c->nsq_F[src];
+                P.sc_eps = c->nsq_eps[src];
+            }
+        };
         if (S.kind == SK_EMBED) {
             P.embed = S.embed;
             P.e_off = c->acc_off[s][0];
@@ -306,6 +351,7 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
             P.n_kv = S.n_kv;
             P.hd = hd;
             P.parts = model->attn_parts;
+            set_scale(S.q_step);
             (void)Q;
             for (int h = 0; h < S.n_heads; ++h)
                 for (int q = 0; q < P.parts; ++q) {
@@ -351,6 +397,7 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
                 P.x2_off = c->acc_off[src][1];
                 P.x2_ks = c->acc_ks[src][1];
                 P.x_sys = steps[src].out_all && world > 1;
+                set_scale(src);
             } else if (S.in_mode == IN_ATTN) {
                 if (steps[src].kind != SK_ATTN) return fail(FASQ_E_ARG, "ATTN input needs an ATTN step");
                 if (c->acc_ld[src][0] != P.F_in) return fail(FASQ_E_SHAPE, "attention width != F_in");
@@ -372,6 +419,15 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
                     P.nsq_off = c->nsq_off[s];
                     P.nsq_n = ks[0];
                     c->nsq_n[s] = ks[0];
+                    c->nsq_F[s] = P.F_in;
+                    c->nsq_eps[s] = S.eps;
+                    c->nsq_epi[s] = S.scale_epilogue ? 1 : 0;
+                    P.epi_scale = S.scale_epilogue ? 1 : 0;
+                    if (c->lazy[src] >= 0) {   // h = words + lazy base words
+                        P.x2_off = c->acc_off[c->lazy[src]][0];
+                        P.x2_ks = c->acc_ks[c->lazy[src]][0];
+                        if (steps[c->lazy[src]].kind == SK_PQ && steps[c->lazy[src]].out_all && world > 1) P.x_sys = 1;
+                    }
                 }
             }
             if (S.in_mode != IN_WORDS && !pair) return fail(FASQ_E_UNSUPPORTED, "input transforms need d <= 2");
@@ -386,6 +442,12 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
             P.res_ks = c->acc_ks[S.res_step][S.res_layer];
             P.res_here = S.res_here ? 1 : 0;
             P.res_sys = steps[S.res_step].kind == SK_PQ && steps[S.res_step].out_all && world > 1;
+            const int lz = c->lazy[S.res_step];
+            if (lz >= 0 && S.res_layer == 0) {
+                P.res2_off = c->acc_off[lz][0];
+                P.res2_ks = c->acc_ks[lz][0];
+                if (steps[lz].kind == SK_PQ && steps[lz].out_all && world > 1) P.res_sys = 1;
+            }
         }
         P.out_all = S.out_all && world > 1;
         for (int l = 0; l < nl; ++l) {
@@ -521,9 +583,13 @@ fasq_status chain_output(const fasq_chain* c, int step, int layer, void* y_dev, 
         FASQ_CUDA_TRY(cudaGetLastError());
         return FASQ_OK;
     }
-    k_counted_convert<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(c->arenas, c->arena_words, c->nctas,
-                                                                  c->acc_off[step][layer], n, c->acc_ks[step][layer],
-                                                                  y_dev, (int)dtype, c->world > 1);
+    const int lz = layer == 0 ? c->lazy[step] : -1;
+    const long long off2 = lz >= 0 ? c->acc_off[lz][0] : -1;
+    const int ks2 = lz >= 0 ? c->acc_ks[lz][0] : 0;
+    const long long sc_off = c->nsq_epi[step] ? -1 : c->nsq_off[step];
+    k_counted_convert<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        c->arenas, c->arena_words, c->nctas, c->acc_off[step][layer], n, c->acc_ks[step][layer], y_dev, (int)dtype,
+        c->world > 1, off2, ks2, sc_off, c->nsq_n[step], c->nsq_F[step], c->nsq_eps[step], c->acc_ld[step][layer]);
     FASQ_CUDA_TRY(cudaGetLastError());
     return FASQ_OK;
 }

@@ -29,6 +29,10 @@ enum ChainInMode : int {
 // contributed by the K ranges of (layer 0, row tile 0) -- they cover F_in
 // exactly once -- into per-range slots (fp32 bits in counted words, count 1);
 // every warp sums the slots in a fixed order, so every CTA applies the same s.
+// The scale is applied by the CONSUMERS of the normed step's outputs (the
+// attention step for q/k/v, the SwiGLU staging for gate/up, chain outputs):
+// their slot loads overlap their own input waits, while in the producing
+// epilogue they were one more L2 round trip on the critical path.
 // Attention output (SK_ATTN): per (token, head, cache part) the unnormalised
 // o [hd], the running max m and the sum l, fp32 bits in counted words
 // [B][heads][parts][hd + 2]; the consumer merges the parts in fixed order.
@@ -40,7 +44,12 @@ struct StepDesc {
     int src_step = -1, src_layer = 0;
     const __half* gamma = nullptr;           // IN_RMSNORM weight [F_in]
     float eps = 1e-5f;
+    bool scale_epilogue = false;             // IN_RMSNORM: apply the scale in this step's epilogue (its
+                                             // consumers cannot hide the slot loads) instead of in the consumers
     int res_step = -1, res_layer = 0;        // SK_PQ: residual added to layer 0's output
+    int lazy_step = -1;                      // SK_PQ, 1 layer: the VALUE of this output is its words + the
+                                             // layer-0 words of lazy_step (a residual sum materialised by
+                                             // its consumers: norm staging, residual epilogue, outputs)
     bool res_here = true;                    // this rank adds the residual (K-sharded steps: one rank)
     // outputs: local (false) or written into every rank's arena (true).  With
     // kshard, every rank holds a K slice (subspaces) of the layer and writes
@@ -108,6 +117,10 @@ struct fasq_chain {
     std::vector<std::vector<int>> acc_ks;        // per step, per output: contributions per word
     std::vector<long long> nsq_off;              // per step: RMSNorm sum-of-squares slots [B][64] (-1: none)
     std::vector<int> nsq_n;                      // per step: slots per token (K ranges of layer 0)
+    std::vector<int> nsq_F;                      // per step: F_in (the normed width)
+    std::vector<float> nsq_eps;
+    std::vector<char> nsq_epi;                   // per step: the scale is applied in the epilogue (outputs are final)
+    std::vector<int> lazy;                       // per step: lazy base step (-1: none)
     std::vector<int> attn_hd, attn_heads;        // per ATTN step: head dim, local heads (output layout)
     int ext_F_in = 0;
     unsigned long long* arenas = nullptr;        // [2][arena_words] + tail (ONE allocation, IPC-exportable)

@@ -35,7 +35,7 @@ struct alignas(128) ChainItem {
 // Per-step description.  The PQ fields fill the first 128-B line.
 struct alignas(128) ChainPhase {
     int kind, in_mode, F_in, x_ks;
-    long long x_off, x2_off;    // input words (WORDS/NORM/ATTN: x; SILU: gate x, up x2)
+    long long x_off, x2_off;    // input words (WORDS/NORM/ATTN: x; SILU: gate x, up x2; NORM: x2 = lazy base, < 0: none)
     int x2_ks, x_sys, res_ks, res_here;   // x_sys: input words written by peers (system-scope polls)
     const __half* gamma;        // IN_RMSNORM
     long long res_off;          // residual words (< 0: none), same [B][ld] indexing as the output
@@ -43,6 +43,13 @@ struct alignas(128) ChainPhase {
     int nsq_n, res_sys, out_all, a_heads;   // out_all: outputs red.add'ed into every rank's arena
     float eps;
     int a_hd, a_parts;          // IN_ATTN: layout of the source attention partials
+    long long res2_off;         // lazy base of the residual (< 0: none)
+    int res2_ks;
+    int sc_n;                   // SILU input / ATTN: RMSNorm scale of the source step, from its
+    long long sc_off;           //   sum-of-squares slots (sc_off < 0: none)
+    int sc_F;
+    float sc_eps;
+    int epi_scale;              // IN_RMSNORM: the scale is applied in this step's epilogue
     // ATTN
     long long q_off, k_off, v_off, o_off;
     int q_ks, k_ks, v_ks, q_ld, kv_ld;
@@ -60,12 +67,12 @@ struct alignas(128) ChainPhase {
 // of SMEM the L1 left for register spills is small, and spills in the loop
 // cost more than the loop saves.
 struct EpiParams {
-    long long y_off, res_off, nsq_off;
+    long long y_off, res_off, res2_off, nsq_off;
     int row0_g, ld, F_out, r0;
     int add_res, res_ks, res_sys, out_all;
-    int nsq_n, F_in;
+    int res2_ks, epi_scale, nsq_n, F_in;
     float eps;
-    int in_mode;
+    int pad;
 };
 
 struct ChainParams {
@@ -176,6 +183,38 @@ __device__ __forceinline__ void embed_item(const ChainPhase* ph, unsigned long l
     }
 }
 
+// RMSNorm scale s[b] = 1/sqrt(sum_k slot[b][k] / n + eps) from the n_slots
+// sum-of-squares slots of a norm step; every warp computes it the same way
+// (lane k and k + 32, xor tree) -> identical in every warp and CTA.
+template <int NB>
+__device__ __forceinline__ void warp_norm_scale(float (&sc)[NB], const unsigned long long* slots, int n_slots, int n,
+                                                float eps, int B, int lane) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        float a = 0.f;
+        if (b < B) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int k = lane + 32 * h;
+                if (k < n_slots) {
+                    unsigned long long v;
+                    const unsigned long long t0 = dev::globaltimer();
+                    while (((v = ld_word(slots + b * 64 + k, false)) >> core::kCntShift) != 1ull)
+                        if (dev::globaltimer() - t0 > 4000000000ull) __trap();
+                    a += word_f32(v);
+                }
+            }
+        }
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) a += __shfl_xor_sync(0xffffffffu, a, m);
+        sc[b] = 1.0f / sqrtf(a / (float)n + eps);
+    }
+}
+
+// MODEL: the whole-model step kinds and input transforms (EMBED, ATTN,
+// RMSNorm / SwiGLU / attention inputs, residual epilogue) are compiled in;
+// plain GEMV chains use the MODEL = false instance (fewer live registers in
+// the gather loop: the kernel runs at the 96-register cap of 17 warps).
 // ---- ATTN: one (local q head, cache part) item ------------------------------
 // Llama attention for the token at `pos` (HF LlamaAttention semantics):
 // RoPE (rotate-half, cos/sin table) on q and k, the new fp16 k/v appended to
@@ -196,6 +235,8 @@ __device__ __forceinline__ void attn_item(const ChainPhase* ph, int head, int pa
     const AttnRows r = attn_rows(part, P, pos, B, hd);
     const int nrow = r.t1 - r.t0, nk = max(0, r.te - r.t0);
     const float qk_scale = 1.0f / sqrtf((float)hd);
+    // RoPE table row of this position (independent of q/k/v: loaded first)
+    const float2 cs = tid < half ? rope[(size_t)pos * half + tid] : make_float2(0.f, 0.f);
     float* s_q = reinterpret_cast<float*>(slot + kAttnKV);   // [128] raw q
     float* s_k = s_q + 128;                                  // [128] raw k
     float* s_v = s_k + 128;                                  // [128] raw v
@@ -230,15 +271,23 @@ __device__ __forceinline__ void attn_item(const ChainPhase* ph, int head, int pa
             const int ks = which == 0 ? ph->q_ks : which == 1 ? ph->k_ks : ph->v_ks;
             const float f = (float)((double)core::poll_value(a, ks, false) * core::kAccInv);
             (which == 0 ? s_q : which == 1 ? s_k : s_v)[e] = f;
+        } else if (warp == NT / 32 - 1) {
+            // the q/k/v words hold the products of the UNSCALED normed input
+            // (chain_internal.cuh): the last warp (idle above, 3 hd <= NT - 32)
+            // computes the qkv step's RMSNorm scale of token b meanwhile
+            float sc[1] = {1.f};
+            if (ph->sc_off >= 0)
+                warp_norm_scale<1>(sc, cur + ph->sc_off + (size_t)b * 64, ph->sc_n, ph->sc_F, ph->sc_eps, 1, lane);
+            if (lane == 0) s_ml[2] = sc[0];
         }
         consumer_bar(NT);
+        const float sb = s_ml[2];
         // 2. RoPE (rotate half): x'[i] = x[i] c - x[i+half] s, x'[i+half] = x[i+half] c + x[i] s
         __half* kc = ph->kc + ((size_t)b * n_kv + kvh) * (size_t)max_T * hd;
         __half* vc = ph->vc + ((size_t)b * n_kv + kvh) * (size_t)max_T * hd;
         const bool writer = head % grp == 0 && r.t1 == pos + 1;   // one cache writer per KV head
         if (tid < half) {
-            const float2 cs = rope[(size_t)pos * half + tid];
-            const float q0 = s_q[tid], q1 = s_q[tid + half], k0 = s_k[tid], k1 = s_k[tid + half];
+            const float q0 = s_q[tid] * sb, q1 = s_q[tid + half] * sb, k0 = s_k[tid] * sb, k1 = s_k[tid + half] * sb;
             s_qr[tid] = q0 * cs.x - q1 * cs.y;
             s_qr[tid + half] = q1 * cs.x + q0 * cs.y;
             const __half kn0 = __float2half_rn(k0 * cs.x - k1 * cs.y), kn1 = __float2half_rn(k1 * cs.x + k0 * cs.y);
@@ -247,7 +296,7 @@ __device__ __forceinline__ void attn_item(const ChainPhase* ph, int head, int pa
             if (writer) { kc[(size_t)pos * hd + tid] = kn0; kc[(size_t)pos * hd + tid + half] = kn1; }
         } else if (tid < half + hd) {
             const int e = tid - half;
-            const __half vn = __float2half_rn(s_v[e]);
+            const __half vn = __float2half_rn(s_v[e] * sb);
             s_vn[e] = vn;
             if (writer) vc[(size_t)pos * hd + e] = vn;
         }
@@ -318,8 +367,7 @@ __device__ __forceinline__ void attn_item(const ChainPhase* ph, int head, int pa
             if (tid == 0) st_word(ob + hd, f32_word(s_ml[0]));
         }
         consumer_bar(NT);
-        if (tid == 0) {   // l last, with release: a reader that sees l final sees this part's o and m
-            __threadfence();
+        if (tid == 0) {   // l last, with release (cumulative over the barrier): a reader that sees l final sees o and m
             asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(ob + hd + 1), "l"(f32_word(s_ml[1])) : "memory");
         }
     }
@@ -395,38 +443,6 @@ __device__ __forceinline__ void stage_x_attn(uint8_t* s_x, const unsigned long l
     }
 }
 
-// RMSNorm scale s[b] = 1/sqrt(sum_k slot[b][k] / n + eps) from the n_slots
-// sum-of-squares slots of a norm step; every warp computes it the same way
-// (lane k and k + 32, xor tree) -> identical in every warp and CTA.
-template <int NB>
-__device__ __forceinline__ void warp_norm_scale(float (&sc)[NB], const unsigned long long* slots, int n_slots, int n,
-                                                float eps, int B, int lane) {
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-        float a = 0.f;
-        if (b < B) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int k = lane + 32 * h;
-                if (k < n_slots) {
-                    unsigned long long v;
-                    const unsigned long long t0 = dev::globaltimer();
-                    while (((v = ld_word(slots + b * 64 + k, false)) >> core::kCntShift) != 1ull)
-                        if (dev::globaltimer() - t0 > 4000000000ull) __trap();
-                    a += word_f32(v);
-                }
-            }
-        }
-#pragma unroll
-        for (int m = 16; m >= 1; m >>= 1) a += __shfl_xor_sync(0xffffffffu, a, m);
-        sc[b] = 1.0f / sqrtf(a / (float)n + eps);
-    }
-}
-
-// MODEL: the whole-model step kinds and input transforms (EMBED, ATTN,
-// RMSNorm / SwiGLU / attention inputs, residual epilogue) are compiled in;
-// plain GEMV chains use the MODEL = false instance (fewer live registers in
-// the gather loop: the kernel runs at the 96-register cap of 17 warps).
 template <int D, int NB, int NW, int ST, bool MODEL>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     constexpr int E = core::Entry<D>::value;
@@ -629,13 +645,26 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                                                  ng, xsys, p.backoff);
         } else if constexpr (PAIR && MODEL) {
             if (in_mode == IN_RMSNORM) {
-                core::stage_x_counted<D, NB, NW, XF, core::XM_GAMMA>(s_x, cur + pv.x_off, pv.x_ks, pv.F_in, p.B,
-                                                                     w.N_ss, w.g_begin, ng, xsys, 0, nullptr, 0,
-                                                                     w.nsq >= 0 ? s_sq : nullptr, pv.gamma);
+                if (pv.x2_off >= 0)   // source = a lazily materialised residual sum (x + x2)
+                    core::stage_x_counted<D, NB, NW, XF, core::XM_GAMMA2>(s_x, cur + pv.x_off, pv.x_ks, pv.F_in, p.B,
+                                                                          w.N_ss, w.g_begin, ng, xsys, 0,
+                                                                          cur + pv.x2_off, pv.x2_ks,
+                                                                          w.nsq >= 0 ? s_sq : nullptr, pv.gamma);
+                else
+                    core::stage_x_counted<D, NB, NW, XF, core::XM_GAMMA>(s_x, cur + pv.x_off, pv.x_ks, pv.F_in, p.B,
+                                                                         w.N_ss, w.g_begin, ng, xsys, 0, nullptr, 0,
+                                                                         w.nsq >= 0 ? s_sq : nullptr, pv.gamma);
             } else if (in_mode == IN_SILU) {
+                // gate/up hold the products of the unscaled normed input: the
+                // RMSNorm scale of their input (slots, warp_norm_scale) applies here
+                float sc[NB];
+#pragma unroll
+                for (int b = 0; b < NB; ++b) sc[b] = 1.f;
+                if (pv.sc_off >= 0) warp_norm_scale<NB>(sc, cur + pv.sc_off, pv.sc_n, pv.sc_F, pv.sc_eps, p.B, lane);
                 core::stage_x_counted<D, NB, NW, XF, core::XM_SILU>(s_x, cur + pv.x_off, pv.x_ks, pv.F_in, p.B,
                                                                     w.N_ss, w.g_begin, ng, xsys, 0,
-                                                                    cur + pv.x2_off, pv.x2_ks);
+                                                                    cur + pv.x2_off, pv.x2_ks, nullptr, nullptr,
+                                                                    pv.sc_off >= 0 ? sc : nullptr);
             } else {
                 stage_x_attn<D, NB, NW, XF>(s_x, cur + pv.x_off, p.B, w.N_ss, w.g_begin, ng, pv.a_heads, pv.a_hd,
                                             pv.a_parts);
@@ -646,7 +675,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             EpiParams e;
             e.y_off = wp->y_off;
             e.res_off = phs->res_off;
+            e.res2_off = phs->res2_off;
+            e.res2_ks = phs->res2_ks;
+            e.epi_scale = phs->epi_scale;
             e.nsq_off = phs->nsq_off;
+            e.nsq_n = phs->nsq_n;
+            e.F_in = phs->F_in;
+            e.eps = phs->eps;
             e.row0_g = wp->row0_g;
             e.ld = wp->ld;
             e.F_out = wp->F_out;
@@ -655,10 +690,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             e.res_ks = phs->res_ks;
             e.res_sys = phs->res_sys;
             e.out_all = phs->out_all;
-            e.nsq_n = phs->nsq_n;
-            e.F_in = phs->F_in;
-            e.eps = phs->eps;
-            e.in_mode = in_mode;
             s_ep = e;
         }
         consumer_bar(NT);
@@ -696,7 +727,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             }
             core::reduce_set<NB, G>(acc, lane);
             if (active) {
-                if (MODEL && s_ep.in_mode == IN_RMSNORM) {
+                if (MODEL && s_ep.epi_scale) {
                     float sc[NB];
                     warp_norm_scale<NB>(sc, cur + s_ep.nsq_off, s_ep.nsq_n, s_ep.F_in, s_ep.eps, p.B, lane);
 #pragma unroll
@@ -709,7 +740,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                 const long long off = (long long)(s_run & 1u) * p.arena_words + s_ep.y_off + row0_g;
                 core::set_values<NB, G>(acc, qv, r0 + wrow0, lane, F_out, p.B,
                                         MODEL && s_ep.add_res ? cur + s_ep.res_off + row0_g : nullptr, ld,
-                                        s_ep.res_ks, s_ep.res_sys != 0, s_tail + T_OVF);
+                                        s_ep.res_ks, s_ep.res_sys != 0, s_tail + T_OVF,
+                                        MODEL && s_ep.res2_off >= 0 ? cur + s_ep.res2_off + row0_g : nullptr,
+                                        s_ep.res2_ks);
                 if (s_ep.out_all) {
                     for (int q = 0; q < p.world; ++q)
                         core::counted_store_q<NB>(qv, p.peers[q] + off, r0 + wrow0, lane, F_out, ld, p.B, sys_out);

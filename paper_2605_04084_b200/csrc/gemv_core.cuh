@@ -590,17 +590,49 @@ __device__ __forceinline__ void counted_store(const RowTotals<NB, RW>& t, unsign
 template <int NB, int G>
 __device__ __forceinline__ void set_values(const float (&v)[2 * G * NB], long long (&q)[2 * NB], int row0w, int lane,
                                            int F_out, int B, const unsigned long long* res, int res_ld, int res_ks,
-                                           bool res_sys, unsigned long long* ovf) {
+                                           bool res_sys, unsigned long long* ovf,
+                                           const unsigned long long* res2 = nullptr, int res2_ks = 0) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int row = row0w + 32 * h + lane;
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-            long long t = __float2ll_rn(v[h * NB + b] * kAccScale);
-            if (res && row < F_out && b < B) t += poll_value(res + (size_t)b * res_ld + row, res_ks, res_sys);
-            q[h * NB + b] = cnt_clamp(t, ovf);
+        for (int b = 0; b < NB; ++b) q[h * NB + b] = __float2ll_rn(v[h * NB + b] * kAccScale);
+    if (res) {
+        // residual words (and the lazy base res2, chain_internal.cuh): every
+        // word of this lane in flight at once, reloaded until all are final
+        constexpr int NR = 4 * NB;
+        unsigned long long w[NR];
+        bool need[NR];
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+            const int src = i / (2 * NB), h = (i / NB) & 1, b = i % NB;
+            const int row = row0w + 32 * h + lane;
+            need[i] = row < F_out && b < B && (src == 0 || res2 != nullptr);
+            w[i] = 0ull;
+        }
+        const unsigned long long t0 = dev::globaltimer();
+        for (bool done = false; !done;) {
+            done = true;
+#pragma unroll
+            for (int i = 0; i < NR; ++i) {
+                const int src = i / (2 * NB), h = (i / NB) & 1, b = i % NB;
+                const int ks = src == 0 ? res_ks : res2_ks;
+                if (!need[i] || (w[i] >> kCntShift) == (unsigned long long)ks) continue;
+                const unsigned long long* a = (src == 0 ? res : res2) + (size_t)b * res_ld + row0w + 32 * h + lane;
+                if (res_sys) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w[i]) : "l"(a) : "memory");
+                else asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w[i]) : "l"(a) : "memory");
+                if ((w[i] >> kCntShift) != (unsigned long long)ks) done = false;
+            }
+            if (!done && dev::globaltimer() - t0 > 4000000000ull) __trap();
+        }
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+            const int src = i / (2 * NB);
+            const int ks = src == 0 ? res_ks : res2_ks;
+            if (need[i]) q[i % (2 * NB)] += (long long)(w[i] & kCntMask) - (long long)ks * kCntBias;
         }
     }
+#pragma unroll
+    for (int i = 0; i < 2 * NB; ++i) q[i] = cnt_clamp(q[i], ovf);
 }
 
 // Counted stores of set_values' results: rows row0w + lane and row0w + 32 +
@@ -632,22 +664,25 @@ __device__ __forceinline__ void counted_store_q(const long long (&q)[2 * NB], un
 //   XM_GAMMA  x = fp16(fp32(value) * gamma[col])               (RMSNorm with the scale folded into
 //             the epilogue, chain_internal.cuh); with sq != NULL also the sum of fp32(value)^2 per
 //             token over this K range: sq[warp * NB + b] = the warp's partial (fixed order)
-//   XM_SILU   x = fp16(silu(g) * u), g/u = values of x / x2    (SwiGLU gate * up, fp32)
-constexpr int XM_WORDS = 0, XM_GAMMA = 1, XM_SILU = 2;
+//   XM_GAMMA2 as XM_GAMMA of the value (x word + x2 word) (a lazily materialised residual sum)
+//   XM_SILU   x = fp16(silu(g) * u), g/u = values of x / x2    (SwiGLU gate * up, fp32), with
+//             xs != NULL: g and u scaled by xs[b] first (the RMSNorm scale of the gate/up input)
+constexpr int XM_WORDS = 0, XM_GAMMA = 1, XM_SILU = 2, XM_GAMMA2 = 3;
 
 template <int D, int NB, int NW, bool XF = false, int MODE = XM_WORDS>
 __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned long long* x, int ks, int F_in, int B,
                                                 int N_ss, int g_begin, int ng, bool sys = true, int backoff = 0,
                                                 const unsigned long long* x2 = nullptr, int ks2 = 0,
-                                                float* sq = nullptr, const __half* gamma = nullptr) {
+                                                float* sq = nullptr, const __half* gamma = nullptr,
+                                                const float* xs = nullptr) {
     constexpr int E = Entry<D>::value;
     float sqa[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) sqa[b] = 0.f;
-    constexpr int NX = MODE == XM_SILU ? 2 : 1;     // words per element
+    constexpr int NX = (MODE == XM_SILU || MODE == XM_GAMMA2) ? 2 : 1;     // words per element
     const int tid = threadIdx.x;
     const int n_ent = ng * 32 * NB;
-    constexpr int XPT = MODE == XM_SILU ? 1 : 2;
+    constexpr int XPT = NX == 2 ? 1 : 2;
     for (int t0 = tid; t0 < n_ent; t0 += NW * 32 * XPT) {
         unsigned long long v[XPT][NX][D];
         bool need[XPT];
@@ -712,16 +747,27 @@ __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned lon
                     uint32_t h;
                     if (MODE == XM_WORDS) {
                         h = __half_as_ushort(__double2half((double)val * kAccInv));
-                    } else if (MODE == XM_GAMMA) {
-                        const float f = (float)((double)val * kAccInv);
+                    } else if (MODE == XM_GAMMA || MODE == XM_GAMMA2) {
+                        long long vs = val;
+                        if (MODE == XM_GAMMA2)
+                            vs += (long long)(v[u][NX - 1][e] & kCntMask) - (long long)ks2 * kCntBias;
+                        const float f = (float)((double)vs * kAccInv);
 #pragma unroll
                         for (int bb = 0; bb < NB; ++bb)
                             if (bb == b) sqa[bb] += f * f;
                         h = __half_as_ushort(__float2half_rn(f * __half2float(gamma[(size_t)ss * D + e])));
                     } else {
                         const long long val2 = (long long)(v[u][NX - 1][e] & kCntMask) - (long long)ks2 * kCntBias;
-                        const float g = (float)((double)val * kAccInv);
-                        const float uu = (float)((double)val2 * kAccInv);
+                        float g = (float)((double)val * kAccInv);
+                        float uu = (float)((double)val2 * kAccInv);
+                        if (xs) {
+                            float sb = xs[0];
+#pragma unroll
+                            for (int bb = 1; bb < NB; ++bb)
+                                if (bb == b) sb = xs[bb];
+                            g *= sb;
+                            uu *= sb;
+                        }
                         h = __half_as_ushort(__float2half_rn(g / (1.0f + expf(-g)) * uu));
                     }
                     w[e >> 1] |= h << (16 * (e & 1));
@@ -736,7 +782,7 @@ __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned lon
             for (int q = 0; q < E / 4; ++q) dst[q] = w[q];
         }
     }
-    if (MODE == XM_GAMMA && sq) {
+    if ((MODE == XM_GAMMA || MODE == XM_GAMMA2) && sq) {
         const int lane = tid & 31;
 #pragma unroll
         for (int b = 0; b < NB; ++b) {

@@ -347,8 +347,7 @@ fasq_status fasq_llama_create(const fasq_llama_desc* d, void* stream, fasq_llama
         o.layers = {D.o[l]};
         o.in_mode = IN_ATTN;
         o.src_step = s_at;
-        o.res_step = h_step;
-        o.res_here = D.rank == 0;
+        o.lazy_step = h_step;   // h' = o + h, materialised by its consumers (chain_internal.cuh)
         o.out_all = W > 1;
         o.kshard = W > 1;
         const int s_o = (int)steps.size();
@@ -359,6 +358,9 @@ fasq_status fasq_llama_create(const fasq_llama_desc* d, void* stream, fasq_llama
         gu.in_mode = IN_RMSNORM;
         gu.src_step = s_o;
         gu.gamma = static_cast<const __half*>(D.mlp_norm[l]);
+        // the scale of gate/up is applied by down's SwiGLU staging (measured: 1.440 ms/token vs 1.471
+        // with scale_epilogue = true, where the slot round trip sits in the gate/up epilogue)
+        gu.scale_epilogue = false;
         gu.eps = D.rms_eps;
         const int s_gu = (int)steps.size();
         steps.push_back(gu);
