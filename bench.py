@@ -224,6 +224,33 @@ def llama_kernel_ms(model, reps, world):
     return ch, lm
 
 
+def llama_split(model, ms_step, n_layers=32):
+    """Per-component time split of one decode token: one traced chain run
+    (%globaltimer stamps per step and CTA, fasq_chain_trace); a step's span is
+    last output of the previous step -> last output of this step.  Sums over
+    the 32 blocks per step kind; lm_head = step time - traced chain span."""
+    import numpy as np
+    import torch
+    T = 1 + 5 * n_layers
+    buf = torch.zeros((T, model.chain.ctas, 4), dtype=torch.int64, device="cuda")
+    model.chain.trace(buf)
+    model.step()
+    torch.cuda.synchronize()
+    model.chain.trace(None)
+    t = buf.cpu().numpy().astype(np.int64)
+    t0 = t[:, :, 0][t[:, :, 0] > 0].min()
+    ends = np.array([t[s][t[s, :, 3] > 0, 3].max() for s in range(T)]) - t0
+    spans = np.diff(np.concatenate([[0], ends])) / 1e3
+    kinds = ["qkv (RMSNorm + PQ q/k/v)", "attention (RoPE + KV + softmax)", "o_proj (PQ, attention merge)",
+             "gate/up (RMSNorm + PQ)", "down (SwiGLU + PQ + residual)"]
+    out = {"embedding": round(float(spans[0]), 2)}
+    for k, name in enumerate(kinds):
+        out[name] = round(float(spans[1 + k::5].sum()), 1)
+    out["lm_head + argmax (+ launch gap)"] = round(ms_step * 1e3 - float(ends[-1]) / 1e3, 1)
+    out["unit"] = "us per token"
+    return out
+
+
 def llama_e2e(model, steps, warmup, rank, world):
     """End to end through the public C-ABI calls with HOST buffers: every step
     copies the B tokens to decode from pinned host memory (fasq_llama_reset,
@@ -931,6 +958,10 @@ def main():
     # ---- e2e through the public API with host buffers ----
     ms_e2e = llama_e2e(model, args.steps, args.warmup, rank, world)
 
+    if world > 1:   # every rank runs the traced step (the chains wait on each other)
+        torch.cuda.synchronize()
+        dist.barrier()
+    split = llama_split(model, ms)
     tok_s = B * 1000.0 / ms
     achieved = by["chain"] / (ch_ms * 1e-3) / 1e9
     lm_gbs = by["lm_head"] / (lm_ms * 1e-3) / 1e9
@@ -989,6 +1020,7 @@ def main():
                                      "GBps": lm_gbs, "frac": lm_gbs / peak,
                                      "traffic": _ncu_traffic("k_lm_head")},
                          "step_frac": by["step"] / (ms * 1e-3) / 1e9 / peak},
+            "component_split": split,
             "clocks": clocks,
             "cpu_baseline": cpu,
             "side": side,

@@ -31,7 +31,8 @@
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls that
  *     take a stream are stream-ordered and asynchronous unless documented.
  *   - Layers are immutable after creation and may be shared across streams
- *     and host threads.
+ *     and host threads: split-K workspaces are per call (allocated in stream
+ *     order from the library allocator, fasq_set_allocator), never per layer.
  *   - No exception crosses the ABI.  Argument errors are returned
  *     synchronously before anything is enqueued.  CUDA launch/allocation
  *     failures return FASQ_E_CUDA / FASQ_E_OOM; asynchronous device faults
@@ -51,7 +52,7 @@
 extern "C" {
 #endif
 
-#define FASQ_ABI_VERSION 2
+#define FASQ_ABI_VERSION 3
 
 typedef enum {
     FASQ_OK = 0,
@@ -379,6 +380,25 @@ int32_t fasq_last_launch_count(void);
 const char* fasq_status_string(fasq_status status);
 const char* fasq_last_error_message(void);
 int32_t fasq_abi_version(void);
+
+/* ---- device memory (north_star: "PyTorch is used only for device memory") ---- */
+
+/* Caller allocator: alloc(ctx, bytes, stream) returns a device pointer on the
+ * current device, 256-B aligned, usable in stream order on `stream` (a
+ * cudaStream_t; NULL = legacy default stream), or NULL on failure;
+ * free(ctx, ptr, stream) releases it in stream order.  Both are called from
+ * the calling host thread of the library call that needs the memory. */
+typedef void* (*fasq_alloc_fn)(void* ctx, size_t bytes, void* stream);
+typedef void (*fasq_free_fn)(void* ctx, void* ptr, void* stream);
+/* Routes every device buffer the library owns -- layer storage, chain arenas
+ * and plans, KV caches, per-call split-K workspaces, pack scratch -- through
+ * alloc/free from now on (a pointer is always released by the allocator that
+ * produced it).  alloc = free = NULL restores the default (CUDA's
+ * stream-ordered allocator, cudaMallocAsync / cudaFreeAsync).  Exception: the
+ * arena of a tensor-parallel chain (world > 1) is always a cudaMalloc
+ * allocation (CUDA IPC exports whole allocations).
+ * FASQ_E_ARG if exactly one of alloc / free is NULL. */
+fasq_status fasq_set_allocator(fasq_alloc_fn alloc, fasq_free_fn free, void* ctx);
 
 #ifdef __cplusplus
 }

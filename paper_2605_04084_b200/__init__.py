@@ -41,7 +41,7 @@ EXPORTED = ["fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_
             "fasq_llama_kv_cache", "fasq_llama_reset", "fasq_llama_step", "fasq_llama_step_ex", "fasq_llama_tokens",
             "fasq_llama_step_host", "fasq_llama_logits", "fasq_llama_token_history", "fasq_llama_free",
             "fasq_last_launch_count", "fasq_status_string", "fasq_last_error_message",
-            "fasq_abi_version"]
+            "fasq_abi_version", "fasq_set_allocator"]
 
 
 class FasqError(RuntimeError):
@@ -143,6 +143,8 @@ def _load():
     L.fasq_llama_free.argtypes = [vp]
     L.fasq_llama_free.restype = None
     L.fasq_gemm.argtypes = [vp, vp, i64, vp, i32, i32, vp]
+    L.fasq_set_allocator.argtypes = [vp, vp, vp]
+    L.fasq_set_allocator.restype = ctypes.c_int32
     L.fasq_status_string.restype = ctypes.c_char_p
     L.fasq_last_error_message.restype = ctypes.c_char_p
     for name in ("fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
@@ -457,6 +459,38 @@ def gemm(layer: Layer, X: torch.Tensor, out: torch.Tensor | None = None,
     yt = FASQ_F32 if out.dtype == torch.float32 else FASQ_F16
     _check(lib.fasq_gemm(layer.handle, X.data_ptr(), M, out.data_ptr(), yt, algo, _stream(stream)))
     return out
+
+
+# ---- device memory through torch (fasq_set_allocator) -------------------------
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+
+def _torch_alloc(ctx, nbytes, stream):
+    try:
+        return torch.cuda.caching_allocator_alloc(int(nbytes), torch.cuda.current_device(), stream or 0)
+    except Exception:   # OOM etc.: the library reports FASQ_E_OOM
+        return None
+
+
+def _torch_free(ctx, ptr, stream):
+    torch.cuda.caching_allocator_delete(ptr)
+
+
+_TORCH_HOOKS = (_ALLOC_FN(_torch_alloc), _FREE_FN(_torch_free))   # kept alive for the process
+
+
+def use_torch_allocator(on: bool = True):
+    """Route every device buffer libfasq owns (layers, chains, KV caches, per-
+    call split-K workspaces, pack scratch) through torch's caching allocator
+    (north_star: PyTorch for device memory), or back to CUDA's stream-ordered
+    allocator with on=False.  Tensor-parallel chain arenas stay cudaMalloc
+    allocations (CUDA IPC)."""
+    if on:
+        _check(lib.fasq_set_allocator(ctypes.cast(_TORCH_HOOKS[0], ctypes.c_void_p),
+                                      ctypes.cast(_TORCH_HOOKS[1], ctypes.c_void_p), None))
+    else:
+        _check(lib.fasq_set_allocator(None, None, None))
 
 
 def plan_ks(shapes, nctas: int = 148, d: int = 2, B: int = 1):

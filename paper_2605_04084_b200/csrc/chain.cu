@@ -127,10 +127,13 @@ __global__ void k_attn_convert(const unsigned long long* __restrict__ arenas, lo
 void destroy_chain(fasq_chain* c) {
     if (!c) return;
     for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
-    if (c->arenas) cudaFree(c->arenas);
-    if (c->peers_dev) cudaFree(c->peers_dev);
-    if (c->items) cudaFree(c->items);
-    if (c->phases) cudaFree(c->phases);
+    if (c->arenas) {
+        if (c->arena_ipc) cudaFree(c->arenas);
+        else dev_free(c->arenas, 0);
+    }
+    dev_free(c->peers_dev, 0);
+    dev_free(c->items, 0);
+    dev_free(c->phases, 0);
     delete c;
 }
 
@@ -509,12 +512,18 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
             }
     }
     const size_t bytes = ((size_t)words * 2 + kTailWords) * 8;
-    if (cudaMalloc(&c->arenas, bytes) != cudaSuccess || cudaMalloc(&c->peers_dev, 8 * sizeof(void*)) != cudaSuccess ||
-        cudaMalloc(&c->items, items.size() * sizeof(ChainItem)) != cudaSuccess ||
-        cudaMalloc(&c->phases, phases.size() * sizeof(ChainPhase)) != cudaSuccess) {
-        cudaGetLastError();
+    // the arena of a tensor-parallel chain is exported with CUDA IPC: a whole
+    // cudaMalloc allocation; everything else through the library allocator
+    c->arena_ipc = world > 1;
+    if (c->arena_ipc) {
+        if (cudaMalloc(&c->arenas, bytes) != cudaSuccess) { cudaGetLastError(); return fail(FASQ_E_OOM, ""); }
+    } else if (dev_alloc_t(&c->arenas, bytes, st) != FASQ_OK) {
         return fail(FASQ_E_OOM, "");
     }
+    if (dev_alloc_t(&c->peers_dev, 8 * sizeof(void*), st) != FASQ_OK ||
+        dev_alloc(&c->items, items.size() * sizeof(ChainItem), st) != FASQ_OK ||
+        dev_alloc(&c->phases, phases.size() * sizeof(ChainPhase), st) != FASQ_OK)
+        return fail(FASQ_E_OOM, "");
     cudaError_t e = cudaMemcpyAsync(c->items, items.data(), items.size() * sizeof(ChainItem), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(c->phases, phases.data(), phases.size() * sizeof(ChainPhase), cudaMemcpyHostToDevice, st);
@@ -688,8 +697,8 @@ fasq_status fasq_chain_run_host(fasq_chain* c, const void* x_host, void* y_host,
     const size_t xb = (size_t)c->B * c->ext_F_in * 2;
     const size_t yb = (size_t)c->B * c->acc_ld[step][layer] * (dtype == FASQ_F32 ? 4 : 2);
     void *xd = nullptr, *yd = nullptr;
-    if (cudaMallocAsync(&xd, xb, st) != cudaSuccess || cudaMallocAsync(&yd, yb, st) != cudaSuccess) {
-        cudaGetLastError();
+    if (dev_alloc(&xd, xb, st) != FASQ_OK || dev_alloc(&yd, yb, st) != FASQ_OK) {
+        dev_free(xd, st);
         return FASQ_E_OOM;
     }
     fasq_status s = FASQ_OK;
@@ -701,8 +710,8 @@ fasq_status fasq_chain_run_host(fasq_chain* c, const void* x_host, void* y_host,
         e = cudaMemcpyAsync(y_host, yd, yb, cudaMemcpyDeviceToHost, st);
         if (e != cudaSuccess) s = cuda_fail(e, "D2H y");
     }
-    cudaFreeAsync(xd, st);
-    cudaFreeAsync(yd, st);
+    dev_free(xd, st);
+    dev_free(yd, st);
     e = cudaStreamSynchronize(st);
     if (s == FASQ_OK && e != cudaSuccess) s = cuda_fail(e, "chain_run_host sync");
     if (s == FASQ_OK) set_launch_count(2);

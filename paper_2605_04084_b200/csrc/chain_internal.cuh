@@ -124,6 +124,7 @@ struct fasq_chain {
     std::vector<int> attn_hd, attn_heads;        // per ATTN step: head dim, local heads (output layout)
     int ext_F_in = 0;
     unsigned long long* arenas = nullptr;        // [2][arena_words] + tail (ONE allocation, IPC-exportable)
+    bool arena_ipc = false;                      // cudaMalloc'ed (world > 1) rather than from the library allocator
     int64_t arena_words = 0;
     unsigned long long** peers_dev = nullptr;    // device [world]: every rank's `arenas`
     std::vector<void*> ipc_opened;

@@ -34,14 +34,10 @@ static fasq_status check_device() {
 
 static void destroy(fasq_layer* L) {
     if (!L) return;
-    if (L->idx) cudaFree(L->idx);
-    if (L->cbimg) cudaFree(L->cbimg);
-    if (L->cbmap) cudaFree(L->cbmap);
-    if (L->cb) cudaFree(L->cb);
-    if (L->ws) cudaFree(L->ws);
-    if (L->tickets) cudaFree(L->tickets);
-    if (L->gws) cudaFree(L->gws);
-    if (L->gtickets) cudaFree(L->gtickets);
+    dev_free(L->idx, 0);
+    dev_free(L->cbimg, 0);
+    dev_free(L->cbmap, 0);
+    dev_free(L->cb, 0);
     delete L;
 }
 
@@ -80,7 +76,7 @@ fasq_status fasq_import(const void* codebooks_dev, const void* indices_dev, int6
     fasq_layer* L = new fasq_layer();
     fasq_status s = init_layer_shape(L, F_out, F_in, d, C, group);
     if (s == FASQ_OK) s = check_device();
-    if (s == FASQ_OK) s = alloc_layer_storage(L);
+    if (s == FASQ_OK) s = alloc_layer_storage(L, (cudaStream_t)stream);
     if (s == FASQ_OK)
         s = build_physical_from_logical(L, static_cast<const __half*>(codebooks_dev),
                                         static_cast<const uint8_t*>(indices_dev), (cudaStream_t)stream);
@@ -101,16 +97,13 @@ fasq_status fasq_pack(const void* W_dev, int64_t F_out, int64_t F_in, const fasq
     if (s == FASQ_OK && (int64_t)prm->C > (int64_t)prm->group * F_out) s = FASQ_E_CLUSTER_OVERFLOW;
     if (s == FASQ_OK && (int64_t)prm->group * F_out > (1ll << 23)) s = FASQ_E_UNSUPPORTED;
     if (s == FASQ_OK) s = check_device();
-    if (s == FASQ_OK) s = alloc_layer_storage(L);
-    uint8_t* idx_log = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
-    if (s == FASQ_OK) {
-        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&idx_log), (size_t)L->N_ss * L->F_out, st);
-        if (e != cudaSuccess) { cudaGetLastError(); s = FASQ_E_OOM; }
-    }
+    if (s == FASQ_OK) s = alloc_layer_storage(L, st);
+    uint8_t* idx_log = nullptr;
+    if (s == FASQ_OK) s = dev_alloc_t(&idx_log, (size_t)L->N_ss * L->F_out, st);
     if (s == FASQ_OK) s = pack_run(static_cast<const __half*>(W_dev), L, prm, st, L->cb, idx_log);
     if (s == FASQ_OK) s = build_physical_from_logical(L, L->cb, idx_log, st);
-    if (idx_log) cudaFreeAsync(idx_log, st);
+    dev_free(idx_log, st);
     if (s != FASQ_OK) { cudaStreamSynchronize(st); destroy(L); return s; }
     *out = L;
     return FASQ_OK;
@@ -136,11 +129,8 @@ fasq_status fasq_shard_rows(const fasq_layer* L, int32_t rank, int32_t world, vo
     uint8_t* full = nullptr;
     uint8_t* part = nullptr;
     fasq_status s = FASQ_OK;
-    if (cudaMallocAsync(reinterpret_cast<void**>(&full), (size_t)L->N_ss * L->F_out, st) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&part), (size_t)L->N_ss * rows, st) != cudaSuccess) {
-        cudaGetLastError();
-        s = FASQ_E_OOM;
-    }
+    s = dev_alloc_t(&full, (size_t)L->N_ss * L->F_out, st);
+    if (s == FASQ_OK) s = dev_alloc_t(&part, (size_t)L->N_ss * rows, st);
     if (s == FASQ_OK) s = export_logical(L, nullptr, full, st);
     if (s == FASQ_OK) {
         cudaError_t e = cudaMemcpy2DAsync(part, (size_t)rows, full + row0, (size_t)L->F_out, (size_t)rows,
@@ -151,12 +141,12 @@ fasq_status fasq_shard_rows(const fasq_layer* L, int32_t rank, int32_t world, vo
     if (s == FASQ_OK) {
         S = new fasq_layer();
         s = init_layer_shape(S, rows, L->F_in, L->d, L->C, L->group);
-        if (s == FASQ_OK) s = alloc_layer_storage(S);
+        if (s == FASQ_OK) s = alloc_layer_storage(S, st);
         if (s == FASQ_OK) s = build_physical_from_logical(S, L->cb, part, st);
         if (s == FASQ_OK) S->row_offset = L->row_offset + (int32_t)row0;
     }
-    if (full) cudaFreeAsync(full, st);
-    if (part) cudaFreeAsync(part, st);
+    dev_free(full, st);
+    dev_free(part, st);
     if (s != FASQ_OK) { cudaStreamSynchronize(st); destroy(S); return s; }
     *out = S;
     return FASQ_OK;
@@ -239,8 +229,8 @@ fasq_status fasq_gemv_host(const fasq_layer* L, const void* x_host, int32_t B, v
     cudaStream_t st = (cudaStream_t)stream;
     const size_t xb = (size_t)B * L->F_in * 2, yb = (size_t)B * L->F_out * (yt == FASQ_F32 ? 4 : 2);
     void *xd = nullptr, *yd = nullptr;
-    if (cudaMallocAsync(&xd, xb, st) != cudaSuccess || cudaMallocAsync(&yd, yb, st) != cudaSuccess) {
-        cudaGetLastError();
+    if (dev_alloc(&xd, xb, st) != FASQ_OK || dev_alloc(&yd, yb, st) != FASQ_OK) {
+        dev_free(xd, st);
         return FASQ_E_OOM;
     }
     fasq_status s = FASQ_OK;
@@ -255,8 +245,8 @@ fasq_status fasq_gemv_host(const fasq_layer* L, const void* x_host, int32_t B, v
         e = cudaMemcpyAsync(y_host, yd, yb, cudaMemcpyDeviceToHost, st);
         if (e != cudaSuccess) s = cuda_fail(e, "D2H y");
     }
-    cudaFreeAsync(xd, st);
-    cudaFreeAsync(yd, st);
+    dev_free(xd, st);
+    dev_free(yd, st);
     e = cudaStreamSynchronize(st);
     if (s == FASQ_OK && e != cudaSuccess) s = cuda_fail(e, "gemv_host sync");
     if (s == FASQ_OK) set_launch_count(launches);

@@ -55,17 +55,6 @@ struct fasq_layer {
                                // codebook PAIR [C][g, g+1][32 words] (256-B k-rows, gemv_core.cuh)
     __half* cb = nullptr;      // logical codebooks
     int64_t idx_bytes = 0, cbimg_bytes = 0, cb_bytes = 0;
-    // GEMV split-K workspace (partials + per-row-tile arrival tickets), grown
-    // lazily outside stream capture; see gemv.cu.
-    float* ws = nullptr;
-    int64_t ws_bytes = 0;
-    unsigned* tickets = nullptr;
-    int32_t n_tickets = 0;
-    // GEMM-EXPAND split-K workspace (small M; gemm_tc.cu), same rules
-    float* gws = nullptr;
-    int64_t gws_bytes = 0;
-    unsigned* gtickets = nullptr;
-    int32_t n_gtickets = 0;
 };
 
 namespace fasq {
@@ -108,12 +97,22 @@ constexpr int kPairSlots = 2;
 constexpr uint32_t kPairSlot = 65536;
 
 // ---- layout kernels (layout.cu) ---------------------------------------------
-fasq_status alloc_layer_storage(fasq_layer* L);   // idx, cbimg, cb and (d <= 2) cbmap
+fasq_status alloc_layer_storage(fasq_layer* L, cudaStream_t st);   // idx, cbimg, cb and (d <= 2) cbmap
 fasq_status build_physical_from_logical(fasq_layer* L, const __half* cb_logical,
                                         const uint8_t* idx_logical, cudaStream_t st);
 fasq_status build_cbimg(fasq_layer* L, cudaStream_t st);
 fasq_status export_logical(const fasq_layer* L, __half* cb_out, uint8_t* idx_out, cudaStream_t st);
 fasq_status copy_rows(const fasq_layer* src, fasq_layer* dst, int32_t row0, cudaStream_t st);
+// Device memory through the library allocator (alloc.cu, fasq_set_allocator).
+fasq_status dev_alloc(void** p, size_t bytes, cudaStream_t st);
+void dev_free(void* p, cudaStream_t st);
+template <class T>
+inline fasq_status dev_alloc_t(T** p, size_t bytes, cudaStream_t st) {
+    void* q = nullptr;
+    fasq_status s = dev_alloc(&q, bytes, st);
+    *p = static_cast<T*>(q);
+    return s;
+}
 fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
                              int32_t group);
 

@@ -460,51 +460,34 @@ fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void
     } else {
         launches[nl][0] = 0; launches[nl][1] = tiles_all; launches[nl][2] = pick_ks(tiles_all); ++nl;
     }
+    uint8_t* wss[2] = {nullptr, nullptr};
     for (int li = 0; li < nl; ++li) {
         const int tiles = launches[li][1], ks = launches[li][2];
         dim3 grid((unsigned)tiles, 1, 1);
         p.tile0 = launches[li][0];
         if (ks > 1) {
-            // per-layer workspace (like the GEMV's): grown outside stream capture
-            static std::mutex mu;
-            std::lock_guard<std::mutex> lk(mu);
-            fasq_layer* Lw = const_cast<fasq_layer*>(L);   // workspace only; the PQ data is immutable
-            const int64_t need = (int64_t)ks * tiles * (TC_M * TC_MT) * TC_N * (int64_t)sizeof(float);
-            if (need > Lw->gws_bytes || 2 * tiles > Lw->n_gtickets) {
-                cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-                cudaStreamIsCapturing(st, &cs);
-                if (cs != cudaStreamCaptureStatusNone) {
-                    set_error("fasq_gemm: split-K workspace must be sized by one uncaptured call with this M first");
-                    return FASQ_E_ARG;
-                }
-                FASQ_CUDA_TRY(cudaStreamSynchronize(st));
-                if (need > Lw->gws_bytes) {
-                    if (Lw->gws) cudaFree(Lw->gws);
-                    Lw->gws = nullptr;
-                    Lw->gws_bytes = 0;
-                    if (cudaMalloc(&Lw->gws, (size_t)need) != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
-                    Lw->gws_bytes = need;
-                }
-                if (2 * tiles > Lw->n_gtickets) {
-                    if (Lw->gtickets) cudaFree(Lw->gtickets);
-                    Lw->gtickets = nullptr;
-                    Lw->n_gtickets = 0;
-                    const int nt = std::max(2 * tiles, 128);   // [tiles][arrive, depart]
-                    if (cudaMalloc(&Lw->gtickets, (size_t)nt * sizeof(unsigned)) != cudaSuccess) {
-                        cudaGetLastError();
-                        return FASQ_E_OOM;
-                    }
-                    FASQ_CUDA_TRY(cudaMemset(Lw->gtickets, 0, (size_t)nt * sizeof(unsigned)));
-                    Lw->n_gtickets = nt;
-                }
-            }
-            p.ws = Lw->gws;
-            p.tickets = Lw->gtickets;
+            // PER-CALL split-K workspace (stream-ordered, library allocator; the
+            // layer stays immutable): fp32 partial tiles + [tiles][arrive, depart]
+            const size_t need = (size_t)ks * tiles * (TC_M * TC_MT) * TC_N * sizeof(float);
+            const size_t tkb = (size_t)2 * tiles * sizeof(unsigned);
+            uint8_t* ws = nullptr;
+            fasq_status s = dev_alloc_t(&ws, need + tkb, st);
+            if (s != FASQ_OK) return s;
+            cudaError_t e = cudaMemsetAsync(ws + need, 0, tkb, st);
+            if (e != cudaSuccess) { dev_free(ws, st); return cuda_fail(e, "gemm workspace tickets"); }
+            wss[li] = ws;
+            p.ws = reinterpret_cast<float*>(ws);
+            p.tickets = reinterpret_cast<unsigned*>(ws + need);
             grid.z = (unsigned)ks;
         }
         k_gemm_tc<<<grid, TC_THREADS, smem, st>>>(map, p);
-        FASQ_CUDA_TRY(cudaGetLastError());
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            for (int q = 0; q <= li; ++q) dev_free(wss[q], st);
+            return cuda_fail(e, "k_gemm_tc launch");
+        }
     }
+    for (int q = 0; q < nl; ++q) dev_free(wss[q], st);   // stream-ordered
     set_launch_count(nl);
     return FASQ_OK;
 }

@@ -493,45 +493,14 @@ static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB, bool spin
     return pl;
 }
 
-// Grows the layer's split-K workspace (outside stream capture only).
-static fasq_status ensure_workspace(fasq_layer* L, int ksplit, int row_tiles, int B, cudaStream_t st) {
-    if (ksplit <= 1) return FASQ_OK;
-    std::lock_guard<std::mutex> lk(g_mu);
-    const int64_t need = (int64_t)ksplit * B * L->F_out_pad * (int64_t)sizeof(float);
-    if (need <= L->ws_bytes && row_tiles <= L->n_tickets) return FASQ_OK;
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(st, &cs);
-    if (cs != cudaStreamCaptureStatusNone) {
-        set_error("fasq_gemv: split-K workspace must be sized by one uncaptured call with this B first");
-        return FASQ_E_ARG;
-    }
-    FASQ_CUDA_TRY(cudaStreamSynchronize(st));
-    if (L->ws) cudaFree(L->ws);
-    if (L->tickets) cudaFree(L->tickets);
-    L->ws = nullptr;
-    L->tickets = nullptr;
-    L->ws_bytes = 0;
-    L->n_tickets = 0;
-    const int64_t wsb = std::max<int64_t>(need, (int64_t)ksplit * 2 * L->F_out_pad * 4);
-    if (cudaMalloc(&L->ws, (size_t)wsb) != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
-    const int nt = std::max(row_tiles, 64);
-    if (cudaMalloc(&L->tickets, (size_t)nt * sizeof(unsigned long long)) != cudaSuccess) {
-        cudaGetLastError();
-        return FASQ_E_OOM;
-    }
-    FASQ_CUDA_TRY(cudaMemset(L->tickets, 0, (size_t)nt * sizeof(unsigned long long)));
-    L->ws_bytes = wsb;
-    L->n_tickets = nt;
-    return FASQ_OK;
-}
-
-static void fill_layer_args(GemvLayerArgs* a, const fasq_layer* L, const GemvPlan& pl, int l, int cta, void* y) {
+static void fill_layer_args(GemvLayerArgs* a, const fasq_layer* L, const GemvPlan& pl, int l, int cta, void* y,
+                            float* partial = nullptr, unsigned long long* arrive = nullptr) {
     a->idx = L->idx;
     a->cbimg = L->cbimg;
     a->cbmap = L->cbmap;
     a->y = y;
-    a->partial = L->ws;
-    a->arrive = reinterpret_cast<unsigned long long*>(L->tickets);
+    a->partial = partial;
+    a->arrive = arrive;
     a->F_out = (int)L->F_out;
     a->F_out_pad = L->F_out_pad;
     a->N_ss = L->N_ss;
@@ -573,14 +542,31 @@ fasq_status gemv_grouped_launch2(const fasq_layer* const* Ls_, int nl, const voi
     p.B = B;
     p.y_f32 = yt == FASQ_F32;
     p.gmax = pl.gmax;
+    // split-K with dense outputs: partials + per-row-tile arrival tickets in a
+    // PER-CALL workspace (stream-ordered, library allocator; graph-capturable),
+    // so layers stay immutable and may be used on several streams at once
+    size_t ws_bytes = 0, tk_bytes = 0;
+    size_t ws_off[kMaxGroup] = {}, tk_off[kMaxGroup] = {};
+    if (!o.y_acc)
+        for (int l = 0; l < nl; ++l)
+            if (pl.ksplit[l] > 1) {
+                ws_off[l] = ws_bytes;
+                ws_bytes += (size_t)pl.ksplit[l] * B * Ls_[l]->F_out_pad * sizeof(float);
+                tk_off[l] = tk_bytes;
+                tk_bytes += (size_t)pl.row_tiles[l] * sizeof(unsigned long long);
+            }
+    uint8_t* ws = nullptr;
+    if (ws_bytes) {
+        fasq_status s = dev_alloc_t(&ws, ws_bytes + tk_bytes, st);
+        if (s != FASQ_OK) return s;
+        cudaError_t e = cudaMemsetAsync(ws + ws_bytes, 0, tk_bytes, st);
+        if (e != cudaSuccess) { dev_free(ws, st); return cuda_fail(e, "gemv workspace tickets"); }
+    }
     int cta = 0;
     for (int l = 0; l < nl; ++l) {
-        fasq_layer* L = const_cast<fasq_layer*>(Ls_[l]);   // workspace only; the PQ data is immutable
-        if (!o.y_acc) {
-            fasq_status s = ensure_workspace(L, pl.ksplit[l], pl.row_tiles[l], B, st);
-            if (s != FASQ_OK) return s;
-        }
-        fill_layer_args(&p.L[l], L, pl, l, cta, ys[l]);
+        const bool sk = ws && pl.ksplit[l] > 1;
+        fill_layer_args(&p.L[l], Ls_[l], pl, l, cta, ys[l], sk ? reinterpret_cast<float*>(ws + ws_off[l]) : nullptr,
+                        sk ? reinterpret_cast<unsigned long long*>(ws + ws_bytes + tk_off[l]) : nullptr);
         cta += pl.row_tiles[l] * pl.ksplit[l];
     }
     // L2-prefetch hints for the next launch of a decode chain (same tiling family)
@@ -607,6 +593,7 @@ fasq_status gemv_grouped_launch2(const fasq_layer* const* Ls_, int nl, const voi
         case 8: s = dispatch_nb<8>(NB, p, pl, flags, st); break;
         default: s = FASQ_E_UNSUPPORTED;
     }
+    dev_free(ws, st);   // stream-ordered: released after the launch completes
     if (s == FASQ_OK) set_launch_count(1);
     return s;
 }

@@ -32,15 +32,13 @@ fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t
     return FASQ_OK;
 }
 
-fasq_status alloc_layer_storage(fasq_layer* L) {
-    cudaError_t e;
+fasq_status alloc_layer_storage(fasq_layer* L, cudaStream_t st) {
     FASQ_CUDA_TRY(cudaGetDevice(&L->device));
-    e = cudaMalloc(&L->idx, (size_t)L->idx_bytes);
-    if (e != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
-    e = cudaMalloc(&L->cbimg, (size_t)L->cbimg_bytes);
-    if (e != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
-    e = cudaMalloc(&L->cb, (size_t)L->cb_bytes);
-    if (e != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
+    // through the library allocator (alloc.cu), in stream order on the creation stream
+    fasq_status s = dev_alloc_t(&L->idx, (size_t)L->idx_bytes, st);
+    if (s == FASQ_OK) s = dev_alloc_t(&L->cbimg, (size_t)L->cbimg_bytes, st);
+    if (s == FASQ_OK) s = dev_alloc_t(&L->cb, (size_t)L->cb_bytes, st);
+    if (s != FASQ_OK) return s;
     if (L->E == 4) {
         // codebook PAIR tensor map (the map only depends on the cbimg pointer and
         // shape, so it is encoded now and stays valid for the layer's lifetime)
@@ -57,9 +55,10 @@ fasq_status alloc_layer_storage(fasq_layer* L) {
             set_error("codebook pair tensor map: encode failed");
             return FASQ_E_CUDA;
         }
-        e = cudaMalloc(&L->cbmap, sizeof(CUtensorMap));
-        if (e != cudaSuccess) { cudaGetLastError(); return FASQ_E_OOM; }
-        FASQ_CUDA_TRY(cudaMemcpy(L->cbmap, &m, sizeof(m), cudaMemcpyHostToDevice));
+        s = dev_alloc_t(&L->cbmap, sizeof(CUtensorMap), st);
+        if (s != FASQ_OK) return s;
+        FASQ_CUDA_TRY(cudaMemcpyAsync(L->cbmap, &m, sizeof(m), cudaMemcpyHostToDevice, st));
+        FASQ_CUDA_TRY(cudaStreamSynchronize(st));   // m is a host local
     }
     return FASQ_OK;
 }

@@ -203,12 +203,12 @@ __global__ void k_llama_tokens(const unsigned long long* tail, int nctas, int B,
 void destroy_model(fasq_llama* m) {
     if (!m) return;
     if (m->chain) chain_destroy(m->chain);
-    for (__half* p : m->kc) if (p) cudaFree(p);
-    for (__half* p : m->vc) if (p) cudaFree(p);
-    if (m->rope) cudaFree(m->rope);
-    if (m->tok_hist) cudaFree(m->tok_hist);
-    if (m->logits) cudaFree(m->logits);
-    if (m->tok_dev) cudaFree(m->tok_dev);
+    for (__half* p : m->kc) dev_free(p, 0);
+    for (__half* p : m->vc) dev_free(p, 0);
+    dev_free(m->rope, 0);
+    dev_free(m->tok_hist, 0);
+    dev_free(m->logits, 0);
+    dev_free(m->tok_dev, 0);
     delete m;
 }
 
@@ -285,10 +285,8 @@ fasq_status fasq_llama_create(const fasq_llama_desc* d, void* stream, fasq_llama
     m->kc.assign(D.n_layers, nullptr);
     m->vc.assign(D.n_layers, nullptr);
     for (int l = 0; l < D.n_layers; ++l) {
-        if (cudaMalloc(&m->kc[l], cache_elems * 2) != cudaSuccess || cudaMalloc(&m->vc[l], cache_elems * 2) != cudaSuccess) {
-            cudaGetLastError();
+        if (dev_alloc_t(&m->kc[l], cache_elems * 2, st) != FASQ_OK || dev_alloc_t(&m->vc[l], cache_elems * 2, st) != FASQ_OK)
             return fail(FASQ_E_OOM, "");
-        }
         if (cudaMemsetAsync(m->kc[l], 0, cache_elems * 2, st) != cudaSuccess ||
             cudaMemsetAsync(m->vc[l], 0, cache_elems * 2, st) != cudaSuccess)
             return fail(FASQ_E_CUDA, "cache memset");
@@ -301,18 +299,17 @@ fasq_status fasq_llama_create(const fasq_llama_desc* d, void* stream, fasq_llama
                 const double a = (double)p * std::pow((double)D.rope_theta, -2.0 * i / hd);
                 tab[(size_t)p * (hd / 2) + i] = make_float2((float)std::cos(a), (float)std::sin(a));
             }
-        if (cudaMalloc(&m->rope, tab.size() * sizeof(float2)) != cudaSuccess) { cudaGetLastError(); return fail(FASQ_E_OOM, ""); }
-        if (cudaMemcpy(m->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice) != cudaSuccess)
+        if (dev_alloc_t(&m->rope, tab.size() * sizeof(float2), st) != FASQ_OK) return fail(FASQ_E_OOM, "");
+        if (cudaMemcpyAsync(m->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
             return fail(FASQ_E_CUDA, "rope upload");
     }
     const int sms = D.max_ctas > 0 ? std::min(D.max_ctas, sm_count()) : sm_count();
     int parts = 1;   // split the cache length so that heads x parts fill the GPU (<= 8)
     while (parts < 8 && m->n_heads_l * parts * 2 <= sms) parts *= 2;
     if (const char* e = getenv("FASQ_ATTN_PARTS")) parts = std::max(1, std::min(8, atoi(e)));
-    if (cudaMalloc(&m->tok_hist, (size_t)D.B * D.max_T * 4) != cudaSuccess || cudaMalloc(&m->tok_dev, 64) != cudaSuccess) {
-        cudaGetLastError();
+    if (dev_alloc_t(&m->tok_hist, (size_t)D.B * D.max_T * 4, st) != FASQ_OK || dev_alloc_t(&m->tok_dev, 64, st) != FASQ_OK)
         return fail(FASQ_E_OOM, "");
-    }
     cudaMemsetAsync(m->tok_hist, 0, (size_t)D.B * D.max_T * 4, st);
     // step list: 0 = EMBED; block l: 1+5l qkv, 2+5l attn, 3+5l o(+h), 4+5l gate/up, 5+5l down(+h')
     std::vector<StepDesc> steps;
@@ -486,14 +483,12 @@ fasq_status fasq_llama_step_host(fasq_llama* m, int32_t* tokens_out_host, void* 
 fasq_status fasq_llama_logits(fasq_llama* m, int32_t enable, void** logits_dev) {
     if (!m) return FASQ_E_ARG;
     if (enable && !m->logits) {
-        if (cudaMalloc(&m->logits, (size_t)m->desc.B * m->vocab_l * 4) != cudaSuccess) {
-            cudaGetLastError();
-            return FASQ_E_OOM;
-        }
+        if (dev_alloc_t(&m->logits, (size_t)m->desc.B * m->vocab_l * 4, 0) != FASQ_OK) return FASQ_E_OOM;
+        FASQ_CUDA_TRY(cudaStreamSynchronize(0));
     }
     if (!enable && m->logits) {
         cudaDeviceSynchronize();
-        cudaFree(m->logits);
+        dev_free(m->logits, 0);
         m->logits = nullptr;
     }
     if (logits_dev) *logits_dev = m->logits;

@@ -277,12 +277,12 @@ struct Scratch {
     template <class T>
     T* get(size_t count) {
         void* p = nullptr;
-        if (cudaMallocAsync(&p, count * sizeof(T) + 16, st) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+        if (dev_alloc(&p, count * sizeof(T) + 16, st) != FASQ_OK) return nullptr;
         ptrs.push_back(p);
         return static_cast<T*>(p);
     }
     ~Scratch() {
-        for (void* p : ptrs) cudaFreeAsync(p, st);
+        for (void* p : ptrs) dev_free(p, st);
     }
 };
 

@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol(fasq):
 
 
 def test_status_strings_and_version(fasq):
-    assert fasq.lib.fasq_abi_version() == 2
+    assert fasq.lib.fasq_abi_version() == 3
     for code in (0, -1, -2, -3, -4, -5, -6, -7, -8, -9):
         s = fasq.lib.fasq_status_string(code).decode()
         assert s.startswith("FASQ_"), s
@@ -86,3 +86,11 @@ def test_llama_argument_errors(fasq):
     assert fasq.lib.fasq_llama_create(ctypes.byref(d), None, ctypes.byref(out)) == -1
     assert fasq.lib.fasq_llama_step(None, None) == -1
     assert fasq.lib.fasq_chain_check(None, None) == -1
+
+
+def test_set_allocator_argument_errors(fasq):
+    """Exactly one NULL hook is an argument error; NULL, NULL restores the default."""
+    import ctypes as C
+    fn = C.cast(fasq._TORCH_HOOKS[0], C.c_void_p)
+    assert fasq.lib.fasq_set_allocator(fn, None, None) == -1
+    assert fasq.lib.fasq_set_allocator(None, None, None) == 0
