@@ -300,6 +300,14 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
     while (c->st > 1 && ring(c->st, c->nw) > kChainSmem) --c->st;   // 16 consumer warps; shallower ring first
     if (ring(c->st, c->nw) > kChainSmem) return fail(FASQ_E_UNSUPPORTED, "SMEM plan too large");
     c->R = c->rw * c->nw;
+    // d = 2, B >= 4: the tensor-core path reads the XOR codebook images (built once per layer)
+    const bool mma = c->d == 2 && NB == 8 && !FASQ_CHAIN_NO_MMA;
+    if (mma)
+        for (const StepDesc& S : steps)
+            for (const fasq_layer* L : S.layers) {
+                fasq_status e = ensure_cbimg_x(L, st);
+                if (e != FASQ_OK) return fail(e, "XOR codebook image");
+            }
     words = (words + 1) & ~(int64_t)1;   // 16-B zeroing stores
     c->arena_words = words;
     // ---- work plan: per step a list of items, dealt to the CTAs round-robin ----
@@ -463,6 +471,7 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
                     w.idx = L->idx;
                     w.cbimg = L->cbimg;
                     w.cbmap = L->cbmap;
+                    w.cbmap_x = mma ? L->cbmap_x : nullptr;
                     w.y_off = c->acc_off[s][l];
                     w.F_out = (int)L->F_out;
                     w.ld = (int)c->acc_ld[s][l];
@@ -490,7 +499,7 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
     for (int s = 0; s < n_steps; ++s)
         for (size_t q = 0; q < per_step[s].size(); ++q)
             items[((size_t)s * c->nctas + q % c->nctas) * c->mi + q / c->nctas] = per_step[s][q];
-    const size_t xg = (pair && NB == 8) ? (size_t)32 * NB * c->d * 4 : (size_t)32 * NB * E;   // k_chain XG
+    const size_t xg = (pair && NB == 8 && !mma) ? (size_t)32 * NB * c->d * 4 : (size_t)32 * NB * E;   // k_chain XG
     auto smem_of = [&](int stg) {   // k_chain's layout: rings, x staging, mbarriers, s_sq [nw][NB], scratch
         return cbring(stg) + (size_t)stg * c->R * 32 + (size_t)c->gmax * xg + 16 * (stg + kChainCS) +
                (size_t)c->nw * NB * 4 + kChainScratch;

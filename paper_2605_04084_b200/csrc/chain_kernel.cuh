@@ -11,6 +11,10 @@
 #include "chain_internal.cuh"
 #include "gemv_core.cuh"
 
+#ifndef FASQ_CHAIN_NO_MMA
+#define FASQ_CHAIN_NO_MMA 0   // 1: batched decode on the FHFMA/FFMA2 row-set path (A/B experiments)
+#endif
+
 namespace fasq {
 namespace chainimpl {
 
@@ -29,6 +33,7 @@ struct alignas(128) ChainItem {
     const uint8_t* idx;
     const uint8_t* cbimg;
     const void* cbmap;          // d <= 2: 3-D tensor map {32 words, n_groups, C} over cbimg (pair boxes)
+    const void* cbmap_x;        // d = 2, B >= 4: the same over the XOR image cbimg_x (tensor-core path)
     int F_out_pad, C;
 };
 
@@ -451,7 +456,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     constexpr int RW = PAIR ? 64 : core::RowsPerWarp<NB>::value;
     constexpr int R = RW * NW;
     constexpr int G = NB <= 2 ? 8 : NB == 4 ? 4 : 2;   // lanes per row set (<= 32 accumulators)
-    constexpr bool XF = PAIR && NB == 8;               // x staged as fp32 (FFMA2 path, compute_group_set)
+    // d = 2, B >= 4: batched decode on the tensor cores (gemv_core.cuh compute_group_mma)
+    // (measured: B = 8 2.95 vs 3.52 ms per 32-block step; B = 4 2.48 vs 1.83 -- the FHFMA path wins there)
+    constexpr bool MMA = D == 2 && NB == 8 && !FASQ_CHAIN_NO_MMA;
+    constexpr bool XF = PAIR && NB == 8 && !MMA;       // x staged as fp32 (FFMA2 path, compute_group_set)
     constexpr int XG = XF ? 32 * NB * D * 4 : 32 * NB * E;
     constexpr int CS = kChainCS;
     constexpr int NT = NW * 32;                        // consumer threads
@@ -544,7 +552,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                             dev::mbar_arrive(cfull0 + 8 * cs);
                         } else {
                             dev::mbar_arrive_expect_tx(cfull0 + 8 * cs, 2u * cbb);
-                            dev::tma_load_3d(cb_u + (uint32_t)cs * kPairSlot, w.cbmap, 0, g, 0, cfull0 + 8 * cs);
+                            dev::tma_load_3d(cb_u + (uint32_t)cs * kPairSlot, MMA ? w.cbmap_x : w.cbmap, 0, g, 0,
+                                             cfull0 + 8 * cs);
                         }
                         ++cit;
                     }
@@ -702,52 +711,97 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
         }
         const bool active = wrow0 < w.rows_valid;
         if constexpr (PAIR) {
-            // pair stages: row-set mapping (gemv_core.cuh), 2G*NB accumulators
-            // per lane, G-lane row reduction
-            float acc[2 * G * NB];
+            if constexpr (MMA) {
+                // tensor-core path: 16 fp32 accumulators per lane (64 rows x 8 tokens per warp)
+                float acc[16];
 #pragma unroll
-            for (int q = 0; q < 2 * G * NB; ++q) acc[q] = 0.f;
-            const bool run_loop = active && !(p.dbg & 1);
-            for (int i = 0; i < ng; i += 2) {
-                dev::mbar_wait(cfull0 + 8 * cslot, cpar);
-                const uint32_t lbs = (uint32_t)cslot << 16;
+                for (int q = 0; q < 16; ++q) acc[q] = 0.f;
+                const bool run_loop = active && !(p.dbg & 1);
+                const uint32_t blk = (uint32_t)(wrow0 >> 6) * 2048u;
+                for (int i = 0; i < ng; i += 2) {
+                    dev::mbar_wait(cfull0 + 8 * cslot, cpar);
+                    const uint32_t lbs = (uint32_t)cslot << 16;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (h == 1 && i + 1 >= ng) break;
-                    dev::mbar_wait(full0 + 8 * slot, par_ring);
-                    if (run_loop)
-                        core::compute_group_set<D, NB, G>(acc, s_idx + slot * R * 32, qm, s_cb,
-                                                          lbs + ((uint32_t)h << 7), s_x + (i + h) * XG);
-                    __syncwarp();
-                    if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
-                    if (++slot == ST) { slot = 0; par_ring ^= 1u; }
+                    for (int h = 0; h < 2; ++h) {
+                        if (h == 1 && i + 1 >= ng) break;
+                        dev::mbar_wait(full0 + 8 * slot, par_ring);
+                        if (run_loop)
+                            core::compute_group_mma<NB>(acc, s_idx + slot * R * 32, blk, lane, s_cb,
+                                                        lbs + ((uint32_t)h << 7), s_x + (i + h) * XG);
+                        __syncwarp();
+                        if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+                        if (++slot == ST) { slot = 0; par_ring ^= 1u; }
+                    }
+                    if (lane == 0) dev::mbar_arrive(cempty0 + 8 * cslot);
+                    if (++cslot == CS) { cslot = 0; cpar ^= 1u; }
                 }
-                if (lane == 0) dev::mbar_arrive(cempty0 + 8 * cslot);
-                if (++cslot == CS) { cslot = 0; cpar ^= 1u; }
-            }
-            core::reduce_set<NB, G>(acc, lane);
-            if (active) {
-                if (MODEL && s_ep.epi_scale) {
+                if (active) {
                     float sc[NB];
-                    warp_norm_scale<NB>(sc, cur + s_ep.nsq_off, s_ep.nsq_n, s_ep.F_in, s_ep.eps, p.B, lane);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h)
-#pragma unroll
-                        for (int b = 0; b < NB; ++b) acc[h * NB + b] *= sc[b];
+                    const bool scl = MODEL && s_ep.epi_scale;
+                    if (scl) warp_norm_scale<NB>(sc, cur + s_ep.nsq_off, s_ep.nsq_n, s_ep.F_in, s_ep.eps, p.B, lane);
+                    const int row0_g = s_ep.row0_g, ld = s_ep.ld, F_out = s_ep.F_out, r0 = s_ep.r0;
+                    long long qv[16];
+                    const long long off = (long long)(s_run & 1u) * p.arena_words + s_ep.y_off + row0_g;
+                    core::mma_values<NB>(acc, qv, r0 + wrow0, lane, F_out, p.B, scl ? sc : nullptr,
+                                         MODEL && s_ep.add_res ? cur + s_ep.res_off + row0_g : nullptr, ld,
+                                         s_ep.res_ks, s_ep.res_sys != 0, s_tail + T_OVF,
+                                         MODEL && s_ep.res2_off >= 0 ? cur + s_ep.res2_off + row0_g : nullptr,
+                                         s_ep.res2_ks);
+                    if (s_ep.out_all) {
+                        for (int q = 0; q < p.world; ++q)
+                            core::counted_store_mma(qv, p.peers[q] + off, r0 + wrow0, lane, F_out, ld, p.B, sys_out);
+                    } else {
+                        core::counted_store_mma(qv, p.peers[p.rank] + off, r0 + wrow0, lane, F_out, ld, p.B, false);
+                    }
                 }
-                const int row0_g = s_ep.row0_g, ld = s_ep.ld, F_out = s_ep.F_out, r0 = s_ep.r0;
-                long long qv[2 * NB];
-                const long long off = (long long)(s_run & 1u) * p.arena_words + s_ep.y_off + row0_g;
-                core::set_values<NB, G>(acc, qv, r0 + wrow0, lane, F_out, p.B,
-                                        MODEL && s_ep.add_res ? cur + s_ep.res_off + row0_g : nullptr, ld,
-                                        s_ep.res_ks, s_ep.res_sys != 0, s_tail + T_OVF,
-                                        MODEL && s_ep.res2_off >= 0 ? cur + s_ep.res2_off + row0_g : nullptr,
-                                        s_ep.res2_ks);
-                if (s_ep.out_all) {
-                    for (int q = 0; q < p.world; ++q)
-                        core::counted_store_q<NB>(qv, p.peers[q] + off, r0 + wrow0, lane, F_out, ld, p.B, sys_out);
-                } else {
-                    core::counted_store_q<NB>(qv, p.peers[p.rank] + off, r0 + wrow0, lane, F_out, ld, p.B, false);
+            } else {
+                // pair stages: row-set mapping (gemv_core.cuh), 2G*NB accumulators
+                // per lane, G-lane row reduction
+                float acc[2 * G * NB];
+#pragma unroll
+                for (int q = 0; q < 2 * G * NB; ++q) acc[q] = 0.f;
+                const bool run_loop = active && !(p.dbg & 1);
+                for (int i = 0; i < ng; i += 2) {
+                    dev::mbar_wait(cfull0 + 8 * cslot, cpar);
+                    const uint32_t lbs = (uint32_t)cslot << 16;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (h == 1 && i + 1 >= ng) break;
+                        dev::mbar_wait(full0 + 8 * slot, par_ring);
+                        if (run_loop)
+                            core::compute_group_set<D, NB, G>(acc, s_idx + slot * R * 32, qm, s_cb,
+                                                              lbs + ((uint32_t)h << 7), s_x + (i + h) * XG);
+                        __syncwarp();
+                        if (lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+                        if (++slot == ST) { slot = 0; par_ring ^= 1u; }
+                    }
+                    if (lane == 0) dev::mbar_arrive(cempty0 + 8 * cslot);
+                    if (++cslot == CS) { cslot = 0; cpar ^= 1u; }
+                }
+                core::reduce_set<NB, G>(acc, lane);
+                if (active) {
+                    if (MODEL && s_ep.epi_scale) {
+                        float sc[NB];
+                        warp_norm_scale<NB>(sc, cur + s_ep.nsq_off, s_ep.nsq_n, s_ep.F_in, s_ep.eps, p.B, lane);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+#pragma unroll
+                            for (int b = 0; b < NB; ++b) acc[h * NB + b] *= sc[b];
+                    }
+                    const int row0_g = s_ep.row0_g, ld = s_ep.ld, F_out = s_ep.F_out, r0 = s_ep.r0;
+                    long long qv[2 * NB];
+                    const long long off = (long long)(s_run & 1u) * p.arena_words + s_ep.y_off + row0_g;
+                    core::set_values<NB, G>(acc, qv, r0 + wrow0, lane, F_out, p.B,
+                                            MODEL && s_ep.add_res ? cur + s_ep.res_off + row0_g : nullptr, ld,
+                                            s_ep.res_ks, s_ep.res_sys != 0, s_tail + T_OVF,
+                                            MODEL && s_ep.res2_off >= 0 ? cur + s_ep.res2_off + row0_g : nullptr,
+                                            s_ep.res2_ks);
+                    if (s_ep.out_all) {
+                        for (int q = 0; q < p.world; ++q)
+                            core::counted_store_q<NB>(qv, p.peers[q] + off, r0 + wrow0, lane, F_out, ld, p.B, sys_out);
+                    } else {
+                        core::counted_store_q<NB>(qv, p.peers[p.rank] + off, r0 + wrow0, lane, F_out, ld, p.B, false);
+                    }
                 }
             }
         } else {

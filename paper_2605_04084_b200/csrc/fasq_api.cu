@@ -38,6 +38,8 @@ static void destroy(fasq_layer* L) {
     dev_free(L->cbimg, 0);
     dev_free(L->cbmap, 0);
     dev_free(L->cb, 0);
+    dev_free(L->cbimg_x, 0);
+    dev_free(L->cbmap_x, 0);
     delete L;
 }
 

@@ -55,6 +55,12 @@ struct fasq_layer {
                                // codebook PAIR [C][g, g+1][32 words] (256-B k-rows, gemv_core.cuh)
     __half* cb = nullptr;      // logical codebooks
     int64_t idx_bytes = 0, cbimg_bytes = 0, cb_bytes = 0;
+    // d = 2, batched decode on the tensor cores (gemv_core.cuh compute_group_mma):
+    // the codebook image with word s of k-row k at position s ^ ((k & 7) << 2)
+    // (8 lanes that gather one subspace's codebook spread over 8 banks), and its
+    // pair tensor map.  Derived from cbimg on first use (ensure_cbimg_x).
+    uint8_t* cbimg_x = nullptr;
+    void* cbmap_x = nullptr;
 };
 
 namespace fasq {
@@ -97,7 +103,8 @@ constexpr int kPairSlots = 2;
 constexpr uint32_t kPairSlot = 65536;
 
 // ---- layout kernels (layout.cu) ---------------------------------------------
-fasq_status alloc_layer_storage(fasq_layer* L, cudaStream_t st);   // idx, cbimg, cb and (d <= 2) cbmap
+fasq_status alloc_layer_storage(fasq_layer* L, cudaStream_t st);
+fasq_status ensure_cbimg_x(const fasq_layer* L, cudaStream_t st);   // d = 2 only; synchronises st   // idx, cbimg, cb and (d <= 2) cbmap
 fasq_status build_physical_from_logical(fasq_layer* L, const __half* cb_logical,
                                         const uint8_t* idx_logical, cudaStream_t st);
 fasq_status build_cbimg(fasq_layer* L, cudaStream_t st);

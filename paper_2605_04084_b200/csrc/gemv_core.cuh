@@ -656,6 +656,146 @@ __device__ __forceinline__ void counted_store_q(const long long (&q)[2 * NB], un
     }
 }
 
+// ---- batched decode on the tensor cores (d = 2, B = 4..8) --
+// mma.sync.m16n8k16 (fp16 x fp16 -> fp32) with the WEIGHTS as A and the NB <= 8
+// tokens as B (N = 8; tokens >= B are zero): a k16 slice is 8 subspaces, and
+// A's register a_i of lane (g, t) is exactly one centroid (d = 2 halves):
+// rows {g, g+8} x k-slots {t, t+4}.  Lane (g, t) owns the 8 consecutive rows
+// 8g..8g+7 of the warp's 64 (MMA tile j: row g -> 8g+2j, row g+8 -> 8g+2j+1),
+// so its indices of one subspace are ONE LDS.64 of the physical layout (2
+// wavefronts per warp, the minimum for 256 B).  The 8 lanes of a k-slot share
+// one subspace's codebook; on the XOR image (word s of k-row k at s ^ ((k&7)<<2),
+// fasq_layer::cbimg_x) they spread over 8 banks and the 4 k-slots never
+// collide, so a warp-gather costs ~2.6 wavefronts for random indices.  Per
+// index: PRMT + SHF + LOP3 + LDS + 1/4 HMMA-equivalent (the FHFMA/FFMA2 path
+// needs 4 + B instructions) -- B-independent.  x is staged [group][32
+// subspaces][NB] fp16x2 words: B's registers are x_s[token g] (conflict-free).
+// The fp16 products are exact and accumulate in fp32 inside the MMA.
+__device__ __forceinline__ uint32_t gather_x(const uint8_t* cbs, uint32_t w, uint32_t lc, int byte) {
+    uint32_t ad = dev::prmt(w, lc, 0x7604u | ((uint32_t)byte << 4));   // (k << 8) | lane constant (slot, h, 4s)
+    ad ^= (ad >> 4) & 0x70u;                                             // XOR image: s ^ ((k & 7) << 2)
+    return lds<uint32_t>(cbs + ad);
+}
+
+__device__ __forceinline__ void mma_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// One group (32 subspaces = 4 k-steps) of the warp's 64 rows on a codebook
+// pair slot (XOR image): acc[4j + c] = C[tile j] (c: rows 8g+2j / 8g+2j+1 x
+// tokens 2t / 2t+1, see mma_values).  blk = the warp's 64-row block offset in
+// the index stage; lbs = slot and half bits of the pair address.
+template <int NB>
+__device__ __forceinline__ void compute_group_mma(float (&acc)[16], const uint8_t* idx_stage, uint32_t blk, int lane,
+                                                  const uint8_t* cbs, uint32_t lbs, const uint8_t* x_grp) {
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int kst = 0; kst < 4; ++kst) {
+        const uint32_t s0 = (uint32_t)(kst * 8 + t), s1 = s0 + 4u;
+        const uint2 i0 = lds<uint2>(idx_stage + blk + s0 * 64u + 16u * ((((uint32_t)g >> 1) + (s0 >> 1)) & 3u) +
+                                    8u * ((uint32_t)g & 1u));
+        const uint2 i1 = lds<uint2>(idx_stage + blk + s1 * 64u + 16u * ((((uint32_t)g >> 1) + (s1 >> 1)) & 3u) +
+                                    8u * ((uint32_t)g & 1u));
+        uint32_t b0 = 0u, b1 = 0u;
+        if (g < NB) {
+            b0 = lds<uint32_t>(x_grp + (s0 * NB + (uint32_t)g) * 4u);
+            b1 = lds<uint32_t>(x_grp + (s1 * NB + (uint32_t)g) * 4u);
+        }
+        const uint32_t c0 = lbs + s0 * 4u, c1 = lbs + s1 * 4u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t w0 = j < 2 ? i0.x : i0.y, w1 = j < 2 ? i1.x : i1.y;
+            const int r = (2 * j) & 3;
+            uint32_t a[4];
+            a[0] = gather_x(cbs, w0, c0, r);       // row 8g+2j,   subspace s0
+            a[1] = gather_x(cbs, w0, c0, r + 1);   // row 8g+2j+1, subspace s0
+            a[2] = gather_x(cbs, w1, c1, r);       // row 8g+2j,   subspace s1
+            a[3] = gather_x(cbs, w1, c1, r + 1);   // row 8g+2j+1, subspace s1
+            float* cj = acc + 4 * j;
+            mma_16816(*reinterpret_cast<float(*)[4]>(cj), a, b0, b1);
+        }
+    }
+}
+
+// The MMA accumulators -> fixed-point values (units 2^-32) with the optional
+// RMSNorm scale per token (sc, NB entries) and residual words (res [+ res2],
+// [B][res_ld] indexing, polled in parallel); q[4j + c] belongs to row
+// row0w + 8g + 2j + (c >> 1), token 2t + (c & 1).
+template <int NB>
+__device__ __forceinline__ void mma_values(const float (&acc)[16], long long (&q)[16], int row0w, int lane, int F_out,
+                                           int B, const float* sc, const unsigned long long* res, int res_ld,
+                                           int res_ks, bool res_sys, unsigned long long* ovf,
+                                           const unsigned long long* res2 = nullptr, int res2_ks = 0) {
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int tok = 2 * t + (i & 1);
+        float v = acc[i];
+        if (sc) {
+            float sb = sc[0];
+#pragma unroll
+            for (int b = 1; b < NB; ++b)
+                if (b == tok) sb = sc[b];
+            v *= sb;
+        }
+        q[i] = __float2ll_rn(v * kAccScale);
+    }
+    if (res) {
+        // 4 batches of 4 outputs (8 words in flight): bounded registers at the
+        // 96-register cap of the chain kernel
+#pragma unroll
+        for (int bt = 0; bt < 4; ++bt) {
+            unsigned long long w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = 0ull;
+            const unsigned long long t0 = dev::globaltimer();
+            for (bool done = false; !done;) {
+                done = true;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int k = 4 * bt + (i & 3), src = i >> 2;
+                    const int row = row0w + 8 * g + 2 * (k >> 2) + ((k >> 1) & 1), tok = 2 * t + (k & 1);
+                    const int ks = src == 0 ? res_ks : res2_ks;
+                    if (row >= F_out || tok >= B || (src == 1 && !res2)) continue;
+                    if ((w[i] >> kCntShift) == (unsigned long long)ks) continue;
+                    const unsigned long long* a = (src == 0 ? res : res2) + (size_t)tok * res_ld + row;
+                    if (res_sys) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w[i]) : "l"(a) : "memory");
+                    else asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w[i]) : "l"(a) : "memory");
+                    if ((w[i] >> kCntShift) != (unsigned long long)ks) done = false;
+                }
+                if (!done && dev::globaltimer() - t0 > 4000000000ull) __trap();
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int k = 4 * bt + (i & 3), src = i >> 2;
+                const int row = row0w + 8 * g + 2 * (k >> 2) + ((k >> 1) & 1), tok = 2 * t + (k & 1);
+                const int ks = src == 0 ? res_ks : res2_ks;
+                if (row >= F_out || tok >= B || (src == 1 && !res2)) continue;
+                q[k] += (long long)(w[i] & kCntMask) - (long long)ks * kCntBias;
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) q[i] = cnt_clamp(q[i], ovf);
+}
+
+// Counted stores of mma_values' results (word tok * ld + row).
+__device__ __forceinline__ void counted_store_mma(const long long (&q)[16], unsigned long long* y, int row0w, int lane,
+                                                  int F_out, int ld, int B, bool sys) {
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int row = row0w + 8 * g + 2 * (i >> 2) + ((i >> 1) & 1), tok = 2 * t + (i & 1);
+        if (row >= F_out || tok >= B) continue;
+        const unsigned long long add = (1ull << kCntShift) + (unsigned long long)(kCntBias + q[i]);
+        if (sys) asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" :: "l"(y + (size_t)tok * ld + row), "l"(add) : "memory");
+        else asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(y + (size_t)tok * ld + row), "l"(add) : "memory");
+    }
+}
+
 // x staging from counted accumulator words [B][F_in] produced by ks K-split
 // CTAs of the previous step: every thread polls its words until all carry
 // count == ks (one L2 round trip once they are final), then forms fp16 x.
@@ -682,7 +822,8 @@ __device__ __forceinline__ void stage_x_counted(uint8_t* s_x, const unsigned lon
     constexpr int NX = (MODE == XM_SILU || MODE == XM_GAMMA2) ? 2 : 1;     // words per element
     const int tid = threadIdx.x;
     const int n_ent = ng * 32 * NB;
-    constexpr int XPT = NX == 2 ? 1 : 2;
+    // entries per thread per pass: every pass is one poll round trip (B = 8 stages 8x the entries)
+    constexpr int XPT = NX == 2 ? (NB >= 8 ? 2 : 1) : (NB >= 8 ? 4 : 2);
     for (int t0 = tid; t0 < n_ent; t0 += NW * 32 * XPT) {
         unsigned long long v[XPT][NX][D];
         bool need[XPT];

@@ -3,6 +3,8 @@
 // Logical (ABI) layout: codebooks fp16 [N_cb][C][d], indices u8 [N_ss][F_out]
 // (Alg. 1 outputs T_cluster / T_index).  Physical layout: see
 // fasq_internal.cuh and DESIGN.md "Data layout in HBM".
+#include <mutex>
+
 #include "fasq_internal.cuh"
 
 namespace fasq {
@@ -32,6 +34,30 @@ fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t
     return FASQ_OK;
 }
 
+// Pair tensor map {32 words, n_groups, C} over a codebook image with strides
+// {C*128, 128} B: a box {32, 2, C} at group g lands in SMEM as the codebook
+// PAIR [C][g, g+1][32 words].
+static fasq_status encode_pair_map(const uint8_t* img, const fasq_layer* L, void** map_out, cudaStream_t st) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return FASQ_E_CUDA; }
+    CUtensorMap m;
+    cuuint64_t gdim[3] = {32, (cuuint64_t)L->n_groups, (cuuint64_t)L->C};
+    cuuint64_t gstr[2] = {(cuuint64_t)L->C * 128, 128};
+    cuuint32_t box[3] = {32, 2, (cuuint32_t)L->C};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint8_t*>(img), gdim, gstr, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+        set_error("codebook pair tensor map: encode failed");
+        return FASQ_E_CUDA;
+    }
+    fasq_status s = dev_alloc(map_out, sizeof(CUtensorMap), st);
+    if (s != FASQ_OK) return s;
+    FASQ_CUDA_TRY(cudaMemcpyAsync(*map_out, &m, sizeof(m), cudaMemcpyHostToDevice, st));
+    FASQ_CUDA_TRY(cudaStreamSynchronize(st));   // m is a host local
+    return FASQ_OK;
+}
+
 fasq_status alloc_layer_storage(fasq_layer* L, cudaStream_t st) {
     FASQ_CUDA_TRY(cudaGetDevice(&L->device));
     // through the library allocator (alloc.cu), in stream order on the creation stream
@@ -42,23 +68,8 @@ fasq_status alloc_layer_storage(fasq_layer* L, cudaStream_t st) {
     if (L->E == 4) {
         // codebook PAIR tensor map (the map only depends on the cbimg pointer and
         // shape, so it is encoded now and stays valid for the layer's lifetime)
-        PFN_encodeTiled enc = get_encode();
-        if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return FASQ_E_CUDA; }
-        CUtensorMap m;
-        cuuint64_t gdim[3] = {32, (cuuint64_t)L->n_groups, (cuuint64_t)L->C};
-        cuuint64_t gstr[2] = {(cuuint64_t)L->C * 128, 128};
-        cuuint32_t box[3] = {32, 2, (cuuint32_t)L->C};
-        cuuint32_t es[3] = {1, 1, 1};
-        if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, L->cbimg, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
-            set_error("codebook pair tensor map: encode failed");
-            return FASQ_E_CUDA;
-        }
-        s = dev_alloc_t(&L->cbmap, sizeof(CUtensorMap), st);
+        s = encode_pair_map(L->cbimg, L, &L->cbmap, st);
         if (s != FASQ_OK) return s;
-        FASQ_CUDA_TRY(cudaMemcpyAsync(L->cbmap, &m, sizeof(m), cudaMemcpyHostToDevice, st));
-        FASQ_CUDA_TRY(cudaStreamSynchronize(st));   // m is a host local
     }
     return FASQ_OK;
 }
@@ -122,6 +133,39 @@ __global__ void k_build_cbimg(const __half* __restrict__ cb, uint8_t* __restrict
 }
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+// cbimg_x: word s of k-row k of every group moves to position s ^ ((k & 7) << 2).
+__global__ void k_build_cbimg_x(const uint32_t* __restrict__ img, uint32_t* __restrict__ img_x, int C,
+                                int64_t total) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= total) return;
+    const int s = (int)(t % kGroupSubs);
+    const int64_t row = t / kGroupSubs;          // g * C + k
+    const int k = (int)(row % C);
+    img_x[row * kGroupSubs + (s ^ ((k & 7) << 2))] = img[t];
+}
+
+fasq_status ensure_cbimg_x(const fasq_layer* Lc, cudaStream_t st) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    fasq_layer* L = const_cast<fasq_layer*>(Lc);   // a derived cache; the PQ data stays immutable
+    if (L->cbimg_x) return FASQ_OK;
+    if (L->d != 2 || L->E != 4) return FASQ_E_UNSUPPORTED;
+    uint8_t* img = nullptr;
+    fasq_status s = dev_alloc_t(&img, (size_t)L->cbimg_bytes, st);
+    if (s != FASQ_OK) return s;
+    const int64_t total = (int64_t)L->n_groups * L->C * kGroupSubs;
+    k_build_cbimg_x<<<nblk(total, 256), 256, 0, st>>>(reinterpret_cast<const uint32_t*>(L->cbimg),
+                                                       reinterpret_cast<uint32_t*>(img), L->C, total);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { dev_free(img, st); return cuda_fail(e, "k_build_cbimg_x"); }
+    void* map = nullptr;
+    s = encode_pair_map(img, L, &map, st);
+    if (s != FASQ_OK) { dev_free(img, st); return s; }
+    L->cbimg_x = img;
+    L->cbmap_x = map;
+    return FASQ_OK;
+}
 
 fasq_status build_physical_from_logical(fasq_layer* L, const __half* cb_logical, const uint8_t* idx_logical,
                                         cudaStream_t st) {
