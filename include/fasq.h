@@ -147,9 +147,13 @@ void fasq_free(fasq_layer* layer);       /* synchronises the device; NULL is a n
 
 /* ---- products ------------------------------------------------------------ */
 
-/* Decode GEMV (Alg. 2's math): y[b] = W_hat . x[b] for B in 1..8.
+/* Decode GEMV (Alg. 2's math): y[b] = W_hat . x[b].
  * x_dev fp16 [B][F_in], y_dev [B][F_out] of y_dtype.  fp32 accumulation of
- * exact fp16 products; the split-K merge is deterministic (fixed order). */
+ * exact fp16 products; the split-K merge is deterministic (fixed order).
+ * B in 1..8 runs the decode GEMV kernels; B > 8 (the paper's future work:
+ * adaptive GEMV <-> tensor-core dispatch for B = 16..64) is the same
+ * product through fasq_gemm (AUTO), with flags == 0 only (else
+ * FASQ_E_UNSUPPORTED). */
 fasq_status fasq_gemv(const fasq_layer* layer, const void* x_dev, int32_t B, void* y_dev,
                       fasq_dtype y_dtype, void* stream);
 fasq_status fasq_gemv_ex(const fasq_layer* layer, const void* x_dev, int32_t B, void* y_dev,

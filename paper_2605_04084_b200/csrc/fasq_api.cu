@@ -184,8 +184,12 @@ void fasq_free(fasq_layer* L) {
 fasq_status fasq_gemv_ex(const fasq_layer* L, const void* x_dev, int32_t B, void* y_dev, fasq_dtype yt,
                          uint32_t flags, void* stream) {
     if (!L || !x_dev || !y_dev) return FASQ_E_ARG;
-    if (B < 1 || B > 8) return FASQ_E_UNSUPPORTED;
+    if (B < 1) return FASQ_E_ARG;
     if (yt != FASQ_F16 && yt != FASQ_F32) return FASQ_E_ARG;
+    if (B > 8) {   // batch beyond the decode kernels: the prefill GEMM path (P:410 dispatch)
+        if (flags) return FASQ_E_UNSUPPORTED;
+        return fasq_gemm(L, x_dev, B, y_dev, yt, FASQ_GEMM_AUTO, stream);
+    }
     return gemv_launch(L, static_cast<const __half*>(x_dev), B, y_dev, yt, flags, (cudaStream_t)stream);
 }
 

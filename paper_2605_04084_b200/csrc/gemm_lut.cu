@@ -14,6 +14,8 @@
 // layout into row-rotated rows (byte p of row r = subspace (p + r) & 31).  The
 // gathers are pure FADD on CUDA cores -- no tensor cores --
 // which is why the EXPAND variant exists (gemm_tc.cu).
+#include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "fasq_internal.cuh"
@@ -32,6 +34,7 @@ struct LutParams {
     const uint8_t* cbimg;     // [n_groups][C][32][E], E = 4*EW bytes (d <= 2: 4, d = 4: 8, d = 8: 16)
     const __half* X;          // [M][F_in]
     void* Y;
+    float* part;              // split-K (gridDim.z > 1): fp32 partials [z][M][F_out] (per-call workspace)
     int M, F_in, F_out, F_out_pad, n_groups, N_ss, C, d, y_f32;
 };
 
@@ -63,7 +66,10 @@ __global__ void __launch_bounds__(LUT_THREADS, 1) k_gemm_lut(LutParams p) {
 #pragma unroll
         for (int t = 0; t < LUT_MT; ++t) acc[q][t] = 0.f;
 
-    for (int g = 0; g < p.n_groups; ++g) {
+    // split-K (short L, Alg. 3's split-K): blockIdx.z owns groups [g0, g1)
+    const int g0 = (int)((long long)blockIdx.z * p.n_groups / gridDim.z);
+    const int g1 = (int)((long long)(blockIdx.z + 1) * p.n_groups / gridDim.z);
+    for (int g = g0; g < g1; ++g) {
         __syncthreads();   // previous group's gathers done
         // build: entry (t, k, sub) = sum_e x[t][sub*d+e] * c[sub][k][e]  (fp32, exact fp16 products)
         const uint32_t* cbg = reinterpret_cast<const uint32_t*>(p.cbimg + (size_t)g * C * 128 * EW);
@@ -142,10 +148,21 @@ __global__ void __launch_bounds__(LUT_THREADS, 1) k_gemm_lut(LutParams p) {
         for (int t = 0; t < LUT_MT; ++t) {
             const int m = m0 + t;
             if (m >= p.M) continue;
+            if (gridDim.z > 1) { p.part[((size_t)blockIdx.z * p.M + m) * p.F_out + row] = acc[q][t]; continue; }
             if (p.y_f32) reinterpret_cast<float*>(p.Y)[(size_t)m * p.F_out + row] = acc[q][t];
             else reinterpret_cast<__half*>(p.Y)[(size_t)m * p.F_out + row] = __float2half_rn(acc[q][t]);
         }
     }
+}
+
+// split-K merge: Y = sum over z = 0..ks-1 in fixed order (deterministic)
+__global__ void k_lut_merge(const float* __restrict__ part, int ks, int64_t n, void* Y, int y_f32) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float v = 0.f;
+    for (int z = 0; z < ks; ++z) v += __ldcs(part + (size_t)z * n + i);
+    if (y_f32) reinterpret_cast<float*>(Y)[i] = v;
+    else reinterpret_cast<__half*>(Y)[i] = __float2half_rn(v);
 }
 
 template <int EW>
@@ -180,11 +197,39 @@ fasq_status gemm_lut_launch(const fasq_layer* L, const __half* X, int64_t M, voi
     p.y_f32 = yt == FASQ_F32;
     const size_t smem = (size_t)(LUT_MT / 2) * L->C * 256 + (size_t)LUT_R * 32;
     dim3 grid((unsigned)((L->F_out_pad + LUT_R - 1) / LUT_R), (unsigned)((M + LUT_MT - 1) / LUT_MT));
+    // short L: fewer (row, token) tiles than 2 waves of SMs -> split the groups
+    // over gridDim.z (fp32 partials in a per-call workspace + a fixed-order merge)
+    int sms = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const long long tiles = (long long)grid.x * grid.y;
+    int ks = 1;
+    if (const char* e = getenv("FASQ_LUT_KSPLIT")) ks = atoi(e);
+    else if (tiles < 2ll * sms) ks = (int)std::min<long long>(L->n_groups, (2ll * sms + tiles - 1) / tiles);
+    ks = std::max(1, std::min(ks, L->n_groups));
+    float* part = nullptr;
+    const int64_t n = M * L->F_out;
+    if (ks > 1) {
+        fasq_status a = dev_alloc_t(&part, (size_t)ks * n * sizeof(float), st);
+        if (a != FASQ_OK) return a;
+        grid.z = (unsigned)ks;
+        p.part = part;
+    }
     fasq_status s = L->d <= 2 ? launch_lut<1>(p, grid, smem, st)
                   : L->d == 4 ? launch_lut<2>(p, grid, smem, st) : launch_lut<4>(p, grid, smem, st);
+    cudaError_t e = cudaGetLastError();
+    if (s == FASQ_OK && e != cudaSuccess) s = cuda_fail(e, "k_gemm_lut");
+    if (s == FASQ_OK && ks > 1) {
+        k_lut_merge<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, ks, n, Y, yt == FASQ_F32);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) s = cuda_fail(e, "k_lut_merge");
+    }
+    dev_free(part, st);
     if (s != FASQ_OK) return s;
-    FASQ_CUDA_TRY(cudaGetLastError());
-    set_launch_count(1);
+    set_launch_count(ks > 1 ? 2 : 1);
     return FASQ_OK;
 }
 

@@ -142,3 +142,45 @@ def test_gemm_lut_all_subvector_sizes(F, oracle_lib, d, C, F_out, F_in, M):
         Y = _run(F, cb, idx, X, F_in, 1, algo)
         ok, info = parity_ok(Y, ref, X, F_in)
         assert ok, (algo, info)
+
+
+@pytest.mark.parametrize("F_out,F_in,M,ks", [(4096, 4096, 8, 0), (1000, 2496, 5, 0), (512, 1024, 13, 7),
+                                             (4096, 14336, 32, 0)])
+def test_gemm_lut_split_k_short_L(F, oracle_lib, monkeypatch, F_out, F_in, M, ks):
+    """NEXT-3 (Alg. 3's split-K for short L): with fewer (row, token)
+    tiles than 2 waves the groups are split over gridDim.z (fp32 partials in a
+    per-call workspace, merged in fixed order).  ks = 0: the library's choice;
+    7: forced, uneven group ranges.  Oracle parity on sampled rows; two calls
+    are bit-identical (deterministic merge)."""
+    if ks:
+        monkeypatch.setenv("FASQ_LUT_KSPLIT", str(ks))
+    cb, idx = synth.random_layer(F_out, F_in, 2, 256, seed=F_out + M)
+    X = synth.activation(M, F_in, seed=M + 5)
+    L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), F_in, 1)
+    Xd = torch.from_numpy(X).cuda()
+    Y1 = F.gemm(L, Xd, out_dtype=torch.float32, algo=F.GEMM_LUT)
+    Y2 = F.gemm(L, Xd, out_dtype=torch.float32, algo=F.GEMM_LUT)
+    torch.cuda.synchronize()
+    assert torch.equal(Y1, Y2)
+    for j0 in (0, F_out - 64):
+        ref = oracle_lib.gemm(cb, idx[:, j0:j0 + 64], X)
+        ok, info = parity_ok(Y1[:, j0:j0 + 64].cpu().numpy().astype(np.float64), ref, X, F_in)
+        assert ok, (j0, info)
+    L.free()
+
+
+@pytest.mark.parametrize("B", [9, 16, 33, 64])
+def test_gemv_large_batch_dispatches_to_gemm(F, oracle_lib, B):
+    """NEXT-3: fasq_gemv with B > 8 runs the prefill GEMM (AUTO ->
+    EXPAND on the tensor cores for d = 2); same product, oracle parity."""
+    cb, idx = synth.random_layer(2048, 4096, 2, 256, seed=B)
+    x = synth.activation(B, 4096, seed=B + 1)
+    L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), 4096, 1)
+    y = F.gemv(L, torch.from_numpy(x).cuda(), out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    ref = oracle_lib.gemm(cb, idx[:, :256], x)
+    ok, info = parity_ok(y[:, :256].cpu().numpy().astype(np.float64), ref, x, 4096)
+    assert ok, info
+    with pytest.raises(F.FasqError):
+        F.gemv(L, torch.from_numpy(x).cuda(), out_dtype=torch.float32, flags=F.FLAG_PDL)
+    L.free()
