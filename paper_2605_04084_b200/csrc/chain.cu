@@ -278,6 +278,8 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
                 return fail(FASQ_E_UNSUPPORTED, "ATTN step: head_dim must be a multiple of 8 in 8..128");
             if (S.q_step < 0 || S.q_step >= s || steps[S.q_step].kind != SK_PQ || steps[S.q_step].layers.size() != 3)
                 return fail(FASQ_E_ARG, "ATTN step needs an earlier q/k/v step");
+            if (model->attn_parts < 1 || model->attn_parts > 4)
+                return fail(FASQ_E_UNSUPPORTED, "attention cache parts must be 1..4");
             // partials [B][heads][parts][hd + 2] (logical output width heads * hd)
             c->acc_off[s].push_back(words);
             c->acc_ld[s].push_back((int64_t)S.n_heads * S.head_dim);
@@ -561,6 +563,8 @@ fasq_status chain_launch(fasq_chain* c, const void* x_dev, cudaStream_t st) {
     p.rank = c->rank;
     p.pf = 0;
     if (const char* e = getenv("FASQ_CHAIN_PF")) p.pf = atoi(e);
+    p.attn_pf = 1;
+    if (const char* e = getenv("FASQ_ATTN_PF")) p.attn_pf = atoi(e);
     p.dbg = 0;
     if (const char* e = getenv("FASQ_CHAIN_DBG")) p.dbg = atoi(e);
     p.backoff = 0;

@@ -91,6 +91,7 @@ struct ChainParams {
     int n_steps, nctas, B, gmax, cbb_max;
     int mi;                     // work items per (step, CTA): [n_steps][nctas][mi]
     int pf;                     // producer: L2-prefetch this many groups of the next step's item
+    int attn_pf;                // producer: L2-prefetch the next attention item's cache rows (FASQ_ATTN_PF, default 1)
     int backoff;                // ns slept between input polls (FASQ_CHAIN_BACKOFF, default 0)
     int dbg;                    // experiments only (FASQ_CHAIN_DBG): bit 0 = consumers skip the gather
                                 // loop, bit 1 = producer skips the copies (compute on stale SMEM),
@@ -396,27 +397,29 @@ __device__ __forceinline__ void stage_x_attn(uint8_t* s_x, const unsigned long l
             const int col = ss * D, head = col / hd, e0 = col - head * hd;
             const unsigned long long* hb = a + ((size_t)b * heads + head) * P * (hd + 2);
             // poll only the l words (written with release after the part's o and m
-            // words, attn_item), all parts in flight; then o and m are final
-            unsigned long long lv[8];
+            // words, attn_item), all parts in flight; then o and m are final.
+            // (Polling all 16 words of an entry in one round trip was measured
+            // slower: register pressure, 1.44 -> 1.58 ms per token.)
+            unsigned long long lv[4];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) lv[q] = 0ull;
+            for (int q = 0; q < 4; ++q) lv[q] = 0ull;
             const unsigned long long t_start = dev::globaltimer();
             for (bool done = false; !done;) {
                 done = true;
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
+                for (int q = 0; q < 4; ++q)
                     if (q < P && (lv[q] >> core::kCntShift) != 1ull) {
                         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(lv[q]) : "l"(hb + (size_t)q * (hd + 2) + hd + 1) : "memory");
                         if ((lv[q] >> core::kCntShift) != 1ull) done = false;
                     }
                 if (!done && dev::globaltimer() - t_start > 4000000000ull) __trap();
             }
-            float m[8], l[8], o[8][D];   // P <= 8, fully unrolled (registers, not local memory)
+            float m[8], l[8], o[8][D];   // P <= 4, fully unrolled (registers, not local memory)
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const unsigned long long* pb = hb + (size_t)q * (hd + 2);
+                const unsigned long long* pb = hb + (size_t)(q & 3) * (hd + 2);
                 m[q] = q < P ? word_f32(ld_word(pb + hd, false)) : -INFINITY;
-                l[q] = q < P ? word_f32(lv[q]) : 0.f;
+                l[q] = q < P ? word_f32(lv[q & 3]) : 0.f;
 #pragma unroll
                 for (int e = 0; e < D; ++e) o[q][e] = q < P ? word_f32(ld_word(pb + e0 + e, false)) : 0.f;
             }
@@ -531,6 +534,24 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                     continue;
                 }
                 if (w.kind != SK_PQ || w.rows_valid <= 0) continue;
+                if (MODEL && p.attn_pf && ph + 1 < p.n_steps && phj % p.mi == 0) {
+                    // the next step is attention: warm L2 with this CTA's cache rows now, so the
+                    // pair-slot TMA (issued once a slot frees up) hits L2, not HBM
+                    const ChainItem& na = p.items[((size_t)(ph + 1) * p.nctas + blockIdx.x) * p.mi];
+                    if (na.kind == SK_ATTN) {
+                        const ChainPhase& P = p.phases[ph + 1];
+                        const AttnRows r = attn_rows(na.kidx, P.parts, pos, p.B, P.hd);
+                        if (r.smem) {
+                            const int kvh = na.head / (P.n_heads / P.n_kv);
+                            const uint32_t rb = (uint32_t)(r.te - r.t0) * P.hd * 2u;
+                            for (int b = 0; b < p.B; ++b) {
+                                const size_t src = (((size_t)b * P.n_kv + kvh) * p.max_T + r.t0) * P.hd;
+                                dev::bulk_prefetch_l2(P.kc + src, rb);
+                                dev::bulk_prefetch_l2(P.vc + src, rb);
+                            }
+                        }
+                    }
+                }
                 const uint32_t cbb = (uint32_t)w.C * 32u * E;
                 const uint32_t chunk = (uint32_t)w.rows_valid * 32u;
                 if (p.pf > 0 && ph + 1 < p.n_steps && phj % p.mi == 0) {

@@ -305,9 +305,9 @@ fasq_status fasq_llama_create(const fasq_llama_desc* d, void* stream, fasq_llama
             return fail(FASQ_E_CUDA, "rope upload");
     }
     const int sms = D.max_ctas > 0 ? std::min(D.max_ctas, sm_count()) : sm_count();
-    int parts = 1;   // split the cache length so that heads x parts fill the GPU (<= 8)
-    while (parts < 8 && m->n_heads_l * parts * 2 <= sms) parts *= 2;
-    if (const char* e = getenv("FASQ_ATTN_PARTS")) parts = std::max(1, std::min(8, atoi(e)));
+    int parts = 1;   // split the cache length so that heads x parts fill the GPU (<= 4: the o staging polls them at once)
+    while (parts < 4 && m->n_heads_l * parts * 2 <= sms) parts *= 2;
+    if (const char* e = getenv("FASQ_ATTN_PARTS")) parts = std::max(1, std::min(4, atoi(e)));
     if (dev_alloc_t(&m->tok_hist, (size_t)D.B * D.max_T * 4, st) != FASQ_OK || dev_alloc_t(&m->tok_dev, 64, st) != FASQ_OK)
         return fail(FASQ_E_OOM, "");
     cudaMemsetAsync(m->tok_hist, 0, (size_t)D.B * D.max_T * 4, st);
