@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <unordered_map>
 
 #include "fasq_internal.cuh"
 #include "gemv_core.cuh"
@@ -42,8 +43,8 @@ struct GemvLayerArgs {
     const uint8_t* cbimg;   // [n_groups][C][32][E]
     const void* cbmap;      // d <= 2: codebook PAIR tensor map (fasq_layer::cbmap)
     void* y;                // [B][F_out]
-    float* partial;         // [ksplit][B][F_out_pad] (ksplit > 1)
-    unsigned long long* arrive;   // [row_tiles] u32 monotonically increasing arrival counters (8-B slots)
+    long long* acc;         // ksplit > 1: int64 fixed-point sums [B][F_out_pad] (per-call workspace, zeroed)
+    unsigned* cnt;          // ksplit > 1: contributions per output [B][F_out_pad] (zeroed)
     int F_out, F_out_pad, N_ss, n_groups, C, ksplit, cta_begin;
 };
 
@@ -294,57 +295,60 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_gemv(GemvParams p) {
         }
         return;
     }
-    // split-K: publish partials, wait until every CTA of this row tile has
-    // published (all CTAs are co-resident: grid <= #SMs, and PDL dependents
-    // launch only after every CTA started), then each CTA sums a
-    // 1/ksplit slice of the tile's rows over ks = 0..ksplit-1 in fixed order
-    // (deterministic; the paper's merge is atomicAdd).
+    // split-K, no merge phase: every K-split CTA adds its partial, rounded once
+    // to int64 units of 2^-32 (exact scaling; integer addition is associative
+    // -> deterministic), into acc[b][row] and then counts itself in cnt[b][row]
+    // with acq_rel; the CTA that brings the count to ksplit is the last
+    // contributor of that output: its acquire sees every add, so it converts
+    // the sum and stores y.  No barrier, no second pass over partials (the
+    // dense-output merge of round 1 cost three L2 round trips per launch).
     if (active && tot.own) {
+        // 1. every add, relaxed; 2. ONE fence (orders this thread's adds before
+        // its counts); 3. relaxed counts; 4. the last contributor fences
+        // (acquire side) and converts.  Per-output acq_rel atomics serialised a
+        // full L2 round trip per output.
 #pragma unroll
         for (int h = 0; h < H; ++h) {
             const int row = r0 + wrow0 + h * 32 + tot.rsel;
+            if (row >= F_out) continue;
 #pragma unroll
-            for (int b = 0; b < NB; ++b)
-                if (b < p.B) __stcg(&la.partial[((size_t)ks * p.B + b) * F_out_pad + row], tot.v[h][b]);
-        }
-    }
-    // arrive: bar.sync orders this CTA's partial stores before thread 0's
-    // release-RMW (cumulative, no full fence).
-    asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
-    if (threadIdx.x == 0) {
-        // monotonically increasing arrival counter: this launch's CTAs of the
-        // tile take the values [n*ksplit, (n+1)*ksplit)
-        unsigned* cnt = reinterpret_cast<unsigned*>(la.arrive + rt);
-        unsigned old;
-        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
-        const unsigned target = (old / (unsigned)ksplit + 1u) * (unsigned)ksplit;
-        unsigned v;
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-        } while ((int)(v - target) < 0);
-    }
-    asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
-    // merge: this CTA owns rows [rb, re) of the tile; sum ks = 0..ksplit-1 in order
-    const int rows_per = (rows_valid + ksplit - 1) / ksplit;
-    const int rb = ks * rows_per, re = min(rows_valid, rb + rows_per);
-    const size_t kstride = (size_t)p.B * F_out_pad;
-    for (int rr = rb + (int)threadIdx.x; rr < re; rr += NW * 32) {
-        const int row = r0 + rr;
-        for (int b = 0; b < p.B; ++b) {
-            const float* src = la.partial + (size_t)b * F_out_pad + row;
-            float sum = 0.f;
-            int k = 0;
-            for (; k + 8 <= ksplit; k += 8) {
-                float v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(k + u) * kstride);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) sum += v[u];
+            for (int b = 0; b < NB; ++b) {
+                if (b >= p.B) continue;
+                const long long v = __float2ll_rn(tot.v[h][b] * kAccScale);
+                asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(la.acc + (size_t)b * F_out_pad + row), "l"(v) : "memory");
             }
-            for (; k < ksplit; ++k) sum += __ldcg(src + (size_t)k * kstride);
-            if (row < F_out) {
-                if (p.y_f32) reinterpret_cast<float*>(la.y)[(size_t)b * F_out + row] = sum;
-                else reinterpret_cast<__half*>(la.y)[(size_t)b * F_out + row] = __float2half_rn(sum);
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        unsigned last = 0u;   // bit (h * NB + b): this thread completed that output
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            const int row = r0 + wrow0 + h * 32 + tot.rsel;
+            if (row >= F_out) continue;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                if (b >= p.B) continue;
+                unsigned old;
+                asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(la.cnt + (size_t)b * F_out_pad + row) : "memory");
+                if (old == (unsigned)ksplit - 1u) last |= 1u << (h * NB + b);
+            }
+        }
+        if (last) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                const int row = r0 + wrow0 + h * 32 + tot.rsel;
+#pragma unroll
+                for (int b = 0; b < NB; ++b) {
+                    if (!(last >> (h * NB + b) & 1u)) continue;
+                    const size_t w = (size_t)b * F_out_pad + row;
+                    long long sum;
+                    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(sum) : "l"(la.acc + w) : "memory");
+                    la.acc[w] = 0ll;   // self-cleaning for the next launch on this stream
+                    la.cnt[w] = 0u;
+                    const double val = (double)sum * kAccInv;
+                    if (p.y_f32) reinterpret_cast<float*>(la.y)[(size_t)b * F_out + row] = (float)val;
+                    else reinterpret_cast<__half*>(la.y)[(size_t)b * F_out + row] = __double2half(val);
+                }
             }
         }
     }
@@ -422,9 +426,9 @@ static fasq_status dispatch_nb(int NB, const GemvParams& p, const GemvPlan& pl, 
 
 // Tiling plan: each layer's work is split into R-row tiles
 // x K-ranges of 32-subspace groups; the CTAs of all layers of a (grouped)
-// launch add up to <= #SMs so they are co-resident (the split-K merge spins on
-// its peers) and each SM runs one CTA of this launch -- the second SM slot is
-// left for the NEXT launch's prefetch under PDL.  CTAs are shared between the
+// launch add up to about #SMs, one CTA per SM -- the second SM slot is left
+// for the NEXT launch's prefetch under PDL (no CTA waits on another: split-K
+// outputs are converted by their last contributor, see the epilogue).  CTAs are shared between the
 // layers in proportion to their index bytes.  Env FASQ_GEMV_CFG="nw,stages"
 // overrides the default tiling (tuning only).
 static int gemv_rows_per_warp(int NB) { return NB == 1 ? 64 : NB == 2 ? 32 : NB == 4 ? 16 : 8; }
@@ -493,14 +497,42 @@ static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB, bool spin
     return pl;
 }
 
+// Per-stream split-K workspace (zeroed; kept zero by the kernels' last
+// contributors).  *out = NULL when the stream is capturing and the cached
+// workspace is too small (the caller falls back to a per-call workspace).
+static fasq_status stream_workspace(cudaStream_t st, size_t bytes, uint8_t** out) {
+    struct Ws { uint8_t* p = nullptr; size_t bytes = 0; };
+    static std::mutex mu;
+    static std::unordered_map<cudaStream_t, Ws> ws_of;
+    std::lock_guard<std::mutex> lk(mu);
+    Ws& w = ws_of[st];
+    *out = nullptr;
+    if (w.bytes >= bytes) { *out = w.p; return FASQ_OK; }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return FASQ_OK;
+    FASQ_CUDA_TRY(cudaStreamSynchronize(st));
+    dev_free(w.p, st);
+    w.p = nullptr;
+    w.bytes = 0;
+    const size_t nb = std::max(bytes, (size_t)1 << 20);
+    fasq_status s = dev_alloc_t(&w.p, nb, st);
+    if (s != FASQ_OK) return s;
+    FASQ_CUDA_TRY(cudaMemsetAsync(w.p, 0, nb, st));
+    FASQ_CUDA_TRY(cudaStreamSynchronize(st));
+    w.bytes = nb;
+    *out = w.p;
+    return FASQ_OK;
+}
+
 static void fill_layer_args(GemvLayerArgs* a, const fasq_layer* L, const GemvPlan& pl, int l, int cta, void* y,
-                            float* partial = nullptr, unsigned long long* arrive = nullptr) {
+                            long long* acc = nullptr, unsigned* cnt = nullptr) {
     a->idx = L->idx;
     a->cbimg = L->cbimg;
     a->cbmap = L->cbmap;
     a->y = y;
-    a->partial = partial;
-    a->arrive = arrive;
+    a->acc = acc;
+    a->cnt = cnt;
     a->F_out = (int)L->F_out;
     a->F_out_pad = L->F_out_pad;
     a->N_ss = L->N_ss;
@@ -530,7 +562,7 @@ fasq_status gemv_grouped_launch2(const fasq_layer* const* Ls_, int nl, const voi
     for (int l = 1; l < nl; ++l)
         if (Ls_[l]->F_in != Ls_[0]->F_in || Ls_[l]->d != Ls_[0]->d) return FASQ_E_SHAPE;
     const int NB = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;
-    GemvPlan pl = plan_gemv(Ls_, nl, NB, !o.y_acc);
+    GemvPlan pl = plan_gemv(Ls_, nl, NB, false);   // no output mode spins on peers any more
     GemvParams p{};
     p.x_acc = o.x_acc;
     p.y_acc = o.y_acc;
@@ -542,31 +574,40 @@ fasq_status gemv_grouped_launch2(const fasq_layer* const* Ls_, int nl, const voi
     p.B = B;
     p.y_f32 = yt == FASQ_F32;
     p.gmax = pl.gmax;
-    // split-K with dense outputs: partials + per-row-tile arrival tickets in a
-    // PER-CALL workspace (stream-ordered, library allocator; graph-capturable),
-    // so layers stay immutable and may be used on several streams at once
-    size_t ws_bytes = 0, tk_bytes = 0;
-    size_t ws_off[kMaxGroup] = {}, tk_off[kMaxGroup] = {};
+    // split-K with dense outputs: int64 sums + contribution counts per output.
+    // Workspace: the calling STREAM's (layers stay immutable; launches on one
+    // stream are ordered, and the last contributor of every output zeroes its
+    // words again -- no memset per launch); grown outside stream capture.  A
+    // first launch inside capture with too small a stream workspace gets a
+    // per-call workspace (allocation + memset nodes) instead.
+    size_t acc_bytes = 0, cnt_bytes = 0;
+    size_t acc_off[kMaxGroup] = {}, cnt_off[kMaxGroup] = {};
     if (!o.y_acc)
         for (int l = 0; l < nl; ++l)
             if (pl.ksplit[l] > 1) {
-                ws_off[l] = ws_bytes;
-                ws_bytes += (size_t)pl.ksplit[l] * B * Ls_[l]->F_out_pad * sizeof(float);
-                tk_off[l] = tk_bytes;
-                tk_bytes += (size_t)pl.row_tiles[l] * sizeof(unsigned long long);
+                acc_off[l] = acc_bytes;
+                acc_bytes += (size_t)B * Ls_[l]->F_out_pad * sizeof(long long);
+                cnt_off[l] = cnt_bytes;
+                cnt_bytes += (size_t)B * Ls_[l]->F_out_pad * sizeof(unsigned);
             }
     uint8_t* ws = nullptr;
-    if (ws_bytes) {
-        fasq_status s = dev_alloc_t(&ws, ws_bytes + tk_bytes, st);
+    uint8_t* ws_call = nullptr;   // per-call workspace (capture fallback), released after the launch
+    if (acc_bytes) {
+        fasq_status s = stream_workspace(st, acc_bytes + cnt_bytes, &ws);
         if (s != FASQ_OK) return s;
-        cudaError_t e = cudaMemsetAsync(ws + ws_bytes, 0, tk_bytes, st);
-        if (e != cudaSuccess) { dev_free(ws, st); return cuda_fail(e, "gemv workspace tickets"); }
+        if (!ws) {
+            s = dev_alloc_t(&ws_call, acc_bytes + cnt_bytes, st);
+            if (s != FASQ_OK) return s;
+            cudaError_t e = cudaMemsetAsync(ws_call, 0, acc_bytes + cnt_bytes, st);
+            if (e != cudaSuccess) { dev_free(ws_call, st); return cuda_fail(e, "gemv workspace"); }
+            ws = ws_call;
+        }
     }
     int cta = 0;
     for (int l = 0; l < nl; ++l) {
         const bool sk = ws && pl.ksplit[l] > 1;
-        fill_layer_args(&p.L[l], Ls_[l], pl, l, cta, ys[l], sk ? reinterpret_cast<float*>(ws + ws_off[l]) : nullptr,
-                        sk ? reinterpret_cast<unsigned long long*>(ws + ws_bytes + tk_off[l]) : nullptr);
+        fill_layer_args(&p.L[l], Ls_[l], pl, l, cta, ys[l], sk ? reinterpret_cast<long long*>(ws + acc_off[l]) : nullptr,
+                        sk ? reinterpret_cast<unsigned*>(ws + acc_bytes + cnt_off[l]) : nullptr);
         cta += pl.row_tiles[l] * pl.ksplit[l];
     }
     // L2-prefetch hints for the next launch of a decode chain (same tiling family)
@@ -574,7 +615,7 @@ fasq_status gemv_grouped_launch2(const fasq_layer* const* Ls_, int nl, const voi
         bool ok = true;
         for (int l = 0; l < n_next; ++l) ok = ok && next[l] && next[l]->d == Ls_[0]->d;
         if (ok) {
-            GemvPlan pn = plan_gemv(next, n_next, NB, !o.y_acc);
+            GemvPlan pn = plan_gemv(next, n_next, NB, false);
             if (pn.R == pl.R && pn.st == pl.st) {
                 int c2 = 0;
                 for (int l = 0; l < n_next; ++l) {
@@ -593,7 +634,7 @@ fasq_status gemv_grouped_launch2(const fasq_layer* const* Ls_, int nl, const voi
         case 8: s = dispatch_nb<8>(NB, p, pl, flags, st); break;
         default: s = FASQ_E_UNSUPPORTED;
     }
-    dev_free(ws, st);   // stream-ordered: released after the launch completes
+    dev_free(ws_call, st);   // stream-ordered: released after the launch completes
     if (s == FASQ_OK) set_launch_count(1);
     return s;
 }

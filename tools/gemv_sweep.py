@@ -27,12 +27,15 @@ def run(F_out, F_in, d, C, B, iters=200, flags=0, min_bytes=600e6):
         del cb, idx
     x = synth.torch_activation(B, F_in)
     ys = [torch.empty((B, F_out), dtype=torch.float32, device="cuda") for _ in range(nrep)]
-    for i in range(2 * nrep):
-        F.gemv(layers[i % nrep], x, out=ys[i % nrep], flags=flags)
-    torch.cuda.synchronize()
-    # capture `iters` launches in a CUDA graph so host overhead is excluded
+    # warm-up on the capture stream (sizes that stream's split-K workspace
+    # outside capture, as a user of a captured decode loop would)
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for i in range(2 * nrep):
+            F.gemv(layers[i % nrep], x, out=ys[i % nrep], flags=flags)
+    torch.cuda.synchronize()
+    # capture `iters` launches in a CUDA graph so host overhead is excluded
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(s):
         with torch.cuda.graph(g, stream=s):
