@@ -821,8 +821,19 @@ def pack_time():
             L.free()
             del W
         block_s += per[key]
+    # NEXT-4 packing variants on one 4096 x 4096 layer (k-means++ init, reseeding)
+    W = synth.torch_activation(4096, 4096, seed=5, std=0.02)
+    var = {}
+    for name, kw in (("kmeanspp", {"init": 1}), ("reseed", {"empty": 1}), ("kmeanspp+reseed", {"init": 1, "empty": 1})):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        L = F.pack(W, d=D, C=C, group=1, seed=0, iters=25, **kw)
+        torch.cuda.synchronize()
+        var[name] = round(time.perf_counter() - t0, 4)
+        L.free()
     return {"d": D, "C": C, "iters": 25, "seconds_per_layer_shape": per,
-            "whole_model_seconds_est": round(block_s * synth.LLAMA3_8B_BLOCKS, 2)}
+            "whole_model_seconds_est": round(block_s * synth.LLAMA3_8B_BLOCKS, 2),
+            "variants_4096x4096_seconds": var}
 
 
 # ----------------------------------------------------------------------------

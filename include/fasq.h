@@ -98,7 +98,11 @@ typedef struct {
     int32_t C;        /* K_s: 1..256 (uint8 indices)                              */
     int32_t group;    /* consecutive subspaces per codebook (1 = paper)           */
     int32_t iters;    /* T >= 0: maximum assign+update rounds (25 = default)      */
-    uint64_t seed;    /* seeded distinct-sample init (splitmix64)                 */
+    uint64_t seed;    /* seeded init (splitmix64)                                 */
+    int32_t init;     /* 0: seeded distinct sample (reading R3); 1: exact-integer
+                         k-means++ (reading R17)                      */
+    int32_t empty;    /* 0: an empty cluster keeps its centroid (R5); 1: reseed it
+                         from the farthest point (reading R18)        */
 } fasq_pack_params;
 
 typedef struct fasq_layer fasq_layer; /* opaque */

@@ -51,6 +51,8 @@ def lib() -> ctypes.CDLL:
         L.fasq_ref_validate.argtypes = [i64, i64, i32, i32, i32]
         L.fasq_ref_pack_range.argtypes = [vp, i64, i64, i32, i32, i32, u64, i32, i64, i64, vp, vp, vp]
         L.fasq_ref_pack.argtypes = [vp, i64, i64, i32, i32, i32, u64, i32, vp, vp, vp]
+        L.fasq_ref_pack_range_ex.argtypes = [vp, i64, i64, i32, i32, i32, u64, i32, i32, i32, i64, i64, vp, vp,
+                                             vp]
         L.fasq_ref_lloyd_fp32.argtypes = [vp, i64, i64, i32, i32, i32, u64, i32, i64, vp, vp]
         L.fasq_ref_reconstruct.argtypes = [vp, vp, i64, i64, i32, i32, i32, vp]
         L.fasq_ref_gemm_rows.argtypes = [vp, vp, i64, i64, i32, i32, i32, vp, i64, i64, i64, vp]
@@ -102,11 +104,14 @@ def num_threads() -> int:
 
 
 def pack(W, d: int, C: int, group: int = 1, seed: int = 0, iters: int = 25,
-         cb_range=None):
+         cb_range=None, init: int = 0, empty: int = 0):
     """Alg. 1: returns (codebooks fp16 [N_cb][C][d], indices u8
     [N_ss][F_out], iters_run int32 [N_cb]).  ``cb_range=(g0, g1)`` packs only
     codebooks g0..g1-1 (rows outside are left zero) -- codebooks are
-    independent k-means problems (Alg. 1 "parallel for")."""
+    independent k-means problems (Alg. 1 "parallel for").
+    init: 0 = seeded distinct sample (reading R3), 1 = exact-integer k-means++
+    (reading R17); empty: 0 = an empty cluster keeps its centroid
+    (R5), 1 = reseed from the farthest point (reading R18)."""
     Wb = _bits16(W)
     F_out, F_in = Wb.shape
     st = validate(F_out, F_in, d, C, group)
@@ -118,8 +123,8 @@ def pack(W, d: int, C: int, group: int = 1, seed: int = 0, iters: int = 25,
     cb = np.zeros((N_cb, C, d), np.uint16)
     idx = np.zeros((N_ss, F_out), np.uint8)
     its = np.zeros((N_cb,), np.int32)
-    st = lib().fasq_ref_pack_range(_ptr(Wb), F_out, F_in, d, C, group, seed & (2**64 - 1),
-                                   iters, g0, g1, _ptr(cb), _ptr(idx), _ptr(its))
+    st = lib().fasq_ref_pack_range_ex(_ptr(Wb), F_out, F_in, d, C, group, seed & (2**64 - 1),
+                                      iters, init, empty, g0, g1, _ptr(cb), _ptr(idx), _ptr(its))
     if st:
         raise OracleError(st)
     return cb.view(np.float16), idx, its

@@ -12,6 +12,10 @@
  *   fasq_ref_pack         Alg. 1: per-codebook k-means -> fp16
  *                         codebooks + uint8 indices, step by step as DESIGN.md
  *                         "Pack reading" fixes it.
+ *   fasq_ref_pack_range_ex  the same with the SPEC's packing variants (NEXT-4):
+ *                         exact-integer k-means++ init (reading R17) and
+ *                         empty-cluster reseeding from the farthest point
+ *                         (reading R18).
  *   fasq_ref_lloyd_fp32   the same Lloyd loop for ONE codebook, stopped before
  *                         finalisation (test hook for WCSS monotonicity).
  *   fasq_ref_reconstruct  the naive reconstruction: W_hat[j][ss*d+e]
@@ -174,7 +178,7 @@ static void merge_sort_rows(const uint16_t* pts, int d, int64_t* idx, int64_t* t
 /* Assign step: a_t = argmin_k D(p_t, c_k), D = sum_e (p_e - c_ke)^2 evaluated
  * left to right with separately rounded fp32 subtract, multiply and add;
  * strict '<' over ascending k so ties go to the lowest k (reading R7). */
-static int32_t nearest(const float* p, const float* cent, int C, int d) {
+static int32_t nearest_d(const float* p, const float* cent, int C, int d, float* bestD_out) {
     int32_t best = 0;
     float bestD = 0.0f;
     for (int k = 0; k < C; ++k) {
@@ -186,7 +190,61 @@ static int32_t nearest(const float* p, const float* cent, int C, int d) {
         }
         if (k == 0 || D < bestD) { bestD = D; best = k; }
     }
+    if (bestD_out) *bestD_out = bestD;
     return best;
+}
+static int32_t nearest(const float* p, const float* cent, int C, int d) { return nearest_d(p, cent, C, d, NULL); }
+
+/* k-means++ initialisation (NEXT-4, reading R17) in
+ * exact integer arithmetic so that any implementation reproduces it bit for
+ * bit: coordinates q = fp16 value * 2^24 (exact int64), D2(t, u) = sum_e
+ * (q_te - q_ue)^2 as an unsigned 128-bit integer.  The first centre is point
+ * next() % n; then, while centres are missing, r = (next() << 64 | next()) mod
+ * total with total = sum_t dist(t) (dist = D2 to the nearest chosen centre),
+ * and the next centre is the smallest t whose inclusive prefix sum of dist
+ * exceeds r (D^2 sampling).  total == 0 (every distinct point is a centre):
+ * the remaining slots copy centre 0 (as reading R3's slots >= m).  The
+ * splitmix64 state is seeded exactly as R3's.  chosen[k] = point id. */
+typedef unsigned __int128 u128;
+static u128 d2_int(const int64_t* q, int64_t t, int64_t u, int d) {
+    u128 s = 0;
+    for (int e = 0; e < d; ++e) {
+        __int128 df = (__int128)q[t * d + e] - (__int128)q[u * d + e];
+        s += (u128)(df * df);
+    }
+    return s;
+}
+static int kmeanspp(const uint16_t* pts, int64_t n, int d, int C, uint64_t seed, int64_t g, int64_t* chosen) {
+    int64_t* q = (int64_t*)malloc((size_t)n * d * sizeof(int64_t));
+    u128* dist = (u128*)malloc((size_t)n * sizeof(u128));
+    if (!q || !dist) { free(q); free(dist); return -1; }
+    for (int64_t t = 0; t < n * d; ++t) q[t] = (int64_t)((double)fasq_ref_f16_to_f32(pts[t]) * 16777216.0);
+    uint64_t st = seed ^ ((uint64_t)(g + 1) * 0x9E3779B97F4A7C15ull);
+    chosen[0] = (int64_t)(fasq_ref_splitmix64_next(&st) % (uint64_t)n);
+    for (int64_t t = 0; t < n; ++t) dist[t] = d2_int(q, t, chosen[0], d);
+    int k = 1;
+    for (; k < C; ++k) {
+        u128 total = 0;
+        for (int64_t t = 0; t < n; ++t) total += dist[t];
+        if (total == 0) break;
+        u128 hi = fasq_ref_splitmix64_next(&st);
+        u128 lo = fasq_ref_splitmix64_next(&st);
+        u128 r = ((hi << 64) | lo) % total;
+        u128 acc = 0;
+        int64_t pick = n - 1;
+        for (int64_t t = 0; t < n; ++t) {
+            acc += dist[t];
+            if (acc > r) { pick = t; break; }
+        }
+        chosen[k] = pick;
+        for (int64_t t = 0; t < n; ++t) {
+            u128 dd = d2_int(q, t, pick, d);
+            if (dd < dist[t]) dist[t] = dd;
+        }
+    }
+    for (; k < C; ++k) chosen[k] = chosen[0];
+    free(q); free(dist);
+    return 0;
 }
 
 /* Runs init + Lloyd for one codebook.  pts: n x d canonical fp16 bits.
@@ -194,7 +252,7 @@ static int32_t nearest(const float* p, const float* cent, int C, int d) {
  * assignment of the last assign pass.  Returns the number of assign passes
  * executed (0..iters), or <0 on allocation failure. */
 static int lloyd_one(const uint16_t* pts, int64_t n, int d, int C, uint64_t seed, int64_t g,
-                     int iters, float* cent, int32_t* assign) {
+                     int iters, float* cent, int32_t* assign, int init_mode, int empty_mode) {
     /* step 3: keys = the d fp16 patterns; U = sorted unique keys */
     int64_t* order = (int64_t*)malloc((size_t)n * sizeof(int64_t));
     int64_t* tmp = (int64_t*)malloc((size_t)n * sizeof(int64_t));
@@ -213,6 +271,15 @@ static int lloyd_one(const uint16_t* pts, int64_t n, int d, int C, uint64_t seed
         if (nU == 0 || cmp_tuple(pts + order[t] * d, pts + order[nU - 1] * d, d) != 0)
             order[nU++] = order[t];
     }
+    if (init_mode == 1) {
+        /* k-means++ (reading R17) */
+        if (kmeanspp(pts, n, d, C, seed, g, order) != 0) {
+            free(order); free(tmp); free(pf); free(prev); free(S); free(cnt);
+            return -1;
+        }
+        for (int k = 0; k < C; ++k)
+            for (int e = 0; e < d; ++e) cent[(size_t)k * d + e] = fasq_ref_f16_to_f32(pts[order[k] * d + e]);
+    } else {
     /* step 4: seeded partial Fisher-Yates over U, m = min(C, |U|) */
     int64_t m = (int64_t)C < nU ? (int64_t)C : nU;
     uint64_t st = seed ^ ((uint64_t)(g + 1) * 0x9E3779B97F4A7C15ull);
@@ -225,14 +292,21 @@ static int lloyd_one(const uint16_t* pts, int64_t n, int d, int C, uint64_t seed
         int64_t src = order[k < m ? k : 0];
         for (int e = 0; e < d; ++e) cent[(size_t)k * d + e] = fasq_ref_f16_to_f32(pts[src * d + e]);
     }
+    }
     for (int64_t t = 0; t < n * d; ++t) pf[t] = fasq_ref_f16_to_f32(pts[t]);
 
     /* step 5: Lloyd */
+    float* bestD = empty_mode == 1 ? (float*)malloc((size_t)(n > 0 ? n : 1) * sizeof(float)) : NULL;
+    int64_t* taken = empty_mode == 1 ? (int64_t*)malloc((size_t)C * sizeof(int64_t)) : NULL;
+    if (empty_mode == 1 && (!bestD || !taken)) {
+        free(bestD); free(taken); free(order); free(tmp); free(pf); free(prev); free(S); free(cnt);
+        return -1;
+    }
     int ran = 0;
     for (int it = 1; it <= iters; ++it) {
         int changed = 0;
         for (int64_t t = 0; t < n; ++t) {
-            int32_t a = nearest(pf + t * d, cent, C, d);
+            int32_t a = nearest_d(pf + t * d, cent, C, d, bestD ? bestD + t : NULL);
             if (it > 1 && a != prev[t]) changed = 1;
             assign[t] = a;
         }
@@ -248,14 +322,34 @@ static int lloyd_one(const uint16_t* pts, int64_t n, int d, int C, uint64_t seed
             for (int e = 0; e < d; ++e)
                 S[(size_t)a * d + e] += (int64_t)((double)pf[t * d + e] * 16777216.0);
         }
+        if (empty_mode == 1) {
+            /* reseed (reading R18): empty clusters, ascending k, take the
+             * points farthest from their assigned centroid (this iteration's fp32
+             * assignment distance), ties -> lowest t, each point at most once */
+            int64_t ntaken = 0;
+            for (int k = 0; k < C; ++k) {
+                if (cnt[k] != 0) continue;
+                int64_t best = -1;
+                for (int64_t t = 0; t < n; ++t) {
+                    int used = 0;
+                    for (int64_t q2 = 0; q2 < ntaken; ++q2) used |= taken[q2] == t;
+                    if (used) continue;
+                    if (best < 0 || bestD[t] > bestD[best]) best = t;
+                }
+                if (best < 0) continue;
+                taken[ntaken++] = best;
+                for (int e = 0; e < d; ++e) cent[(size_t)k * d + e] = pf[best * d + e];
+            }
+        }
         for (int k = 0; k < C; ++k) {
-            if (cnt[k] == 0) continue;       /* empty cluster keeps its centroid (reading R5) */
+            if (cnt[k] == 0) continue;       /* empty cluster: kept (R5) or reseeded above (R18) */
             for (int e = 0; e < d; ++e) {
                 double mean = (double)S[(size_t)k * d + e] / (double)cnt[k];
                 cent[(size_t)k * d + e] = (float)(mean * (1.0 / 16777216.0));
             }
         }
     }
+    free(bestD); free(taken);
     free(order); free(tmp); free(pf); free(prev); free(S); free(cnt);
     return ran;
 }
@@ -278,9 +372,10 @@ static void gather_points(const uint16_t* W, int64_t F_out, int64_t F_in, int d,
  * indices:   [N_ss][F_out] uint8 (only subspaces of codebooks g0..g1-1 written);
  * iters_run: optional [N_cb] number of assign passes executed.
  * Deterministic for any OpenMP thread count (codebooks are independent). */
-int fasq_ref_pack_range(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
-                        int32_t group, uint64_t seed, int32_t iters, int64_t g0, int64_t g1,
-                        uint16_t* codebooks, uint8_t* indices, int32_t* iters_run) {
+int fasq_ref_pack_range_ex(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
+                           int32_t group, uint64_t seed, int32_t iters, int32_t init_mode, int32_t empty_mode,
+                           int64_t g0, int64_t g1, uint16_t* codebooks, uint8_t* indices, int32_t* iters_run) {
+    if (init_mode < 0 || init_mode > 1 || empty_mode < 0 || empty_mode > 1) return REF_E_ARG;
     int st = fasq_ref_validate(F_out, F_in, d, C, group);
     if (st != REF_OK) return st;
     if (iters < 0) return REF_E_ARG;
@@ -304,7 +399,7 @@ int fasq_ref_pack_range(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t 
             fail = 1;
         } else {
             gather_points(W, F_out, F_in, d, group, g, pts);
-            int ran = lloyd_one(pts, n, d, C, seed, g, iters, cent, asg);
+            int ran = lloyd_one(pts, n, d, C, seed, g, iters, cent, asg, init_mode, empty_mode);
             if (ran < 0) {
 #pragma omp atomic write
                 fail = 1;
@@ -332,6 +427,13 @@ int fasq_ref_pack_range(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t 
     return fail ? REF_E_OOM : REF_OK;
 }
 
+int fasq_ref_pack_range(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
+                        int32_t group, uint64_t seed, int32_t iters, int64_t g0, int64_t g1,
+                        uint16_t* codebooks, uint8_t* indices, int32_t* iters_run) {
+    return fasq_ref_pack_range_ex(W, F_out, F_in, d, C, group, seed, iters, 0, 0, g0, g1, codebooks, indices,
+                                  iters_run);
+}
+
 int fasq_ref_pack(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
                   int32_t group, uint64_t seed, int32_t iters, uint16_t* codebooks,
                   uint8_t* indices, int32_t* iters_run) {
@@ -353,7 +455,7 @@ int fasq_ref_lloyd_fp32(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t 
     uint16_t* pts = (uint16_t*)malloc((size_t)n * d * sizeof(uint16_t));
     if (!pts) return REF_E_OOM;
     gather_points(W, F_out, F_in, d, group, g, pts);
-    int ran = lloyd_one(pts, n, d, C, seed, g, iters, cent, assign);
+    int ran = lloyd_one(pts, n, d, C, seed, g, iters, cent, assign, 0, 0);
     free(pts);
     return ran < 0 ? REF_E_OOM : ran;
 }

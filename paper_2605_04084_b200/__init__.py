@@ -52,7 +52,8 @@ class FasqError(RuntimeError):
 
 class _PackParams(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int32), ("C", ctypes.c_int32), ("group", ctypes.c_int32),
-                ("iters", ctypes.c_int32), ("seed", ctypes.c_uint64)]
+                ("iters", ctypes.c_int32), ("seed", ctypes.c_uint64), ("init", ctypes.c_int32),
+                ("empty", ctypes.c_int32)]
 
 
 class GemvOpts(ctypes.Structure):
@@ -239,10 +240,10 @@ class Layer:
 
 
 def pack(W: torch.Tensor, d: int, C: int, group: int = 1, seed: int = 0, iters: int = 25,
-         stream=None) -> Layer:
+         stream=None, init: int = 0, empty: int = 0) -> Layer:
     """Alg. 1 on the GPU: k-means per codebook -> Layer."""
     W = _cuda(W, torch.float16, "W")
-    prm = _PackParams(d, C, group, iters, seed & (2**64 - 1))
+    prm = _PackParams(d, C, group, iters, seed & (2**64 - 1), init, empty)
     out = ctypes.c_void_p()
     _check(lib.fasq_pack(W.data_ptr(), W.shape[0], W.shape[1], ctypes.byref(prm), _stream(stream),
                          ctypes.byref(out)))

@@ -93,7 +93,7 @@ fasq_status fasq_pack(const void* W_dev, int64_t F_out, int64_t F_in, const fasq
     if (!out) return FASQ_E_ARG;
     *out = nullptr;
     if (!W_dev || !prm) return FASQ_E_ARG;
-    if (prm->iters < 0) return FASQ_E_ARG;
+    if (prm->iters < 0 || prm->init < 0 || prm->init > 1 || prm->empty < 0 || prm->empty > 1) return FASQ_E_ARG;
     fasq_layer* L = new fasq_layer();
     fasq_status s = init_layer_shape(L, F_out, F_in, prm->d, prm->C, prm->group);
     if (s == FASQ_OK && (int64_t)prm->C > (int64_t)prm->group * F_out) s = FASQ_E_CLUSTER_OVERFLOW;

@@ -128,7 +128,7 @@ __global__ void k_init(uint64_t* __restrict__ Uhi, uint64_t* __restrict__ Ulo, c
 // argmin_k D(p, c_k): D = sum_e (p_e - c_ke)^2 left to right, separately
 // rounded fp32 ops (never contracted), strict '<', ascending k.
 template <int D>
-__device__ __forceinline__ int nearest(const float* p, const float* __restrict__ sc, int C) {
+__device__ __forceinline__ int nearest(const float* p, const float* __restrict__ sc, int C, float* bestD_out = nullptr) {
     int best = 0;
     float bestD = 0.f;
     for (int k = 0; k < C; ++k) {
@@ -141,7 +141,87 @@ __device__ __forceinline__ int nearest(const float* p, const float* __restrict__
         }
         if (k == 0 || acc < bestD) { bestD = acc; best = k; }
     }
+    if (bestD_out) *bestD_out = bestD;
     return best;
+}
+
+// ---- packing variants (NEXT-4) ------------------------------------------------
+// k-means++ (reading R17) in exact integer arithmetic, one CTA per
+// codebook: q = fp16 value * 2^24 (exact int64), D2 = sum_e (dq)^2 as u128;
+// centre 0 = point next() % n; then r = (next() << 64 | next()) mod total and
+// the next centre is the smallest t whose inclusive prefix of dist exceeds r;
+// total == 0: remaining slots copy centre 0.  Same splitmix64 stream as R3.
+typedef unsigned __int128 u128;
+constexpr int kPPThreads = 512;
+
+template <int D>
+__device__ __forceinline__ u128 d2_pts(const uint16_t* __restrict__ a, const uint16_t* __restrict__ b) {
+    u128 s = 0;
+#pragma unroll
+    for (int e = 0; e < D; ++e) {
+        const long long qa = (long long)__dmul_rn((double)__half2float(__ushort_as_half(a[e])), 16777216.0);
+        const long long qb = (long long)__dmul_rn((double)__half2float(__ushort_as_half(b[e])), 16777216.0);
+        const __int128 df = (__int128)qa - (__int128)qb;
+        s += (u128)(df * df);
+    }
+    return s;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kPPThreads) k_kmeanspp(const uint16_t* __restrict__ P, int64_t n, int C,
+                                                         uint64_t seed, u128* __restrict__ dist_all,
+                                                         float* __restrict__ cent) {
+    const int g = blockIdx.x, tid = threadIdx.x;
+    const uint16_t* Pg = P + (size_t)g * n * D;
+    u128* dist = dist_all + (size_t)g * n;
+    __shared__ u128 s_sum[kPPThreads];
+    __shared__ long long s_pick;
+    __shared__ int s_stop;
+    const int64_t per = (n + kPPThreads - 1) / kPPThreads;
+    const int64_t t0 = min(n, per * tid), t1 = min(n, t0 + per);
+    uint64_t st = seed ^ ((uint64_t)(g + 1) * kGolden);   // thread 0's stream
+    if (tid == 0) s_pick = (long long)(splitmix64_next(st) % (uint64_t)n);
+    __syncthreads();
+    long long first = s_pick;
+    for (int64_t t = t0; t < t1; ++t) dist[t] = d2_pts<D>(Pg + t * D, Pg + first * D);
+    if (tid < D) cent[((size_t)g * C) * D + tid] = __half2float(__ushort_as_half(Pg[first * D + tid]));
+    int k = 1;
+    for (; k < C; ++k) {
+        u128 cs = 0;
+        for (int64_t t = t0; t < t1; ++t) cs += dist[t];
+        s_sum[tid] = cs;
+        __syncthreads();
+        if (tid == 0) {
+            u128 total = 0;
+            for (int i = 0; i < kPPThreads; ++i) total += s_sum[i];
+            s_stop = total == 0;
+            if (total != 0) {
+                const u128 hi = splitmix64_next(st), lo = splitmix64_next(st);
+                u128 r = ((hi << 64) | lo) % total;
+                int c = 0;
+                while (r >= s_sum[c]) { r -= s_sum[c]; ++c; }   // chunk holding r (its sum > r)
+                const int64_t c0 = min(n, per * c), c1 = min(n, c0 + per);
+                long long pick = c1 - 1;
+                u128 acc = 0;
+                for (int64_t t = c0; t < c1; ++t) {
+                    acc += dist[t];
+                    if (acc > r) { pick = t; break; }
+                }
+                s_pick = pick;
+            }
+        }
+        __syncthreads();
+        if (s_stop) break;
+        const long long pk = s_pick;
+        for (int64_t t = t0; t < t1; ++t) {
+            const u128 dd = d2_pts<D>(Pg + t * D, Pg + pk * D);
+            if (dd < dist[t]) dist[t] = dd;
+        }
+        if (tid < D) cent[((size_t)g * C + k) * D + tid] = __half2float(__ushort_as_half(Pg[pk * D + tid]));
+        __syncthreads();   // s_sum / s_pick reuse
+    }
+    __syncthreads();
+    for (int q = k * D + tid; q < C * D; q += kPPThreads) cent[(size_t)g * C * D + q] = cent[(size_t)g * C * D + q % D];
 }
 
 constexpr int kAssignThreads = 256;
@@ -150,7 +230,8 @@ template <int D>
 __global__ void __launch_bounds__(kAssignThreads) k_assign_accum(
     const uint16_t* __restrict__ P, const float* __restrict__ cent, int64_t n, int C, int it,
     uint8_t* __restrict__ asg, const uint8_t* __restrict__ prev, unsigned long long* __restrict__ S,
-    unsigned long long* __restrict__ cnt, int* __restrict__ changed, const int* __restrict__ done) {
+    unsigned long long* __restrict__ cnt, int* __restrict__ changed, const int* __restrict__ done,
+    float* __restrict__ bestD) {
     const int g = blockIdx.y;
     if (done[g]) return;
     extern __shared__ __align__(16) uint8_t sm[];
@@ -169,7 +250,9 @@ __global__ void __launch_bounds__(kAssignThreads) k_assign_accum(
         float p[D];
 #pragma unroll
         for (int e = 0; e < D; ++e) p[e] = __half2float(__ushort_as_half(P[i * D + e]));
-        const int a = nearest<D>(p, sc, C);
+        float bd;
+        const int a = nearest<D>(p, sc, C, &bd);
+        if (bestD) bestD[i] = bd;
         asg[i] = (uint8_t)a;
         if (it > 1 && a != prev[i]) chg = true;
         atomicAdd(&sN[a], 1ull);
@@ -187,11 +270,18 @@ __global__ void __launch_bounds__(kAssignThreads) k_assign_accum(
 }
 
 // One block per codebook: stop test, then c = fp32((fp64(S)/fp64(n)) * 2^-24).
+// With bestD (empty = 1, reading R18): empty clusters, ascending
+// k, are reseeded with the points farthest from their assigned centroid
+// (this iteration's fp32 distance), ties -> lowest t, each point at most once.
 __global__ void k_update(float* __restrict__ cent, unsigned long long* __restrict__ S,
                          unsigned long long* __restrict__ cnt, int* __restrict__ changed, int* __restrict__ done,
-                         int* __restrict__ iters_run, int C, int d, int it) {
+                         int* __restrict__ iters_run, int C, int d, int it, const float* __restrict__ bestD,
+                         const uint16_t* __restrict__ P, int64_t n) {
     const int g = blockIdx.x;
     __shared__ int s_skip;
+    __shared__ unsigned long long s_best;
+    __shared__ long long s_taken[256];
+    __shared__ int s_ntaken;
     if (threadIdx.x == 0) {
         int sk = done[g];
         if (!sk) {
@@ -202,6 +292,35 @@ __global__ void k_update(float* __restrict__ cent, unsigned long long* __restric
     }
     __syncthreads();
     if (s_skip) return;
+    if (bestD) {
+        if (threadIdx.x == 0) s_ntaken = 0;
+        __syncthreads();
+        for (int k = 0; k < C; ++k) {
+            if (cnt[(int64_t)g * C + k] != 0ull) continue;   // block-uniform
+            if (threadIdx.x == 0) s_best = 0ull;
+            __syncthreads();
+            // key: distance bits (>= 0: order-preserving) high, ~t low -> max = farthest, lowest t
+            unsigned long long mine = 0ull;
+            for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
+                bool used = false;
+                for (int q2 = 0; q2 < s_ntaken; ++q2) used |= s_taken[q2] == t;
+                if (used) continue;
+                const unsigned long long key = ((unsigned long long)__float_as_uint(bestD[(int64_t)g * n + t]) << 32) |
+                                               (unsigned long long)(0xFFFFFFFFu - (unsigned)t);
+                mine = max(mine, key);
+            }
+            atomicMax(&s_best, mine);
+            __syncthreads();
+            if (s_best != 0ull) {
+                const long long t = (long long)(0xFFFFFFFFu - (unsigned)(s_best & 0xFFFFFFFFull));
+                if (threadIdx.x < d)
+                    cent[((int64_t)g * C + k) * d + threadIdx.x] =
+                        __half2float(__ushort_as_half(P[((int64_t)g * n + t) * d + threadIdx.x]));
+                if (threadIdx.x == 0) s_taken[s_ntaken++] = t;
+            }
+            __syncthreads();
+        }
+    }
     for (int q = threadIdx.x; q < C * d; q += blockDim.x) {
         const int k = q / d;
         const int64_t off = (int64_t)g * C * d + q;
@@ -250,16 +369,22 @@ template <int D>
 fasq_status lloyd_and_finalize(const uint16_t* P, float* cent, int64_t n, int N_cb, int C, int group,
                                int64_t F_out, int iters, uint8_t* asg0, uint8_t* asg1, unsigned long long* S,
                                unsigned long long* cnt, int* changed, int* done, int* iters_run, __half* cb_out,
-                               uint8_t* idx_out, cudaStream_t st) {
+                               uint8_t* idx_out, cudaStream_t st, float* bestD, u128* ppdist, uint64_t seed) {
+    if (ppdist) {   // k-means++ init replaces the distinct-sample init (reading R17)
+        k_kmeanspp<D><<<N_cb, kPPThreads, 0, st>>>(P, n, C, seed, ppdist, cent);
+        FASQ_CUDA_TRY(cudaGetLastError());
+        add_launch_count(1);
+    }
     const size_t smem = ((size_t)C * D * 4 + 15) / 16 * 16 + (size_t)C * D * 8 + (size_t)C * 8;
     const int chunks = (int)std::min<int64_t>((n + kAssignThreads - 1) / kAssignThreads, 64);
     dim3 grid(chunks, N_cb);
     for (int it = 1; it <= iters; ++it) {
         uint8_t* cur = (it & 1) ? asg1 : asg0;
         uint8_t* prv = (it & 1) ? asg0 : asg1;
-        k_assign_accum<D><<<grid, kAssignThreads, smem, st>>>(P, cent, n, C, it, cur, prv, S, cnt, changed, done);
+        k_assign_accum<D><<<grid, kAssignThreads, smem, st>>>(P, cent, n, C, it, cur, prv, S, cnt, changed, done,
+                                                              bestD);
         FASQ_CUDA_TRY(cudaGetLastError());
-        k_update<<<N_cb, 256, 0, st>>>(cent, S, cnt, changed, done, iters_run, C, D, it);
+        k_update<<<N_cb, 256, 0, st>>>(cent, S, cnt, changed, done, iters_run, C, D, it, bestD, P, n);
         FASQ_CUDA_TRY(cudaGetLastError());
     }
     k_finalize_cb<<<nb((int64_t)N_cb * C * D, 256), 256, 0, st>>>(cent, cb_out, (int64_t)N_cb * C * D);
@@ -326,6 +451,9 @@ fasq_status pack_run(const __half* W_, fasq_layer* L, const fasq_pack_params* pr
     int* changed = sc.get<int>(N_cb);
     int* done = sc.get<int>(N_cb);
     int* iters_run = sc.get<int>(N_cb);
+    float* bestD = prm->empty == 1 ? sc.get<float>(total) : nullptr;
+    u128* ppdist = prm->init == 1 ? sc.get<u128>(total) : nullptr;
+    if ((prm->empty == 1 && !bestD) || (prm->init == 1 && !ppdist)) return FASQ_E_OOM;
     if (!P || !khi || !shi || !off || !uflag || !pos || !cent || !asg0 || !asg1 || !S || !cnt || !changed ||
         !done || !iters_run || (wide && (!klo || !slo)))
         return FASQ_E_OOM;
@@ -386,13 +514,17 @@ fasq_status pack_run(const __half* W_, fasq_layer* L, const fasq_pack_params* pr
     // (a3) Lloyd + (a4) finalize
     switch (d) {
         case 1: return lloyd_and_finalize<1>(P, cent, n, N_cb, C, group, F_out, prm->iters, asg0, asg1, S, cnt,
-                                             changed, done, iters_run, cb_out, idx_out, st);
+                                             changed, done, iters_run, cb_out, idx_out, st, bestD,
+                                             ppdist, prm->seed);
         case 2: return lloyd_and_finalize<2>(P, cent, n, N_cb, C, group, F_out, prm->iters, asg0, asg1, S, cnt,
-                                             changed, done, iters_run, cb_out, idx_out, st);
+                                             changed, done, iters_run, cb_out, idx_out, st, bestD,
+                                             ppdist, prm->seed);
         case 4: return lloyd_and_finalize<4>(P, cent, n, N_cb, C, group, F_out, prm->iters, asg0, asg1, S, cnt,
-                                             changed, done, iters_run, cb_out, idx_out, st);
+                                             changed, done, iters_run, cb_out, idx_out, st, bestD,
+                                             ppdist, prm->seed);
         case 8: return lloyd_and_finalize<8>(P, cent, n, N_cb, C, group, F_out, prm->iters, asg0, asg1, S, cnt,
-                                             changed, done, iters_run, cb_out, idx_out, st);
+                                             changed, done, iters_run, cb_out, idx_out, st, bestD,
+                                             ppdist, prm->seed);
     }
     return FASQ_E_UNSUPPORTED;
 }

@@ -97,3 +97,37 @@ def test_pack_errors(F):
     with pytest.raises(F.FasqError) as e:
         F.pack(torch.from_numpy(synth.weight(4, 8)).cuda(), d=2, C=5)
     assert e.value.code == -3
+
+
+VARIANT_CASES = [
+    # F_out, F_in, d, C, group, seed, iters
+    (64, 32, 2, 16, 1, 0, 25),
+    (100, 48, 1, 8, 1, 1, 25),
+    (96, 64, 4, 32, 2, 2, 25),
+    (80, 64, 8, 16, 1, 3, 10),
+    (300, 128, 2, 256, 1, 4, 25),
+    (200, 32, 2, 7, 16, 6, 25),
+    (513, 96, 2, 64, 3, 7, 0),
+    (1024, 256, 2, 256, 1, 9, 25),
+]
+
+
+@pytest.mark.parametrize("init,empty", [(1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("F_out,F_in,d,C,group,seed,iters", VARIANT_CASES)
+def test_pack_variants_bit_exact(F, oracle_lib, F_out, F_in, d, C, group, seed, iters, init, empty):
+    """NEXT-4 packing variants (SPEC S:138 k-means++, S:140 reseed; readings
+    R17/R18): the GPU's bytes equal the oracle's."""
+    W = synth.weight(F_out, F_in, seed=seed)
+    ref_cb, ref_idx, _ = oracle_lib.pack(W, d=d, C=C, group=group, seed=seed, iters=iters, init=init, empty=empty)
+    L = F.pack(torch.from_numpy(W).cuda(), d=d, C=C, group=group, seed=seed, iters=iters, init=init, empty=empty)
+    cb, idx = L.export()
+    torch.cuda.synchronize()
+    _assert_same(cb.cpu().numpy(), idx.cpu().numpy(), ref_cb, ref_idx)
+    L.free()
+
+
+def test_pack_variant_arguments(F):
+    W = torch.from_numpy(synth.weight(64, 32, seed=0)).cuda()
+    for kw in ({"init": 2}, {"empty": -1}):
+        with pytest.raises(F.FasqError):
+            F.pack(W, d=2, C=8, **kw)
