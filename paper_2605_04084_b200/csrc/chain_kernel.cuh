@@ -199,17 +199,18 @@ __device__ __forceinline__ void warp_norm_scale(float (&sc)[NB], const unsigned 
     for (int b = 0; b < NB; ++b) {
         float a = 0.f;
         if (b < B) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int k = lane + 32 * h;
-                if (k < n_slots) {
-                    unsigned long long v;
-                    const unsigned long long t0 = dev::globaltimer();
-                    while (((v = ld_word(slots + b * 64 + k, false)) >> core::kCntShift) != 1ull)
-                        if (dev::globaltimer() - t0 > 4000000000ull) __trap();
-                    a += word_f32(v);
-                }
+            // both slots of this lane in flight, then the checks
+            unsigned long long v0 = 0ull, v1 = 0ull;   // count 0: not yet loaded
+            const bool h0 = lane < n_slots, h1 = lane + 32 < n_slots;
+            const unsigned long long t0 = dev::globaltimer();
+            for (bool done = false; !done;) {
+                if (h0 && (v0 >> core::kCntShift) != 1ull) v0 = ld_word(slots + b * 64 + lane, false);
+                if (h1 && (v1 >> core::kCntShift) != 1ull) v1 = ld_word(slots + b * 64 + lane + 32, false);
+                done = (!h0 || (v0 >> core::kCntShift) == 1ull) && (!h1 || (v1 >> core::kCntShift) == 1ull);
+                if (!done && dev::globaltimer() - t0 > 4000000000ull) __trap();
             }
+            if (h0) a += word_f32(v0);
+            if (h1) a += word_f32(v1);
         }
 #pragma unroll
         for (int m = 16; m >= 1; m >>= 1) a += __shfl_xor_sync(0xffffffffu, a, m);
@@ -408,10 +409,11 @@ __device__ __forceinline__ void stage_x_attn(uint8_t* s_x, const unsigned long l
                 done = true;
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    if (q < P && (lv[q] >> core::kCntShift) != 1ull) {
+                    if (q < P && (lv[q] >> core::kCntShift) != 1ull)
                         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(lv[q]) : "l"(hb + (size_t)q * (hd + 2) + hd + 1) : "memory");
-                        if ((lv[q] >> core::kCntShift) != 1ull) done = false;
-                    }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)   // checks after all loads were issued
+                    if (q < P && (lv[q] >> core::kCntShift) != 1ull) done = false;
                 if (!done && dev::globaltimer() - t_start > 4000000000ull) __trap();
             }
             float m[8], l[8], o[8][D];   // P <= 4, fully unrolled (registers, not local memory)
