@@ -563,13 +563,14 @@ def prefill_tflops(M=2048, iters=10):
         for name, algo in (("expand_tc", F.GEMM_EXPAND_TC), ("lut", F.GEMM_LUT)):
             try:
                 n_it = iters if algo == F.GEMM_EXPAND_TC else 2
-                F.gemm(L, X, out=Y, algo=algo)   # sizes workspaces outside capture
-                torch.cuda.synchronize()
                 # device time: n_it launches replayed from a CUDA graph (the
                 # ~40 us of Python/ctypes/tensor-map host work per call would
                 # otherwise starve the GPU at these sizes)
                 gs = torch.cuda.Stream()
                 gs.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(gs):
+                    F.gemm(L, X, out=Y, algo=algo)   # sizes the capture stream's workspace outside capture
+                torch.cuda.synchronize()
                 gr = torch.cuda.CUDAGraph()
                 with torch.cuda.stream(gs):
                     with torch.cuda.graph(gr, stream=gs):
@@ -636,10 +637,11 @@ def prefill_model(dense_peak, Ms=(512, 2048), reps=3):
                     F.gemm(Ls[n], bufs["o_proj"], out=bufs[n], algo=F.GEMM_EXPAND_TC)
                 F.gemm(Ls["down_proj"], bufs["gate_proj"], out=bufs["down_proj"], algo=F.GEMM_EXPAND_TC)
                 h = bufs["down_proj"]
-        one_pass()                      # sizes split-K workspaces outside capture
-        torch.cuda.synchronize()
         gs = torch.cuda.Stream()
         gs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(gs):
+            one_pass()                  # sizes the capture stream's split-K workspace outside capture
+        torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(gs):
             with torch.cuda.graph(g, stream=gs):

@@ -80,6 +80,38 @@ void dev_free(void* p, cudaStream_t st) {
     else cudaFreeAsync(p, st);
 }
 
+// Per-(stream, purpose) workspace, zeroed when (re)allocated; kernels keep
+// it in the state they need (GEMV: last contributors zero their words; EXPAND:
+// the last CTA of a tile resets its tickets; LUT: partials are overwritten).
+// Launches on one stream are ordered, so a workspace per stream keeps layers
+// immutable without a per-launch allocation or memset.  Grown outside stream
+// capture only: *out = NULL when `st` is capturing and the workspace is too
+// small (callers fall back to a per-call workspace).
+fasq_status stream_workspace(cudaStream_t st, int purpose, size_t bytes, void** out) {
+    struct Ws { void* p = nullptr; size_t bytes = 0; };
+    static std::mutex mu;
+    static std::unordered_map<cudaStream_t, Ws> ws_of[WS_KINDS];
+    std::lock_guard<std::mutex> lk(mu);
+    Ws& w = ws_of[purpose][st];
+    *out = nullptr;
+    if (w.bytes >= bytes) { *out = w.p; return FASQ_OK; }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return FASQ_OK;
+    FASQ_CUDA_TRY(cudaStreamSynchronize(st));
+    dev_free(w.p, st);
+    w.p = nullptr;
+    w.bytes = 0;
+    const size_t nb = bytes > ((size_t)1 << 20) ? bytes : ((size_t)1 << 20);
+    fasq_status s = dev_alloc(&w.p, nb, st);
+    if (s != FASQ_OK) return s;
+    FASQ_CUDA_TRY(cudaMemsetAsync(w.p, 0, nb, st));
+    FASQ_CUDA_TRY(cudaStreamSynchronize(st));
+    w.bytes = nb;
+    *out = w.p;
+    return FASQ_OK;
+}
+
 }  // namespace fasq
 
 using namespace fasq;

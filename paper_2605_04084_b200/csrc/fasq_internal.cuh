@@ -113,6 +113,8 @@ fasq_status copy_rows(const fasq_layer* src, fasq_layer* dst, int32_t row0, cuda
 // Device memory through the library allocator (alloc.cu, fasq_set_allocator).
 fasq_status dev_alloc(void** p, size_t bytes, cudaStream_t st);
 void dev_free(void* p, cudaStream_t st);
+enum { WS_GEMV = 0, WS_GEMM_TC = 1, WS_GEMM_LUT = 2, WS_KINDS = 3 };
+fasq_status stream_workspace(cudaStream_t st, int purpose, size_t bytes, void** out);   // alloc.cu
 template <class T>
 inline fasq_status dev_alloc_t(T** p, size_t bytes, cudaStream_t st) {
     void* q = nullptr;

@@ -212,9 +212,15 @@ fasq_status gemm_lut_launch(const fasq_layer* L, const __half* X, int64_t M, voi
     ks = std::max(1, std::min(ks, L->n_groups));
     float* part = nullptr;
     const int64_t n = M * L->F_out;
-    if (ks > 1) {
-        fasq_status a = dev_alloc_t(&part, (size_t)ks * n * sizeof(float), st);
+    float* part_call = nullptr;
+    if (ks > 1) {   // partials are overwritten: the stream's workspace, else a per-call one
+        fasq_status a = stream_workspace(st, WS_GEMM_LUT, (size_t)ks * n * sizeof(float), reinterpret_cast<void**>(&part));
         if (a != FASQ_OK) return a;
+        if (!part) {
+            a = dev_alloc_t(&part_call, (size_t)ks * n * sizeof(float), st);
+            if (a != FASQ_OK) return a;
+            part = part_call;
+        }
         grid.z = (unsigned)ks;
         p.part = part;
     }
@@ -227,7 +233,7 @@ fasq_status gemm_lut_launch(const fasq_layer* L, const __half* X, int64_t M, voi
         e = cudaGetLastError();
         if (e != cudaSuccess) s = cuda_fail(e, "k_lut_merge");
     }
-    dev_free(part, st);
+    dev_free(part_call, st);
     if (s != FASQ_OK) return s;
     set_launch_count(ks > 1 ? 2 : 1);
     return FASQ_OK;

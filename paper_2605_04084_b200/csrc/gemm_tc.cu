@@ -470,12 +470,20 @@ fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void
             // layer stays immutable): fp32 partial tiles + [tiles][arrive, depart]
             const size_t need = (size_t)ks * tiles * (TC_M * TC_MT) * TC_N * sizeof(float);
             const size_t tkb = (size_t)2 * tiles * sizeof(unsigned);
+            // the stream's workspace (tickets zero at allocation, reset by the last
+            // CTA of each tile; partials overwritten), else a per-call one
             uint8_t* ws = nullptr;
-            fasq_status s = dev_alloc_t(&ws, need + tkb, st);
+            fasq_status s = stream_workspace(st, WS_GEMM_TC, (size_t)(need + tkb) * (li + 1), reinterpret_cast<void**>(&ws));
             if (s != FASQ_OK) return s;
-            cudaError_t e = cudaMemsetAsync(ws + need, 0, tkb, st);
-            if (e != cudaSuccess) { dev_free(ws, st); return cuda_fail(e, "gemm workspace tickets"); }
-            wss[li] = ws;
+            if (ws) {
+                ws += (size_t)(need + tkb) * li;   // the two launches of one call use disjoint halves
+            } else {
+                s = dev_alloc_t(&ws, need + tkb, st);
+                if (s != FASQ_OK) return s;
+                cudaError_t e = cudaMemsetAsync(ws + need, 0, tkb, st);
+                if (e != cudaSuccess) { dev_free(ws, st); return cuda_fail(e, "gemm workspace tickets"); }
+                wss[li] = ws;
+            }
             p.ws = reinterpret_cast<float*>(ws);
             p.tickets = reinterpret_cast<unsigned*>(ws + need);
             grid.z = (unsigned)ks;

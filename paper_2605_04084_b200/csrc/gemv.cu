@@ -497,34 +497,6 @@ static GemvPlan plan_gemv(const fasq_layer* const* Ls, int nl, int NB, bool spin
     return pl;
 }
 
-// Per-stream split-K workspace (zeroed; kept zero by the kernels' last
-// contributors).  *out = NULL when the stream is capturing and the cached
-// workspace is too small (the caller falls back to a per-call workspace).
-static fasq_status stream_workspace(cudaStream_t st, size_t bytes, uint8_t** out) {
-    struct Ws { uint8_t* p = nullptr; size_t bytes = 0; };
-    static std::mutex mu;
-    static std::unordered_map<cudaStream_t, Ws> ws_of;
-    std::lock_guard<std::mutex> lk(mu);
-    Ws& w = ws_of[st];
-    *out = nullptr;
-    if (w.bytes >= bytes) { *out = w.p; return FASQ_OK; }
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(st, &cs);
-    if (cs != cudaStreamCaptureStatusNone) return FASQ_OK;
-    FASQ_CUDA_TRY(cudaStreamSynchronize(st));
-    dev_free(w.p, st);
-    w.p = nullptr;
-    w.bytes = 0;
-    const size_t nb = std::max(bytes, (size_t)1 << 20);
-    fasq_status s = dev_alloc_t(&w.p, nb, st);
-    if (s != FASQ_OK) return s;
-    FASQ_CUDA_TRY(cudaMemsetAsync(w.p, 0, nb, st));
-    FASQ_CUDA_TRY(cudaStreamSynchronize(st));
-    w.bytes = nb;
-    *out = w.p;
-    return FASQ_OK;
-}
-
 static void fill_layer_args(GemvLayerArgs* a, const fasq_layer* L, const GemvPlan& pl, int l, int cta, void* y,
                             long long* acc = nullptr, unsigned* cnt = nullptr) {
     a->idx = L->idx;
@@ -593,7 +565,7 @@ fasq_status gemv_grouped_launch2(const fasq_layer* const* Ls_, int nl, const voi
     uint8_t* ws = nullptr;
     uint8_t* ws_call = nullptr;   // per-call workspace (capture fallback), released after the launch
     if (acc_bytes) {
-        fasq_status s = stream_workspace(st, acc_bytes + cnt_bytes, &ws);
+        fasq_status s = stream_workspace(st, WS_GEMV, acc_bytes + cnt_bytes, reinterpret_cast<void**>(&ws));
         if (s != FASQ_OK) return s;
         if (!ws) {
             s = dev_alloc_t(&ws_call, acc_bytes + cnt_bytes, st);
