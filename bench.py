@@ -667,6 +667,24 @@ def prefill_model(dense_peak, Ms=(512, 2048), reps=3):
     return out
 
 
+def prefill_token_sharded(world, rank, dense_peak, M=2048):
+    """NEXT-1 (iii) token-sharded prefill: every rank holds the whole PQ model
+    (4.1 GB of weights: replicas fit 180 GB HBM easily) and runs M / world of
+    the M prompt tokens through the 224 PQ GEMMs (EXPAND) -- no collective on
+    the data path.  tok/s = M / (max over ranks of the pass time)."""
+    import torch
+    import torch.distributed as dist
+    m_local = M // world
+    r = prefill_model(dense_peak, Ms=(m_local,))["M%d" % m_local]
+    ms = r["ms_per_pass"]
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"global_tokens": M, "tokens_per_rank": m_local, "ranks": world, "ms_per_pass": round(ms, 3),
+            "tok_s": round(M * 1e3 / ms, 1), "collective": "none (weights replicated per rank)"}
+
+
 def decode_batch(peak, batches=(2, 4, 8), runs=20):
     """decode batch B in {2, 4, 8} at (2,256) through the
     chain kernel (one step = B tokens through the 224 layers).  Bytes per step
@@ -980,6 +998,11 @@ def main():
     lm_gbs = by["lm_head"] / (lm_ms * 1e-3) / 1e9
 
     side = {}
+    if world > 1 and not args.no_side:
+        try:   # every rank takes part (NEXT-1 iii; at N = 1 it is side.prefill_model M2048); reported by rank 0
+            side["prefill_token_sharded"] = prefill_token_sharded(world, rank, float(peaks.get("bf16_tflops", 1692.0)))
+        except Exception as e:
+            side["prefill_token_sharded"] = {"error": str(e)[:300]}
     if rank == 0 and not args.no_side:
         del g
         for name, fn in (("pq_chain", lambda: pq_chain_side(peak)),
