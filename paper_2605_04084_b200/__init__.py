@@ -41,7 +41,7 @@ EXPORTED = ["fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_
             "fasq_llama_kv_cache", "fasq_llama_reset", "fasq_llama_step", "fasq_llama_step_ex", "fasq_llama_tokens",
             "fasq_llama_step_host", "fasq_llama_logits", "fasq_llama_token_history", "fasq_llama_free",
             "fasq_last_launch_count", "fasq_status_string", "fasq_last_error_message",
-            "fasq_abi_version", "fasq_set_allocator"]
+            "fasq_abi_version", "fasq_set_allocator", "fasq_layer_distinct_centroids"]
 
 
 class FasqError(RuntimeError):
@@ -145,6 +145,8 @@ def _load():
     L.fasq_llama_free.restype = None
     L.fasq_gemm.argtypes = [vp, vp, i64, vp, i32, i32, vp]
     L.fasq_set_allocator.argtypes = [vp, vp, vp]
+    L.fasq_layer_distinct_centroids.argtypes = [vp, ctypes.POINTER(i64), vp]
+    L.fasq_layer_distinct_centroids.restype = ctypes.c_int32
     L.fasq_set_allocator.restype = ctypes.c_int32
     L.fasq_status_string.restype = ctypes.c_char_p
     L.fasq_last_error_message.restype = ctypes.c_char_p
@@ -232,6 +234,13 @@ class Layer:
         idx = torch.empty((self.N_ss, self.F_out), dtype=torch.uint8, device="cuda")
         _check(lib.fasq_export(self._h, cb.data_ptr(), idx.data_ptr(), _stream(stream)))
         return cb, idx
+
+    def distinct_centroids(self, stream=None) -> int:
+        """P:241 dedup: distinct fp16 centroids over all codebooks (dedup'd
+        codebook bytes = this * d * 2)."""
+        n = ctypes.c_int64()
+        _check(lib.fasq_layer_distinct_centroids(self._h, ctypes.byref(n), _stream(stream)))
+        return n.value
 
     def shard_rows(self, rank: int, world: int, stream=None) -> "Layer":
         out = ctypes.c_void_p()

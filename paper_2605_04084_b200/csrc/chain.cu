@@ -518,7 +518,8 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
                 // attn_item's scratch after the staged cache rows (the rows fall back to
                 // global loads when they do not fit; the scratch must)
                 const int Tp = (model->max_T + model->attn_parts - 1) / model->attn_parts + 1;
-                const size_t need = kAttnKV + kAttnScratchFixed + (size_t)(Tp + 4) * 4;
+                const size_t need = B == 1 ? kAttnKV + kAttnScratchFixed + (size_t)(Tp + 4) * 4
+                                           : (size_t)attn_batched_scratch(B, Tp);
                 if (need > kPairSlot) return fail(FASQ_E_UNSUPPORTED, "attention scratch exceeds a pair slot (max_T)");
             }
     }

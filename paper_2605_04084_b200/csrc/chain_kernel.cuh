@@ -149,7 +149,7 @@ __device__ __forceinline__ AttnRows attn_rows(int part, int P, int pos, int B, i
     r.t1 = (int)((long long)(part + 1) * Tn / P);
     r.te = min(r.t1, pos);
     const long long kv = (long long)B * max(0, r.te - r.t0) * hd * 4;
-    r.smem = r.te > r.t0 && kv <= (long long)kAttnKV &&
+    r.smem = B == 1 && r.te > r.t0 && kv <= (long long)kAttnKV &&
              kAttnKV + kAttnScratchFixed + (uint32_t)(r.t1 - r.t0 + 4) * 4u <= kPairSlot;
     return r;
 }
@@ -380,6 +380,171 @@ __device__ __forceinline__ void attn_item(const ChainPhase* ph, int head, int pa
     }
 }
 
+// ---- ATTN, B > 1: all tokens of a (q head, cache part) item at once --------
+// Same arithmetic as attn_item, per token b, but every phase covers all B
+// tokens (5 CTA barriers per item instead of 5 per token): the loop over b
+// cost ~9 us per token at B = 8.  The cache rows of B sequences do not fit
+// the SMEM prefetch, so they come from L2 (the producer warms them); the whole
+// 64 KiB pair slot is scratch: q, k, v, q' [B][128] fp32, k/v new [B][128]
+// fp16, scores [B][rows], o row-group partials [4][B][128], (m, l, s) [B].
+constexpr uint32_t attn_batched_scratch(int B, int rows) {
+    return (uint32_t)B * (4 * 128 * 4 + 2 * 128 * 2 + 4 * 128 * 4 + 16) + (uint32_t)B * (rows + 4) * 4;
+}
+
+__device__ __forceinline__ void attn_item_batched(const ChainPhase* ph, int head, int part, unsigned long long* cur,
+                                                  int B, int pos, int max_T, const float2* rope, uint8_t* slot,
+                                                  int NT) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int hd = ph->hd, half = hd / 2;
+    const int n_heads = ph->n_heads, n_kv = ph->n_kv, P = ph->parts;
+    const int grp = n_heads / n_kv, kvh = head / grp;
+    const AttnRows r = attn_rows(part, P, pos, B, hd);
+    const int nrow = r.t1 - r.t0;
+    const float qk_scale = 1.0f / sqrtf((float)hd);
+    float* s_q = reinterpret_cast<float*>(slot);             // [B][128]
+    float* s_k = s_q + B * 128;
+    float* s_v = s_k + B * 128;
+    float* s_qr = s_v + B * 128;
+    __half* s_kn = reinterpret_cast<__half*>(s_qr + B * 128);   // [B][128]
+    __half* s_vn = s_kn + B * 128;
+    float* s_o = reinterpret_cast<float*>(s_vn + B * 128);      // [4][B][128]
+    float* s_ml = s_o + 4 * B * 128;                            // [B][4]: m, l, scale
+    float* s_sc = s_ml + 4 * B;                                 // [B][nrow + 4]
+    const int scw = nrow + 4;
+    const size_t out_bstride = (size_t)n_heads * P * (hd + 2);
+    unsigned long long* out_base = cur + ph->o_off + (size_t)head * P * (hd + 2) + (size_t)part * (hd + 2);
+    if (nrow <= 0) {
+        for (int i = tid; i < B * hd; i += NT) st_word(out_base + (size_t)(i / hd) * out_bstride + i % hd, f32_word(0.f));
+        if (tid < B) st_word(out_base + (size_t)tid * out_bstride + hd, f32_word(-INFINITY));
+        consumer_bar(NT);
+        if (tid < B)
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(out_base + (size_t)tid * out_bstride + hd + 1),
+                         "l"(f32_word(0.f)) : "memory");
+        return;
+    }
+    // 0. the qkv step's RMSNorm scale of every token: warp b (idle in phase 1's tail)
+    if (warp < B) {
+        float sc[1] = {1.f};
+        if (ph->sc_off >= 0)
+            warp_norm_scale<1>(sc, cur + ph->sc_off + (size_t)warp * 64, ph->sc_n, ph->sc_F, ph->sc_eps, 1, lane);
+        if (lane == 0) s_ml[warp * 4 + 2] = sc[0];
+    }
+    // 1. q (this head), k, v (its KV head) of every token, all in flight
+    for (int i = tid; i < B * 3 * hd; i += NT) {
+        const int b = i / (3 * hd), rem = i - b * 3 * hd, which = rem / hd, e = rem - which * hd;
+        const unsigned long long* a =
+            which == 0 ? cur + ph->q_off + (size_t)b * ph->q_ld + (size_t)head * hd + e
+                       : cur + (which == 1 ? ph->k_off : ph->v_off) + (size_t)b * ph->kv_ld + (size_t)kvh * hd + e;
+        const int ks = which == 0 ? ph->q_ks : which == 1 ? ph->k_ks : ph->v_ks;
+        (which == 0 ? s_q : which == 1 ? s_k : s_v)[b * 128 + e] = (float)((double)core::poll_value(a, ks, false) * core::kAccInv);
+    }
+    consumer_bar(NT);
+    // 2. RoPE, new k/v (fp16), cache append (one writer per KV head, last part)
+    const bool writer = head % grp == 0 && r.t1 == pos + 1;
+    for (int i = tid; i < B * hd; i += NT) {
+        const int b = i / hd, e = i - b * hd;
+        const float sb = s_ml[b * 4 + 2];
+        __half* kc = ph->kc + ((size_t)b * n_kv + kvh) * (size_t)max_T * hd;
+        __half* vc = ph->vc + ((size_t)b * n_kv + kvh) * (size_t)max_T * hd;
+        if (e < half) {
+            const float2 cs = rope[(size_t)pos * half + e];
+            const float q0 = s_q[b * 128 + e] * sb, q1 = s_q[b * 128 + e + half] * sb;
+            const float k0 = s_k[b * 128 + e] * sb, k1 = s_k[b * 128 + e + half] * sb;
+            s_qr[b * 128 + e] = q0 * cs.x - q1 * cs.y;
+            s_qr[b * 128 + e + half] = q1 * cs.x + q0 * cs.y;
+            const __half kn0 = __float2half_rn(k0 * cs.x - k1 * cs.y), kn1 = __float2half_rn(k1 * cs.x + k0 * cs.y);
+            s_kn[b * 128 + e] = kn0;
+            s_kn[b * 128 + e + half] = kn1;
+            if (writer) { kc[(size_t)pos * hd + e] = kn0; kc[(size_t)pos * hd + e + half] = kn1; }
+        }
+        const __half vn = __float2half_rn(s_v[b * 128 + e] * sb);
+        s_vn[b * 128 + e] = vn;
+        if (writer) vc[(size_t)pos * hd + e] = vn;
+    }
+    consumer_bar(NT);
+    // 3. scores of every (token, row): 16 lanes per pair, 4 pairs in flight per lane group
+    {
+        const int nch = hd / 8;
+        const int c = tid & 15, gi = tid >> 4, ngr = NT / 16;
+        const int npair = B * nrow;
+        for (int base = gi; base < npair; base += 4 * ngr) {
+            uint4 kv[4];
+            float qv[4][8];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int pr = base + u * ngr;
+                kv[u] = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+                for (int i2 = 0; i2 < 8; ++i2) qv[u][i2] = 0.f;
+                if (pr < npair && c < nch) {
+                    const int b = pr / nrow, t = r.t0 + pr - b * nrow;
+                    const __half* kc = ph->kc + ((size_t)b * n_kv + kvh) * (size_t)max_T * hd;
+                    kv[u] = t == pos ? *reinterpret_cast<const uint4*>(s_kn + b * 128 + c * 8)
+                                     : __ldcg(reinterpret_cast<const uint4*>(kc + (size_t)t * hd + c * 8));
+#pragma unroll
+                    for (int i2 = 0; i2 < 8; ++i2) qv[u][i2] = s_qr[b * 128 + c * 8 + i2];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int pr = base + u * ngr;
+                const __half* kh = reinterpret_cast<const __half*>(&kv[u]);
+                float dsum = 0.f;
+#pragma unroll
+                for (int i2 = 0; i2 < 8; ++i2) dsum += qv[u][i2] * __half2float(kh[i2]);
+#pragma unroll
+                for (int m = 8; m >= 1; m >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, m);
+                if (c == 0 && pr < npair) {
+                    const int b = pr / nrow;
+                    s_sc[b * scw + pr - b * nrow] = dsum * qk_scale;
+                }
+            }
+        }
+    }
+    consumer_bar(NT);
+    // 4. softmax statistics of token b: warp b (fixed order: strided per lane, xor tree)
+    if (warp < B) {
+        float* sc = s_sc + warp * scw;
+        float mx = -INFINITY;
+        for (int i = lane; i < nrow; i += 32) mx = fmaxf(mx, sc[i]);
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, m));
+        float sm = 0.f;
+        for (int i = lane; i < nrow; i += 32) {
+            const float pe = expf(sc[i] - mx);
+            sc[i] = pe;
+            sm += pe;
+        }
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, m);
+        if (lane == 0) { s_ml[warp * 4] = mx; s_ml[warp * 4 + 1] = sm; }
+    }
+    consumer_bar(NT);
+    // 5. o partials: task (row group, token, dim), 4 row groups
+    for (int i = tid; i < 4 * B * hd; i += NT) {
+        const int rg = i / (B * hd), rem = i - rg * B * hd, b = rem / hd, dim = rem - b * hd;
+        const __half* vc = ph->vc + ((size_t)b * n_kv + kvh) * (size_t)max_T * hd;
+        float o = 0.f;
+        for (int t = r.t0 + rg; t < r.t1; t += 4) {
+            const __half vh = t == pos ? s_vn[b * 128 + dim] : __ldcg(vc + (size_t)t * hd + dim);
+            o += s_sc[b * scw + t - r.t0] * __half2float(vh);
+        }
+        s_o[(rg * B + b) * 128 + dim] = o;
+    }
+    consumer_bar(NT);
+    for (int i = tid; i < B * hd; i += NT) {
+        const int b = i / hd, dim = i - b * hd;
+        float od = 0.f;
+        for (int g2 = 0; g2 < 4; ++g2) od += s_o[(g2 * B + b) * 128 + dim];
+        st_word(out_base + (size_t)b * out_bstride + dim, f32_word(od));
+    }
+    if (tid < B) st_word(out_base + (size_t)tid * out_bstride + hd, f32_word(s_ml[tid * 4]));
+    consumer_bar(NT);
+    if (tid < B)   // l last, with release (cumulative over the barrier)
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(out_base + (size_t)tid * out_bstride + hd + 1),
+                     "l"(f32_word(s_ml[tid * 4 + 1])) : "memory");
+}
+
 // x staging of the o projection from the attention partials of an ATTN step
 // (counted words [B][heads][P][hd + 2], count 1): element col of token b is
 // head col / hd, dim col % hd; x = fp16(sum_q e_q o_q / sum_q e_q l_q) with
@@ -543,7 +708,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                     if (na.kind == SK_ATTN) {
                         const ChainPhase& P = p.phases[ph + 1];
                         const AttnRows r = attn_rows(na.kidx, P.parts, pos, p.B, P.hd);
-                        if (r.smem) {
+                        if (r.te > r.t0) {
                             const int kvh = na.head / (P.n_heads / P.n_kv);
                             const uint32_t rb = (uint32_t)(r.te - r.t0) * P.hd * 2u;
                             for (int b = 0; b < p.B; ++b) {
@@ -659,7 +824,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             if constexpr (PAIR) {
                 dev::mbar_wait(cfull0 + 8 * cslot, cpar);
                 if (tr && threadIdx.x == 0 && j == 0) *FASQ_TR(1) = *FASQ_TR(2) = dev::globaltimer();
-                attn_item(phs, w.head, w.kidx, cur, p.B, s_pos, p.max_T, p.rope, s_cb + (size_t)cslot * kPairSlot, NT);
+                if (NB == 1)
+                    attn_item(phs, w.head, w.kidx, cur, p.B, s_pos, p.max_T, p.rope, s_cb + (size_t)cslot * kPairSlot,
+                              NT);
+                else
+                    attn_item_batched(phs, w.head, w.kidx, cur, p.B, s_pos, p.max_T, p.rope,
+                                      s_cb + (size_t)cslot * kPairSlot, NT);
                 __syncwarp();
                 if (lane == 0) dev::mbar_arrive(cempty0 + 8 * cslot);
                 if (++cslot == CS) { cslot = 0; cpar ^= 1u; }

@@ -167,12 +167,17 @@ fasq_status fasq_layer_info_get(const fasq_layer* L, fasq_layer_info* info) {
     info->row_offset = L->row_offset;
     info->index_bytes = (int64_t)L->N_ss * L->F_out;
     info->codebook_bytes = L->cb_bytes;
-    info->device_bytes = L->idx_bytes + L->cbimg_bytes + L->cb_bytes;
+    info->device_bytes = L->idx_bytes + L->cbimg_bytes + L->cb_bytes + (L->cbimg_x ? L->cbimg_bytes : 0);
     info->bits_per_weight = 8.0 * (double)(info->index_bytes + info->codebook_bytes) / ((double)L->F_out * L->F_in);
     int lg = 0;
     while ((1 << lg) < L->C) ++lg;
     info->eff_bits_W = (double)lg / L->d;
     return FASQ_OK;
+}
+
+fasq_status fasq_layer_distinct_centroids(const fasq_layer* L, int64_t* distinct, void* stream) {
+    if (!L || !distinct) return FASQ_E_ARG;
+    return count_distinct_centroids(L, distinct, (cudaStream_t)stream);
 }
 
 void fasq_free(fasq_layer* L) {

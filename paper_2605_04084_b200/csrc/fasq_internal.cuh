@@ -104,7 +104,8 @@ constexpr uint32_t kPairSlot = 65536;
 
 // ---- layout kernels (layout.cu) ---------------------------------------------
 fasq_status alloc_layer_storage(fasq_layer* L, cudaStream_t st);
-fasq_status ensure_cbimg_x(const fasq_layer* L, cudaStream_t st);   // d = 2 only; synchronises st   // idx, cbimg, cb and (d <= 2) cbmap
+fasq_status ensure_cbimg_x(const fasq_layer* L, cudaStream_t st);   // d = 2 only; synchronises st
+fasq_status count_distinct_centroids(const fasq_layer* L, int64_t* distinct, cudaStream_t st);   // layout.cu   // idx, cbimg, cb and (d <= 2) cbmap
 fasq_status build_physical_from_logical(fasq_layer* L, const __half* cb_logical,
                                         const uint8_t* idx_logical, cudaStream_t st);
 fasq_status build_cbimg(fasq_layer* L, cudaStream_t st);

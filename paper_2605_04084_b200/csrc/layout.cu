@@ -198,4 +198,44 @@ fasq_status export_logical(const fasq_layer* L, __half* cb_out, uint8_t* idx_out
     return FASQ_OK;
 }
 
+// Distinct fp16 centroids per codebook (P:241 dedup): one thread per
+// codebook, entry k counts if no k' < k has identical bits (O(C^2 d)).
+__global__ void k_count_distinct(const uint16_t* __restrict__ cb, int N_cb, int C, int d,
+                                 unsigned long long* __restrict__ total) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= N_cb) return;
+    const uint16_t* c = cb + (size_t)g * C * d;
+    unsigned n = 0;
+    for (int k = 0; k < C; ++k) {
+        bool dup = false;
+        for (int k2 = 0; k2 < k && !dup; ++k2) {
+            bool eq = true;
+            for (int e = 0; e < d; ++e) eq &= c[k * d + e] == c[k2 * d + e];
+            dup = eq;
+        }
+        n += dup ? 0u : 1u;
+    }
+    atomicAdd(total, (unsigned long long)n);
+}
+
+fasq_status count_distinct_centroids(const fasq_layer* L, int64_t* distinct, cudaStream_t st) {
+    unsigned long long* t = nullptr;
+    fasq_status s = dev_alloc_t(&t, sizeof(unsigned long long), st);
+    if (s != FASQ_OK) return s;
+    unsigned long long h = 0;
+    cudaError_t e = cudaMemsetAsync(t, 0, sizeof(h), st);
+    if (e == cudaSuccess) {
+        k_count_distinct<<<nblk(L->N_cb, 128), 128, 0, st>>>(reinterpret_cast<const uint16_t*>(L->cb), L->N_cb,
+                                                             L->C, L->d, t);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, t, sizeof(h), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    dev_free(t, st);
+    if (e != cudaSuccess) return cuda_fail(e, "count_distinct_centroids");
+    *distinct = (int64_t)h;
+    set_launch_count(1);
+    return FASQ_OK;
+}
+
 }  // namespace fasq

@@ -131,3 +131,22 @@ def test_pack_variant_arguments(F):
     for kw in ({"init": 2}, {"empty": -1}):
         with pytest.raises(F.FasqError):
             F.pack(W, d=2, C=8, **kw)
+
+
+def test_dedup_distinct_centroids_and_lowest_copy(F, oracle_lib):
+    """P:241 dedup: the layer reports the distinct fp16 centroids per codebook
+    (counted independently here with numpy), and indices only ever reference
+    the FIRST copy of a repeated centroid (ties -> lowest k), so dropping the
+    later copies needs no index rewrite."""
+    W = synth.structured_weight(128, 64, 2, 5, seed=3)     # <= 5 distinct sub-vectors per codebook, C = 16
+    cb, idx, L = _gpu_pack(F, W, 2, 16, 1, 0, 25)
+    bits = cb.view(np.uint16)
+    want = sum(len({tuple(r) for r in bits[g]}) for g in range(bits.shape[0]))
+    assert L.distinct_centroids() == want
+    for g in range(bits.shape[0]):
+        first = {}
+        for k in range(16):
+            first.setdefault(tuple(bits[g, k]), k)
+        for k in set(idx[g].tolist()):
+            assert first[tuple(bits[g, k])] == k, (g, k)
+    L.free()
