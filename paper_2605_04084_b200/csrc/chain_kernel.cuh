@@ -180,12 +180,26 @@ __device__ __forceinline__ void embed_item(const ChainPhase* ph, unsigned long l
         asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(slot + 1), "l"(0ull) : "memory");
     }
     consumer_bar(NT);
+    // 8 rows' loads in flight per thread (a load -> store chain per element
+    // serialised one HBM round trip per iteration: 7 us at B = 1, 38 us at B = 8)
     const int n = ph->hidden;
-    for (int i = tid; i < B * n; i += NT) {
-        const int b = i / n, c = i - b * n;
-        const float v = __half2float(ph->embed[(size_t)s_tok[b] * n + c]);
-        const long long q = __float2ll_rn(v * core::kAccScale);
-        st_word(cur + ph->e_off + i, cnt_word(q));
+    constexpr int U = 8;
+    for (int i0 = tid; i0 < B * n; i0 += NT * U) {
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * NT;
+            v[u] = 0.f;
+            if (i < B * n) {
+                const int b = i / n, c = i - b * n;
+                v[u] = __half2float(ph->embed[(size_t)s_tok[b] * n + c]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * NT;
+            if (i < B * n) st_word(cur + ph->e_off + i, cnt_word(__float2ll_rn(v[u] * core::kAccScale)));
+        }
     }
 }
 
@@ -786,12 +800,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     const unsigned run = s_run;
     const unsigned par = run & 1u;
     unsigned long long* const cur = p.peers[p.rank] + (long long)par * p.arena_words;   // this run's buffer
-    {   // zero this CTA's share of the other buffer for run + 1 (16-B stores; arena_words is even)
-        ulonglong2* nxt = reinterpret_cast<ulonglong2*>(p.peers[p.rank] + (long long)(par ^ 1u) * p.arena_words);
+    // zero this CTA's share of the other buffer for run + 1 (16-B stores;
+    // arena_words is even).  Model chains do it after step 0 (the embedding,
+    // one CTA): the embedding CTA starts at once, the others zero while they
+    // would wait for it anyway.
+    auto zero_next = [&]() {
+        ulonglong2* nxt = reinterpret_cast<ulonglong2*>(p.peers[p.rank] + (long long)((s_run & 1u) ^ 1u) * p.arena_words);
         const long long n2 = p.arena_words / 2, per = (n2 + p.nctas - 1) / p.nctas;
         const long long zb = per * blockIdx.x, ze = min(n2, zb + per);
         for (long long i = zb + threadIdx.x; i < ze; i += NT) nxt[i] = make_ulonglong2(0ull, 0ull);
-    }
+    };
+    if (!MODEL) zero_next();
     const bool sys_out = p.world > 1;
 
     const int wrow0 = warp * RW;
@@ -803,6 +822,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
     uint32_t cpar = 0;
     for (int phj = 0; phj < p.n_steps * p.mi; ++phj) {
         const int ph = phj / p.mi, j = phj % p.mi;
+        if (MODEL && phj == p.mi) zero_next();   // start of step 1
         const ChainItem* wp = p.items + ((size_t)ph * p.nctas + blockIdx.x) * p.mi + j;
         const ChainPhase* phs = p.phases + ph;
         // item and phase fields by value: their loads issue here, before the
