@@ -149,6 +149,14 @@ fasq_status fasq_shard_rows(const fasq_layer* layer, int32_t rank, int32_t world
 fasq_status fasq_layer_info_get(const fasq_layer* layer, fasq_layer_info* info);
 void fasq_free(fasq_layer* layer);       /* synchronises the device; NULL is a no-op */
 
+/* Deduplication ("removing repeated centroids within each subspace"):
+ * *distinct = the number of distinct fp16 centroids summed over the layer's
+ * codebooks (at most N_cb * C); the deduplicated codebook size is
+ * distinct * d * 2 bytes.  Indices already reference only the first copy of a
+ * repeated centroid (nearest-centroid ties go to the lowest k, reading R5), so
+ * removing the later copies needs no index rewrite.  Synchronous. */
+fasq_status fasq_layer_distinct_centroids(const fasq_layer* layer, int64_t* distinct, void* stream);
+
 /* ---- products ------------------------------------------------------------ */
 
 /* Decode GEMV (Alg. 2's math): y[b] = W_hat . x[b].
