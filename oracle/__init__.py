@@ -49,6 +49,13 @@ def lib() -> ctypes.CDLL:
         i64, i32, u64 = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64
         vp = ctypes.c_void_p
         L.fasq_ref_validate.argtypes = [i64, i64, i32, i32, i32]
+        L.fasq_ref_validate16.argtypes = [i64, i64, i32, i32, i32]
+        L.fasq_ref_index_bits.argtypes = [i32]
+        L.fasq_ref_index_bits.restype = i32
+        L.fasq_ref_pack16_range_ex.argtypes = [vp, i64, i64, i32, i32, i32, u64, i32, i32, i32, i64, i64, vp, vp,
+                                               vp]
+        L.fasq_ref_reconstruct16.argtypes = [vp, vp, i64, i64, i32, i32, i32, vp]
+        L.fasq_ref_gemm_rows16.argtypes = [vp, vp, i64, i64, i32, i32, i32, vp, i64, i64, i64, vp]
         L.fasq_ref_pack_range.argtypes = [vp, i64, i64, i32, i32, i32, u64, i32, i64, i64, vp, vp, vp]
         L.fasq_ref_pack.argtypes = [vp, i64, i64, i32, i32, i32, u64, i32, vp, vp, vp]
         L.fasq_ref_pack_range_ex.argtypes = [vp, i64, i64, i32, i32, i32, u64, i32, i32, i32, i64, i64, vp, vp,
@@ -90,6 +97,19 @@ def _bits16(W) -> np.ndarray:
     return np.ascontiguousarray(W)
 
 
+def index_bits(C: int) -> int:
+    """Eq. 4: bits of one index, ceil(log2 K_s)."""
+    return int(lib().fasq_ref_index_bits(C))
+
+
+def _indices(indices) -> tuple[np.ndarray, bool]:
+    """A uint8 (C <= 256) or uint16 (C <= 1024, NEXT-2) index table and whether it is wide."""
+    a = np.asarray(indices)
+    if a.dtype == np.uint16:
+        return np.ascontiguousarray(a), True
+    return np.ascontiguousarray(a, dtype=np.uint8), False
+
+
 def validate(F_out: int, F_in: int, d: int, C: int, group: int) -> int:
     """(a1) Eq. 2 partition checks; 0 = ok, else a status code."""
     return int(lib().fasq_ref_validate(F_out, F_in, d, C, group))
@@ -106,7 +126,7 @@ def num_threads() -> int:
 def pack(W, d: int, C: int, group: int = 1, seed: int = 0, iters: int = 25,
          cb_range=None, init: int = 0, empty: int = 0):
     """Alg. 1: returns (codebooks fp16 [N_cb][C][d], indices u8
-    [N_ss][F_out], iters_run int32 [N_cb]).  ``cb_range=(g0, g1)`` packs only
+    [N_ss][F_out] -- uint16 when C > 256 --, iters_run int32 [N_cb]).  ``cb_range=(g0, g1)`` packs only
     codebooks g0..g1-1 (rows outside are left zero) -- codebooks are
     independent k-means problems (Alg. 1 "parallel for").
     init: 0 = seeded distinct sample (reading R3), 1 = exact-integer k-means++
@@ -114,17 +134,19 @@ def pack(W, d: int, C: int, group: int = 1, seed: int = 0, iters: int = 25,
     (R5), 1 = reseed from the farthest point (reading R18)."""
     Wb = _bits16(W)
     F_out, F_in = Wb.shape
-    st = validate(F_out, F_in, d, C, group)
+    wide = C > 256   # NEXT-2: uint16 indices for C <= 1024 (Eq. 4, Table 2 2-512 / 2-1024)
+    st = lib().fasq_ref_validate16(F_out, F_in, d, C, group) if wide else validate(F_out, F_in, d, C, group)
     if st:
         raise OracleError(st)
     N_ss = F_in // d
     N_cb = N_ss // group
     g0, g1 = (0, N_cb) if cb_range is None else cb_range
     cb = np.zeros((N_cb, C, d), np.uint16)
-    idx = np.zeros((N_ss, F_out), np.uint8)
+    idx = np.zeros((N_ss, F_out), np.uint16 if wide else np.uint8)
     its = np.zeros((N_cb,), np.int32)
-    st = lib().fasq_ref_pack_range_ex(_ptr(Wb), F_out, F_in, d, C, group, seed & (2**64 - 1),
-                                      iters, init, empty, g0, g1, _ptr(cb), _ptr(idx), _ptr(its))
+    fn = lib().fasq_ref_pack16_range_ex if wide else lib().fasq_ref_pack_range_ex
+    st = fn(_ptr(Wb), F_out, F_in, d, C, group, seed & (2**64 - 1), iters, init, empty, g0, g1, _ptr(cb),
+            _ptr(idx), _ptr(its))
     if st:
         raise OracleError(st)
     return cb.view(np.float16), idx, its
@@ -147,11 +169,12 @@ def lloyd_fp32(W, d: int, C: int, group: int, seed: int, iters: int, g: int):
 def reconstruct(codebooks, indices, F_in: int, group: int = 1) -> np.ndarray:
     """Naive reconstruction: W_hat fp16 [F_out][F_in]."""
     cb = _bits16(codebooks)
-    idx = np.ascontiguousarray(indices, dtype=np.uint8)
+    idx, wide = _indices(indices)
     N_cb, C, d = cb.shape
     N_ss, F_out = idx.shape
     out = np.zeros((F_out, F_in), np.uint16)
-    st = lib().fasq_ref_reconstruct(_ptr(cb), _ptr(idx), F_out, F_in, d, C, group, _ptr(out))
+    fn = lib().fasq_ref_reconstruct16 if wide else lib().fasq_ref_reconstruct
+    st = fn(_ptr(cb), _ptr(idx), F_out, F_in, d, C, group, _ptr(out))
     if st:
         raise OracleError(st)
     return out.view(np.float16)
@@ -161,7 +184,7 @@ def gemm(codebooks, indices, X, group: int = 1, rows=None) -> np.ndarray:
     """Reconstruct-then-multiply in fp64 (Eq. 3, P:200-203): Y [M][F_out]
     (or [M][j1-j0] for ``rows=(j0, j1)``)."""
     cb = _bits16(codebooks)
-    idx = np.ascontiguousarray(indices, dtype=np.uint8)
+    idx, wide = _indices(indices)
     Xb = _bits16(X)
     if Xb.ndim == 1:
         Xb = Xb[None, :]
@@ -171,8 +194,8 @@ def gemm(codebooks, indices, X, group: int = 1, rows=None) -> np.ndarray:
     M, F_in = Xb.shape
     j0, j1 = (0, F_out) if rows is None else rows
     Y = np.zeros((M, j1 - j0), np.float64)
-    st = lib().fasq_ref_gemm_rows(_ptr(cb), _ptr(idx), F_out, F_in, d, C, group, _ptr(Xb), M,
-                                  j0, j1, _ptr(Y))
+    fn = lib().fasq_ref_gemm_rows16 if wide else lib().fasq_ref_gemm_rows
+    st = fn(_ptr(cb), _ptr(idx), F_out, F_in, d, C, group, _ptr(Xb), M, j0, j1, _ptr(Y))
     if st:
         raise OracleError(st)
     return Y

@@ -18,6 +18,11 @@
  *                         (reading R18).
  *   fasq_ref_lloyd_fp32   the same Lloyd loop for ONE codebook, stopped before
  *                         finalisation (test hook for WCSS monotonicity).
+ *   fasq_ref_pack16_range_ex / _reconstruct16 / _gemm_rows16   the same with
+ *                         uint16 index tables for C <= 1024 (NEXT-2: Eq. 4's
+ *                         ceil(log2 K_s)-bit indices; 2-512 /
+ *                         2-1024 in Table 2); fasq_ref_index_bits
+ *                         = ceil(log2 K_s).
  *   fasq_ref_reconstruct  the naive reconstruction: W_hat[j][ss*d+e]
  *                         = T_cluster[cb(ss)][T_index[ss][j]][e].
  *   fasq_ref_gemm_rows    y[b][j] = sum_ss sum_e fp64(W_hat[j][ss*d+e]) *
@@ -129,10 +134,13 @@ uint64_t fasq_ref_splitmix64_next(uint64_t* state) {
 /* ------------------------------------------------------------------------ */
 /* (a1) partition and validate -- Eq. 2, SPEC plan_config        */
 /* ------------------------------------------------------------------------ */
-int fasq_ref_validate(int64_t F_out, int64_t F_in, int32_t d, int32_t C, int32_t group) {
+/* cmax: 256 for uint8 indices (the kernels' "1 B index"), 1024 for the
+ * uint16 entry points (Eq. 4: ceil(log2 K_s)-bit indices; Table 2's
+ * 2-512 / 2-1024 design points, P:479-488 -- NEXT-2). */
+static int validate_c(int64_t F_out, int64_t F_in, int32_t d, int32_t C, int32_t group, int32_t cmax) {
     if (F_out < 1 || F_in < 1 || d < 1 || C < 1 || group < 1) return REF_E_ARG;
     if (d != 1 && d != 2 && d != 4 && d != 8) return REF_E_UNSUPPORTED;
-    if (C > 256) return REF_E_UNSUPPORTED;                 /* uint8 indices */
+    if (C > cmax) return REF_E_UNSUPPORTED;
     if (F_in % d != 0) return REF_E_NONDIVISIBLE;
     int64_t N_ss = F_in / d;
     if (N_ss % group != 0) return REF_E_NONDIVISIBLE;
@@ -140,6 +148,20 @@ int fasq_ref_validate(int64_t F_out, int64_t F_in, int32_t d, int32_t C, int32_t
     if ((int64_t)C > n_pts) return REF_E_CLUSTER_OVERFLOW;
     if (n_pts > (1ll << 23)) return REF_E_UNSUPPORTED;    /* int64 exact-sum bound, R5 */
     return REF_OK;
+}
+int fasq_ref_validate(int64_t F_out, int64_t F_in, int32_t d, int32_t C, int32_t group) {
+    return validate_c(F_out, F_in, d, C, group, 256);
+}
+int fasq_ref_validate16(int64_t F_out, int64_t F_in, int32_t d, int32_t C, int32_t group) {
+    return validate_c(F_out, F_in, d, C, group, 1024);
+}
+
+/* Eq. 4: bits of one index = ceil(log2 K_s), the smallest b with
+ * 2^b >= K_s (0 for K_s = 1). */
+int32_t fasq_ref_index_bits(int32_t C) {
+    int32_t b = 0;
+    while (((int64_t)1 << b) < (int64_t)C) ++b;
+    return b;
 }
 
 /* ------------------------------------------------------------------------ */
@@ -372,11 +394,14 @@ static void gather_points(const uint16_t* W, int64_t F_out, int64_t F_in, int d,
  * indices:   [N_ss][F_out] uint8 (only subspaces of codebooks g0..g1-1 written);
  * iters_run: optional [N_cb] number of assign passes executed.
  * Deterministic for any OpenMP thread count (codebooks are independent). */
-int fasq_ref_pack_range_ex(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
+/* idx8 (C <= 256) or idx16 (C <= 1024, NEXT-2): exactly one is non-NULL; the
+ * arithmetic is the same for both, only the stored index width differs. */
+static int pack_range_impl(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
                            int32_t group, uint64_t seed, int32_t iters, int32_t init_mode, int32_t empty_mode,
-                           int64_t g0, int64_t g1, uint16_t* codebooks, uint8_t* indices, int32_t* iters_run) {
+                           int64_t g0, int64_t g1, uint16_t* codebooks, uint8_t* idx8, uint16_t* idx16,
+                           int32_t* iters_run) {
     if (init_mode < 0 || init_mode > 1 || empty_mode < 0 || empty_mode > 1) return REF_E_ARG;
-    int st = fasq_ref_validate(F_out, F_in, d, C, group);
+    int st = validate_c(F_out, F_in, d, C, group, idx16 ? 1024 : 256);
     if (st != REF_OK) return st;
     if (iters < 0) return REF_E_ARG;
     int64_t N_ss = F_in / d, N_cb = N_ss / group;
@@ -417,7 +442,9 @@ int fasq_ref_pack_range_ex(const uint16_t* W, int64_t F_out, int64_t F_in, int32
                     for (int64_t j = 0; j < F_out; ++j) {
                         int64_t t = s * F_out + j;
                         for (int e = 0; e < d; ++e) pf[e] = fasq_ref_f16_to_f32(pts[t * d + e]);
-                        indices[ss * F_out + j] = (uint8_t)nearest(pf, centh, C, d);
+                        const int32_t a = nearest(pf, centh, C, d);
+                        if (idx16) idx16[ss * F_out + j] = (uint16_t)a;
+                        else idx8[ss * F_out + j] = (uint8_t)a;
                     }
                 }
             }
@@ -425,6 +452,24 @@ int fasq_ref_pack_range_ex(const uint16_t* W, int64_t F_out, int64_t F_in, int32
         free(pts); free(cent); free(centh); free(asg); free(pf);
     }
     return fail ? REF_E_OOM : REF_OK;
+}
+
+int fasq_ref_pack_range_ex(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
+                           int32_t group, uint64_t seed, int32_t iters, int32_t init_mode, int32_t empty_mode,
+                           int64_t g0, int64_t g1, uint16_t* codebooks, uint8_t* indices, int32_t* iters_run) {
+    if (!indices) return REF_E_ARG;
+    return pack_range_impl(W, F_out, F_in, d, C, group, seed, iters, init_mode, empty_mode, g0, g1, codebooks,
+                           indices, NULL, iters_run);
+}
+
+/* The same with uint16 indices, C <= 1024 (NEXT-2: Eq. 4's ceil(log2 K_s)-bit
+ * indices for K_s = 512 / 1024, Table 2). */
+int fasq_ref_pack16_range_ex(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
+                             int32_t group, uint64_t seed, int32_t iters, int32_t init_mode, int32_t empty_mode,
+                             int64_t g0, int64_t g1, uint16_t* codebooks, uint16_t* indices, int32_t* iters_run) {
+    if (!indices) return REF_E_ARG;
+    return pack_range_impl(W, F_out, F_in, d, C, group, seed, iters, init_mode, empty_mode, g0, g1, codebooks,
+                           NULL, indices, iters_run);
 }
 
 int fasq_ref_pack_range(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
@@ -449,7 +494,7 @@ int fasq_ref_pack(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t d, int
 int fasq_ref_lloyd_fp32(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
                         int32_t group, uint64_t seed, int32_t iters, int64_t g, float* cent,
                         int32_t* assign) {
-    int st = fasq_ref_validate(F_out, F_in, d, C, group);
+    int st = fasq_ref_validate16(F_out, F_in, d, C, group);   /* int32 assignment: any C <= 1024 */
     if (st != REF_OK) return st;
     int64_t n = (int64_t)group * F_out;
     uint16_t* pts = (uint16_t*)malloc((size_t)n * d * sizeof(uint16_t));
@@ -464,30 +509,43 @@ int fasq_ref_lloyd_fp32(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t 
 /* Product: reconstruct-then-multiply (P:195-196 naive path; Eq. 3) */
 /* ------------------------------------------------------------------------ */
 
+/* T_index[ss][j] from a uint8 (wide = 0) or uint16 (wide = 1) table */
+static int64_t index_at(const void* indices, int wide, int64_t i) {
+    return wide ? (int64_t)((const uint16_t*)indices)[i] : (int64_t)((const uint8_t*)indices)[i];
+}
+
 /* W_hat[j][ss*d+e] = codebooks[ss/group][indices[ss][j]][e]  (fp16 bits) */
-int fasq_ref_reconstruct(const uint16_t* codebooks, const uint8_t* indices, int64_t F_out,
-                         int64_t F_in, int32_t d, int32_t C, int32_t group, uint16_t* W_hat) {
+static int reconstruct_impl(const uint16_t* codebooks, const void* indices, int wide, int64_t F_out,
+                            int64_t F_in, int32_t d, int32_t C, int32_t group, uint16_t* W_hat) {
     if (F_out < 1 || F_in < 1 || d < 1 || C < 1 || group < 1) return REF_E_ARG;
     if (F_in % d) return REF_E_NONDIVISIBLE;
     int64_t N_ss = F_in / d;
     if (N_ss % group) return REF_E_NONDIVISIBLE;
     for (int64_t j = 0; j < F_out; ++j)
         for (int64_t ss = 0; ss < N_ss; ++ss) {
-            int64_t k = indices[ss * F_out + j];
+            int64_t k = index_at(indices, wide, ss * F_out + j);
             if (k >= C) return REF_E_ARG;
             for (int e = 0; e < d; ++e)
                 W_hat[j * F_in + ss * d + e] = codebooks[((ss / group) * C + k) * d + e];
         }
     return REF_OK;
 }
+int fasq_ref_reconstruct(const uint16_t* codebooks, const uint8_t* indices, int64_t F_out,
+                         int64_t F_in, int32_t d, int32_t C, int32_t group, uint16_t* W_hat) {
+    return reconstruct_impl(codebooks, indices, 0, F_out, F_in, d, C, group, W_hat);
+}
+int fasq_ref_reconstruct16(const uint16_t* codebooks, const uint16_t* indices, int64_t F_out,
+                           int64_t F_in, int32_t d, int32_t C, int32_t group, uint16_t* W_hat) {
+    return reconstruct_impl(codebooks, indices, 1, F_out, F_in, d, C, group, W_hat);
+}
 
 /* Y[b][j - j0] = sum over (ss, e) ascending of fp64(W_hat[j][ss*d+e]) *
  * fp64(X[b][ss*d+e]) for rows j in [j0, j1) and b in [0, M).  fp16 x fp16
  * products are exact in fp64; only the running sum rounds.  Parallel over
  * (b, j) -- every output is computed independently in a fixed order. */
-int fasq_ref_gemm_rows(const uint16_t* codebooks, const uint8_t* indices, int64_t F_out,
-                       int64_t F_in, int32_t d, int32_t C, int32_t group, const uint16_t* X,
-                       int64_t M, int64_t j0, int64_t j1, double* Y) {
+static int gemm_rows_impl(const uint16_t* codebooks, const void* indices, int wide, int64_t F_out,
+                          int64_t F_in, int32_t d, int32_t C, int32_t group, const uint16_t* X,
+                          int64_t M, int64_t j0, int64_t j1, double* Y) {
     if (F_out < 1 || F_in < 1 || d < 1 || C < 1 || group < 1 || M < 0) return REF_E_ARG;
     if (F_in % d) return REF_E_NONDIVISIBLE;
     int64_t N_ss = F_in / d;
@@ -501,7 +559,7 @@ int fasq_ref_gemm_rows(const uint16_t* codebooks, const uint8_t* indices, int64_
     int bad = 0;
     for (int64_t r = 0; r < R; ++r)
         for (int64_t ss = 0; ss < N_ss; ++ss) {
-            int64_t k = indices[ss * F_out + (j0 + r)];
+            int64_t k = index_at(indices, wide, ss * F_out + (j0 + r));
             if (k >= C) bad = 1;
             for (int e = 0; e < d; ++e)
                 Wr[r * F_in + ss * d + e] =
@@ -520,6 +578,16 @@ int fasq_ref_gemm_rows(const uint16_t* codebooks, const uint8_t* indices, int64_
         }
     free(Wr); free(Xd);
     return REF_OK;
+}
+int fasq_ref_gemm_rows(const uint16_t* codebooks, const uint8_t* indices, int64_t F_out,
+                       int64_t F_in, int32_t d, int32_t C, int32_t group, const uint16_t* X,
+                       int64_t M, int64_t j0, int64_t j1, double* Y) {
+    return gemm_rows_impl(codebooks, indices, 0, F_out, F_in, d, C, group, X, M, j0, j1, Y);
+}
+int fasq_ref_gemm_rows16(const uint16_t* codebooks, const uint16_t* indices, int64_t F_out,
+                         int64_t F_in, int32_t d, int32_t C, int32_t group, const uint16_t* X,
+                         int64_t M, int64_t j0, int64_t j1, double* Y) {
+    return gemm_rows_impl(codebooks, indices, 1, F_out, F_in, d, C, group, X, M, j0, j1, Y);
 }
 
 int fasq_ref_gemm(const uint16_t* codebooks, const uint8_t* indices, int64_t F_out, int64_t F_in,

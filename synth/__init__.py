@@ -56,14 +56,14 @@ def random_layer(F_out: int, F_in: int, d: int, C: int, group: int = 1, seed: in
     """Logical PQ layer with uniform-random indices (worst-case locality) and
     fp16 N(0, std^2) codebooks; std defaults to 1/sqrt(F_in) so that a chain of
     layers keeps activations O(1).  Returns (codebooks [N_cb][C][d] fp16,
-    indices [N_ss][F_out] uint8)."""
+    indices [N_ss][F_out] uint8, uint16 when C > 256)."""
     g = rng(seed)
     N_ss = F_in // d
     N_cb = N_ss // group
     if std is None:
         std = 1.0 / np.sqrt(F_in)
     cb = g.normal(0.0, std, size=(N_cb, C, d)).astype(np.float16)
-    idx = g.integers(0, C, size=(N_ss, F_out), dtype=np.uint8) if C <= 256 else None
+    idx = g.integers(0, C, size=(N_ss, F_out), dtype=np.uint8 if C <= 256 else np.uint16)
     return cb, idx
 
 
@@ -80,7 +80,8 @@ def torch_random_layer(F_out: int, F_in: int, d: int, C: int, group: int = 1, se
     if std is None:
         std = 1.0 / float(np.sqrt(F_in))
     cb = (torch.randn((N_cb, C, d), generator=g, device=device) * std).to(torch.float16)
-    idx = torch.randint(0, C, (N_ss, F_out), generator=g, device=device, dtype=torch.int32).to(torch.uint8)
+    idx = torch.randint(0, C, (N_ss, F_out), generator=g, device=device, dtype=torch.int32)
+    idx = idx.to(torch.uint8) if C <= 256 else idx.to(torch.int16)   # int16 holds 0..1023 (uint16 bits)
     return cb, idx
 
 
