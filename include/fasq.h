@@ -17,7 +17,9 @@
  * Logical arrays (the only layouts that cross this ABI):
  *   W         fp16 [F_out][F_in]            row major
  *   codebooks fp16 [N_cb][C][d]             T_cluster
- *   indices   uint8 [N_ss][F_out]           T_index  ("1 B index" P:274)
+ *   indices   uint8 [N_ss][F_out]           T_index  ("1 B index" P:274);
+ *             uint16 when C > 256 (C <= 1024: Eq. 4's ceil(log2 K_s)-bit indices,
+ *             P:224-231, Table 2's 2-512 / 2-1024 points P:479-488)
  *   x / X     fp16 [B or M][F_in]           row major
  *   y / Y     fp16 or fp32 [B or M][F_out]  row major
  * A layer stores these in a private physical layout tuned for the kernels
@@ -52,7 +54,7 @@
 extern "C" {
 #endif
 
-#define FASQ_ABI_VERSION 3
+#define FASQ_ABI_VERSION 4
 
 typedef enum {
     FASQ_OK = 0,
@@ -61,7 +63,7 @@ typedef enum {
     FASQ_E_CLUSTER_OVERFLOW = -3, /* C > group*F_out points per codebook    */
     FASQ_E_NONFINITE = -4,        /* W holds inf/NaN (SPEC S:73 DegenerateInput)         */
     FASQ_E_SHAPE = -5,            /* operand shape mismatch          */
-    FASQ_E_UNSUPPORTED = -6,      /* d not in {1,2,4,8}, C > 256, B > 8, n_pts > 2^23    */
+    FASQ_E_UNSUPPORTED = -6,      /* d not in {1,2,4,8}, C > 1024 (or > 256 unpacked), B > 8, n_pts > 2^23 */
     FASQ_E_CUDA = -7,             /* CUDA runtime / launch error, or no device           */
     FASQ_E_OOM = -8,              /* device allocation failed                            */
     FASQ_E_RANGE = -9             /* a counted partial left its |v| < 2^18 range (fasq_chain_check) */
@@ -95,7 +97,7 @@ typedef enum {
 /* Pack parameters (Alg. 1). */
 typedef struct {
     int32_t d;        /* SZ_ss: 1, 2, 4 or 8                                     */
-    int32_t C;        /* K_s: 1..256 (uint8 indices)                              */
+    int32_t C;        /* K_s: 1..256 (uint8 indices); 257..1024 packed (d = 2)    */
     int32_t group;    /* consecutive subspaces per codebook (1 = paper)           */
     int32_t iters;    /* T >= 0: maximum assign+update rounds (25 = default)      */
     uint64_t seed;    /* seeded init (splitmix64)                                 */
@@ -103,6 +105,11 @@ typedef struct {
                          k-means++ (reading R17)                      */
     int32_t empty;    /* 0: an empty cluster keeps its centroid (R5); 1: reseed it
                          from the farthest point (reading R18)        */
+    int32_t packed;   /* NEXT-2 (Eq. 4): 1 = store ceil(log2 C)-bit
+                         packed indices (d = 2 only); 0 = uint8 indices.  Forced
+                         to 1 for C > 256.  Packed layers run fasq_gemv (B <=
+                         8) and fasq_gemm (as 8-token GEMV slices); the decode
+                         chain and fasq_llama_* reject them.                      */
 } fasq_pack_params;
 
 typedef struct fasq_layer fasq_layer; /* opaque */
@@ -111,11 +118,13 @@ typedef struct {
     int64_t F_out, F_in;
     int32_t d, C, group, N_ss, N_cb;
     int32_t row_offset;          /* first output row held (fasq_shard_rows), else 0 */
-    int64_t index_bytes;         /* logical: N_ss * F_out                         */
+    int64_t index_bytes;         /* Eq. 4 index table: ceil(N_ss*F_out*index_bits/8) */
     int64_t codebook_bytes;      /* logical: N_cb * C * d * 2                     */
     int64_t device_bytes;        /* physical HBM bytes this layer owns            */
     double bits_per_weight;      /* 8*(index+codebook bytes)/(F_out*F_in)         */
     double eff_bits_W;           /* paper #W = ceil(log2 C)/d             */
+    int32_t index_bits;          /* stored bits per index: 8 (uint8 layout) or
+                                    ceil(log2 C) (packed, NEXT-2)                 */
 } fasq_layer_info;
 
 /* ---- creation --------------------------------------------------------- */
@@ -129,14 +138,26 @@ fasq_status fasq_pack(const void* W_dev, int64_t F_out, int64_t F_in,
                       const fasq_pack_params* params, void* stream, fasq_layer** out);
 
 /* Creates a layer from logical codebooks (fp16 [N_cb][C][d]) and indices
- * (uint8 [N_ss][F_out]), both device pointers, e.g. an oracle-packed layer.
- * Indices >= C are a caller error (undefined results).  Asynchronous. */
+ * (uint8 [N_ss][F_out]; uint16 when C > 256), both device pointers, e.g. an
+ * oracle-packed layer.  C > 256 makes a packed layer (as fasq_import_packed
+ * with packed = 1).  Indices >= C are a caller error (undefined results for
+ * uint8 layers).  Asynchronous. */
 fasq_status fasq_import(const void* codebooks_dev, const void* indices_dev,
                         int64_t F_out, int64_t F_in, int32_t d, int32_t C, int32_t group,
                         void* stream, fasq_layer** out);
 
+/* NEXT-2 (Eq. 4): the same with the index storage chosen by the
+ * caller: packed = 1 stores ceil(log2 C) bits per index (d = 2, C in 2..1024;
+ * e.g. 7 bits for Table 2's 2-128), packed = 0 uint8 (C <= 256).  For a
+ * packed layer indices >= C return FASQ_E_ARG (checked on the device; this
+ * call synchronises `stream`). */
+fasq_status fasq_import_packed(const void* codebooks_dev, const void* indices_dev,
+                               int64_t F_out, int64_t F_in, int32_t d, int32_t C, int32_t group,
+                               int32_t packed, void* stream, fasq_layer** out);
+
 /* Writes the layer's logical codebooks / indices to device buffers of
- * N_cb*C*d fp16 and N_ss*F_out bytes (either pointer may be NULL). */
+ * N_cb*C*d fp16 and N_ss*F_out uint8 (uint16 when C > 256) elements (either
+ * pointer may be NULL). */
 fasq_status fasq_export(const fasq_layer* layer, void* codebooks_dev, void* indices_dev,
                         void* stream);
 
@@ -384,7 +405,9 @@ fasq_status fasq_gemv_host(const fasq_layer* layer, const void* x_host, int32_t 
                            void* y_host, fasq_dtype y_dtype, void* stream);
 
 /* Prefill GEMM (Alg. 3's math): Y = X . W_hat^T for M >= 1 rows.
- * X_dev fp16 [M][F_in], Y_dev [M][F_out] of y_dtype. */
+ * X_dev fp16 [M][F_in], Y_dev [M][F_out] of y_dtype.  On a packed-index layer
+ * (NEXT-2) only FASQ_GEMM_AUTO is accepted and the product runs as packed
+ * GEMVs over 8-token slices (no tensor-core kernel reads the packed layout). */
 fasq_status fasq_gemm(const fasq_layer* layer, const void* X_dev, int64_t M, void* Y_dev,
                       fasq_dtype y_dtype, fasq_gemm_algo algo, void* stream);
 

@@ -30,7 +30,7 @@ _STATUS = {0: "FASQ_OK", -1: "FASQ_E_ARG", -2: "FASQ_E_NONDIVISIBLE", -3: "FASQ_
            -8: "FASQ_E_OOM", -9: "FASQ_E_RANGE"}
 
 # Every symbol include/fasq.h declares (checked by tests/test_abi.py).
-EXPORTED = ["fasq_pack", "fasq_import", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
+EXPORTED = ["fasq_pack", "fasq_import", "fasq_import_packed", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
             "fasq_free", "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_acc_convert",
             "fasq_chain_create", "fasq_chain_create_tp", "fasq_chain_ipc_handle", "fasq_chain_set_peers",
             "fasq_chain_set_peer_chains", "fasq_chain_run", "fasq_chain_output", "fasq_chain_trace",
@@ -53,7 +53,7 @@ class FasqError(RuntimeError):
 class _PackParams(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int32), ("C", ctypes.c_int32), ("group", ctypes.c_int32),
                 ("iters", ctypes.c_int32), ("seed", ctypes.c_uint64), ("init", ctypes.c_int32),
-                ("empty", ctypes.c_int32)]
+                ("empty", ctypes.c_int32), ("packed", ctypes.c_int32)]
 
 
 class GemvOpts(ctypes.Structure):
@@ -86,7 +86,7 @@ class LayerInfo(ctypes.Structure):
                 ("N_cb", ctypes.c_int32), ("row_offset", ctypes.c_int32),
                 ("index_bytes", ctypes.c_int64), ("codebook_bytes", ctypes.c_int64),
                 ("device_bytes", ctypes.c_int64), ("bits_per_weight", ctypes.c_double),
-                ("eff_bits_W", ctypes.c_double)]
+                ("eff_bits_W", ctypes.c_double), ("index_bits", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -101,6 +101,7 @@ def _load():
     pp = ctypes.POINTER(ctypes.c_void_p)
     L.fasq_pack.argtypes = [vp, i64, i64, ctypes.POINTER(_PackParams), vp, pp]
     L.fasq_import.argtypes = [vp, vp, i64, i64, i32, i32, i32, vp, pp]
+    L.fasq_import_packed.argtypes = [vp, vp, i64, i64, i32, i32, i32, i32, vp, pp]
     L.fasq_export.argtypes = [vp, vp, vp, vp]
     L.fasq_shard_rows.argtypes = [vp, i32, i32, vp, pp]
     L.fasq_layer_info_get.argtypes = [vp, ctypes.POINTER(LayerInfo)]
@@ -211,6 +212,7 @@ class Layer:
         self.F_out, self.F_in = inf.F_out, inf.F_in
         self.d, self.C, self.group = inf.d, inf.C, inf.group
         self.N_ss, self.N_cb = inf.N_ss, inf.N_cb
+        self.index_bits = inf.index_bits   # 8, or ceil(log2 C) for a packed layer (NEXT-2)
 
     @property
     def handle(self):
@@ -229,9 +231,11 @@ class Layer:
             pass
 
     def export(self, stream=None):
-        """Logical arrays: (codebooks fp16 [N_cb][C][d], indices uint8 [N_ss][F_out])."""
+        """Logical arrays: (codebooks fp16 [N_cb][C][d], indices [N_ss][F_out] uint8, or
+        int16 holding the uint16 values when C > 256)."""
         cb = torch.empty((self.N_cb, self.C, self.d), dtype=torch.float16, device="cuda")
-        idx = torch.empty((self.N_ss, self.F_out), dtype=torch.uint8, device="cuda")
+        idx = torch.empty((self.N_ss, self.F_out), dtype=torch.uint8 if self.C <= 256 else torch.int16,
+                          device="cuda")
         _check(lib.fasq_export(self._h, cb.data_ptr(), idx.data_ptr(), _stream(stream)))
         return cb, idx
 
@@ -249,10 +253,11 @@ class Layer:
 
 
 def pack(W: torch.Tensor, d: int, C: int, group: int = 1, seed: int = 0, iters: int = 25,
-         stream=None, init: int = 0, empty: int = 0) -> Layer:
-    """Alg. 1 on the GPU: k-means per codebook -> Layer."""
+         stream=None, init: int = 0, empty: int = 0, packed: bool = False) -> Layer:
+    """Alg. 1 on the GPU: k-means per codebook -> Layer.  ``packed``
+    (implied for C > 256): ceil(log2 C)-bit packed index storage (Eq. 4, NEXT-2)."""
     W = _cuda(W, torch.float16, "W")
-    prm = _PackParams(d, C, group, iters, seed & (2**64 - 1), init, empty)
+    prm = _PackParams(d, C, group, iters, seed & (2**64 - 1), init, empty, 1 if packed else 0)
     out = ctypes.c_void_p()
     _check(lib.fasq_pack(W.data_ptr(), W.shape[0], W.shape[1], ctypes.byref(prm), _stream(stream),
                          ctypes.byref(out)))
@@ -260,15 +265,22 @@ def pack(W: torch.Tensor, d: int, C: int, group: int = 1, seed: int = 0, iters: 
 
 
 def import_layer(codebooks: torch.Tensor, indices: torch.Tensor, F_in: int, group: int = 1,
-                 stream=None) -> Layer:
-    """Layer from logical codebooks fp16 [N_cb][C][d] + indices uint8 [N_ss][F_out]."""
+                 stream=None, packed: bool | None = None) -> Layer:
+    """Layer from logical codebooks fp16 [N_cb][C][d] + indices [N_ss][F_out]
+    (uint8 for C <= 256, int16/uint16 bits above).  ``packed`` (default: C > 256)
+    stores ceil(log2 C)-bit indices (Eq. 4, NEXT-2)."""
     cb = _cuda(codebooks, torch.float16, "codebooks")
-    idx = _cuda(indices, torch.uint8, "indices")
     N_cb, C, d = cb.shape
+    wide = C > 256
+    if isinstance(indices, torch.Tensor) and indices.dtype in (torch.int16, torch.uint16):
+        indices = indices.view(torch.int16)
+    idx = _cuda(indices, torch.int16 if wide else torch.uint8, "indices")
     N_ss, F_out = idx.shape
+    if packed is None:
+        packed = wide
     out = ctypes.c_void_p()
-    _check(lib.fasq_import(cb.data_ptr(), idx.data_ptr(), F_out, F_in, d, C, group, _stream(stream),
-                           ctypes.byref(out)))
+    _check(lib.fasq_import_packed(cb.data_ptr(), idx.data_ptr(), F_out, F_in, d, C, group, 1 if packed else 0,
+                                  _stream(stream), ctypes.byref(out)))
     return Layer(out.value)
 
 

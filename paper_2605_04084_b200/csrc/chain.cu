@@ -203,6 +203,12 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
     if (n_steps < 1) return FASQ_E_ARG;
     if (world < 1 || world > 8 || rank < 0 || rank >= world || max_ctas < 0) return FASQ_E_ARG;
     if (B < 1 || B > 8) return FASQ_E_UNSUPPORTED;
+    for (const StepDesc& sd : steps)
+        for (const fasq_layer* L : sd.layers)
+            if (L && L->bits) {   // NEXT-2 packed indices: per-launch fasq_gemv only
+                set_error("chain: packed-index layers run through fasq_gemv, not the decode chain");
+                return FASQ_E_UNSUPPORTED;
+            }
     const int NB = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;
     fasq_chain* c = new fasq_chain();
     auto fail = [&](fasq_status s, const std::string& msg) {

@@ -1,6 +1,7 @@
 // fasq_api.cu -- the extern "C" boundary of libfasq.so (include/fasq.h).
 // Argument marshalling, validation, layer lifetime; all compute is in the
 // kernels of layout.cu / gemv.cu / gemm_*.cu / pack.cu.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -70,22 +71,27 @@ const char* fasq_status_string(fasq_status s) {
 const char* fasq_last_error_message(void) { return t_err.c_str(); }
 int32_t fasq_last_launch_count(void) { return t_launches; }
 
-fasq_status fasq_import(const void* codebooks_dev, const void* indices_dev, int64_t F_out, int64_t F_in,
-                        int32_t d, int32_t C, int32_t group, void* stream, fasq_layer** out) {
+fasq_status fasq_import_packed(const void* codebooks_dev, const void* indices_dev, int64_t F_out, int64_t F_in,
+                               int32_t d, int32_t C, int32_t group, int32_t packed, void* stream, fasq_layer** out) {
     if (!out) return FASQ_E_ARG;
     *out = nullptr;
     if (!codebooks_dev || !indices_dev) return FASQ_E_ARG;
     fasq_layer* L = new fasq_layer();
-    fasq_status s = init_layer_shape(L, F_out, F_in, d, C, group);
+    fasq_status s = init_layer_shape(L, F_out, F_in, d, C, group, packed);
     if (s == FASQ_OK) s = check_device();
     if (s == FASQ_OK) s = alloc_layer_storage(L, (cudaStream_t)stream);
     if (s == FASQ_OK)
-        s = build_physical_from_logical(L, static_cast<const __half*>(codebooks_dev),
-                                        static_cast<const uint8_t*>(indices_dev), (cudaStream_t)stream);
+        s = build_physical_from_logical(L, static_cast<const __half*>(codebooks_dev), indices_dev,
+                                        (cudaStream_t)stream);
     if (s != FASQ_OK) { destroy(L); return s; }
     set_launch_count(2);
     *out = L;
     return FASQ_OK;
+}
+
+fasq_status fasq_import(const void* codebooks_dev, const void* indices_dev, int64_t F_out, int64_t F_in,
+                        int32_t d, int32_t C, int32_t group, void* stream, fasq_layer** out) {
+    return fasq_import_packed(codebooks_dev, indices_dev, F_out, F_in, d, C, group, C > 256 ? 1 : 0, stream, out);
 }
 
 fasq_status fasq_pack(const void* W_dev, int64_t F_out, int64_t F_in, const fasq_pack_params* prm,
@@ -94,18 +100,28 @@ fasq_status fasq_pack(const void* W_dev, int64_t F_out, int64_t F_in, const fasq
     *out = nullptr;
     if (!W_dev || !prm) return FASQ_E_ARG;
     if (prm->iters < 0 || prm->init < 0 || prm->init > 1 || prm->empty < 0 || prm->empty > 1) return FASQ_E_ARG;
+    if (prm->packed < 0 || prm->packed > 1) return FASQ_E_ARG;
     fasq_layer* L = new fasq_layer();
-    fasq_status s = init_layer_shape(L, F_out, F_in, prm->d, prm->C, prm->group);
+    fasq_status s = init_layer_shape(L, F_out, F_in, prm->d, prm->C, prm->group,
+                                     (prm->packed || prm->C > 256) ? 1 : 0);
     if (s == FASQ_OK && (int64_t)prm->C > (int64_t)prm->group * F_out) s = FASQ_E_CLUSTER_OVERFLOW;
     if (s == FASQ_OK && (int64_t)prm->group * F_out > (1ll << 23)) s = FASQ_E_UNSUPPORTED;
     if (s == FASQ_OK) s = check_device();
     cudaStream_t st = (cudaStream_t)stream;
     if (s == FASQ_OK) s = alloc_layer_storage(L, st);
-    uint8_t* idx_log = nullptr;
-    if (s == FASQ_OK) s = dev_alloc_t(&idx_log, (size_t)L->N_ss * L->F_out, st);
+    uint16_t* idx_log = nullptr;   // the packer writes uint16 indices for every C
+    uint8_t* idx8 = nullptr;
+    const int64_t nidx = (int64_t)L->N_ss * L->F_out;
+    if (s == FASQ_OK) s = dev_alloc_t(&idx_log, (size_t)nidx * 2, st);
     if (s == FASQ_OK) s = pack_run(static_cast<const __half*>(W_dev), L, prm, st, L->cb, idx_log);
-    if (s == FASQ_OK) s = build_physical_from_logical(L, L->cb, idx_log, st);
+    if (s == FASQ_OK && L->idx_w == 1) {
+        s = dev_alloc_t(&idx8, (size_t)nidx, st);
+        if (s == FASQ_OK) s = idx16_to_8(idx_log, idx8, nidx, st);
+    }
+    if (s == FASQ_OK)
+        s = build_physical_from_logical(L, L->cb, L->idx_w == 1 ? static_cast<const void*>(idx8) : idx_log, st);
     dev_free(idx_log, st);
+    dev_free(idx8, st);
     if (s != FASQ_OK) { cudaStreamSynchronize(st); destroy(L); return s; }
     *out = L;
     return FASQ_OK;
@@ -113,8 +129,7 @@ fasq_status fasq_pack(const void* W_dev, int64_t F_out, int64_t F_in, const fasq
 
 fasq_status fasq_export(const fasq_layer* L, void* codebooks_dev, void* indices_dev, void* stream) {
     if (!L) return FASQ_E_ARG;
-    fasq_status s = export_logical(L, static_cast<__half*>(codebooks_dev), static_cast<uint8_t*>(indices_dev),
-                                   (cudaStream_t)stream);
+    fasq_status s = export_logical(L, static_cast<__half*>(codebooks_dev), indices_dev, (cudaStream_t)stream);
     if (s == FASQ_OK) set_launch_count(indices_dev ? 1 : 0);
     return s;
 }
@@ -131,18 +146,19 @@ fasq_status fasq_shard_rows(const fasq_layer* L, int32_t rank, int32_t world, vo
     uint8_t* full = nullptr;
     uint8_t* part = nullptr;
     fasq_status s = FASQ_OK;
-    s = dev_alloc_t(&full, (size_t)L->N_ss * L->F_out, st);
-    if (s == FASQ_OK) s = dev_alloc_t(&part, (size_t)L->N_ss * rows, st);
+    const size_t w = (size_t)L->idx_w;   // logical index element bytes
+    s = dev_alloc_t(&full, (size_t)L->N_ss * L->F_out * w, st);
+    if (s == FASQ_OK) s = dev_alloc_t(&part, (size_t)L->N_ss * rows * w, st);
     if (s == FASQ_OK) s = export_logical(L, nullptr, full, st);
     if (s == FASQ_OK) {
-        cudaError_t e = cudaMemcpy2DAsync(part, (size_t)rows, full + row0, (size_t)L->F_out, (size_t)rows,
-                                          (size_t)L->N_ss, cudaMemcpyDeviceToDevice, st);
+        cudaError_t e = cudaMemcpy2DAsync(part, (size_t)rows * w, full + row0 * w, (size_t)L->F_out * w,
+                                          (size_t)rows * w, (size_t)L->N_ss, cudaMemcpyDeviceToDevice, st);
         if (e != cudaSuccess) s = cuda_fail(e, "shard copy");
     }
     fasq_layer* S = nullptr;
     if (s == FASQ_OK) {
         S = new fasq_layer();
-        s = init_layer_shape(S, rows, L->F_in, L->d, L->C, L->group);
+        s = init_layer_shape(S, rows, L->F_in, L->d, L->C, L->group, L->bits ? 1 : 0);
         if (s == FASQ_OK) s = alloc_layer_storage(S, st);
         if (s == FASQ_OK) s = build_physical_from_logical(S, L->cb, part, st);
         if (s == FASQ_OK) S->row_offset = L->row_offset + (int32_t)row0;
@@ -165,12 +181,14 @@ fasq_status fasq_layer_info_get(const fasq_layer* L, fasq_layer_info* info) {
     info->N_ss = L->N_ss;
     info->N_cb = L->N_cb;
     info->row_offset = L->row_offset;
-    info->index_bytes = (int64_t)L->N_ss * L->F_out;
+    int lg = 0;
+    while ((1 << lg) < L->C) ++lg;
+    info->index_bits = L->bits ? L->bits : 8;
+    // Eq. 4's index table: index_bits per (subspace, row), rounded up to bytes
+    info->index_bytes = ((int64_t)L->N_ss * L->F_out * info->index_bits + 7) / 8;
     info->codebook_bytes = L->cb_bytes;
     info->device_bytes = L->idx_bytes + L->cbimg_bytes + L->cb_bytes + (L->cbimg_x ? L->cbimg_bytes : 0);
     info->bits_per_weight = 8.0 * (double)(info->index_bytes + info->codebook_bytes) / ((double)L->F_out * L->F_in);
-    int lg = 0;
-    while ((1 << lg) < L->C) ++lg;
     info->eff_bits_W = (double)lg / L->d;
     return FASQ_OK;
 }
@@ -206,6 +224,14 @@ fasq_status fasq_gemv_grouped(const fasq_layer* const* layers, int32_t n, const 
         if (!layers[i] || !ys_dev[i]) return FASQ_E_ARG;
     if (B < 1 || B > 8) return FASQ_E_UNSUPPORTED;
     if (yt != FASQ_F16 && yt != FASQ_F32 && yt != FASQ_ACC_I64) return FASQ_E_ARG;
+    bool packed = false;
+    for (int i = 0; i < n; ++i) packed = packed || layers[i]->bits;
+    if (packed) {   // NEXT-2: one packed layer per launch, fp16 x, no chain options
+        if (n != 1 || (opts && (opts->flags & FASQ_FLAG_X_ACC || opts->n_next || opts->zero_dev)))
+            return FASQ_E_UNSUPPORTED;
+        return gemv_packed_launch(layers[0], static_cast<const __half*>(x_dev), B, ys_dev[0], yt,
+                                  opts ? opts->flags : 0u, (cudaStream_t)stream);
+    }
     GemvOpts o{};
     if (opts) {
         if (opts->n_next < 0 || opts->n_next > 4 || opts->zero_bytes < 0 || (opts->zero_bytes & 7)) return FASQ_E_ARG;
@@ -271,6 +297,23 @@ fasq_status fasq_gemm(const fasq_layer* L, const void* X_dev, int64_t M, void* Y
     if (yt != FASQ_F16 && yt != FASQ_F32) return FASQ_E_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     const __half* X = static_cast<const __half*>(X_dev);
+    if (L->bits) {
+        // NEXT-2 packed indices: no tensor-core / LUT prefill kernel reads the
+        // packed layout; the product runs as packed GEMVs over 8-token slices
+        // (correct for any M, not a prefill-speed path -- DESIGN.md §11)
+        if (algo != FASQ_GEMM_AUTO) return FASQ_E_UNSUPPORTED;
+        const size_t yb = yt == FASQ_F32 ? 4 : 2;
+        int launches = 0;
+        for (int64_t m0 = 0; m0 < M; m0 += 8) {
+            const int b = (int)std::min<int64_t>(8, M - m0);
+            fasq_status s = gemv_packed_launch(L, X + m0 * L->F_in, b,
+                                               static_cast<uint8_t*>(Y_dev) + (size_t)m0 * L->F_out * yb, yt, 0u, st);
+            if (s != FASQ_OK) return s;
+            launches += t_launches;
+        }
+        set_launch_count(launches);
+        return FASQ_OK;
+    }
     switch (algo) {
         case FASQ_GEMM_LUT: return gemm_lut_launch(L, X, M, Y_dev, yt, st);
         case FASQ_GEMM_EXPAND_TC:

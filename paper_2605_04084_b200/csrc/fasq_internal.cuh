@@ -61,6 +61,16 @@ struct fasq_layer {
     // pair tensor map.  Derived from cbimg on first use (ensure_cbimg_x).
     uint8_t* cbimg_x = nullptr;
     void* cbmap_x = nullptr;
+    // NEXT-2 packed indices (Eq. 4: ceil(log2 K_s) bits per index).
+    // bits = 0: the uint8 layout above (C <= 256).  bits > 0: `idx` holds
+    // [n_groups][F_out_pad/64][32 subspaces][seg bytes], one segment per (group,
+    // 64-row block, subspace) = the LSB-first bitstream of its 64 rows' codes
+    // (row r at bits [r*bits, r*bits + bits)), seg = 8*bits bytes; rows
+    // [r0, r0 + n) of a group (multiples of 64) are ONE contiguous range.  The
+    // logical table that crosses the ABI is uint8 for C <= 256, uint16 above.
+    int32_t bits = 0;
+    int32_t seg = 0;
+    int32_t idx_w = 1;         // logical index element bytes (1: C <= 256, 2: C <= 1024)
 };
 
 namespace fasq {
@@ -106,10 +116,18 @@ constexpr uint32_t kPairSlot = 65536;
 fasq_status alloc_layer_storage(fasq_layer* L, cudaStream_t st);
 fasq_status ensure_cbimg_x(const fasq_layer* L, cudaStream_t st);   // d = 2 only; synchronises st
 fasq_status count_distinct_centroids(const fasq_layer* L, int64_t* distinct, cudaStream_t st);   // layout.cu   // idx, cbimg, cb and (d <= 2) cbmap
+// idx_logical: uint8 or (L->idx_w == 2) uint16 [N_ss][F_out]
 fasq_status build_physical_from_logical(fasq_layer* L, const __half* cb_logical,
-                                        const uint8_t* idx_logical, cudaStream_t st);
+                                        const void* idx_logical, cudaStream_t st);
 fasq_status build_cbimg(fasq_layer* L, cudaStream_t st);
-fasq_status export_logical(const fasq_layer* L, __half* cb_out, uint8_t* idx_out, cudaStream_t st);
+fasq_status idx16_to_8(const uint16_t* a, uint8_t* b, int64_t n, cudaStream_t st);
+fasq_status export_logical(const fasq_layer* L, __half* cb_out, void* idx_out, cudaStream_t st);
+// packed: 0 = uint8 layout (C <= 256), 1 = ceil(log2 C)-bit packed layout (C <= 1024)
+fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t d, int32_t C, int32_t group,
+                             int32_t packed);
+// NEXT-2: decode GEMV on a packed layer (gemv_packed.cu), B = 1..8
+fasq_status gemv_packed_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt, uint32_t flags,
+                               cudaStream_t st);
 fasq_status copy_rows(const fasq_layer* src, fasq_layer* dst, int32_t row0, cudaStream_t st);
 // Device memory through the library allocator (alloc.cu, fasq_set_allocator).
 fasq_status dev_alloc(void** p, size_t bytes, cudaStream_t st);
@@ -123,8 +141,6 @@ inline fasq_status dev_alloc_t(T** p, size_t bytes, cudaStream_t st) {
     *p = static_cast<T*>(q);
     return s;
 }
-fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
-                             int32_t group);
 
 // ---- compute entry points ---------------------------------------------------
 fasq_status gemv_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt,
@@ -155,7 +171,7 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 PFN_encodeTiled get_encode();
 fasq_status pack_run(const __half* W, fasq_layer* L, const fasq_pack_params* p, cudaStream_t st,
-                     __half* cb_logical_out, uint8_t* idx_logical_out);
+                     __half* cb_logical_out, uint16_t* idx_logical_out);   // uint16 indices for every C
 
 // ---- device helpers -----------------------------------------------------------
 namespace dev {

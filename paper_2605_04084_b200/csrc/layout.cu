@@ -10,10 +10,14 @@
 namespace fasq {
 
 fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
-                             int32_t group) {
-    if (F_out < 1 || F_in < 1 || d < 1 || C < 1 || group < 1) return FASQ_E_ARG;
+                             int32_t group, int32_t packed) {
+    if (F_out < 1 || F_in < 1 || d < 1 || C < 1 || group < 1 || packed < 0 || packed > 1) return FASQ_E_ARG;
     if (d != 1 && d != 2 && d != 4 && d != 8) return FASQ_E_UNSUPPORTED;
-    if (C > 256) return FASQ_E_UNSUPPORTED;
+    if (C > 1024 || (C > 256 && !packed)) return FASQ_E_UNSUPPORTED;
+    // packed layers (NEXT-2): d = 2, the sub-vector size of every Table 2 point
+    // (2-128 ... 2-1024); the GEMV stages one group's codebook image
+    // (C x 32 x 4 B <= 128 KiB) per SMEM slot
+    if (packed && (d != 2 || C < 2)) return FASQ_E_UNSUPPORTED;
     if (F_in % d) return FASQ_E_NONDIVISIBLE;
     int64_t N_ss = F_in / d;
     if (N_ss % group) return FASQ_E_NONDIVISIBLE;
@@ -28,7 +32,16 @@ fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t
     L->F_out_pad = (int32_t)((F_out + kRowBlock - 1) / kRowBlock * kRowBlock);
     L->n_groups = (int32_t)((N_ss + kGroupSubs - 1) / kGroupSubs);
     L->E = entry_bytes(d);
-    L->idx_bytes = (int64_t)L->n_groups * L->F_out_pad * kGroupSubs;
+    L->idx_w = C > 256 ? 2 : 1;
+    if (packed) {
+        int b = 1;
+        while ((1 << b) < C) ++b;   // ceil(log2 C), >= 1
+        L->bits = b;
+        L->seg = 8 * b;             // 64 codes x b bits
+        L->idx_bytes = (int64_t)L->n_groups * (L->F_out_pad / kRowBlock) * kGroupSubs * L->seg;
+    } else {
+        L->idx_bytes = (int64_t)L->n_groups * L->F_out_pad * kGroupSubs;
+    }
     L->cbimg_bytes = (int64_t)L->n_groups * C * kGroupSubs * L->E;
     L->cb_bytes = (int64_t)L->N_cb * C * d * 2;
     return FASQ_OK;
@@ -65,7 +78,7 @@ fasq_status alloc_layer_storage(fasq_layer* L, cudaStream_t st) {
     if (s == FASQ_OK) s = dev_alloc_t(&L->cbimg, (size_t)L->cbimg_bytes, st);
     if (s == FASQ_OK) s = dev_alloc_t(&L->cb, (size_t)L->cb_bytes, st);
     if (s != FASQ_OK) return s;
-    if (L->E == 4) {
+    if (L->E == 4 && L->bits == 0) {
         // codebook PAIR tensor map (the map only depends on the cbimg pointer and
         // shape, so it is encoded now and stays valid for the layer's lifetime)
         s = encode_pair_map(L->cbimg, L, &L->cbmap, st);
@@ -111,6 +124,63 @@ __global__ void k_idx_phys_to_logical(const uint8_t* __restrict__ phys, uint8_t*
     }
 }
 
+// Packed layout (NEXT-2): one thread per (group g, 64-row block, subspace s)
+// segment = the LSB-first bitstream of the 64 rows' codes.  Codes >= C (a
+// caller error) raise *bad.
+template <class IT>
+__global__ void k_idx_logical_to_packed(const IT* __restrict__ idx_log, uint8_t* __restrict__ phys, int F_out,
+                                        int F_out_pad, int N_ss, int n_groups, int C, int bits,
+                                        int* __restrict__ bad) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nblk = F_out_pad / kRowBlock;
+    if (t >= (int64_t)n_groups * nblk * kGroupSubs) return;
+    const int s = (int)(t % kGroupSubs);
+    const int64_t blk = (t / kGroupSubs) % nblk;
+    const int64_t g = t / (kGroupSubs * nblk);
+    const int64_t ss = g * kGroupSubs + s;
+    uint32_t w[20];
+    for (int i = 0; i < 2 * bits; ++i) w[i] = 0u;
+    for (int r = 0; r < kRowBlock; ++r) {
+        const int64_t row = blk * kRowBlock + r;
+        uint32_t v = (ss < N_ss && row < F_out) ? (uint32_t)idx_log[ss * F_out + row] : 0u;
+        if (v >= (uint32_t)C) { atomicOr(bad, 1); v = 0u; }
+        const int p = r * bits;
+        w[p >> 5] |= v << (p & 31);
+        if ((p & 31) + bits > 32) w[(p >> 5) + 1] |= v >> (32 - (p & 31));
+    }
+    uint32_t* dst = reinterpret_cast<uint32_t*>(phys + t * (8 * bits));
+    for (int i = 0; i < 2 * bits; ++i) dst[i] = w[i];
+}
+
+template <class IT>
+__global__ void k_idx_packed_to_logical(const uint8_t* __restrict__ phys, IT* __restrict__ idx_log, int F_out,
+                                        int F_out_pad, int N_ss, int n_groups, int bits) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nblk = F_out_pad / kRowBlock;
+    if (t >= (int64_t)n_groups * nblk * kGroupSubs) return;
+    const int s = (int)(t % kGroupSubs);
+    const int64_t blk = (t / kGroupSubs) % nblk;
+    const int64_t g = t / (kGroupSubs * nblk);
+    const int64_t ss = g * kGroupSubs + s;
+    if (ss >= N_ss) return;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(phys + t * (8 * bits));
+    const uint32_t mask = (1u << bits) - 1u;
+    for (int r = 0; r < kRowBlock; ++r) {
+        const int64_t row = blk * kRowBlock + r;
+        if (row >= F_out) break;
+        const int p = r * bits;
+        uint32_t v = src[p >> 5] >> (p & 31);
+        if ((p & 31) + bits > 32) v |= src[(p >> 5) + 1] << (32 - (p & 31));
+        idx_log[ss * F_out + row] = (IT)(v & mask);
+    }
+}
+
+// uint8 logical -> the byte layout, from a uint16 logical table (GPU pack output)
+__global__ void k_idx16_to_8(const uint16_t* __restrict__ a, uint8_t* __restrict__ b, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = (uint8_t)a[i];
+}
+
 // One thread per (group g, k, lane): entry of E bytes.
 __global__ void k_build_cbimg(const __half* __restrict__ cb, uint8_t* __restrict__ img, int C, int d,
                               int group, int N_ss, int n_groups, int E) {
@@ -150,7 +220,7 @@ fasq_status ensure_cbimg_x(const fasq_layer* Lc, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(mu);
     fasq_layer* L = const_cast<fasq_layer*>(Lc);   // a derived cache; the PQ data stays immutable
     if (L->cbimg_x) return FASQ_OK;
-    if (L->d != 2 || L->E != 4) return FASQ_E_UNSUPPORTED;
+    if (L->d != 2 || L->E != 4 || L->bits) return FASQ_E_UNSUPPORTED;
     uint8_t* img = nullptr;
     fasq_status s = dev_alloc_t(&img, (size_t)L->cbimg_bytes, st);
     if (s != FASQ_OK) return s;
@@ -167,15 +237,47 @@ fasq_status ensure_cbimg_x(const fasq_layer* Lc, cudaStream_t st) {
     return FASQ_OK;
 }
 
-fasq_status build_physical_from_logical(fasq_layer* L, const __half* cb_logical, const uint8_t* idx_logical,
+fasq_status build_physical_from_logical(fasq_layer* L, const __half* cb_logical, const void* idx_logical,
                                         cudaStream_t st) {
     if (cb_logical != L->cb)
         FASQ_CUDA_TRY(cudaMemcpyAsync(L->cb, cb_logical, (size_t)L->cb_bytes, cudaMemcpyDeviceToDevice, st));
-    int64_t n = (int64_t)L->n_groups * (L->F_out_pad / 16) * kGroupSubs;
-    k_idx_logical_to_phys<<<nblk(n, 256), 256, 0, st>>>(idx_logical, L->idx, (int)L->F_out, L->F_out_pad,
-                                                         L->N_ss, L->n_groups);
-    FASQ_CUDA_TRY(cudaGetLastError());
+    if (L->bits == 0) {
+        int64_t n = (int64_t)L->n_groups * (L->F_out_pad / 16) * kGroupSubs;
+        k_idx_logical_to_phys<<<nblk(n, 256), 256, 0, st>>>(static_cast<const uint8_t*>(idx_logical), L->idx,
+                                                             (int)L->F_out, L->F_out_pad, L->N_ss, L->n_groups);
+        FASQ_CUDA_TRY(cudaGetLastError());
+        return build_cbimg(L, st);
+    }
+    // packed (NEXT-2): codes >= C are rejected (checked here, one small D2H)
+    int* bad = nullptr;
+    fasq_status s = dev_alloc_t(&bad, sizeof(int), st);
+    if (s != FASQ_OK) return s;
+    int h = 0;
+    cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(int), st);
+    const int64_t n = (int64_t)L->n_groups * (L->F_out_pad / kRowBlock) * kGroupSubs;
+    if (e == cudaSuccess) {
+        if (L->idx_w == 2)
+            k_idx_logical_to_packed<uint16_t><<<nblk(n, 128), 128, 0, st>>>(
+                static_cast<const uint16_t*>(idx_logical), L->idx, (int)L->F_out, L->F_out_pad, L->N_ss,
+                L->n_groups, L->C, L->bits, bad);
+        else
+            k_idx_logical_to_packed<uint8_t><<<nblk(n, 128), 128, 0, st>>>(
+                static_cast<const uint8_t*>(idx_logical), L->idx, (int)L->F_out, L->F_out_pad, L->N_ss,
+                L->n_groups, L->C, L->bits, bad);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    dev_free(bad, st);
+    if (e != cudaSuccess) return cuda_fail(e, "packed index layout");
+    if (h) { set_error("import: an index is >= C"); return FASQ_E_ARG; }
     return build_cbimg(L, st);
+}
+
+fasq_status idx16_to_8(const uint16_t* a, uint8_t* b, int64_t n, cudaStream_t st) {
+    k_idx16_to_8<<<nblk(n, 256), 256, 0, st>>>(a, b, n);
+    FASQ_CUDA_TRY(cudaGetLastError());
+    return FASQ_OK;
 }
 
 fasq_status build_cbimg(fasq_layer* L, cudaStream_t st) {
@@ -186,9 +288,21 @@ fasq_status build_cbimg(fasq_layer* L, cudaStream_t st) {
     return FASQ_OK;
 }
 
-fasq_status export_logical(const fasq_layer* L, __half* cb_out, uint8_t* idx_out, cudaStream_t st) {
+fasq_status export_logical(const fasq_layer* L, __half* cb_out, void* idx_out_, cudaStream_t st) {
     if (cb_out)
         FASQ_CUDA_TRY(cudaMemcpyAsync(cb_out, L->cb, (size_t)L->cb_bytes, cudaMemcpyDeviceToDevice, st));
+    if (idx_out_ && L->bits) {
+        const int64_t n = (int64_t)L->n_groups * (L->F_out_pad / kRowBlock) * kGroupSubs;
+        if (L->idx_w == 2)
+            k_idx_packed_to_logical<uint16_t><<<nblk(n, 128), 128, 0, st>>>(
+                L->idx, static_cast<uint16_t*>(idx_out_), (int)L->F_out, L->F_out_pad, L->N_ss, L->n_groups, L->bits);
+        else
+            k_idx_packed_to_logical<uint8_t><<<nblk(n, 128), 128, 0, st>>>(
+                L->idx, static_cast<uint8_t*>(idx_out_), (int)L->F_out, L->F_out_pad, L->N_ss, L->n_groups, L->bits);
+        FASQ_CUDA_TRY(cudaGetLastError());
+        return FASQ_OK;
+    }
+    uint8_t* idx_out = static_cast<uint8_t*>(idx_out_);
     if (idx_out) {
         int64_t n = (int64_t)L->n_groups * (L->F_out_pad / 16) * kGroupSubs;
         k_idx_phys_to_logical<<<nblk(n, 256), 256, 0, st>>>(L->idx, idx_out, (int)L->F_out, L->F_out_pad,

@@ -229,7 +229,7 @@ constexpr int kAssignThreads = 256;
 template <int D>
 __global__ void __launch_bounds__(kAssignThreads) k_assign_accum(
     const uint16_t* __restrict__ P, const float* __restrict__ cent, int64_t n, int C, int it,
-    uint8_t* __restrict__ asg, const uint8_t* __restrict__ prev, unsigned long long* __restrict__ S,
+    uint16_t* __restrict__ asg, const uint16_t* __restrict__ prev, unsigned long long* __restrict__ S,
     unsigned long long* __restrict__ cnt, int* __restrict__ changed, const int* __restrict__ done,
     float* __restrict__ bestD) {
     const int g = blockIdx.y;
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kAssignThreads) k_assign_accum(
         float bd;
         const int a = nearest<D>(p, sc, C, &bd);
         if (bestD) bestD[i] = bd;
-        asg[i] = (uint8_t)a;
+        asg[i] = (uint16_t)a;
         if (it > 1 && a != prev[i]) chg = true;
         atomicAdd(&sN[a], 1ull);
 #pragma unroll
@@ -280,7 +280,7 @@ __global__ void k_update(float* __restrict__ cent, unsigned long long* __restric
     const int g = blockIdx.x;
     __shared__ int s_skip;
     __shared__ unsigned long long s_best;
-    __shared__ long long s_taken[256];
+    __shared__ long long s_taken[1024];   // <= C empty clusters (C <= 1024)
     __shared__ int s_ntaken;
     if (threadIdx.x == 0) {
         int sk = done[g];
@@ -346,7 +346,7 @@ __global__ void k_finalize_cb(const float* __restrict__ cent, __half* __restrict
 template <int D>
 __global__ void __launch_bounds__(kAssignThreads) k_final_assign(const uint16_t* __restrict__ P,
                                                                  const __half* __restrict__ cb, int64_t n, int C,
-                                                                 int group, int64_t F_out, uint8_t* __restrict__ idx) {
+                                                                 int group, int64_t F_out, uint16_t* __restrict__ idx) {
     const int g = blockIdx.y;
     extern __shared__ __align__(16) uint8_t sm[];
     float* sc = reinterpret_cast<float*>(sm);
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(kAssignThreads) k_final_assign(const uint16_t*
         for (int e = 0; e < D; ++e) p[e] = __half2float(__ushort_as_half(P[i * D + e]));
         const int a = nearest<D>(p, sc, C);
         const int64_t ss = (int64_t)g * group + t / F_out, j = t % F_out;
-        idx[ss * F_out + j] = (uint8_t)a;
+        idx[ss * F_out + j] = (uint16_t)a;
     }
 }
 
@@ -367,9 +367,9 @@ inline unsigned nb(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
 template <int D>
 fasq_status lloyd_and_finalize(const uint16_t* P, float* cent, int64_t n, int N_cb, int C, int group,
-                               int64_t F_out, int iters, uint8_t* asg0, uint8_t* asg1, unsigned long long* S,
+                               int64_t F_out, int iters, uint16_t* asg0, uint16_t* asg1, unsigned long long* S,
                                unsigned long long* cnt, int* changed, int* done, int* iters_run, __half* cb_out,
-                               uint8_t* idx_out, cudaStream_t st, float* bestD, u128* ppdist, uint64_t seed) {
+                               uint16_t* idx_out, cudaStream_t st, float* bestD, u128* ppdist, uint64_t seed) {
     if (ppdist) {   // k-means++ init replaces the distinct-sample init (reading R17)
         k_kmeanspp<D><<<N_cb, kPPThreads, 0, st>>>(P, n, C, seed, ppdist, cent);
         FASQ_CUDA_TRY(cudaGetLastError());
@@ -379,8 +379,8 @@ fasq_status lloyd_and_finalize(const uint16_t* P, float* cent, int64_t n, int N_
     const int chunks = (int)std::min<int64_t>((n + kAssignThreads - 1) / kAssignThreads, 64);
     dim3 grid(chunks, N_cb);
     for (int it = 1; it <= iters; ++it) {
-        uint8_t* cur = (it & 1) ? asg1 : asg0;
-        uint8_t* prv = (it & 1) ? asg0 : asg1;
+        uint16_t* cur = (it & 1) ? asg1 : asg0;
+        uint16_t* prv = (it & 1) ? asg0 : asg1;
         k_assign_accum<D><<<grid, kAssignThreads, smem, st>>>(P, cent, n, C, it, cur, prv, S, cnt, changed, done,
                                                               bestD);
         FASQ_CUDA_TRY(cudaGetLastError());
@@ -414,7 +414,7 @@ struct Scratch {
 }  // namespace
 
 fasq_status pack_run(const __half* W_, fasq_layer* L, const fasq_pack_params* prm, cudaStream_t st,
-                     __half* cb_out, uint8_t* idx_out) {
+                     __half* cb_out, uint16_t* idx_out) {
     const uint16_t* W = reinterpret_cast<const uint16_t*>(W_);
     const int d = L->d, C = L->C, group = L->group, N_cb = L->N_cb;
     const int64_t F_out = L->F_out, F_in = L->F_in;
@@ -444,8 +444,8 @@ fasq_status pack_run(const __half* W_, fasq_layer* L, const fasq_pack_params* pr
     int* uflag = sc.get<int>(total);
     int* pos = sc.get<int>(total);
     float* cent = sc.get<float>((size_t)N_cb * C * d);
-    uint8_t* asg0 = sc.get<uint8_t>(total);
-    uint8_t* asg1 = sc.get<uint8_t>(total);
+    uint16_t* asg0 = sc.get<uint16_t>(total);
+    uint16_t* asg1 = sc.get<uint16_t>(total);
     unsigned long long* S = sc.get<unsigned long long>((size_t)N_cb * C * d);
     unsigned long long* cnt = sc.get<unsigned long long>((size_t)N_cb * C);
     int* changed = sc.get<int>(N_cb);

@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol(fasq):
 
 
 def test_status_strings_and_version(fasq):
-    assert fasq.lib.fasq_abi_version() == 3
+    assert fasq.lib.fasq_abi_version() == 4
     for code in (0, -1, -2, -3, -4, -5, -6, -7, -8, -9):
         s = fasq.lib.fasq_status_string(code).decode()
         assert s.startswith("FASQ_"), s
@@ -48,6 +48,7 @@ def test_argument_errors_are_synchronous(fasq):
     out = ctypes.c_void_p()
     # NULL pointers -> FASQ_E_ARG before touching any device
     assert fasq.lib.fasq_import(None, None, 8, 8, 2, 4, 1, None, ctypes.byref(out)) == -1
+    assert fasq.lib.fasq_import_packed(None, None, 8, 8, 2, 4, 1, 1, None, ctypes.byref(out)) == -1
     assert fasq.lib.fasq_gemv(None, None, 1, None, 0, None) == -1
     assert fasq.lib.fasq_gemm(None, None, 1, None, 0, 0, None) == -1
     assert fasq.lib.fasq_export(None, None, None, None) == -1
