@@ -817,6 +817,24 @@ def decode_sweep(peak, settings=((2, 256), (2, 128), (4, 256), (1, 256), (2, 64)
     return out
 
 
+def packed_gemv_side(peak):
+    """NEXT-2 (Eq. 4): per-launch decode GEMV (B = 1, CUDA graph of
+    launches over > L2 of replicas) with byte indices vs ceil(log2 C)-bit
+    packed indices on the Llama-3-8B shapes; bytes = Eq. 4 index bits +
+    codebooks + x + y."""
+    from tools.packed_time import run
+    out = {}
+    for tag, C, packed in (("d2_C256_u8", 256, False), ("d2_C128_u8", 128, False), ("d2_C128_p7", 128, True),
+                           ("d2_C512_p9", 512, True), ("d2_C1024_p10", 1024, True)):
+        per = {}
+        for (o, i) in ((4096, 4096), (14336, 4096), (4096, 14336)):
+            r = run(o, i, C, packed, iters=100)
+            per["%dx%d" % (o, i)] = {"us": r["us"], "bytes": r["bytes"], "GBps": r["GBps"],
+                                     "frac": round(r["GBps"] / peak, 3)}
+        out[tag] = per
+    return out
+
+
 def pack_time():
     """GPU k-means pack (Alg. 1, 25 Lloyd rounds, d=2, C=256) of one seeded
     layer of each Llama-3-8B shape, and the whole-model estimate (x 32 blocks);
@@ -1012,7 +1030,8 @@ def main():
                          ("decode_sweep", lambda: decode_sweep(peak)),
                          ("decode_batch", lambda: decode_batch(peak)),
                          ("prefill_model", lambda: prefill_model(float(peaks.get("bf16_tflops", 1692.0)))),
-                         ("gpu_pack", pack_time)):
+                         ("gpu_pack", pack_time),
+                         ("packed_gemv", lambda: packed_gemv_side(peak))):
             try:
                 side[name] = fn()
             except Exception as e:  # report, never hide
