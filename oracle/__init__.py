@@ -55,6 +55,10 @@ def lib() -> ctypes.CDLL:
         L.fasq_ref_pack16_range_ex.argtypes = [vp, i64, i64, i32, i32, i32, u64, i32, i32, i32, i64, i64, vp, vp,
                                                vp]
         L.fasq_ref_reconstruct16.argtypes = [vp, vp, i64, i64, i32, i32, i32, vp]
+        L.fasq_ref_pack_dim0_range.argtypes = [vp, i64, i64, i32, i32, i32, u64, i32, i32, i32, i64, i64, vp,
+                                               vp, vp]
+        L.fasq_ref_reconstruct_dim0.argtypes = [vp, vp, i64, i64, i32, i32, i32, vp]
+        L.fasq_ref_gemm_rows_dim0.argtypes = [vp, vp, i64, i64, i32, i32, i32, vp, i64, i64, i64, vp]
         L.fasq_ref_gemm_rows16.argtypes = [vp, vp, i64, i64, i32, i32, i32, vp, i64, i64, i64, vp]
         L.fasq_ref_pack_range.argtypes = [vp, i64, i64, i32, i32, i32, u64, i32, i64, i64, vp, vp, vp]
         L.fasq_ref_pack.argtypes = [vp, i64, i64, i32, i32, i32, u64, i32, vp, vp, vp]
@@ -150,6 +154,61 @@ def pack(W, d: int, C: int, group: int = 1, seed: int = 0, iters: int = 25,
     if st:
         raise OracleError(st)
     return cb.view(np.float16), idx, its
+
+
+def pack_dim0(W, d: int, C: int, group: int = 1, seed: int = 0, iters: int = 25, init: int = 0, empty: int = 0):
+    """The paper's dim = 0 partition (Eq. 2 first case; its experiments):
+    subspaces along the OUTPUT axis.  Returns (codebooks fp16 [N_cb][C][d], indices
+    uint8 [N_ss = F_out/d][F_in], iters_run)."""
+    Wb = _bits16(W)
+    F_out, F_in = Wb.shape
+    st = validate(F_in, F_out, d, C, group)          # dim = 0 is dim = 1 of W^T
+    if st:
+        raise OracleError(st)
+    N_ss = F_out // d
+    N_cb = N_ss // group
+    cb = np.zeros((N_cb, C, d), np.uint16)
+    idx = np.zeros((N_ss, F_in), np.uint8)
+    its = np.zeros((N_cb,), np.int32)
+    st = lib().fasq_ref_pack_dim0_range(_ptr(Wb), F_out, F_in, d, C, group, seed & (2**64 - 1), iters, init,
+                                        empty, 0, N_cb, _ptr(cb), _ptr(idx), _ptr(its))
+    if st:
+        raise OracleError(st)
+    return cb.view(np.float16), idx, its
+
+
+def reconstruct_dim0(codebooks, indices, F_out: int, group: int = 1) -> np.ndarray:
+    """dim = 0 reconstruction: W_hat[ss*d+e][j] = T_cluster[ss/group][T_index[ss][j]][e]."""
+    cb = _bits16(codebooks)
+    idx = np.ascontiguousarray(indices, dtype=np.uint8)
+    N_cb, C, d = cb.shape
+    N_ss, F_in = idx.shape
+    out = np.zeros((F_out, F_in), np.uint16)
+    st = lib().fasq_ref_reconstruct_dim0(_ptr(cb), _ptr(idx), F_out, F_in, d, C, group, _ptr(out))
+    if st:
+        raise OracleError(st)
+    return out.view(np.float16)
+
+
+def gemm_dim0(codebooks, indices, X, group: int = 1, rows=None) -> np.ndarray:
+    """y = W_hat . x in fp64 with the dim = 0 reconstruction (F_out = N_ss * d)."""
+    cb = _bits16(codebooks)
+    idx = np.ascontiguousarray(indices, dtype=np.uint8)
+    Xb = _bits16(X)
+    if Xb.ndim == 1:
+        Xb = Xb[None, :]
+    Xb = np.ascontiguousarray(Xb)
+    N_cb, C, d = cb.shape
+    N_ss, F_in = idx.shape
+    F_out = N_ss * d
+    M = Xb.shape[0]
+    j0, j1 = (0, F_out) if rows is None else rows
+    Y = np.zeros((M, j1 - j0), np.float64)
+    st = lib().fasq_ref_gemm_rows_dim0(_ptr(cb), _ptr(idx), F_out, F_in, d, C, group, _ptr(Xb), M, j0, j1,
+                                       _ptr(Y))
+    if st:
+        raise OracleError(st)
+    return Y
 
 
 def lloyd_fp32(W, d: int, C: int, group: int, seed: int, iters: int, g: int):

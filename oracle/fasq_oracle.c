@@ -23,6 +23,10 @@
  *                         ceil(log2 K_s)-bit indices; 2-512 /
  *                         2-1024 in Table 2); fasq_ref_index_bits
  *                         = ceil(log2 K_s).
+ *   fasq_ref_pack_dim0_range / _reconstruct_dim0 / _gemm_rows_dim0   the
+ *                         paper's dim = 0 partition (Eq. 2 first case; the
+ *                         layout of its experiments): subspaces along
+ *                         the OUTPUT axis, T_index [N_ss = F_out/d][F_in].
  *   fasq_ref_reconstruct  the naive reconstruction: W_hat[j][ss*d+e]
  *                         = T_cluster[cb(ss)][T_index[ss][j]][e].
  *   fasq_ref_gemm_rows    y[b][j] = sum_ss sum_e fp64(W_hat[j][ss*d+e]) *
@@ -487,6 +491,82 @@ int fasq_ref_pack(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t d, int
     int64_t N_cb = (F_in / d) / group;
     return fasq_ref_pack_range(W, F_out, F_in, d, C, group, seed, iters, 0, N_cb, codebooks,
                                indices, iters_run);
+}
+
+/* ------------------------------------------------------------------------ */
+/* dim = 0: subspaces along the OUTPUT axis (Eq. 2 first case;   */
+/* the layout of the paper's experiments, P:444 -- NEXT-4)                  */
+/* ------------------------------------------------------------------------ */
+/* W in R^{F_out x F_in}; subspace ss = output rows [ss*d, ss*d + d), N_ss =
+ * F_out/d; the datapoints are the F_in columns: point (ss, j) = (W[ss*d+0][j],
+ * ..., W[ss*d+d-1][j]); T_index is [N_ss][F_in].  This is exactly the dim = 1
+ * partition of W^T (its rows are W's columns), so the pack runs Alg. 1 on
+ * the transposed matrix with the same arithmetic: point t = s*F_in + j of
+ * codebook g is W^T[j, ss*d : ss*d+d] = W[ss*d : ss*d+d, j]. */
+int fasq_ref_pack_dim0_range(const uint16_t* W, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
+                             int32_t group, uint64_t seed, int32_t iters, int32_t init_mode, int32_t empty_mode,
+                             int64_t g0, int64_t g1, uint16_t* codebooks, uint8_t* indices, int32_t* iters_run) {
+    if (!W || !indices || F_out < 1 || F_in < 1) return REF_E_ARG;
+    uint16_t* WT = (uint16_t*)malloc((size_t)F_out * F_in * sizeof(uint16_t));
+    if (!WT) return REF_E_OOM;
+    for (int64_t o = 0; o < F_out; ++o)
+        for (int64_t j = 0; j < F_in; ++j) WT[j * F_out + o] = W[o * F_in + j];
+    int st = pack_range_impl(WT, F_in, F_out, d, C, group, seed, iters, init_mode, empty_mode, g0, g1, codebooks,
+                             indices, NULL, iters_run);
+    free(WT);
+    return st;
+}
+
+/* W_hat[ss*d+e][j] = codebooks[ss/group][indices[ss][j]][e]  (fp16 bits), dim = 0 */
+int fasq_ref_reconstruct_dim0(const uint16_t* codebooks, const uint8_t* indices, int64_t F_out, int64_t F_in,
+                              int32_t d, int32_t C, int32_t group, uint16_t* W_hat) {
+    if (F_out < 1 || F_in < 1 || d < 1 || C < 1 || group < 1) return REF_E_ARG;
+    if (F_out % d) return REF_E_NONDIVISIBLE;
+    int64_t N_ss = F_out / d;
+    if (N_ss % group) return REF_E_NONDIVISIBLE;
+    for (int64_t ss = 0; ss < N_ss; ++ss)
+        for (int64_t j = 0; j < F_in; ++j) {
+            int64_t k = indices[ss * F_in + j];
+            if (k >= C) return REF_E_ARG;
+            for (int e = 0; e < d; ++e)
+                W_hat[(ss * d + e) * F_in + j] = codebooks[((ss / group) * C + k) * d + e];
+        }
+    return REF_OK;
+}
+
+/* Y[b][r] = sum over i ascending of fp64(W_hat[j0+r][i]) * fp64(X[b][i]) with
+ * W_hat the dim = 0 reconstruction: the plain definition y = W_hat . x. */
+int fasq_ref_gemm_rows_dim0(const uint16_t* codebooks, const uint8_t* indices, int64_t F_out, int64_t F_in,
+                            int32_t d, int32_t C, int32_t group, const uint16_t* X, int64_t M, int64_t j0,
+                            int64_t j1, double* Y) {
+    if (F_out < 1 || F_in < 1 || d < 1 || C < 1 || group < 1 || M < 0) return REF_E_ARG;
+    if (F_out % d) return REF_E_NONDIVISIBLE;
+    if ((F_out / d) % group) return REF_E_NONDIVISIBLE;
+    if (j0 < 0 || j1 > F_out || j0 > j1) return REF_E_ARG;
+    int64_t R = j1 - j0;
+    double* Wr = (double*)malloc((size_t)(R > 0 ? R : 1) * F_in * sizeof(double));
+    double* Xd = (double*)malloc((size_t)(M > 0 ? M : 1) * F_in * sizeof(double));
+    if (!Wr || !Xd) { free(Wr); free(Xd); return REF_E_OOM; }
+    int bad = 0;
+    for (int64_t r = 0; r < R; ++r) {
+        const int64_t o = j0 + r, ss = o / d, e = o % d;
+        for (int64_t i = 0; i < F_in; ++i) {
+            int64_t k = indices[ss * F_in + i];
+            if (k >= C) { bad = 1; k = 0; }
+            Wr[r * F_in + i] = (double)fasq_ref_f16_to_f32(codebooks[((ss / group) * C + k) * d + e]);
+        }
+    }
+    for (int64_t q = 0; q < M * F_in; ++q) Xd[q] = (double)fasq_ref_f16_to_f32(X[q]);
+    if (bad) { free(Wr); free(Xd); return REF_E_ARG; }
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t b = 0; b < M; ++b)
+        for (int64_t r = 0; r < R; ++r) {
+            double acc = 0.0;
+            for (int64_t i = 0; i < F_in; ++i) acc = acc + Wr[r * F_in + i] * Xd[b * F_in + i];
+            Y[b * R + r] = acc;
+        }
+    free(Wr); free(Xd);
+    return REF_OK;
 }
 
 /* Test hook: init + Lloyd for codebook g only, WITHOUT finalisation.
