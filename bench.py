@@ -835,6 +835,21 @@ def packed_gemv_side(peak):
     return out
 
 
+def dim0_gemv_side(peak):
+    """NEXT-4: per-launch decode GEMV on the paper's dim = 0 layout (output-axis
+    subspaces) next to Eq. 3's input-axis layout, d = 2, C = 256, B = 1 / 8."""
+    from tools.dim0_time import run
+    out = {}
+    for B in (1, 8):
+        for dim0 in (False, True):
+            per = {}
+            for (o, i) in ((4096, 4096), (14336, 4096), (4096, 14336), (1024, 4096)):
+                r = run(o, i, dim0, B=B, iters=100)
+                per["%dx%d" % (o, i)] = {"us": r["us"], "GBps": r["GBps"], "frac": round(r["GBps"] / peak, 3)}
+            out["%s_B%d" % ("dim0" if dim0 else "dim1", B)] = per
+    return out
+
+
 def pack_time():
     """GPU k-means pack (Alg. 1, 25 Lloyd rounds, d=2, C=256) of one seeded
     layer of each Llama-3-8B shape, and the whole-model estimate (x 32 blocks);
@@ -1031,7 +1046,8 @@ def main():
                          ("decode_batch", lambda: decode_batch(peak)),
                          ("prefill_model", lambda: prefill_model(float(peaks.get("bf16_tflops", 1692.0)))),
                          ("gpu_pack", pack_time),
-                         ("packed_gemv", lambda: packed_gemv_side(peak))):
+                         ("packed_gemv", lambda: packed_gemv_side(peak)),
+                         ("dim0_gemv", lambda: dim0_gemv_side(peak))):
             try:
                 side[name] = fn()
             except Exception as e:  # report, never hide

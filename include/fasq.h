@@ -105,12 +105,26 @@ typedef struct {
                          k-means++ (reading R17)                      */
     int32_t empty;    /* 0: an empty cluster keeps its centroid (R5); 1: reseed it
                          from the farthest point (reading R18)        */
-    int32_t packed;   /* NEXT-2 (Eq. 4): 1 = store ceil(log2 C)-bit
-                         packed indices (d = 2 only); 0 = uint8 indices.  Forced
-                         to 1 for C > 256.  Packed layers run fasq_gemv (B <=
-                         8) and fasq_gemm (as 8-token GEMV slices); the decode
-                         chain and fasq_llama_* reject them.                      */
+    uint32_t layout;  /* FASQ_LAYOUT_* bits (0 = Eq. 3's input-axis subspaces,
+                         uint8 indices).  FASQ_LAYOUT_PACKED is forced for
+                         C > 256.                                                 */
 } fasq_pack_params;
+
+/* Layout flags (fasq_pack_params.layout, fasq_import_ex).  Layers with either
+ * flag run fasq_gemv / fasq_gemv_ex / fasq_gemv_host (B <= 8), a one-layer
+ * fasq_gemv_grouped, and fasq_gemm (FASQ_GEMM_AUTO, as 8-token GEMV slices);
+ * the decode chain, fasq_llama_* and (FASQ_LAYOUT_DIM0) fasq_shard_rows
+ * return FASQ_E_UNSUPPORTED for them. */
+#define FASQ_LAYOUT_PACKED 1u   /* NEXT-2 (Eq. 4): ceil(log2 C)-bit packed
+                                   indices, d = 2, C = 2..1024 (Table 2's 2-128 ...
+                                   2-1024)                                  */
+#define FASQ_LAYOUT_DIM0 2u     /* NEXT-4: the paper's dim = 0 partition (Eq. 2 first
+                                   case P:174-186; its experiments): subspace
+                                   ss = OUTPUT rows [ss*d, ss*d+d), N_ss = F_out/d,
+                                   indices [N_ss][F_in] (the datapoints are W's
+                                   columns), y[ss*d+e] = sum_j x[j] *
+                                   T_cluster[ss/group][T_index[ss][j]][e].  uint8
+                                   indices (C <= 256); not combinable with PACKED.     */
 
 typedef struct fasq_layer fasq_layer; /* opaque */
 
@@ -125,6 +139,7 @@ typedef struct {
     double eff_bits_W;           /* paper #W = ceil(log2 C)/d             */
     int32_t index_bits;          /* stored bits per index: 8 (uint8 layout) or
                                     ceil(log2 C) (packed, NEXT-2)                 */
+    uint32_t layout;             /* FASQ_LAYOUT_* bits of the layer               */
 } fasq_layer_info;
 
 /* ---- creation --------------------------------------------------------- */
@@ -146,14 +161,14 @@ fasq_status fasq_import(const void* codebooks_dev, const void* indices_dev,
                         int64_t F_out, int64_t F_in, int32_t d, int32_t C, int32_t group,
                         void* stream, fasq_layer** out);
 
-/* NEXT-2 (Eq. 4): the same with the index storage chosen by the
- * caller: packed = 1 stores ceil(log2 C) bits per index (d = 2, C in 2..1024;
- * e.g. 7 bits for Table 2's 2-128), packed = 0 uint8 (C <= 256).  For a
- * packed layer indices >= C return FASQ_E_ARG (checked on the device; this
- * call synchronises `stream`). */
-fasq_status fasq_import_packed(const void* codebooks_dev, const void* indices_dev,
-                               int64_t F_out, int64_t F_in, int32_t d, int32_t C, int32_t group,
-                               int32_t packed, void* stream, fasq_layer** out);
+/* The same with a chosen layout (FASQ_LAYOUT_* bits): FASQ_LAYOUT_PACKED stores
+ * ceil(log2 C) bits per index (NEXT-2, e.g. 7 bits for Table 2's 2-128,
+ * P:496); FASQ_LAYOUT_DIM0 reads indices_dev as [F_out/d][F_in] (the dim = 0
+ * partition, NEXT-4).  For a packed layer indices >= C return FASQ_E_ARG
+ * (checked on the device; the call then synchronises `stream`). */
+fasq_status fasq_import_ex(const void* codebooks_dev, const void* indices_dev,
+                           int64_t F_out, int64_t F_in, int32_t d, int32_t C, int32_t group,
+                           uint32_t layout, void* stream, fasq_layer** out);
 
 /* Writes the layer's logical codebooks / indices to device buffers of
  * N_cb*C*d fp16 and N_ss*F_out uint8 (uint16 when C > 256) elements (either

@@ -30,7 +30,7 @@ _STATUS = {0: "FASQ_OK", -1: "FASQ_E_ARG", -2: "FASQ_E_NONDIVISIBLE", -3: "FASQ_
            -8: "FASQ_E_OOM", -9: "FASQ_E_RANGE"}
 
 # Every symbol include/fasq.h declares (checked by tests/test_abi.py).
-EXPORTED = ["fasq_pack", "fasq_import", "fasq_import_packed", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
+EXPORTED = ["fasq_pack", "fasq_import", "fasq_import_ex", "fasq_export", "fasq_shard_rows", "fasq_layer_info_get",
             "fasq_free", "fasq_gemv", "fasq_gemv_ex", "fasq_gemv_grouped", "fasq_acc_convert",
             "fasq_chain_create", "fasq_chain_create_tp", "fasq_chain_ipc_handle", "fasq_chain_set_peers",
             "fasq_chain_set_peer_chains", "fasq_chain_run", "fasq_chain_output", "fasq_chain_trace",
@@ -44,6 +44,10 @@ EXPORTED = ["fasq_pack", "fasq_import", "fasq_import_packed", "fasq_export", "fa
             "fasq_abi_version", "fasq_set_allocator", "fasq_layer_distinct_centroids"]
 
 
+LAYOUT_PACKED = 1   # FASQ_LAYOUT_PACKED: ceil(log2 C)-bit indices (NEXT-2)
+LAYOUT_DIM0 = 2     # FASQ_LAYOUT_DIM0: output-axis subspaces (NEXT-4)
+
+
 class FasqError(RuntimeError):
     def __init__(self, code: int, msg: str = ""):
         super().__init__("%s (%d)%s" % (_STATUS.get(code, "?"), code, (": " + msg) if msg else ""))
@@ -53,7 +57,7 @@ class FasqError(RuntimeError):
 class _PackParams(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int32), ("C", ctypes.c_int32), ("group", ctypes.c_int32),
                 ("iters", ctypes.c_int32), ("seed", ctypes.c_uint64), ("init", ctypes.c_int32),
-                ("empty", ctypes.c_int32), ("packed", ctypes.c_int32)]
+                ("empty", ctypes.c_int32), ("layout", ctypes.c_uint32)]
 
 
 class GemvOpts(ctypes.Structure):
@@ -86,7 +90,7 @@ class LayerInfo(ctypes.Structure):
                 ("N_cb", ctypes.c_int32), ("row_offset", ctypes.c_int32),
                 ("index_bytes", ctypes.c_int64), ("codebook_bytes", ctypes.c_int64),
                 ("device_bytes", ctypes.c_int64), ("bits_per_weight", ctypes.c_double),
-                ("eff_bits_W", ctypes.c_double), ("index_bits", ctypes.c_int32)]
+                ("eff_bits_W", ctypes.c_double), ("index_bits", ctypes.c_int32), ("layout", ctypes.c_uint32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -101,7 +105,7 @@ def _load():
     pp = ctypes.POINTER(ctypes.c_void_p)
     L.fasq_pack.argtypes = [vp, i64, i64, ctypes.POINTER(_PackParams), vp, pp]
     L.fasq_import.argtypes = [vp, vp, i64, i64, i32, i32, i32, vp, pp]
-    L.fasq_import_packed.argtypes = [vp, vp, i64, i64, i32, i32, i32, i32, vp, pp]
+    L.fasq_import_ex.argtypes = [vp, vp, i64, i64, i32, i32, i32, u32, vp, pp]
     L.fasq_export.argtypes = [vp, vp, vp, vp]
     L.fasq_shard_rows.argtypes = [vp, i32, i32, vp, pp]
     L.fasq_layer_info_get.argtypes = [vp, ctypes.POINTER(LayerInfo)]
@@ -213,6 +217,8 @@ class Layer:
         self.d, self.C, self.group = inf.d, inf.C, inf.group
         self.N_ss, self.N_cb = inf.N_ss, inf.N_cb
         self.index_bits = inf.index_bits   # 8, or ceil(log2 C) for a packed layer (NEXT-2)
+        self.layout = inf.layout           # FASQ_LAYOUT_* bits
+        self.dim0 = bool(inf.layout & LAYOUT_DIM0)
 
     @property
     def handle(self):
@@ -234,8 +240,8 @@ class Layer:
         """Logical arrays: (codebooks fp16 [N_cb][C][d], indices [N_ss][F_out] uint8, or
         int16 holding the uint16 values when C > 256)."""
         cb = torch.empty((self.N_cb, self.C, self.d), dtype=torch.float16, device="cuda")
-        idx = torch.empty((self.N_ss, self.F_out), dtype=torch.uint8 if self.C <= 256 else torch.int16,
-                          device="cuda")
+        idx = torch.empty((self.N_ss, self.F_in if self.dim0 else self.F_out),
+                          dtype=torch.uint8 if self.C <= 256 else torch.int16, device="cuda")
         _check(lib.fasq_export(self._h, cb.data_ptr(), idx.data_ptr(), _stream(stream)))
         return cb, idx
 
@@ -253,11 +259,14 @@ class Layer:
 
 
 def pack(W: torch.Tensor, d: int, C: int, group: int = 1, seed: int = 0, iters: int = 25,
-         stream=None, init: int = 0, empty: int = 0, packed: bool = False) -> Layer:
+         stream=None, init: int = 0, empty: int = 0, packed: bool = False, dim0: bool = False) -> Layer:
     """Alg. 1 on the GPU: k-means per codebook -> Layer.  ``packed``
-    (implied for C > 256): ceil(log2 C)-bit packed index storage (Eq. 4, NEXT-2)."""
+    (implied for C > 256): ceil(log2 C)-bit packed index storage (Eq. 4, NEXT-2).
+    ``dim0``: the paper's dim = 0 partition (subspaces along the output axis,
+    P:444; NEXT-4)."""
     W = _cuda(W, torch.float16, "W")
-    prm = _PackParams(d, C, group, iters, seed & (2**64 - 1), init, empty, 1 if packed else 0)
+    prm = _PackParams(d, C, group, iters, seed & (2**64 - 1), init, empty,
+                      (LAYOUT_PACKED if packed else 0) | (LAYOUT_DIM0 if dim0 else 0))
     out = ctypes.c_void_p()
     _check(lib.fasq_pack(W.data_ptr(), W.shape[0], W.shape[1], ctypes.byref(prm), _stream(stream),
                          ctypes.byref(out)))
@@ -265,22 +274,30 @@ def pack(W: torch.Tensor, d: int, C: int, group: int = 1, seed: int = 0, iters: 
 
 
 def import_layer(codebooks: torch.Tensor, indices: torch.Tensor, F_in: int, group: int = 1,
-                 stream=None, packed: bool | None = None) -> Layer:
+                 stream=None, packed: bool | None = None, dim0: bool = False) -> Layer:
     """Layer from logical codebooks fp16 [N_cb][C][d] + indices [N_ss][F_out]
     (uint8 for C <= 256, int16/uint16 bits above).  ``packed`` (default: C > 256)
-    stores ceil(log2 C)-bit indices (Eq. 4, NEXT-2)."""
+    stores ceil(log2 C)-bit indices (Eq. 4, NEXT-2).  ``dim0``: indices are
+    [N_ss = F_out/d][F_in] of the paper's dim = 0 partition (NEXT-4)."""
     cb = _cuda(codebooks, torch.float16, "codebooks")
     N_cb, C, d = cb.shape
     wide = C > 256
     if isinstance(indices, torch.Tensor) and indices.dtype in (torch.int16, torch.uint16):
         indices = indices.view(torch.int16)
     idx = _cuda(indices, torch.int16 if wide else torch.uint8, "indices")
-    N_ss, F_out = idx.shape
+    if dim0:
+        N_ss, F_in_idx = idx.shape
+        if F_in_idx != F_in:
+            raise FasqError(-5, "dim0 indices must be [F_out/d][F_in]")
+        F_out = N_ss * d
+    else:
+        N_ss, F_out = idx.shape
     if packed is None:
         packed = wide
+    layout = (LAYOUT_PACKED if packed else 0) | (LAYOUT_DIM0 if dim0 else 0)
     out = ctypes.c_void_p()
-    _check(lib.fasq_import_packed(cb.data_ptr(), idx.data_ptr(), F_out, F_in, d, C, group, 1 if packed else 0,
-                                  _stream(stream), ctypes.byref(out)))
+    _check(lib.fasq_import_ex(cb.data_ptr(), idx.data_ptr(), F_out, F_in, d, C, group, layout,
+                              _stream(stream), ctypes.byref(out)))
     return Layer(out.value)
 
 

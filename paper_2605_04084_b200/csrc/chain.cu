@@ -205,8 +205,8 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
     if (B < 1 || B > 8) return FASQ_E_UNSUPPORTED;
     for (const StepDesc& sd : steps)
         for (const fasq_layer* L : sd.layers)
-            if (L && L->bits) {   // NEXT-2 packed indices: per-launch fasq_gemv only
-                set_error("chain: packed-index layers run through fasq_gemv, not the decode chain");
+            if (L && (L->bits || L->dim0)) {   // NEXT-2 packed / NEXT-4 dim = 0: per-launch fasq_gemv only
+                set_error("chain: packed-index and dim = 0 layers run through fasq_gemv, not the decode chain");
                 return FASQ_E_UNSUPPORTED;
             }
     const int NB = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;

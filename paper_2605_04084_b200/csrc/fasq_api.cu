@@ -71,13 +71,13 @@ const char* fasq_status_string(fasq_status s) {
 const char* fasq_last_error_message(void) { return t_err.c_str(); }
 int32_t fasq_last_launch_count(void) { return t_launches; }
 
-fasq_status fasq_import_packed(const void* codebooks_dev, const void* indices_dev, int64_t F_out, int64_t F_in,
-                               int32_t d, int32_t C, int32_t group, int32_t packed, void* stream, fasq_layer** out) {
+fasq_status fasq_import_ex(const void* codebooks_dev, const void* indices_dev, int64_t F_out, int64_t F_in,
+                           int32_t d, int32_t C, int32_t group, uint32_t layout, void* stream, fasq_layer** out) {
     if (!out) return FASQ_E_ARG;
     *out = nullptr;
     if (!codebooks_dev || !indices_dev) return FASQ_E_ARG;
     fasq_layer* L = new fasq_layer();
-    fasq_status s = init_layer_shape(L, F_out, F_in, d, C, group, packed);
+    fasq_status s = init_layer_shape(L, F_out, F_in, d, C, group, layout);
     if (s == FASQ_OK) s = check_device();
     if (s == FASQ_OK) s = alloc_layer_storage(L, (cudaStream_t)stream);
     if (s == FASQ_OK)
@@ -91,7 +91,8 @@ fasq_status fasq_import_packed(const void* codebooks_dev, const void* indices_de
 
 fasq_status fasq_import(const void* codebooks_dev, const void* indices_dev, int64_t F_out, int64_t F_in,
                         int32_t d, int32_t C, int32_t group, void* stream, fasq_layer** out) {
-    return fasq_import_packed(codebooks_dev, indices_dev, F_out, F_in, d, C, group, C > 256 ? 1 : 0, stream, out);
+    return fasq_import_ex(codebooks_dev, indices_dev, F_out, F_in, d, C, group, C > 256 ? FASQ_LAYOUT_PACKED : 0u,
+                          stream, out);
 }
 
 fasq_status fasq_pack(const void* W_dev, int64_t F_out, int64_t F_in, const fasq_pack_params* prm,
@@ -100,20 +101,38 @@ fasq_status fasq_pack(const void* W_dev, int64_t F_out, int64_t F_in, const fasq
     *out = nullptr;
     if (!W_dev || !prm) return FASQ_E_ARG;
     if (prm->iters < 0 || prm->init < 0 || prm->init > 1 || prm->empty < 0 || prm->empty > 1) return FASQ_E_ARG;
-    if (prm->packed < 0 || prm->packed > 1) return FASQ_E_ARG;
     fasq_layer* L = new fasq_layer();
-    fasq_status s = init_layer_shape(L, F_out, F_in, prm->d, prm->C, prm->group,
-                                     (prm->packed || prm->C > 256) ? 1 : 0);
-    if (s == FASQ_OK && (int64_t)prm->C > (int64_t)prm->group * F_out) s = FASQ_E_CLUSTER_OVERFLOW;
-    if (s == FASQ_OK && (int64_t)prm->group * F_out > (1ll << 23)) s = FASQ_E_UNSUPPORTED;
+    const uint32_t layout = prm->layout | (prm->C > 256 ? FASQ_LAYOUT_PACKED : 0u);
+    fasq_status s = init_layer_shape(L, F_out, F_in, prm->d, prm->C, prm->group, layout);
+    // points per codebook: group x (datapoints = F_out rows, or F_in columns for dim = 0)
+    const int64_t n_dp = L->dim0 ? F_in : F_out;
+    if (s == FASQ_OK && (int64_t)prm->C > (int64_t)prm->group * n_dp) s = FASQ_E_CLUSTER_OVERFLOW;
+    if (s == FASQ_OK && (int64_t)prm->group * n_dp > (1ll << 23)) s = FASQ_E_UNSUPPORTED;
     if (s == FASQ_OK) s = check_device();
     cudaStream_t st = (cudaStream_t)stream;
     if (s == FASQ_OK) s = alloc_layer_storage(L, st);
     uint16_t* idx_log = nullptr;   // the packer writes uint16 indices for every C
     uint8_t* idx8 = nullptr;
-    const int64_t nidx = (int64_t)L->N_ss * L->F_out;
+    __half* WT = nullptr;
+    const int64_t nidx = (int64_t)L->N_ss * n_dp;
     if (s == FASQ_OK) s = dev_alloc_t(&idx_log, (size_t)nidx * 2, st);
-    if (s == FASQ_OK) s = pack_run(static_cast<const __half*>(W_dev), L, prm, st, L->cb, idx_log);
+    if (s == FASQ_OK && L->dim0) {
+        // dim = 0 (Eq. 2 first case) is the dim = 1 partition of W^T: pack the
+        // transposed matrix with the same kernels (exactly as the oracle does)
+        s = dev_alloc_t(&WT, (size_t)F_out * F_in * 2, st);
+        if (s == FASQ_OK) s = transpose_f16(static_cast<const __half*>(W_dev), WT, F_out, F_in, st);
+        fasq_layer T{};
+        T.F_out = F_in;
+        T.F_in = F_out;
+        T.d = L->d;
+        T.C = L->C;
+        T.group = L->group;
+        T.N_ss = L->N_ss;
+        T.N_cb = L->N_cb;
+        if (s == FASQ_OK) s = pack_run(WT, &T, prm, st, L->cb, idx_log);
+    } else if (s == FASQ_OK) {
+        s = pack_run(static_cast<const __half*>(W_dev), L, prm, st, L->cb, idx_log);
+    }
     if (s == FASQ_OK && L->idx_w == 1) {
         s = dev_alloc_t(&idx8, (size_t)nidx, st);
         if (s == FASQ_OK) s = idx16_to_8(idx_log, idx8, nidx, st);
@@ -122,6 +141,7 @@ fasq_status fasq_pack(const void* W_dev, int64_t F_out, int64_t F_in, const fasq
         s = build_physical_from_logical(L, L->cb, L->idx_w == 1 ? static_cast<const void*>(idx8) : idx_log, st);
     dev_free(idx_log, st);
     dev_free(idx8, st);
+    dev_free(WT, st);
     if (s != FASQ_OK) { cudaStreamSynchronize(st); destroy(L); return s; }
     *out = L;
     return FASQ_OK;
@@ -139,6 +159,7 @@ fasq_status fasq_shard_rows(const fasq_layer* L, int32_t rank, int32_t world, vo
     *out = nullptr;
     if (!L || world < 1 || rank < 0 || rank >= world) return FASQ_E_ARG;
     if (L->F_out % world) return FASQ_E_SHAPE;
+    if (L->dim0) { set_error("shard_rows: dim = 0 layers are not row-sharded"); return FASQ_E_UNSUPPORTED; }
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t rows = L->F_out / world, row0 = rows * rank;
     // via the logical form: export -> slice rows -> import (any row0; the
@@ -158,7 +179,7 @@ fasq_status fasq_shard_rows(const fasq_layer* L, int32_t rank, int32_t world, vo
     fasq_layer* S = nullptr;
     if (s == FASQ_OK) {
         S = new fasq_layer();
-        s = init_layer_shape(S, rows, L->F_in, L->d, L->C, L->group, L->bits ? 1 : 0);
+        s = init_layer_shape(S, rows, L->F_in, L->d, L->C, L->group, layer_layout(L));
         if (s == FASQ_OK) s = alloc_layer_storage(S, st);
         if (s == FASQ_OK) s = build_physical_from_logical(S, L->cb, part, st);
         if (s == FASQ_OK) S->row_offset = L->row_offset + (int32_t)row0;
@@ -184,8 +205,9 @@ fasq_status fasq_layer_info_get(const fasq_layer* L, fasq_layer_info* info) {
     int lg = 0;
     while ((1 << lg) < L->C) ++lg;
     info->index_bits = L->bits ? L->bits : 8;
-    // Eq. 4's index table: index_bits per (subspace, row), rounded up to bytes
-    info->index_bytes = ((int64_t)L->N_ss * L->F_out * info->index_bits + 7) / 8;
+    info->layout = layer_layout(L);
+    // Eq. 4's index table: index_bits per (subspace, datapoint), rounded up to bytes
+    info->index_bytes = ((int64_t)L->N_ss * (L->dim0 ? L->F_in : L->F_out) * info->index_bits + 7) / 8;
     info->codebook_bytes = L->cb_bytes;
     info->device_bytes = L->idx_bytes + L->cbimg_bytes + L->cb_bytes + (L->cbimg_x ? L->cbimg_bytes : 0);
     info->bits_per_weight = 8.0 * (double)(info->index_bytes + info->codebook_bytes) / ((double)L->F_out * L->F_in);
@@ -224,13 +246,17 @@ fasq_status fasq_gemv_grouped(const fasq_layer* const* layers, int32_t n, const 
         if (!layers[i] || !ys_dev[i]) return FASQ_E_ARG;
     if (B < 1 || B > 8) return FASQ_E_UNSUPPORTED;
     if (yt != FASQ_F16 && yt != FASQ_F32 && yt != FASQ_ACC_I64) return FASQ_E_ARG;
-    bool packed = false;
-    for (int i = 0; i < n; ++i) packed = packed || layers[i]->bits;
-    if (packed) {   // NEXT-2: one packed layer per launch, fp16 x, no chain options
+    bool special = false;
+    for (int i = 0; i < n; ++i) special = special || layers[i]->bits || layers[i]->dim0;
+    if (special) {   // NEXT-2 packed / NEXT-4 dim = 0: one layer per launch, fp16 x, no chain options
         if (n != 1 || (opts && (opts->flags & FASQ_FLAG_X_ACC || opts->n_next || opts->zero_dev)))
             return FASQ_E_UNSUPPORTED;
-        return gemv_packed_launch(layers[0], static_cast<const __half*>(x_dev), B, ys_dev[0], yt,
-                                  opts ? opts->flags : 0u, (cudaStream_t)stream);
+        const uint32_t fl = opts ? opts->flags : 0u;
+        if (layers[0]->dim0)
+            return gemv_dim0_launch(layers[0], static_cast<const __half*>(x_dev), B, ys_dev[0], yt, fl,
+                                    (cudaStream_t)stream);
+        return gemv_packed_launch(layers[0], static_cast<const __half*>(x_dev), B, ys_dev[0], yt, fl,
+                                  (cudaStream_t)stream);
     }
     GemvOpts o{};
     if (opts) {
@@ -297,17 +323,17 @@ fasq_status fasq_gemm(const fasq_layer* L, const void* X_dev, int64_t M, void* Y
     if (yt != FASQ_F16 && yt != FASQ_F32) return FASQ_E_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     const __half* X = static_cast<const __half*>(X_dev);
-    if (L->bits) {
-        // NEXT-2 packed indices: no tensor-core / LUT prefill kernel reads the
-        // packed layout; the product runs as packed GEMVs over 8-token slices
-        // (correct for any M, not a prefill-speed path -- DESIGN.md §11)
+    if (L->bits || L->dim0) {
+        // NEXT-2 packed indices / NEXT-4 dim = 0: no tensor-core / LUT prefill
+        // kernel reads these layouts; the product runs as their GEMVs over
+        // 8-token slices (correct for any M, not a prefill-speed path)
         if (algo != FASQ_GEMM_AUTO) return FASQ_E_UNSUPPORTED;
         const size_t yb = yt == FASQ_F32 ? 4 : 2;
         int launches = 0;
         for (int64_t m0 = 0; m0 < M; m0 += 8) {
             const int b = (int)std::min<int64_t>(8, M - m0);
-            fasq_status s = gemv_packed_launch(L, X + m0 * L->F_in, b,
-                                               static_cast<uint8_t*>(Y_dev) + (size_t)m0 * L->F_out * yb, yt, 0u, st);
+            fasq_status s = gemv_launch(L, X + m0 * L->F_in, b,
+                                        static_cast<uint8_t*>(Y_dev) + (size_t)m0 * L->F_out * yb, yt, 0u, st);
             if (s != FASQ_OK) return s;
             launches += t_launches;
         }

@@ -71,6 +71,13 @@ struct fasq_layer {
     int32_t bits = 0;
     int32_t seg = 0;
     int32_t idx_w = 1;         // logical index element bytes (1: C <= 256, 2: C <= 1024)
+    // NEXT-4 dim = 0 (FASQ_LAYOUT_DIM0): subspace ss = output rows [ss*d, ss*d+d),
+    // N_ss = F_out/d, datapoints = the F_in columns.  `idx` holds
+    // [n_groups][K_pad/16][32 subspaces][16 columns] uint8 (lane s = subspace s
+    // loads 16 columns' indices with one LDS.128; a (group, column range) chunk
+    // is ONE contiguous range); cbimg/cbmap/cb as above (per subspace).
+    int32_t dim0 = 0;
+    int32_t K_pad = 0;         // dim0: F_in rounded up to 64
 };
 
 namespace fasq {
@@ -122,9 +129,15 @@ fasq_status build_physical_from_logical(fasq_layer* L, const __half* cb_logical,
 fasq_status build_cbimg(fasq_layer* L, cudaStream_t st);
 fasq_status idx16_to_8(const uint16_t* a, uint8_t* b, int64_t n, cudaStream_t st);
 fasq_status export_logical(const fasq_layer* L, __half* cb_out, void* idx_out, cudaStream_t st);
-// packed: 0 = uint8 layout (C <= 256), 1 = ceil(log2 C)-bit packed layout (C <= 1024)
+// layout: FASQ_LAYOUT_* bits (PACKED: ceil(log2 C)-bit indices, C <= 1024; DIM0: output-axis subspaces)
 fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t d, int32_t C, int32_t group,
-                             int32_t packed);
+                             uint32_t layout);
+uint32_t layer_layout(const fasq_layer* L);
+// NEXT-4: decode GEMV on a dim = 0 layer (gemv_dim0.cu), B = 1..8
+fasq_status gemv_dim0_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt, uint32_t flags,
+                             cudaStream_t st);
+// out[j][i] = in[i][j] for fp16 [rows][cols] (dim = 0 pack)
+fasq_status transpose_f16(const __half* in, __half* out, int64_t rows, int64_t cols, cudaStream_t st);
 // NEXT-2: decode GEMV on a packed layer (gemv_packed.cu), B = 1..8
 fasq_status gemv_packed_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt, uint32_t flags,
                                cudaStream_t st);

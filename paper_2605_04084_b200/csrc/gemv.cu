@@ -631,6 +631,7 @@ fasq_status acc_convert_launch(const void* acc, int64_t n, void* out, fasq_dtype
 fasq_status gemv_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt, uint32_t flags,
                         cudaStream_t st) {
     if (L->bits) return gemv_packed_launch(L, x, B, y, yt, flags, st);   // NEXT-2 packed indices
+    if (L->dim0) return gemv_dim0_launch(L, x, B, y, yt, flags, st);     // NEXT-4 output-axis subspaces
     void* ys[1] = {y};
     return gemv_grouped_launch(&L, 1, x, B, ys, yt, flags, st);
 }

@@ -9,10 +9,42 @@
 
 namespace fasq {
 
+uint32_t layer_layout(const fasq_layer* L) {
+    return (L->bits ? FASQ_LAYOUT_PACKED : 0u) | (L->dim0 ? FASQ_LAYOUT_DIM0 : 0u);
+}
+
 fasq_status init_layer_shape(fasq_layer* L, int64_t F_out, int64_t F_in, int32_t d, int32_t C,
-                             int32_t group, int32_t packed) {
-    if (F_out < 1 || F_in < 1 || d < 1 || C < 1 || group < 1 || packed < 0 || packed > 1) return FASQ_E_ARG;
+                             int32_t group, uint32_t layout) {
+    if (F_out < 1 || F_in < 1 || d < 1 || C < 1 || group < 1) return FASQ_E_ARG;
+    if (layout & ~(FASQ_LAYOUT_PACKED | FASQ_LAYOUT_DIM0)) return FASQ_E_ARG;
     if (d != 1 && d != 2 && d != 4 && d != 8) return FASQ_E_UNSUPPORTED;
+    if (layout & FASQ_LAYOUT_DIM0) {
+        // NEXT-4: dim = 0 (Eq. 2 first case): subspaces over the OUTPUT rows
+        if (layout & FASQ_LAYOUT_PACKED) return FASQ_E_UNSUPPORTED;
+        if (C > 256) return FASQ_E_UNSUPPORTED;
+        if (F_out % d) return FASQ_E_NONDIVISIBLE;
+        const int64_t N_ss = F_out / d;
+        if (N_ss % group) return FASQ_E_NONDIVISIBLE;
+        if (F_in > (1ll << 24) || N_ss > (1ll << 24)) return FASQ_E_UNSUPPORTED;
+        L->F_out = F_out;
+        L->F_in = F_in;
+        L->d = d;
+        L->C = C;
+        L->group = group;
+        L->N_ss = (int32_t)N_ss;
+        L->N_cb = (int32_t)(N_ss / group);
+        L->dim0 = 1;
+        L->K_pad = (int32_t)((F_in + 63) / 64 * 64);
+        L->F_out_pad = (int32_t)((F_out + kRowBlock - 1) / kRowBlock * kRowBlock);
+        L->n_groups = (int32_t)((N_ss + kGroupSubs - 1) / kGroupSubs);
+        L->E = entry_bytes(d);
+        L->idx_w = 1;
+        L->idx_bytes = (int64_t)L->n_groups * L->K_pad * kGroupSubs;
+        L->cbimg_bytes = (int64_t)L->n_groups * C * kGroupSubs * L->E;
+        L->cb_bytes = (int64_t)L->N_cb * C * d * 2;
+        return FASQ_OK;
+    }
+    const int32_t packed = (layout & FASQ_LAYOUT_PACKED) ? 1 : 0;
     if (C > 1024 || (C > 256 && !packed)) return FASQ_E_UNSUPPORTED;
     // packed layers (NEXT-2): d = 2, the sub-vector size of every Table 2 point
     // (2-128 ... 2-1024); the GEMV stages one group's codebook image
@@ -175,6 +207,64 @@ __global__ void k_idx_packed_to_logical(const uint8_t* __restrict__ phys, IT* __
     }
 }
 
+// dim = 0 layout: one thread per (group g, 16-column block, subspace s): 16 bytes
+// (columns >= F_in and subspaces >= N_ss hold 0).
+__global__ void k_idx_dim0_to_phys(const uint8_t* __restrict__ idx_log, uint8_t* __restrict__ phys, int F_in,
+                                   int K_pad, int N_ss, int n_groups) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nb = K_pad / 16;
+    if (t >= (int64_t)n_groups * nb * kGroupSubs) return;
+    const int s = (int)(t % kGroupSubs);
+    const int64_t jb = (t / kGroupSubs) % nb;
+    const int64_t g = t / (kGroupSubs * nb);
+    const int64_t ss = g * kGroupSubs + s;
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    for (int q = 0; q < 16; ++q) {
+        const int64_t j = jb * 16 + q;
+        const uint32_t v = (ss < N_ss && j < F_in) ? idx_log[ss * F_in + j] : 0u;
+        w[q >> 2] |= v << (8 * (q & 3));
+    }
+    *reinterpret_cast<uint4*>(phys + t * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__global__ void k_idx_dim0_to_logical(const uint8_t* __restrict__ phys, uint8_t* __restrict__ idx_log, int F_in,
+                                      int K_pad, int N_ss, int n_groups) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nb = K_pad / 16;
+    if (t >= (int64_t)n_groups * nb * kGroupSubs) return;
+    const int s = (int)(t % kGroupSubs);
+    const int64_t jb = (t / kGroupSubs) % nb;
+    const int64_t g = t / (kGroupSubs * nb);
+    const int64_t ss = g * kGroupSubs + s;
+    if (ss >= N_ss) return;
+    for (int q = 0; q < 16; ++q) {
+        const int64_t j = jb * 16 + q;
+        if (j < F_in) idx_log[ss * F_in + j] = phys[t * 16 + q];
+    }
+}
+
+// 32 x 32 tiles through SMEM (coalesced both ways)
+__global__ void k_transpose_f16(const __half* __restrict__ in, __half* __restrict__ out, int64_t rows, int64_t cols) {
+    __shared__ __half tile[32][33];
+    const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][i];
+    }
+}
+
+fasq_status transpose_f16(const __half* in, __half* out, int64_t rows, int64_t cols, cudaStream_t st) {
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+    k_transpose_f16<<<grid, dim3(32, 8), 0, st>>>(in, out, rows, cols);
+    FASQ_CUDA_TRY(cudaGetLastError());
+    return FASQ_OK;
+}
+
 // uint8 logical -> the byte layout, from a uint16 logical table (GPU pack output)
 __global__ void k_idx16_to_8(const uint16_t* __restrict__ a, uint8_t* __restrict__ b, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -220,7 +310,7 @@ fasq_status ensure_cbimg_x(const fasq_layer* Lc, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(mu);
     fasq_layer* L = const_cast<fasq_layer*>(Lc);   // a derived cache; the PQ data stays immutable
     if (L->cbimg_x) return FASQ_OK;
-    if (L->d != 2 || L->E != 4 || L->bits) return FASQ_E_UNSUPPORTED;
+    if (L->d != 2 || L->E != 4 || L->bits || L->dim0) return FASQ_E_UNSUPPORTED;
     uint8_t* img = nullptr;
     fasq_status s = dev_alloc_t(&img, (size_t)L->cbimg_bytes, st);
     if (s != FASQ_OK) return s;
@@ -241,6 +331,13 @@ fasq_status build_physical_from_logical(fasq_layer* L, const __half* cb_logical,
                                         cudaStream_t st) {
     if (cb_logical != L->cb)
         FASQ_CUDA_TRY(cudaMemcpyAsync(L->cb, cb_logical, (size_t)L->cb_bytes, cudaMemcpyDeviceToDevice, st));
+    if (L->dim0) {
+        const int64_t n = (int64_t)L->n_groups * (L->K_pad / 16) * kGroupSubs;
+        k_idx_dim0_to_phys<<<nblk(n, 256), 256, 0, st>>>(static_cast<const uint8_t*>(idx_logical), L->idx,
+                                                         (int)L->F_in, L->K_pad, L->N_ss, L->n_groups);
+        FASQ_CUDA_TRY(cudaGetLastError());
+        return build_cbimg(L, st);
+    }
     if (L->bits == 0) {
         int64_t n = (int64_t)L->n_groups * (L->F_out_pad / 16) * kGroupSubs;
         k_idx_logical_to_phys<<<nblk(n, 256), 256, 0, st>>>(static_cast<const uint8_t*>(idx_logical), L->idx,
@@ -291,6 +388,13 @@ fasq_status build_cbimg(fasq_layer* L, cudaStream_t st) {
 fasq_status export_logical(const fasq_layer* L, __half* cb_out, void* idx_out_, cudaStream_t st) {
     if (cb_out)
         FASQ_CUDA_TRY(cudaMemcpyAsync(cb_out, L->cb, (size_t)L->cb_bytes, cudaMemcpyDeviceToDevice, st));
+    if (idx_out_ && L->dim0) {
+        const int64_t n = (int64_t)L->n_groups * (L->K_pad / 16) * kGroupSubs;
+        k_idx_dim0_to_logical<<<nblk(n, 256), 256, 0, st>>>(L->idx, static_cast<uint8_t*>(idx_out_), (int)L->F_in,
+                                                            L->K_pad, L->N_ss, L->n_groups);
+        FASQ_CUDA_TRY(cudaGetLastError());
+        return FASQ_OK;
+    }
     if (idx_out_ && L->bits) {
         const int64_t n = (int64_t)L->n_groups * (L->F_out_pad / kRowBlock) * kGroupSubs;
         if (L->idx_w == 2)

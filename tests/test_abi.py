@@ -48,7 +48,7 @@ def test_argument_errors_are_synchronous(fasq):
     out = ctypes.c_void_p()
     # NULL pointers -> FASQ_E_ARG before touching any device
     assert fasq.lib.fasq_import(None, None, 8, 8, 2, 4, 1, None, ctypes.byref(out)) == -1
-    assert fasq.lib.fasq_import_packed(None, None, 8, 8, 2, 4, 1, 1, None, ctypes.byref(out)) == -1
+    assert fasq.lib.fasq_import_ex(None, None, 8, 8, 2, 4, 1, 1, None, ctypes.byref(out)) == -1
     assert fasq.lib.fasq_gemv(None, None, 1, None, 0, None) == -1
     assert fasq.lib.fasq_gemm(None, None, 1, None, 0, 0, None) == -1
     assert fasq.lib.fasq_export(None, None, None, None) == -1
