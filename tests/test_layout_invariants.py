@@ -91,3 +91,24 @@ def test_pair_stage_gather_hits_bank_s_for_any_k():
     for k, h in itertools.product((0, 1, 77, 128, 255), (0, 1)):
         banks = [(((k << 8) | (h * 128 + 4 * s)) // 4) % 32 for s in range(32)]
         assert banks == list(range(32))
+
+
+# ---- host-only chain planner (K-split counts must fit the 6-bit
+# counted-word field for the full Llama shapes at every world size) ----------
+def test_chain_planner_llama_shapes_all_world_sizes():
+    import paper_2605_04084_b200 as F
+    blocks = {"qkv": [(4096, 4096), (1024, 4096), (1024, 4096)], "o": [(4096, 4096)],
+              "gateup": [(14336, 4096), (14336, 4096)], "down": [(4096, 14336)]}
+    for world in (1, 2, 4, 8):
+        for nctas in (148, 148 // world):
+            for B in (1, 2, 4, 8):
+                for name, shapes in blocks.items():
+                    # row shards (q/k/v, gate/up) and Megatron K shards (o, down)
+                    if name in ("o", "down"):
+                        sh = [(fo, fi // world) for fo, fi in shapes]
+                    else:
+                        sh = [(fo // world, fi) for fo, fi in shapes]
+                    ks = F.plan_ks(sh, nctas=nctas, d=2, B=B)
+                    assert all(1 <= k <= 63 for k in ks), (world, nctas, B, name, ks)
+                    full = F.plan_ks(shapes, nctas=nctas, d=2, B=B)
+                    assert all(1 <= k <= 63 for k in full), (world, nctas, B, name, full)
