@@ -77,6 +77,13 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         :: "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar) : "memory");
 }
 
+// PAIR: a 2-CTA cluster shares each 256-row B tile (cta_group::2, M = 256 per
+// MMA): CTA r expands weight rows [n0 + 128 r, n0 + 128 r + 128) only, keeps its
+// own 2 x 128 tokens (its 1-CTA tile), and the leader (r = 0) issues the pair
+// MMAs reading both CTAs' A and B halves -- half the expansion work, B-tile
+// SMEM and UMMA B-operand reads per SM (the 1-CTA kernel is SMEM-bandwidth
+// bound: TC + LSU + TMA wavefronts ~ 80 % of the SMEM data path, ncu).
+template <bool PAIR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -85,54 +92,77 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     const int C = p.C;
     constexpr int A_TILE = TC_M * TC_K * 2;       // 16 KiB per token tile
     constexpr int A_BYTES = TC_MT * A_TILE;       // per stage
-    constexpr int B_BYTES = TC_N * TC_K * 2;      // 32 KiB
-    constexpr int IDX_BYTES = TC_N * 32;          // 8 KiB
+    constexpr int NR = PAIR ? TC_N / 2 : TC_N;    // weight rows expanded by this CTA
+    constexpr int B_BYTES = NR * TC_K * 2;        // 32 KiB (16 KiB per CTA of a pair)
+    constexpr int IDX_BYTES = NR * 32;            // 8 KiB (4 KiB)
     const int CB_BYTES = C * 128;                 // per stage: [C][32][4]
     uint8_t* sA = smem;                                   // STAGES * A
-    uint8_t* sB = sA + TC_STAGES * A_BYTES;               // STAGES * B
-    uint8_t* sI = sB + TC_STAGES * B_BYTES;               // STAGES * IDX
-    uint8_t* sC = sI + TC_STAGES * IDX_BYTES;             // STAGES * [C][32][4] (one bulk copy each)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sC + TC_STAGES * CB_BYTES);
+    // SX stages of the X/B ring (PAIR: 3 -- the halved B tile frees the SMEM, and the
+    // cross-CTA hand-off per chunk needs the slack), SL of the codebook/index ring
+    constexpr int SX = PAIR ? 3 : TC_STAGES, SL = TC_STAGES;
+    uint8_t* sB = sA + SX * A_BYTES;                      // SX * B
+    uint8_t* sI = sB + SX * B_BYTES;                      // SL * IDX
+    uint8_t* sC = sI + SL * IDX_BYTES;                    // SL * [C][32][4] (one bulk copy each)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sC + SL * CB_BYTES);
     // bars: full[S] (X tiles), bfull[S] (B tile expanded), empty[S] (MMA done:
     // X and B slot free), lfull[S] / lempty[S] (codebook + index chunk ring,
     // released by the expansion warps -- not by the MMA -- so the next chunks'
     // loads start one MMA period earlier), accum
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 * TC_STAGES + 1);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * SX + 2 * SL + 1);   // + pair[SX]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // tiles in PAIR order: tile 2i + r = (row tile (i % ntx), token tile 2 (i / ntx) + r),
+    // so the two CTAs of a cluster share the row tile (both kernels use it)
     const int tile_g = p.tile0 + (int)blockIdx.x;            // tile of the whole problem
-    const int n0 = (tile_g % p.ntx) * TC_N;                  // weight-row tile
-    const int m0 = (tile_g / p.ntx) * TC_M * TC_MT;          // first token of this CTA's token tiles
+    const int rank = tile_g & 1;                             // = %cluster_ctarank for PAIR
+    const int nrt = (tile_g >> 1) % p.ntx, ntt = 2 * ((tile_g >> 1) / p.ntx) + rank;
+    const int n0t = nrt * TC_N;                              // weight-row tile (epilogue rows)
+    const int n0 = n0t + (PAIR ? rank * NR : 0);             // rows this CTA expands
+    const int m0 = ntt * TC_M * TC_MT;                       // first token of this CTA's token tiles
     // split-K (small M: too few tiles for the SMs): this CTA's K chunks [kb, kb + nk)
     const int ksplit = (int)gridDim.z, kz = (int)blockIdx.z;
     const int kb = (int)((int64_t)kz * p.n_groups / ksplit);
     const int nk = (int)((int64_t)(kz + 1) * p.n_groups / ksplit) - kb;
     const uint32_t bar0 = dev::smem_u32(bars);
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
-    auto bfull_bar = [&](int s) { return bar0 + 8u * (TC_STAGES + s); };
-    auto empty_bar = [&](int s) { return bar0 + 8u * (2 * TC_STAGES + s); };
-    auto lfull_bar = [&](int s) { return bar0 + 8u * (3 * TC_STAGES + s); };
-    auto lempty_bar = [&](int s) { return bar0 + 8u * (4 * TC_STAGES + s); };
-    const uint32_t accum_bar = bar0 + 8u * (5 * TC_STAGES);
+    auto bfull_bar = [&](int s) { return bar0 + 8u * (SX + s); };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (2 * SX + s); };
+    auto lfull_bar = [&](int s) { return bar0 + 8u * (3 * SX + s); };
+    auto lempty_bar = [&](int s) { return bar0 + 8u * (3 * SX + SL + s); };
+    const uint32_t accum_bar = bar0 + 8u * (3 * SX + 2 * SL);
+    auto pair_bar = [&](int s) { return bar0 + 8u * (3 * SX + 2 * SL + 1 + s); };   // PAIR leader: peer stage ready
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < TC_STAGES; ++s) {
+        for (int s = 0; s < SX; ++s) {
             dev::mbar_init(full_bar(s), 1);
             dev::mbar_init(bfull_bar(s), TC_EXP_WARPS);
             dev::mbar_init(empty_bar(s), 1);
+            dev::mbar_init(pair_bar(s), 1);
+        }
+        for (int s = 0; s < SL; ++s) {
             dev::mbar_init(lfull_bar(s), 1);
             dev::mbar_init(lempty_bar(s), TC_EXP_WARPS);
         }
         dev::mbar_init(accum_bar, 1);
         dev::fence_barrier_init();
     }
-    if (warp == 1) {   // TMEM allocation (256 fp32 columns = the 128x256 accumulator)
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     :: "r"(dev::smem_u32(tmem_slot)), "n"(256 * TC_MT));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (warp == 1) {   // TMEM allocation (2 x 256 fp32 columns: the two 128x256 accumulators)
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                         :: "r"(dev::smem_u32(tmem_slot)), "n"(256 * TC_MT));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                         :: "r"(dev::smem_u32(tmem_slot)), "n"(256 * TC_MT));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
+    if constexpr (PAIR) {   // barriers initialised in both CTAs before any remote arrive
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
 
@@ -140,8 +170,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
         // ---------------------------- X producer -----------------------------
         if (lane == 0) asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
         for (int i = 0; i < nk; ++i) {
-            const int s = i % TC_STAGES;
-            if (i >= TC_STAGES) dev::mbar_wait(empty_bar(s), ((i / TC_STAGES) + 1) & 1);
+            const int s = i % SX;
+            if (i >= SX) dev::mbar_wait(empty_bar(s), ((i / SX) + 1) & 1);
             if (lane == 0) {
                 dev::mbar_arrive_expect_tx(full_bar(s), (uint32_t)A_BYTES);
 #pragma unroll
@@ -153,16 +183,20 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
         }
     } else if (warp == 2 + TC_EXP_WARPS) {
         // ---------------------- codebook + index producer ----------------------
-        const int rows = min(TC_N, p.F_out_pad - n0);          // idx rows present (multiple of 64)
+        const int rows = max(0, min(NR, p.F_out_pad - n0));    // idx rows present (multiple of 64)
         const uint32_t idx_bytes = (uint32_t)rows * 32u;
         const uint32_t cb_u = dev::smem_u32(sC);
         for (int i = 0; i < nk; ++i) {
-            const int s = i % TC_STAGES;
-            if (i >= TC_STAGES) dev::mbar_wait(lempty_bar(s), ((i / TC_STAGES) + 1) & 1);
+            const int s = i % SL;
+            if (i >= SL) dev::mbar_wait(lempty_bar(s), ((i / SL) + 1) & 1);
             if (lane == 0) {
                 dev::mbar_arrive_expect_tx(lfull_bar(s), idx_bytes + (uint32_t)CB_BYTES);
-                dev::bulk_g2s(dev::smem_u32(sI + s * IDX_BYTES), p.idx + ((size_t)(kb + i) * p.F_out_pad + n0) * 32,
-                              idx_bytes, lfull_bar(s));
+                if (idx_bytes)
+                    dev::bulk_g2s(dev::smem_u32(sI + s * IDX_BYTES),
+                                  p.idx + ((size_t)(kb + i) * p.F_out_pad + n0) * 32, idx_bytes, lfull_bar(s));
+                // (a PAIR variant fetching one codebook half per CTA with
+                // .multicast::cluster was measured 25 % slower: the shared slot
+                // couples the two CTAs' rings; profiles/r02/gemm_pair_ab.txt)
                 dev::bulk_g2s(cb_u + (uint32_t)s * (uint32_t)CB_BYTES, p.cbimg + (size_t)(kb + i) * CB_BYTES,
                               (uint32_t)CB_BYTES, lfull_bar(s));
             }
@@ -170,12 +204,29 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
         }
     } else if (warp == 1) {
         // ------------------------------ MMA issuer -----------------------------
-        constexpr uint32_t idesc = idesc_f16(TC_M, TC_N);
+        if (PAIR && rank == 1) {
+            // the peer's relay: once this CTA's X tiles and B half of stage s are
+            // in SMEM, arrive (release, cluster scope) on the leader's pair_bar(s)
+            for (int i = 0; i < nk; ++i) {
+                const int s = i % SX;
+                const uint32_t ph = (i / SX) & 1;
+                dev::mbar_wait(full_bar(s), ph);
+                dev::mbar_wait(bfull_bar(s), ph);
+                if (lane == 0) {
+                    uint32_t rb;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(pair_bar(s)));
+                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(rb) : "memory");
+                }
+                __syncwarp();
+            }
+        } else {
+        constexpr uint32_t idesc = idesc_f16(PAIR ? 2 * TC_M : TC_M, TC_N);
         for (int i = 0; i < nk; ++i) {
-            const int s = i % TC_STAGES;
-            const uint32_t ph = (i / TC_STAGES) & 1;
+            const int s = i % SX;
+            const uint32_t ph = (i / SX) & 1;
             dev::mbar_wait(full_bar(s), ph);
             dev::mbar_wait(bfull_bar(s), ph);
+            if (PAIR) dev::mbar_wait_cluster(pair_bar(s), ph);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (lane == 0) {
                 const uint32_t b_base = dev::smem_u32(sB + s * B_BYTES);
@@ -187,20 +238,37 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
                         const uint64_t ad = umma_desc_sw128(a_base + kk * 32);
                         const uint64_t bd = umma_desc_sw128(b_base + kk * 32);
                         const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-                        asm volatile(
-                            "{.reg .pred p;\n\t"
-                            "setp.ne.b32 p, %4, 0;\n\t"
-                            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
-                            :: "r"(tmem + (uint32_t)(t * TC_N)), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                        if constexpr (PAIR)
+                            asm volatile(
+                                "{.reg .pred p;\n\t"
+                                "setp.ne.b32 p, %4, 0;\n\t"
+                                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;}"
+                                :: "r"(tmem + (uint32_t)(t * TC_N)), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                        else
+                            asm volatile(
+                                "{.reg .pred p;\n\t"
+                                "setp.ne.b32 p, %4, 0;\n\t"
+                                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
+                                :: "r"(tmem + (uint32_t)(t * TC_N)), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
                     }
                 }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                             :: "r"(empty_bar(s)) : "memory");
-                if (i == nk - 1)
+                if constexpr (PAIR) {
+                    // frees stage s in BOTH CTAs (X producers and expansion warps)
+                    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                                 :: "r"(empty_bar(s)), "h"((unsigned short)3) : "memory");
+                    if (i == nk - 1)
+                        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                                     :: "r"(accum_bar), "h"((unsigned short)3) : "memory");
+                } else {
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                                 :: "r"(accum_bar) : "memory");
+                                 :: "r"(empty_bar(s)) : "memory");
+                    if (i == nk - 1)
+                        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                                     :: "r"(accum_bar) : "memory");
+                }
             }
             __syncwarp();
+        }
         }
     } else {
         // ------------------------------ expansion ------------------------------
@@ -211,24 +279,26 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
         // lanes of one STS fill one 128-B B-tile row (K-major SWIZZLE_128B:
         // 16-B chunk c of row r at c ^ (r & 7)) -> conflict-free.
         const int ew = warp - 2;                 // 0..7
+        constexpr int RPW = NR / TC_EXP_WARPS;   // rows per expansion warp (32, PAIR: 16)
         uint32_t xo[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) xo[q] = ((uint32_t)(((lane >> 2) ^ q) << 4)) | ((uint32_t)(lane & 3) << 2);
         const uint32_t cb_u = dev::smem_u32(sC);
-        const uint32_t ib0 = (uint32_t)(ew >> 1) * 2048u + (uint32_t)lane * 64u;
+        const uint32_t ib0 = (uint32_t)((ew * RPW) >> 6) * 2048u + (uint32_t)lane * 64u;   // 64-row block
+        const uint32_t cw0 = (uint32_t)(((ew * RPW) & 63) >> 4);                          // first 16-row chunk
         const uint32_t rot = (uint32_t)(lane >> 1);
-        const bool have = n0 + ew * 32 < p.F_out_pad;   // this warp's rows were loaded (64-row blocks)
+        const bool have = n0 + ew * RPW < p.F_out_pad;   // this warp's rows were loaded (64-row blocks)
         for (int i = 0; i < nk; ++i) {
-            const int s = i % TC_STAGES;
-            const uint32_t ph = (i / TC_STAGES) & 1;
+            const int s = i % SL, sx = i % SX;
+            const uint32_t ph = (i / SL) & 1;
             dev::mbar_wait(lfull_bar(s), ph);                                       // codebook + indices
-            if (i >= TC_STAGES) dev::mbar_wait(empty_bar(s), ((i / TC_STAGES) + 1) & 1);   // B slot free
+            if (i >= SX) dev::mbar_wait(empty_bar(sx), ((i / SX) + 1) & 1);          // B slot free
             const uint32_t ia = dev::smem_u32(sI + s * IDX_BYTES) + ib0;
             const uint32_t cbl = cb_u + (uint32_t)s * (uint32_t)CB_BYTES + (uint32_t)lane * 4u;
-            const uint32_t bst = dev::smem_u32(sB + s * B_BYTES) + (uint32_t)ew * 32u * 128u;
+            const uint32_t bst = dev::smem_u32(sB + sx * B_BYTES) + (uint32_t)(ew * RPW) * 128u;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t c = (uint32_t)(2 * (ew & 1) + h);
+            for (int h = 0; h < RPW / 16; ++h) {
+                const uint32_t c = cw0 + (uint32_t)h;
                 uint4 v = make_uint4(0, 0, 0, 0);
                 if (have) v = dev::lds128(ia + 16u * ((c + rot) & 3u));
                 const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -243,7 +313,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
             dev::fence_proxy_async();      // generic-proxy STS -> visible to tcgen05 (async proxy)
             __syncwarp();
             if (lane == 0) {
-                dev::mbar_arrive(bfull_bar(s));
+                dev::mbar_arrive(bfull_bar(sx));
                 dev::mbar_arrive(lempty_bar(s));
             }
         }
@@ -316,7 +386,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
                     for (int v = 0; v < 8; ++v)
                         __stcg(reinterpret_cast<float4*>(wr) + v, make_float4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]));
                 } else {
-                    store32(n0 + c0, f);
+                    store32(n0t + c0, f);
                 }
             }
             if (ksplit > 1) {
@@ -360,22 +430,31 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
                             f[4 * v + 3] += w.w;
                         }
                     }
-                    store32(n0 + c0, f);
+                    store32(n0t + c0, f);
                 }
             }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
+    if constexpr (PAIR) {   // both CTAs done with the pair's TMEM before it is released
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(256 * TC_MT));
+        if constexpr (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(256 * TC_MT));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(256 * TC_MT));
     }
 }
 
-size_t tc_smem_bytes(int C) {
-    return 1024 + (size_t)TC_STAGES * (TC_MT * TC_M * TC_K * 2 + TC_N * TC_K * 2 + TC_N * 32 + (size_t)C * 128) +
-           8 * (5 * TC_STAGES + 1) + 16;
+size_t tc_smem_bytes(int C, bool pair = false) {
+    const size_t nr = pair ? TC_N / 2 : TC_N;
+    const size_t sx = pair ? 3 : TC_STAGES, sl = TC_STAGES;
+    return 1024 + sx * (TC_MT * TC_M * TC_K * 2 + nr * TC_K * 2) + sl * (nr * 32 + (size_t)C * 128) +
+           8 * (4 * sx + 2 * sl + 1) + 16;
 }
 
 }  // namespace
@@ -422,15 +501,26 @@ fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void
     p.n_groups = L->n_groups;
     p.C = L->C;
     p.y_f32 = yt == FASQ_F32;
-    const size_t smem = tc_smem_bytes(L->C);
+    const size_t smem = tc_smem_bytes(L->C), smem2 = tc_smem_bytes(L->C, true);
     static std::once_flag once;
-    static size_t lim = 0;
-    std::call_once(once, [] { lim = set_max_dyn_smem(k_gemm_tc); });
+    static size_t lim = 0, lim2 = 0;
+    std::call_once(once, [] {
+        lim = set_max_dyn_smem(k_gemm_tc<false>);
+        lim2 = set_max_dyn_smem(k_gemm_tc<true>);
+    });
     if (lim < smem) { set_error("gemm_tc: SMEM"); return FASQ_E_UNSUPPORTED; }
+    // 2-CTA pairs (cta_group::2) for the launches without split-K: opt-in
+    // (FASQ_GEMM_PAIR=1) -- measured equal at 4096^2 and 3-5 % slower on the
+    // 14336-row / 14336-column shapes (profiles/r02/gemm_pair_ab.txt)
+    const char* pe = getenv("FASQ_GEMM_PAIR");
+    const bool pair_env = pe && atoi(pe) == 1;
+    const bool pair_ok = pair_env && lim2 >= smem2;
     // F_out_pad rows of the idx table exist; tiles past F_out_pad read beyond it
     // -> require the row tile grid to stay within F_out_pad (pad logic below).
     const int ntx = (L->F_out_pad + TC_N - 1) / TC_N;
-    const int nty = (int)((M + TC_M * TC_MT - 1) / (TC_M * TC_MT));
+    // token tiles rounded up to an even count: tiles are numbered in pair order
+    // (kernel), the phantom tile of an odd count reads zero-filled X and stores nothing
+    const int nty = (int)((M + TC_M * TC_MT - 1) / (TC_M * TC_MT) + 1) / 2 * 2;
     const int tiles_all = ntx * nty;
     p.ntx = ntx;
     int dev = 0, sms = 148;
@@ -453,7 +543,8 @@ fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void
     };
     int launches[2][3];   // {tile0, tiles, ks}
     int nl = 0;
-    const int tail = tiles_all > sms ? tiles_all % sms : 0;
+    int tail = tiles_all > sms ? tiles_all % sms : 0;
+    if (tail & 1) ++tail;   // the full-wave launch keeps whole pairs
     if (tail > 0 && tail <= sms / 4 && getenv("FASQ_GEMM_KSPLIT") == nullptr) {
         launches[nl][0] = 0; launches[nl][1] = tiles_all - tail; launches[nl][2] = 1; ++nl;
         launches[nl][0] = tiles_all - tail; launches[nl][1] = tail; launches[nl][2] = pick_ks(tail); ++nl;
@@ -488,8 +579,25 @@ fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void
             p.tickets = reinterpret_cast<unsigned*>(ws + need);
             grid.z = (unsigned)ks;
         }
-        k_gemm_tc<<<grid, TC_THREADS, smem, st>>>(map, p);
-        cudaError_t e = cudaGetLastError();
+        cudaError_t e;
+        if (ks == 1 && pair_ok && (tiles & 1) == 0 && (p.tile0 & 1) == 0) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = grid;
+            cfg.blockDim = dim3(TC_THREADS, 1, 1);
+            cfg.dynamicSmemBytes = smem2;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            e = cudaLaunchKernelEx(&cfg, k_gemm_tc<true>, map, p);
+        } else {
+            k_gemm_tc<false><<<grid, TC_THREADS, smem, st>>>(map, p);
+            e = cudaGetLastError();
+        }
         if (e != cudaSuccess) {
             for (int q = 0; q <= li; ++q) dev_free(wss[q], st);
             return cuda_fail(e, "k_gemm_tc launch");

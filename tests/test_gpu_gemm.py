@@ -184,3 +184,26 @@ def test_gemv_large_batch_dispatches_to_gemm(F, oracle_lib, B):
     with pytest.raises(F.FasqError):
         F.gemv(L, torch.from_numpy(x).cuda(), out_dtype=torch.float32, flags=F.FLAG_PDL)
     L.free()
+
+
+@pytest.mark.parametrize("F_out,F_in,M", [(4096, 4096, 2048), (14336, 4096, 2048), (4096, 14336, 1536),
+                                          (1000, 512, 1300)])
+def test_gemm_tc_pair_cta_group2(F, oracle_lib, monkeypatch, F_out, F_in, M):
+    """The opt-in 2-CTA EXPAND (FASQ_GEMM_PAIR=1: cta_group::2, each CTA of a
+    cluster expands half of the 256-row B tile, the leader issues M = 256 MMAs):
+    sampled rows against the fp64 oracle, and equal to the 1-CTA kernel's Y
+    (same K order per output)."""
+    monkeypatch.setenv("FASQ_GEMM_PAIR", "1")
+    cb, idx = synth.random_layer(F_out, F_in, 2, 256, seed=F_out + M)
+    X = synth.activation(M, F_in, seed=3)
+    L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), F_in)
+    Xd = torch.from_numpy(X).cuda()
+    Y = F.gemm(L, Xd, algo=F.GEMM_EXPAND_TC).float().cpu().numpy()
+    rows = (F_out // 2 - 32, F_out // 2 + 32)
+    Y_ref = oracle_lib.gemm(cb, idx, X[::97], rows=rows)
+    ok, m = parity_ok(Y[::97, rows[0]:rows[1]], Y_ref, X[::97], F_in)
+    assert ok, m
+    monkeypatch.setenv("FASQ_GEMM_PAIR", "0")
+    Y1 = F.gemm(L, Xd, algo=F.GEMM_EXPAND_TC).float().cpu().numpy()
+    rel = np.linalg.norm(Y - Y1) / np.linalg.norm(Y1)
+    assert rel <= 1e-6, rel
