@@ -534,16 +534,46 @@ __device__ __forceinline__ void attn_item_batched(const ChainPhase* ph, int head
         if (lane == 0) { s_ml[warp * 4] = mx; s_ml[warp * 4 + 1] = sm; }
     }
     consumer_bar(NT);
-    // 5. o partials: task (row group, token, dim), 4 row groups
-    for (int i = tid; i < 4 * B * hd; i += NT) {
-        const int rg = i / (B * hd), rem = i - rg * B * hd, b = rem / hd, dim = rem - b * hd;
-        const __half* vc = ph->vc + ((size_t)b * n_kv + kvh) * (size_t)max_T * hd;
-        float o = 0.f;
-        for (int t = r.t0 + rg; t < r.t1; t += 4) {
-            const __half vh = t == pos ? s_vn[b * 128 + dim] : __ldcg(vc + (size_t)t * hd + dim);
-            o += s_sc[b * scw + t - r.t0] * __half2float(vh);
+    // 5. o partials: task (row group, token, 8-dim chunk) -- one 16-B load per
+    // cache row covers 8 dims, 8 rows in flight (the per-dim version issued one
+    // dependent 2-B L2 load per row: ~16 serial L2 round trips per item).  Per
+    // dim the rows are still added in ascending t (same sums as before).
+    {
+        const int nc8 = hd / 8;
+        for (int i = tid; i < 4 * B * nc8; i += NT) {
+            const int rg = i / (B * nc8), rem = i - rg * B * nc8, b = rem / nc8, c8 = rem - b * nc8;
+            const __half* vc = ph->vc + ((size_t)b * n_kv + kvh) * (size_t)max_T * hd + c8 * 8;
+            const uint4 vnew = *reinterpret_cast<const uint4*>(s_vn + b * 128 + c8 * 8);
+            const float* sc = s_sc + b * scw - r.t0;
+            float o[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = 0.f;
+            int t = r.t0 + rg;
+            for (; t + 28 < r.t1; t += 32) {
+                uint4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int tt = t + 4 * u;
+                    v[u] = tt == pos ? vnew : __ldcg(reinterpret_cast<const uint4*>(vc + (size_t)tt * hd));
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const float pu = sc[t + 4 * u];
+                    const __half* vh = reinterpret_cast<const __half*>(&v[u]);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) o[e] += pu * __half2float(vh[e]);
+                }
+            }
+            for (; t < r.t1; t += 4) {
+                const uint4 v = t == pos ? vnew : __ldcg(reinterpret_cast<const uint4*>(vc + (size_t)t * hd));
+                const float pu = sc[t];
+                const __half* vh = reinterpret_cast<const __half*>(&v);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) o[e] += pu * __half2float(vh[e]);
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) s_o[(rg * B + b) * 128 + c8 * 8 + e] = o[e];
         }
-        s_o[(rg * B + b) * 128 + dim] = o;
     }
     consumer_bar(NT);
     for (int i = tid; i < B * hd; i += NT) {
