@@ -492,6 +492,7 @@ fasq_status chain_build(const std::vector<StepDesc>& steps, int B, int world, in
                     w.g_begin = (int)((int64_t)k * L->n_groups / ks[l]);
                     w.g_end = (int)((int64_t)(k + 1) * L->n_groups / ks[l]);
                     w.kidx = k;
+                    w.kn = ks[l];
                     // (layer 0, row tile 0) K ranges cover F_in once: they contribute the RMSNorm sum of squares
                     w.nsq = (S.in_mode == IN_RMSNORM && l == 0 && r == 0) ? k : -1;
                     c->gmax = std::max(c->gmax, w.g_end - w.g_begin);

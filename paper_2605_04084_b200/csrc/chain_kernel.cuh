@@ -27,6 +27,8 @@ struct alignas(128) ChainItem {
     int g_begin, g_end, rows_valid;
     int N_ss, r0, kidx, head;   // kidx: PQ K-range index in its row tile (0 adds the residual); ATTN: cache part
     int nsq;                    // PQ: RMSNorm sum-of-squares slot this item contributes (-1: none)
+    int kn;                     // PQ: K ranges of this item's row tile (the residual of warp w's rows
+                                //     is added by the range kidx == w % kn)
     int F_out, ld, row0_g;      // local rows, words per batch row of the output, output index of local row 0
     long long y_off;            // word offset of the output [B][ld] in a buffer
     // producer
@@ -75,6 +77,7 @@ struct EpiParams {
     long long y_off, res_off, res2_off, nsq_off;
     int row0_g, ld, F_out, r0;
     int add_res, res_ks, res_sys, out_all;
+    int kidx, kn;
     int res2_ks, epi_scale, nsq_n, F_in;
     float eps;
     int pad;
@@ -938,7 +941,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
             e.ld = wp->ld;
             e.F_out = wp->F_out;
             e.r0 = wp->r0;
-            e.add_res = e.res_off >= 0 && phs->res_here && w.kidx == 0;
+            // the residual is spread over the row tile's K ranges (warp w's rows: range
+            // w % kn) -- a single range polling all 1024 rows' residual words was the
+            // slowest CTA of the o / down steps (at B = 8: 1.6x the median item)
+            e.add_res = e.res_off >= 0 && phs->res_here;
+            e.kidx = w.kidx;
+            e.kn = w.kn > 0 ? w.kn : 1;
             e.res_ks = phs->res_ks;
             e.res_sys = phs->res_sys;
             e.out_all = phs->out_all;
@@ -986,7 +994,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                     long long qv[16];
                     const long long off = (long long)(s_run & 1u) * p.arena_words + s_ep.y_off + row0_g;
                     core::mma_values<NB>(acc, qv, r0 + wrow0, lane, F_out, p.B, scl ? sc : nullptr,
-                                         MODEL && s_ep.add_res ? cur + s_ep.res_off + row0_g : nullptr, ld,
+                                         MODEL && s_ep.add_res && warp % s_ep.kn == s_ep.kidx
+                                             ? cur + s_ep.res_off + row0_g : nullptr, ld,
                                          s_ep.res_ks, s_ep.res_sys != 0, s_tail + T_OVF,
                                          MODEL && s_ep.res2_off >= 0 ? cur + s_ep.res2_off + row0_g : nullptr,
                                          s_ep.res2_ks);
@@ -1035,7 +1044,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_chain(ChainParams p) {
                     long long qv[2 * NB];
                     const long long off = (long long)(s_run & 1u) * p.arena_words + s_ep.y_off + row0_g;
                     core::set_values<NB, G>(acc, qv, r0 + wrow0, lane, F_out, p.B,
-                                            MODEL && s_ep.add_res ? cur + s_ep.res_off + row0_g : nullptr, ld,
+                                            MODEL && s_ep.add_res && warp % s_ep.kn == s_ep.kidx
+                                                ? cur + s_ep.res_off + row0_g : nullptr, ld,
                                             s_ep.res_ks, s_ep.res_sys != 0, s_tail + T_OVF,
                                             MODEL && s_ep.res2_off >= 0 ? cur + s_ep.res2_off + row0_g : nullptr,
                                             s_ep.res2_ks);
