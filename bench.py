@@ -202,6 +202,30 @@ def llama_timed(model, steps, warmup, rank, world):
     return timed(g, steps, warmup, rank, world), g
 
 
+def llama_sustained(g, seconds=2.5):
+    """Sustained decode (burst vs sustained): the one-step CUDA graph
+    replayed back to back for >= `seconds` (long enough for the 1 kW board power
+    cap to act), CUDA events around chunks of 200 replays; tok/s over the whole
+    window and over its last half, with the clocks sampled during it."""
+    import torch
+    chunks = []
+    t_end = time.time() + seconds
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        while time.time() < t_end:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(200):
+                g.replay()
+            e1.record()
+            e1.synchronize()
+            chunks.append(e0.elapsed_time(e1))
+    tot_ms = sum(chunks)
+    half = chunks[len(chunks) // 2:]
+    return {"seconds": round(tot_ms / 1e3, 2), "tok_s": round(200 * len(chunks) * 1e3 / tot_ms, 1),
+            "tok_s_last_half": round(200 * len(half) * 1e3 / sum(half), 1),
+            "ms_per_token_last_half": round(sum(half) / (200 * len(half)), 4), "clocks": clk.summary()}
+
+
 def llama_kernel_ms(model, reps, world):
     """Per-kernel device time of the two launches of a step (chain, lm_head):
     eager steps with CUDA events before / between (fasq_llama_step_ex
@@ -1036,6 +1060,11 @@ def main():
             side["prefill_token_sharded"] = prefill_token_sharded(world, rank, float(peaks.get("bf16_tflops", 1692.0)))
         except Exception as e:
             side["prefill_token_sharded"] = {"error": str(e)[:300]}
+    if rank == 0 and world == 1 and not args.no_side:
+        try:
+            side["sustained_decode"] = llama_sustained(g)
+        except Exception as e:
+            side["sustained_decode"] = {"error": str(e)[:300]}
     if rank == 0 and not args.no_side:
         del g
         for name, fn in (("pq_chain", lambda: pq_chain_side(peak)),
@@ -1058,6 +1087,19 @@ def main():
         r, thr, sample, _ = oracle_decode_rate(budget_s=15.0)
         cpu = {"value": r, "unit": "tok/s", "cores": thr, "kind": "oracle", "sample": sample,
                "cpu": _cpu_model()}
+        try:   # the same on one thread, and the oracle's pack of configs[0]
+            import oracle
+            import synth
+            oracle.set_threads(1)
+            r1, _, sample1, _ = oracle_decode_rate(budget_s=3.0)
+            oracle.set_threads(thr)
+            W0 = synth.weight(256, 512, seed=0)
+            t0 = time.perf_counter()
+            oracle.pack(W0, d=4, C=256, group=128, seed=0, iters=25)
+            cpu["one_thread"] = {"value": r1, "sample": sample1}
+            cpu["pack_config0_seconds"] = round(time.perf_counter() - t0, 3)
+        except Exception as e:
+            cpu["one_thread"] = {"error": str(e)[:200]}
 
     if rank == 0:
         line = {
