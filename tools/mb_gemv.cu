@@ -44,7 +44,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     static_assert(VAR != 3 || R == 64 * NW, "");
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* s_cb = smem;
-    uint8_t* s_idx = s_cb + (VAR >= 2 ? 2 * 65536 : ST * CBB);
+    uint8_t* s_idx = s_cb + (VAR == 5 ? ST * CBB + 65536 : VAR >= 2 ? 2 * 65536 : ST * CBB);
     uint8_t* s_x = s_idx + ST * IDXB;                     // [64][E] (VAR 0) / [32][E] (VAR 1)
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_x + 64 * E);
     const uint32_t cb_u = dev::smem_u32(s_cb), idx_u = dev::smem_u32(s_idx), x_u = dev::smem_u32(s_x);
@@ -181,6 +181,70 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
         transpose_reduce32<NW>(hi, lane);
         out[blockIdx.x * R + warp * 64 + lane] = lo[0];
         out[blockIdx.x * R + warp * 64 + 32 + lane] = hi[0];
+    } else if (VAR == 5) {
+        // G3: per group, the 16 consumer warps build the fp32 LUT
+        // [C][32 subspaces] = dot(x_s, c_s[k]) from the staged codebook (double-
+        // buffered next to the codebook ring: lut[g & 1]), one named barrier, then
+        // lane = subspace gathers its row's LUT entry (PRMT with the 256-B paired
+        // row trick: the two LUT buffers interleave as [C][2][32] words) and adds
+        // it: PRMT, LDS, then FADD2 over two rows' entries (f32x2).
+        float acc[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+        const uint32_t wrow = (uint32_t)warp * 64u * 32u + (uint32_t)lane * 64u;
+        const uint32_t swz = (uint32_t)(lane >> 1);
+        const uint32_t lut_u = cb_u + (uint32_t)ST * CBB;        // [C][2][32] fp32 = 64 KiB
+        const int tid = threadIdx.x;
+        for (int g = 0; g < ng; ++g) {
+            const int slot = g % ST;
+            if (MODE != 2 || g < ST) dev::mbar_wait(full0 + 8 * slot, (g / ST) & 1);
+            const uint32_t h = (uint32_t)(g & 1);
+            if (MODE != 1 && MODE != 3) {
+                // build: entry (k, s) of buffer h at word k*64 + 32h + s
+                for (int e = tid; e < C * 32; e += NW * 32) {
+                    const uint32_t k = (uint32_t)e >> 5, sub = (uint32_t)e & 31u;
+                    const uint32_t cv = dev::lds32(cb_u + slot * CBB + (uint32_t)e * 4u);
+                    const uint32_t xs = dev::lds32(x_u + sub * 4u);
+                    const float v = dev::fhfma2(cv, xs, 0.f);
+                    asm volatile("st.shared.f32 [%0], %1;" :: "r"(lut_u + k * 256u + h * 128u + sub * 4u), "f"(v) : "memory");
+                }
+            }
+            asm volatile("bar.sync 1, %0;" :: "n"(NW * 32) : "memory");
+            if (MODE != 1 && MODE != 3) {
+                const uint32_t ib = idx_u + slot * IDXB + wrow;
+                const uint32_t Lc = h * 128u + (uint32_t)lane * 4u;   // byte 0 of the PRMT address
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const uint4 v = dev::lds128(ib + 16u * ((c + swz) & 3u));
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int q = 0; q < 16; q += 2) {
+                        const uint32_t a0 = dev::prmt(w[q >> 2], Lc, 0x7740u | ((uint32_t)(q & 3) << 4) | 4u);
+                        const uint32_t a1 = dev::prmt(w[(q + 1) >> 2], Lc, 0x7740u | ((uint32_t)((q + 1) & 3) << 4) | 4u);
+                        float e0, e1;
+                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e0) : "r"(lut_u + a0));
+                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e1) : "r"(lut_u + a1));
+                        float& x0 = acc[c * 16 + q];
+                        float& x1 = acc[c * 16 + q + 1];
+                        asm("{.reg .b64 a, b;\n\tmov.b64 a, {%0, %1};\n\tmov.b64 b, {%2, %3};\n\t"
+                            "add.rn.f32x2 a, a, b;\n\tmov.b64 {%0, %1}, a;}"
+                            : "+f"(x0), "+f"(x1) : "f"(e0), "f"(e1));
+                    }
+                }
+            }
+            __syncwarp();
+            if (MODE != 2 && lane == 0) dev::mbar_arrive(empty0 + 8 * slot);
+        }
+        float lo[32], hi[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            lo[i] = acc[i];
+            hi[i] = acc[32 + i];
+        }
+        transpose_reduce32<NW>(lo, lane);
+        transpose_reduce32<NW>(hi, lane);
+        out[blockIdx.x * R + warp * 64 + lane] = lo[0];
+        out[blockIdx.x * R + warp * 64 + 32 + lane] = hi[0];
     } else if (VAR == 2) {
         float acc[64];
 #pragma unroll
@@ -264,7 +328,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 template <int VAR, int RPL, int NW, int ST, int MODE>
 void run(const uint8_t* idx, const uint8_t* cb, int ng, float* out, int nsm, const char* name) {
     constexpr int R = VAR == 0 ? 32 * NW * RPL : 64 * NW;
-    const size_t smem = (VAR >= 2 ? 2 * 65536 - (long)ST * CBB : 0) + ST * (CBB + (size_t)R * 32) + 64 * E + 16 * ST;
+    const size_t smem = (VAR == 5 ? 65536 : VAR >= 2 ? 2 * 65536 - (long)ST * CBB : 0) + ST * (CBB + (size_t)R * 32) +
+                        64 * E + 16 * ST;
     auto kern = k_mb<VAR, RPL, NW, ST, MODE>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         printf("%-28s smem %zu too large\n", name, smem);
@@ -313,6 +378,7 @@ int main() {
     run<VAR, RPL, NW, ST, 1>(idx, cb, ng, out, nsm, NAME);    \
     run<VAR, RPL, NW, ST, 2>(idx, cb, ng, out, nsm, NAME);    \
     run<VAR, RPL, NW, ST, 3>(idx, cb, ng, out, nsm, NAME);
+    RUN3(5, 1, 16, 2, "G3 lut nw16 st2");
     RUN3(1, 1, 16, 3, "sub  nw16 st3");
     RUN3(2, 1, 16, 2, "sub256 nw16 st2");
     RUN3(4, 1, 16, 2, "pair+ldg nw16 st2");
