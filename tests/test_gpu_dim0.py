@@ -162,3 +162,20 @@ def test_dim0_errors(F):
     with pytest.raises(F.FasqError):
         F.import_layer(torch.from_numpy(cb3).cuda(), torch.zeros((42, 64), dtype=torch.uint8).cuda(), 64,
                        dim0=True)
+
+
+def test_dim0_host_and_large_batch(F, oracle_lib):
+    """dim = 0 layers through fasq_gemv_host (host buffers) and fasq_gemv with
+    B > 8 (fasq_gemm's GEMV slices)."""
+    F_out, F_in = 512, 1024
+    cb, idx = _layer(F_out, F_in, 2, 256, 1, seed=41)
+    L = _import(F, cb, idx, F_in)
+    x = synth.activation(2, F_in, seed=42)
+    y_host = torch.empty((2, F_out), dtype=torch.float32)
+    F.gemv_host(L, torch.from_numpy(x), y_host)
+    ok, m = parity_ok(y_host.numpy(), oracle_lib.gemm_dim0(cb, idx, x), x, F_in)
+    assert ok, m
+    X = synth.activation(11, F_in, seed=43)
+    Y = F.gemv(L, torch.from_numpy(X).cuda()).float().cpu().numpy()
+    ok, m = parity_ok(Y, oracle_lib.gemm_dim0(cb, idx, X), X, F_in)
+    assert ok, m

@@ -181,3 +181,26 @@ def test_packed_errors(F):
     with pytest.raises(F.FasqError) as e:               # the decode chain reads byte indices only
         F.Chain([([L], None)])
     assert e.value.code == -6
+
+
+def test_packed_shard_host_and_large_batch(F, oracle_lib):
+    """Packed layers through the other entry points: fasq_shard_rows (row shards
+    keep the packed layout and export the same rows), fasq_gemv_host (host
+    buffers) and fasq_gemv with B > 8 (dispatched to fasq_gemm's GEMV slices)."""
+    F_out, F_in, C = 1024, 512, 512
+    cb, idx = synth.random_layer(F_out, F_in, 2, C, seed=31)
+    L = _import(F, cb, idx, F_in)
+    for r in range(2):
+        S = L.shard_rows(r, 2)
+        assert S.index_bits == 9 and S.F_out == F_out // 2
+        _, sidx = _export_np(S)
+        assert np.array_equal(sidx, idx[:, r * 512:(r + 1) * 512])
+    x = synth.activation(3, F_in, seed=32)
+    y_host = torch.empty((3, F_out), dtype=torch.float32)
+    F.gemv_host(L, torch.from_numpy(x), y_host)
+    ok, m = parity_ok(y_host.numpy(), oracle_lib.gemv(cb, idx, x), x, F_in)
+    assert ok, m
+    X = synth.activation(12, F_in, seed=33)
+    Y = F.gemv(L, torch.from_numpy(X).cuda()).float().cpu().numpy()
+    ok, m = parity_ok(Y, oracle_lib.gemm(cb, idx, X), X, F_in)
+    assert ok, m
