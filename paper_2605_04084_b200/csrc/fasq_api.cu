@@ -231,7 +231,10 @@ fasq_status fasq_gemv_ex(const fasq_layer* L, const void* x_dev, int32_t B, void
     if (!L || !x_dev || !y_dev) return FASQ_E_ARG;
     if (B < 1) return FASQ_E_ARG;
     if (yt != FASQ_F16 && yt != FASQ_F32) return FASQ_E_ARG;
-    if (B > 8) {   // batch beyond the decode kernels: the prefill GEMM path (P:410 dispatch)
+    if (B > 8) {   // beyond the CUDA-core decode kernels (P:410 dispatch)
+        // B <= 64: the tcgen05 decode kernel (weights as the UMMA M operand); else the prefill GEMM
+        if (B <= 64 && B >= gemv_tc_min_batch() && gemv_tc_supported(L, B) && !(flags & ~FASQ_FLAG_PDL))
+            return gemv_tc_launch(L, static_cast<const __half*>(x_dev), B, y_dev, yt, flags, (cudaStream_t)stream);
         if (flags) return FASQ_E_UNSUPPORTED;
         return fasq_gemm(L, x_dev, B, y_dev, yt, FASQ_GEMM_AUTO, stream);
     }

@@ -138,6 +138,12 @@ fasq_status gemv_dim0_launch(const fasq_layer* L, const __half* x, int B, void* 
                              cudaStream_t st);
 // out[j][i] = in[i][j] for fp16 [rows][cols] (dim = 0 pack)
 fasq_status transpose_f16(const __half* in, __half* out, int64_t rows, int64_t cols, cudaStream_t st);
+// G5 / NEXT-3: batched decode (B <= 64) on tcgen05, weights as the UMMA A operand (gemv_tc.cu)
+bool gemv_tc_supported(const fasq_layer* L, int B);
+constexpr int kGemvTcMinBatch = 5;   // measured crossover (profiles/r02/gemv_tc_sweep.jsonl)
+int gemv_tc_min_batch();
+fasq_status gemv_tc_launch(const fasq_layer* L, const __half* X, int B, void* y, fasq_dtype yt, uint32_t flags,
+                           cudaStream_t st);
 // NEXT-2: decode GEMV on a packed layer (gemv_packed.cu), B = 1..8
 fasq_status gemv_packed_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt, uint32_t flags,
                                cudaStream_t st);
@@ -145,7 +151,7 @@ fasq_status copy_rows(const fasq_layer* src, fasq_layer* dst, int32_t row0, cuda
 // Device memory through the library allocator (alloc.cu, fasq_set_allocator).
 fasq_status dev_alloc(void** p, size_t bytes, cudaStream_t st);
 void dev_free(void* p, cudaStream_t st);
-enum { WS_GEMV = 0, WS_GEMM_TC = 1, WS_GEMM_LUT = 2, WS_KINDS = 3 };
+enum { WS_GEMV = 0, WS_GEMM_TC = 1, WS_GEMM_LUT = 2, WS_GEMV_TC = 3, WS_KINDS = 4 };
 fasq_status stream_workspace(cudaStream_t st, int purpose, size_t bytes, void** out);   // alloc.cu
 template <class T>
 inline fasq_status dev_alloc_t(T** p, size_t bytes, cudaStream_t st) {

@@ -628,10 +628,20 @@ fasq_status acc_convert_launch(const void* acc, int64_t n, void* out, fasq_dtype
     return FASQ_OK;
 }
 
+int gemv_tc_min_batch() {
+    // the smallest decode batch routed to the tcgen05 kernel (FASQ_GEMV_TC_MIN_B overrides;
+    // 0 or > 64 disables it); default from profiles/r02/gemv_tc_sweep.jsonl
+    const char* e = getenv("FASQ_GEMV_TC_MIN_B");
+    const int v = e ? atoi(e) : kGemvTcMinBatch;
+    return v <= 0 ? 1 << 30 : v;
+}
+
 fasq_status gemv_launch(const fasq_layer* L, const __half* x, int B, void* y, fasq_dtype yt, uint32_t flags,
                         cudaStream_t st) {
     if (L->bits) return gemv_packed_launch(L, x, B, y, yt, flags, st);   // NEXT-2 packed indices
     if (L->dim0) return gemv_dim0_launch(L, x, B, y, yt, flags, st);     // NEXT-4 output-axis subspaces
+    // batched decode on tcgen05 (gemv_tc.cu) from B >= FASQ_GEMV_TC_MIN_B (measured default below)
+    if (B >= gemv_tc_min_batch() && gemv_tc_supported(L, B)) return gemv_tc_launch(L, x, B, y, yt, flags, st);
     void* ys[1] = {y};
     return gemv_grouped_launch(&L, 1, x, B, ys, yt, flags, st);
 }

@@ -169,10 +169,11 @@ def test_gemm_lut_split_k_short_L(F, oracle_lib, monkeypatch, F_out, F_in, M, ks
     L.free()
 
 
-@pytest.mark.parametrize("B", [9, 16, 33, 64])
+@pytest.mark.parametrize("B", [9, 16, 33, 64, 80])
 def test_gemv_large_batch_dispatches_to_gemm(F, oracle_lib, B):
-    """NEXT-3: fasq_gemv with B > 8 runs the prefill GEMM (AUTO ->
-    EXPAND on the tensor cores for d = 2); same product, oracle parity."""
+    """NEXT-3: fasq_gemv with B > 8 runs the tcgen05 decode kernel up to
+    B = 64 (gemv_tc.cu, PDL allowed) and the prefill GEMM above (AUTO -> EXPAND,
+    no flags); same product, oracle parity."""
     cb, idx = synth.random_layer(2048, 4096, 2, 256, seed=B)
     x = synth.activation(B, 4096, seed=B + 1)
     L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), 4096, 1)
@@ -181,8 +182,12 @@ def test_gemv_large_batch_dispatches_to_gemm(F, oracle_lib, B):
     ref = oracle_lib.gemm(cb, idx[:, :256], x)
     ok, info = parity_ok(y[:, :256].cpu().numpy().astype(np.float64), ref, x, 4096)
     assert ok, info
-    with pytest.raises(F.FasqError):
-        F.gemv(L, torch.from_numpy(x).cuda(), out_dtype=torch.float32, flags=F.FLAG_PDL)
+    if B <= 64:
+        y2 = F.gemv(L, torch.from_numpy(x).cuda(), out_dtype=torch.float32, flags=F.FLAG_PDL)
+        assert torch.equal(y2, y)
+    else:
+        with pytest.raises(F.FasqError):
+            F.gemv(L, torch.from_numpy(x).cuda(), out_dtype=torch.float32, flags=F.FLAG_PDL)
     L.free()
 
 
