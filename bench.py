@@ -874,6 +874,24 @@ def dim0_gemv_side(peak):
     return out
 
 
+def batch_gemv_side(peak):
+    """NEXT-3 / G5: per-launch decode GEMV at B = 8 / 16 / 64 on the tcgen05 decode
+    kernel (gemv_tc.cu; the default dispatch for B >= 5) next to the CUDA-core
+    GEMV (B = 8) / prefill EXPAND (B > 8) it replaces, Llama-3-8B shapes."""
+    from tools.gemv_tc_sweep import run
+    out = {}
+    for B in (8, 16, 64):
+        per = {}
+        for (o, i) in ((4096, 4096), (14336, 4096), (4096, 14336)):
+            tc = run(o, i, B, True, iters=50)
+            base = run(o, i, B, False, iters=50)
+            per["%dx%d" % (o, i)] = {"tcgen05_us": tc["us"], "tcgen05_GBps": tc["GBps"],
+                                     "tcgen05_frac": round(tc["GBps"] / peak, 3), "previous_path_us": base["us"]}
+        out["B%d" % B] = per
+    os.environ.pop("FASQ_GEMV_TC_MIN_B", None)
+    return out
+
+
 def pack_time():
     """GPU k-means pack (Alg. 1, 25 Lloyd rounds, d=2, C=256) of one seeded
     layer of each Llama-3-8B shape, and the whole-model estimate (x 32 blocks);
@@ -1076,7 +1094,8 @@ def main():
                          ("prefill_model", lambda: prefill_model(float(peaks.get("bf16_tflops", 1692.0)))),
                          ("gpu_pack", pack_time),
                          ("packed_gemv", lambda: packed_gemv_side(peak)),
-                         ("dim0_gemv", lambda: dim0_gemv_side(peak))):
+                         ("dim0_gemv", lambda: dim0_gemv_side(peak)),
+                         ("batch_gemv", lambda: batch_gemv_side(peak))):
             try:
                 side[name] = fn()
             except Exception as e:  # report, never hide
