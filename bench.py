@@ -276,24 +276,22 @@ def llama_split(model, ms_step, n_layers=32):
 
 
 def llama_e2e(model, steps, warmup, rank, world):
-    """End to end through the public C-ABI calls with HOST buffers: every step
-    copies the B tokens to decode from pinned host memory (fasq_llama_reset,
-    H2D) and runs fasq_llama_step_host (chain + lm_head + D2H of the chosen
-    tokens); wall clock around K synchronous steps, max over ranks."""
+    """End to end through the public C-ABI call with HOST buffers: every step
+    (fasq_llama_step_io) copies the B tokens to decode to the device (through
+    the model's pinned staging), runs the chain + lm_head and copies the chosen
+    tokens back; wall clock around K synchronous steps, max over ranks."""
     import torch
     import torch.distributed as dist
     toks = [128000 + b for b in range(model.B)]
     model.reset(toks, PROMPT)
     for _ in range(warmup):
-        toks = model.step_host()
-        model.reset(toks, -1)
+        toks = model.step_io(toks, -1)
     if world > 1:
         torch.cuda.synchronize()
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
-        model.reset(toks, -1)
-        toks = model.step_host()
+        toks = model.step_io(toks, -1)   # H2D of the tokens, chain + lm_head, D2H of the choice: one sync
     dt = (time.perf_counter() - t0) * 1e3 / steps
     if world > 1:
         t = torch.tensor([dt], device="cuda")
@@ -1139,8 +1137,8 @@ def main():
                        "timing": "CUDA graph of one step (2 launches), K replays between CUDA events, max over ranks"},
             "e2e": {"value": B * 1000.0 / ms_e2e, "unit": "tok/s", "h2d_bytes_per_step": 4 * B,
                     "d2h_bytes_per_step": 4 * B,
-                    "how": "per step fasq_llama_reset (H2D of the B tokens from pinned host memory) + "
-                           "fasq_llama_step_host (chain + lm_head + D2H of the chosen tokens), wall clock"},
+                    "how": "per step fasq_llama_step_io: H2D of the B tokens (pinned staging), chain + lm_head, "
+                           "D2H of the chosen tokens, one synchronisation; wall clock"},
             "gpu_launches": 2 * args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _ncu_traffic("k_chain"),

@@ -405,6 +405,12 @@ fasq_status fasq_llama_tokens(const fasq_llama* model, int32_t* tokens_dev, void
 /* End to end with a HOST buffer: one step, then the chosen tokens are copied
  * to tokens_out_host (int32 [B]).  Synchronous. */
 fasq_status fasq_llama_step_host(fasq_llama* model, int32_t* tokens_out_host, void* stream);
+/* End to end in one call: the B tokens tokens_in_host (int32, host) are decoded
+ * at position pos (< 0: the current position) -- fasq_llama_reset + one step +
+ * the chosen tokens to tokens_out_host -- with a single synchronisation (the
+ * inputs go through the model's pinned staging).  Synchronous. */
+fasq_status fasq_llama_step_io(fasq_llama* model, const int32_t* tokens_in_host, int32_t pos,
+                               int32_t* tokens_out_host, void* stream);
 /* Diagnostics: enable (1) / disable (0) writing the lm_head logits (fp32
  * [B][vocab/world]) of every later step; *logits_dev receives the buffer. */
 fasq_status fasq_llama_logits(fasq_llama* model, int32_t enable, void** logits_dev);

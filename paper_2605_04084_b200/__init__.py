@@ -39,7 +39,7 @@ EXPORTED = ["fasq_pack", "fasq_import", "fasq_import_ex", "fasq_export", "fasq_s
             "fasq_llama_create", "fasq_llama_ipc_handle", "fasq_llama_set_peers", "fasq_llama_set_peer_models",
             "fasq_llama_chain",
             "fasq_llama_kv_cache", "fasq_llama_reset", "fasq_llama_step", "fasq_llama_step_ex", "fasq_llama_tokens",
-            "fasq_llama_step_host", "fasq_llama_logits", "fasq_llama_token_history", "fasq_llama_free",
+            "fasq_llama_step_host", "fasq_llama_step_io", "fasq_llama_logits", "fasq_llama_token_history", "fasq_llama_free",
             "fasq_last_launch_count", "fasq_status_string", "fasq_last_error_message",
             "fasq_abi_version", "fasq_set_allocator", "fasq_layer_distinct_centroids"]
 
@@ -144,6 +144,7 @@ def _load():
     L.fasq_llama_tokens.argtypes = [vp, vp, vp]
     L.fasq_llama_step_ex.argtypes = [vp, vp, i32]
     L.fasq_llama_step_host.argtypes = [vp, ctypes.POINTER(i32), vp]
+    L.fasq_llama_step_io.argtypes = [vp, ctypes.POINTER(i32), i32, ctypes.POINTER(i32), vp]
     L.fasq_llama_logits.argtypes = [vp, i32, pp]
     L.fasq_llama_token_history.argtypes = [vp, vp, vp]
     L.fasq_llama_free.argtypes = [vp]
@@ -626,6 +627,14 @@ class Llama:
         arr = (ctypes.c_int32 * self.B)()
         _check(lib.fasq_llama_step_host(self._h, arr, _stream(stream)))
         return list(arr)
+
+    def step_io(self, tokens, pos: int = -1, stream=None):
+        """fasq_llama_step_io: decode `tokens` (host list of B ints) at `pos`
+        (-1: the current position) and return the chosen tokens; one sync."""
+        tin = (ctypes.c_int32 * self.B)(*tokens)
+        tout = (ctypes.c_int32 * self.B)()
+        _check(lib.fasq_llama_step_io(self._h, tin, pos, tout, _stream(stream)))
+        return list(tout)
 
     def enable_logits(self, on: bool = True):
         p = ctypes.c_void_p()

@@ -43,6 +43,8 @@ struct fasq_llama {
     int* tok_hist = nullptr;
     float* logits = nullptr;           // optional debug output (fasq_llama_logits)
     int* tok_dev = nullptr;            // staging for fasq_llama_step_host / reset
+    int* tok_pin = nullptr;            // pinned host staging [16] (in 0..7, out 8..15) of fasq_llama_step_io
+    cudaGraphExec_t io_exec = nullptr; // fasq_llama_step_io at pos < 0: the whole step as one graph launch
     int lm_ctas = 0;
     int n_heads_l = 0, n_kv_l = 0, ffn_l = 0, vocab_l = 0;
     int last_step = 0;                 // chain step of the last down projection
@@ -209,6 +211,8 @@ void destroy_model(fasq_llama* m) {
     dev_free(m->tok_hist, 0);
     dev_free(m->logits, 0);
     dev_free(m->tok_dev, 0);
+    if (m->tok_pin) cudaFreeHost(m->tok_pin);
+    if (m->io_exec) cudaGraphExecDestroy(m->io_exec);
     delete m;
 }
 
@@ -310,6 +314,10 @@ fasq_status fasq_llama_create(const fasq_llama_desc* d, void* stream, fasq_llama
     if (const char* e = getenv("FASQ_ATTN_PARTS")) parts = std::max(1, std::min(4, atoi(e)));
     if (dev_alloc_t(&m->tok_hist, (size_t)D.B * D.max_T * 4, st) != FASQ_OK || dev_alloc_t(&m->tok_dev, 64, st) != FASQ_OK)
         return fail(FASQ_E_OOM, "");
+    if (cudaHostAlloc(&m->tok_pin, 64, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FASQ_E_OOM, "pinned token staging");
+    }
     cudaMemsetAsync(m->tok_hist, 0, (size_t)D.B * D.max_T * 4, st);
     // step list: 0 = EMBED; block l: 1+5l qkv, 2+5l attn, 3+5l o(+h), 4+5l gate/up, 5+5l down(+h')
     std::vector<StepDesc> steps;
@@ -477,6 +485,67 @@ fasq_status fasq_llama_step_host(fasq_llama* m, int32_t* tokens_out_host, void* 
         if (e != cudaSuccess) s = cuda_fail(e, "llama step_host");
     }
     if (s == FASQ_OK) set_launch_count(3);
+    return s;
+}
+
+fasq_status fasq_llama_step_io(fasq_llama* m, const int32_t* tokens_in_host, int32_t pos, int32_t* tokens_out_host,
+                               void* stream) {
+    if (!m || !tokens_in_host || !tokens_out_host) return FASQ_E_ARG;
+    if (pos >= m->desc.max_T) return FASQ_E_ARG;
+    const int B = m->desc.B;
+    for (int b = 0; b < B; ++b)
+        if (tokens_in_host[b] < 0 || tokens_in_host[b] >= m->desc.vocab) return FASQ_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    // the input tokens go through the model's pinned staging (the copy is truly
+    // asynchronous and the caller's buffer is free on return); ONE synchronisation
+    // at the end instead of fasq_llama_reset's + fasq_llama_step_host's two
+    auto enqueue = [&](cudaStream_t q, int p) -> fasq_status {
+        cudaError_t e = cudaMemcpyAsync(m->tok_dev, m->tok_pin, (size_t)B * 4, cudaMemcpyHostToDevice, q);
+        if (e != cudaSuccess) return cuda_fail(e, "llama step_io H2D");
+        k_llama_reset<<<1, 32, 0, q>>>(m->chain->tail(), m->chain->nctas, m->tok_dev, B, p,
+                                       (long long)m->desc.world * m->lm_ctas);
+        FASQ_CUDA_TRY(cudaGetLastError());
+        fasq_status s = chain_launch(m->chain, m->rope, q);
+        if (s == FASQ_OK) s = lm_launch(m, q);
+        if (s != FASQ_OK) return s;
+        k_llama_tokens<<<1, 32, 0, q>>>(m->chain->tail(), m->chain->nctas, B, (long long)m->desc.world * m->lm_ctas,
+                                        m->tok_dev + 8);
+        FASQ_CUDA_TRY(cudaGetLastError());
+        FASQ_CUDA_TRY(cudaMemcpyAsync(m->tok_pin + 8, m->tok_dev + 8, (size_t)B * 4, cudaMemcpyDeviceToHost, q));
+        return FASQ_OK;
+    };
+    for (int b = 0; b < B; ++b) m->tok_pin[b] = tokens_in_host[b];
+    fasq_status s = FASQ_OK;
+    if (pos < 0 && getenv("FASQ_LLAMA_IO_GRAPH") == nullptr) {
+        // continue at the current position: the six operations as ONE graph launch
+        // (captured once on a private stream; the graph's addresses are the model's)
+        if (!m->io_exec) {
+            cudaStream_t cs;
+            FASQ_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            cudaGraph_t g = nullptr;
+            cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+            if (e == cudaSuccess) {
+                s = enqueue(cs, -1);
+                e = cudaStreamEndCapture(cs, &g);
+            }
+            if (e == cudaSuccess && s == FASQ_OK) e = cudaGraphInstantiate(&m->io_exec, g, 0);
+            if (g) cudaGraphDestroy(g);
+            cudaStreamDestroy(cs);
+            if (s != FASQ_OK) return s;
+            if (e != cudaSuccess) { m->io_exec = nullptr; return cuda_fail(e, "llama step_io graph"); }
+        }
+        FASQ_CUDA_TRY(cudaGraphLaunch(m->io_exec, st));
+    } else {
+        s = enqueue(st, pos);
+    }
+    if (s == FASQ_OK) {
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) s = cuda_fail(e, "llama step_io");
+    }
+    if (s == FASQ_OK) {
+        for (int b = 0; b < B; ++b) tokens_out_host[b] = m->tok_pin[8 + b];
+        set_launch_count(4);
+    }
     return s;
 }
 

@@ -232,6 +232,14 @@ def test_llama_decode_deterministic_and_replayable(F):
     # step_host (end-to-end host API) continues the sequence
     t = model.step_host()
     assert 0 <= t[0] < cfg["vocab"]
+    # step_io (host tokens in and out, one sync) reproduces the greedy sequence:
+    # feeding each chosen token back gives the device-side history
+    hist = runs[0][1][0].cpu().tolist()          # tokens embedded at positions 0..3
+    tok = model.step_io([5], 0)
+    assert tok[0] == hist[1]
+    for pos in (1, 2):
+        tok = model.step_io(tok, -1)
+        assert tok[0] == hist[pos + 1]
     model.free()
 
 
