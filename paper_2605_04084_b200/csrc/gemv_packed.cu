@@ -42,6 +42,7 @@ struct PackedParams {
     long long* acc;         // split-K workspace [B][F_out_pad] (zeroed, self-cleaning)
     unsigned* cnt;          // [B][F_out_pad]
     int F_out, F_out_pad, F_in, N_ss, n_groups, C, ksplit, B, y_mode, cs, st;
+    int gmax;               // max groups per CTA (x staging capacity)
 };
 
 template <int BITS, int NB>
@@ -124,24 +125,24 @@ __global__ void __launch_bounds__((kPW + 1) * 32, 1) k_gemv_packed(PackedParams 
         for (int b = 0; b < NB; ++b) acc[r][b] = 0.f;
 
     dev::pdl_wait();   // x (and the outputs we add into) are the previous kernel's
-    auto load_x = [&](int g, uint32_t (&xv)[NB]) {
-        const int ss = g * 32 + lane;
-#pragma unroll
-        for (int b = 0; b < NB; ++b)
-            xv[b] = (b < p.B && ss < p.N_ss)
-                        ? __ldg(reinterpret_cast<const unsigned int*>(p.x + (size_t)b * p.F_in) + ss)
-                        : 0u;
-    };
-    uint32_t xn[NB];
-    if (ng > 0) load_x(g_begin, xn);
+    // x of the whole K range -> SMEM [group][32 lanes][NB] words once (one global
+    // load per word, all in flight) instead of per-group loads on the critical
+    // path (ncu: long-scoreboard stalls 5 per issue)
+    uint32_t* s_x = reinterpret_cast<uint32_t*>(bars + 2 * ST + 2 * CS);
+    for (int e = threadIdx.x; e < ng * 32 * NB; e += kPW * 32) {
+        const int gl = e / (32 * NB), rem = e - gl * 32 * NB, sl = rem / NB, b = rem - sl * NB;
+        const int ss = (g_begin + gl) * 32 + sl;
+        s_x[e] = (b < p.B && ss < p.N_ss) ? __ldg(reinterpret_cast<const unsigned int*>(p.x + (size_t)b * p.F_in) + ss)
+                                          : 0u;
+    }
+    asm volatile("bar.sync 1, %0;" :: "n"(kPW * 32) : "memory");
 
     int slot = 0, cslot = 0;
     uint32_t par = 0, cpar = 0;
     for (int i = 0; i < ng; ++i) {
         uint32_t xv[NB];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) xv[b] = xn[b];
-        if (i + 1 < ng) load_x(g_begin + i + 1, xn);   // next group's x in flight during this one
+        for (int b = 0; b < NB; ++b) xv[b] = s_x[(i * 32 + lane) * NB + b];
         dev::mbar_wait(full0 + 8 * slot, par);
         dev::mbar_wait(cfull0 + 8 * cslot, cpar);
         if (active) {
@@ -336,20 +337,22 @@ fasq_status gemv_packed_launch(const fasq_layer* L, const __half* x, int B, void
     const int RW = 64 / NB, R = RW * kPW;
     const size_t CBB = (size_t)L->C * 128;
     const size_t IDXB = (size_t)(R / 64) * 32 * L->seg;
-    // rings: two codebook slots when they fit next to two index stages, else one
-    int cs = 2, stg = 3;
-    auto smem_of = [&](int c, int s) { return (size_t)c * CBB + (size_t)s * IDXB + 16 * (size_t)(c + s); };
-    while (stg > 2 && smem_of(cs, stg) > kSmemMax) --stg;
-    if (smem_of(cs, stg) > kSmemMax) cs = 1;
-    while (stg > 1 && smem_of(cs, stg) > kSmemMax) --stg;
-    const size_t smem = smem_of(cs, stg);
-    if (smem > kSmemMax) { set_error("gemv (packed): codebook image too large"); return FASQ_E_UNSUPPORTED; }
     // grid: row tiles x K-splits over groups, ~ one CTA per SM, equal groups per CTA
     const int row_tiles = (L->F_out_pad + R - 1) / R;
     int ks = std::max(1, num_sms_packed() / row_tiles);
     ks = std::min(ks, L->n_groups);
     const int gper = (L->n_groups + ks - 1) / ks;
     ks = (L->n_groups + gper - 1) / gper;
+    // rings: two codebook slots when they fit next to two index stages, else one;
+    // plus the K range's x ([gper][32][NB] words)
+    const size_t xbytes = (size_t)gper * 32 * NB * 4;
+    int cs = 2, stg = 3;
+    auto smem_of = [&](int c, int s) { return (size_t)c * CBB + (size_t)s * IDXB + 16 * (size_t)(c + s) + xbytes; };
+    while (stg > 2 && smem_of(cs, stg) > kSmemMax) --stg;
+    if (smem_of(cs, stg) > kSmemMax) cs = 1;
+    while (stg > 1 && smem_of(cs, stg) > kSmemMax) --stg;
+    const size_t smem = smem_of(cs, stg);
+    if (smem > kSmemMax) { set_error("gemv (packed): codebook image too large"); return FASQ_E_UNSUPPORTED; }
 
     PackedParams p{};
     p.idx = L->idx;
@@ -367,6 +370,7 @@ fasq_status gemv_packed_launch(const fasq_layer* L, const __half* x, int B, void
     p.y_mode = yt == FASQ_ACC_I64 ? 2 : yt == FASQ_F32 ? 1 : 0;
     p.cs = cs;
     p.st = stg;
+    p.gmax = gper;
     uint8_t* ws_call = nullptr;
     if (ks > 1 && p.y_mode != 2) {
         // per-(stream, purpose) workspace shared with gemv.cu (stream-ordered, self-cleaning)
