@@ -244,3 +244,22 @@ def test_gemv_acc_mode_and_chain(F, oracle_lib):
     ref2 = oracle_lib.gemv(cb2, idx2, x2)
     ok, info = parity_ok(y2, ref2, x2, 2048)
     assert ok, info
+
+
+@pytest.mark.parametrize("F_out,F_in,B", [(1000, 640, 5), (1000, 640, 7), (4096, 1024, 16), (3000, 2048, 33),
+                                          (14336, 4096, 8), (700, 4096, 64)])
+def test_gemv_tc_batched_decode(F, oracle_lib, F_out, F_in, B):
+    """The tcgen05 batched-decode kernel (gemv_tc.cu, B >= 5): ragged row tiles
+    (384 rows per CTA), token tiles NT = 16 / 32 / 64 with zero-filled rows past
+    B, split-K slices; fp32 and fp16 outputs, PDL, run-to-run bit identity."""
+    cb, idx = synth.random_layer(F_out, F_in, 2, 256, seed=F_out + B)
+    x = synth.activation(B, F_in, seed=B)
+    L = _import(F, cb, idx, F_in, 1)
+    rows = (0, F_out) if F_out <= 4096 else (F_out - 512, F_out)
+    y = _gemv(F, L, x)
+    ok, m = parity_ok(y[:, rows[0]:rows[1]], oracle_lib.gemv(cb, idx, x, rows=rows), x, F_in)
+    assert ok, m
+    assert np.array_equal(_gemv(F, L, x, flags=F.FLAG_PDL), y)
+    yh = _gemv(F, L, x, out_dtype=torch.float16)
+    ok, m = parity_ok(yh[:, rows[0]:rows[1]], oracle_lib.gemv(cb, idx, x, rows=rows), x, F_in)
+    assert ok, m
