@@ -183,37 +183,9 @@ __device__ __forceinline__ void embed_item(const ChainPhase* ph, unsigned long l
         asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(slot + 1), "l"(0ull) : "memory");
     }
     consumer_bar(NT);
-    // 16-B loads (8 elements), up to 8 in flight per thread: at B = 8 the whole
-    // [8][4096] gather is ONE round of loads per thread (the 2-B version needed 8
-    // dependent rounds: 48 us of the B = 8 token; a load -> store chain per
-    // element before that cost 7 us at B = 1, 38 us at B = 8)
+    // 8 rows' loads in flight per thread (a load -> store chain per element
+    // serialised one HBM round trip per iteration: 7 us at B = 1, 38 us at B = 8)
     const int n = ph->hidden;
-    if ((n & 7) == 0) {
-        const int nv = B * n / 8, vpr = n / 8;
-        constexpr int U = 8;
-        for (int v0 = tid; v0 < nv; v0 += NT * U) {
-            uint4 v[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int vi = v0 + u * NT;
-                v[u] = make_uint4(0u, 0u, 0u, 0u);
-                if (vi < nv) {
-                    const int b = vi / vpr, c8 = vi - b * vpr;
-                    v[u] = __ldg(reinterpret_cast<const uint4*>(ph->embed + (size_t)s_tok[b] * n) + c8);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int vi = v0 + u * NT;
-                if (vi >= nv) continue;
-                const __half* h = reinterpret_cast<const __half*>(&v[u]);
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    st_word(cur + ph->e_off + (size_t)vi * 8 + e, cnt_word(__float2ll_rn(__half2float(h[e]) * core::kAccScale)));
-            }
-        }
-        return;
-    }
     constexpr int U = 8;
     for (int i0 = tid; i0 < B * n; i0 += NT * U) {
         float v[U];
