@@ -3,6 +3,7 @@
 // kernels of layout.cu / gemv.cu / gemm_*.cu / pack.cu.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -232,8 +233,8 @@ fasq_status fasq_gemv_ex(const fasq_layer* L, const void* x_dev, int32_t B, void
     if (B < 1) return FASQ_E_ARG;
     if (yt != FASQ_F16 && yt != FASQ_F32) return FASQ_E_ARG;
     if (B > 8) {   // beyond the CUDA-core decode kernels (P:410 dispatch)
-        // B <= 64: the tcgen05 decode kernel (weights as the UMMA M operand); else the prefill GEMM
-        if (B <= 64 && B >= gemv_tc_min_batch() && gemv_tc_supported(L, B) && !(flags & ~FASQ_FLAG_PDL))
+        // B <= 128: the tcgen05 decode kernel (weights as the UMMA M operand); else the prefill GEMM
+        if (B <= 128 && B >= gemv_tc_min_batch() && gemv_tc_supported(L, B) && !(flags & ~FASQ_FLAG_PDL))
             return gemv_tc_launch(L, static_cast<const __half*>(x_dev), B, y_dev, yt, flags, (cudaStream_t)stream);
         if (flags) return FASQ_E_UNSUPPORTED;
         return fasq_gemm(L, x_dev, B, y_dev, yt, FASQ_GEMM_AUTO, stream);
@@ -319,6 +320,13 @@ fasq_status fasq_gemv_host(const fasq_layer* L, const void* x_host, int32_t B, v
     return s;
 }
 
+// measured crossover against EXPAND (profiles/r02/short_gemm_sweep.jsonl): M <= 128 on the
+// 4096-row layers, M <= 96 on the 14336-row ones (more row tiles: EXPAND fills the SMs)
+static int64_t gemm_short_max(const fasq_layer* L) {
+    const char* e = getenv("FASQ_GEMM_TC_DECODE_MAX");
+    return e ? atoll(e) : (L->F_out > 8192 ? 96 : 128);
+}
+
 fasq_status fasq_gemm(const fasq_layer* L, const void* X_dev, int64_t M, void* Y_dev, fasq_dtype yt,
                       fasq_gemm_algo algo, void* stream) {
     if (!L || !X_dev || !Y_dev) return FASQ_E_ARG;
@@ -349,6 +357,10 @@ fasq_status fasq_gemm(const fasq_layer* L, const void* X_dev, int64_t M, void* Y
             if (!gemm_tc_supported(L, M)) return FASQ_E_UNSUPPORTED;
             return gemm_tc_launch(L, X, M, Y_dev, yt, st);
         case FASQ_GEMM_AUTO:
+            // short L (M <= FASQ_GEMM_TC_DECODE_MAX, default 128): the tcgen05 decode kernel
+            // (weights as UMMA M, tokens as N); the 256-token EXPAND tiles run mostly empty there
+            if (M <= gemm_short_max(L) && gemv_tc_supported(L, (int)M))
+                return gemv_tc_launch(L, X, (int)M, Y_dev, yt, 0u, st);
             if (gemm_tc_supported(L, M)) return gemm_tc_launch(L, X, M, Y_dev, yt, st);
             return gemm_lut_launch(L, X, M, Y_dev, yt, st);
     }

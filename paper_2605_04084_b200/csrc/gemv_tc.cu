@@ -231,9 +231,11 @@ __global__ void __launch_bounds__(TT_THREADS, 1) k_gemv_tc(const __grid_constant
         for (int m = grp; m < TT_MS; m += TT_EXP / 4) {
             const int rl = m * 128 + q * 32 + lane;            // row within the CTA tile
             const int row = n0 + rl;
-            float f[NT];
-#pragma unroll
+            // 16 token columns at a time: TMEM -> registers -> y (or the split-K
+            // partial tile); bounded registers for NT up to 128
+#pragma unroll 1
             for (int c0 = 0; c0 < NT; c0 += 16) {
+                if (c0 >= p.B) break;
                 uint32_t r[16];
                 const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(m * NT + c0);
                 asm volatile(
@@ -244,23 +246,23 @@ __global__ void __launch_bounds__(TT_THREADS, 1) k_gemv_tc(const __grid_constant
                       "=r"(r[14]), "=r"(r[15])
                     : "r"(taddr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (ksplit == 1) {
+                    if (row < p.F_out) {
 #pragma unroll
-                for (int v = 0; v < 16; ++v) f[c0 + v] = __uint_as_float(r[v]);
-            }
-            if (ksplit == 1) {
-                if (row < p.F_out) {
-#pragma unroll
-                    for (int t = 0; t < NT; ++t) {
-                        if (t >= p.B) break;
-                        if (p.y_f32) reinterpret_cast<float*>(p.y)[(size_t)t * p.F_out + row] = f[t];
-                        else reinterpret_cast<__half*>(p.y)[(size_t)t * p.F_out + row] = __float2half_rn(f[t]);
+                        for (int v = 0; v < 16; ++v) {
+                            const int t = c0 + v;
+                            if (t >= p.B) break;
+                            const float fv = __uint_as_float(r[v]);
+                            if (p.y_f32) reinterpret_cast<float*>(p.y)[(size_t)t * p.F_out + row] = fv;
+                            else reinterpret_cast<__half*>(p.y)[(size_t)t * p.F_out + row] = __float2half_rn(fv);
+                        }
                     }
-                }
-            } else {
-                float* wr = p.ws + ((size_t)kz * p.row_tiles + tile) * NT * TT_R;
+                } else {
+                    float* wr = p.ws + ((size_t)kz * p.row_tiles + tile) * NT * TT_R;
 #pragma unroll
-                for (int t = 0; t < NT; ++t)
-                    if (t < p.B) __stcg(wr + (size_t)t * TT_R + rl, f[t]);
+                    for (int v = 0; v < 16; ++v)
+                        if (c0 + v < p.B) __stcg(wr + (size_t)(c0 + v) * TT_R + rl, __uint_as_float(r[v]));
+                }
             }
         }
         if (ksplit > 1) {
@@ -349,15 +351,15 @@ fasq_status launch_tt(const CUtensorMap& map, const TtParams& p, dim3 grid, size
 }  // namespace
 
 bool gemv_tc_supported(const fasq_layer* L, int B) {
-    return L->d == 2 && L->C <= 256 && !L->bits && !L->dim0 && (L->F_in % 64) == 0 && B >= 1 && B <= 64 &&
-           tt_smem(B <= 16 ? 16 : B <= 32 ? 32 : 64, L->C) <= kSmemMax && get_encode() != nullptr;
+    return L->d == 2 && L->C <= 256 && !L->bits && !L->dim0 && (L->F_in % 64) == 0 && B >= 1 && B <= 128 &&
+           tt_smem(B <= 16 ? 16 : B <= 32 ? 32 : B <= 64 ? 64 : 128, L->C) <= kSmemMax && get_encode() != nullptr;
 }
 
 fasq_status gemv_tc_launch(const fasq_layer* L, const __half* X, int B, void* y, fasq_dtype yt, uint32_t flags,
                            cudaStream_t st) {
     if (!gemv_tc_supported(L, B)) return FASQ_E_UNSUPPORTED;
     if ((reinterpret_cast<uintptr_t>(X) & 15) != 0) return FASQ_E_ARG;
-    const int NT = B <= 16 ? 16 : B <= 32 ? 32 : 64;
+    const int NT = B <= 16 ? 16 : B <= 32 ? 32 : B <= 64 ? 64 : 128;
     PFN_encodeTiled enc = get_encode();
     CUtensorMap map;
     cuuint64_t gdim[2] = {(cuuint64_t)L->F_in, (cuuint64_t)B};
@@ -411,7 +413,8 @@ fasq_status gemv_tc_launch(const fasq_layer* L, const __half* X, int B, void* y,
     switch (NT) {
         case 16: s = launch_tt<16>(map, p, grid, smem, flags, st); break;
         case 32: s = launch_tt<32>(map, p, grid, smem, flags, st); break;
-        default: s = launch_tt<64>(map, p, grid, smem, flags, st); break;
+        case 64: s = launch_tt<64>(map, p, grid, smem, flags, st); break;
+        default: s = launch_tt<128>(map, p, grid, smem, flags, st); break;
     }
     dev_free(ws_call, st);
     if (s == FASQ_OK) set_launch_count(1);

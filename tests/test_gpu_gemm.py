@@ -169,10 +169,10 @@ def test_gemm_lut_split_k_short_L(F, oracle_lib, monkeypatch, F_out, F_in, M, ks
     L.free()
 
 
-@pytest.mark.parametrize("B", [9, 16, 33, 64, 80])
+@pytest.mark.parametrize("B", [9, 16, 33, 64, 80, 128, 140])
 def test_gemv_large_batch_dispatches_to_gemm(F, oracle_lib, B):
     """NEXT-3: fasq_gemv with B > 8 runs the tcgen05 decode kernel up to
-    B = 64 (gemv_tc.cu, PDL allowed) and the prefill GEMM above (AUTO -> EXPAND,
+    B = 128 (gemv_tc.cu, PDL allowed) and the prefill GEMM above (AUTO -> EXPAND,
     no flags); same product, oracle parity."""
     cb, idx = synth.random_layer(2048, 4096, 2, 256, seed=B)
     x = synth.activation(B, 4096, seed=B + 1)
@@ -182,7 +182,7 @@ def test_gemv_large_batch_dispatches_to_gemm(F, oracle_lib, B):
     ref = oracle_lib.gemm(cb, idx[:, :256], x)
     ok, info = parity_ok(y[:, :256].cpu().numpy().astype(np.float64), ref, x, 4096)
     assert ok, info
-    if B <= 64:
+    if B <= 128:
         y2 = F.gemv(L, torch.from_numpy(x).cuda(), out_dtype=torch.float32, flags=F.FLAG_PDL)
         assert torch.equal(y2, y)
     else:
@@ -212,3 +212,20 @@ def test_gemm_tc_pair_cta_group2(F, oracle_lib, monkeypatch, F_out, F_in, M):
     Y1 = F.gemm(L, Xd, algo=F.GEMM_EXPAND_TC).float().cpu().numpy()
     rel = np.linalg.norm(Y - Y1) / np.linalg.norm(Y1)
     assert rel <= 1e-6, rel
+
+
+@pytest.mark.parametrize("F_out,F_in,M", [(4096, 4096, 128), (14336, 4096, 96), (1000, 2048, 77)])
+def test_gemm_auto_short_L_runs_tcgen05_decode(F, oracle_lib, F_out, F_in, M):
+    """Short-L prefill (NEXT-3): fasq_gemm AUTO with M <= 96 / 128 runs
+    the tcgen05 decode kernel (weights as UMMA M); sampled rows against the oracle
+    and against the EXPAND kernel's Y."""
+    cb, idx = synth.random_layer(F_out, F_in, 2, 256, seed=M)
+    X = synth.activation(M, F_in, seed=M + 1)
+    L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), F_in)
+    Xd = torch.from_numpy(X).cuda()
+    Y = F.gemm(L, Xd).float().cpu().numpy()
+    rows = (F_out // 2 - 64, F_out // 2 + 64)
+    ok, m = parity_ok(Y[:, rows[0]:rows[1]], oracle_lib.gemm(cb, idx, X, rows=rows), X, F_in)
+    assert ok, m
+    Ye = F.gemm(L, Xd, algo=F.GEMM_EXPAND_TC).float().cpu().numpy()
+    assert np.linalg.norm(Y - Ye) / np.linalg.norm(Ye) <= 1e-5

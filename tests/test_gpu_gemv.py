@@ -177,8 +177,8 @@ def test_gemv_host_e2e(F, oracle_lib):
 def test_errors(F):
     cb, idx = synth.random_layer(64, 64, 2, 16, seed=1)
     L = _import(F, cb, idx, 64, 1)
-    with pytest.raises(F.FasqError):   # B > 64 runs fasq_gemm: flags are not supported there
-        F.gemv(L, torch.zeros((65, 64), dtype=torch.float16, device="cuda"), flags=F.FLAG_PDL)
+    with pytest.raises(F.FasqError):   # B > 128 runs fasq_gemm: flags are not supported there
+        F.gemv(L, torch.zeros((129, 64), dtype=torch.float16, device="cuda"), flags=F.FLAG_PDL)
     with pytest.raises(F.FasqError):
         F.gemv(L, torch.zeros((1, 32), dtype=torch.float16, device="cuda"))   # shape
     with pytest.raises(F.FasqError) as e:
