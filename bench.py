@@ -622,12 +622,13 @@ KINDS = (("qkv", ("q_proj", "k_proj", "v_proj")), ("o", ("o_proj",)), ("gate_up"
          ("down", ("down_proj",)))
 
 
-def prefill_model(dense_peak, Ms=(512, 2048), reps=3):
+def prefill_model(dense_peak, Ms=(128, 512, 2048), reps=3):
     """configs[4] at N = 1: the prefill pass of the whole PQ linear stack --
     M tokens through the 224 Llama-3-8B-shaped PQ layers with fasq_gemm
-    (EXPAND, tcgen05), fp16 activations chained block to block like the decode
-    chain (q/k/v and gate/up read the same input); attention/norms excluded.
-    Replayed from a CUDA graph; tok/s = M / pass time."""
+    (AUTO: the tcgen05 decode kernel at M = 128 -- the paper's prompt length,
+    P:438 -- EXPAND on tcgen05 above), fp16 activations chained block to block
+    like the decode chain (q/k/v and gate/up read the same input); attention /
+    norms excluded.  Replayed from a CUDA graph; tok/s = M / pass time."""
     import torch
 
     import paper_2605_04084_b200 as F
@@ -646,6 +647,7 @@ def prefill_model(dense_peak, Ms=(512, 2048), reps=3):
     flops = 2.0 * nb * sum(fo * fi for (fo, fi) in shapes.values())
     out = {}
     for M in Ms:
+        algo = F.GEMM_AUTO if M <= 128 else F.GEMM_EXPAND_TC
         x0 = synth.torch_activation(M, 4096)
         bufs = {n: torch.empty((M, fo), dtype=torch.float16, device="cuda") for n, (fo, fi) in shapes.items()}
 
@@ -653,11 +655,11 @@ def prefill_model(dense_peak, Ms=(512, 2048), reps=3):
             h = x0
             for Ls in blocks:
                 for n in ("q_proj", "k_proj", "v_proj"):
-                    F.gemm(Ls[n], h, out=bufs[n], algo=F.GEMM_EXPAND_TC)
-                F.gemm(Ls["o_proj"], bufs["q_proj"], out=bufs["o_proj"], algo=F.GEMM_EXPAND_TC)
+                    F.gemm(Ls[n], h, out=bufs[n], algo=algo)
+                F.gemm(Ls["o_proj"], bufs["q_proj"], out=bufs["o_proj"], algo=algo)
                 for n in ("gate_proj", "up_proj"):
-                    F.gemm(Ls[n], bufs["o_proj"], out=bufs[n], algo=F.GEMM_EXPAND_TC)
-                F.gemm(Ls["down_proj"], bufs["gate_proj"], out=bufs["down_proj"], algo=F.GEMM_EXPAND_TC)
+                    F.gemm(Ls[n], bufs["o_proj"], out=bufs[n], algo=algo)
+                F.gemm(Ls["down_proj"], bufs["gate_proj"], out=bufs["down_proj"], algo=algo)
                 h = bufs["down_proj"]
         gs = torch.cuda.Stream()
         gs.wait_stream(torch.cuda.current_stream())
