@@ -226,6 +226,38 @@ def llama_sustained(g, seconds=2.5):
             "ms_per_token_last_half": round(sum(half) / (200 * len(half)), 4), "clocks": clk.summary()}
 
 
+def llama_prefill_side(model, M=PROMPT, reps=5):
+    """The paper's E2E protocol on the bench model: a 128-token prompt
+    through fasq_llama_prefill (whole model: RMSNorm, PQ q/k/v/o/gate/up/down on
+    the tcgen05 decode kernel at M = 128, RoPE, KV-cache write, causal attention,
+    SwiGLU, residuals, lm_head + argmax of the last position), then 128 greedy
+    decode steps (one CUDA graph per step); CUDA events."""
+    import torch
+    toks = torch.arange(1000, 1000 + M, dtype=torch.int32, device="cuda")
+    model.prefill(toks, 0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        model.prefill(toks, 0)
+    e1.record()
+    torch.cuda.synchronize()
+    pf_ms = e0.elapsed_time(e1) / reps
+    g = capture(lambda: model.step(), 1)
+    model.prefill(toks, 0)
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record()
+    model.prefill(toks, 0)
+    for _ in range(MAX_T - PROMPT):
+        g.replay()
+    e3.record()
+    torch.cuda.synchronize()
+    tot = e2.elapsed_time(e3)
+    return {"prompt": M, "prefill_ms": round(pf_ms, 3), "prefill_tok_s": round(M * 1e3 / pf_ms, 1),
+            "e2e_prompt128_gen128_ms": round(tot, 2),
+            "e2e_gen_tok_s": round((MAX_T - PROMPT) * 1e3 / (tot - pf_ms), 1)}
+
+
 def llama_kernel_ms(model, reps, world):
     """Per-kernel device time of the two launches of a step (chain, lm_head):
     eager steps with CUDA events before / between (fasq_llama_step_ex
@@ -1083,6 +1115,10 @@ def main():
             side["sustained_decode"] = llama_sustained(g)
         except Exception as e:
             side["sustained_decode"] = {"error": str(e)[:300]}
+        try:
+            side["prefill_e2e"] = llama_prefill_side(model)
+        except Exception as e:
+            side["prefill_e2e"] = {"error": str(e)[:300]}
     if rank == 0 and not args.no_side:
         del g
         for name, fn in (("pq_chain", lambda: pq_chain_side(peak)),

@@ -120,3 +120,30 @@ def lm_head_logits(h, final_norm, W_lm, eps: float) -> np.ndarray:
 def greedy(logits) -> int:
     """argmax with ties to the lowest token id (numpy's first maximum)."""
     return int(np.argmax(np.asarray(logits)))
+
+
+def prefill(tokens, layers, embed, k_cache, v_cache, pos0: int, n_heads: int, n_kv: int, eps: float, theta: float):
+    """Causal prefill of ONE sequence: the prompt tokens at positions pos0, pos0+1, ...
+    By definition of causal attention this is the decode step applied to each
+    prompt token in order with the KV cache growing (no blocking, no batching).
+    k_cache / v_cache: per layer, per KV head, python lists of fp16-valued rows for
+    positions < pos0 (extended in place).  Returns the last position's h_out and
+    the per-layer new K/V rows [M][n_kv][hd]."""
+    new_k = [[] for _ in layers]
+    new_v = [[] for _ in layers]
+    h = None
+    for i, t in enumerate(tokens):
+        pos = pos0 + i
+        h = np.asarray(embed[t], np.float64)
+        for l, L in enumerate(layers):
+            hd = L["q"][1].shape[1] // n_heads          # q rows (T_index [N_ss][F_out]) / heads
+            K = [np.asarray(k_cache[l][j], np.float64).reshape(len(k_cache[l][j]), hd) for j in range(n_kv)]
+            V = [np.asarray(v_cache[l][j], np.float64).reshape(len(v_cache[l][j]), hd) for j in range(n_kv)]
+            r = block_decode(h, L, pos, K, V, n_heads, n_kv, eps, theta)
+            for j in range(n_kv):
+                k_cache[l][j].append(r["k_new"][j])
+                v_cache[l][j].append(r["v_new"][j])
+            new_k[l].append(r["k_new"])
+            new_v[l].append(r["v_new"])
+            h = r["h_out"]
+    return h, [np.array(x) for x in new_k], [np.array(x) for x in new_v]

@@ -39,7 +39,7 @@ EXPORTED = ["fasq_pack", "fasq_import", "fasq_import_ex", "fasq_export", "fasq_s
             "fasq_llama_create", "fasq_llama_ipc_handle", "fasq_llama_set_peers", "fasq_llama_set_peer_models",
             "fasq_llama_chain",
             "fasq_llama_kv_cache", "fasq_llama_reset", "fasq_llama_step", "fasq_llama_step_ex", "fasq_llama_tokens",
-            "fasq_llama_step_host", "fasq_llama_step_io", "fasq_llama_logits", "fasq_llama_token_history", "fasq_llama_free",
+            "fasq_llama_step_host", "fasq_llama_step_io", "fasq_llama_prefill", "fasq_llama_logits", "fasq_llama_token_history", "fasq_llama_free",
             "fasq_last_launch_count", "fasq_status_string", "fasq_last_error_message",
             "fasq_abi_version", "fasq_set_allocator", "fasq_layer_distinct_centroids"]
 
@@ -145,6 +145,7 @@ def _load():
     L.fasq_llama_step_ex.argtypes = [vp, vp, i32]
     L.fasq_llama_step_host.argtypes = [vp, ctypes.POINTER(i32), vp]
     L.fasq_llama_step_io.argtypes = [vp, ctypes.POINTER(i32), i32, ctypes.POINTER(i32), vp]
+    L.fasq_llama_prefill.argtypes = [vp, vp, i32, i32, vp]
     L.fasq_llama_logits.argtypes = [vp, i32, pp]
     L.fasq_llama_token_history.argtypes = [vp, vp, vp]
     L.fasq_llama_free.argtypes = [vp]
@@ -627,6 +628,15 @@ class Llama:
         arr = (ctypes.c_int32 * self.B)()
         _check(lib.fasq_llama_step_host(self._h, arr, _stream(stream)))
         return list(arr)
+
+    def prefill(self, tokens, pos0: int = 0, stream=None):
+        """fasq_llama_prefill: run the prompt `tokens` (device int32 tensor or
+        list) at positions pos0.. through the whole model; the next step()
+        decodes the greedy continuation."""
+        if not isinstance(tokens, torch.Tensor):
+            tokens = torch.tensor(tokens, dtype=torch.int32, device="cuda")
+        t = _cuda(tokens, torch.int32, "tokens")
+        _check(lib.fasq_llama_prefill(self._h, t.data_ptr(), t.numel(), pos0, _stream(stream)))
 
     def step_io(self, tokens, pos: int = -1, stream=None):
         """fasq_llama_step_io: decode `tokens` (host list of B ints) at `pos`

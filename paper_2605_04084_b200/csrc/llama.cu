@@ -239,6 +239,173 @@ fasq_status lm_launch(fasq_llama* m, cudaStream_t st) {
 
 using namespace fasq;
 
+
+// ---- whole-model PREFILL (the paper's E2E protocol: a 128-token prompt) ----
+// M prompt tokens of sequence 0 through every block with the prefill products
+// (fasq_gemm AUTO: the tcgen05 decode kernel for M <= 128, EXPAND above) and
+// plain kernels for the glue; it writes the KV cache of positions [pos0, pos0+M)
+// and hands the decode chain the greedy token of the last prompt position at
+// position pos0 + M.  Same arithmetic as the decode step (HF Llama, R14): fp32
+// residual stream, fp16 PQ inputs and KV cache, RMSNorm as x = fp16(h * r * gamma).
+namespace fasq {
+namespace {
+
+__global__ void k_pf_embed(const int* __restrict__ tok, const __half* __restrict__ E, float* __restrict__ h, int M,
+                           int n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)M * n) return;
+    const int m = (int)(i / n), c = (int)(i - (int64_t)m * n);
+    h[i] = __half2float(E[(size_t)tok[m] * n + c]);
+}
+
+// one CTA per row: x[m] = fp16(h[m] / sqrt(mean(h[m]^2) + eps) * gamma)
+__global__ void k_pf_rmsnorm(const float* __restrict__ h, const __half* __restrict__ gamma, __half* __restrict__ x,
+                             int n, float eps, int row0) {
+    const int m = row0 + (int)blockIdx.x;
+    const float* hr = h + (size_t)m * n;
+    float a = 0.f;
+    for (int c = threadIdx.x; c < n; c += blockDim.x) a += hr[c] * hr[c];
+    __shared__ float red[32];
+    for (int o = 16; o >= 1; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float b = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+        for (int o = 16; o >= 1; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+        if (threadIdx.x == 0) red[0] = b;
+    }
+    __syncthreads();
+    const float r = 1.0f / sqrtf(red[0] / (float)n + eps);
+    for (int c = threadIdx.x; c < n; c += blockDim.x)
+        x[(size_t)(m - row0) * n + c] = __float2half_rn(hr[c] * r * __half2float(gamma[c]));
+}
+
+// RoPE on q (in place, fp32) and k; the new k (rotated) / v enter the cache as fp16
+__global__ void k_pf_rope_cache(float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
+                                __half* __restrict__ kc, __half* __restrict__ vc, const float2* __restrict__ rope,
+                                int M, int pos0, int H, int KV, int hd, int max_T) {
+    const int half = hd / 2;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int per = (H + 2 * KV) * half;   // rotation pairs (q, k) and v pairs per token
+    if (i >= (int64_t)M * per) return;
+    const int m = (int)(i / per), r = (int)(i - (int64_t)m * per);
+    const int pos = pos0 + m;
+    if (r < H * half) {
+        const int hh = r / half, e = r - hh * half;
+        const float2 cs = rope[(size_t)pos * half + e];
+        float* qr = q + (size_t)m * H * hd + (size_t)hh * hd;
+        const float q0 = qr[e], q1 = qr[e + half];
+        qr[e] = q0 * cs.x - q1 * cs.y;
+        qr[e + half] = q1 * cs.x + q0 * cs.y;
+    } else if (r < (H + KV) * half) {
+        const int j = (r - H * half) / half, e = (r - H * half) - j * half;
+        const float2 cs = rope[(size_t)pos * half + e];
+        const float* kr = k + (size_t)m * KV * hd + (size_t)j * hd;
+        const float k0 = kr[e], k1 = kr[e + half];
+        __half* dst = kc + ((size_t)j * max_T + pos) * hd;
+        dst[e] = __float2half_rn(k0 * cs.x - k1 * cs.y);
+        dst[e + half] = __float2half_rn(k1 * cs.x + k0 * cs.y);
+    } else {
+        const int j = (r - (H + KV) * half) / half, e = (r - (H + KV) * half) - j * half;
+        const float* vr = v + (size_t)m * KV * hd + (size_t)j * hd;
+        __half* dst = vc + ((size_t)j * max_T + pos) * hd;
+        dst[e] = __float2half_rn(vr[e]);
+        dst[e + half] = __float2half_rn(vr[e + half]);
+    }
+}
+
+// causal GQA attention: one warp per (token m, q head); lane holds DPL = hd / 32
+// consecutive dims (hd = 64 or 128); one pass over the positions t <= pos0 + m
+// with an online softmax
+template <int DPL>
+__global__ void k_pf_attn(const float* __restrict__ q, const __half* __restrict__ kc, const __half* __restrict__ vc,
+                          __half* __restrict__ out, int M, int pos0, int H, int KV, int max_T) {
+    constexpr int hd = 32 * DPL;
+    const int wg = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (wg >= M * H) return;
+    const int m = wg / H, hh = wg - m * H, j = hh / (H / KV), pos = pos0 + m;
+    const float sc = 1.0f / sqrtf((float)hd);
+    const float* qr = q + (size_t)m * H * hd + (size_t)hh * hd + DPL * lane;
+    float qv[DPL], o[DPL];
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) { qv[e] = qr[e]; o[e] = 0.f; }
+    const __half* K = kc + (size_t)j * max_T * hd + DPL * lane;
+    const __half* V = vc + (size_t)j * max_T * hd + DPL * lane;
+    float mx = -INFINITY, l = 0.f;
+    for (int t = 0; t <= pos; ++t) {
+        __half kh[DPL], vh[DPL];
+#pragma unroll
+        for (int e = 0; e < DPL; e += 2) {
+            *reinterpret_cast<__half2*>(kh + e) = *reinterpret_cast<const __half2*>(K + (size_t)t * hd + e);
+            *reinterpret_cast<__half2*>(vh + e) = *reinterpret_cast<const __half2*>(V + (size_t)t * hd + e);
+        }
+        float s = 0.f;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) s += qv[e] * __half2float(kh[e]);
+        for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        s *= sc;
+        const float mn = fmaxf(mx, s), cf = expf(mx - mn), p = expf(s - mn);
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) o[e] = o[e] * cf + p * __half2float(vh[e]);
+        l = l * cf + p;
+        mx = mn;
+    }
+    __half* dst = out + (size_t)m * H * hd + (size_t)hh * hd + DPL * lane;
+    const float inv = 1.0f / l;
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) dst[e] = __float2half_rn(o[e] * inv);
+}
+
+__global__ void k_pf_silu_mul(const float* __restrict__ g, const float* __restrict__ u, __half* __restrict__ a,
+                              int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float x = g[i];
+    a[i] = __float2half_rn(x / (1.0f + expf(-x)) * u[i]);
+}
+
+__global__ void k_pf_add(float* __restrict__ h, const float* __restrict__ y, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) h[i] += y[i];
+}
+
+__device__ __forceinline__ unsigned long long pf_key(float f, unsigned tok) {
+    const unsigned b = __float_as_uint(f);
+    const unsigned ord = (b & 0x80000000u) ? ~b : (b | 0x80000000u);   // order-preserving
+    return ((unsigned long long)ord << 32) | (unsigned long long)(0xFFFFFFFFu - tok);   // ties -> lowest id
+}
+
+// lm_head of ONE token: a warp per vocab row (16-B loads), max of (logit, ~token) keys
+__global__ void k_pf_lm_argmax(const __half* __restrict__ W, const __half* __restrict__ x, int V, int n,
+                               unsigned long long* __restrict__ best) {
+    const int row = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (row >= V) return;
+    const uint4* wr = reinterpret_cast<const uint4*>(W + (size_t)row * n);
+    const uint4* xr = reinterpret_cast<const uint4*>(x);
+    float a = 0.f;
+    for (int c = lane; c < n / 8; c += 32) {
+        const uint4 wv = __ldg(wr + c), xv = xr[c];
+        const __half2* w2 = reinterpret_cast<const __half2*>(&wv);
+        const __half2* x2 = reinterpret_cast<const __half2*>(&xv);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 wf = __half22float2(w2[e]), xf = __half22float2(x2[e]);
+            a += wf.x * xf.x + wf.y * xf.y;
+        }
+    }
+    for (int o = 16; o >= 1; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) atomicMax(best, pf_key(a, (unsigned)row));
+}
+
+__global__ void k_pf_token(const unsigned long long* __restrict__ best, int* __restrict__ tok) {
+    tok[0] = (int)(0xFFFFFFFFu - (unsigned)(*best & 0xFFFFFFFFull));
+}
+
+inline unsigned pf_blocks(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+}  // namespace
+}  // namespace fasq
+
 extern "C" {
 
 fasq_status fasq_llama_create(const fasq_llama_desc* d, void* stream, fasq_llama** out) {
@@ -546,6 +713,88 @@ fasq_status fasq_llama_step_io(fasq_llama* m, const int32_t* tokens_in_host, int
         for (int b = 0; b < B; ++b) tokens_out_host[b] = m->tok_pin[8 + b];
         set_launch_count(4);
     }
+    return s;
+}
+
+fasq_status fasq_llama_prefill(fasq_llama* m, const int32_t* tokens_dev, int32_t M, int32_t pos0, void* stream) {
+    if (!m || !tokens_dev || M < 1 || pos0 < 0) return FASQ_E_ARG;
+    const fasq_llama_desc& D = m->desc;
+    if (pos0 + M > D.max_T) return FASQ_E_ARG;
+    if (D.B != 1 || D.world != 1 || (D.head_dim != 128 && D.head_dim != 64) || D.hidden % 8) {
+        set_error("llama prefill: one sequence (B = 1), one GPU, head_dim 64 or 128");
+        return FASQ_E_UNSUPPORTED;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int n = D.hidden, H = D.n_heads, KV = D.n_kv_heads, hd = D.head_dim, ffn = D.ffn;
+    const int64_t Mn = (int64_t)M * n;
+    float *h = nullptr, *q = nullptr, *k = nullptr, *v = nullptr, *y = nullptr, *g = nullptr, *u = nullptr;
+    __half *x = nullptr, *a = nullptr;
+    unsigned long long* best = nullptr;
+    fasq_status s = dev_alloc_t(&h, (size_t)Mn * 4, st);
+    if (s == FASQ_OK) s = dev_alloc_t(&q, (size_t)M * H * hd * 4, st);
+    if (s == FASQ_OK) s = dev_alloc_t(&k, (size_t)M * KV * hd * 4, st);
+    if (s == FASQ_OK) s = dev_alloc_t(&v, (size_t)M * KV * hd * 4, st);
+    if (s == FASQ_OK) s = dev_alloc_t(&y, (size_t)Mn * 4, st);
+    if (s == FASQ_OK) s = dev_alloc_t(&g, (size_t)M * ffn * 4, st);
+    if (s == FASQ_OK) s = dev_alloc_t(&u, (size_t)M * ffn * 4, st);
+    if (s == FASQ_OK) s = dev_alloc_t(&x, (size_t)M * std::max(n, std::max(ffn, H * hd)) * 2, st);
+    if (s == FASQ_OK) s = dev_alloc_t(&a, (size_t)M * std::max(ffn, H * hd) * 2, st);
+    if (s == FASQ_OK) s = dev_alloc_t(&best, 8, st);
+    auto check = [&](cudaError_t e, const char* w) { if (s == FASQ_OK && e != cudaSuccess) s = cuda_fail(e, w); };
+    auto gemm = [&](const fasq_layer* L, const __half* X, float* Y) {
+        if (s == FASQ_OK) s = fasq_gemm(L, X, M, Y, FASQ_F32, FASQ_GEMM_AUTO, st);
+    };
+    if (s == FASQ_OK) {
+        k_pf_embed<<<pf_blocks(Mn, 256), 256, 0, st>>>(tokens_dev, static_cast<const __half*>(D.embed), h, M, n);
+        check(cudaGetLastError(), "prefill embed");
+    }
+    for (int l = 0; l < D.n_layers && s == FASQ_OK; ++l) {
+        k_pf_rmsnorm<<<M, 256, 0, st>>>(h, static_cast<const __half*>(D.attn_norm[l]), x, n, D.rms_eps, 0);
+        check(cudaGetLastError(), "prefill rmsnorm");
+        gemm(D.q[l], x, q);
+        gemm(D.k[l], x, k);
+        gemm(D.v[l], x, v);
+        if (s != FASQ_OK) break;
+        k_pf_rope_cache<<<pf_blocks((int64_t)M * (H + 2 * KV) * (hd / 2), 256), 256, 0, st>>>(
+            q, k, v, m->kc[l], m->vc[l], m->rope, M, pos0, H, KV, hd, D.max_T);
+        check(cudaGetLastError(), "prefill rope");
+        if (hd == 128)
+            k_pf_attn<4><<<pf_blocks((int64_t)M * H * 32, 256), 256, 0, st>>>(q, m->kc[l], m->vc[l], a, M, pos0, H, KV,
+                                                                               D.max_T);
+        else
+            k_pf_attn<2><<<pf_blocks((int64_t)M * H * 32, 256), 256, 0, st>>>(q, m->kc[l], m->vc[l], a, M, pos0, H, KV,
+                                                                               D.max_T);
+        check(cudaGetLastError(), "prefill attention");
+        gemm(D.o[l], a, y);
+        if (s != FASQ_OK) break;
+        k_pf_add<<<pf_blocks(Mn, 256), 256, 0, st>>>(h, y, Mn);
+        k_pf_rmsnorm<<<M, 256, 0, st>>>(h, static_cast<const __half*>(D.mlp_norm[l]), x, n, D.rms_eps, 0);
+        check(cudaGetLastError(), "prefill mlp norm");
+        gemm(D.gate[l], x, g);
+        gemm(D.up[l], x, u);
+        if (s != FASQ_OK) break;
+        k_pf_silu_mul<<<pf_blocks((int64_t)M * ffn, 256), 256, 0, st>>>(g, u, a, (int64_t)M * ffn);
+        check(cudaGetLastError(), "prefill swiglu");
+        gemm(D.down[l], a, y);
+        if (s != FASQ_OK) break;
+        k_pf_add<<<pf_blocks(Mn, 256), 256, 0, st>>>(h, y, Mn);
+        check(cudaGetLastError(), "prefill residual");
+    }
+    if (s == FASQ_OK) {
+        // the last prompt position's greedy token -> the decode chain's token slot
+        k_pf_rmsnorm<<<1, 256, 0, st>>>(h, static_cast<const __half*>(D.final_norm), x, n, D.rms_eps, M - 1);
+        check(cudaMemsetAsync(best, 0, 8, st), "prefill argmax");
+        k_pf_lm_argmax<<<pf_blocks((int64_t)D.vocab * 32, 256), 256, 0, st>>>(
+            static_cast<const __half*>(D.lm_head), x, D.vocab, n, best);
+        k_pf_token<<<1, 1, 0, st>>>(best, m->tok_dev);
+        k_llama_reset<<<1, 32, 0, st>>>(m->chain->tail(), m->chain->nctas, m->tok_dev, 1, pos0 + M,
+                                        (long long)D.world * m->lm_ctas);
+        check(cudaGetLastError(), "prefill token");
+    }
+    for (void* p : {(void*)h, (void*)q, (void*)k, (void*)v, (void*)y, (void*)g, (void*)u, (void*)x, (void*)a,
+                    (void*)best})
+        dev_free(p, st);
+    if (s == FASQ_OK) set_launch_count(0);
     return s;
 }
 

@@ -330,3 +330,84 @@ def test_llama3_block_full_size(F):
         assert _rel(logits.cpu().numpy()[0], ref[st]["logits"][0]) <= 1e-3
         assert model.tokens().cpu().tolist() == ref[st]["tok_out"]
     model.free()
+
+
+@pytest.mark.parametrize("hd,M,P0", [(64, 6, 3), (128, 9, 0), (128, 1, 4)])
+def test_llama_prefill_matches_oracle(F, hd, M, P0):
+    """fasq_llama_prefill (the paper's E2E prompt phase): the KV-cache rows
+    it writes for the prompt positions, the greedy token it hands to the decode
+    chain and the first decode step after it, against the oracle's causal prefill
+    (oracle.llama.prefill: the decode step over the prompt tokens in order)."""
+    cfg = dict(SMALL, head_dim=hd, n_heads=256 // hd, n_kv=max(1, 128 // hd), hidden=256)
+    layers, fn, emb, lm = make_model(cfg, seed=31 + hd)
+    kc, vc = prompt_cache(cfg, 1, max(P0, 1), seed=32)
+    prompt = [(37 * i + 11) % cfg["vocab"] for i in range(M)]
+    ocache_k = [[list(np.asarray(kc[l, 0, j, :P0], np.float64)) for j in range(cfg["n_kv"])]
+                for l in range(cfg["n_layers"])]
+    ocache_v = [[list(np.asarray(vc[l, 0, j, :P0], np.float64)) for j in range(cfg["n_kv"])]
+                for l in range(cfg["n_layers"])]
+    h, nk, nv = ol.prefill(prompt, layers, emb, ocache_k, ocache_v, P0, cfg["n_heads"], cfg["n_kv"], 1e-5,
+                           cfg["theta"])
+    logits = ol.lm_head_logits(h, fn, lm, 1e-5)
+    top2 = np.sort(logits)[-2:]
+    assert top2[1] - top2[0] > 1e-2, "near tie; pick another seed"
+    tok = ol.greedy(logits)
+
+    model = build_gpu(F, cfg, layers, fn, emb, lm, 1)
+    for l in range(cfg["n_layers"]):
+        K, V = model.kv_cache(l)
+        K[:, :, :P0].copy_(torch.from_numpy(kc[l][:, :, :P0]).cuda())
+        V[:, :, :P0].copy_(torch.from_numpy(vc[l][:, :, :P0]).cuda())
+    model.prefill(prompt, P0)
+    torch.cuda.synchronize()
+    for l in range(cfg["n_layers"]):
+        K, V = model.kv_cache(l)
+        gk = K[0, :, P0:P0 + M].cpu().numpy().astype(np.float64).transpose(1, 0, 2)   # [M][n_kv][hd]
+        gv = V[0, :, P0:P0 + M].cpu().numpy().astype(np.float64).transpose(1, 0, 2)
+        assert _rel(gk, nk[l]) <= 3e-3 * (l + 1), (l, "k", _rel(gk, nk[l]))
+        assert _rel(gv, nv[l]) <= 3e-3 * (l + 1), (l, "v", _rel(gv, nv[l]))
+    # the decode chain continues from the prefill: its first step embeds the
+    # greedy token at position P0 + M and decodes the next one
+    lg = model.enable_logits(True)
+    model.step()
+    torch.cuda.synchronize()
+    hist = model.token_history().cpu().numpy()
+    assert hist[0, P0 + M] == tok
+    h2, _, _ = ol.prefill([tok], layers, emb, ocache_k, ocache_v, P0 + M, cfg["n_heads"], cfg["n_kv"], 1e-5,
+                          cfg["theta"])
+    ref2 = ol.lm_head_logits(h2, fn, lm, 1e-5)
+    assert _rel(lg.cpu().numpy()[0], ref2) <= 1e-2
+    model.free()
+
+
+def test_llama3_prefill_full_size(F):
+    """fasq_llama_prefill on one Llama-3-8B-shaped block at full size with the full
+    128256-token lm_head: 8 prompt tokens after a 120-position cache (the prefill
+    products at M = 8 run the tcgen05 decode kernel); K/V rows and the handed-over
+    greedy token against the oracle's causal prefill."""
+    cfg = LLAMA3
+    layers, fn, emb, lm = make_model(cfg, seed=61)
+    P0, M = 120, 8
+    kc, vc = prompt_cache(cfg, 1, P0, seed=62)
+    prompt = [128000 + i for i in range(M)]
+    ok_ = [[list(np.asarray(kc[0, 0, j], np.float64)) for j in range(cfg["n_kv"])]]
+    ov_ = [[list(np.asarray(vc[0, 0, j], np.float64)) for j in range(cfg["n_kv"])]]
+    h, nk, nv = ol.prefill(prompt, layers, emb, ok_, ov_, P0, cfg["n_heads"], cfg["n_kv"], 1e-5, cfg["theta"])
+    logits = ol.lm_head_logits(h, fn, lm, 1e-5)
+    top2 = np.sort(logits)[-2:]
+    model = build_gpu(F, cfg, layers, fn, emb, lm, 1, max_T=256)
+    K, V = model.kv_cache(0)
+    K[:, :, :P0].copy_(torch.from_numpy(kc[0]).cuda())
+    V[:, :, :P0].copy_(torch.from_numpy(vc[0]).cuda())
+    model.prefill(prompt, P0)
+    model.step()
+    torch.cuda.synchronize()
+    gk = K[0, :, P0:P0 + M].cpu().numpy().astype(np.float64).transpose(1, 0, 2)
+    gv = V[0, :, P0:P0 + M].cpu().numpy().astype(np.float64).transpose(1, 0, 2)
+    assert _rel(gk, nk[0]) <= 3e-3 and _rel(gv, nv[0]) <= 3e-3, (_rel(gk, nk[0]), _rel(gv, nv[0]))
+    tok = int(model.token_history().cpu().numpy()[0, P0 + M])
+    if top2[1] - top2[0] > 1e-2 * max(1.0, abs(top2[1])):
+        assert tok == ol.greedy(logits)
+    else:   # near tie: the chosen token is within 2 % of the maximum
+        assert logits[tok] >= top2[1] - 0.02 * abs(top2[1])
+    model.free()
