@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "chain_internal.cuh"
@@ -250,21 +251,58 @@ using namespace fasq;
 namespace fasq {
 namespace {
 
-__global__ void k_pf_embed(const int* __restrict__ tok, const __half* __restrict__ E, float* __restrict__ h, int M,
-                           int n) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (int64_t)M * n) return;
-    const int m = (int)(i / n), c = (int)(i - (int64_t)m * n);
-    h[i] = __half2float(E[(size_t)tok[m] * n + c]);
-}
-
-// one CTA per row: x[m] = fp16(h[m] / sqrt(mean(h[m]^2) + eps) * gamma)
-__global__ void k_pf_rmsnorm(const float* __restrict__ h, const __half* __restrict__ gamma, __half* __restrict__ x,
-                             int n, float eps, int row0) {
-    const int m = row0 + (int)blockIdx.x;
-    const float* hr = h + (size_t)m * n;
+// one CTA per row m = row0 + blockIdx.x: the residual update, then the RMSNorm
+// of the updated row, x[m - row0] = fp16(h[m] / sqrt(mean(h[m]^2) + eps) * gamma);
+// the update is h[m] = E[tok[m]] (tok != null: the embedding, block 0's input),
+// h[m] += y[m] (y != null: the previous product's residual add) or none.  n % 4
+// == 0; each thread keeps up to PF_NV float4 groups of the row in registers (all
+// loads issued before the reduction: one row per SM is latency-, not
+// bandwidth-bound), the rest of a longer row streams through L1
+constexpr int PF_NV = 8;
+__global__ void __launch_bounds__(256) k_pf_resid_norm(float* __restrict__ h, const float* __restrict__ y,
+                                                       const int* __restrict__ tok, const __half* __restrict__ E,
+                                                       const __half* __restrict__ gamma, __half* __restrict__ x,
+                                                       int n, float eps, int row0) {
+    const int m = row0 + (int)blockIdx.x, n4 = n / 4;
+    float4* hr = reinterpret_cast<float4*>(h + (size_t)m * n);
+    const float4* yr = y ? reinterpret_cast<const float4*>(y + (size_t)m * n) : nullptr;
+    const uint2* er = tok ? reinterpret_cast<const uint2*>(E + (size_t)tok[m] * n) : nullptr;
+    auto update = [&](int c4) -> float4 {
+        float4 v;
+        if (er) {
+            const uint2 e = er[c4];
+            const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&e.x));
+            const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&e.y));
+            v = make_float4(a.x, a.y, b.x, b.y);
+        } else {
+            v = hr[c4];
+            if (yr) {
+                const float4 d = yr[c4];
+                v.x += d.x; v.y += d.y; v.z += d.z; v.w += d.w;
+            }
+        }
+        return v;
+    };
+    float4 vals[PF_NV];
+#pragma unroll
+    for (int k = 0; k < PF_NV; ++k) {
+        const int c4 = threadIdx.x + k * blockDim.x;
+        vals[k] = c4 < n4 ? update(c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     float a = 0.f;
-    for (int c = threadIdx.x; c < n; c += blockDim.x) a += hr[c] * hr[c];
+    const bool write = er || yr;
+#pragma unroll
+    for (int k = 0; k < PF_NV; ++k) {
+        const int c4 = threadIdx.x + k * blockDim.x;
+        const float4 v = vals[k];
+        a += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+        if (write && c4 < n4) hr[c4] = v;
+    }
+    for (int c4 = threadIdx.x + PF_NV * blockDim.x; c4 < n4; c4 += blockDim.x) {
+        const float4 v = update(c4);
+        a += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+        if (write) hr[c4] = v;
+    }
     __shared__ float red[32];
     for (int o = 16; o >= 1; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
@@ -276,8 +314,22 @@ __global__ void k_pf_rmsnorm(const float* __restrict__ h, const __half* __restri
     }
     __syncthreads();
     const float r = 1.0f / sqrtf(red[0] / (float)n + eps);
-    for (int c = threadIdx.x; c < n; c += blockDim.x)
-        x[(size_t)(m - row0) * n + c] = __float2half_rn(hr[c] * r * __half2float(gamma[c]));
+    const uint2* gr = reinterpret_cast<const uint2*>(gamma);
+    uint2* xr = reinterpret_cast<uint2*>(x + (size_t)(m - row0) * n);
+    auto emit = [&](int c4, float4 v) {
+        const uint2 gg = gr[c4];
+        const float2 g0 = __half22float2(*reinterpret_cast<const __half2*>(&gg.x));
+        const float2 g1 = __half22float2(*reinterpret_cast<const __half2*>(&gg.y));
+        __half2 o[2] = {__floats2half2_rn(v.x * r * g0.x, v.y * r * g0.y),
+                        __floats2half2_rn(v.z * r * g1.x, v.w * r * g1.y)};
+        xr[c4] = *reinterpret_cast<const uint2*>(o);
+    };
+#pragma unroll
+    for (int k = 0; k < PF_NV; ++k) {
+        const int c4 = threadIdx.x + k * blockDim.x;
+        if (c4 < n4) emit(c4, vals[k]);
+    }
+    for (int c4 = threadIdx.x + PF_NV * blockDim.x; c4 < n4; c4 += blockDim.x) emit(c4, hr[c4]);   // own writes
 }
 
 // RoPE on q (in place, fp32) and k; the new k (rotated) / v enter the cache as fp16
@@ -314,40 +366,76 @@ __global__ void k_pf_rope_cache(float* __restrict__ q, const float* __restrict__
     }
 }
 
-// causal GQA attention: one warp per (token m, q head); lane holds DPL = hd / 32
-// consecutive dims (hd = 64 or 128); one pass over the positions t <= pos0 + m
-// with an online softmax
+// causal GQA attention: one warp per (token m, q head), positions t <= pos0 + m
+// in chunks of 32 with an online softmax over chunks.  Scores: lane L takes
+// position t0 + L (its K row in 16-B loads against q broadcast from shared
+// memory); P.V: lane L holds DPL = hd / 32 consecutive output dims and walks the
+// chunk's V rows (coalesced rows, independent loads in flight) -- the per-position
+// dependent chain (load, 5 shuffles, exp) of a lane-per-dim walk was latency-bound
 template <int DPL>
-__global__ void k_pf_attn(const float* __restrict__ q, const __half* __restrict__ kc, const __half* __restrict__ vc,
-                          __half* __restrict__ out, int M, int pos0, int H, int KV, int max_T) {
+__global__ void __launch_bounds__(128, 3) k_pf_attn(const float* __restrict__ q, const __half* __restrict__ kc,
+                                                 const __half* __restrict__ vc, __half* __restrict__ out, int M,
+                                                 int pos0, int H, int KV, int max_T) {
     constexpr int hd = 32 * DPL;
-    const int wg = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    __shared__ __align__(16) float qs[4][hd];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wg = (int)blockIdx.x * 4 + w;
     if (wg >= M * H) return;
     const int m = wg / H, hh = wg - m * H, j = hh / (H / KV), pos = pos0 + m;
     const float sc = 1.0f / sqrtf((float)hd);
-    const float* qr = q + (size_t)m * H * hd + (size_t)hh * hd + DPL * lane;
-    float qv[DPL], o[DPL];
+    const float* qr = q + (size_t)m * H * hd + (size_t)hh * hd;
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) { qv[e] = qr[e]; o[e] = 0.f; }
-    const __half* K = kc + (size_t)j * max_T * hd + DPL * lane;
+    for (int e = 0; e < DPL; ++e) qs[w][e * 32 + lane] = qr[e * 32 + lane];
+    __syncwarp();
+    const __half* K = kc + (size_t)j * max_T * hd;
     const __half* V = vc + (size_t)j * max_T * hd + DPL * lane;
-    float mx = -INFINITY, l = 0.f;
-    for (int t = 0; t <= pos; ++t) {
-        __half kh[DPL], vh[DPL];
+    float mx = -INFINITY, l = 0.f, o[DPL];
 #pragma unroll
-        for (int e = 0; e < DPL; e += 2) {
-            *reinterpret_cast<__half2*>(kh + e) = *reinterpret_cast<const __half2*>(K + (size_t)t * hd + e);
-            *reinterpret_cast<__half2*>(vh + e) = *reinterpret_cast<const __half2*>(V + (size_t)t * hd + e);
+    for (int e = 0; e < DPL; ++e) o[e] = 0.f;
+    for (int t0 = 0; t0 <= pos; t0 += 32) {
+        const int t = t0 + lane;
+        // the chunk's 32 V rows in flight with its K rows: rows past pos are clamped to
+        // pos (finite cache data) and weighted by p = 0
+        using VT = typename std::conditional<DPL == 4, uint2, unsigned>::type;
+        VT vr[32];
+#pragma unroll
+        for (int tt = 0; tt < 32; ++tt)
+            vr[tt] = *reinterpret_cast<const VT*>(V + (size_t)min(t0 + tt, pos) * hd);
+        float s = -INFINITY;
+        if (t <= pos) {
+            const uint4* kr = reinterpret_cast<const uint4*>(K + (size_t)t * hd);
+            uint4 kv[hd / 8];
+#pragma unroll
+            for (int c = 0; c < hd / 8; ++c) kv[c] = kr[c];
+            float acc = 0.f;
+#pragma unroll
+            for (int c = 0; c < hd / 8; ++c) {
+                const float4 qa = *reinterpret_cast<const float4*>(&qs[w][8 * c]);
+                const float4 qb = *reinterpret_cast<const float4*>(&qs[w][8 * c + 4]);
+                const __half2* k2 = reinterpret_cast<const __half2*>(&kv[c]);
+                const float2 k0 = __half22float2(k2[0]), k1 = __half22float2(k2[1]);
+                const float2 k2f = __half22float2(k2[2]), k3 = __half22float2(k2[3]);
+                acc += qa.x * k0.x + qa.y * k0.y + qa.z * k1.x + qa.w * k1.y;
+                acc += qb.x * k2f.x + qb.y * k2f.y + qb.z * k3.x + qb.w * k3.y;
+            }
+            s = acc * sc;
         }
-        float s = 0.f;
+        float cm = s;
+        for (int off = 16; off >= 1; off >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, off));
+        const float mn = fmaxf(mx, cm), cf = expf(mx - mn);
+        const float p = t <= pos ? expf(s - mn) : 0.f;
+        float ps = p;
+        for (int off = 16; off >= 1; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+        l = l * cf + ps;
 #pragma unroll
-        for (int e = 0; e < DPL; ++e) s += qv[e] * __half2float(kh[e]);
-        for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        s *= sc;
-        const float mn = fmaxf(mx, s), cf = expf(mx - mn), p = expf(s - mn);
+        for (int e = 0; e < DPL; ++e) o[e] *= cf;
 #pragma unroll
-        for (int e = 0; e < DPL; ++e) o[e] = o[e] * cf + p * __half2float(vh[e]);
-        l = l * cf + p;
+        for (int tt = 0; tt < 32; ++tt) {
+            const float pt = __shfl_sync(0xffffffffu, p, tt);
+            const __half* vh = reinterpret_cast<const __half*>(&vr[tt]);
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) o[e] += pt * __half2float(vh[e]);
+        }
         mx = mn;
     }
     __half* dst = out + (size_t)m * H * hd + (size_t)hh * hd + DPL * lane;
@@ -356,17 +444,22 @@ __global__ void k_pf_attn(const float* __restrict__ q, const __half* __restrict_
     for (int e = 0; e < DPL; ++e) dst[e] = __float2half_rn(o[e] * inv);
 }
 
+__device__ __forceinline__ float pf_silu_mul(float x, float u) { return x / (1.0f + expf(-x)) * u; }
+
+// a = fp16(silu(g) * u); n4 = n / 4 float4 groups, then the scalar tail
 __global__ void k_pf_silu_mul(const float* __restrict__ g, const float* __restrict__ u, __half* __restrict__ a,
                               int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const float x = g[i];
-    a[i] = __float2half_rn(x / (1.0f + expf(-x)) * u[i]);
-}
-
-__global__ void k_pf_add(float* __restrict__ h, const float* __restrict__ y, int64_t n) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) h[i] += y[i];
+    const int64_t n4 = n / 4;
+    if (i < n4) {
+        const float4 gv = reinterpret_cast<const float4*>(g)[i], uv = reinterpret_cast<const float4*>(u)[i];
+        __half2 r[2] = {__floats2half2_rn(pf_silu_mul(gv.x, uv.x), pf_silu_mul(gv.y, uv.y)),
+                        __floats2half2_rn(pf_silu_mul(gv.z, uv.z), pf_silu_mul(gv.w, uv.w))};
+        reinterpret_cast<uint2*>(a)[i] = *reinterpret_cast<const uint2*>(r);
+    } else if (i < n4 + (n - 4 * n4)) {
+        const int64_t k = 4 * n4 + (i - n4);
+        a[k] = __float2half_rn(pf_silu_mul(g[k], u[k]));
+    }
 }
 
 __device__ __forceinline__ unsigned long long pf_key(float f, unsigned tok) {
@@ -375,26 +468,53 @@ __device__ __forceinline__ unsigned long long pf_key(float f, unsigned tok) {
     return ((unsigned long long)ord << 32) | (unsigned long long)(0xFFFFFFFFu - tok);   // ties -> lowest id
 }
 
-// lm_head of ONE token: a warp per vocab row (16-B loads), max of (logit, ~token) keys
-__global__ void k_pf_lm_argmax(const __half* __restrict__ W, const __half* __restrict__ x, int V, int n,
-                               unsigned long long* __restrict__ best) {
-    const int row = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
-    if (row >= V) return;
-    const uint4* wr = reinterpret_cast<const uint4*>(W + (size_t)row * n);
+// lm_head of ONE token: warps stride over the vocab rows (a lane's first 16
+// 16-B loads of a row issued before any use), keep the max of (logit, ~token)
+// keys, reduce in the CTA and publish ONE atomicMax per CTA (one per row
+// serialises 128 K same-address atomics in L2)
+__global__ void __launch_bounds__(256, 1) k_pf_lm_argmax(const __half* __restrict__ W, const __half* __restrict__ x,
+                                                         int V, int n, unsigned long long* __restrict__ best) {
+    __shared__ unsigned long long s_best[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gw = (int)blockIdx.x * 8 + warp, nw = (int)gridDim.x * 8;
     const uint4* xr = reinterpret_cast<const uint4*>(x);
-    float a = 0.f;
-    for (int c = lane; c < n / 8; c += 32) {
-        const uint4 wv = __ldg(wr + c), xv = xr[c];
+    const int n8 = n / 8;
+    auto dot8 = [](uint4 wv, uint4 xv) {
         const __half2* w2 = reinterpret_cast<const __half2*>(&wv);
         const __half2* x2 = reinterpret_cast<const __half2*>(&xv);
+        float a = 0.f;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const float2 wf = __half22float2(w2[e]), xf = __half22float2(x2[e]);
             a += wf.x * xf.x + wf.y * xf.y;
         }
+        return a;
+    };
+    constexpr int NL = 16;
+    unsigned long long kb = 0ull;
+    for (int row = gw; row < V; row += nw) {
+        const uint4* wr = reinterpret_cast<const uint4*>(W + (size_t)row * n);
+        float a = 0.f;
+        int c0 = lane;
+        if (n8 >= 32 * NL) {
+            uint4 wv[NL];
+#pragma unroll
+            for (int k = 0; k < NL; ++k) wv[k] = __ldcs(wr + lane + 32 * k);
+#pragma unroll
+            for (int k = 0; k < NL; ++k) a += dot8(wv[k], xr[lane + 32 * k]);
+            c0 += 32 * NL;
+        }
+        for (int c = c0; c < n8; c += 32) a += dot8(__ldcs(wr + c), xr[c]);
+        for (int o = 16; o >= 1; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        kb = max(kb, pf_key(a, (unsigned)row));
     }
-    for (int o = 16; o >= 1; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) atomicMax(best, pf_key(a, (unsigned)row));
+    if (lane == 0) s_best[warp] = kb;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long b = 0ull;
+        for (int w = 0; w < 8; ++w) b = max(b, s_best[w]);
+        if (b) atomicMax(best, b);
+    }
 }
 
 __global__ void k_pf_token(const unsigned long long* __restrict__ best, int* __restrict__ tok) {
@@ -744,12 +864,11 @@ fasq_status fasq_llama_prefill(fasq_llama* m, const int32_t* tokens_dev, int32_t
     auto gemm = [&](const fasq_layer* L, const __half* X, float* Y) {
         if (s == FASQ_OK) s = fasq_gemm(L, X, M, Y, FASQ_F32, FASQ_GEMM_AUTO, st);
     };
-    if (s == FASQ_OK) {
-        k_pf_embed<<<pf_blocks(Mn, 256), 256, 0, st>>>(tokens_dev, static_cast<const __half*>(D.embed), h, M, n);
-        check(cudaGetLastError(), "prefill embed");
-    }
     for (int l = 0; l < D.n_layers && s == FASQ_OK; ++l) {
-        k_pf_rmsnorm<<<M, 256, 0, st>>>(h, static_cast<const __half*>(D.attn_norm[l]), x, n, D.rms_eps, 0);
+        // block 0: h = embedding; block l > 0: h += the previous block's down product
+        k_pf_resid_norm<<<M, 256, 0, st>>>(h, l ? y : nullptr, l ? nullptr : tokens_dev,
+                                           static_cast<const __half*>(D.embed),
+                                           static_cast<const __half*>(D.attn_norm[l]), x, n, D.rms_eps, 0);
         check(cudaGetLastError(), "prefill rmsnorm");
         gemm(D.q[l], x, q);
         gemm(D.k[l], x, k);
@@ -759,32 +878,31 @@ fasq_status fasq_llama_prefill(fasq_llama* m, const int32_t* tokens_dev, int32_t
             q, k, v, m->kc[l], m->vc[l], m->rope, M, pos0, H, KV, hd, D.max_T);
         check(cudaGetLastError(), "prefill rope");
         if (hd == 128)
-            k_pf_attn<4><<<pf_blocks((int64_t)M * H * 32, 256), 256, 0, st>>>(q, m->kc[l], m->vc[l], a, M, pos0, H, KV,
+            k_pf_attn<4><<<pf_blocks((int64_t)M * H, 4), 128, 0, st>>>(q, m->kc[l], m->vc[l], a, M, pos0, H, KV,
                                                                                D.max_T);
         else
-            k_pf_attn<2><<<pf_blocks((int64_t)M * H * 32, 256), 256, 0, st>>>(q, m->kc[l], m->vc[l], a, M, pos0, H, KV,
+            k_pf_attn<2><<<pf_blocks((int64_t)M * H, 4), 128, 0, st>>>(q, m->kc[l], m->vc[l], a, M, pos0, H, KV,
                                                                                D.max_T);
         check(cudaGetLastError(), "prefill attention");
         gemm(D.o[l], a, y);
         if (s != FASQ_OK) break;
-        k_pf_add<<<pf_blocks(Mn, 256), 256, 0, st>>>(h, y, Mn);
-        k_pf_rmsnorm<<<M, 256, 0, st>>>(h, static_cast<const __half*>(D.mlp_norm[l]), x, n, D.rms_eps, 0);
+        k_pf_resid_norm<<<M, 256, 0, st>>>(h, y, nullptr, nullptr, static_cast<const __half*>(D.mlp_norm[l]), x, n,
+                                           D.rms_eps, 0);
         check(cudaGetLastError(), "prefill mlp norm");
         gemm(D.gate[l], x, g);
         gemm(D.up[l], x, u);
         if (s != FASQ_OK) break;
-        k_pf_silu_mul<<<pf_blocks((int64_t)M * ffn, 256), 256, 0, st>>>(g, u, a, (int64_t)M * ffn);
+        k_pf_silu_mul<<<pf_blocks((int64_t)M * ffn / 4 + 3, 256), 256, 0, st>>>(g, u, a, (int64_t)M * ffn);
         check(cudaGetLastError(), "prefill swiglu");
         gemm(D.down[l], a, y);
-        if (s != FASQ_OK) break;
-        k_pf_add<<<pf_blocks(Mn, 256), 256, 0, st>>>(h, y, Mn);
-        check(cudaGetLastError(), "prefill residual");
     }
     if (s == FASQ_OK) {
         // the last prompt position's greedy token -> the decode chain's token slot
-        k_pf_rmsnorm<<<1, 256, 0, st>>>(h, static_cast<const __half*>(D.final_norm), x, n, D.rms_eps, M - 1);
+        // only the last position's residual is still needed: its final add + norm
+        k_pf_resid_norm<<<1, 256, 0, st>>>(h, y, nullptr, nullptr, static_cast<const __half*>(D.final_norm), x, n,
+                                           D.rms_eps, M - 1);
         check(cudaMemsetAsync(best, 0, 8, st), "prefill argmax");
-        k_pf_lm_argmax<<<pf_blocks((int64_t)D.vocab * 32, 256), 256, 0, st>>>(
+        k_pf_lm_argmax<<<std::min<int64_t>(pf_blocks(D.vocab, 8), (int64_t)sm_count() * 2), 256, 0, st>>>(
             static_cast<const __half*>(D.lm_head), x, D.vocab, n, best);
         k_pf_token<<<1, 1, 0, st>>>(best, m->tok_dev);
         k_llama_reset<<<1, 32, 0, st>>>(m->chain->tail(), m->chain->nctas, m->tok_dev, 1, pos0 + M,
