@@ -366,82 +366,124 @@ __global__ void k_pf_rope_cache(float* __restrict__ q, const float* __restrict__
     }
 }
 
-// causal GQA attention: one warp per (token m, q head), positions t <= pos0 + m
-// in chunks of 32 with an online softmax over chunks.  Scores: lane L takes
-// position t0 + L (its K row in 16-B loads against q broadcast from shared
-// memory); P.V: lane L holds DPL = hd / 32 consecutive output dims and walks the
-// chunk's V rows (coalesced rows, independent loads in flight) -- the per-position
-// dependent chain (load, 5 shuffles, exp) of a lane-per-dim walk was latency-bound
-template <int DPL>
+// causal GQA attention: one warp per (token m, G q heads of one KV head),
+// positions t <= pos0 + m in chunks of 32 with an online softmax over chunks.
+// Scores: lane L takes position t0 + L (its K row in 16-B loads, converted once
+// and dotted with the G queries broadcast from shared memory); P.V: lane L holds
+// DPL = hd / 32 consecutive output dims of each head and walks the chunk's V rows
+// (loaded once for the G heads).  The chunk's K and V rows are in flight together.
+template <int DPL, int G>
 __global__ void __launch_bounds__(128, 3) k_pf_attn(const float* __restrict__ q, const __half* __restrict__ kc,
-                                                 const __half* __restrict__ vc, __half* __restrict__ out, int M,
-                                                 int pos0, int H, int KV, int max_T) {
+                                                    const __half* __restrict__ vc, __half* __restrict__ out, int M,
+                                                    int pos0, int H, int KV, int max_T) {
     constexpr int hd = 32 * DPL;
-    __shared__ __align__(16) float qs[4][hd];
+    __shared__ __align__(16) float qs[4][G][hd];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int wg = (int)blockIdx.x * 4 + w;
-    if (wg >= M * H) return;
-    const int m = wg / H, hh = wg - m * H, j = hh / (H / KV), pos = pos0 + m;
+    const int HG = H / G, wg = (int)blockIdx.x * 4 + w;
+    if (wg >= M * HG) return;
+    const int m = wg / HG, hh0 = (wg - m * HG) * G, j = hh0 / (H / KV), pos = pos0 + m;
     const float sc = 1.0f / sqrtf((float)hd);
-    const float* qr = q + (size_t)m * H * hd + (size_t)hh * hd;
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) qs[w][e * 32 + lane] = qr[e * 32 + lane];
+    for (int g = 0; g < G; ++g) {
+        const float* qr = q + (size_t)m * H * hd + (size_t)(hh0 + g) * hd;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) qs[w][g][e * 32 + lane] = qr[e * 32 + lane];
+    }
     __syncwarp();
     const __half* K = kc + (size_t)j * max_T * hd;
     const __half* V = vc + (size_t)j * max_T * hd + DPL * lane;
-    float mx = -INFINITY, l = 0.f, o[DPL];
+    float mx[G], l[G], o[G][DPL];
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) o[e] = 0.f;
+    for (int g = 0; g < G; ++g) {
+        mx[g] = -INFINITY;
+        l[g] = 0.f;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) o[g][e] = 0.f;
+    }
+    using VT = typename std::conditional<DPL == 4, uint2, unsigned>::type;
     for (int t0 = 0; t0 <= pos; t0 += 32) {
         const int t = t0 + lane;
-        // the chunk's 32 V rows in flight with its K rows: rows past pos are clamped to
-        // pos (finite cache data) and weighted by p = 0
-        using VT = typename std::conditional<DPL == 4, uint2, unsigned>::type;
+        // rows past pos are clamped to pos (finite cache data) and weighted by p = 0
         VT vr[32];
 #pragma unroll
         for (int tt = 0; tt < 32; ++tt)
             vr[tt] = *reinterpret_cast<const VT*>(V + (size_t)min(t0 + tt, pos) * hd);
-        float s = -INFINITY;
+        float s[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) s[g] = -INFINITY;
         if (t <= pos) {
             const uint4* kr = reinterpret_cast<const uint4*>(K + (size_t)t * hd);
             uint4 kv[hd / 8];
 #pragma unroll
             for (int c = 0; c < hd / 8; ++c) kv[c] = kr[c];
-            float acc = 0.f;
+            float acc[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) acc[g] = 0.f;
 #pragma unroll
             for (int c = 0; c < hd / 8; ++c) {
-                const float4 qa = *reinterpret_cast<const float4*>(&qs[w][8 * c]);
-                const float4 qb = *reinterpret_cast<const float4*>(&qs[w][8 * c + 4]);
                 const __half2* k2 = reinterpret_cast<const __half2*>(&kv[c]);
                 const float2 k0 = __half22float2(k2[0]), k1 = __half22float2(k2[1]);
                 const float2 k2f = __half22float2(k2[2]), k3 = __half22float2(k2[3]);
-                acc += qa.x * k0.x + qa.y * k0.y + qa.z * k1.x + qa.w * k1.y;
-                acc += qb.x * k2f.x + qb.y * k2f.y + qb.z * k3.x + qb.w * k3.y;
-            }
-            s = acc * sc;
-        }
-        float cm = s;
-        for (int off = 16; off >= 1; off >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, off));
-        const float mn = fmaxf(mx, cm), cf = expf(mx - mn);
-        const float p = t <= pos ? expf(s - mn) : 0.f;
-        float ps = p;
-        for (int off = 16; off >= 1; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
-        l = l * cf + ps;
 #pragma unroll
-        for (int e = 0; e < DPL; ++e) o[e] *= cf;
+                for (int g = 0; g < G; ++g) {
+                    const float4 qa = *reinterpret_cast<const float4*>(&qs[w][g][8 * c]);
+                    const float4 qb = *reinterpret_cast<const float4*>(&qs[w][g][8 * c + 4]);
+                    acc[g] += qa.x * k0.x + qa.y * k0.y + qa.z * k1.x + qa.w * k1.y;
+                    acc[g] += qb.x * k2f.x + qb.y * k2f.y + qb.z * k3.x + qb.w * k3.y;
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) s[g] = acc[g] * sc;
+        }
+        float p[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            float cm = s[g];
+            for (int off = 16; off >= 1; off >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, off));
+            const float mn = fmaxf(mx[g], cm), cf = expf(mx[g] - mn);
+            p[g] = t <= pos ? expf(s[g] - mn) : 0.f;
+            float ps = p[g];
+            for (int off = 16; off >= 1; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+            l[g] = l[g] * cf + ps;
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) o[g][e] *= cf;
+            mx[g] = mn;
+        }
 #pragma unroll
         for (int tt = 0; tt < 32; ++tt) {
-            const float pt = __shfl_sync(0xffffffffu, p, tt);
             const __half* vh = reinterpret_cast<const __half*>(&vr[tt]);
+            float vf[DPL];
 #pragma unroll
-            for (int e = 0; e < DPL; ++e) o[e] += pt * __half2float(vh[e]);
+            for (int e = 0; e < DPL; ++e) vf[e] = __half2float(vh[e]);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float pt = __shfl_sync(0xffffffffu, p[g], tt);
+#pragma unroll
+                for (int e = 0; e < DPL; ++e) o[g][e] += pt * vf[e];
+            }
         }
-        mx = mn;
     }
-    __half* dst = out + (size_t)m * H * hd + (size_t)hh * hd + DPL * lane;
-    const float inv = 1.0f / l;
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) dst[e] = __float2half_rn(o[e] * inv);
+    for (int g = 0; g < G; ++g) {
+        __half* dst = out + (size_t)m * H * hd + (size_t)(hh0 + g) * hd + DPL * lane;
+        const float inv = 1.0f / l[g];
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) dst[e] = __float2half_rn(o[g][e] * inv);
+    }
+}
+
+template <int DPL>
+void pf_attn_launch(const float* q, const __half* kc, const __half* vc, __half* out, int M, int pos0, int H, int KV,
+                    int max_T, cudaStream_t st) {
+    const int grp = H / KV;
+    const int G = grp % 4 == 0 ? 4 : grp % 2 == 0 ? 2 : 1;
+    const unsigned blocks = (unsigned)(((int64_t)M * (H / G) + 3) / 4);
+    if (G == 4)
+        k_pf_attn<DPL, 4><<<blocks, 128, 0, st>>>(q, kc, vc, out, M, pos0, H, KV, max_T);
+    else if (G == 2)
+        k_pf_attn<DPL, 2><<<blocks, 128, 0, st>>>(q, kc, vc, out, M, pos0, H, KV, max_T);
+    else
+        k_pf_attn<DPL, 1><<<blocks, 128, 0, st>>>(q, kc, vc, out, M, pos0, H, KV, max_T);
 }
 
 __device__ __forceinline__ float pf_silu_mul(float x, float u) { return x / (1.0f + expf(-x)) * u; }
@@ -878,11 +920,9 @@ fasq_status fasq_llama_prefill(fasq_llama* m, const int32_t* tokens_dev, int32_t
             q, k, v, m->kc[l], m->vc[l], m->rope, M, pos0, H, KV, hd, D.max_T);
         check(cudaGetLastError(), "prefill rope");
         if (hd == 128)
-            k_pf_attn<4><<<pf_blocks((int64_t)M * H, 4), 128, 0, st>>>(q, m->kc[l], m->vc[l], a, M, pos0, H, KV,
-                                                                               D.max_T);
+            pf_attn_launch<4>(q, m->kc[l], m->vc[l], a, M, pos0, H, KV, D.max_T, st);
         else
-            k_pf_attn<2><<<pf_blocks((int64_t)M * H, 4), 128, 0, st>>>(q, m->kc[l], m->vc[l], a, M, pos0, H, KV,
-                                                                               D.max_T);
+            pf_attn_launch<2>(q, m->kc[l], m->vc[l], a, M, pos0, H, KV, D.max_T, st);
         check(cudaGetLastError(), "prefill attention");
         gemm(D.o[l], a, y);
         if (s != FASQ_OK) break;

@@ -332,15 +332,17 @@ def test_llama3_block_full_size(F):
     model.free()
 
 
-@pytest.mark.parametrize("hd,M,P0", [(64, 6, 3), (128, 9, 0), (128, 1, 4), (64, 40, 5), (128, 50, 10)])
-def test_llama_prefill_matches_oracle(F, hd, M, P0):
+@pytest.mark.parametrize("hd,M,P0,n_kv", [(64, 6, 3, 2), (128, 9, 0, 1), (128, 1, 4, 1), (64, 40, 5, 2),
+                                          (128, 50, 10, 1), (64, 37, 2, 4), (64, 33, 0, 1)])
+def test_llama_prefill_matches_oracle(F, hd, M, P0, n_kv):
     """fasq_llama_prefill (the paper's E2E prompt phase): the KV-cache rows
     it writes for the prompt positions, the greedy token it hands to the decode
     chain and the first decode step after it, against the oracle's causal prefill
     (oracle.llama.prefill: the decode step over the prompt tokens in order).
     M = 40 / 50 after P0 = 5 / 10 cached positions span two 32-position chunks of
-    the prefill attention with a ragged tail."""
-    cfg = dict(SMALL, head_dim=hd, n_heads=256 // hd, n_kv=max(1, 128 // hd), hidden=256)
+    the prefill attention with a ragged tail; n_kv = 4 / 1 at 4 heads of 64
+    put 1 / 4 query heads on a KV head (each warp's head group G = 1 / 4)."""
+    cfg = dict(SMALL, head_dim=hd, n_heads=256 // hd, n_kv=n_kv, hidden=256)
     layers, fn, emb, lm = make_model(cfg, seed=31 + hd)
     kc, vc = prompt_cache(cfg, 1, max(P0, 1), seed=32)
     prompt = [(37 * i + 11) % cfg["vocab"] for i in range(M)]
