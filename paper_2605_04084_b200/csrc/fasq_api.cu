@@ -324,7 +324,12 @@ fasq_status fasq_gemv_host(const fasq_layer* L, const void* x_host, int32_t B, v
 // 4096-row layers, M <= 96 on the 14336-row ones (more row tiles: EXPAND fills the SMs)
 static int64_t gemm_short_max(const fasq_layer* L) {
     const char* e = getenv("FASQ_GEMM_TC_DECODE_MAX");
-    return e ? atoll(e) : (L->F_out > 8192 ? 96 : 128);
+    if (e) return atoll(e);
+    // measured crossovers against EXPAND's split-K (profiles/r02/short_gemm_sweep_v2.jsonl):
+    // 4096 x 14336 <= 96, 1024 x 4096 <= 64, 4096^2 and 14336 x 4096 <= 32
+    if (L->F_in > 8192) return 96;
+    if (L->F_out <= 2048) return 64;
+    return 32;
 }
 
 fasq_status fasq_gemm(const fasq_layer* L, const void* X_dev, int64_t M, void* Y_dev, fasq_dtype yt,

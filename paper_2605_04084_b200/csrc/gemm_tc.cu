@@ -53,6 +53,7 @@ struct TcParams {
     unsigned* tickets;       // [tiles][2] arrive / depart counters (zero between launches)
     int M, F_out, F_out_pad, n_groups, C, y_f32;
     int tile0, ntx;          // this launch covers tiles tile0 + blockIdx.x (row tile = tile % ntx)
+    int pair_order;          // 1: tiles in pair order (even token-tile count); 0: row-major (tile % ntx, tile / ntx)
 };
 
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
@@ -115,7 +116,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     // so the two CTAs of a cluster share the row tile (both kernels use it)
     const int tile_g = p.tile0 + (int)blockIdx.x;            // tile of the whole problem
     const int rank = tile_g & 1;                             // = %cluster_ctarank for PAIR
-    const int nrt = (tile_g >> 1) % p.ntx, ntt = 2 * ((tile_g >> 1) / p.ntx) + rank;
+    // an odd token-tile count without pairs runs row-major: no phantom token tile
+    const bool po = PAIR || p.pair_order;
+    const int nrt = po ? (tile_g >> 1) % p.ntx : tile_g % p.ntx;
+    const int ntt = po ? 2 * ((tile_g >> 1) / p.ntx) + rank : tile_g / p.ntx;
     const int n0t = nrt * TC_N;                              // weight-row tile (epilogue rows)
     const int n0 = n0t + (PAIR ? rank * NR : 0);             // rows this CTA expands
     const int m0 = ntt * TC_M * TC_MT;                       // first token of this CTA's token tiles
@@ -322,9 +326,16 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
             dev::mbar_wait(accum_bar, 0);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int q = warp & 3;                    // TMEM lane quarter this warp may access
-            const int t = ew >> 2;                     // accumulator (token tile) this warp drains
-            const int ml = t * TC_M + q * 32 + lane;   // token within the CTA tile
+            const int t = ew >> 2;
+            // <= 128 real tokens left in this tile (short prefill): the second
+            // accumulator is all phantom -> both warp halves drain accumulator 0,
+            // each half of its columns; else warp half t drains accumulator t
+            const bool one_acc = m0 + TC_M >= p.M;
+            const int ta = one_acc ? 0 : t;            // accumulator (token tile) this warp drains
+            const int cbeg = one_acc ? t * (TC_N / 2) : 0, cend = one_acc ? cbeg + TC_N / 2 : TC_N;
+            const int ml = ta * TC_M + q * 32 + lane;  // token within the CTA tile
             const int m = m0 + ml;                     // token
+            constexpr int TT = TC_M * TC_MT;           // tokens per CTA tile (workspace column pitch)
             const int tile = (int)blockIdx.x;         // tile within this launch (workspace / tickets)
             // 32 consecutive outputs (rows n .. n+31) of token m -> Y (fp32 / fp16)
             auto store32 = [&](int n, const float* r) {
@@ -362,9 +373,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
                 }
             };
 #pragma unroll 1
-            for (int c0 = 0; c0 < TC_N; c0 += 32) {
+            for (int c0 = cbeg; c0 < cend; c0 += 32) {
                 uint32_t r[32];
-                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(t * TC_N + c0);
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ta * TC_N + c0);
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
                     "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -380,11 +391,16 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
 #pragma unroll
                 for (int v = 0; v < 32; ++v) f[v] = __uint_as_float(r[v]);
                 if (ksplit > 1) {
-                    // partial tile -> workspace, merged below in fixed ks order (deterministic)
-                    float* wr = p.ws + (((size_t)kz * gridDim.x + tile) * (TC_M * TC_MT) + ml) * TC_N + c0;
+                    // partial tile -> workspace, merged below in fixed ks order
+                    // (deterministic).  Column-major [kz][tile][col][token]: one
+                    // column of a warp's 32 tokens is one 128-B line (a token-major
+                    // row per lane scattered 16-B pieces over 32 lines per store).
+                    // Warps holding only phantom tokens skip it (never read).
+                    if (m0 + ta * TC_M + q * 32 < p.M) {
+                        float* wc = p.ws + ((size_t)kz * gridDim.x + tile) * (size_t)(TT * TC_N) + (size_t)c0 * TT + ml;
 #pragma unroll
-                    for (int v = 0; v < 8; ++v)
-                        __stcg(reinterpret_cast<float4*>(wr) + v, make_float4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]));
+                        for (int v = 0; v < 32; ++v) __stcg(wc + (size_t)v * TT, f[v]);
+                    }
                 } else {
                     store32(n0t + c0, f);
                 }
@@ -413,24 +429,31 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
                 }
                 asm volatile("bar.sync 1, %0;" :: "n"(TC_EXP_WARPS * 32) : "memory");
                 const int cw = TC_N / ksplit;     // ks in {2, 4, 8}: multiples of 32 columns
-#pragma unroll 1
-                for (int c0 = kz * cw; c0 < (kz + 1) * cw; c0 += 32) {
-                    float f[32];
-#pragma unroll
-                    for (int v = 0; v < 32; ++v) f[v] = 0.f;
-                    for (int z = 0; z < ksplit; ++z) {
-                        const float4* rd = reinterpret_cast<const float4*>(
-                            p.ws + (((size_t)z * gridDim.x + tile) * (TC_M * TC_MT) + ml) * TC_N + c0);
-#pragma unroll
-                        for (int v = 0; v < 8; ++v) {
-                            const float4 w = __ldcg(rd + v);
-                            f[4 * v] += w.x;
-                            f[4 * v + 1] += w.y;
-                            f[4 * v + 2] += w.z;
-                            f[4 * v + 3] += w.w;
-                        }
+                // this CTA's column slice; with one real accumulator the two warp
+                // halves (same tokens) split it when it holds >= 2 chunks of 32
+                int mb = kz * cw, me = mb + cw;
+                if (one_acc) {
+                    if (cw >= 64) {
+                        mb += t * (cw / 2);
+                        me = mb + cw / 2;
+                    } else if (t) {
+                        me = mb;
                     }
-                    store32(n0t + c0, f);
+                }
+                if (m < p.M) {
+#pragma unroll 1
+                    for (int c0 = mb; c0 < me; c0 += 32) {
+                        float f[32];
+#pragma unroll
+                        for (int v = 0; v < 32; ++v) f[v] = 0.f;
+                        for (int z = 0; z < ksplit; ++z) {   // fixed order
+                            const float* rd = p.ws + ((size_t)z * gridDim.x + tile) * (size_t)(TT * TC_N) +
+                                              (size_t)c0 * TT + ml;
+#pragma unroll
+                            for (int v = 0; v < 32; ++v) f[v] += __ldcg(rd + (size_t)v * TT);
+                        }
+                        store32(n0t + c0, f);
+                    }
                 }
             }
         }
@@ -518,9 +541,13 @@ fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void
     // F_out_pad rows of the idx table exist; tiles past F_out_pad read beyond it
     // -> require the row tile grid to stay within F_out_pad (pad logic below).
     const int ntx = (L->F_out_pad + TC_N - 1) / TC_N;
-    // token tiles rounded up to an even count: tiles are numbered in pair order
-    // (kernel), the phantom tile of an odd count reads zero-filled X and stores nothing
-    const int nty = (int)((M + TC_M * TC_MT - 1) / (TC_M * TC_MT) + 1) / 2 * 2;
+    // token tiles: an even count is numbered in pair order (kernel); an odd count
+    // runs row-major with the exact count (a phantom tile would expand its weight
+    // slab for nothing: half the CTAs at M <= 256), unless 2-CTA pairs are on, which
+    // round it up to even (the phantom tile reads zero-filled X and stores nothing)
+    const int nty_exact = (int)((M + TC_M * TC_MT - 1) / (TC_M * TC_MT));
+    p.pair_order = (nty_exact % 2 == 0 || pair_env) ? 1 : 0;
+    const int nty = p.pair_order ? (nty_exact + 1) / 2 * 2 : nty_exact;
     const int tiles_all = ntx * nty;
     p.ntx = ntx;
     int dev = 0, sms = 148;
@@ -580,7 +607,7 @@ fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void
             grid.z = (unsigned)ks;
         }
         cudaError_t e;
-        if (ks == 1 && pair_ok && (tiles & 1) == 0 && (p.tile0 & 1) == 0) {
+        if (ks == 1 && pair_ok && p.pair_order && (tiles & 1) == 0 && (p.tile0 & 1) == 0) {
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = grid;
             cfg.blockDim = dim3(TC_THREADS, 1, 1);

@@ -42,7 +42,7 @@ def run(o, i, M, short, it=20):
 
 
 if __name__ == "__main__":
-    for (o, i) in ((4096, 4096), (14336, 4096), (4096, 14336)):
-        for M in (16, 64, 96, 128, 192, 256):
+    for (o, i) in ((4096, 4096), (14336, 4096), (4096, 14336), (1024, 4096)):
+        for M in (16, 32, 64, 96, 128, 192, 256):
             for short in (False, True):
                 print(json.dumps(run(o, i, M, short)), flush=True)
