@@ -283,11 +283,14 @@ __global__ void __launch_bounds__(256) k_pf_resid_norm(float* __restrict__ h, co
         }
         return v;
     };
+    const uint2* gr = reinterpret_cast<const uint2*>(gamma);
     float4 vals[PF_NV];
+    uint2 gv[PF_NV];   // gamma with the row (not one more round trip after the reduction)
 #pragma unroll
     for (int k = 0; k < PF_NV; ++k) {
         const int c4 = threadIdx.x + k * blockDim.x;
         vals[k] = c4 < n4 ? update(c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        gv[k] = c4 < n4 ? gr[c4] : make_uint2(0u, 0u);
     }
     float a = 0.f;
     const bool write = er || yr;
@@ -314,10 +317,8 @@ __global__ void __launch_bounds__(256) k_pf_resid_norm(float* __restrict__ h, co
     }
     __syncthreads();
     const float r = 1.0f / sqrtf(red[0] / (float)n + eps);
-    const uint2* gr = reinterpret_cast<const uint2*>(gamma);
     uint2* xr = reinterpret_cast<uint2*>(x + (size_t)(m - row0) * n);
-    auto emit = [&](int c4, float4 v) {
-        const uint2 gg = gr[c4];
+    auto emit = [&](int c4, float4 v, uint2 gg) {
         const float2 g0 = __half22float2(*reinterpret_cast<const __half2*>(&gg.x));
         const float2 g1 = __half22float2(*reinterpret_cast<const __half2*>(&gg.y));
         __half2 o[2] = {__floats2half2_rn(v.x * r * g0.x, v.y * r * g0.y),
@@ -327,9 +328,9 @@ __global__ void __launch_bounds__(256) k_pf_resid_norm(float* __restrict__ h, co
 #pragma unroll
     for (int k = 0; k < PF_NV; ++k) {
         const int c4 = threadIdx.x + k * blockDim.x;
-        if (c4 < n4) emit(c4, vals[k]);
+        if (c4 < n4) emit(c4, vals[k], gv[k]);
     }
-    for (int c4 = threadIdx.x + PF_NV * blockDim.x; c4 < n4; c4 += blockDim.x) emit(c4, hr[c4]);   // own writes
+    for (int c4 = threadIdx.x + PF_NV * blockDim.x; c4 < n4; c4 += blockDim.x) emit(c4, hr[c4], gr[c4]);   // own writes
 }
 
 // RoPE on q (in place, fp32) and k; the new k (rotated) / v enter the cache as fp16
