@@ -231,3 +231,26 @@ def test_gemm_auto_short_L_runs_tcgen05_decode(F, oracle_lib, F_out, F_in, M):
     assert ok, m
     Ye = F.gemm(L, Xd, algo=F.GEMM_EXPAND_TC).float().cpu().numpy()
     assert np.linalg.norm(Y - Ye) / np.linalg.norm(Ye) <= 1e-5
+
+
+@pytest.mark.parametrize("M", [1, 77, 128, 129, 255, 256, 257, 384, 640])
+def test_gemm_tc_token_tile_edges(F, oracle_lib, M):
+    """EXPAND's token tiling at every edge of its 256-token CTA tile: an odd
+    token-tile count (row-major tiles, no phantom tile), tiles with <= 128 real
+    tokens (one accumulator drained by both warp halves, no phantom workspace
+    rows), split-K chosen automatically (few row tiles -> ks up to 8) and the
+    column-major partial-tile merge; sampled rows at both ends and the middle
+    against the oracle, and bit-identical repeats (fixed merge order)."""
+    F_out, F_in = 768, 4096
+    cb, idx = synth.random_layer(F_out, F_in, 2, 256, seed=M + 5)
+    X = synth.activation(M, F_in, seed=M + 6)
+    L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), F_in)
+    Xd = torch.from_numpy(X).cuda()
+    Y = F.gemm(L, Xd, out_dtype=torch.float32, algo=F.GEMM_EXPAND_TC)
+    Y2 = F.gemm(L, Xd, out_dtype=torch.float32, algo=F.GEMM_EXPAND_TC)
+    torch.cuda.synchronize()
+    Yn = Y.cpu().numpy().astype(np.float64)
+    assert np.array_equal(Yn, Y2.cpu().numpy().astype(np.float64))
+    for r0 in (0, 352, F_out - 32):
+        ok, m = parity_ok(Yn[:, r0:r0 + 32], oracle_lib.gemm(cb, idx, X, rows=(r0, r0 + 32)), X, F_in)
+        assert ok, (r0, m)
