@@ -656,11 +656,12 @@ KINDS = (("qkv", ("q_proj", "k_proj", "v_proj")), ("o", ("o_proj",)), ("gate_up"
 
 def prefill_model(dense_peak, Ms=(128, 512, 2048), reps=3):
     """configs[4] at N = 1: the prefill pass of the whole PQ linear stack --
-    M tokens through the 224 Llama-3-8B-shaped PQ layers with fasq_gemm
-    (AUTO: the tcgen05 decode kernel at M = 128 -- the paper's prompt length,
-    P:438 -- EXPAND on tcgen05 above), fp16 activations chained block to block
-    like the decode chain (q/k/v and gate/up read the same input); attention /
-    norms excluded.  Replayed from a CUDA graph; tok/s = M / pass time."""
+    M tokens through the 224 Llama-3-8B-shaped PQ layers (AUTO at M = 128 --
+    the paper's prompt length, P:438 -- EXPAND on tcgen05 above), fp16
+    activations chained block to block like the decode chain; q/k/v and
+    gate/up read the same input and run as fasq_gemm_grouped (one EXPAND launch
+    each); attention / norms excluded.  Replayed from a CUDA graph; tok/s = M /
+    pass time."""
     import torch
 
     import paper_2605_04084_b200 as F
@@ -686,11 +687,11 @@ def prefill_model(dense_peak, Ms=(128, 512, 2048), reps=3):
         def one_pass():
             h = x0
             for Ls in blocks:
-                for n in ("q_proj", "k_proj", "v_proj"):
-                    F.gemm(Ls[n], h, out=bufs[n], algo=algo)
+                qkv = ("q_proj", "k_proj", "v_proj")
+                F.gemm_grouped([Ls[n] for n in qkv], h, outs=[bufs[n] for n in qkv], algo=algo)
                 F.gemm(Ls["o_proj"], bufs["q_proj"], out=bufs["o_proj"], algo=algo)
-                for n in ("gate_proj", "up_proj"):
-                    F.gemm(Ls[n], bufs["o_proj"], out=bufs[n], algo=algo)
+                gu = ("gate_proj", "up_proj")
+                F.gemm_grouped([Ls[n] for n in gu], bufs["o_proj"], outs=[bufs[n] for n in gu], algo=algo)
                 F.gemm(Ls["down_proj"], bufs["gate_proj"], out=bufs["down_proj"], algo=algo)
                 h = bufs["down_proj"]
         gs = torch.cuda.Stream()

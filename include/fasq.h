@@ -442,6 +442,20 @@ fasq_status fasq_gemv_host(const fasq_layer* layer, const void* x_host, int32_t 
 fasq_status fasq_gemm(const fasq_layer* layer, const void* X_dev, int64_t M, void* Y_dev,
                       fasq_dtype y_dtype, fasq_gemm_algo algo, void* stream);
 
+/* Prefill GEMMs of n layers reading the same X (a block's q / k / v, or gate /
+ * up): Y_dev[l] = X . W_hat_l^T, each as fasq_gemm(layers[l], ...) computes
+ * it, except that a grouped launch may split K differently (its tile count
+ * differs), so the fp32 sums can differ in the last bits; the result is still
+ * deterministic for a given (layers, M).  layers[]
+ * and Y_dev[] are host arrays of n pointers (n >= 1); every layer has the same
+ * F_in (FASQ_E_SHAPE otherwise); Y_dev[l] is [M][F_out_l] of y_dtype.  When
+ * every layer would run EXPAND on its own (AUTO above the short-L crossover,
+ * or FASQ_GEMM_EXPAND_TC) and n <= 4 layers share K groups, C and d, ONE
+ * launch covers all their row tiles; otherwise the layers run one fasq_gemm
+ * each, in order.  Errors as fasq_gemm. */
+fasq_status fasq_gemm_grouped(const fasq_layer* const* layers, int32_t n, const void* X_dev, int64_t M,
+                              void* const* Y_dev, fasq_dtype y_dtype, fasq_gemm_algo algo, void* stream);
+
 /* ---- diagnostics ---------------------------------------------------------- */
 
 /* Number of kernel launches the last successful compute call on this host

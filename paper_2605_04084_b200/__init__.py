@@ -35,7 +35,7 @@ EXPORTED = ["fasq_pack", "fasq_import", "fasq_import_ex", "fasq_export", "fasq_s
             "fasq_chain_create", "fasq_chain_create_tp", "fasq_chain_ipc_handle", "fasq_chain_set_peers",
             "fasq_chain_set_peer_chains", "fasq_chain_run", "fasq_chain_output", "fasq_chain_trace",
             "fasq_chain_ctas", "fasq_chain_free", "fasq_chain_run_host", "fasq_chain_check",
-            "fasq_chain_plan_ks", "fasq_gemv_host", "fasq_gemm",
+            "fasq_chain_plan_ks", "fasq_gemv_host", "fasq_gemm", "fasq_gemm_grouped",
             "fasq_llama_create", "fasq_llama_ipc_handle", "fasq_llama_set_peers", "fasq_llama_set_peer_models",
             "fasq_llama_chain",
             "fasq_llama_kv_cache", "fasq_llama_reset", "fasq_llama_step", "fasq_llama_step_ex", "fasq_llama_tokens",
@@ -151,6 +151,8 @@ def _load():
     L.fasq_llama_free.argtypes = [vp]
     L.fasq_llama_free.restype = None
     L.fasq_gemm.argtypes = [vp, vp, i64, vp, i32, i32, vp]
+    L.fasq_gemm_grouped.argtypes = [vp, i32, vp, i64, vp, i32, i32, vp]
+    L.fasq_gemm_grouped.restype = ctypes.c_int32
     L.fasq_set_allocator.argtypes = [vp, vp, vp]
     L.fasq_layer_distinct_centroids.argtypes = [vp, ctypes.POINTER(i64), vp]
     L.fasq_layer_distinct_centroids.restype = ctypes.c_int32
@@ -500,6 +502,30 @@ def gemm(layer: Layer, X: torch.Tensor, out: torch.Tensor | None = None,
     yt = FASQ_F32 if out.dtype == torch.float32 else FASQ_F16
     _check(lib.fasq_gemm(layer.handle, X.data_ptr(), M, out.data_ptr(), yt, algo, _stream(stream)))
     return out
+
+
+def gemm_grouped(layers, X: torch.Tensor, outs=None, out_dtype: torch.dtype = torch.float32, algo: int = GEMM_AUTO,
+                 stream=None):
+    """fasq_gemm_grouped: the prefill GEMMs of layers sharing X (q / k / v,
+    gate / up) -- one EXPAND launch over all their row tiles when each would run
+    EXPAND on its own.  Returns the list of Y [M][F_out_l]."""
+    X = _cuda(X, torch.float16, "X")
+    M = X.shape[0]
+    for L in layers:
+        if X.shape[1] != L.F_in:
+            raise FasqError(-5, "X has %d columns, layer F_in=%d" % (X.shape[1], L.F_in))
+    if outs is None:
+        outs = [torch.empty((M, L.F_out), dtype=out_dtype, device=X.device) for L in layers]
+    for L, o in zip(layers, outs):
+        _check_out(o, (M, L.F_out), (torch.float16, torch.float32))
+    if len({o.dtype for o in outs}) != 1:
+        raise FasqError(-1, "outs must share one dtype")
+    yt = FASQ_F32 if outs[0].dtype == torch.float32 else FASQ_F16
+    n = len(layers)
+    hs = (ctypes.c_void_p * n)(*[L.handle.value for L in layers])
+    ys = (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs])
+    _check(lib.fasq_gemm_grouped(hs, n, X.data_ptr(), M, ys, yt, algo, _stream(stream)))
+    return outs
 
 
 # ---- device memory through torch (fasq_set_allocator) -------------------------

@@ -362,14 +362,39 @@ fasq_status fasq_gemm(const fasq_layer* L, const void* X_dev, int64_t M, void* Y
             if (!gemm_tc_supported(L, M)) return FASQ_E_UNSUPPORTED;
             return gemm_tc_launch(L, X, M, Y_dev, yt, st);
         case FASQ_GEMM_AUTO:
-            // short L (M <= FASQ_GEMM_TC_DECODE_MAX, default 128): the tcgen05 decode kernel
-            // (weights as UMMA M, tokens as N); the 256-token EXPAND tiles run mostly empty there
+            // short L (M <= gemm_short_max: 32-96 by shape, FASQ_GEMM_TC_DECODE_MAX): the
+            // tcgen05 decode kernel (weights as UMMA M, tokens as N); above it EXPAND
             if (M <= gemm_short_max(L) && gemv_tc_supported(L, (int)M))
                 return gemv_tc_launch(L, X, (int)M, Y_dev, yt, 0u, st);
             if (gemm_tc_supported(L, M)) return gemm_tc_launch(L, X, M, Y_dev, yt, st);
             return gemm_lut_launch(L, X, M, Y_dev, yt, st);
     }
     return FASQ_E_ARG;
+}
+
+fasq_status fasq_gemm_grouped(const fasq_layer* const* layers, int32_t n, const void* X_dev, int64_t M,
+                              void* const* Y_dev, fasq_dtype yt, fasq_gemm_algo algo, void* stream) {
+    if (!layers || !Y_dev || !X_dev || n < 1 || M < 1) return FASQ_E_ARG;
+    if (yt != FASQ_F16 && yt != FASQ_F32) return FASQ_E_ARG;
+    for (int l = 0; l < n; ++l) {
+        if (!layers[l] || !Y_dev[l]) return FASQ_E_ARG;
+        if (layers[l]->F_in != layers[0]->F_in) return FASQ_E_SHAPE;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    // one EXPAND launch when every layer would run EXPAND on its own
+    bool one = n > 1 && (algo == FASQ_GEMM_AUTO || algo == FASQ_GEMM_EXPAND_TC) && gemm_tc_groupable(layers, n, M);
+    if (one && algo == FASQ_GEMM_AUTO)
+        for (int l = 0; l < n; ++l)
+            if (M <= gemm_short_max(layers[l]) && gemv_tc_supported(layers[l], (int)M)) one = false;
+    if (one) return gemm_tc_launch_grouped(layers, n, static_cast<const __half*>(X_dev), M, Y_dev, yt, st);
+    int launches = 0;
+    for (int l = 0; l < n; ++l) {
+        const fasq_status s = fasq_gemm(layers[l], X_dev, M, Y_dev[l], yt, algo, stream);
+        if (s != FASQ_OK) return s;
+        launches += fasq_last_launch_count();
+    }
+    set_launch_count(launches);
+    return FASQ_OK;
 }
 
 }  // extern "C"

@@ -183,6 +183,9 @@ fasq_status gemm_lut_launch(const fasq_layer* L, const __half* X, int64_t M, voi
 fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void* Y,
                            fasq_dtype yt, cudaStream_t st);
 bool gemm_tc_supported(const fasq_layer* L, int64_t M);
+bool gemm_tc_groupable(const fasq_layer* const* Ls, int n, int64_t M);
+fasq_status gemm_tc_launch_grouped(const fasq_layer* const* Ls, int n, const __half* X, int64_t M, void* const* Ys,
+                                   fasq_dtype yt, cudaStream_t st);
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda);
 // nullptr if unavailable (gemm_tc.cu).
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

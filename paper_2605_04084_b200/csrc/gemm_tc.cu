@@ -45,13 +45,21 @@ constexpr int TC_STAGES = 2;
 constexpr int TC_EXP_WARPS = 8;    // expansion warps (lane = weight row)
 constexpr int TC_THREADS = (3 + TC_EXP_WARPS) * 32;   // + X producer, MMA, codebook/index producer
 
-struct TcParams {
+// One layer of a (grouped) launch: its row tiles are [rt0, next layer's rt0).
+constexpr int kTcGroup = 4;
+struct TcLayer {
     const uint8_t* idx;      // [n_groups][F_out_pad/64][32][64] (fasq_internal.cuh)
     const uint8_t* cbimg;    // [n_groups][C][32][4]
-    void* Y;
+    void* Y;                 // [M][F_out]
+    int F_out, F_out_pad, rt0;
+};
+
+struct TcParams {
+    TcLayer lay[kTcGroup];   // layers sharing X, F_in, n_groups and C (q/k/v, gate/up): one launch
+    int n_lay;
     float* ws;               // split-K (gridDim.z > 1): fp32 partial tiles [ks][tiles][256 tokens][256 rows]
     unsigned* tickets;       // [tiles][2] arrive / depart counters (zero between launches)
-    int M, F_out, F_out_pad, n_groups, C, y_f32;
+    int M, n_groups, C, y_f32;
     int tile0, ntx;          // this launch covers tiles tile0 + blockIdx.x (row tile = tile % ntx)
     int pair_order;          // 1: tiles in pair order (even token-tile count); 0: row-major (tile % ntx, tile / ntx)
 };
@@ -120,7 +128,22 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     const bool po = PAIR || p.pair_order;
     const int nrt = po ? (tile_g >> 1) % p.ntx : tile_g % p.ntx;
     const int ntt = po ? 2 * ((tile_g >> 1) / p.ntx) + rank : tile_g / p.ntx;
-    const int n0t = nrt * TC_N;                              // weight-row tile (epilogue rows)
+    // the layer owning row tile nrt (static indices: the params stay in the constant bank)
+    const uint8_t* g_idx = p.lay[0].idx;
+    const uint8_t* g_cb = p.lay[0].cbimg;
+    void* g_Y = p.lay[0].Y;
+    int F_out = p.lay[0].F_out, F_out_pad = p.lay[0].F_out_pad, rt0 = 0;
+#pragma unroll
+    for (int l = 1; l < kTcGroup; ++l)
+        if (l < p.n_lay && nrt >= p.lay[l].rt0) {
+            g_idx = p.lay[l].idx;
+            g_cb = p.lay[l].cbimg;
+            g_Y = p.lay[l].Y;
+            F_out = p.lay[l].F_out;
+            F_out_pad = p.lay[l].F_out_pad;
+            rt0 = p.lay[l].rt0;
+        }
+    const int n0t = (nrt - rt0) * TC_N;                      // weight-row tile of its layer (epilogue rows)
     const int n0 = n0t + (PAIR ? rank * NR : 0);             // rows this CTA expands
     const int m0 = ntt * TC_M * TC_MT;                       // first token of this CTA's token tiles
     // split-K (small M: too few tiles for the SMs): this CTA's K chunks [kb, kb + nk)
@@ -187,7 +210,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
         }
     } else if (warp == 2 + TC_EXP_WARPS) {
         // ---------------------- codebook + index producer ----------------------
-        const int rows = max(0, min(NR, p.F_out_pad - n0));    // idx rows present (multiple of 64)
+        const int rows = max(0, min(NR, F_out_pad - n0));      // idx rows present (multiple of 64)
         const uint32_t idx_bytes = (uint32_t)rows * 32u;
         const uint32_t cb_u = dev::smem_u32(sC);
         for (int i = 0; i < nk; ++i) {
@@ -197,11 +220,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
                 dev::mbar_arrive_expect_tx(lfull_bar(s), idx_bytes + (uint32_t)CB_BYTES);
                 if (idx_bytes)
                     dev::bulk_g2s(dev::smem_u32(sI + s * IDX_BYTES),
-                                  p.idx + ((size_t)(kb + i) * p.F_out_pad + n0) * 32, idx_bytes, lfull_bar(s));
+                                  g_idx + ((size_t)(kb + i) * F_out_pad + n0) * 32, idx_bytes, lfull_bar(s));
                 // (a PAIR variant fetching one codebook half per CTA with
                 // .multicast::cluster was measured 25 % slower: the shared slot
                 // couples the two CTAs' rings; profiles/r02/gemm_pair_ab.txt)
-                dev::bulk_g2s(cb_u + (uint32_t)s * (uint32_t)CB_BYTES, p.cbimg + (size_t)(kb + i) * CB_BYTES,
+                dev::bulk_g2s(cb_u + (uint32_t)s * (uint32_t)CB_BYTES, g_cb + (size_t)(kb + i) * CB_BYTES,
                               (uint32_t)CB_BYTES, lfull_bar(s));
             }
             __syncwarp();
@@ -291,7 +314,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
         const uint32_t ib0 = (uint32_t)((ew * RPW) >> 6) * 2048u + (uint32_t)lane * 64u;   // 64-row block
         const uint32_t cw0 = (uint32_t)(((ew * RPW) & 63) >> 4);                          // first 16-row chunk
         const uint32_t rot = (uint32_t)(lane >> 1);
-        const bool have = n0 + ew * RPW < p.F_out_pad;   // this warp's rows were loaded (64-row blocks)
+        const bool have = n0 + ew * RPW < F_out_pad;     // this warp's rows were loaded (64-row blocks)
         for (int i = 0; i < nk; ++i) {
             const int s = i % SL, sx = i % SX;
             const uint32_t ph = (i / SL) & 1;
@@ -339,21 +362,21 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
             const int tile = (int)blockIdx.x;         // tile within this launch (workspace / tickets)
             // 32 consecutive outputs (rows n .. n+31) of token m -> Y (fp32 / fp16)
             auto store32 = [&](int n, const float* r) {
-                if (m >= p.M || n >= p.F_out) return;
-                const bool full = n + 32 <= p.F_out;
+                if (m >= p.M || n >= F_out) return;
+                const bool full = n + 32 <= F_out;
                 if (p.y_f32) {
-                    float* yr = reinterpret_cast<float*>(p.Y) + (size_t)m * p.F_out + n;
-                    if (full && (p.F_out % 4 == 0)) {
+                    float* yr = reinterpret_cast<float*>(g_Y) + (size_t)m * F_out + n;
+                    if (full && (F_out % 4 == 0)) {
 #pragma unroll
                         for (int v = 0; v < 8; ++v)
                             reinterpret_cast<float4*>(yr)[v] = make_float4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
                     } else {
                         for (int v = 0; v < 32; ++v)
-                            if (n + v < p.F_out) yr[v] = r[v];
+                            if (n + v < F_out) yr[v] = r[v];
                     }
                 } else {
-                    __half* yr = reinterpret_cast<__half*>(p.Y) + (size_t)m * p.F_out + n;
-                    if (full && (p.F_out % 8 == 0)) {
+                    __half* yr = reinterpret_cast<__half*>(g_Y) + (size_t)m * F_out + n;
+                    if (full && (F_out % 8 == 0)) {
 #pragma unroll
                         for (int v = 0; v < 4; ++v) {
                             __half2 h[4];
@@ -368,7 +391,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
                         }
                     } else {
                         for (int v = 0; v < 32; ++v)
-                            if (n + v < p.F_out) yr[v] = __float2half_rn(r[v]);
+                            if (n + v < F_out) yr[v] = __float2half_rn(r[v]);
                     }
                 }
             };
@@ -501,7 +524,30 @@ bool gemm_tc_supported(const fasq_layer* L, int64_t M) {
            tc_smem_bytes(L->C) <= kSmemBudget && get_encode() != nullptr;
 }
 
+// Layers one grouped launch can take: the same input X (F_in), K groups, C and d.
+bool gemm_tc_groupable(const fasq_layer* const* Ls, int n, int64_t M) {
+    if (n < 1 || n > kTcGroup) return false;
+    for (int l = 0; l < n; ++l) {
+        if (!Ls[l] || Ls[l]->bits || Ls[l]->dim0 || !gemm_tc_supported(Ls[l], M)) return false;
+        if (Ls[l]->F_in != Ls[0]->F_in || Ls[l]->n_groups != Ls[0]->n_groups || Ls[l]->C != Ls[0]->C ||
+            Ls[l]->d != Ls[0]->d)
+            return false;
+    }
+    return true;
+}
+
 fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void* Y, fasq_dtype yt, cudaStream_t st) {
+    return gemm_tc_launch_grouped(&L, 1, X, M, &Y, yt, st);
+}
+
+// One EXPAND launch over n layers sharing X: the row tiles of all layers form
+// one tile grid (layer l owns [rt0_l, rt0_l + ntx_l)), so the small layers of a
+// step (k / v: 4 row tiles) share the SMs with the large ones instead of each
+// paying a launch, a pipeline fill and a split-K merge on a mostly idle GPU.
+fasq_status gemm_tc_launch_grouped(const fasq_layer* const* Ls, int n, const __half* X, int64_t M, void* const* Ys,
+                                   fasq_dtype yt, cudaStream_t st) {
+    if (!gemm_tc_groupable(Ls, n, M)) return FASQ_E_UNSUPPORTED;
+    const fasq_layer* L = Ls[0];
     PFN_encodeTiled enc = get_encode();
     if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return FASQ_E_CUDA; }
     if ((reinterpret_cast<uintptr_t>(X) & 15) != 0) return FASQ_E_ARG;
@@ -515,12 +561,19 @@ fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed"); return FASQ_E_CUDA; }
     TcParams p{};
-    p.idx = L->idx;
-    p.cbimg = L->cbimg;
-    p.Y = Y;
+    int ntx = 0;
+    for (int l = 0; l < n; ++l) {
+        p.lay[l].idx = Ls[l]->idx;
+        p.lay[l].cbimg = Ls[l]->cbimg;
+        p.lay[l].Y = Ys[l];
+        p.lay[l].F_out = (int)Ls[l]->F_out;
+        p.lay[l].F_out_pad = Ls[l]->F_out_pad;
+        p.lay[l].rt0 = ntx;
+        // F_out_pad rows of each idx table exist; a tile past F_out_pad loads none
+        ntx += (Ls[l]->F_out_pad + TC_N - 1) / TC_N;
+    }
+    p.n_lay = n;
     p.M = (int)M;
-    p.F_out = (int)L->F_out;
-    p.F_out_pad = L->F_out_pad;
     p.n_groups = L->n_groups;
     p.C = L->C;
     p.y_f32 = yt == FASQ_F32;
@@ -538,9 +591,6 @@ fasq_status gemm_tc_launch(const fasq_layer* L, const __half* X, int64_t M, void
     const char* pe = getenv("FASQ_GEMM_PAIR");
     const bool pair_env = pe && atoi(pe) == 1;
     const bool pair_ok = pair_env && lim2 >= smem2;
-    // F_out_pad rows of the idx table exist; tiles past F_out_pad read beyond it
-    // -> require the row tile grid to stay within F_out_pad (pad logic below).
-    const int ntx = (L->F_out_pad + TC_N - 1) / TC_N;
     // token tiles: an even count is numbered in pair order (kernel); an odd count
     // runs row-major with the exact count (a phantom tile would expand its weight
     // slab for nothing: half the CTAs at M <= 256), unless 2-CTA pairs are on, which

@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <initializer_list>
 #include <type_traits>
 #include <vector>
 
@@ -907,15 +908,24 @@ fasq_status fasq_llama_prefill(fasq_llama* m, const int32_t* tokens_dev, int32_t
     auto gemm = [&](const fasq_layer* L, const __half* X, float* Y) {
         if (s == FASQ_OK) s = fasq_gemm(L, X, M, Y, FASQ_F32, FASQ_GEMM_AUTO, st);
     };
+    // products sharing their input (q / k / v, gate / up): one EXPAND launch above the short-L crossover
+    auto gemm_group = [&](std::initializer_list<const fasq_layer*> Ls, const __half* X,
+                          std::initializer_list<float*> Ys) {
+        const fasq_layer* lv[4];
+        void* yv[4];
+        int n = 0;
+        for (const fasq_layer* L : Ls) lv[n++] = L;
+        n = 0;
+        for (float* Y : Ys) yv[n++] = Y;
+        if (s == FASQ_OK) s = fasq_gemm_grouped(lv, n, X, M, yv, FASQ_F32, FASQ_GEMM_AUTO, st);
+    };
     for (int l = 0; l < D.n_layers && s == FASQ_OK; ++l) {
         // block 0: h = embedding; block l > 0: h += the previous block's down product
         k_pf_resid_norm<<<M, 256, 0, st>>>(h, l ? y : nullptr, l ? nullptr : tokens_dev,
                                            static_cast<const __half*>(D.embed),
                                            static_cast<const __half*>(D.attn_norm[l]), x, n, D.rms_eps, 0);
         check(cudaGetLastError(), "prefill rmsnorm");
-        gemm(D.q[l], x, q);
-        gemm(D.k[l], x, k);
-        gemm(D.v[l], x, v);
+        gemm_group({D.q[l], D.k[l], D.v[l]}, x, {q, k, v});
         if (s != FASQ_OK) break;
         k_pf_rope_cache<<<pf_blocks((int64_t)M * (H + 2 * KV) * (hd / 2), 256), 256, 0, st>>>(
             q, k, v, m->kc[l], m->vc[l], m->rope, M, pos0, H, KV, hd, D.max_T);
@@ -930,8 +940,7 @@ fasq_status fasq_llama_prefill(fasq_llama* m, const int32_t* tokens_dev, int32_t
         k_pf_resid_norm<<<M, 256, 0, st>>>(h, y, nullptr, nullptr, static_cast<const __half*>(D.mlp_norm[l]), x, n,
                                            D.rms_eps, 0);
         check(cudaGetLastError(), "prefill mlp norm");
-        gemm(D.gate[l], x, g);
-        gemm(D.up[l], x, u);
+        gemm_group({D.gate[l], D.up[l]}, x, {g, u});
         if (s != FASQ_OK) break;
         k_pf_silu_mul<<<pf_blocks((int64_t)M * ffn / 4 + 3, 256), 256, 0, st>>>(g, u, a, (int64_t)M * ffn);
         check(cudaGetLastError(), "prefill swiglu");

@@ -254,3 +254,48 @@ def test_gemm_tc_token_tile_edges(F, oracle_lib, M):
     for r0 in (0, 352, F_out - 32):
         ok, m = parity_ok(Yn[:, r0:r0 + 32], oracle_lib.gemm(cb, idx, X, rows=(r0, r0 + 32)), X, F_in)
         assert ok, (r0, m)
+
+
+@pytest.mark.parametrize("M,algo", [(128, "auto"), (300, "tc"), (2048, "tc"), (16, "auto")])
+def test_gemm_grouped_qkv_gate_up(F, oracle_lib, M, algo):
+    """fasq_gemm_grouped: q / k / v (4096 / 1024 / 1024 rows) and gate / up of
+    one input.  Above the short-L crossover ONE EXPAND launch covers all row
+    tiles (launch count 1 or 2 with a tail wave); at M = 16 AUTO runs one
+    fasq_gemm per layer.  Each Y against the oracle on sampled rows, against
+    the single-layer fasq_gemm (within the fp32 split-K rounding), and
+    bit-identical on repeat."""
+    a = F.GEMM_AUTO if algo == "auto" else F.GEMM_EXPAND_TC
+    X = synth.activation(M, 4096, seed=M + 70)
+    Xd = torch.from_numpy(X).cuda()
+    for shapes in (((4096, 4096), (1024, 4096), (1024, 4096)), ((14336, 4096), (14336, 4096))):
+        host, Ls = [], []
+        for i, (fo, fi) in enumerate(shapes):
+            cb, idx = synth.random_layer(fo, fi, 2, 256, seed=M + 10 * i + fo)
+            host.append((cb, idx))
+            Ls.append(F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), fi))
+        Ys = F.gemm_grouped(Ls, Xd, algo=a)
+        n_launch = F.last_launch_count()
+        Ys2 = F.gemm_grouped(Ls, Xd, algo=a)
+        torch.cuda.synchronize()
+        if M >= 128:
+            assert n_launch <= 2, n_launch
+        for (cb, idx), L, Y, Y2 in zip(host, Ls, Ys, Ys2):
+            Yn = Y.cpu().numpy().astype(np.float64)
+            assert np.array_equal(Yn, Y2.cpu().numpy().astype(np.float64))
+            fo = L.F_out
+            for r0 in (0, fo // 2 + 64, fo - 64):
+                ok, m = parity_ok(Yn[:, r0:r0 + 64], oracle_lib.gemm(cb, idx, X, rows=(r0, r0 + 64)), X, 4096)
+                assert ok, (fo, r0, m)
+            Ys1 = F.gemm(L, Xd, algo=a).cpu().numpy().astype(np.float64)
+            assert np.linalg.norm(Yn - Ys1) / np.linalg.norm(Ys1) <= 1e-5
+
+
+def test_gemm_grouped_errors(F):
+    cb, idx = synth.random_layer(256, 512, 2, 16, seed=1)
+    cb2, idx2 = synth.random_layer(256, 1024, 2, 16, seed=2)
+    L1 = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), 512)
+    L2 = F.import_layer(torch.from_numpy(cb2).cuda(), torch.from_numpy(idx2).cuda(), 1024)
+    X = torch.zeros((4, 512), dtype=torch.float16, device="cuda")
+    with pytest.raises(F.FasqError) as e:
+        F.gemm_grouped([L1, L2], X)
+    assert e.value.code == -5
