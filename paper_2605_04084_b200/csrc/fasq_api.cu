@@ -325,10 +325,10 @@ fasq_status fasq_gemv_host(const fasq_layer* L, const void* x_host, int32_t B, v
 static int64_t gemm_short_max(const fasq_layer* L) {
     const char* e = getenv("FASQ_GEMM_TC_DECODE_MAX");
     if (e) return atoll(e);
-    // measured crossovers against EXPAND's split-K (profiles/r02/short_gemm_sweep_v2.jsonl):
-    // 4096 x 14336 <= 96, 1024 x 4096 <= 64, 4096^2 and 14336 x 4096 <= 32
-    if (L->F_in > 8192) return 96;
-    if (L->F_out <= 2048) return 64;
+    // measured crossovers against EXPAND's split-K (profiles/r02/short_gemm_sweep_v3.jsonl):
+    // 4096 x 14336 and 1024 x 4096 <= 64, 4096^2 <= 32, 14336 x 4096 <= 16
+    if (L->F_in > 8192 || L->F_out <= 2048) return 64;
+    if (L->F_out > 8192) return 16;
     return 32;
 }
 

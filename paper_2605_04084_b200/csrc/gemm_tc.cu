@@ -146,6 +146,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
     const int n0t = (nrt - rt0) * TC_N;                      // weight-row tile of its layer (epilogue rows)
     const int n0 = n0t + (PAIR ? rank * NR : 0);             // rows this CTA expands
     const int m0 = ntt * TC_M * TC_MT;                       // first token of this CTA's token tiles
+    // token tiles with real tokens: a tile with <= 128 left loads one X tile and
+    // issues one accumulator's MMAs (the second would multiply zero-filled rows;
+    // at M <= 128 that was half the tensor time of every chunk).  PAIR MMAs span
+    // both CTAs' tiles: always both.
+    const int nmt = (!PAIR && m0 + TC_M >= p.M) ? 1 : TC_MT;
     // split-K (small M: too few tiles for the SMs): this CTA's K chunks [kb, kb + nk)
     const int ksplit = (int)gridDim.z, kz = (int)blockIdx.z;
     const int kb = (int)((int64_t)kz * p.n_groups / ksplit);
@@ -200,11 +205,12 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
             const int s = i % SX;
             if (i >= SX) dev::mbar_wait(empty_bar(s), ((i / SX) + 1) & 1);
             if (lane == 0) {
-                dev::mbar_arrive_expect_tx(full_bar(s), (uint32_t)A_BYTES);
+                dev::mbar_arrive_expect_tx(full_bar(s), (uint32_t)(nmt * A_TILE));
 #pragma unroll
                 for (int t = 0; t < TC_MT; ++t)
-                    tma_load_2d(dev::smem_u32(sA + s * A_BYTES + t * A_TILE), &xmap, (kb + i) * TC_K, m0 + t * TC_M,
-                                full_bar(s));
+                    if (t < nmt)
+                        tma_load_2d(dev::smem_u32(sA + s * A_BYTES + t * A_TILE), &xmap, (kb + i) * TC_K,
+                                    m0 + t * TC_M, full_bar(s));
             }
             __syncwarp();
         }
@@ -259,6 +265,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
                 const uint32_t b_base = dev::smem_u32(sB + s * B_BYTES);
 #pragma unroll
                 for (int t = 0; t < TC_MT; ++t) {
+                    if (t >= nmt) break;
                     const uint32_t a_base = dev::smem_u32(sA + s * A_BYTES + t * A_TILE);
 #pragma unroll
                     for (int kk = 0; kk < TC_K / 16; ++kk) {

@@ -383,7 +383,8 @@ __global__ void __launch_bounds__(128, 3) k_pf_attn(const float* __restrict__ q,
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int HG = H / G, wg = (int)blockIdx.x * 4 + w;
     if (wg >= M * HG) return;
-    const int m = wg / HG, hh0 = (wg - m * HG) * G, j = hh0 / (H / KV), pos = pos0 + m;
+    // the longest rows (last tokens) first: the tail wave holds the short ones
+    const int mi = wg / HG, m = M - 1 - mi, hh0 = (wg - mi * HG) * G, j = hh0 / (H / KV), pos = pos0 + m;
     const float sc = 1.0f / sqrtf((float)hd);
 #pragma unroll
     for (int g = 0; g < G; ++g) {

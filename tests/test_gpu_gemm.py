@@ -214,13 +214,14 @@ def test_gemm_tc_pair_cta_group2(F, oracle_lib, monkeypatch, F_out, F_in, M):
     assert rel <= 1e-6, rel
 
 
-@pytest.mark.parametrize("F_out,F_in,M", [(4096, 4096, 32), (14336, 4096, 29), (4096, 14336, 96), (1000, 2048, 61),
-                                          (4096, 4096, 128), (1024, 4096, 100)])
+@pytest.mark.parametrize("F_out,F_in,M", [(4096, 4096, 32), (14336, 4096, 13), (4096, 14336, 64), (1000, 2048, 61),
+                                          (4096, 4096, 128), (1024, 4096, 100), (14336, 4096, 29)])
 def test_gemm_auto_short_L_runs_tcgen05_decode(F, oracle_lib, F_out, F_in, M):
     """Short-L prefill (NEXT-3): fasq_gemm AUTO at M up to the measured
-    crossover (32 / 64 / 96 by shape) runs the tcgen05 decode kernel (weights as
-    UMMA M), above it EXPAND with split-K (M = 128 / 100: one real accumulator per
-    tile); sampled rows against the oracle and against the EXPAND kernel's Y."""
+    crossover (16 / 32 / 64 by shape) runs the tcgen05 decode kernel (weights as
+    UMMA M), above it EXPAND with split-K (M = 128 / 100 / 29: one real
+    accumulator per tile); sampled rows against the oracle and against the
+    EXPAND kernel's Y."""
     cb, idx = synth.random_layer(F_out, F_in, 2, 256, seed=M)
     X = synth.activation(M, F_in, seed=M + 1)
     L = F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), F_in)
