@@ -397,12 +397,20 @@ fasq_status fasq_llama_step(fasq_llama* model, void* stream);
 /* Whole-model PREFILL of a prompt (the paper's E2E protocol: prompt 128)
  * for a one-sequence, one-GPU model (B = 1, world = 1, head_dim 64 or 128): the M
  * tokens tokens_dev (int32, device) at positions [pos0, pos0 + M) go through
- * every block -- RMSNorm, PQ q/k/v (fasq_gemm AUTO), RoPE, the KV cache write,
- * causal GQA attention over positions <= each token's, PQ o + residual,
- * RMSNorm, PQ gate/up, SwiGLU, PQ down + residual -- and the greedy token of
- * the last prompt position becomes the next fasq_llama_step's input at
- * position pos0 + M.  Cache positions < pos0 must already hold the earlier
- * context.  Stream-ordered (per-call workspaces from the library allocator). */
+ * every block -- RMSNorm, PQ q/k/v (fasq_gemm_grouped AUTO), RoPE, the KV
+ * cache write, causal GQA attention over positions <= each token's, PQ o +
+ * residual, RMSNorm, PQ gate/up, SwiGLU, PQ down + residual -- and the greedy
+ * token of the last prompt position becomes the next fasq_llama_step's input
+ * at position pos0 + M.  Cache positions < pos0 must already hold the earlier
+ * context.  Stream-ordered with respect to `stream`.  Outside stream capture
+ * the work runs on a model-private stream joined to `stream` by events: the
+ * first call for a given M launches eagerly and captures a CUDA graph that the
+ * next calls with that M replay (tokens and pos0 are staged into device memory
+ * it reads; the model keeps a working set for the largest M seen).  Inside a
+ * caller's capture (or with FASQ_PREFILL_EAGER set) every call launches its
+ * kernels on `stream` with a per-call working set from the library allocator.
+ * tokens_dev may be overwritten by work ordered after the call on `stream`.
+ * Not thread-safe per model. */
 fasq_status fasq_llama_prefill(fasq_llama* model, const int32_t* tokens_dev, int32_t M, int32_t pos0, void* stream);
 /* One step in parts, for per-kernel timing: part 0 = both launches
  * (fasq_llama_step), 1 = the chain kernel only, 2 = the lm_head kernel only.

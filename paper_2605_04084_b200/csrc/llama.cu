@@ -51,6 +51,15 @@ struct fasq_llama {
     int n_heads_l = 0, n_kv_l = 0, ffn_l = 0, vocab_l = 0;
     int last_step = 0;                 // chain step of the last down projection
     size_t lm_smem = 0;
+    // fasq_llama_prefill: persistent buffers for up to pf_cap tokens, the staged
+    // tokens / pos0, a private capture stream and the graph of the last M
+    int pf_cap = 0;
+    uint8_t* pf_buf = nullptr;
+    int* pf_tok = nullptr;             // [pf_cap] prompt tokens, [pf_cap] = pos0
+    cudaStream_t pf_stream = nullptr;
+    cudaEvent_t pf_ev[2] = {nullptr, nullptr};
+    cudaGraphExec_t pf_exec = nullptr;
+    int pf_exec_M = 0;
 };
 
 namespace fasq {
@@ -171,8 +180,9 @@ k_lm_head(const __half* __restrict__ W, int V_local, int v0, int hidden, long lo
 // keep the position).  Writes the token slot the next run reads (parity of
 // the previous run, derived on the device) as if an lm_head had chosen it.
 __global__ void k_llama_reset(unsigned long long* tail, int nctas, const int* tokens, int B, int pos,
-                              long long expect) {
+                              long long expect, const int* pos_base = nullptr) {
     const int b = threadIdx.x;
+    if (pos_base) pos += *pos_base;   // prefill: pos = pos0 (device-resident) + M
     const unsigned long long runs = tail[T_ENTRY] / (unsigned long long)nctas;
     const unsigned pp = (unsigned)((runs + 1ull) & 1ull);   // (runs - 1) & 1
     if (b < 8) {
@@ -215,6 +225,14 @@ void destroy_model(fasq_llama* m) {
     dev_free(m->tok_dev, 0);
     if (m->tok_pin) cudaFreeHost(m->tok_pin);
     if (m->io_exec) cudaGraphExecDestroy(m->io_exec);
+    if (m->pf_exec) cudaGraphExecDestroy(m->pf_exec);
+    if (m->pf_buf) {
+        if (m->pf_stream) cudaStreamSynchronize(m->pf_stream);
+        dev_free(m->pf_buf, 0);
+    }
+    for (cudaEvent_t e : m->pf_ev)
+        if (e) cudaEventDestroy(e);
+    if (m->pf_stream) cudaStreamDestroy(m->pf_stream);
     delete m;
 }
 
@@ -337,7 +355,8 @@ __global__ void __launch_bounds__(256) k_pf_resid_norm(float* __restrict__ h, co
 // RoPE on q (in place, fp32) and k; the new k (rotated) / v enter the cache as fp16
 __global__ void k_pf_rope_cache(float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
                                 __half* __restrict__ kc, __half* __restrict__ vc, const float2* __restrict__ rope,
-                                int M, int pos0, int H, int KV, int hd, int max_T) {
+                                int M, const int* __restrict__ pos0_p, int H, int KV, int hd, int max_T) {
+    const int pos0 = *pos0_p;   // device-resident: the cached prefill graph serves any pos0
     const int half = hd / 2;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int per = (H + 2 * KV) * half;   // rotation pairs (q, k) and v pairs per token
@@ -377,14 +396,14 @@ __global__ void k_pf_rope_cache(float* __restrict__ q, const float* __restrict__
 template <int DPL, int G>
 __global__ void __launch_bounds__(128, 3) k_pf_attn(const float* __restrict__ q, const __half* __restrict__ kc,
                                                     const __half* __restrict__ vc, __half* __restrict__ out, int M,
-                                                    int pos0, int H, int KV, int max_T) {
+                                                    const int* __restrict__ pos0_p, int H, int KV, int max_T) {
     constexpr int hd = 32 * DPL;
     __shared__ __align__(16) float qs[4][G][hd];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int HG = H / G, wg = (int)blockIdx.x * 4 + w;
     if (wg >= M * HG) return;
     // the longest rows (last tokens) first: the tail wave holds the short ones
-    const int mi = wg / HG, m = M - 1 - mi, hh0 = (wg - mi * HG) * G, j = hh0 / (H / KV), pos = pos0 + m;
+    const int mi = wg / HG, m = M - 1 - mi, hh0 = (wg - mi * HG) * G, j = hh0 / (H / KV), pos = *pos0_p + m;
     const float sc = 1.0f / sqrtf((float)hd);
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -476,7 +495,7 @@ __global__ void __launch_bounds__(128, 3) k_pf_attn(const float* __restrict__ q,
 }
 
 template <int DPL>
-void pf_attn_launch(const float* q, const __half* kc, const __half* vc, __half* out, int M, int pos0, int H, int KV,
+void pf_attn_launch(const float* q, const __half* kc, const __half* vc, __half* out, int M, const int* pos0, int H, int KV,
                     int max_T, cudaStream_t st) {
     const int grp = H / KV;
     const int G = grp % 4 == 0 ? 4 : grp % 2 == 0 ? 2 : 1;
@@ -567,6 +586,8 @@ __global__ void k_pf_token(const unsigned long long* __restrict__ best, int* __r
 }
 
 inline unsigned pf_blocks(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+__global__ void k_pf_set(int* __restrict__ dst, int v) { *dst = v; }
 
 }  // namespace
 }  // namespace fasq
@@ -881,30 +902,50 @@ fasq_status fasq_llama_step_io(fasq_llama* m, const int32_t* tokens_in_host, int
     return s;
 }
 
-fasq_status fasq_llama_prefill(fasq_llama* m, const int32_t* tokens_dev, int32_t M, int32_t pos0, void* stream) {
-    if (!m || !tokens_dev || M < 1 || pos0 < 0) return FASQ_E_ARG;
-    const fasq_llama_desc& D = m->desc;
-    if (pos0 + M > D.max_T) return FASQ_E_ARG;
-    if (D.B != 1 || D.world != 1 || (D.head_dim != 128 && D.head_dim != 64) || D.hidden % 8) {
-        set_error("llama prefill: one sequence (B = 1), one GPU, head_dim 64 or 128");
-        return FASQ_E_UNSUPPORTED;
-    }
-    cudaStream_t st = (cudaStream_t)stream;
+}  // extern "C"
+
+namespace fasq {
+namespace {
+
+// prefill working set for M tokens (fp32 residual / products, fp16 inputs)
+struct PfBufs {
+    float *h, *q, *k, *v, *y, *g, *u;
+    __half *x, *a;
+    unsigned long long* best;
+};
+
+size_t pf_layout(const fasq_llama_desc& D, int M, PfBufs* b, uint8_t* base) {
     const int n = D.hidden, H = D.n_heads, KV = D.n_kv_heads, hd = D.head_dim, ffn = D.ffn;
-    const int64_t Mn = (int64_t)M * n;
-    float *h = nullptr, *q = nullptr, *k = nullptr, *v = nullptr, *y = nullptr, *g = nullptr, *u = nullptr;
-    __half *x = nullptr, *a = nullptr;
-    unsigned long long* best = nullptr;
-    fasq_status s = dev_alloc_t(&h, (size_t)Mn * 4, st);
-    if (s == FASQ_OK) s = dev_alloc_t(&q, (size_t)M * H * hd * 4, st);
-    if (s == FASQ_OK) s = dev_alloc_t(&k, (size_t)M * KV * hd * 4, st);
-    if (s == FASQ_OK) s = dev_alloc_t(&v, (size_t)M * KV * hd * 4, st);
-    if (s == FASQ_OK) s = dev_alloc_t(&y, (size_t)Mn * 4, st);
-    if (s == FASQ_OK) s = dev_alloc_t(&g, (size_t)M * ffn * 4, st);
-    if (s == FASQ_OK) s = dev_alloc_t(&u, (size_t)M * ffn * 4, st);
-    if (s == FASQ_OK) s = dev_alloc_t(&x, (size_t)M * std::max(n, std::max(ffn, H * hd)) * 2, st);
-    if (s == FASQ_OK) s = dev_alloc_t(&a, (size_t)M * std::max(ffn, H * hd) * 2, st);
-    if (s == FASQ_OK) s = dev_alloc_t(&best, 8, st);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        uint8_t* p = base ? base + off : nullptr;
+        off += (bytes + 255) / 256 * 256;
+        return p;
+    };
+    const size_t Mn = (size_t)M * n;
+    PfBufs t;
+    t.h = reinterpret_cast<float*>(take(Mn * 4));
+    t.q = reinterpret_cast<float*>(take((size_t)M * H * hd * 4));
+    t.k = reinterpret_cast<float*>(take((size_t)M * KV * hd * 4));
+    t.v = reinterpret_cast<float*>(take((size_t)M * KV * hd * 4));
+    t.y = reinterpret_cast<float*>(take(Mn * 4));
+    t.g = reinterpret_cast<float*>(take((size_t)M * ffn * 4));
+    t.u = reinterpret_cast<float*>(take((size_t)M * ffn * 4));
+    t.x = reinterpret_cast<__half*>(take((size_t)M * std::max(n, std::max(ffn, H * hd)) * 2));
+    t.a = reinterpret_cast<__half*>(take((size_t)M * std::max(ffn, H * hd) * 2));
+    t.best = reinterpret_cast<unsigned long long*>(take(8));
+    if (b) *b = t;
+    return off;
+}
+
+// The whole prefill as stream work on st: tokens / pos0 read from device memory
+// (so the captured graph serves any prompt and position of M tokens).
+fasq_status pf_enqueue(fasq_llama* m, const int* tok, const int* pos0_p, int M, const PfBufs& B, cudaStream_t st) {
+    const fasq_llama_desc& D = m->desc;
+    const int n = D.hidden, H = D.n_heads, KV = D.n_kv_heads, hd = D.head_dim, ffn = D.ffn;
+    float *h = B.h, *q = B.q, *k = B.k, *v = B.v, *y = B.y, *g = B.g, *u = B.u;
+    __half *x = B.x, *a = B.a;
+    fasq_status s = FASQ_OK;
     auto check = [&](cudaError_t e, const char* w) { if (s == FASQ_OK && e != cudaSuccess) s = cuda_fail(e, w); };
     auto gemm = [&](const fasq_layer* L, const __half* X, float* Y) {
         if (s == FASQ_OK) s = fasq_gemm(L, X, M, Y, FASQ_F32, FASQ_GEMM_AUTO, st);
@@ -914,27 +955,26 @@ fasq_status fasq_llama_prefill(fasq_llama* m, const int32_t* tokens_dev, int32_t
                           std::initializer_list<float*> Ys) {
         const fasq_layer* lv[4];
         void* yv[4];
-        int n = 0;
-        for (const fasq_layer* L : Ls) lv[n++] = L;
-        n = 0;
-        for (float* Y : Ys) yv[n++] = Y;
-        if (s == FASQ_OK) s = fasq_gemm_grouped(lv, n, X, M, yv, FASQ_F32, FASQ_GEMM_AUTO, st);
+        int c = 0;
+        for (const fasq_layer* L : Ls) lv[c++] = L;
+        c = 0;
+        for (float* Y : Ys) yv[c++] = Y;
+        if (s == FASQ_OK) s = fasq_gemm_grouped(lv, c, X, M, yv, FASQ_F32, FASQ_GEMM_AUTO, st);
     };
     for (int l = 0; l < D.n_layers && s == FASQ_OK; ++l) {
         // block 0: h = embedding; block l > 0: h += the previous block's down product
-        k_pf_resid_norm<<<M, 256, 0, st>>>(h, l ? y : nullptr, l ? nullptr : tokens_dev,
-                                           static_cast<const __half*>(D.embed),
+        k_pf_resid_norm<<<M, 256, 0, st>>>(h, l ? y : nullptr, l ? nullptr : tok, static_cast<const __half*>(D.embed),
                                            static_cast<const __half*>(D.attn_norm[l]), x, n, D.rms_eps, 0);
         check(cudaGetLastError(), "prefill rmsnorm");
         gemm_group({D.q[l], D.k[l], D.v[l]}, x, {q, k, v});
         if (s != FASQ_OK) break;
         k_pf_rope_cache<<<pf_blocks((int64_t)M * (H + 2 * KV) * (hd / 2), 256), 256, 0, st>>>(
-            q, k, v, m->kc[l], m->vc[l], m->rope, M, pos0, H, KV, hd, D.max_T);
+            q, k, v, m->kc[l], m->vc[l], m->rope, M, pos0_p, H, KV, hd, D.max_T);
         check(cudaGetLastError(), "prefill rope");
         if (hd == 128)
-            pf_attn_launch<4>(q, m->kc[l], m->vc[l], a, M, pos0, H, KV, D.max_T, st);
+            pf_attn_launch<4>(q, m->kc[l], m->vc[l], a, M, pos0_p, H, KV, D.max_T, st);
         else
-            pf_attn_launch<2>(q, m->kc[l], m->vc[l], a, M, pos0, H, KV, D.max_T, st);
+            pf_attn_launch<2>(q, m->kc[l], m->vc[l], a, M, pos0_p, H, KV, D.max_T, st);
         check(cudaGetLastError(), "prefill attention");
         gemm(D.o[l], a, y);
         if (s != FASQ_OK) break;
@@ -948,22 +988,125 @@ fasq_status fasq_llama_prefill(fasq_llama* m, const int32_t* tokens_dev, int32_t
         gemm(D.down[l], a, y);
     }
     if (s == FASQ_OK) {
-        // the last prompt position's greedy token -> the decode chain's token slot
+        // the last prompt position's greedy token -> the decode chain's token slot;
         // only the last position's residual is still needed: its final add + norm
         k_pf_resid_norm<<<1, 256, 0, st>>>(h, y, nullptr, nullptr, static_cast<const __half*>(D.final_norm), x, n,
                                            D.rms_eps, M - 1);
-        check(cudaMemsetAsync(best, 0, 8, st), "prefill argmax");
+        check(cudaMemsetAsync(B.best, 0, 8, st), "prefill argmax");
         k_pf_lm_argmax<<<std::min<int64_t>(pf_blocks(D.vocab, 8), (int64_t)sm_count() * 2), 256, 0, st>>>(
-            static_cast<const __half*>(D.lm_head), x, D.vocab, n, best);
-        k_pf_token<<<1, 1, 0, st>>>(best, m->tok_dev);
-        k_llama_reset<<<1, 32, 0, st>>>(m->chain->tail(), m->chain->nctas, m->tok_dev, 1, pos0 + M,
-                                        (long long)D.world * m->lm_ctas);
+            static_cast<const __half*>(D.lm_head), x, D.vocab, n, B.best);
+        k_pf_token<<<1, 1, 0, st>>>(B.best, m->tok_dev);
+        k_llama_reset<<<1, 32, 0, st>>>(m->chain->tail(), m->chain->nctas, m->tok_dev, 1, M,
+                                        (long long)D.world * m->lm_ctas, pos0_p);
         check(cudaGetLastError(), "prefill token");
     }
-    for (void* p : {(void*)h, (void*)q, (void*)k, (void*)v, (void*)y, (void*)g, (void*)u, (void*)x, (void*)a,
-                    (void*)best})
-        dev_free(p, st);
-    if (s == FASQ_OK) set_launch_count(0);
+    return s;
+}
+
+}  // namespace
+}  // namespace fasq
+
+extern "C" {
+
+fasq_status fasq_llama_prefill(fasq_llama* m, const int32_t* tokens_dev, int32_t M, int32_t pos0, void* stream) {
+    if (!m || !tokens_dev || M < 1 || pos0 < 0) return FASQ_E_ARG;
+    const fasq_llama_desc& D = m->desc;
+    if (pos0 + M > D.max_T) return FASQ_E_ARG;
+    if (D.B != 1 || D.world != 1 || (D.head_dim != 128 && D.head_dim != 64) || D.hidden % 8) {
+        set_error("llama prefill: one sequence (B = 1), one GPU, head_dim 64 or 128");
+        return FASQ_E_UNSUPPORTED;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    FASQ_CUDA_TRY(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone || getenv("FASQ_PREFILL_EAGER")) {
+        // the caller is capturing (or asked for eager launches): per-call working
+        // set and staging (stream-ordered allocations become graph memory nodes)
+        PfBufs B;
+        const size_t bytes = pf_layout(D, M, nullptr, nullptr);
+        uint8_t* base = nullptr;
+        int* pos_d = nullptr;
+        fasq_status s = dev_alloc_t(&base, bytes, st);
+        if (s == FASQ_OK) s = dev_alloc_t(&pos_d, sizeof(int), st);
+        if (s == FASQ_OK) {
+            pf_layout(D, M, &B, base);
+            k_pf_set<<<1, 1, 0, st>>>(pos_d, pos0);
+            s = pf_enqueue(m, tokens_dev, pos_d, M, B, st);
+        }
+        dev_free(pos_d, st);
+        dev_free(base, st);
+        if (s == FASQ_OK) set_launch_count(1 + 8 * D.n_layers + 5);
+        return s;
+    }
+    // Not capturing: the prefill of M tokens runs as ONE cached CUDA graph on a
+    // private stream joined to `stream` (the ~230 launches of a Llama-3-8B
+    // prefill cost ~0.5 ms of host launch time eagerly).  The first call for a
+    // given M runs eagerly on that stream -- which also sizes its split-K
+    // workspaces -- and captures the graph for the next calls; tokens and pos0
+    // are staged into device memory the graph reads.
+    if (!m->pf_stream) {
+        FASQ_CUDA_TRY(cudaStreamCreateWithFlags(&m->pf_stream, cudaStreamNonBlocking));
+        FASQ_CUDA_TRY(cudaEventCreateWithFlags(&m->pf_ev[0], cudaEventDisableTiming));
+        FASQ_CUDA_TRY(cudaEventCreateWithFlags(&m->pf_ev[1], cudaEventDisableTiming));
+    }
+    cudaStream_t ps = m->pf_stream;
+    FASQ_CUDA_TRY(cudaEventRecord(m->pf_ev[0], st));
+    FASQ_CUDA_TRY(cudaStreamWaitEvent(ps, m->pf_ev[0], 0));
+    fasq_status s = FASQ_OK;
+    if (M > m->pf_cap) {   // grow the persistent working set; the old graph referenced the old one
+        if (m->pf_exec) {
+            cudaStreamSynchronize(ps);   // rare path: no launch of the old graph in flight
+            cudaGraphExecDestroy(m->pf_exec);
+            m->pf_exec = nullptr;
+            m->pf_exec_M = 0;
+        }
+        dev_free(m->pf_buf, ps);
+        m->pf_buf = nullptr;
+        m->pf_cap = 0;
+        const size_t bytes = pf_layout(D, M, nullptr, nullptr) + (size_t)(M + 1) * sizeof(int) + 256;
+        s = dev_alloc_t(&m->pf_buf, bytes, ps);
+        if (s == FASQ_OK) {
+            m->pf_cap = M;
+            m->pf_tok = reinterpret_cast<int*>(m->pf_buf + pf_layout(D, M, nullptr, nullptr));
+        }
+    }
+    if (s == FASQ_OK) {
+        PfBufs B;
+        pf_layout(D, m->pf_cap, &B, m->pf_buf);
+        int* pos_d = m->pf_tok + m->pf_cap;
+        cudaError_t e = cudaMemcpyAsync(m->pf_tok, tokens_dev, (size_t)M * sizeof(int), cudaMemcpyDeviceToDevice, ps);
+        if (e != cudaSuccess) s = cuda_fail(e, "prefill tokens");
+        if (s == FASQ_OK) {
+            k_pf_set<<<1, 1, 0, ps>>>(pos_d, pos0);
+            if (m->pf_exec && m->pf_exec_M == M) {
+                e = cudaGraphLaunch(m->pf_exec, ps);
+                if (e != cudaSuccess) s = cuda_fail(e, "prefill graph launch");
+                if (s == FASQ_OK) set_launch_count(2);
+            } else {
+                s = pf_enqueue(m, m->pf_tok, pos_d, M, B, ps);   // this call's prefill, eagerly
+                if (s == FASQ_OK) {
+                    // capture the same sequence for the next calls with this M
+                    if (m->pf_exec) cudaGraphExecDestroy(m->pf_exec);
+                    m->pf_exec = nullptr;
+                    m->pf_exec_M = 0;
+                    cudaGraph_t gr = nullptr;
+                    e = cudaStreamBeginCapture(ps, cudaStreamCaptureModeThreadLocal);
+                    if (e == cudaSuccess) {
+                        const fasq_status sc = pf_enqueue(m, m->pf_tok, pos_d, M, B, ps);
+                        e = cudaStreamEndCapture(ps, &gr);
+                        if (sc == FASQ_OK && e == cudaSuccess &&
+                            cudaGraphInstantiate(&m->pf_exec, gr, 0) == cudaSuccess)
+                            m->pf_exec_M = M;
+                        if (gr) cudaGraphDestroy(gr);
+                    }
+                    cudaGetLastError();   // a failed capture only leaves the next call eager
+                    set_launch_count(1 + 8 * D.n_layers + 5);
+                }
+            }
+        }
+    }
+    FASQ_CUDA_TRY(cudaEventRecord(m->pf_ev[1], ps));
+    FASQ_CUDA_TRY(cudaStreamWaitEvent(st, m->pf_ev[1], 0));
     return s;
 }
 

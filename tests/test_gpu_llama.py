@@ -362,6 +362,11 @@ def test_llama_prefill_matches_oracle(F, hd, M, P0, n_kv):
         K, V = model.kv_cache(l)
         K[:, :, :P0].copy_(torch.from_numpy(kc[l][:, :, :P0]).cuda())
         V[:, :, :P0].copy_(torch.from_numpy(vc[l][:, :, :P0]).cuda())
+    # a first prefill of other tokens at another position runs eagerly and
+    # captures the cached graph; the checked one below replays that graph with
+    # the staged tokens / pos0 (the same M)
+    other = [(13 * i + 5) % cfg["vocab"] for i in range(M)]
+    model.prefill(other, P0 + 1 if P0 + 1 + M <= 64 else P0)
     model.prefill(prompt, P0)
     torch.cuda.synchronize()
     for l in range(cfg["n_layers"]):
