@@ -635,32 +635,42 @@ fasq_status gemm_tc_launch_grouped(const fasq_layer* const* Ls, int n, const __h
     } else {
         launches[nl][0] = 0; launches[nl][1] = tiles_all; launches[nl][2] = pick_ks(tiles_all); ++nl;
     }
-    uint8_t* wss[2] = {nullptr, nullptr};
+    // Split-K workspace: a FIXED ticket header (kTicketHdr bytes; launch li's
+    // [tiles][arrive, depart] at li * kTicketHdr / 2 -- tiles <= #SMs when ks > 1)
+    // followed by the launches' fp32 partial tiles.  The header never moves: a
+    // ticket region placed after the partials moved with the call's size and
+    // could land on an earlier call's partials (garbage counters on a shared
+    // stream workspace); each launch's last CTAs leave its tickets at zero.
+    constexpr size_t kTicketHdr = 4096;
+    size_t part_off[2] = {0, 0}, total = kTicketHdr;
+    for (int li = 0; li < nl; ++li) {
+        part_off[li] = total;
+        if (launches[li][2] > 1) {
+            if ((size_t)2 * launches[li][1] * sizeof(unsigned) > kTicketHdr / 2) return FASQ_E_UNSUPPORTED;
+            total += (size_t)launches[li][2] * launches[li][1] * (TC_M * TC_MT) * TC_N * sizeof(float);
+        }
+    }
+    uint8_t* ws = nullptr;
+    uint8_t* ws_call = nullptr;
+    if (total > kTicketHdr) {
+        // the stream's workspace (zero at allocation), else a per-call one (capture)
+        fasq_status s = stream_workspace(st, WS_GEMM_TC, total, reinterpret_cast<void**>(&ws));
+        if (s != FASQ_OK) return s;
+        if (!ws) {
+            s = dev_alloc_t(&ws_call, total, st);
+            if (s != FASQ_OK) return s;
+            cudaError_t e = cudaMemsetAsync(ws_call, 0, kTicketHdr, st);
+            if (e != cudaSuccess) { dev_free(ws_call, st); return cuda_fail(e, "gemm workspace tickets"); }
+            ws = ws_call;
+        }
+    }
     for (int li = 0; li < nl; ++li) {
         const int tiles = launches[li][1], ks = launches[li][2];
         dim3 grid((unsigned)tiles, 1, 1);
         p.tile0 = launches[li][0];
         if (ks > 1) {
-            // PER-CALL split-K workspace (stream-ordered, library allocator; the
-            // layer stays immutable): fp32 partial tiles + [tiles][arrive, depart]
-            const size_t need = (size_t)ks * tiles * (TC_M * TC_MT) * TC_N * sizeof(float);
-            const size_t tkb = (size_t)2 * tiles * sizeof(unsigned);
-            // the stream's workspace (tickets zero at allocation, reset by the last
-            // CTA of each tile; partials overwritten), else a per-call one
-            uint8_t* ws = nullptr;
-            fasq_status s = stream_workspace(st, WS_GEMM_TC, (size_t)(need + tkb) * (li + 1), reinterpret_cast<void**>(&ws));
-            if (s != FASQ_OK) return s;
-            if (ws) {
-                ws += (size_t)(need + tkb) * li;   // the two launches of one call use disjoint halves
-            } else {
-                s = dev_alloc_t(&ws, need + tkb, st);
-                if (s != FASQ_OK) return s;
-                cudaError_t e = cudaMemsetAsync(ws + need, 0, tkb, st);
-                if (e != cudaSuccess) { dev_free(ws, st); return cuda_fail(e, "gemm workspace tickets"); }
-                wss[li] = ws;
-            }
-            p.ws = reinterpret_cast<float*>(ws);
-            p.tickets = reinterpret_cast<unsigned*>(ws + need);
+            p.ws = reinterpret_cast<float*>(ws + part_off[li]);
+            p.tickets = reinterpret_cast<unsigned*>(ws + (size_t)li * (kTicketHdr / 2));
             grid.z = (unsigned)ks;
         }
         cudaError_t e;
@@ -683,11 +693,11 @@ fasq_status gemm_tc_launch_grouped(const fasq_layer* const* Ls, int n, const __h
             e = cudaGetLastError();
         }
         if (e != cudaSuccess) {
-            for (int q = 0; q <= li; ++q) dev_free(wss[q], st);
+            dev_free(ws_call, st);
             return cuda_fail(e, "k_gemm_tc launch");
         }
     }
-    for (int q = 0; q < nl; ++q) dev_free(wss[q], st);   // stream-ordered
+    dev_free(ws_call, st);   // stream-ordered
     set_launch_count(nl);
     return FASQ_OK;
 }

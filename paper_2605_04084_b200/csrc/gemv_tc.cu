@@ -392,7 +392,11 @@ fasq_status gemv_tc_launch(const fasq_layer* L, const __half* X, int B, void* y,
     ks = (L->n_groups + gper - 1) / gper;
     uint8_t* ws_call = nullptr;
     if (ks > 1) {
-        const size_t tkb = ((size_t)p.row_tiles * 8 + 255) / 256 * 256;
+        // a FIXED ticket header (row_tiles <= #SMs): a header sized by this call's
+        // row tiles would move and could overlap an earlier call's partials on
+        // the shared stream workspace (garbage counters)
+        const size_t tkb = 4096;
+        if ((size_t)p.row_tiles * 8 > tkb) return FASQ_E_UNSUPPORTED;
         const size_t need = tkb + (size_t)ks * p.row_tiles * NT * TT_R * sizeof(float);
         uint8_t* ws = nullptr;
         fasq_status s = stream_workspace(st, WS_GEMV_TC, need, reinterpret_cast<void**>(&ws));

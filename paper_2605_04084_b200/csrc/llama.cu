@@ -494,9 +494,176 @@ __global__ void __launch_bounds__(128, 3) k_pf_attn(const float* __restrict__ q,
     }
 }
 
+// ---- causal GQA attention on the tensor cores (mma.sync.m16n8k16, fp16 in, fp32
+// accumulate), FlashAttention-2 style: a warp owns 16 consecutive tokens x one
+// q head; S = Q K^T over 32-position chunks of its KV head's cache (staged in
+// shared memory by the CTA, shared by its 4 warps = 4 (token block, head) items
+// of that KV head), an online softmax over chunks in registers, P (fp16) re-used
+// in registers as the A operand of O += P V (V fragments by ldmatrix.trans).
+// Scores are scaled by 1/sqrt(hd) in fp32; q, P and the cache are fp16.
+__device__ __forceinline__ void pf_mma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pf_h2(float a, float b) {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(128) k_pf_attn_tc(const float* __restrict__ q, const __half* __restrict__ kc,
+                                                    const __half* __restrict__ vc, __half* __restrict__ out, int M,
+                                                    const int* __restrict__ pos0_p, int H, int KV, int max_T) {
+    constexpr int LD = HD + 8;   // halves per staged row (+16 B: conflict-free fragment loads)
+    __shared__ __align__(16) __half Ks[32 * LD];
+    __shared__ __align__(16) __half Vs[32 * LD];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int G = H / KV, NTB = (M + 15) / 16, n_items = NTB * G, ipj = (n_items + 3) / 4;
+    const int j = (int)blockIdx.x / ipj, ib = (int)blockIdx.x - j * ipj;
+    const int pos0 = *pos0_p;
+    const int item = ib * 4 + warp;
+    const bool active = item < n_items;
+    const int tb = active ? item / G : 0, hh = j * G + (active ? item - (item / G) * G : 0);
+    const int last_item = min(ib * 4 + 3, n_items - 1);
+    const int pos_hi = pos0 + min(M - 1, (last_item / G) * 16 + 15);   // the CTA's last position
+    const int r0 = tb * 16 + g, r1 = r0 + 8;                             // this thread's two rows (tokens)
+    const int pr0 = pos0 + min(r0, M - 1), pr1 = pos0 + min(r1, M - 1);  // their last positions
+    const float sc = 1.0f / sqrtf((float)HD);
+    uint32_t qa[HD / 16][4];
+    {
+        const float* q0 = q + ((size_t)r0 * H + hh) * HD;
+        const float* q1 = q + ((size_t)r1 * H + hh) * HD;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+            const int c = kk * 16 + 2 * t;
+            float2 a = make_float2(0.f, 0.f), b = a, cc = a, d = a;
+            if (active && r0 < M) {
+                a = *reinterpret_cast<const float2*>(q0 + c);
+                cc = *reinterpret_cast<const float2*>(q0 + c + 8);
+            }
+            if (active && r1 < M) {
+                b = *reinterpret_cast<const float2*>(q1 + c);
+                d = *reinterpret_cast<const float2*>(q1 + c + 8);
+            }
+            qa[kk][0] = pf_h2(a.x, a.y);
+            qa[kk][1] = pf_h2(b.x, b.y);
+            qa[kk][2] = pf_h2(cc.x, cc.y);
+            qa[kk][3] = pf_h2(d.x, d.y);
+        }
+    }
+    float o[HD / 8][4];
+#pragma unroll
+    for (int nd = 0; nd < HD / 8; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.f;
+    float mx0 = -INFINITY, mx1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    const __half* K = kc + (size_t)j * max_T * HD;
+    const __half* V = vc + (size_t)j * max_T * HD;
+    for (int t0 = 0; t0 <= pos_hi; t0 += 32) {
+        __syncthreads();   // the previous chunk's fragments are consumed
+        for (int i = threadIdx.x; i < 32 * HD / 8; i += 128) {
+            const int r = i / (HD / 8), c = i - r * (HD / 8);
+            uint4 kv = make_uint4(0u, 0u, 0u, 0u), vv = kv;
+            if (t0 + r <= pos_hi) {   // rows past the CTA's last position: zeros (never NaN garbage)
+                kv = *reinterpret_cast<const uint4*>(K + (size_t)(t0 + r) * HD + c * 8);
+                vv = *reinterpret_cast<const uint4*>(V + (size_t)(t0 + r) * HD + c * 8);
+            }
+            *reinterpret_cast<uint4*>(Ks + r * LD + c * 8) = kv;
+            *reinterpret_cast<uint4*>(Vs + r * LD + c * 8) = vv;
+        }
+        __syncthreads();
+        if (!active || t0 > pos0 + min(tb * 16 + 15, M - 1)) continue;   // warp-uniform: its rows are done
+        float sv[4][4];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+            sv[nt][0] = sv[nt][1] = sv[nt][2] = sv[nt][3] = 0.f;
+            const __half* kr = Ks + (nt * 8 + g) * LD + 2 * t;
+#pragma unroll
+            for (int kk = 0; kk < HD / 16; ++kk)
+                pf_mma(sv[nt], qa[kk], *reinterpret_cast<const uint32_t*>(kr + kk * 16),
+                       *reinterpret_cast<const uint32_t*>(kr + kk * 16 + 8));
+        }
+        float m0n = mx0, m1n = mx1;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int p = t0 + nt * 8 + 2 * t + e;
+                sv[nt][e] = p <= pr0 ? sv[nt][e] * sc : -INFINITY;
+                sv[nt][2 + e] = p <= pr1 ? sv[nt][2 + e] * sc : -INFINITY;
+                m0n = fmaxf(m0n, sv[nt][e]);
+                m1n = fmaxf(m1n, sv[nt][2 + e]);
+            }
+        m0n = fmaxf(m0n, __shfl_xor_sync(0xffffffffu, m0n, 1));
+        m0n = fmaxf(m0n, __shfl_xor_sync(0xffffffffu, m0n, 2));
+        m1n = fmaxf(m1n, __shfl_xor_sync(0xffffffffu, m1n, 1));
+        m1n = fmaxf(m1n, __shfl_xor_sync(0xffffffffu, m1n, 2));
+        const float c0 = expf(mx0 - m0n), c1 = expf(mx1 - m1n);   // 0 on the first chunk (mx = -inf)
+        float ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                sv[nt][e] = expf(sv[nt][e] - m0n);
+                sv[nt][2 + e] = expf(sv[nt][2 + e] - m1n);
+                ls0 += sv[nt][e];
+                ls1 += sv[nt][2 + e];
+            }
+        ls0 += __shfl_xor_sync(0xffffffffu, ls0, 1);
+        ls0 += __shfl_xor_sync(0xffffffffu, ls0, 2);
+        ls1 += __shfl_xor_sync(0xffffffffu, ls1, 1);
+        ls1 += __shfl_xor_sync(0xffffffffu, ls1, 2);
+        l0 = l0 * c0 + ls0;
+        l1 = l1 * c1 + ls1;
+        mx0 = m0n;
+        mx1 = m1n;
+#pragma unroll
+        for (int nd = 0; nd < HD / 8; ++nd) {
+            o[nd][0] *= c0;
+            o[nd][1] *= c0;
+            o[nd][2] *= c1;
+            o[nd][3] *= c1;
+        }
+#pragma unroll
+        for (int k2 = 0; k2 < 2; ++k2) {   // 16 positions per k-step
+            const uint32_t pa[4] = {pf_h2(sv[2 * k2][0], sv[2 * k2][1]), pf_h2(sv[2 * k2][2], sv[2 * k2][3]),
+                                    pf_h2(sv[2 * k2 + 1][0], sv[2 * k2 + 1][1]),
+                                    pf_h2(sv[2 * k2 + 1][2], sv[2 * k2 + 1][3])};
+            const int vr = k2 * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+            for (int nd = 0; nd < HD / 8; nd += 2) {
+                const uint32_t va = dev::smem_u32(Vs + vr * LD + 8 * (nd + (lane >> 4)));
+                uint32_t b0, b1, b2, b3;
+                asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3) : "r"(va));
+                pf_mma(o[nd], pa, b0, b1);
+                pf_mma(o[nd + 1], pa, b2, b3);
+            }
+        }
+    }
+    if (!active) return;
+    const float i0 = 1.0f / l0, i1 = 1.0f / l1;
+#pragma unroll
+    for (int nd = 0; nd < HD / 8; ++nd) {
+        const int c = nd * 8 + 2 * t;
+        if (r0 < M)
+            *reinterpret_cast<__half2*>(out + ((size_t)r0 * H + hh) * HD + c) =
+                __floats2half2_rn(o[nd][0] * i0, o[nd][1] * i0);
+        if (r1 < M)
+            *reinterpret_cast<__half2*>(out + ((size_t)r1 * H + hh) * HD + c) =
+                __floats2half2_rn(o[nd][2] * i1, o[nd][3] * i1);
+    }
+}
+
 template <int DPL>
 void pf_attn_launch(const float* q, const __half* kc, const __half* vc, __half* out, int M, const int* pos0, int H, int KV,
                     int max_T, cudaStream_t st) {
+    if (!getenv("FASQ_PF_ATTN_SIMT")) {   // tensor cores (default); the SIMT kernel below is the A/B reference
+        const int items = (M + 15) / 16 * (H / KV);
+        k_pf_attn_tc<32 * DPL><<<(unsigned)(KV * ((items + 3) / 4)), 128, 0, st>>>(q, kc, vc, out, M, pos0, H, KV,
+                                                                                  max_T);
+        return;
+    }
     const int grp = H / KV;
     const int G = grp % 4 == 0 ? 4 : grp % 2 == 0 ? 2 : 1;
     const unsigned blocks = (unsigned)(((int64_t)M * (H / G) + 3) / 4);

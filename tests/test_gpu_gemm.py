@@ -300,3 +300,32 @@ def test_gemm_grouped_errors(F):
     with pytest.raises(F.FasqError) as e:
         F.gemm_grouped([L1, L2], X)
     assert e.value.code == -5
+
+
+def test_split_k_workspace_shared_across_shapes(F):
+    """The per-stream split-K workspace is shared by every layer and call: EXPAND
+    (and the tcgen05 decode kernel) keep their arrive / depart tickets in a
+    FIXED header, so a call after one with another tile count / K split can
+    never find its counters on the earlier call's partial tiles.  Interleaved
+    calls of different shapes, repeated: bit-identical every time (a misplaced
+    ticket made the first call after a shape change race)."""
+    cases = [(1024, 4096, 300), (4096, 4096, 300), (768, 4096, 129), (14336, 4096, 100), (4096, 14336, 200),
+             (1024, 4096, 16), (4096, 4096, 24), (14336, 4096, 12)]
+    layers, xs = [], []
+    for i, (fo, fi, M) in enumerate(cases):
+        cb, idx = synth.random_layer(fo, fi, 2, 256, seed=900 + i)
+        layers.append(F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), fi))
+        xs.append(torch.from_numpy(synth.activation(M, fi, seed=950 + i)).cuda())
+    first = None
+    for rep in range(3):
+        order = list(range(len(cases)))
+        if rep == 1:
+            order.reverse()
+        ys = {}
+        for i in order:
+            ys[i] = F.gemm(layers[i], xs[i], out_dtype=torch.float32).cpu()
+        if first is None:
+            first = ys
+        else:
+            for i in range(len(cases)):
+                assert torch.equal(ys[i], first[i]), (rep, cases[i])
