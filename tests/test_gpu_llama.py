@@ -420,3 +420,45 @@ def test_llama3_prefill_full_size(F):
     else:   # near tie: the chosen token is within 2 % of the maximum
         assert logits[tok] >= top2[1] - 0.02 * abs(top2[1])
     model.free()
+
+
+@pytest.mark.parametrize("mode", ["eager_env", "user_capture"])
+def test_llama_prefill_launch_modes_agree(F, monkeypatch, mode):
+    """fasq_llama_prefill's three launch modes write the same KV-cache rows and
+    hand the decode chain the same token: the cached-graph replay (default,
+    second call), eager launches (FASQ_PREFILL_EAGER) and a call inside the
+    caller's own stream capture (per-call working set as graph memory nodes)."""
+    cfg = dict(SMALL, head_dim=64, n_heads=4, n_kv=2, hidden=256)
+    layers, fn, emb, lm = make_model(cfg, seed=77)
+    prompt = [(29 * i + 3) % cfg["vocab"] for i in range(37)]
+
+    def run(how):
+        model = build_gpu(F, cfg, layers, fn, emb, lm, 1)
+        if how == "graph":
+            model.prefill(prompt, 0)          # eager + capture
+            model.prefill(prompt, 0)          # replay
+        elif how == "eager_env":
+            monkeypatch.setenv("FASQ_PREFILL_EAGER", "1")
+            model.prefill(prompt, 0)
+            monkeypatch.delenv("FASQ_PREFILL_EAGER")
+        else:
+            toks = torch.tensor(prompt, dtype=torch.int32, device="cuda")
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    model.prefill(toks, 0)
+            g.replay()
+        model.step()
+        torch.cuda.synchronize()
+        kv = [tuple(t[0, :, 0:len(prompt)].float().cpu() for t in model.kv_cache(l)) for l in range(cfg["n_layers"])]
+        tok = int(model.token_history().cpu().numpy()[0, len(prompt)])
+        model.free()
+        return kv, tok
+
+    kv_ref, tok_ref = run("graph")
+    kv, tok = run(mode)
+    assert tok == tok_ref
+    for (k0, v0), (k1, v1) in zip(kv_ref, kv):
+        assert torch.equal(k0, k1) and torch.equal(v0, v1)
