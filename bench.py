@@ -933,20 +933,27 @@ def pack_time():
 
     import paper_2605_04084_b200 as F
     import synth
-    per = {}
+    per, first = {}, {}
     block_s = 0.0
     for (name, fo, fi) in synth.LLAMA3_8B_LAYERS:
         key = "%dx%d" % (fo, fi)
         if key not in per:
             W = synth.torch_activation(fo, fi, seed=5, std=0.02)
-            F.pack(synth.torch_activation(64, fi, seed=6, std=0.02), d=D, C=min(C, 64), group=1, seed=0,
-                   iters=1).free()   # warm-up (allocations, CUB temp storage)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            L = F.pack(W, d=D, C=C, group=1, seed=0, iters=25)
-            torch.cuda.synchronize()
-            per[key] = round(time.perf_counter() - t0, 4)
-            L.free()
+            # the first pack of a shape grows the allocator pools / CUB temp
+            # storage and is reported separately; the estimate uses the fastest
+            # of three warm packs of the same layer (host wall clock: the pack
+            # loop synchronises with the host, which adds run-to-run noise)
+            for rep in range(4):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                L = F.pack(W, d=D, C=C, group=1, seed=0, iters=25)
+                torch.cuda.synchronize()
+                dt = round(time.perf_counter() - t0, 4)
+                if rep == 0:
+                    first[key] = dt
+                else:
+                    per[key] = min(per.get(key, dt), dt)
+                L.free()
             del W
         block_s += per[key]
     # NEXT-4 packing variants on one 4096 x 4096 layer (k-means++ init, reseeding)
@@ -959,7 +966,7 @@ def pack_time():
         torch.cuda.synchronize()
         var[name] = round(time.perf_counter() - t0, 4)
         L.free()
-    return {"d": D, "C": C, "iters": 25, "seconds_per_layer_shape": per,
+    return {"d": D, "C": C, "iters": 25, "seconds_per_layer_shape": per, "first_pack_seconds": first,
             "whole_model_seconds_est": round(block_s * synth.LLAMA3_8B_BLOCKS, 2),
             "variants_4096x4096_seconds": var}
 
