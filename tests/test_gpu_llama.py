@@ -462,3 +462,38 @@ def test_llama_prefill_launch_modes_agree(F, monkeypatch, mode):
     assert tok == tok_ref
     for (k0, v0), (k1, v1) in zip(kv_ref, kv):
         assert torch.equal(k0, k1) and torch.equal(v0, v1)
+
+
+def test_llama_prefill_graph_cache_across_lengths(F, monkeypatch):
+    """The prefill graph cache across prompt lengths: M = 9, 33 (working set
+    grows: the cached graph is dropped), 9 (re-captured), 33, each at its own
+    pos0 and with its own tokens -- every call's KV rows and handed-over token
+    bit-identical to the same call with eager launches (FASQ_PREFILL_EAGER)."""
+    cfg = dict(SMALL, head_dim=64, n_heads=4, n_kv=2, hidden=256)
+    layers, fn, emb, lm = make_model(cfg, seed=78)
+    calls = [(9, 0), (33, 0), (9, 20), (33, 4), (9, 20)]
+
+    def run(eager):
+        if eager:
+            monkeypatch.setenv("FASQ_PREFILL_EAGER", "1")
+        model = build_gpu(F, cfg, layers, fn, emb, lm, 1)
+        outs = []
+        for i, (M, p0) in enumerate(calls):
+            prompt = [(31 * k + 7 * i + 1) % cfg["vocab"] for k in range(M)]
+            model.prefill(prompt, p0)
+            torch.cuda.synchronize()
+            kv = [tuple(t[0, :, p0:p0 + M].float().cpu().clone() for t in model.kv_cache(l))
+                  for l in range(cfg["n_layers"])]
+            model.step()
+            torch.cuda.synchronize()
+            outs.append((kv, int(model.token_history().cpu().numpy()[0, p0 + M])))
+        model.free()
+        monkeypatch.delenv("FASQ_PREFILL_EAGER", raising=False)
+        return outs
+
+    ref = run(True)
+    got = run(False)
+    for (kv_r, tok_r), (kv_g, tok_g), c in zip(ref, got, calls):
+        assert tok_g == tok_r, c
+        for (k0, v0), (k1, v1) in zip(kv_r, kv_g):
+            assert torch.equal(k0, k1) and torch.equal(v0, v1), c
