@@ -517,8 +517,8 @@ __global__ void __launch_bounds__(128) k_pf_attn_tc(const float* __restrict__ q,
                                                     const __half* __restrict__ vc, __half* __restrict__ out, int M,
                                                     const int* __restrict__ pos0_p, int H, int KV, int max_T) {
     constexpr int LD = HD + 8;   // halves per staged row (+16 B: conflict-free fragment loads)
-    __shared__ __align__(16) __half Ks[32 * LD];
-    __shared__ __align__(16) __half Vs[32 * LD];
+    __shared__ __align__(16) __half Kbuf[2][32 * LD];   // double-buffered chunk staging (cp.async)
+    __shared__ __align__(16) __half Vbuf[2][32 * LD];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int G = H / KV, NTB = (M + 15) / 16, n_items = NTB * G, ipj = (n_items + 3) / 4;
     const int j = (int)blockIdx.x / ipj, ib = (int)blockIdx.x - j * ipj;
@@ -559,87 +559,107 @@ __global__ void __launch_bounds__(128) k_pf_attn_tc(const float* __restrict__ q,
     float mx0 = -INFINITY, mx1 = -INFINITY, l0 = 0.f, l1 = 0.f;
     const __half* K = kc + (size_t)j * max_T * HD;
     const __half* V = vc + (size_t)j * max_T * HD;
-    for (int t0 = 0; t0 <= pos_hi; t0 += 32) {
-        __syncthreads();   // the previous chunk's fragments are consumed
+    // chunk c's rows [32 c, 32 c + 32) -> buffer c & 1 with cp.async (16 B each; rows
+    // past the CTA's last position are zero-filled: src-size 0, never NaN garbage)
+    auto stage = [&](int c) {
+        const int t0s = c * 32;
+        __half* ks = Kbuf[c & 1];
+        __half* vs = Vbuf[c & 1];
         for (int i = threadIdx.x; i < 32 * HD / 8; i += 128) {
-            const int r = i / (HD / 8), c = i - r * (HD / 8);
-            uint4 kv = make_uint4(0u, 0u, 0u, 0u), vv = kv;
-            if (t0 + r <= pos_hi) {   // rows past the CTA's last position: zeros (never NaN garbage)
-                kv = *reinterpret_cast<const uint4*>(K + (size_t)(t0 + r) * HD + c * 8);
-                vv = *reinterpret_cast<const uint4*>(V + (size_t)(t0 + r) * HD + c * 8);
-            }
-            *reinterpret_cast<uint4*>(Ks + r * LD + c * 8) = kv;
-            *reinterpret_cast<uint4*>(Vs + r * LD + c * 8) = vv;
+            const int r = i / (HD / 8), cc = i - r * (HD / 8);
+            const bool ok = t0s + r <= pos_hi;
+            const size_t off = (size_t)(ok ? t0s + r : 0) * HD + cc * 8;
+            const uint32_t n = ok ? 16u : 0u;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                         :: "r"(dev::smem_u32(ks + r * LD + cc * 8)), "l"(K + off), "r"(n) : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                         :: "r"(dev::smem_u32(vs + r * LD + cc * 8)), "l"(V + off), "r"(n) : "memory");
         }
-        __syncthreads();
-        if (!active || t0 > pos0 + min(tb * 16 + 15, M - 1)) continue;   // warp-uniform: its rows are done
-        float sv[4][4];
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-            sv[nt][0] = sv[nt][1] = sv[nt][2] = sv[nt][3] = 0.f;
-            const __half* kr = Ks + (nt * 8 + g) * LD + 2 * t;
-#pragma unroll
-            for (int kk = 0; kk < HD / 16; ++kk)
-                pf_mma(sv[nt], qa[kk], *reinterpret_cast<const uint32_t*>(kr + kk * 16),
-                       *reinterpret_cast<const uint32_t*>(kr + kk * 16 + 8));
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const int n_chunks = pos_hi / 32 + 1;
+    stage(0);
+    for (int ch = 0; ch < n_chunks; ++ch) {
+        const int t0 = ch * 32;
+        if (ch + 1 < n_chunks) {   // the next chunk's copies overlap this chunk's math
+            stage(ch + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-        float m0n = mx0, m1n = mx1;
+        __syncthreads();   // chunk ch staged by every thread
+        const __half* Ks = Kbuf[ch & 1];
+        const __half* Vs = Vbuf[ch & 1];
+        if (active && t0 <= pos0 + min(tb * 16 + 15, M - 1)) {   // warp-uniform: rows left for this warp
+            float sv[4][4];
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+            for (int nt = 0; nt < 4; ++nt) {
+                sv[nt][0] = sv[nt][1] = sv[nt][2] = sv[nt][3] = 0.f;
+                const __half* kr = Ks + (nt * 8 + g) * LD + 2 * t;
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int p = t0 + nt * 8 + 2 * t + e;
-                sv[nt][e] = p <= pr0 ? sv[nt][e] * sc : -INFINITY;
-                sv[nt][2 + e] = p <= pr1 ? sv[nt][2 + e] * sc : -INFINITY;
-                m0n = fmaxf(m0n, sv[nt][e]);
-                m1n = fmaxf(m1n, sv[nt][2 + e]);
+                for (int kk = 0; kk < HD / 16; ++kk)
+                    pf_mma(sv[nt], qa[kk], *reinterpret_cast<const uint32_t*>(kr + kk * 16),
+                           *reinterpret_cast<const uint32_t*>(kr + kk * 16 + 8));
             }
-        m0n = fmaxf(m0n, __shfl_xor_sync(0xffffffffu, m0n, 1));
-        m0n = fmaxf(m0n, __shfl_xor_sync(0xffffffffu, m0n, 2));
-        m1n = fmaxf(m1n, __shfl_xor_sync(0xffffffffu, m1n, 1));
-        m1n = fmaxf(m1n, __shfl_xor_sync(0xffffffffu, m1n, 2));
-        const float c0 = expf(mx0 - m0n), c1 = expf(mx1 - m1n);   // 0 on the first chunk (mx = -inf)
-        float ls0 = 0.f, ls1 = 0.f;
+            float m0n = mx0, m1n = mx1;
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+            for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                sv[nt][e] = expf(sv[nt][e] - m0n);
-                sv[nt][2 + e] = expf(sv[nt][2 + e] - m1n);
-                ls0 += sv[nt][e];
-                ls1 += sv[nt][2 + e];
+                for (int e = 0; e < 2; ++e) {
+                    const int p = t0 + nt * 8 + 2 * t + e;
+                    sv[nt][e] = p <= pr0 ? sv[nt][e] * sc : -INFINITY;
+                    sv[nt][2 + e] = p <= pr1 ? sv[nt][2 + e] * sc : -INFINITY;
+                    m0n = fmaxf(m0n, sv[nt][e]);
+                    m1n = fmaxf(m1n, sv[nt][2 + e]);
+                }
+            m0n = fmaxf(m0n, __shfl_xor_sync(0xffffffffu, m0n, 1));
+            m0n = fmaxf(m0n, __shfl_xor_sync(0xffffffffu, m0n, 2));
+            m1n = fmaxf(m1n, __shfl_xor_sync(0xffffffffu, m1n, 1));
+            m1n = fmaxf(m1n, __shfl_xor_sync(0xffffffffu, m1n, 2));
+            const float c0 = expf(mx0 - m0n), c1 = expf(mx1 - m1n);   // 0 on the first chunk (mx = -inf)
+            float ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    sv[nt][e] = expf(sv[nt][e] - m0n);
+                    sv[nt][2 + e] = expf(sv[nt][2 + e] - m1n);
+                    ls0 += sv[nt][e];
+                    ls1 += sv[nt][2 + e];
+                }
+            ls0 += __shfl_xor_sync(0xffffffffu, ls0, 1);
+            ls0 += __shfl_xor_sync(0xffffffffu, ls0, 2);
+            ls1 += __shfl_xor_sync(0xffffffffu, ls1, 1);
+            ls1 += __shfl_xor_sync(0xffffffffu, ls1, 2);
+            l0 = l0 * c0 + ls0;
+            l1 = l1 * c1 + ls1;
+            mx0 = m0n;
+            mx1 = m1n;
+#pragma unroll
+            for (int nd = 0; nd < HD / 8; ++nd) {
+                o[nd][0] *= c0;
+                o[nd][1] *= c0;
+                o[nd][2] *= c1;
+                o[nd][3] *= c1;
             }
-        ls0 += __shfl_xor_sync(0xffffffffu, ls0, 1);
-        ls0 += __shfl_xor_sync(0xffffffffu, ls0, 2);
-        ls1 += __shfl_xor_sync(0xffffffffu, ls1, 1);
-        ls1 += __shfl_xor_sync(0xffffffffu, ls1, 2);
-        l0 = l0 * c0 + ls0;
-        l1 = l1 * c1 + ls1;
-        mx0 = m0n;
-        mx1 = m1n;
 #pragma unroll
-        for (int nd = 0; nd < HD / 8; ++nd) {
-            o[nd][0] *= c0;
-            o[nd][1] *= c0;
-            o[nd][2] *= c1;
-            o[nd][3] *= c1;
+            for (int k2 = 0; k2 < 2; ++k2) {   // 16 positions per k-step
+                const uint32_t pa[4] = {pf_h2(sv[2 * k2][0], sv[2 * k2][1]), pf_h2(sv[2 * k2][2], sv[2 * k2][3]),
+                                        pf_h2(sv[2 * k2 + 1][0], sv[2 * k2 + 1][1]),
+                                        pf_h2(sv[2 * k2 + 1][2], sv[2 * k2 + 1][3])};
+                const int vr = k2 * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+                for (int nd = 0; nd < HD / 8; nd += 2) {
+                    const uint32_t va = dev::smem_u32(Vs + vr * LD + 8 * (nd + (lane >> 4)));
+                    uint32_t b0, b1, b2, b3;
+                    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3) : "r"(va));
+                    pf_mma(o[nd], pa, b0, b1);
+                    pf_mma(o[nd + 1], pa, b2, b3);
+                }
+            }
         }
-#pragma unroll
-        for (int k2 = 0; k2 < 2; ++k2) {   // 16 positions per k-step
-            const uint32_t pa[4] = {pf_h2(sv[2 * k2][0], sv[2 * k2][1]), pf_h2(sv[2 * k2][2], sv[2 * k2][3]),
-                                    pf_h2(sv[2 * k2 + 1][0], sv[2 * k2 + 1][1]),
-                                    pf_h2(sv[2 * k2 + 1][2], sv[2 * k2 + 1][3])};
-            const int vr = k2 * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-#pragma unroll
-            for (int nd = 0; nd < HD / 8; nd += 2) {
-                const uint32_t va = dev::smem_u32(Vs + vr * LD + 8 * (nd + (lane >> 4)));
-                uint32_t b0, b1, b2, b3;
-                asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                             : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3) : "r"(va));
-                pf_mma(o[nd], pa, b0, b1);
-                pf_mma(o[nd + 1], pa, b2, b3);
-            }
-        }
+        __syncthreads();   // buffer ch & 1 is re-staged by the next iteration's copy of chunk ch + 2
     }
     if (!active) return;
     const float i0 = 1.0f / l0, i1 = 1.0f / l1;
