@@ -458,14 +458,16 @@ k_gemm_tc(const __grid_constant__ CUtensorMap xmap, TcParams p) {
                     }
                 }
                 asm volatile("bar.sync 1, %0;" :: "n"(TC_EXP_WARPS * 32) : "memory");
-                const int cw = TC_N / ksplit;     // ks in {2, 4, 8}: multiples of 32 columns
-                // this CTA's column slice; with one real accumulator the two warp
-                // halves (same tokens) split it when it holds >= 2 chunks of 32
-                int mb = kz * cw, me = mb + cw;
+                // this CTA's column slice: 32-column chunks [kz * 8 / ks, (kz + 1) * 8 / ks)
+                // (ks = 2..8); with one real accumulator the two warp halves (same
+                // tokens) split it when it holds >= 2 chunks
+                int mb = (kz * (TC_N / 32)) / ksplit * 32, me = ((kz + 1) * (TC_N / 32)) / ksplit * 32;
                 if (one_acc) {
-                    if (cw >= 64) {
-                        mb += t * (cw / 2);
-                        me = mb + cw / 2;
+                    const int nc = (me - mb) / 32;
+                    if (nc >= 2) {
+                        const int hc = nc / 2 * 32;
+                        if (t) mb += hc;
+                        else me = mb + hc;
                     } else if (t) {
                         me = mb;
                     }
@@ -621,8 +623,8 @@ fasq_status gemm_tc_launch_grouped(const fasq_layer* const* Ls, int n, const __h
         int ks = 1;
         if (const char* e = getenv("FASQ_GEMM_KSPLIT")) ks = atoi(e);
         else if (tiles < sms) ks = std::min(sms / tiles, L->n_groups / 8);
-        ks = ks >= 8 ? 8 : ks >= 4 ? 4 : ks >= 2 ? 2 : 1;          // the merge splits 256 columns by ks
-        while (ks > 1 && (tiles * ks > sms || ks > L->n_groups)) ks >>= 1;   // co-resident, >= 1 chunk each
+        ks = std::max(1, std::min(ks, 8));   // the merge deals 8 chunks of 32 columns over the ks CTAs
+        while (ks > 1 && (tiles * ks > sms || ks > L->n_groups)) --ks;   // co-resident, >= 1 chunk each
         return ks;
     };
     int launches[2][3];   // {tile0, tiles, ks}

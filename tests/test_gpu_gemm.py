@@ -87,11 +87,14 @@ def test_gemm_llama_sampled(F, oracle_lib, F_out, F_in):
         assert ok, (j0, info)
 
 
-@pytest.mark.parametrize("F_out,F_in,M,ks", [(512, 2048, 100, 0), (1000, 2496, 300, 4), (256, 4096, 17, 0)])
+@pytest.mark.parametrize("F_out,F_in,M,ks", [(512, 2048, 100, 0), (1000, 2496, 300, 4), (256, 4096, 17, 0),
+                                             (1000, 2496, 300, 3), (512, 4096, 77, 5), (768, 4096, 260, 6),
+                                             (256, 4096, 129, 7)])
 def test_gemm_tc_split_k(F, oracle_lib, monkeypatch, F_out, F_in, M, ks):
     """Small M -> fewer tiles than SMs -> split-K over gridDim.z with an fp32
     workspace merged by the last CTA of each tile in fixed order (ks = 0: the
-    library's choice; 4: forced, uneven chunk counts (39 chunks)).  Two calls in a row also
+    library's choice; 4: forced, uneven chunk counts (39 chunks); 3 / 5 / 6 / 7: the merge deals
+    the 8 column chunks of a tile unevenly over the K slices).  Two calls in a row also
     check the per-tile ticket reset, and the result must be bit-identical."""
     if ks:
         monkeypatch.setenv("FASQ_GEMM_KSPLIT", str(ks))
