@@ -225,11 +225,9 @@ void destroy_model(fasq_llama* m) {
     dev_free(m->tok_dev, 0);
     if (m->tok_pin) cudaFreeHost(m->tok_pin);
     if (m->io_exec) cudaGraphExecDestroy(m->io_exec);
+    if (m->pf_stream) cudaStreamSynchronize(m->pf_stream);   // no prefill in flight below
     if (m->pf_exec) cudaGraphExecDestroy(m->pf_exec);
-    if (m->pf_buf) {
-        if (m->pf_stream) cudaStreamSynchronize(m->pf_stream);
-        dev_free(m->pf_buf, 0);
-    }
+    if (m->pf_buf) dev_free(m->pf_buf, 0);
     for (cudaEvent_t e : m->pf_ev)
         if (e) cudaEventDestroy(e);
     if (m->pf_stream) cudaStreamDestroy(m->pf_stream);
