@@ -332,3 +332,28 @@ def test_split_k_workspace_shared_across_shapes(F):
         else:
             for i in range(len(cases)):
                 assert torch.equal(ys[i], first[i]), (rep, cases[i])
+
+
+def test_gemm_grouped_fp16_and_lut_fallback(F, oracle_lib):
+    """fasq_gemm_grouped with fp16 outputs (one EXPAND launch) and with the LUT
+    algorithm (no grouped kernel: one fasq_gemm per layer, in order): each Y
+    within tolerance of the oracle, and the fp16 grouped result equal to the
+    per-layer fp16 EXPAND result to fp16 rounding."""
+    M = 200
+    X = synth.activation(M, 1024, seed=501)
+    Xd = torch.from_numpy(X).cuda()
+    host, Ls = [], []
+    for i, fo in enumerate((768, 256, 256)):
+        cb, idx = synth.random_layer(fo, 1024, 2, 64, seed=510 + i)
+        host.append((cb, idx))
+        Ls.append(F.import_layer(torch.from_numpy(cb).cuda(), torch.from_numpy(idx).cuda(), 1024))
+    Yh = F.gemm_grouped(Ls, Xd, out_dtype=torch.float16, algo=F.GEMM_EXPAND_TC)
+    Yl = F.gemm_grouped(Ls, Xd, algo=F.GEMM_LUT)
+    torch.cuda.synchronize()
+    for (cb, idx), L, yh, yl in zip(host, Ls, Yh, Yl):
+        ref = oracle_lib.gemm(cb, idx, X)
+        ok, m = parity_ok(yl.cpu().numpy().astype(np.float64), ref, X, 1024)
+        assert ok, m
+        y1 = F.gemm(L, Xd, out_dtype=torch.float16, algo=F.GEMM_EXPAND_TC).float().cpu().numpy()
+        yg = yh.float().cpu().numpy()
+        assert np.max(np.abs(yg - y1)) <= 2.0 ** -10 * (np.max(np.abs(y1)) + 1e-3)
